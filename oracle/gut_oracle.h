@@ -1,0 +1,125 @@
+/*
+ * gut_oracle.h — fp64 CPU ORACLE for the 3DGUT forward rasterizer.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load or call this code.
+ * The product path (include/gut.h, paper_2412_12507_b200/) never includes,
+ * links or imports anything under oracle/, and this file includes nothing of
+ * the product.  The two share only the seeded input generators (scenegen/).
+ *
+ * The oracle follows PAPER.md step by step:
+ *   O1 Gaussian setup, UT weights, sigma points  PAPER L84-95 (Eq.1-2), L139-168 (Eq.6-8)
+ *   O2 exact projection of each sigma point       PAPER L170 ; rolling shutter L34, L393
+ *   O3 UT estimate, extent, tiles, depth, colour PAPER L170-178 (Eq.9-10), Alg.1
+ *   O4 per-tile depth-ordered lists
+ *   O5 pixel rays
+ *   O6 front-to-back compositing, 3D max response PAPER L115-121 (Eq.5), L192-200 (Eq.11)
+ * Readings of silent/ambiguous points are listed in DESIGN.md "Readings".
+ */
+#ifndef GUT_ORACLE_H
+#define GUT_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORC_PINHOLE = 0, ORC_OPENCV = 1, ORC_FISHEYE = 2, ORC_ORTHO = 3 };
+enum { ORC_GLOBAL = 0, ORC_TOP_TO_BOTTOM = 1, ORC_LEFT_TO_RIGHT = 2,
+       ORC_BOTTOM_TO_TOP = 3, ORC_RIGHT_TO_LEFT = 4 };
+
+typedef struct {
+  int32_t model, width, height, shutter;
+  double fx, fy, cx, cy;
+  double k[6];
+  double p[2];
+  double fov_limit;       /* FISHEYE theta_max [rad]; OPENCV r_lim (normalised); 0 = none */
+  double q[2][4];         /* camera->world quaternion (w,x,y,z) at t=0, t=1 */
+  double c[2][3];         /* camera centre (world) at t=0, t=1 */
+} orc_camera;
+
+typedef struct {
+  double ut_alpha, ut_beta, ut_kappa;
+  double alpha_min, alpha_max, t_min, dilation, near_plane;
+  double bg[3];
+  int32_t tile_cull;      /* 0 AABB, 1 ellipse-tile */
+  int32_t pad;
+} orc_options;
+
+/* cull reasons (0 = visible) */
+enum { ORC_OK = 0, ORC_CULL_PARAM = 1, ORC_CULL_OPACITY = 2, ORC_CULL_SIGMA = 3,
+       ORC_CULL_COV = 4, ORC_CULL_OFFSCREEN = 5, ORC_CULL_NOTILE = 6 };
+
+typedef struct {
+  int32_t reason;          /* ORC_OK or a cull reason */
+  int32_t tiles;           /* tiles kept (0 if culled) */
+  int32_t rect[4];         /* tile x0,y0,x1,y1 (inclusive, clamped) */
+  int32_t cull_ambig;      /* a validity quantity is within its margin */
+  int32_t bin_ambig;       /* some candidate tile decision flips under +-1e-3 px */
+  int32_t rs_iters;        /* max fixed-point iterations over the 7 points (RS) */
+  int32_t rs_fail;         /* non-convergence */
+  double vx, vy;           /* 2D mean v_mu (Eq. 9) */
+  double cxx, cxy, cyy;    /* 2D covariance Sigma' (Eq. 10) + dilation */
+  double k2;               /* 2 ln(sigma/alpha_min) */
+  double hx, hy;           /* extent (AABB half sizes) */
+  double depth;            /* ||x0 in camera frame|| at its own shutter time */
+  double t0;               /* shutter time of the centre point */
+  double rgb[3];           /* SH colour at d = normalize(mu - c(t0)) */
+} orc_proj;
+
+typedef struct {
+  int32_t visited, contributed, terminated, invalid;
+  double min_alpha_gap;    /* min |alpha - alpha_min| over visited entries */
+  double min_term_gap;     /* min |T' - T_min| over blended/stopping entries */
+  double min_order_gap;    /* min relative depth gap between consecutive contributing entries */
+  int32_t amb_bin;         /* a binning-ambiguous pair could change this pixel */
+  int32_t amb_cull;        /* a cull-ambiguous Gaussian could change this pixel */
+} orc_pixdiag;
+
+/* ---- O1 ---- */
+int  orc_ut_weights(double a, double b, double k, double wmu[7], double wsig[7], double *lambda);
+int  orc_quat_to_rot(const double q[4], double R[9]);
+void orc_sigma_points(const double mu[3], const double R[9], const double s[3], double lambda,
+                      double X[7][3]);
+/* ---- O2 ---- */
+void orc_pose_at(const orc_camera *cam, double t, double Rc2w[9], double c[3]);
+int  orc_project_cam(const orc_camera *cam, const orc_options *o, const double xc[3], double uv[2],
+                     double *margin);
+int  orc_project_point(const orc_camera *cam, const orc_options *o, const double x[3], double uv[2],
+                       double *t_out, int32_t *iters, double *margin);
+/* ---- O3 ---- */
+void orc_sh_basis(const double d[3], double Y[16]);
+int  orc_tile_hits_ellipse(double vx, double vy, double cxx, double cxy, double cyy, double k2,
+                           double x0, double y0, double x1, double y1);
+void orc_preprocess(const float *means, const float *rots, const float *scales, const float *opac,
+                    const float *sh, int32_t sh_degree, int64_t n, const orc_camera *cam,
+                    const orc_options *o, orc_proj *out);
+/* ---- O4 ---- (pairs: tile-major, then (depth, gid); returns K) */
+int64_t orc_tile_lists(const orc_proj *proj, int64_t n, const orc_camera *cam, const orc_options *o,
+                       const float *means, const float *scales, int32_t *tile_of, int32_t *gid_of,
+                       int64_t cap, int32_t *ranges);
+/* ---- O5 ---- */
+int  orc_pixel_ray(const orc_camera *cam, double u, double v, double o[3], double d[3]);
+/* ---- O6 ---- */
+double orc_max_response(const double mu[3], const double R[9], const double s[3], const double o[3],
+                        const double d[3], double *tau);
+void orc_composite(const float *means, const float *rots, const float *scales, const float *opac,
+                   const orc_proj *proj, const int32_t *gids, const int32_t *ranges,
+                   const orc_camera *cam, const orc_options *o, const int32_t *tile_subset,
+                   int32_t n_subset, float *rgb, float *alpha, float *depth, orc_pixdiag *diag);
+/* full render: binned (brute = 0) or brute force over all valid Gaussians (brute = 1) */
+int64_t orc_render(const float *means, const float *rots, const float *scales, const float *opac,
+                   const float *sh, int32_t sh_degree, int64_t n, const orc_camera *cam,
+                   const orc_options *o, int32_t brute, const int32_t *tile_subset, int32_t n_subset,
+                   float *rgb, float *alpha, float *depth, orc_pixdiag *diag, orc_proj *proj_out,
+                   int64_t *n_keys_out);
+/* flag pixels that an ambiguous (Gaussian, tile) pair or a cull-ambiguous Gaussian could change */
+void orc_mark_ambiguity(const float *means, const float *rots, const float *scales, const float *opac,
+                        const orc_proj *proj, int64_t n, const orc_camera *cam, const orc_options *o,
+                        double alpha_eps, orc_pixdiag *diag);
+int  orc_threads(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
