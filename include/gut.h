@@ -1,0 +1,204 @@
+/*
+ * gut.h — C ABI of the B200-native 3DGUT forward rasterizer (ABI version 1).
+ *
+ * What it computes (PAPER.md = arXiv 2412.12507):
+ *   render(gaussians, camera model, pose/shutter params) -> RGB, alpha, depth
+ *   1. UT projection (Sec. 4.1, Eq. 6-10; Alg. 1-2):
+ *      7 sigma points per Gaussian with weights from (alpha, beta, kappa),
+ *      each projected exactly through the camera (pinhole, OpenCV rad-tan,
+ *      Kannala-Brandt / equidistant fisheye, orthographic); rolling shutter
+ *      gives every sigma point its own row-time extrinsic;
+ *      then the 2D mean and covariance are re-estimated (Eq. 9-10).
+ *   2. opacity-aware extent and tile binning with key duplication (Alg. 1
+ *      lines 3-5), a (tile, depth) radix sort and
+ *      per-tile ranges.
+ *   3. per-pixel front-to-back compositing (Eq. 5) of each
+ *      particle's 3D response at its maximum along the ray (Eq. 11,
+ *      P:L192-200), SH colour, early transmittance termination.
+ * Readings of silent points (quaternion order, thresholds, depth key, ...)
+ * are DESIGN.md "Readings" R1..R27 and are shared with the test oracle.
+ *
+ * Conventions
+ *   - All device work is enqueued asynchronously on the caller's stream;
+ *     no call synchronises unless documented (stats != NULL, sync-capacity).
+ *   - Every call returns gut_status; gut_last_error(ctx) names the offending
+ *     field of the last non-OK status on that context.  No C++ exception,
+ *     abort or exit crosses the ABI.
+ *   - There is no CPU fallback: a device that is not sm_100 returns
+ *     GUT_E_UNSUPPORTED from gut_context_create.
+ *   - A context must not be used by two host threads at once (one context
+ *     per thread / per rank).
+ */
+#ifndef GUT_H
+#define GUT_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GUT_ABI_VERSION 1u
+
+typedef struct gut_context gut_context; /* opaque: device, workspace, last error */
+typedef struct gut_scene gut_scene;     /* opaque: packed device SoA copy of one Gaussian set */
+typedef void *gut_stream;               /* a cudaStream_t (NULL = legacy default stream) */
+
+typedef enum {
+  GUT_OK = 0,
+  GUT_E_INVALID_ARGUMENT = 1, /* bad struct_size, sizes, pointers, camera or options */
+  GUT_E_UNSUPPORTED = 2,      /* device is not sm_100, or an unsupported combination */
+  GUT_E_OUT_OF_MEMORY = 3,    /* device allocation failed */
+  GUT_E_CAPACITY = 4,         /* key count exceeded the reserved capacity (graph mode) */
+  GUT_E_CUDA = 5,             /* a CUDA runtime error; message in gut_last_error */
+  GUT_E_INTERNAL = 6
+} gut_status;
+
+typedef enum { GUT_CAM_PINHOLE = 0, GUT_CAM_OPENCV = 1, GUT_CAM_FISHEYE = 2, GUT_CAM_ORTHO = 3 } gut_camera_model;
+
+typedef enum {
+  GUT_SHUTTER_GLOBAL = 0,
+  GUT_SHUTTER_TOP_TO_BOTTOM = 1, /* shutter time of image row v is v/H        */
+  GUT_SHUTTER_LEFT_TO_RIGHT = 2, /* u/W                                       */
+  GUT_SHUTTER_BOTTOM_TO_TOP = 3, /* 1 - v/H                                   */
+  GUT_SHUTTER_RIGHT_TO_LEFT = 4  /* 1 - u/W                                   */
+} gut_shutter;
+
+/* Camera (host struct, by value).  Doubles so the oracle and the GPU consume
+ * identical values.  Camera axes are OpenCV (x right, y down, z forward).
+ * Pixel (i,j) covers [i,i+1)x[j,j+1); its centre is (i+0.5, j+0.5) in the
+ * same frame as (cx, cy).  The pose is camera->world: orientation quaternion
+ * (w,x,y,z) and centre, at shutter time t=0 and t=1 (slerp / lerp in between,
+ * reading R15).  GLOBAL shutter uses the t=0 pose only. */
+typedef struct {
+  uint32_t struct_size; /* = sizeof(gut_camera) */
+  int32_t model;        /* gut_camera_model */
+  int32_t width, height;
+  double fx, fy, cx, cy; /* pixels (ORTHO: pixels per world unit) */
+  double k[6];           /* OPENCV k1..k6 (k4..k6 rational denominator); FISHEYE k1..k4 */
+  double p[2];           /* OPENCV p1, p2 */
+  double fov_limit;      /* FISHEYE theta_max [rad] (required); OPENCV max normalised
+                            undistorted radius r_lim (required if any k/p != 0) */
+  int32_t shutter;       /* gut_shutter */
+  int32_t pad0;
+  double q_c2w[2][4];
+  double c_w[2][3];
+} gut_camera;
+
+/* Gaussians (PAPER Sec. 3, Eq. 1-2: mu, q, s, sigma, SH of order <= 3).
+ * count >= 0.  Arrays are read once by gut_scene_create (host pointers are
+ * copied; device pointers are read on the given stream).  Parameters are
+ * ACTIVATED (scale > 0, opacity in [0,1], reading R2).  Degenerate Gaussians
+ * (non-finite, scale <= 0, zero quaternion, opacity <= alpha_min) are culled
+ * and counted, not errors. */
+typedef struct {
+  uint32_t struct_size; /* = sizeof(gut_gaussians) */
+  int32_t sh_degree;    /* 0..3 */
+  int64_t count;
+  int32_t on_device; /* 1: CUDA device pointers; 0: host pointers */
+  int32_t pad0;
+  const float *means;     /* [count][3] world units */
+  const float *rotations; /* [count][4] (w,x,y,z), normalised inside (reading R1) */
+  const float *scales;    /* [count][3] */
+  const float *opacities; /* [count] */
+  const float *sh;        /* [count][(sh_degree+1)^2][3] (3DGS layout) */
+} gut_gaussians;
+
+typedef struct {
+  uint32_t struct_size;
+  float ut_alpha, ut_beta, ut_kappa; /* 1, 2, 0; 3 + lambda > 0 required */
+  float alpha_min;                   /* (float)(1/255): skip hits below (reading R20) */
+  float alpha_max;                   /* 0.99: alpha clamp (reading R20) */
+  float transmittance_min;           /* 1e-4: stop before T would drop below (R21) */
+  float cov2d_dilation;              /* 0.3 px^2 added to Sigma' (reading R10) */
+  float near_plane;                  /* 0.2 (z; distance for FISHEYE) (reading R9) */
+  int32_t rs_max_iterations;         /* 8 secant steps per sigma point (R14) */
+  float rs_tolerance_px;             /* 1e-4 px */
+  int32_t tile_cull;                 /* 0 = AABB, 1 = ellipse-tile (default) */
+  float background[3];               /* composited with the final T (R22) */
+  int32_t timing;                    /* 1: record per-stage CUDA-event times (adds events) */
+} gut_options;
+
+/* Outputs, HWC: rgb [H][W][3], alpha [H][W] (= 1 - T_final), depth [H][W]
+ * (= sum alpha_i T_i tau_i, un-normalised, reading R23).  depth may be NULL.
+ * on_device = 1: device pointers written on the stream.  on_device = 0: host
+ * pointers (pinned recommended) filled by device->host copies enqueued on the
+ * stream; valid once the stream has reached the end of the call. */
+typedef struct {
+  float *rgb;
+  float *alpha;
+  float *depth;
+  int32_t on_device;
+  int32_t pad0;
+} gut_outputs;
+
+typedef struct {
+  int64_t n_input, n_visible, n_keys;
+  int32_t n_tiles, max_tile_len;
+  int64_t pairs_evaluated;   /* (pixel, list entry) evaluations in the blend */
+  int64_t pairs_contributing;
+  int64_t pixels_terminated;
+  float ms_stage[6];         /* project, sort-depth, emit, sort-tile, ranges+blend, total (timing=1) */
+  int32_t overflow;          /* 1 if the reserved key capacity was exceeded */
+  int32_t pad0;
+} gut_stats;
+
+typedef enum {
+  GUT_STAGE_PROJECT = 1, /* per Gaussian gut_proj_record [n_input] */
+  GUT_STAGE_DEPTH_ORDER = 2, /* uint32 gid [n_visible], visible Gaussians by (depth, gid) */
+  GUT_STAGE_SORTED = 3,  /* uint32 pairs (tile, gid) [n_keys], sorted by (tile, depth, gid) */
+  GUT_STAGE_RANGES = 4   /* uint32 pairs [start, end) [n_tiles] */
+} gut_stage;
+
+typedef struct { /* GUT_STAGE_PROJECT record (K1 output, fp32) */
+  float vx, vy, cxx, cxy, cyy, k2; /* Eq. 9-10 mean / covariance (+dilation), extent level */
+  float depth;                     /* depth key (reading R13) */
+  float rgb[3];                    /* SH colour (reading R18) */
+  uint32_t tiles;                  /* tiles kept (0 = culled) */
+  uint16_t rect[4];                /* tile x0, y0, x1, y1 (inclusive) */
+} gut_proj_record;
+
+uint32_t gut_abi_version(void);
+void gut_options_default(gut_options *o);
+
+/* Creates a context on CUDA device `cuda_device` (must be sm_100).  out != NULL. */
+gut_status gut_context_create(int32_t cuda_device, gut_context **out);
+void gut_context_destroy(gut_context *ctx);
+/* Message for the last non-OK status on ctx (or a global message if ctx is NULL). */
+const char *gut_last_error(const gut_context *ctx);
+
+/* Capacity mode: pre-size the workspace for up to max_keys (Gaussian,tile)
+ * keys, max_gaussians Gaussians and max_w x max_h images.  After this call
+ * gut_render never synchronises; a frame whose key count exceeds max_keys is
+ * truncated and reported through gut_stats.overflow / GUT_E_CAPACITY on the
+ * next call that synchronises.  Without it, gut_render reads the key count
+ * back (one stream sync per view) and grows the workspace. */
+gut_status gut_workspace_reserve(gut_context *ctx, int64_t max_keys, int64_t max_gaussians,
+                                 int32_t max_w, int32_t max_h);
+
+/* Packs and validates a Gaussian set once (SoA, 16-byte aligned, on the
+ * context's device).  Amortised over views.  The scene is owned by the
+ * library until gut_scene_destroy. */
+gut_status gut_scene_create(gut_context *ctx, const gut_gaussians *g, gut_stream s, gut_scene **out);
+void gut_scene_destroy(gut_context *ctx, gut_scene *scene);
+
+/* Renders one view.  stats (nullable): if non-NULL the call synchronises the
+ * stream and fills it. */
+gut_status gut_render(gut_context *ctx, const gut_scene *scene, const gut_camera *cam,
+                      const gut_options *opt, const gut_outputs *out, gut_stream s, gut_stats *stats);
+
+/* Renders n_views views in order (outs[i] for cams[i]); stats nullable [n_views]. */
+gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_camera *cams,
+                            int32_t n_views, const gut_options *opt, const gut_outputs *outs,
+                            gut_stream s, gut_stats *stats);
+
+/* Tests only: copies an intermediate buffer of the LAST render on ctx to host
+ * memory (synchronises).  *bytes_needed receives the size; if host_dst is
+ * NULL or bytes is too small nothing is copied. */
+gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst, size_t bytes,
+                                size_t *bytes_needed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -708,9 +708,12 @@ int64_t orc_render(const float *means, const float *rots, const float *scales, c
  * is >= alpha_min - alpha_eps. */
 void orc_mark_ambiguity(const float *means, const float *rots, const float *scales, const float *opac,
                         const orc_proj *proj, int64_t n, const orc_camera *cam, const orc_options *o,
-                        double alpha_eps, orc_pixdiag *diag) {
+                        double alpha_eps, const int32_t *tile_subset, int32_t n_subset, orc_pixdiag *diag) {
   int tx_n = (cam->width + TILE - 1) / TILE, ty_n = (cam->height + TILE - 1) / TILE;
   const double e = 1e-3;
+  char *in_sub = (char *)malloc((size_t)tx_n * ty_n);
+  memset(in_sub, tile_subset ? 0 : 1, (size_t)tx_n * ty_n);
+  if (tile_subset) for (int k = 0; k < n_subset; ++k) in_sub[tile_subset[k]] = 1;
   for (int64_t i = 0; i < n; ++i) {
     const orc_proj *p = &proj[i];
     int is_bin = p->bin_ambig && (p->reason == ORC_OK || p->reason == ORC_CULL_OFFSCREEN || p->reason == ORC_CULL_NOTILE);
@@ -729,6 +732,7 @@ void orc_mark_ambiguity(const float *means, const float *rots, const float *scal
     }
     for (int ty = ay0; ty <= ay1; ++ty)
       for (int tx = ax0; tx <= ax1; ++tx) {
+        if (!in_sub[ty * tx_n + tx]) continue;
         if (!is_cull && tile_test(p, o->tile_cull, tx, ty, e) == tile_test(p, o->tile_cull, tx, ty, -e)) continue;
 #pragma omp parallel for schedule(static)
         for (int py = ty * TILE; py < ty * TILE + TILE; ++py) {
@@ -746,4 +750,5 @@ void orc_mark_ambiguity(const float *means, const float *rots, const float *scal
         }
       }
   }
+  free(in_sub);
 }

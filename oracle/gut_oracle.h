@@ -116,7 +116,8 @@ int64_t orc_render(const float *means, const float *rots, const float *scales, c
 /* flag pixels that an ambiguous (Gaussian, tile) pair or a cull-ambiguous Gaussian could change */
 void orc_mark_ambiguity(const float *means, const float *rots, const float *scales, const float *opac,
                         const orc_proj *proj, int64_t n, const orc_camera *cam, const orc_options *o,
-                        double alpha_eps, orc_pixdiag *diag);
+                        double alpha_eps, const int32_t *tile_subset, int32_t n_subset,
+                        orc_pixdiag *diag);
 int  orc_threads(void);
 
 #ifdef __cplusplus

@@ -106,7 +106,7 @@ def lib():
                                  C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]
         L.orc_render.restype = C.c_int64
         L.orc_mark_ambiguity.argtypes = [fp, fp, fp, fp, C.c_void_p, C.c_int64, C.POINTER(OrcCamera),
-                                         C.POINTER(OrcOptions), C.c_double, C.c_void_p]
+                                         C.POINTER(OrcOptions), C.c_double, ip, C.c_int32, C.c_void_p]
         L.orc_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -305,7 +305,8 @@ def render(scene, cam, opt, brute=False, tile_subset=None, ambiguity=True, alpha
                      proj.ctypes.data, C.byref(K))
     if ambiguity:
         lib().orc_mark_ambiguity(_fp(m), _fp(r), _fp(s), _fp(o), proj.ctypes.data, scene.count, C.byref(oc),
-                                 C.byref(oo), float(alpha_eps), diag.ctypes.data)
+                                 C.byref(oo), float(alpha_eps), None if sub is None else _ip(sub),
+                                 0 if sub is None else sub.size, diag.ctypes.data)
     return dict(rgb=rgb, alpha=alpha, depth=depth, diag=diag.reshape(H, W), proj=proj, n_keys=int(K.value))
 
 

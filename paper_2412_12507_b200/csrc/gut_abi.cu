@@ -1,0 +1,563 @@
+// gut_abi.cu — host side of the C ABI declared in include/gut.h.
+//
+// Validates arguments, owns the device workspace (grown on demand or reserved
+// up front), builds the per-view kernel parameters and enqueues K1..K5 on the
+// caller's stream.  No arithmetic of the method runs here: every step of the
+// path is a kernel (k1_project.cu, k3_sort.cu, k2_emit.cu, k5_blend.cu).  The
+// only host-side numbers are the per-view camera constants (pose at t = 0,
+// the slerp axis-angle, UT weights from alpha/beta/kappa).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/gut.h"
+#include "launch.h"
+
+using namespace gut;
+
+struct gut_scene {
+  SceneDev d;
+  int device;
+};
+
+struct gut_context {
+  int device = 0;
+  std::string err;
+  // workspace
+  size_t cap_n = 0, cap_k = 0, cap_tiles = 0, cap_pix = 0;
+  uint32_t *dkey = nullptr, *tiles = nullptr;
+  float4 *ell = nullptr, *payload = nullptr;
+  uint32_t *sa_k = nullptr, *sa_v = nullptr, *sb_k = nullptr, *sb_v = nullptr;
+  uint32_t *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr;
+  uint2 *ranges = nullptr;
+  float *img = nullptr;
+  unsigned long long *st_depth = nullptr, *st_emit = nullptr, *st_tile = nullptr;
+  uint32_t *counters = nullptr, *h_counters = nullptr;
+  uint32_t epoch = 0;
+  bool reserved = false;
+  cudaEvent_t ev[7] = {};
+  // last render (for gut_debug_copy_stage)
+  int64_t last_n = 0;
+  int last_tiles = 0;
+  const uint32_t *last_order = nullptr, *last_keys = nullptr, *last_vals = nullptr;
+};
+
+static thread_local std::string g_err;
+
+static gut_status fail(gut_context *ctx, gut_status s, const std::string &msg) {
+  if (ctx) ctx->err = msg; else g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(ctx, call)                                                                        \
+  do {                                                                                             \
+    cudaError_t e__ = (call);                                                                      \
+    if (e__ != cudaSuccess) {                                                                      \
+      return fail(ctx, e__ == cudaErrorMemoryAllocation ? GUT_E_OUT_OF_MEMORY : GUT_E_CUDA,        \
+                  std::string(#call) + ": " + cudaGetErrorString(e__));                            \
+    }                                                                                              \
+  } while (0)
+
+template <class T>
+static cudaError_t regrow(T *&p, size_t &cap_field_unused, size_t count) {
+  (void)cap_field_unused;
+  if (p) cudaFree(p);
+  p = nullptr;
+  return cudaMalloc((void **)&p, count * sizeof(T) + 16);
+}
+
+static gut_status ensure_n(gut_context *ctx, size_t n) {
+  if (n <= ctx->cap_n) return GUT_OK;
+  size_t c = n + n / 8 + 1024, dummy = 0;
+  CUDA_TRY(ctx, regrow(ctx->dkey, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->tiles, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->ell, dummy, 2 * c));
+  CUDA_TRY(ctx, regrow(ctx->payload, dummy, 4 * c));
+  CUDA_TRY(ctx, regrow(ctx->sa_k, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->sa_v, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->sb_k, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->sb_v, dummy, c));
+  size_t parts = (c + GUT_SORT_PART - 1) / GUT_SORT_PART + 1;
+  CUDA_TRY(ctx, regrow(ctx->st_depth, dummy, parts * 256));
+  CUDA_TRY(ctx, cudaMemset(ctx->st_depth, 0, parts * 256 * sizeof(unsigned long long)));
+  size_t eparts = (c + GUT_EMIT_PART - 1) / GUT_EMIT_PART + 1;
+  CUDA_TRY(ctx, regrow(ctx->st_emit, dummy, eparts));
+  CUDA_TRY(ctx, cudaMemset(ctx->st_emit, 0, eparts * sizeof(unsigned long long)));
+  ctx->cap_n = c;
+  return GUT_OK;
+}
+
+static gut_status ensure_k(gut_context *ctx, size_t k) {
+  if (k <= ctx->cap_k && ctx->ka) return GUT_OK;
+  size_t c = k + k / 4 + 4096, dummy = 0;
+  if (c >= (size_t)0x3FFFFFFF) return fail(ctx, GUT_E_CAPACITY, "key count exceeds 2^30");
+  CUDA_TRY(ctx, regrow(ctx->ka, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->va, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->kb, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->vb, dummy, c));
+  size_t parts = (c + GUT_SORT_PART - 1) / GUT_SORT_PART + 1;
+  CUDA_TRY(ctx, regrow(ctx->st_tile, dummy, parts * 256));
+  CUDA_TRY(ctx, cudaMemset(ctx->st_tile, 0, parts * 256 * sizeof(unsigned long long)));
+  ctx->cap_k = c;
+  return GUT_OK;
+}
+
+static gut_status ensure_tiles(gut_context *ctx, size_t t) {
+  if (t <= ctx->cap_tiles) return GUT_OK;
+  size_t dummy = 0;
+  CUDA_TRY(ctx, regrow(ctx->ranges, dummy, t));
+  ctx->cap_tiles = t;
+  return GUT_OK;
+}
+
+static gut_status ensure_pix(gut_context *ctx, size_t p) {
+  if (p <= ctx->cap_pix) return GUT_OK;
+  size_t dummy = 0;
+  CUDA_TRY(ctx, regrow(ctx->img, dummy, 5 * p));
+  ctx->cap_pix = p;
+  return GUT_OK;
+}
+
+// ------------------------------------------------------------- validation
+static bool quat_ok(const double q[4]) {
+  double n = q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3];
+  return std::isfinite(n) && n > 0;
+}
+
+static gut_status build_cam(gut_context *ctx, const gut_camera *cam, const gut_options *o, DevCam &c) {
+  if (!cam) return fail(ctx, GUT_E_INVALID_ARGUMENT, "camera: NULL");
+  if (cam->struct_size != sizeof(gut_camera)) return fail(ctx, GUT_E_INVALID_ARGUMENT, "camera.struct_size");
+  if (cam->model < 0 || cam->model > 3) return fail(ctx, GUT_E_INVALID_ARGUMENT, "camera.model");
+  if (cam->width <= 0 || cam->height <= 0) return fail(ctx, GUT_E_INVALID_ARGUMENT, "camera.width/height");
+  if (!(cam->fx > 0) || !(cam->fy > 0) || !std::isfinite(cam->fx) || !std::isfinite(cam->fy))
+    return fail(ctx, GUT_E_INVALID_ARGUMENT, "camera.fx/fy");
+  if (!std::isfinite(cam->cx) || !std::isfinite(cam->cy)) return fail(ctx, GUT_E_INVALID_ARGUMENT, "camera.cx/cy");
+  if (cam->shutter < 0 || cam->shutter > 4) return fail(ctx, GUT_E_INVALID_ARGUMENT, "camera.shutter");
+  if (!quat_ok(cam->q_c2w[0]) || !quat_ok(cam->q_c2w[1])) return fail(ctx, GUT_E_INVALID_ARGUMENT, "camera.q_c2w");
+  bool distorted = false;
+  for (int i = 0; i < 6; ++i) distorted |= cam->k[i] != 0;
+  distorted |= cam->p[0] != 0 || cam->p[1] != 0;
+  if (cam->model == GUT_CAM_FISHEYE && !(cam->fov_limit > 0 && cam->fov_limit <= M_PI))
+    return fail(ctx, GUT_E_INVALID_ARGUMENT, "camera.fov_limit (FISHEYE needs theta_max in (0, pi])");
+  if (cam->model == GUT_CAM_OPENCV && distorted && !(cam->fov_limit > 0))
+    return fail(ctx, GUT_E_INVALID_ARGUMENT, "camera.fov_limit (distorted OPENCV needs r_lim > 0)");
+  if (cam->model == GUT_CAM_ORTHO && cam->shutter != GUT_SHUTTER_GLOBAL)
+    return fail(ctx, GUT_E_UNSUPPORTED, "camera: rolling shutter with ORTHO is not supported");
+  if (!o) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options: NULL");
+  if (o->struct_size != sizeof(gut_options)) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.struct_size");
+  double a = o->ut_alpha, be = o->ut_beta, ka = o->ut_kappa;
+  double lam = a * a * (3.0 + ka) - 3.0;
+  if (!(3.0 + lam > 0)) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.ut_alpha/ut_kappa: 3 + lambda <= 0");
+  if (!(o->alpha_min > 0 && o->alpha_min < 1)) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.alpha_min");
+  if (!(o->alpha_max > o->alpha_min && o->alpha_max <= 1)) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.alpha_max");
+  if (!(o->transmittance_min >= 0 && o->transmittance_min < 1))
+    return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.transmittance_min");
+  if (!(o->cov2d_dilation >= 0) || !(o->near_plane >= 0)) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.cov2d_dilation/near_plane");
+  if (o->rs_max_iterations < 0 || !(o->rs_tolerance_px >= 0)) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.rs_*");
+  if (o->tile_cull != 0 && o->tile_cull != 1) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.tile_cull");
+
+  memset(&c, 0, sizeof(c));
+  c.model = cam->model; c.width = cam->width; c.height = cam->height; c.shutter = cam->shutter;
+  c.tiles_x = (cam->width + GUT_TILE - 1) / GUT_TILE;
+  c.tiles_y = (cam->height + GUT_TILE - 1) / GUT_TILE;
+  if ((int64_t)c.tiles_x * c.tiles_y > 65536) return fail(ctx, GUT_E_UNSUPPORTED, "camera: more than 65536 tiles");
+  c.n_tiles = c.tiles_x * c.tiles_y;
+  c.tile_cull = o->tile_cull;
+  c.fx = cam->fx; c.fy = cam->fy; c.cx = cam->cx; c.cy = cam->cy;
+  for (int i = 0; i < 6; ++i) { c.k[i] = cam->k[i]; c.kf[i] = (float)cam->k[i]; }
+  c.p[0] = cam->p[0]; c.p[1] = cam->p[1];
+  c.fov = cam->model == GUT_CAM_FISHEYE ? cam->fov_limit : (cam->fov_limit > 0 ? cam->fov_limit : 0);
+  c.fxf = (float)c.fx; c.fyf = (float)c.fy; c.cxf = (float)c.cx; c.cyf = (float)c.cy;
+  c.pf[0] = (float)c.p[0]; c.pf[1] = (float)c.p[1]; c.fovf = (float)c.fov;
+  // pose: R0 from the normalised t=0 quaternion; slerp axis-angle of q0^-1 q1
+  double q0[4], q1[4];
+  double n0 = sqrt(cam->q_c2w[0][0] * cam->q_c2w[0][0] + cam->q_c2w[0][1] * cam->q_c2w[0][1] +
+                   cam->q_c2w[0][2] * cam->q_c2w[0][2] + cam->q_c2w[0][3] * cam->q_c2w[0][3]);
+  double n1 = sqrt(cam->q_c2w[1][0] * cam->q_c2w[1][0] + cam->q_c2w[1][1] * cam->q_c2w[1][1] +
+                   cam->q_c2w[1][2] * cam->q_c2w[1][2] + cam->q_c2w[1][3] * cam->q_c2w[1][3]);
+  for (int i = 0; i < 4; ++i) { q0[i] = cam->q_c2w[0][i] / n0; q1[i] = cam->q_c2w[1][i] / n1; }
+  {
+    double w = q0[0], x = q0[1], y = q0[2], z = q0[3];
+    double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                   2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                   2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+    for (int i = 0; i < 9; ++i) { c.R0[i] = R[i]; c.R0f[i] = (float)R[i]; }
+  }
+  for (int i = 0; i < 3; ++i) c.c0[i] = cam->c_w[0][i];
+  c.phi_axis[0] = 1; c.phi_axisf[0] = 1;
+  if (cam->shutter != GUT_SHUTTER_GLOBAL) {
+    for (int i = 0; i < 3; ++i) { c.dc[i] = cam->c_w[1][i] - cam->c_w[0][i]; c.dcf[i] = (float)c.dc[i]; }
+    double d = q0[0] * q1[0] + q0[1] * q1[1] + q0[2] * q1[2] + q0[3] * q1[3];
+    if (d < 0) for (int i = 0; i < 4; ++i) q1[i] = -q1[i];
+    // q_rel = conj(q0) * q1
+    double aw = q0[0], ax = -q0[1], ay = -q0[2], az = -q0[3];
+    double bw = q1[0], bx = q1[1], by = q1[2], bz = q1[3];
+    double rw = aw * bw - ax * bx - ay * by - az * bz;
+    double rx = aw * bx + ax * bw + ay * bz - az * by;
+    double ry = aw * by - ax * bz + ay * bw + az * bx;
+    double rz = aw * bz + ax * by - ay * bx + az * bw;
+    double vn = sqrt(rx * rx + ry * ry + rz * rz);
+    c.phi_angle = 2.0 * atan2(vn, rw);
+    if (vn > 0) { c.phi_axis[0] = rx / vn; c.phi_axis[1] = ry / vn; c.phi_axis[2] = rz / vn; }
+    for (int i = 0; i < 3; ++i) c.phi_axisf[i] = (float)c.phi_axis[i];
+    c.phi_anglef = (float)c.phi_angle;
+  }
+  // UT weights (Eq. 7-8)
+  c.gamma = (float)sqrt(3.0 + lam);
+  c.wmu0 = (float)(lam / (3.0 + lam));
+  c.wmui = (float)(1.0 / (2.0 * (3.0 + lam)));
+  c.wsig0 = (float)(lam / (3.0 + lam) + (1.0 - a * a + be));
+  c.wsigi = c.wmui;
+  c.alpha_min = o->alpha_min; c.alpha_max = o->alpha_max; c.t_min = o->transmittance_min;
+  c.dilation = o->cov2d_dilation; c.near_plane = o->near_plane;
+  c.rs_tol_px = o->rs_tolerance_px; c.rs_max_iter = o->rs_max_iterations;
+  for (int i = 0; i < 3; ++i) c.bg[i] = o->background[i];
+  return GUT_OK;
+}
+
+// ------------------------------------------------------------------- ABI
+extern "C" {
+
+uint32_t gut_abi_version(void) { return GUT_ABI_VERSION; }
+
+void gut_options_default(gut_options *o) {
+  if (!o) return;
+  memset(o, 0, sizeof(*o));
+  o->struct_size = sizeof(gut_options);
+  o->ut_alpha = 1.0f; o->ut_beta = 2.0f; o->ut_kappa = 0.0f;
+  o->alpha_min = (float)(1.0 / 255.0);
+  o->alpha_max = 0.99f;
+  o->transmittance_min = 1e-4f;
+  o->cov2d_dilation = 0.3f;
+  o->near_plane = 0.2f;
+  o->rs_max_iterations = 8;
+  o->rs_tolerance_px = 1e-4f;
+  o->tile_cull = 1;
+}
+
+gut_status gut_context_create(int32_t dev, gut_context **out) {
+  if (!out) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "out: NULL");
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(nullptr, GUT_E_UNSUPPORTED, "no CUDA device (there is no CPU fallback)");
+  if (dev < 0 || dev >= ndev) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "cuda_device out of range");
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return fail(nullptr, GUT_E_CUDA, "cudaGetDeviceProperties");
+  if (p.major != 10 || p.minor != 0)
+    return fail(nullptr, GUT_E_UNSUPPORTED, "device is not sm_100 (B200); libgut is built for sm_100a only");
+  if (cudaSetDevice(dev) != cudaSuccess) return fail(nullptr, GUT_E_CUDA, "cudaSetDevice");
+  gut_context *ctx = new (std::nothrow) gut_context();
+  if (!ctx) return fail(nullptr, GUT_E_OUT_OF_MEMORY, "context");
+  ctx->device = dev;
+  if (cudaMalloc((void **)&ctx->counters, CNT_WORDS * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMallocHost((void **)&ctx->h_counters, CNT_WORDS * sizeof(uint32_t)) != cudaSuccess) {
+    delete ctx;
+    return fail(nullptr, GUT_E_OUT_OF_MEMORY, "counters");
+  }
+  for (auto &e : ctx->ev) cudaEventCreate(&e);
+  *out = ctx;
+  return GUT_OK;
+}
+
+void gut_context_destroy(gut_context *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->payload, ctx->sa_k, ctx->sa_v, ctx->sb_k, ctx->sb_v,
+                ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->img, ctx->st_depth, ctx->st_emit,
+                ctx->st_tile, ctx->counters};
+  for (void *p : ps) if (p) cudaFree(p);
+  if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
+  for (auto &e : ctx->ev) if (e) cudaEventDestroy(e);
+  delete ctx;
+}
+
+const char *gut_last_error(const gut_context *ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+gut_status gut_workspace_reserve(gut_context *ctx, int64_t max_keys, int64_t max_gaussians, int32_t max_w,
+                                 int32_t max_h) {
+  if (!ctx) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "ctx: NULL");
+  if (max_keys <= 0 || max_gaussians < 0 || max_w <= 0 || max_h <= 0)
+    return fail(ctx, GUT_E_INVALID_ARGUMENT, "gut_workspace_reserve: sizes");
+  cudaSetDevice(ctx->device);
+  gut_status s;
+  if ((s = ensure_n(ctx, (size_t)max_gaussians)) != GUT_OK) return s;
+  if ((s = ensure_k(ctx, (size_t)max_keys)) != GUT_OK) return s;
+  size_t tiles = (size_t)((max_w + 15) / 16) * ((max_h + 15) / 16);
+  if ((s = ensure_tiles(ctx, tiles)) != GUT_OK) return s;
+  if ((s = ensure_pix(ctx, (size_t)max_w * max_h)) != GUT_OK) return s;
+  ctx->reserved = true;
+  return GUT_OK;
+}
+
+gut_status gut_scene_create(gut_context *ctx, const gut_gaussians *g, gut_stream stream, gut_scene **out) {
+  if (!ctx || !g || !out) return fail(ctx, GUT_E_INVALID_ARGUMENT, "gut_scene_create: NULL argument");
+  *out = nullptr;
+  if (g->struct_size != sizeof(gut_gaussians)) return fail(ctx, GUT_E_INVALID_ARGUMENT, "gaussians.struct_size");
+  if (g->count < 0 || g->count > 0x3FFFFFFF) return fail(ctx, GUT_E_INVALID_ARGUMENT, "gaussians.count");
+  if (g->sh_degree < 0 || g->sh_degree > 3) return fail(ctx, GUT_E_INVALID_ARGUMENT, "gaussians.sh_degree");
+  if (g->count > 0 && (!g->means || !g->rotations || !g->scales || !g->opacities || !g->sh))
+    return fail(ctx, GUT_E_INVALID_ARGUMENT, "gaussians: NULL array");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  gut_scene *sc = new (std::nothrow) gut_scene();
+  if (!sc) return fail(ctx, GUT_E_OUT_OF_MEMORY, "scene");
+  sc->device = ctx->device;
+  SceneDev &d = sc->d;
+  d.n = g->count;
+  d.sh_degree = g->sh_degree;
+  const int nf = 3 * (g->sh_degree + 1) * (g->sh_degree + 1);
+  d.sh_chunks = (nf + 3) / 4;
+  size_t n = (size_t)(g->count > 0 ? g->count : 1);
+  if (cudaMalloc((void **)&d.pos_opa, n * 16) != cudaSuccess || cudaMalloc((void **)&d.rot, n * 16) != cudaSuccess ||
+      cudaMalloc((void **)&d.scale, n * 16) != cudaSuccess ||
+      cudaMalloc((void **)&d.sh, n * 16 * d.sh_chunks) != cudaSuccess) {
+    gut_scene_destroy(ctx, sc);
+    return fail(ctx, GUT_E_OUT_OF_MEMORY, "scene arrays");
+  }
+  if (g->count > 0) {
+    const float *m = g->means, *r = g->rotations, *s = g->scales, *o = g->opacities, *h = g->sh;
+    float *raw = nullptr;
+    if (!g->on_device) {
+      size_t tot = n * (3 + 4 + 3 + 1 + nf);
+      if (cudaMalloc((void **)&raw, tot * sizeof(float)) != cudaSuccess) {
+        gut_scene_destroy(ctx, sc);
+        return fail(ctx, GUT_E_OUT_OF_MEMORY, "scene staging");
+      }
+      float *p = raw;
+      const float *src[5] = {g->means, g->rotations, g->scales, g->opacities, g->sh};
+      size_t cnt[5] = {3, 4, 3, 1, (size_t)nf};
+      const float **dst[5] = {&m, &r, &s, &o, &h};
+      for (int k = 0; k < 5; ++k) {
+        cudaMemcpyAsync(p, src[k], n * cnt[k] * sizeof(float), cudaMemcpyHostToDevice, st);
+        *dst[k] = p;
+        p += n * cnt[k];
+      }
+    }
+    launch_pack_scene(m, r, s, o, h, d, st);
+    if (raw) {
+      cudaStreamSynchronize(st);
+      cudaFree(raw);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      gut_scene_destroy(ctx, sc);
+      return fail(ctx, GUT_E_CUDA, std::string("scene pack: ") + cudaGetErrorString(e));
+    }
+  }
+  *out = sc;
+  return GUT_OK;
+}
+
+void gut_scene_destroy(gut_context *ctx, gut_scene *sc) {
+  (void)ctx;
+  if (!sc) return;
+  cudaSetDevice(sc->device);
+  if (sc->d.pos_opa) cudaFree(sc->d.pos_opa);
+  if (sc->d.rot) cudaFree(sc->d.rot);
+  if (sc->d.scale) cudaFree(sc->d.scale);
+  if (sc->d.sh) cudaFree(sc->d.sh);
+  delete sc;
+}
+
+static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut_camera *cam, const gut_options *opt,
+                             const gut_outputs *out, cudaStream_t st, gut_stats *stats) {
+  if (!ctx) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "ctx: NULL");
+  if (!scene) return fail(ctx, GUT_E_INVALID_ARGUMENT, "scene: NULL");
+  if (!out || !out->rgb || !out->alpha) return fail(ctx, GUT_E_INVALID_ARGUMENT, "outputs.rgb/alpha: NULL");
+  if (scene->device != ctx->device) return fail(ctx, GUT_E_INVALID_ARGUMENT, "scene belongs to another device");
+  DevCam dc;
+  gut_status s = build_cam(ctx, cam, opt, dc);
+  if (s != GUT_OK) return s;
+  cudaSetDevice(ctx->device);
+  const int64_t N = scene->d.n;
+  const size_t npix = (size_t)dc.width * dc.height;
+  if ((s = ensure_n(ctx, (size_t)N)) != GUT_OK) return s;
+  if ((s = ensure_tiles(ctx, (size_t)dc.n_tiles)) != GUT_OK) return s;
+  if (!out->on_device && (s = ensure_pix(ctx, npix)) != GUT_OK) return s;
+  if (!ctx->ka && (s = ensure_k(ctx, (size_t)N * 4 + 1024)) != GUT_OK) return s;
+  const bool timing = opt->timing != 0;
+  if (timing) cudaEventRecord(ctx->ev[0], st);
+
+  uint32_t *cnt = ctx->counters;
+  CUDA_TRY(ctx, cudaMemsetAsync(cnt, 0, CNT_WORDS * sizeof(uint32_t), st));
+  // K1: UT projection
+  launch_project(dc, scene->d, ctx->dkey, ctx->tiles, ctx->ell, ctx->payload, cnt, st);
+  if (timing) cudaEventRecord(ctx->ev[1], st);
+  // K3 level 1: depth sort of the visible Gaussians (4 LSD passes, first one compacts)
+  const uint32_t n32 = (uint32_t)N;
+  const uint32_t *hd = cnt + CNT_HIST_DEPTH;
+  launch_sort_pass(ctx->dkey, nullptr, ctx->sa_k, ctx->sa_v, nullptr, n32, 0, hd, ctx->st_depth,
+                   cnt + CNT_TICKETS + 0, ++ctx->epoch, true, st);
+  launch_sort_pass(ctx->sa_k, ctx->sa_v, ctx->sb_k, ctx->sb_v, cnt + CNT_NVIS, n32, 8, hd + 256, ctx->st_depth,
+                   cnt + CNT_TICKETS + 1, ++ctx->epoch, false, st);
+  launch_sort_pass(ctx->sb_k, ctx->sb_v, ctx->sa_k, ctx->sa_v, cnt + CNT_NVIS, n32, 16, hd + 512, ctx->st_depth,
+                   cnt + CNT_TICKETS + 2, ++ctx->epoch, false, st);
+  launch_sort_pass(ctx->sa_k, ctx->sa_v, nullptr, ctx->sb_v, cnt + CNT_NVIS, n32, 24, hd + 768, ctx->st_depth,
+                   cnt + CNT_TICKETS + 3, ++ctx->epoch, false, st);
+  const uint32_t *order = ctx->sb_v;
+  if (timing) cudaEventRecord(ctx->ev[2], st);
+  // key count: capacity mode keeps the stream asynchronous; otherwise read K back
+  size_t n_keys_host;
+  if (ctx->reserved) {
+    n_keys_host = ctx->cap_k;
+  } else {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_counters, cnt, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    unsigned long long K;
+    memcpy(&K, &ctx->h_counters[CNT_K], 8);
+    if ((s = ensure_k(ctx, (size_t)K)) != GUT_OK) return s;
+    n_keys_host = (size_t)K;
+  }
+  // K2: depth-ordered scan + emission of (tile, gid) keys
+  launch_emit(order, cnt + CNT_NVIS, n32, ctx->tiles, ctx->ell, dc.tiles_x, dc.tile_cull, ctx->ka, ctx->va,
+              (uint32_t)ctx->cap_k, cnt, ctx->st_emit, ++ctx->epoch, st);
+  if (timing) cudaEventRecord(ctx->ev[3], st);
+  // K3 level 2: stable tile passes
+  const uint32_t *ht = cnt + CNT_HIST_TILE;
+  const uint32_t *kdev = cnt + CNT_K;  // low word of the u64 key count (K < 2^30)
+  const uint32_t nk = (uint32_t)n_keys_host;
+  const uint32_t *fk, *fv;
+  launch_sort_pass(ctx->ka, ctx->va, ctx->kb, ctx->vb, kdev, nk, 0, ht, ctx->st_tile, cnt + CNT_TICKETS + 5,
+                   ++ctx->epoch, false, st);
+  fk = ctx->kb; fv = ctx->vb;
+  if (dc.n_tiles > 256) {
+    launch_sort_pass(ctx->kb, ctx->vb, ctx->ka, ctx->va, kdev, nk, 8, ht + 256, ctx->st_tile,
+                     cnt + CNT_TICKETS + 6, ++ctx->epoch, false, st);
+    fk = ctx->ka; fv = ctx->va;
+  }
+  if (timing) cudaEventRecord(ctx->ev[4], st);
+  // K4 ranges, K5 blend
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->ranges, 0, (size_t)dc.n_tiles * sizeof(uint2), st));
+  launch_ranges(fk, cnt, (uint32_t)ctx->cap_k, ctx->ranges, st);
+  float *rgb = out->rgb, *alpha = out->alpha, *depth = out->depth;
+  if (!out->on_device) {
+    rgb = ctx->img;
+    alpha = ctx->img + 3 * npix;
+    depth = out->depth ? ctx->img + 4 * npix : nullptr;
+  }
+  launch_blend(dc, ctx->ranges, fv, ctx->payload, rgb, alpha, depth, cnt, st);
+  if (timing) cudaEventRecord(ctx->ev[5], st);
+  {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ctx, GUT_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  }
+  if (!out->on_device) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(out->rgb, rgb, 3 * npix * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(out->alpha, alpha, npix * sizeof(float), cudaMemcpyDeviceToHost, st));
+    if (out->depth)
+      CUDA_TRY(ctx, cudaMemcpyAsync(out->depth, depth, npix * sizeof(float), cudaMemcpyDeviceToHost, st));
+  }
+  ctx->last_n = N;
+  ctx->last_tiles = dc.n_tiles;
+  ctx->last_order = order;
+  ctx->last_keys = fk;
+  ctx->last_vals = fv;
+  if (stats) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_counters, cnt, 32 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    const uint32_t *h = ctx->h_counters;
+    memset(stats, 0, sizeof(*stats));
+    unsigned long long K, pe, pc, pt;
+    memcpy(&K, &h[CNT_K], 8);
+    memcpy(&pe, &h[CNT_PAIRS_EVAL], 8);
+    memcpy(&pc, &h[CNT_PAIRS_CONTRIB], 8);
+    memcpy(&pt, &h[CNT_TERMINATED], 8);
+    stats->n_input = N;
+    stats->n_visible = h[CNT_NVIS];
+    stats->n_keys = (int64_t)K;
+    stats->n_tiles = dc.n_tiles;
+    stats->max_tile_len = (int32_t)h[CNT_MAXLEN];
+    stats->pairs_evaluated = (int64_t)pe;
+    stats->pairs_contributing = (int64_t)pc;
+    stats->pixels_terminated = (int64_t)pt;
+    stats->overflow = (h[CNT_OVERFLOW] != 0 || K > ctx->cap_k) ? 1 : 0;
+    if (timing) {
+      float t[5];
+      for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], ctx->ev[i], ctx->ev[i + 1]);
+      stats->ms_stage[0] = t[0]; stats->ms_stage[1] = t[1]; stats->ms_stage[2] = t[2];
+      stats->ms_stage[3] = t[3]; stats->ms_stage[4] = t[4];
+      cudaEventElapsedTime(&stats->ms_stage[5], ctx->ev[0], ctx->ev[5]);
+    }
+    if (stats->overflow) return fail(ctx, GUT_E_CAPACITY, "key capacity exceeded (gut_workspace_reserve)");
+  }
+  return GUT_OK;
+}
+
+gut_status gut_render(gut_context *ctx, const gut_scene *scene, const gut_camera *cam, const gut_options *opt,
+                      const gut_outputs *out, gut_stream s, gut_stats *stats) {
+  return render_one(ctx, scene, cam, opt, out, (cudaStream_t)s, stats);
+}
+
+gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_camera *cams, int32_t n_views,
+                            const gut_options *opt, const gut_outputs *outs, gut_stream s, gut_stats *stats) {
+  if (!ctx) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "ctx: NULL");
+  if (n_views < 0 || (n_views > 0 && (!cams || !outs))) return fail(ctx, GUT_E_INVALID_ARGUMENT, "batch arguments");
+  for (int32_t v = 0; v < n_views; ++v) {
+    gut_status r = render_one(ctx, scene, &cams[v], opt, &outs[v], (cudaStream_t)s, stats ? &stats[v] : nullptr);
+    if (r != GUT_OK) return r;
+  }
+  return GUT_OK;
+}
+
+gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst, size_t bytes, size_t *bytes_needed) {
+  if (!ctx) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "ctx: NULL");
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaDeviceSynchronize());
+  uint32_t h[8];
+  CUDA_TRY(ctx, cudaMemcpy(h, ctx->counters, sizeof(h), cudaMemcpyDeviceToHost));
+  unsigned long long K;
+  memcpy(&K, &h[CNT_K], 8);
+  if (K > ctx->cap_k) K = ctx->cap_k;
+  const size_t N = (size_t)ctx->last_n, nv = h[CNT_NVIS];
+  size_t need = 0;
+  switch (stage) {
+    case GUT_STAGE_PROJECT: need = N * sizeof(gut_proj_record); break;
+    case GUT_STAGE_DEPTH_ORDER: need = nv * sizeof(uint32_t); break;
+    case GUT_STAGE_SORTED: need = (size_t)K * 2 * sizeof(uint32_t); break;
+    case GUT_STAGE_RANGES: need = (size_t)ctx->last_tiles * 2 * sizeof(uint32_t); break;
+    default: return fail(ctx, GUT_E_INVALID_ARGUMENT, "stage");
+  }
+  if (bytes_needed) *bytes_needed = need;
+  if (!host_dst || bytes < need) return GUT_OK;
+  if (stage == GUT_STAGE_PROJECT) {
+    uint32_t *tl = new uint32_t[N + 1], *dk = new uint32_t[N + 1];
+    float4 *el = new float4[2 * N + 1], *pl = new float4[4 * N + 1];
+    cudaMemcpy(tl, ctx->tiles, N * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(dk, ctx->dkey, N * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(el, ctx->ell, N * 32, cudaMemcpyDeviceToHost);
+    cudaMemcpy(pl, ctx->payload, N * 64, cudaMemcpyDeviceToHost);
+    gut_proj_record *r = (gut_proj_record *)host_dst;
+    for (size_t i = 0; i < N; ++i) {
+      memset(&r[i], 0, sizeof(r[i]));
+      r[i].tiles = tl[i];
+      if (!tl[i]) continue;
+      float4 a = el[2 * i], b = el[2 * i + 1], p3 = pl[4 * i + 3];
+      r[i].vx = a.x; r[i].vy = a.y; r[i].cxx = a.z; r[i].cxy = a.w; r[i].cyy = b.x; r[i].k2 = b.y;
+      memcpy(&r[i].depth, &dk[i], 4);
+      r[i].rgb[0] = p3.y; r[i].rgb[1] = p3.z; r[i].rgb[2] = p3.w;
+      uint32_t r0, r1;
+      memcpy(&r0, &b.z, 4);
+      memcpy(&r1, &b.w, 4);
+      r[i].rect[0] = (uint16_t)(r0 & 0xFFFF); r[i].rect[1] = (uint16_t)(r0 >> 16);
+      r[i].rect[2] = (uint16_t)(r1 & 0xFFFF); r[i].rect[3] = (uint16_t)(r1 >> 16);
+    }
+    delete[] tl; delete[] dk; delete[] el; delete[] pl;
+  } else if (stage == GUT_STAGE_DEPTH_ORDER) {
+    CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->last_order, need, cudaMemcpyDeviceToHost));
+  } else if (stage == GUT_STAGE_SORTED) {
+    uint32_t *t = new uint32_t[K + 1], *g = new uint32_t[K + 1];
+    cudaMemcpy(t, ctx->last_keys, K * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(g, ctx->last_vals, K * 4, cudaMemcpyDeviceToHost);
+    uint32_t *o = (uint32_t *)host_dst;
+    for (size_t k = 0; k < K; ++k) { o[2 * k] = t[k]; o[2 * k + 1] = g[k]; }
+    delete[] t; delete[] g;
+  } else {
+    CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->ranges, need, cudaMemcpyDeviceToHost));
+  }
+  return GUT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,198 @@
+// gut_internal.cuh — device-side types and helpers shared by the sm_100a kernels.
+// Product code: never includes anything under oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define GUT_TILE 16
+#define GUT_BLEND_THREADS 256
+#define GUT_SORT_THREADS 256
+#define GUT_SORT_ITEMS 16
+#define GUT_SORT_PART (GUT_SORT_THREADS * GUT_SORT_ITEMS)  // 4096 keys per onesweep partition
+#define GUT_EMIT_THREADS 256
+#define GUT_EMIT_ITEMS 4
+#define GUT_EMIT_PART (GUT_EMIT_THREADS * GUT_EMIT_ITEMS)  // 1024 Gaussians per emit partition
+#define GUT_CULLED_KEY 0xFFFFFFFFu
+
+namespace gut {
+
+enum { CAM_PINHOLE = 0, CAM_OPENCV = 1, CAM_FISHEYE = 2, CAM_ORTHO = 3 };
+enum { SH_GLOBAL = 0, SH_T2B = 1, SH_L2R = 2, SH_B2T = 3, SH_R2L = 4 };
+
+// Per-view camera + options, passed by value as a kernel parameter.
+struct DevCam {
+  int model, width, height, shutter;
+  int tiles_x, tiles_y, n_tiles, tile_cull;
+  // intrinsics (fp64 master copy; fp32 copies for K1)
+  double fx, fy, cx, cy, k[6], p[2], fov;
+  float fxf, fyf, cxf, cyf, kf[6], pf[2], fovf;
+  // pose: R0 = camera->world at t=0 (row-major), c0 = centre at t=0,
+  // dc = c1 - c0, phi = axis-angle (body frame) of R0^T R1 (slerp = R0 Exp(t phi))
+  double R0[9], c0[3], dc[3], phi_axis[3], phi_angle;
+  float R0f[9], dcf[3], phi_axisf[3], phi_anglef;
+  // UT weights (Eq. 7-8) and thresholds
+  float gamma;        // sqrt(3 + lambda)
+  float wmu0, wmui, wsig0, wsigi;
+  float alpha_min, alpha_max, t_min, dilation, near_plane;
+  float rs_tol_px;
+  int rs_max_iter;
+  float bg[3];
+};
+
+// ---------------------------------------------------------------- small math
+struct f3 { float x, y, z; };
+struct d3 { double x, y, z; };
+
+__host__ __device__ __forceinline__ f3 mk(float x, float y, float z) { return {x, y, z}; }
+__host__ __device__ __forceinline__ d3 mkd(double x, double y, double z) { return {x, y, z}; }
+__host__ __device__ __forceinline__ f3 operator+(f3 a, f3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__host__ __device__ __forceinline__ f3 operator-(f3 a, f3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__host__ __device__ __forceinline__ f3 operator*(float s, f3 a) { return {s * a.x, s * a.y, s * a.z}; }
+__host__ __device__ __forceinline__ float dot(f3 a, f3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__host__ __device__ __forceinline__ f3 cross(f3 a, f3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__host__ __device__ __forceinline__ d3 operator+(d3 a, d3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__host__ __device__ __forceinline__ d3 operator-(d3 a, d3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__host__ __device__ __forceinline__ d3 operator*(double s, d3 a) { return {s * a.x, s * a.y, s * a.z}; }
+__host__ __device__ __forceinline__ double dot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__host__ __device__ __forceinline__ d3 cross(d3 a, d3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__host__ __device__ __forceinline__ f3 tof(d3 a) { return {(float)a.x, (float)a.y, (float)a.z}; }
+__host__ __device__ __forceinline__ d3 tod(f3 a) { return {(double)a.x, (double)a.y, (double)a.z}; }
+// row-major 3x3 times vector / transposed times vector
+template <class M, class V>
+__host__ __device__ __forceinline__ V mv(const M *m, V v) {
+  return {m[0] * v.x + m[1] * v.y + m[2] * v.z, m[3] * v.x + m[4] * v.y + m[5] * v.z,
+          m[6] * v.x + m[7] * v.y + m[8] * v.z};
+}
+template <class M, class V>
+__host__ __device__ __forceinline__ V mtv(const M *m, V v) {
+  return {m[0] * v.x + m[3] * v.y + m[6] * v.z, m[1] * v.x + m[4] * v.y + m[7] * v.z,
+          m[2] * v.x + m[5] * v.y + m[8] * v.z};
+}
+
+// Rodrigues: R = I + sin(a) [u]x + (1 - cos(a)) [u]x^2, row-major (fp32)
+__device__ __forceinline__ void rodrigues(f3 u, float ang, float R[9]) {
+  float s, c;
+  sincosf(ang, &s, &c);
+  float t = 1.f - c;
+  R[0] = c + t * u.x * u.x;       R[1] = t * u.x * u.y - s * u.z; R[2] = t * u.x * u.z + s * u.y;
+  R[3] = t * u.x * u.y + s * u.z; R[4] = c + t * u.y * u.y;       R[5] = t * u.y * u.z - s * u.x;
+  R[6] = t * u.x * u.z - s * u.y; R[7] = t * u.y * u.z + s * u.x; R[8] = c + t * u.z * u.z;
+}
+__device__ __forceinline__ void rodrigues_d(d3 u, double ang, double R[9]) {
+  double s, c;
+  sincos(ang, &s, &c);
+  double t = 1.0 - c;
+  R[0] = c + t * u.x * u.x;       R[1] = t * u.x * u.y - s * u.z; R[2] = t * u.x * u.z + s * u.y;
+  R[3] = t * u.x * u.y + s * u.z; R[4] = c + t * u.y * u.y;       R[5] = t * u.y * u.z - s * u.x;
+  R[6] = t * u.x * u.z - s * u.y; R[7] = t * u.y * u.z + s * u.x; R[8] = c + t * u.z * u.z;
+}
+template <class T>
+__host__ __device__ __forceinline__ void matmul3(const T *A, const T *B, T *C) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) C[3 * i + j] = A[3 * i] * B[j] + A[3 * i + 1] * B[3 + j] + A[3 * i + 2] * B[6 + j];
+}
+
+// ----------------------------------------------------------- tile row spans
+// Ellipse-tile test in closed form per tile row (StopThePop-style culling,
+// PAPER L216): E = {v : (v - vmu)^T Sigma'^-1 (v - vmu) <= k2}.  The band
+// y in [16 ty, 16 ty + 16] cuts E in a convex set whose x-extent is either the
+// ellipse's extreme point (if it lies in the band) or the chord at the band
+// edge nearest to it.  Tiles whose closed x-range meets that extent are kept.
+// K1 (counting) and K2 (emission) call this same function, so counts and
+// emitted keys agree bit for bit.
+struct Ell {
+  float vx, vy, cxx, cxy, cyy, k2;
+  int x0, y0, x1, y1;  // clamped tile rectangle
+};
+
+__device__ __forceinline__ void row_span(const Ell &e, int ty, int tile_cull, int &lo, int &hi) {
+  if (tile_cull == 0) { lo = e.x0; hi = e.x1; return; }
+  float hy = sqrtf(e.k2 * e.cyy);
+  float a = fmaxf((float)(GUT_TILE * ty) - e.vy, -hy);
+  float b = fminf((float)(GUT_TILE * ty + GUT_TILE) - e.vy, hy);
+  if (a > b) { lo = 1; hi = 0; return; }
+  float hx = sqrtf(e.k2 * e.cxx);
+  float ystar = e.cxy * sqrtf(e.k2 / e.cxx);  // dy of the rightmost point (leftmost at -ystar)
+  float slope = e.cxy / e.cyy;
+  float cond = fmaxf(e.cxx - e.cxy * slope, 0.f);  // det / cyy
+  float xr, xl;
+  if (ystar >= a && ystar <= b) xr = hx;
+  else {
+    float yy = ystar < a ? a : b;
+    xr = slope * yy + sqrtf(fmaxf(cond * (e.k2 - yy * yy / e.cyy), 0.f));
+  }
+  if (-ystar >= a && -ystar <= b) xl = -hx;
+  else {
+    float yy = -ystar < a ? a : b;
+    xl = slope * yy - sqrtf(fmaxf(cond * (e.k2 - yy * yy / e.cyy), 0.f));
+  }
+  float XL = e.vx + xl, XR = e.vx + xr;
+  int l = (int)ceilf(XL * (1.f / GUT_TILE)) - 1;
+  int h = (int)floorf(XR * (1.f / GUT_TILE));
+  lo = max(l, e.x0);
+  hi = min(h, e.x1);
+}
+
+__device__ __forceinline__ int ell_tile_count(const Ell &e, int tile_cull) {
+  if (tile_cull == 0) return (e.x1 - e.x0 + 1) * (e.y1 - e.y0 + 1);
+  int n = 0;
+  for (int ty = e.y0; ty <= e.y1; ++ty) {
+    int lo, hi;
+    row_span(e, ty, tile_cull, lo, hi);
+    n += max(hi - lo + 1, 0);
+  }
+  return n;
+}
+
+__device__ __forceinline__ Ell load_ell(const float4 *ell, uint32_t g) {
+  float4 a = ell[2 * g], b = ell[2 * g + 1];
+  Ell e;
+  e.vx = a.x; e.vy = a.y; e.cxx = a.z; e.cxy = a.w; e.cyy = b.x; e.k2 = b.y;
+  uint32_t r0 = __float_as_uint(b.z), r1 = __float_as_uint(b.w);
+  e.x0 = (int)(r0 & 0xFFFF); e.y0 = (int)(r0 >> 16); e.x1 = (int)(r1 & 0xFFFF); e.y1 = (int)(r1 >> 16);
+  return e;
+}
+
+// ------------------------------------------------------ decoupled look-back
+// 64-bit status words: [63:32] epoch, [31:30] flag (1 = aggregate, 2 = inclusive),
+// [29:0] count.  A word from an older epoch reads as "not ready", so the
+// status arrays never need clearing between passes / renders.
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long mk_status(uint32_t epoch, uint32_t flag, uint32_t cnt) {
+  return ((unsigned long long)epoch << 32) | ((unsigned long long)flag << 30) | (cnt & 0x3FFFFFFFu);
+}
+// exclusive prefix of `mine` for partition `part`, lane of status row `col`
+__device__ __forceinline__ uint32_t lookback(unsigned long long *status, int stride, int part, int col,
+                                             uint32_t mine, uint32_t epoch) {
+  if (part == 0) {
+    st_relaxed(&status[col], mk_status(epoch, 2, mine));
+    return 0;
+  }
+  st_relaxed(&status[(size_t)part * stride + col], mk_status(epoch, 1, mine));
+  uint32_t sum = 0;
+  int j = part - 1;
+  while (true) {
+    unsigned long long s = ld_relaxed(&status[(size_t)j * stride + col]);
+    if ((uint32_t)(s >> 32) != epoch) continue;  // not ready yet
+    uint32_t flag = (uint32_t)(s >> 30) & 3u;
+    if (flag == 0) continue;
+    sum += (uint32_t)s & 0x3FFFFFFFu;
+    if (flag == 2) break;
+    --j;
+  }
+  st_relaxed(&status[(size_t)part * stride + col], mk_status(epoch, 2, sum + mine));
+  return sum;
+}
+
+}  // namespace gut

@@ -1,0 +1,325 @@
+// k1_project.cu — K1: per-Gaussian Unscented-Transform projection (sm_100a).
+//
+// PAPER.md Sec. 4.1 (L135-178), Alg. 1 Rasterize + Alg. 2 Estimate2DGaussian
+// (L627-667): lambda, sigma points (Eq. 6), weights (Eq. 7-8), exact
+// projection of every sigma point g(x) (L170) — with its own row-time pose
+// under rolling shutter (L34, L393) — then the 2D mean / covariance (Eq. 9-10),
+// the opacity-aware extent (Alg. 1 l.3), the rectangle (l.5), the tile count
+// (StopThePop-style ellipse culling, L216), the depth key and the SH colour.
+//
+// One thread per Gaussian; SoA float4 loads (3 x 16 B for every Gaussian, the
+// SH block only for survivors).  fp32 arithmetic except the camera-frame
+// centre R0^T (mu - c0), which is formed in fp64 so that sigma-point pixels
+// carry only the error of their small offsets.  Block-aggregated atomics
+// produce the visible count, the key total K and the four 8-bit digit
+// histograms of the depth keys consumed by the onesweep passes (K3).
+#include "launch.h"
+
+namespace gut {
+
+__device__ __forceinline__ bool project_cam_f(const DevCam &c, f3 x, float &du, float &dv) {
+  // returns pixel offsets from the principal point (du, dv); validity first
+  switch (c.model) {
+    case CAM_PINHOLE: {
+      if (!(x.z > c.near_plane)) return false;
+      du = c.fxf * (x.x / x.z);
+      dv = c.fyf * (x.y / x.z);
+      return true;
+    }
+    case CAM_ORTHO: {
+      if (!(x.z > c.near_plane)) return false;
+      du = c.fxf * x.x;
+      dv = c.fyf * x.y;
+      return true;
+    }
+    case CAM_OPENCV: {
+      if (!(x.z > c.near_plane)) return false;
+      float xn = x.x / x.z, yn = x.y / x.z, r2 = xn * xn + yn * yn;
+      if (c.fovf > 0.f && !(r2 <= c.fovf * c.fovf)) return false;
+      float num = 1.f + r2 * (c.kf[0] + r2 * (c.kf[1] + r2 * c.kf[2]));
+      float den = 1.f + r2 * (c.kf[3] + r2 * (c.kf[4] + r2 * c.kf[5]));
+      float a = num / den;
+      float xd = xn * a + 2.f * c.pf[0] * xn * yn + c.pf[1] * (r2 + 2.f * xn * xn);
+      float yd = yn * a + c.pf[0] * (r2 + 2.f * yn * yn) + 2.f * c.pf[1] * xn * yn;
+      du = c.fxf * xd;
+      dv = c.fyf * yd;
+      return true;
+    }
+    case CAM_FISHEYE: {
+      float nrm = sqrtf(x.x * x.x + x.y * x.y + x.z * x.z);
+      if (!(nrm > c.near_plane)) return false;
+      float rho = sqrtf(x.x * x.x + x.y * x.y);
+      float th = atan2f(rho, x.z);
+      if (!(th <= c.fovf)) return false;
+      if (rho == 0.f) { du = 0.f; dv = 0.f; return true; }
+      float t2 = th * th;
+      float td = th * (1.f + t2 * (c.kf[0] + t2 * (c.kf[1] + t2 * (c.kf[2] + t2 * c.kf[3]))));
+      float s = td / rho;
+      du = c.fxf * (s * x.x);
+      dv = c.fyf * (s * x.y);
+      return true;
+    }
+  }
+  return false;
+}
+
+__device__ __forceinline__ float shutter_coord(const DevCam &c, float du, float dv) {
+  float r;
+  switch (c.shutter) {
+    case SH_T2B: r = (dv + c.cyf) / (float)c.height; break;
+    case SH_B2T: r = 1.f - (dv + c.cyf) / (float)c.height; break;
+    case SH_L2R: r = (du + c.cxf) / (float)c.width; break;
+    case SH_R2L: r = 1.f - (du + c.cxf) / (float)c.width; break;
+    default: return 0.f;
+  }
+  return fminf(fmaxf(r, 0.f), 1.f);
+}
+
+// camera-frame point at shutter time t: x_c(t) = R(t)^T (x - c(t)) with
+// R(t) = R0 Exp(t phi), c(t) = c0 + t dc  =>  Exp(t phi)^T (y - t w),
+// y = R0^T (x - c0), w = R0^T dc.
+__device__ __forceinline__ f3 cam_point_at(const DevCam &c, f3 y, f3 w, float t) {
+  float Rt[9];
+  rodrigues(mk(c.phi_axisf[0], c.phi_axisf[1], c.phi_axisf[2]), t * c.phi_anglef, Rt);
+  return mtv(Rt, y - t * w);
+}
+
+// g(x) with the sigma point's own extrinsic (reading R14): the shutter time is
+// the fixed point t* = clamp(rho(g(x; pose(t*)))), solved by secant steps from
+// (0.5, rho(g(x; pose(0.5)))) until the pixel moves < rs_tol_px.
+__device__ __forceinline__ bool project_sigma(const DevCam &c, f3 y, f3 w, float &du, float &dv,
+                                              float &t_out) {
+  if (c.shutter == SH_GLOBAL) {
+    t_out = 0.f;
+    return project_cam_f(c, y, du, dv);
+  }
+  float t0 = 0.5f, u0, v0;
+  if (!project_cam_f(c, cam_point_at(c, y, w, t0), u0, v0)) return false;
+  float f0 = shutter_coord(c, u0, v0) - t0;
+  float t1 = t0 + f0, u1, v1;
+  if (!project_cam_f(c, cam_point_at(c, y, w, t1), u1, v1)) return false;
+  float f1 = shutter_coord(c, u1, v1) - t1;
+  for (int it = 0; it < c.rs_max_iter; ++it) {
+    if (hypotf(u1 - u0, v1 - v0) < c.rs_tol_px) break;
+    float den = f1 - f0;
+    float t2 = fabsf(den) > 1e-12f ? t1 - f1 * (t1 - t0) / den : t1 + f1;
+    t2 = fminf(fmaxf(t2, 0.f), 1.f);
+    t0 = t1; u0 = u1; v0 = v1; f0 = f1; t1 = t2;
+    if (!project_cam_f(c, cam_point_at(c, y, w, t1), u1, v1)) return false;
+    f1 = shutter_coord(c, u1, v1) - t1;
+  }
+  du = u1; dv = v1; t_out = t1;
+  return true;
+}
+
+// 3DGS real SH basis up to degree DEG (reading R19), colour = max(sum + 0.5, 0)
+template <int DEG>
+__device__ __forceinline__ f3 sh_colour(const float4 *sh, int64_t n, int64_t i, f3 d) {
+  constexpr int NC = (DEG + 1) * (DEG + 1);
+  constexpr int CH = (3 * NC + 3) / 4;
+  float f[CH * 4];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    float4 v = __ldg(&sh[(int64_t)c * n + i]);
+    f[4 * c] = v.x; f[4 * c + 1] = v.y; f[4 * c + 2] = v.z; f[4 * c + 3] = v.w;
+  }
+  float Y[16];
+  float x = d.x, y = d.y, z = d.z, xx = x * x, yy = y * y, zz = z * z;
+  Y[0] = 0.28209479177387814f;
+  if (DEG >= 1) { Y[1] = -0.4886025119029199f * y; Y[2] = 0.4886025119029199f * z; Y[3] = -0.4886025119029199f * x; }
+  if (DEG >= 2) {
+    Y[4] = 1.0925484305920792f * x * y; Y[5] = -1.0925484305920792f * y * z;
+    Y[6] = 0.31539156525252005f * (2.f * zz - xx - yy); Y[7] = -1.0925484305920792f * x * z;
+    Y[8] = 0.5462742152960396f * (xx - yy);
+  }
+  if (DEG >= 3) {
+    Y[9] = -0.5900435899266435f * y * (3.f * xx - yy); Y[10] = 2.890611442640554f * x * y * z;
+    Y[11] = -0.4570457994644658f * y * (4.f * zz - xx - yy);
+    Y[12] = 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+    Y[13] = -0.4570457994644658f * x * (4.f * zz - xx - yy); Y[14] = 1.445305721320277f * z * (xx - yy);
+    Y[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
+  }
+  float r = 0.5f, g = 0.5f, b = 0.5f;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) { r += Y[k] * f[3 * k]; g += Y[k] * f[3 * k + 1]; b += Y[k] * f[3 * k + 2]; }
+  return mk(fmaxf(r, 0.f), fmaxf(g, 0.f), fmaxf(b, 0.f));
+}
+
+template <int DEG>
+__global__ __launch_bounds__(256) void project_kernel(DevCam c, SceneDev s, uint32_t *__restrict__ dkey,
+                                                      uint32_t *__restrict__ tiles, float4 *__restrict__ ell,
+                                                      float4 *__restrict__ payload, uint32_t *counters) {
+  __shared__ uint32_t s_hist[4][256];
+  __shared__ unsigned long long s_k[8];
+  __shared__ uint32_t s_nv[8];
+  for (int j = threadIdx.x; j < 1024; j += 256) (&s_hist[0][0])[j] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  uint32_t my_tiles = 0, key = GUT_CULLED_KEY;
+  if (i < s.n) {
+    float4 po = __ldg(&s.pos_opa[i]), ro = __ldg(&s.rot[i]), sc = __ldg(&s.scale[i]);
+    float qn2 = ro.x * ro.x + ro.y * ro.y + ro.z * ro.z + ro.w * ro.w;
+    bool ok = isfinite(po.x) && isfinite(po.y) && isfinite(po.z) && isfinite(qn2) && qn2 > 0.f &&
+              sc.x > 0.f && sc.y > 0.f && sc.z > 0.f && isfinite(sc.x) && isfinite(sc.y) &&
+              isfinite(sc.z) && po.w > c.alpha_min && isfinite(po.w);
+    float du[7], dv[7], tt[7];
+    f3 y0;
+    d3 y0d;
+    float R[9];
+    f3 wv = mk(0.f, 0.f, 0.f);
+    if (ok) {
+      // O1: R(q) from the normalised quaternion (w,x,y,z), Eq. 2
+      float inv = 1.f / sqrtf(qn2);
+      float w = ro.x * inv, x = ro.y * inv, y = ro.z * inv, z = ro.w * inv;
+      R[0] = 1.f - 2.f * (y * y + z * z); R[1] = 2.f * (x * y - w * z); R[2] = 2.f * (x * z + w * y);
+      R[3] = 2.f * (x * y + w * z); R[4] = 1.f - 2.f * (x * x + z * z); R[5] = 2.f * (y * z - w * x);
+      R[6] = 2.f * (x * z - w * y); R[7] = 2.f * (y * z + w * x); R[8] = 1.f - 2.f * (x * x + y * y);
+      // camera-frame centre in fp64, sigma offsets gamma s_j R[:,j] rotated in fp32 (Eq. 6)
+      y0d = mtv(c.R0, mkd(po.x, po.y, po.z) - mkd(c.c0[0], c.c0[1], c.c0[2]));
+      y0 = tof(y0d);
+      wv = mtv(c.R0f, mk(c.dcf[0], c.dcf[1], c.dcf[2]));
+      float sj[3] = {sc.x, sc.y, sc.z};
+      ok = project_sigma(c, y0, wv, du[0], dv[0], tt[0]);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        f3 L = (c.gamma * sj[j]) * mk(R[j], R[3 + j], R[6 + j]);
+        f3 Lc = mtv(c.R0f, L);
+        ok = ok && project_sigma(c, y0 + Lc, wv, du[1 + j], dv[1 + j], tt[1 + j]);
+        ok = ok && project_sigma(c, y0 - Lc, wv, du[4 + j], dv[4 + j], tt[4 + j]);
+      }
+    }
+    float vx = 0, vy = 0, cxx = 0, cxy = 0, cyy = 0, k2 = 0;
+    if (ok) {
+      // Eq. 9-10, then + dilation (reading R10)
+      vx = c.wmu0 * du[0] + c.wmui * (((du[1] + du[4]) + (du[2] + du[5])) + (du[3] + du[6]));
+      vy = c.wmu0 * dv[0] + c.wmui * (((dv[1] + dv[4]) + (dv[2] + dv[5])) + (dv[3] + dv[6]));
+      float ex = du[0] - vx, ey = dv[0] - vy;
+      cxx = c.wsig0 * ex * ex; cxy = c.wsig0 * ex * ey; cyy = c.wsig0 * ey * ey;
+      float sxx = 0, sxy = 0, syy = 0;
+#pragma unroll
+      for (int k = 1; k < 7; ++k) {
+        float ax = du[k] - vx, ay = dv[k] - vy;
+        sxx += ax * ax; sxy += ax * ay; syy += ay * ay;
+      }
+      cxx += c.wsigi * sxx + c.dilation;
+      cxy += c.wsigi * sxy;
+      cyy += c.wsigi * syy + c.dilation;
+      float det = cxx * cyy - cxy * cxy;
+      ok = cxx > 0.f && cyy > 0.f && det > 0.f && isfinite(det);
+      // opacity-aware extent level (Alg. 1 l.3, reading R11)
+      k2 = 2.f * logf(po.w / c.alpha_min);
+      ok = ok && k2 > 0.f;
+    }
+    Ell e;
+    if (ok) {
+      float hx = sqrtf(k2 * cxx), hy = sqrtf(k2 * cyy);
+      e.vx = vx + c.cxf; e.vy = vy + c.cyf;
+      e.cxx = cxx; e.cxy = cxy; e.cyy = cyy; e.k2 = k2;
+      float fx0 = floorf(fminf(fmaxf((e.vx - hx) * (1.f / GUT_TILE), -1e6f), 1e6f));
+      float fx1 = floorf(fminf(fmaxf((e.vx + hx) * (1.f / GUT_TILE), -1e6f), 1e6f));
+      float fy0 = floorf(fminf(fmaxf((e.vy - hy) * (1.f / GUT_TILE), -1e6f), 1e6f));
+      float fy1 = floorf(fminf(fmaxf((e.vy + hy) * (1.f / GUT_TILE), -1e6f), 1e6f));
+      e.x0 = max((int)fx0, 0); e.x1 = min((int)fx1, c.tiles_x - 1);
+      e.y0 = max((int)fy0, 0); e.y1 = min((int)fy1, c.tiles_y - 1);
+      ok = e.x0 <= e.x1 && e.y0 <= e.y1;
+      if (ok) {
+        my_tiles = (uint32_t)ell_tile_count(e, c.tile_cull);
+        ok = my_tiles > 0;
+      }
+    }
+    if (ok) {
+      // depth key (reading R13): camera-frame distance of mu at its own time t0
+      double t0 = tt[0];
+      d3 dcw = mkd(c.dc[0], c.dc[1], c.dc[2]);
+      d3 yc = y0d - t0 * mtv(c.R0, dcw);
+      float depth = (float)sqrt(dot(yc, yc));
+      key = __float_as_uint(depth);
+      // colour (reading R18): SH at d = normalize(mu - c(t0))
+      d3 dw = mkd(po.x, po.y, po.z) - (mkd(c.c0[0], c.c0[1], c.c0[2]) + t0 * dcw);
+      double nd = sqrt(dot(dw, dw));
+      f3 dir = tof((1.0 / nd) * dw);
+      f3 rgb = sh_colour<DEG>(s.sh, s.n, i, dir);
+      ell[2 * i] = make_float4(e.vx, e.vy, e.cxx, e.cxy);
+      ell[2 * i + 1] = make_float4(e.cyy, e.k2, __uint_as_float((uint32_t)e.x0 | ((uint32_t)e.y0 << 16)),
+                                   __uint_as_float((uint32_t)e.x1 | ((uint32_t)e.y1 << 16)));
+      // blend payload: mu, sigma, M = diag(1/s) R^T (Eq. 11 o_g = M (o - mu)), rgb
+      float is0 = 1.f / sc.x, is1 = 1.f / sc.y, is2 = 1.f / sc.z;
+      payload[4 * i] = po;
+      payload[4 * i + 1] = make_float4(R[0] * is0, R[3] * is0, R[6] * is0, R[1] * is1);
+      payload[4 * i + 2] = make_float4(R[4] * is1, R[7] * is1, R[2] * is2, R[5] * is2);
+      payload[4 * i + 3] = make_float4(R[8] * is2, rgb.x, rgb.y, rgb.z);
+    } else {
+      my_tiles = 0;
+      key = GUT_CULLED_KEY;
+    }
+    dkey[i] = key;
+    tiles[i] = my_tiles;
+  }
+  if (my_tiles) {
+    atomicAdd(&s_hist[0][key & 255u], 1u);
+    atomicAdd(&s_hist[1][(key >> 8) & 255u], 1u);
+    atomicAdd(&s_hist[2][(key >> 16) & 255u], 1u);
+    atomicAdd(&s_hist[3][key >> 24], 1u);
+  }
+  // block totals: visible count and K
+  unsigned long long kk = my_tiles;
+  uint32_t nv = my_tiles ? 1u : 0u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kk += __shfl_xor_sync(0xffffffffu, kk, o);
+    nv += __shfl_xor_sync(0xffffffffu, nv, o);
+  }
+  if ((threadIdx.x & 31) == 0) { s_k[threadIdx.x >> 5] = kk; s_nv[threadIdx.x >> 5] = nv; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long K = 0;
+    uint32_t V = 0;
+    for (int w = 0; w < 8; ++w) { K += s_k[w]; V += s_nv[w]; }
+    if (V) {
+      atomicAdd(&counters[CNT_NVIS], V);
+      atomicAdd(reinterpret_cast<unsigned long long *>(&counters[CNT_K]), K);
+    }
+  }
+  for (int j = threadIdx.x; j < 1024; j += 256) {
+    uint32_t v = (&s_hist[0][0])[j];
+    if (v) atomicAdd(&counters[CNT_HIST_DEPTH + j], v);
+  }
+}
+
+__global__ void pack_scene_kernel(const float *__restrict__ means, const float *__restrict__ rots,
+                                  const float *__restrict__ scales, const float *__restrict__ opac,
+                                  const float *__restrict__ sh, SceneDev s) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= s.n) return;
+  s.pos_opa[i] = make_float4(means[3 * i], means[3 * i + 1], means[3 * i + 2], opac[i]);
+  s.rot[i] = make_float4(rots[4 * i], rots[4 * i + 1], rots[4 * i + 2], rots[4 * i + 3]);
+  s.scale[i] = make_float4(scales[3 * i], scales[3 * i + 1], scales[3 * i + 2], 0.f);
+  int nf = 3 * (s.sh_degree + 1) * (s.sh_degree + 1);
+  const float *src = sh + (int64_t)nf * i;
+  for (int c = 0; c < s.sh_chunks; ++c) {
+    float v[4];
+    for (int j = 0; j < 4; ++j) v[j] = (4 * c + j < nf) ? src[4 * c + j] : 0.f;
+    s.sh[(int64_t)c * s.n + i] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+void launch_pack_scene(const float *means, const float *rots, const float *scales, const float *opac,
+                       const float *sh, SceneDev s, cudaStream_t st) {
+  if (s.n == 0) return;
+  int64_t blocks = (s.n + 255) / 256;
+  pack_scene_kernel<<<(unsigned)blocks, 256, 0, st>>>(means, rots, scales, opac, sh, s);
+}
+
+void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32_t *tiles, float4 *ell,
+                    float4 *payload, uint32_t *counters, cudaStream_t st) {
+  if (s.n == 0) return;
+  unsigned blocks = (unsigned)((s.n + 255) / 256);
+  switch (s.sh_degree) {
+    case 0: project_kernel<0><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters); break;
+    case 1: project_kernel<1><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters); break;
+    case 2: project_kernel<2><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters); break;
+    default: project_kernel<3><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters); break;
+  }
+}
+
+}  // namespace gut

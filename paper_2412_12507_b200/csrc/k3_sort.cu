@@ -1,0 +1,161 @@
+// k3_sort.cu — K3: hand-written onesweep LSD radix-sort pass (sm_100a).
+//
+// The (tile_id, depth) order of PAPER L208 ("3DGS sorts them globally for each
+// tile") is produced as an LSD radix sort in two levels:
+//   level 1: 4 passes over the 32-bit depth key of the N_vis visible Gaussians
+//            (value = Gaussian index; the first pass also drops culled ones);
+//   level 2: after depth-ordered emission (K2), 1-2 passes over the tile id.
+// Stable LSD passes give exactly the (tile, depth, index) order of one 64-bit
+// key sort while moving 3-5x fewer bytes.
+//
+// One pass = one kernel: a CTA claims a 4096-key partition by ticket (forward
+// progress for the look-back), ranks its keys per 8-bit digit with warp
+// match-any (stable: items are ranked in sequence order), publishes its digit
+// histogram and resolves its global digit offsets by decoupled look-back
+// (epoch-tagged status words), then reorders through shared memory so the
+// global writes are digit runs (coalesced).  Placement comes only from scans:
+// deterministic, no atomics choose positions.
+#include "launch.h"
+
+namespace gut {
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// exclusive block scan of one value per thread (256 threads); returns exclusive, *total
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t *s_tmp, uint32_t *total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_tmp[w] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t t = threadIdx.x < 8 ? s_tmp[threadIdx.x] : 0;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (threadIdx.x < 8) s_tmp[8 + threadIdx.x] = t;  // inclusive warp prefix
+  }
+  __syncthreads();
+  uint32_t wpre = w > 0 ? s_tmp[8 + w - 1] : 0;
+  if (total) *total = s_tmp[15];
+  uint32_t r = wpre + x - v;
+  __syncthreads();
+  return r;
+}
+
+template <bool FIRST>
+__global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
+    const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, uint32_t *__restrict__ keys_out,
+    uint32_t *__restrict__ vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
+    const uint32_t *__restrict__ hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch) {
+  constexpr int W = GUT_SORT_THREADS / 32;
+  __shared__ uint32_t s_keys[GUT_SORT_PART];
+  __shared__ uint32_t s_vals[GUT_SORT_PART];
+  __shared__ uint32_t s_wcnt[W][256];
+  __shared__ uint32_t s_goff[256];
+  __shared__ uint32_t s_loff[256];
+  __shared__ uint32_t s_tmp[16];
+  __shared__ uint32_t s_part;
+
+  const uint32_t n = n_dev ? min(*n_dev, n_host) : n_host;
+  if (threadIdx.x == 0) s_part = atomicAdd(ticket, 1u);
+  for (int j = threadIdx.x; j < W * 256; j += GUT_SORT_THREADS) (&s_wcnt[0][0])[j] = 0;
+  __syncthreads();
+  const uint32_t part = s_part;
+  const uint32_t base = part * GUT_SORT_PART;
+  if (base >= n) return;
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  uint32_t key[GUT_SORT_ITEMS], val[GUT_SORT_ITEMS], rank[GUT_SORT_ITEMS];
+  // warp w owns the contiguous sub-range [base + w*512, base + (w+1)*512)
+#pragma unroll
+  for (int j = 0; j < GUT_SORT_ITEMS; ++j) {
+    uint32_t idx = base + w * (32 * GUT_SORT_ITEMS) + j * 32 + lane;
+    bool in = idx < n;
+    key[j] = in ? __ldg(&keys_in[idx]) : GUT_CULLED_KEY;
+    if (FIRST) val[j] = idx;
+    else val[j] = in ? __ldg(&vals_in[idx]) : 0u;
+    if (!FIRST && !in) key[j] = 0xFFFFFFFFu;
+    // validity travels in rank's top bit until ranking
+    rank[j] = (in && (!FIRST || key[j] != GUT_CULLED_KEY)) ? 1u : 0u;
+  }
+  // stable per-warp ranking, rounds in sequence order
+#pragma unroll
+  for (int j = 0; j < GUT_SORT_ITEMS; ++j) {
+    const bool valid = rank[j] != 0;
+    const uint32_t d = valid ? (key[j] >> shift) & 255u : 256u;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t before = __popc(peers & lt);
+    uint32_t prev = valid ? s_wcnt[w][d] : 0u;
+    __syncwarp();
+    if (valid && before == 0) s_wcnt[w][d] = prev + __popc(peers);
+    __syncwarp();
+    rank[j] = valid ? (prev + before) : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  // per-digit: exclusive over warps, partition total
+  const uint32_t dgt = threadIdx.x;  // 256 threads = 256 digits
+  uint32_t tot = 0;
+#pragma unroll
+  for (int ww = 0; ww < W; ++ww) {
+    uint32_t c = s_wcnt[ww][dgt];
+    s_wcnt[ww][dgt] = tot;
+    tot += c;
+  }
+  // publish + decoupled look-back for this digit
+  const uint32_t gpre = lookback(status, 256, (int)part, (int)dgt, tot, epoch);
+  // global digit start (exclusive scan of the pass histogram) and local digit start
+  uint32_t hsum;
+  const uint32_t hex = block_excl_scan256(__ldg(&hist[dgt]), s_tmp, &hsum);
+  uint32_t ltotal;
+  const uint32_t lex = block_excl_scan256(tot, s_tmp, &ltotal);
+  s_goff[dgt] = hex + gpre;
+  s_loff[dgt] = lex;
+  __syncthreads();
+  // scatter into shared memory in digit order
+#pragma unroll
+  for (int j = 0; j < GUT_SORT_ITEMS; ++j) {
+    if (rank[j] != 0xFFFFFFFFu) {
+      const uint32_t d = (key[j] >> shift) & 255u;
+      const uint32_t pos = s_loff[d] + s_wcnt[w][d] + rank[j];
+      s_keys[pos] = key[j];
+      s_vals[pos] = val[j];
+    }
+  }
+  __syncthreads();
+  // coalesced write-out of the digit runs
+  for (uint32_t p = threadIdx.x; p < ltotal; p += GUT_SORT_THREADS) {
+    const uint32_t k = s_keys[p];
+    const uint32_t d = (k >> shift) & 255u;
+    const uint32_t o = s_goff[d] + (p - s_loff[d]);
+    if (keys_out) keys_out[o] = k;
+    vals_out[o] = s_vals[p];
+  }
+}
+
+void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                      uint32_t *vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
+                      const uint32_t *hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch,
+                      bool first, cudaStream_t st) {
+  if (n_host == 0) return;
+  unsigned blocks = (n_host + GUT_SORT_PART - 1) / GUT_SORT_PART;
+  if (first)
+    onesweep_kernel<true><<<blocks, GUT_SORT_THREADS, 0, st>>>(keys_in, vals_in, keys_out, vals_out, n_dev,
+                                                               n_host, shift, hist, status, ticket, epoch);
+  else
+    onesweep_kernel<false><<<blocks, GUT_SORT_THREADS, 0, st>>>(keys_in, vals_in, keys_out, vals_out, n_dev,
+                                                                n_host, shift, hist, status, ticket, epoch);
+}
+
+}  // namespace gut

@@ -1,0 +1,57 @@
+// launch.h — host-side launchers of the sm_100a kernels (internal to libgut).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gut_internal.cuh"
+
+namespace gut {
+
+// Packed scene (device SoA).  pos_opa = (mu, sigma), rot = (w,x,y,z) raw,
+// scale = (s, 0), sh = float4 chunk c of Gaussian i at sh[c * n + i].
+struct SceneDev {
+  int64_t n;
+  int sh_degree, sh_chunks;
+  float4 *pos_opa, *rot, *scale, *sh;
+};
+
+// Counters block (uint32 words), zeroed at the start of every render.
+enum : int {
+  CNT_NVIS = 0,
+  CNT_K = 2,          // u64
+  CNT_TICKETS = 4,    // 12 tickets
+  CNT_OVERFLOW = 16,
+  CNT_PAIRS_EVAL = 18,     // u64
+  CNT_PAIRS_CONTRIB = 20,  // u64
+  CNT_TERMINATED = 22,     // u64
+  CNT_MAXLEN = 24,
+  CNT_HIST_DEPTH = 32,     // 4 x 256
+  CNT_HIST_TILE = 32 + 1024,  // 2 x 256
+  CNT_WORDS = 32 + 1024 + 512
+};
+
+void launch_pack_scene(const float *means, const float *rots, const float *scales, const float *opac,
+                       const float *sh, SceneDev s, cudaStream_t st);
+
+void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32_t *tiles, float4 *ell,
+                    float4 *payload, uint32_t *counters, cudaStream_t st);
+
+// one onesweep LSD pass over 8-bit digit `shift`; first = keys only, value = index,
+// items equal to GUT_CULLED_KEY dropped.  n_dev: device count (nullable, then n_host).
+void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                      uint32_t *vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
+                      const uint32_t *hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch,
+                      bool first, cudaStream_t st);
+
+void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper, const uint32_t *tiles,
+                 const float4 *ell, int tiles_x, int tile_cull, uint32_t *out_tile, uint32_t *out_gid,
+                 uint32_t cap_k, uint32_t *counters, unsigned long long *status, uint32_t epoch,
+                 cudaStream_t st);
+
+void launch_ranges(const uint32_t *tile_sorted, const uint32_t *counters, uint32_t cap_k, uint2 *ranges,
+                   cudaStream_t st);
+
+void launch_blend(const DevCam &cam, const uint2 *ranges, const uint32_t *gids, const float4 *payload,
+                  float *rgb, float *alpha, float *depth, uint32_t *counters, cudaStream_t st);
+
+}  // namespace gut

@@ -1,0 +1,290 @@
+"""Thin Python binding of libgut (include/gut.h): argument marshalling only.
+
+Every step of the render runs in the sm_100a kernels behind the C ABI; this
+module only converts Python values into the ABI structs and passes pointers.
+PyTorch is used for device memory and streams.  There is no CPU fallback: if
+libgut.so is missing or the device is not a B200, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgut.so")
+
+GUT_OK = 0
+STATUS = {0: "GUT_OK", 1: "GUT_E_INVALID_ARGUMENT", 2: "GUT_E_UNSUPPORTED", 3: "GUT_E_OUT_OF_MEMORY",
+          4: "GUT_E_CAPACITY", 5: "GUT_E_CUDA", 6: "GUT_E_INTERNAL"}
+MODELS = {"pinhole": 0, "opencv": 1, "fisheye": 2, "ortho": 3}
+SHUTTERS = {"global": 0, "top_to_bottom": 1, "left_to_right": 2, "bottom_to_top": 3, "right_to_left": 4}
+STAGE_PROJECT, STAGE_DEPTH_ORDER, STAGE_SORTED, STAGE_RANGES = 1, 2, 3, 4
+
+
+class gut_camera(C.Structure):
+    _fields_ = [("struct_size", C.c_uint32), ("model", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
+                ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("k", C.c_double * 6), ("p", C.c_double * 2), ("fov_limit", C.c_double),
+                ("shutter", C.c_int32), ("pad0", C.c_int32), ("q_c2w", (C.c_double * 4) * 2),
+                ("c_w", (C.c_double * 3) * 2)]
+
+
+class gut_gaussians(C.Structure):
+    _fields_ = [("struct_size", C.c_uint32), ("sh_degree", C.c_int32), ("count", C.c_int64),
+                ("on_device", C.c_int32), ("pad0", C.c_int32), ("means", C.c_void_p), ("rotations", C.c_void_p),
+                ("scales", C.c_void_p), ("opacities", C.c_void_p), ("sh", C.c_void_p)]
+
+
+class gut_options(C.Structure):
+    _fields_ = [("struct_size", C.c_uint32), ("ut_alpha", C.c_float), ("ut_beta", C.c_float),
+                ("ut_kappa", C.c_float), ("alpha_min", C.c_float), ("alpha_max", C.c_float),
+                ("transmittance_min", C.c_float), ("cov2d_dilation", C.c_float), ("near_plane", C.c_float),
+                ("rs_max_iterations", C.c_int32), ("rs_tolerance_px", C.c_float), ("tile_cull", C.c_int32),
+                ("background", C.c_float * 3), ("timing", C.c_int32)]
+
+
+class gut_outputs(C.Structure):
+    _fields_ = [("rgb", C.c_void_p), ("alpha", C.c_void_p), ("depth", C.c_void_p), ("on_device", C.c_int32),
+                ("pad0", C.c_int32)]
+
+
+class gut_stats(C.Structure):
+    _fields_ = [("n_input", C.c_int64), ("n_visible", C.c_int64), ("n_keys", C.c_int64), ("n_tiles", C.c_int32),
+                ("max_tile_len", C.c_int32), ("pairs_evaluated", C.c_int64), ("pairs_contributing", C.c_int64),
+                ("pixels_terminated", C.c_int64), ("ms_stage", C.c_float * 6), ("overflow", C.c_int32),
+                ("pad0", C.c_int32)]
+
+    def as_dict(self):
+        return {k: (list(getattr(self, k)) if k == "ms_stage" else getattr(self, k))
+                for k, _ in self._fields_ if k != "pad0"}
+
+
+class gut_proj_record(C.Structure):
+    _fields_ = [("vx", C.c_float), ("vy", C.c_float), ("cxx", C.c_float), ("cxy", C.c_float), ("cyy", C.c_float),
+                ("k2", C.c_float), ("depth", C.c_float), ("rgb", C.c_float * 3), ("tiles", C.c_uint32),
+                ("rect", C.c_uint16 * 4)]
+
+
+EXPORTS = ["gut_abi_version", "gut_options_default", "gut_context_create", "gut_context_destroy",
+           "gut_last_error", "gut_workspace_reserve", "gut_scene_create", "gut_scene_destroy", "gut_render",
+           "gut_render_batch", "gut_debug_copy_stage"]
+
+_lib = None
+
+
+class GutError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def lib():
+    """Loads libgut.so; raises if it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2412_12507_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        L.gut_abi_version.restype = C.c_uint32
+        L.gut_options_default.argtypes = [C.POINTER(gut_options)]
+        L.gut_context_create.argtypes = [i32, C.POINTER(vp)]
+        L.gut_context_destroy.argtypes = [vp]
+        L.gut_last_error.argtypes = [vp]
+        L.gut_last_error.restype = C.c_char_p
+        L.gut_workspace_reserve.argtypes = [vp, i64, i64, i32, i32]
+        L.gut_scene_create.argtypes = [vp, C.POINTER(gut_gaussians), vp, C.POINTER(vp)]
+        L.gut_scene_destroy.argtypes = [vp, vp]
+        L.gut_render.argtypes = [vp, vp, C.POINTER(gut_camera), C.POINTER(gut_options), C.POINTER(gut_outputs), vp,
+                                 C.POINTER(gut_stats)]
+        L.gut_render_batch.argtypes = [vp, vp, C.POINTER(gut_camera), i32, C.POINTER(gut_options),
+                                       C.POINTER(gut_outputs), vp, C.POINTER(gut_stats)]
+        L.gut_debug_copy_stage.argtypes = [vp, i32, vp, C.c_size_t, C.POINTER(C.c_size_t)]
+        for name in ("gut_context_create", "gut_workspace_reserve", "gut_scene_create", "gut_render",
+                     "gut_render_batch", "gut_debug_copy_stage"):
+            getattr(L, name).restype = C.c_int
+        L.gut_options_default.restype = None
+        L.gut_context_destroy.restype = None
+        L.gut_scene_destroy.restype = None
+        _lib = L
+    return _lib
+
+
+def _check(status, ctx=None):
+    if status != GUT_OK:
+        msg = lib().gut_last_error(ctx)
+        raise GutError(status, msg.decode() if msg else "")
+
+
+# ------------------------------------------------------------- marshalling
+def make_camera(cam) -> gut_camera:
+    """Any object with the scenegen.Camera attributes -> gut_camera."""
+    c = gut_camera()
+    c.struct_size = C.sizeof(gut_camera)
+    c.model = MODELS[cam.model]
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    for i in range(6):
+        c.k[i] = float(cam.k[i])
+    c.p[0], c.p[1] = float(cam.p[0]), float(cam.p[1])
+    c.fov_limit = float(cam.fov_limit)
+    c.shutter = SHUTTERS[cam.shutter]
+    for t in range(2):
+        for i in range(4):
+            c.q_c2w[t][i] = float(cam.q_c2w[t][i])
+        for i in range(3):
+            c.c_w[t][i] = float(cam.c_w[t][i])
+    return c
+
+
+def make_options(opt=None, timing: bool = False) -> gut_options:
+    o = gut_options()
+    lib().gut_options_default(C.byref(o))
+    if opt is not None:
+        o.ut_alpha, o.ut_beta, o.ut_kappa = opt.ut_alpha, opt.ut_beta, opt.ut_kappa
+        o.alpha_min, o.alpha_max = opt.alpha_min, opt.alpha_max
+        o.transmittance_min, o.cov2d_dilation = opt.transmittance_min, opt.cov2d_dilation
+        o.near_plane, o.rs_max_iterations = opt.near_plane, int(opt.rs_max_iterations)
+        o.rs_tolerance_px, o.tile_cull = opt.rs_tolerance_px, int(opt.tile_cull)
+        for i in range(3):
+            o.background[i] = opt.background[i]
+    o.timing = int(timing)
+    return o
+
+
+# ------------------------------------------------------------- same-name calls
+def gut_abi_version() -> int:
+    return int(lib().gut_abi_version())
+
+
+def gut_context_create(device: int = 0):
+    h = C.c_void_p()
+    _check(lib().gut_context_create(device, C.byref(h)))
+    return h
+
+
+def gut_context_destroy(ctx):
+    lib().gut_context_destroy(ctx)
+
+
+def gut_workspace_reserve(ctx, max_keys: int, max_gaussians: int, max_w: int, max_h: int):
+    _check(lib().gut_workspace_reserve(ctx, int(max_keys), int(max_gaussians), int(max_w), int(max_h)), ctx)
+
+
+def gut_scene_create(ctx, means, rotations, scales, opacities, sh, sh_degree: int, stream=None):
+    """Arrays are torch CUDA tensors (on_device) or numpy float32 arrays (host)."""
+    g = gut_gaussians()
+    g.struct_size = C.sizeof(gut_gaussians)
+    g.sh_degree = int(sh_degree)
+    g.count = int(means.shape[0])
+    import numpy as np
+    if isinstance(means, np.ndarray):
+        arrs = [np.ascontiguousarray(a, np.float32) for a in (means, rotations, scales, opacities, sh)]
+        g.on_device = 0
+        ptrs = [a.ctypes.data for a in arrs]
+        keep = arrs
+    else:
+        arrs = [a.contiguous().float() for a in (means, rotations, scales, opacities, sh)]
+        g.on_device = 1
+        ptrs = [a.data_ptr() for a in arrs]
+        keep = arrs
+    g.means, g.rotations, g.scales, g.opacities, g.sh = ptrs
+    h = C.c_void_p()
+    _check(lib().gut_scene_create(ctx, C.byref(g), _stream_ptr(stream), C.byref(h)), ctx)
+    del keep
+    return h
+
+
+def gut_scene_destroy(ctx, scene):
+    lib().gut_scene_destroy(ctx, scene)
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except Exception:
+            pass
+        return None
+    return C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
+
+
+def gut_render(ctx, scene, cam: gut_camera, opt: gut_options, out: gut_outputs, stream=None, stats=True):
+    st = gut_stats() if stats else None
+    _check(lib().gut_render(ctx, scene, C.byref(cam), C.byref(opt), C.byref(out), _stream_ptr(stream),
+                            C.byref(st) if st is not None else None), ctx)
+    return st
+
+
+def gut_render_batch(ctx, scene, cams: Sequence[gut_camera], opt: gut_options, outs: Sequence[gut_outputs],
+                     stream=None, stats=False):
+    n = len(cams)
+    carr = (gut_camera * n)(*cams)
+    oarr = (gut_outputs * n)(*outs)
+    st = (gut_stats * n)() if stats else None
+    _check(lib().gut_render_batch(ctx, scene, carr, n, C.byref(opt), oarr, _stream_ptr(stream), st), ctx)
+    return st
+
+
+def gut_debug_copy_stage(ctx, stage: int):
+    import numpy as np
+    need = C.c_size_t(0)
+    _check(lib().gut_debug_copy_stage(ctx, stage, None, 0, C.byref(need)), ctx)
+    buf = (C.c_ubyte * max(int(need.value), 1))()
+    _check(lib().gut_debug_copy_stage(ctx, stage, buf, need.value, C.byref(need)), ctx)
+    raw = bytes(buf)[: need.value]
+    if stage == STAGE_PROJECT:
+        dt = np.dtype([("vx", "<f4"), ("vy", "<f4"), ("cxx", "<f4"), ("cxy", "<f4"), ("cyy", "<f4"), ("k2", "<f4"),
+                       ("depth", "<f4"), ("rgb", "<f4", 3), ("tiles", "<u4"), ("rect", "<u2", 4)])
+        assert dt.itemsize == C.sizeof(gut_proj_record)
+        return np.frombuffer(raw, dt).copy()
+    arr = np.frombuffer(raw, np.uint32).copy()
+    if stage in (STAGE_SORTED, STAGE_RANGES):
+        arr = arr.reshape(-1, 2)
+    return arr
+
+
+# ------------------------------------------------------------- convenience
+class Renderer:
+    """Context + resident scene.  render() returns torch tensors (device)."""
+
+    def __init__(self, scene, device: int = 0, reserve_keys: Optional[int] = None, max_wh=(1920, 1280)):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.ctx = gut_context_create(device)
+        if reserve_keys:
+            gut_workspace_reserve(self.ctx, reserve_keys, scene.count, max_wh[0], max_wh[1])
+        self.scene = gut_scene_create(self.ctx, scene.means, scene.rotations, scene.scales, scene.opacities,
+                                      scene.sh, scene.sh_degree)
+        torch.cuda.synchronize(device)
+
+    def render(self, cam, opt=None, timing=False, stats=True, out=None):
+        torch = self.torch
+        H, W = cam.height, cam.width
+        if out is None:
+            dev = torch.device("cuda", self.device)
+            out = (torch.empty((H, W, 3), device=dev), torch.empty((H, W), device=dev),
+                   torch.empty((H, W), device=dev))
+        o = gut_outputs(out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr() if out[2] is not None else None, 1, 0)
+        st = gut_render(self.ctx, self.scene, make_camera(cam), make_options(opt, timing), o, stats=stats)
+        return out[0], out[1], out[2], st
+
+    def stage(self, stage):
+        return gut_debug_copy_stage(self.ctx, stage)
+
+    def close(self):
+        if self.ctx:
+            gut_scene_destroy(self.ctx, self.scene)
+            gut_context_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,246 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the fp64 oracle on
+the same seeded inputs.  Stage by stage (K1 projection, K2/K3/K4 binning,
+sort and ranges, K5 blend on the GPU's own lists) and end to end, on the
+tiny config and its camera variants (ragged edges: 64x64 -> 4x4 tiles; 70x50
+-> partial tiles), on reduced-N / reduced-resolution versions of the large
+configs (several tiles, ragged tails), and at full size on sampled tiles."""
+import dataclasses
+import math
+
+import numpy as np
+import pytest
+
+import scenegen as S
+from gpu_common import (TOL_DEPTH_REL, TOL_RGB, assert_images_close, gpu_lists, gpu_render, pixel_mask)
+
+pytestmark = pytest.mark.gpu
+
+OPT = S.RenderOptions()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2412_12507_b200 import build
+    build.build()
+
+
+def _proj_parity(scene, cam, g, o_proj, opt=OPT):
+    gp = g["proj"]
+    vis_g = gp["tiles"] > 0
+    vis_o = o_proj["reason"] == 0
+    amb = (o_proj["cull_ambig"] != 0) | (o_proj["bin_ambig"] != 0)
+    # culling identical outside the ambiguity set
+    bad = (vis_g != vis_o) & ~amb
+    assert not bad.any(), np.nonzero(bad)[0][:10]
+    both = vis_g & vis_o & ~amb
+    # tile counts bit-exact outside the 1e-3 px band
+    np.testing.assert_array_equal(gp["tiles"][both], o_proj["tiles"][both])
+    # mean within 1e-3 px, covariance within 1e-4 relative, depth, colour
+    assert np.abs(gp["vx"][both] - o_proj["vx"][both]).max(initial=0) < 1e-3
+    assert np.abs(gp["vy"][both] - o_proj["vy"][both]).max(initial=0) < 1e-3
+    for f in ("cxx", "cyy"):
+        rel = np.abs(gp[f][both] - o_proj[f][both]) / np.abs(o_proj[f][both])
+        assert rel.max(initial=0) < 1e-4, f
+    sc = np.sqrt(o_proj["cxx"][both] * o_proj["cyy"][both])
+    assert (np.abs(gp["cxy"][both] - o_proj["cxy"][both]) / sc).max(initial=0) < 1e-4
+    rel = np.abs(gp["depth"][both] - o_proj["depth"][both]) / o_proj["depth"][both]
+    assert rel.max(initial=0) < 2e-6
+    assert np.abs(gp["rgb"][both] - o_proj["rgb"][both]).max(initial=0) < 1e-5
+    np.testing.assert_array_equal(gp["rect"][both].astype(np.int32), o_proj["rect"][both])
+    return int(both.sum()), int(amb.sum())
+
+
+def _sort_parity(scene, cam, g):
+    """K2-K4 on the GPU's own K1 output: the sorted pairs are exactly the pairs
+    implied by the GPU tile counts, ordered by (tile, fp32 depth, index)."""
+    gp = g["proj"]
+    pairs = g["sorted"]
+    K = pairs.shape[0]
+    assert K == int(gp["tiles"].sum()) == g["stats"]["n_keys"]
+    tiles, gids = pairs[:, 0].astype(np.int64), pairs[:, 1].astype(np.int64)
+    depth = gp["depth"][gids]
+    order = np.lexsort((gids, depth, tiles))
+    assert np.array_equal(order, np.arange(K)), "not sorted by (tile, depth, gid)"
+    np.testing.assert_array_equal(np.bincount(gids, minlength=scene.count), gp["tiles"])
+    assert len(set(zip(tiles.tolist(), gids.tolist()))) == K
+    # each Gaussian's tiles lie in its rectangle
+    r = gp["rect"][gids].astype(np.int64)
+    tx, ty = tiles % cam.tiles[0], tiles // cam.tiles[0]
+    assert np.all((tx >= r[:, 0]) & (tx <= r[:, 2]) & (ty >= r[:, 1]) & (ty <= r[:, 3]))
+    # ranges
+    ranges = g["ranges"]
+    for t in range(ranges.shape[0]):
+        a, b = ranges[t]
+        assert np.all(tiles[a:b] == t)
+        assert (b - a) == int((tiles == t).sum())
+    # depth order of the visible Gaussians
+    vis = np.nonzero(gp["tiles"] > 0)[0]
+    exp = vis[np.lexsort((vis, gp["depth"][vis]))]
+    np.testing.assert_array_equal(g["order"], exp)
+
+
+def _tile_sets_match_oracle(g, o_proj, cam, opt):
+    """For non-ambiguous Gaussians the GPU's (tile, gid) set equals the oracle's."""
+    from oracle import oracle as O
+    tiles_o, gids_o, _ = O.tile_lists(o_proj, cam, opt)
+    amb = (o_proj["cull_ambig"] != 0) | (o_proj["bin_ambig"] != 0)
+    so = set((int(t), int(i)) for t, i in zip(tiles_o, gids_o) if not amb[i])
+    sg = set((int(t), int(i)) for t, i in g["sorted"] if not amb[i])
+    assert so == sg, (len(so - sg), len(sg - so))
+
+
+def _blend_parity(scene, cam, g, opt=OPT):
+    """K5 isolated: oracle O6 on the GPU's own sorted lists."""
+    from oracle import oracle as O
+    proj = O.preprocess(scene, cam, opt)
+    gids, ranges = gpu_lists(g, cam.tiles[0] * cam.tiles[1])
+    rgb, alpha, depth, diag = O.composite(scene, proj, gids, ranges, cam, opt)
+    o = dict(rgb=rgb, alpha=alpha, depth=depth)
+    m = (diag["min_alpha_gap"] > 1e-5) & (diag["min_term_gap"] > 2e-8)
+    return assert_images_close(g, o, m, f"blend {cam.model}/{cam.shutter}", max_excluded=0.01)
+
+
+def _full_parity(scene, cam, opt=OPT, max_excluded=0.01, label=""):
+    from oracle import oracle as O
+    g = gpu_render(scene, cam, opt)
+    o = O.render(scene, cam, opt)
+    _proj_parity(scene, cam, g, o["proj"], opt)
+    _sort_parity(scene, cam, g)
+    _tile_sets_match_oracle(g, o["proj"], cam, opt)
+    _blend_parity(scene, cam, g, opt)
+    res = assert_images_close(g, o, pixel_mask(o["diag"]), label or f"e2e {cam.model}/{cam.shutter}",
+                              max_excluded=max_excluded)
+    # invariants on the GPU output
+    T = 1 - g["alpha"]
+    assert np.all(np.isfinite(g["rgb"])) and np.all(np.isfinite(g["depth"]))
+    assert np.all(T >= 0) and np.all(T <= 1) and np.all(g["alpha"] <= 1 - opt.transmittance_min + 1e-6)
+    return g, o, res
+
+
+@pytest.mark.parametrize("variant", S.TINY_VARIANTS)
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_tiny_parity(variant, seed):
+    scene, cam = S.tiny(seed, variant)
+    _full_parity(scene, cam)
+
+
+@pytest.mark.parametrize("variant", ["pinhole", "fisheye", "rs"])
+def test_tiny_ragged_and_sh3(variant):
+    """70x50 image (partial tiles on both edges), 200 Gaussians, SH degree 3."""
+    scene, cam = S.tiny(7, variant, n=200, size=64, sh_degree=3)
+    cam = dataclasses.replace(cam, width=70, height=50, cx=35.0, cy=25.0)
+    _full_parity(scene, cam)
+
+
+def test_tiny_aabb_mode():
+    scene, cam = S.tiny(5, "pinhole", n=128)
+    _full_parity(scene, cam, S.RenderOptions(tile_cull=0))
+
+
+def test_nondefault_ut_params_and_background():
+    scene, cam = S.tiny(6, "opencv", n=128)
+    opt = S.RenderOptions(ut_alpha=0.8, ut_beta=1.0, ut_kappa=1.0, background=(0.2, 0.4, 0.6))
+    _full_parity(scene, cam, opt)
+
+
+@pytest.mark.parametrize("config,n,factor,view", [
+    ("mipnerf360", 60_000, 0.25, 0),
+    ("scannetpp", 40_000, 0.2, 3),
+    ("waymo", 80_000, 0.15, 1),
+    ("multiview", 100_000, 0.2, 5),
+])
+def test_reduced_configs(config, n, factor, view):
+    """The large configs' recipes at reduced N and resolution (seconds for the
+    oracle), spanning tens of tiles with ragged edges."""
+    scene = S.make_scene(config, n=n)
+    cam = S.scaled_camera(S.make_views(config)[view], factor)
+    g, o, _ = _full_parity(scene, cam, max_excluded=0.02, label=f"{config} n={n} x{factor}")
+    assert g["stats"]["n_keys"] > 0
+
+
+def test_full_size_sampled_tiles():
+    """BASELINE configs[4] (3M Gaussians, 1920x1080 fisheye) in the launch
+    configuration bench.py times: sampled tiles against the oracle."""
+    from oracle import oracle as O
+    scene = S.make_scene("multiview")
+    cam = S.make_views("multiview")[0]
+    g = gpu_render(scene, cam, reserve=int(scene.count * 12))
+    tx, ty = cam.tiles
+    rng = np.random.default_rng(0)
+    sub = np.sort(rng.choice(tx * ty, 24, replace=False)).astype(np.int32)
+    o = O.render(scene, cam, OPT, tile_subset=sub)
+    mask = np.zeros((cam.height, cam.width), bool)
+    for t in sub:
+        x0, y0 = (t % tx) * 16, (t // tx) * 16
+        mask[y0:y0 + 16, x0:x0 + 16] = True
+    mask &= pixel_mask(o["diag"])
+    assert mask.sum() > 0.9 * 24 * 256 * 0.9
+    e_rgb = np.abs(g["rgb"] - o["rgb"]).max(-1)[mask].max()
+    e_a = np.abs(g["alpha"] - o["alpha"])[mask].max()
+    print(f"full-size sampled: rgb {e_rgb:.2e} alpha {e_a:.2e}; K={g['stats']['n_keys']}")
+    assert e_rgb <= TOL_RGB and e_a <= TOL_RGB
+    _proj_parity(scene, cam, g, o["proj"])
+
+
+def test_edge_cases():
+    """Empty scene, all-culled scene, a single Gaussian, Gaussians behind the camera."""
+    scene, cam = S.tiny(0, "pinhole", n=8)
+    empty = scene.subset(np.zeros(0, np.int64))
+    g = gpu_render(empty, cam)
+    assert np.all(g["alpha"] == 0) and g["stats"]["n_keys"] == 0
+    behind = scene.subset(np.arange(8))
+    behind.means[:, 2] = -3.0
+    g = gpu_render(behind, cam)
+    assert np.all(g["alpha"] == 0) and g["stats"]["n_visible"] == 0
+    bad = scene.subset(np.arange(8))
+    bad.scales[0] = 0.0
+    bad.rotations[1] = 0.0
+    bad.opacities[2] = 0.0
+    bad.means[3, 0] = np.nan
+    _full_parity(bad, cam)
+    one = scene.subset(np.arange(1))
+    _full_parity(one, cam)
+
+
+def test_determinism_and_modes():
+    """Bitwise-identical re-runs; capacity mode == sync mode; host outputs ==
+    device outputs."""
+    import torch
+    from paper_2412_12507_b200 import gut
+    scene = S.make_scene("multiview", n=50_000)
+    cam = S.scaled_camera(S.make_views("multiview")[2], 0.3)
+    a = gpu_render(scene, cam)
+    b = gpu_render(scene, cam)
+    c = gpu_render(scene, cam, reserve=2_000_000)
+    for k in ("rgb", "alpha", "depth"):
+        assert np.array_equal(a[k], b[k]) and np.array_equal(a[k], c[k])
+    assert np.array_equal(a["sorted"], c["sorted"])
+    r = gut.Renderer(scene)
+    H, W = cam.height, cam.width
+    hr = torch.empty((H, W, 3), pin_memory=True)
+    ha = torch.empty((H, W), pin_memory=True)
+    hd = torch.empty((H, W), pin_memory=True)
+    o = gut.gut_outputs(hr.data_ptr(), ha.data_ptr(), hd.data_ptr(), 0, 0)
+    gut.gut_render(r.ctx, r.scene, gut.make_camera(cam), gut.make_options(), o)
+    torch.cuda.synchronize()
+    assert np.array_equal(hr.numpy(), a["rgb"]) and np.array_equal(ha.numpy(), a["alpha"])
+    r.close()
+
+
+def test_invalid_arguments():
+    from paper_2412_12507_b200 import gut
+    scene, cam = S.tiny(0)
+    r = gut.Renderer(scene)
+    bad = dataclasses.replace(cam, model="fisheye", fov_limit=0.0)
+    with pytest.raises(gut.GutError) as e:
+        r.render(bad)
+    assert e.value.status == 1 and "fov_limit" in str(e.value)
+    with pytest.raises(gut.GutError):
+        r.render(cam, S.RenderOptions(ut_alpha=0.0))
+    with pytest.raises(gut.GutError) as e:
+        r.render(dataclasses.replace(cam, model="ortho", shutter="top_to_bottom"))
+    assert e.value.status == 2
+    r.close()
