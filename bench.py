@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the B200-native 3DGUT forward rasterizer.
+
+Workload (BASELINE.json configs[4], the config its metric is quoted on):
+3M Gaussians (SH degree 3, MipNeRF360-like "garden" recipe), equidistant
+fisheye 1920x1080 (f = 620, theta_max = 105 deg), 256 views on a spiral.
+A step = one full pass of the hot path (K1 UT projection, K3 depth passes,
+K2 emission, K3 tile passes, K4 ranges, K5 blend) for one view on every rank;
+rank r renders view (s * N + r) mod 256 at step s (weak scaling in views).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  value = frames/s over all ranks with the
+scene resident in HBM (device-timed with CUDA events, max over ranks);
+e2e = the same metric through the C ABI with HOST output buffers (device->host
+copy of RGB/alpha/depth inside the timed region, camera struct in by value).
+--impl reference times the fp64 CPU oracle (the paper's algorithm written out)
+on the box's host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/sec & Mpix/s at 1080p, 3M Gaussians (fisheye) at 1/2/4/8 B200; ms/stage"
+CONFIG = "multiview"
+WORKLOAD = ("multiview: 3,000,000 Gaussians SH3 (garden recipe, s_med 0.007), equidistant fisheye 1920x1080 "
+            "f=620 theta_max=105deg, 256-view spiral (BASELINE.json configs[4])")
+PEAK_FP32_NOTE = "148 SMs x 128 FP32 lanes x 2 FLOP/FMA x 1.965 GHz (B200_PROFILING.md unit counts, max clock)"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-tiles", type=int, default=512, help="tiles in the oracle's bounded sample")
+    p.add_argument("--n", type=int, default=None, help="override N (debug only; the default is the config)")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 100 ms during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.count(",") >= 9]
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        util = [float(r[9]) if r[9].strip().replace(".", "").isdigit() else 0.0 for r in rows]
+        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, name in enumerate(names):
+                if "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- roofline
+def algorithmic_work(n, nv, k, tiles, pixels, pe, pc, sh_chunks=12):
+    """Algorithmic bytes / FLOPs per launch of each kernel.
+    n: Gaussians, nv: visible, k: keys, pe/pc: evaluated / contributing pairs."""
+    return {
+        "K1_project": ("hbm", 48 * n + 8 * n + nv * (16 * sh_chunks + 32 + 64)),
+        "K3_sort_depth": ("hbm", 4 * n + 8 * nv + 3 * 16 * nv - 4 * nv),
+        "K2_emit": ("hbm", 4 * nv + 4 * nv + 32 * nv + 8 * k),
+        "K3_sort_tile": ("hbm", (32 if tiles > 256 else 16) * k),
+        "K4_ranges": ("hbm", 4 * k + 8 * tiles),
+        # FP32 work of Eq. 11 in the anchored form: 36 FLOP to the reject test per
+        # evaluated pair (n: 12, e: 12, |n|^2: 5, |e|^2: 5, k^2|e|^2: 1, compare: 1)
+        # + 30 FLOP per contributing pair (rcp, omega^2, ex2 argument, clamp,
+        # tau: 5, blend: 4 x 2 + transmittance: 2, ...)
+        "K5_blend": ("alu", 36 * pe + 30 * pc),
+    }
+
+
+def roofline(stage_ms, work, peaks, clocks):
+    out = {}
+    for name, (bound, amount) in work.items():
+        ms = stage_ms.get(name)
+        if not ms:
+            continue
+        if bound == "hbm":
+            ach = amount / (ms * 1e-3) / 1e9
+            peak = peaks["hbm_gbs"]
+            out[name] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "ms": ms, "algorithmic": amount}
+        else:
+            ach = amount / (ms * 1e-3) / 1e12
+            peak = peaks["fp32_tflops"]
+            out[name] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                         "ms": ms, "algorithmic": amount}
+    return out
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = {"hbm_gbs": 6650.0, "hbm_source": "fallback (B200_PROFILING.md)"}
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if d.get("hbm_gbs"):
+            peaks = {"hbm_gbs": float(d["hbm_gbs"]), "hbm_source": "measured (MEASURED_PEAKS.json)"}
+    peaks["fp32_tflops"] = 148 * 128 * 2 * 1.965e9 / 1e12
+    peaks["fp32_source"] = PEAK_FP32_NOTE
+    return peaks
+
+
+# ---------------------------------------------------------------- CPU oracle
+def oracle_frame_seconds(scene, cam, opt, n_tiles_sample, seed=0):
+    """The fp64 oracle as it stands, on the box's host cores: full O1-O4 for
+    the view, O5-O6 on a random sample of tiles, extrapolated to the frame."""
+    import numpy as np
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    proj = O.preprocess(scene, cam, opt)
+    t1 = time.perf_counter()
+    tiles, gids, ranges = O.tile_lists(proj, cam, opt)
+    t2 = time.perf_counter()
+    tx, ty = cam.tiles
+    T = tx * ty
+    rng = np.random.default_rng(seed)
+    sub = np.sort(rng.choice(T, min(n_tiles_sample, T), replace=False)).astype(np.int32)
+    O.composite(scene, proj, gids, ranges, cam, opt, tile_subset=sub)
+    t3 = time.perf_counter()
+    frame = (t1 - t0) + (t2 - t1) + (t3 - t2) * T / len(sub)
+    return frame, {"preprocess_s": t1 - t0, "lists_s": t2 - t1, "composite_sample_s": t3 - t2,
+                   "tiles_sampled": int(len(sub)), "tiles_total": T, "K": int(gids.size)}
+
+
+def run_reference(args):
+    """--impl reference: the oracle arm (rank 0 only; other ranks exit 0)."""
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if rank != 0:
+        return
+    import scenegen as S
+    from oracle import oracle as O
+    scene = S.make_scene(CONFIG, n=args.n)
+    views = S.make_views(CONFIG)
+    opt = S.RenderOptions()
+    cores = O.threads()
+    for s in range(args.warmup):
+        oracle_frame_seconds(scene, views[s % len(views)], opt, args.cpu_tiles, seed=s)
+    tot = 0.0
+    detail = None
+    for s in range(args.steps):
+        f, detail = oracle_frame_seconds(scene, views[(args.warmup + s) % len(views)], opt, args.cpu_tiles, seed=s)
+        tot += f
+    fps = args.steps / tot
+    sample = (f"per step: one view, O1-O4 over all {scene.count} Gaussians + O5-O6 on {detail['tiles_sampled']} "
+              f"of {detail['tiles_total']} tiles, extrapolated to the full frame")
+    line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "oracle": "oracle/gut_oracle.c (fp64, OpenMP)"},
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "detail": detail}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- ours
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import scenegen as S
+    from paper_2412_12507_b200 import gut
+    from paper_2412_12507_b200 import parallel as P
+
+    rank, local, world = P.init("nccl")
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    N, deg = S.CONFIGS[CONFIG][0], S.CONFIGS[CONFIG][1]
+    if args.n:
+        N = args.n
+    nc = (deg + 1) ** 2
+    # scene: generated on rank 0 (seeded recipe), broadcast once over NCCL
+    t_b0 = time.perf_counter()
+    if rank == 0:
+        sc = S.make_scene(CONFIG, n=N)
+        arrs = {"means": sc.means, "rotations": sc.rotations, "scales": sc.scales, "opacities": sc.opacities,
+                "sh": sc.sh}
+        ten = {k: torch.from_numpy(v).to(dev) for k, v in arrs.items()}
+    else:
+        shapes = {"means": (N, 3), "rotations": (N, 4), "scales": (N, 3), "opacities": (N,), "sh": (N, nc, 3)}
+        ten = {k: torch.empty(s, dtype=torch.float32, device=dev) for k, s in shapes.items()}
+    torch.cuda.synchronize()
+    t_b1 = time.perf_counter()
+    P.broadcast_scene(ten)
+    torch.cuda.synchronize()
+    t_b2 = time.perf_counter()
+    views = S.make_views(CONFIG)
+    nv = len(views)
+    opt = S.RenderOptions()
+    ctx = gut.gut_context_create(local)
+    scene = gut.gut_scene_create(ctx, ten["means"], ten["rotations"], ten["scales"], ten["opacities"], ten["sh"],
+                                 deg)
+    torch.cuda.synchronize()
+    cams = [gut.make_camera(v) for v in views]
+    gopt = gut.make_options(opt, timing=False)
+    topt = gut.make_options(opt, timing=True)
+    W, H = views[0].width, views[0].height
+    npix = W * H
+    rgb = torch.empty((H, W, 3), device=dev)
+    alpha = torch.empty((H, W), device=dev)
+    depth = torch.empty((H, W), device=dev)
+    out_dev = gut.gut_outputs(rgb.data_ptr(), alpha.data_ptr(), depth.data_ptr(), 1, 0)
+    stream = torch.cuda.current_stream()
+    e2e_steps = args.e2e_steps or max(3, args.steps // 2)
+    # sizing pass (sync mode, with stats): key count of every view this rank will render
+    used = sorted(set(P.views_of_rank(args.warmup + args.steps + 2 + e2e_steps, rank, world, nv)))
+    per_view = {}
+    for v in used:
+        st = gut.gut_render(ctx, scene, cams[v], gopt, out_dev, stream=stream, stats=True)
+        per_view[v] = st.as_dict()
+    kmax = max(d["n_keys"] for d in per_view.values())
+    gut.gut_workspace_reserve(ctx, int(kmax * 1.02) + 65536, N, W, H)
+    # warm-up (capacity mode: fully asynchronous)
+    for s in range(args.warmup):
+        gut.gut_render(ctx, scene, cams[P.view_of(s, rank, world, nv)], gopt, out_dev, stream=stream, stats=False)
+    gut.gut_timing_read(ctx, reset=True)
+    torch.cuda.synchronize()
+    P.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    timed_views = [P.view_of(args.warmup + s, rank, world, nv) for s in range(args.steps)]
+    ev0.record(stream)
+    for v in timed_views:
+        gut.gut_render(ctx, scene, cams[v], topt, out_dev, stream=stream, stats=False)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    P.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    ms_max = P.max_over_ranks(ms, device=dev)
+    stage_sum, n_timed = gut.gut_timing_read(ctx, reset=True)
+    stage_ms = {k: v / max(n_timed, 1) for k, v in stage_sum.items()}
+    # e2e: host (pinned) outputs through the same C-ABI call; D2H inside the timed region
+    hr = torch.empty((H, W, 3), pin_memory=True)
+    ha = torch.empty((H, W), pin_memory=True)
+    hd = torch.empty((H, W), pin_memory=True)
+    out_host = gut.gut_outputs(hr.data_ptr(), ha.data_ptr(), hd.data_ptr(), 0, 0)
+    e2e_first = args.warmup + args.steps
+    for s in range(2):
+        gut.gut_render(ctx, scene, cams[P.view_of(e2e_first + s, rank, world, nv)], gopt, out_host, stream=stream,
+                       stats=False)
+    torch.cuda.synchronize()
+    P.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(e2e_steps):
+        v = P.view_of(e2e_first + 2 + s, rank, world, nv)
+        gut.gut_render(ctx, scene, cams[v], gopt, out_host, stream=stream, stats=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = P.max_over_ranks(e0.elapsed_time(e1), device=dev)
+    # per-view statistics of the timed views (deterministic renders) gathered to rank 0
+    rows = [[v, per_view[v]["n_visible"], per_view[v]["n_keys"], per_view[v]["pairs_evaluated"],
+             per_view[v]["pairs_contributing"], per_view[v]["max_tile_len"]] for v in timed_views]
+    all_rows = P.gather_stats(rows, device=dev)
+    overflow = any(per_view[v]["n_keys"] > int(kmax * 1.02) + 65536 for v in timed_views)
+    gut.gut_scene_destroy(ctx, scene)
+    gut.gut_context_destroy(ctx)
+    if rank != 0:
+        return
+    a = np.array(all_rows, dtype=np.float64)
+    mean_nv, mean_k, mean_pe, mean_pc = (float(a[:, i].mean()) for i in (1, 2, 3, 4))
+    n_tiles = views[0].tiles[0] * views[0].tiles[1]
+    peaks = load_peaks()
+    work = algorithmic_work(N, mean_nv, mean_k, n_tiles, npix, mean_pe, mean_pc)
+    rl = roofline(stage_ms, work, peaks, clk)
+    dom = max(rl, key=lambda k: rl[k]["ms"])
+    d = rl[dom]
+    launches_per_render = 1 + 4 + 1 + (2 if n_tiles > 256 else 1) + 1 + 1
+    total_views = world * args.steps
+    fps = total_views / (ms_max * 1e-3)
+    line = {
+        "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "views_per_step": world, "parallelism": f"views sharded over {world} GPU(s), "
+                   "scene replicated", "l2": "inputs larger than L2 (720 MB resident scene; 41 MB output/view)",
+                   "capacity_mode": True, "reserved_keys": int(kmax * 1.02) + 65536},
+        "mpix_per_s": fps * npix / 1e6,
+        "ms_stage": stage_ms,
+        "clocks": clk,
+        "e2e": {"value": world * e2e_steps / (e2e_ms * 1e-3), "unit": "frames/s", "h2d_bytes_per_step": 240,
+                "d2h_bytes_per_step": npix * 5 * 4,
+                "what": "gut_render with host (pinned) output buffers: RGB+alpha+depth copied device->host each "
+                        "step; camera struct (240 B) passed by value; scene resident (uploaded once)"},
+        "gpu_launches": launches_per_render * args.steps,
+        "roofline": {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
+                     "unit": d["unit"], "frac": d["frac"], "traffic": None,
+                     "peak_source": peaks["hbm_source"] if d["bound"] == "hbm" else peaks["fp32_source"]},
+        "roofline_all": rl,
+        "workload_stats": {"n": N, "n_visible_mean": mean_nv, "keys_mean": mean_k, "kappa": mean_k / max(mean_nv, 1),
+                           "pairs_evaluated_per_px": mean_pe / npix, "pairs_contributing_per_px": mean_pc / npix,
+                           "max_tile_len": float(a[:, 5].max()), "overflow": overflow},
+        "scene_broadcast_s": t_b2 - t_b1, "scene_generate_s": t_b1 - t_b0,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import oracle as O
+            f, det = oracle_frame_seconds(sc, views[0], opt, args.cpu_tiles)
+            line["cpu_baseline"] = {"value": 1.0 / f, "unit": "frames/s", "cores": O.threads(), "kind": "oracle",
+                                    "sample": f"view 0: O1-O4 over all {N} Gaussians + O5-O6 on "
+                                              f"{det['tiles_sampled']}/{det['tiles_total']} tiles, extrapolated "
+                                              f"to the frame ({det})"}
+        except Exception as e:  # reported, never fatal for the GPU number
+            line["cpu_baseline"] = {"value": None, "unit": "frames/s", "cores": None, "kind": "oracle",
+                                    "sample": f"failed: {e}"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+    try:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
+
+
+if __name__ == "__main__":
+    main()

@@ -138,7 +138,8 @@ typedef struct {
   int64_t pairs_evaluated;   /* (pixel, list entry) evaluations in the blend */
   int64_t pairs_contributing;
   int64_t pixels_terminated;
-  float ms_stage[6];         /* project, sort-depth, emit, sort-tile, ranges+blend, total (timing=1) */
+  float ms_stage[7];         /* K1 project, K3 depth passes, K2 emit, K3 tile passes, K4 ranges,
+                                K5 blend, total (timing = 1 only) */
   int32_t overflow;          /* 1 if the reserved key capacity was exceeded */
   int32_t pad0;
 } gut_stats;
@@ -191,6 +192,13 @@ gut_status gut_render(gut_context *ctx, const gut_scene *scene, const gut_camera
 gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_camera *cams,
                             int32_t n_views, const gut_options *opt, const gut_outputs *outs,
                             gut_stream s, gut_stats *stats);
+
+/* Per-stage device times of every render issued with options.timing = 1 since
+ * the last reset: CUDA events recorded on the render's stream between the
+ * stages.  Synchronises.  ms_sum[7] receives the summed milliseconds per stage
+ * (order of gut_stats.ms_stage), *n_renders the number of renders summed;
+ * reset != 0 clears the accumulator. */
+gut_status gut_timing_read(gut_context *ctx, double ms_sum[7], int32_t *n_renders, int32_t reset);
 
 /* Tests only: copies an intermediate buffer of the LAST render on ctx to host
  * memory (synchronises).  *bytes_needed receives the size; if host_dst is

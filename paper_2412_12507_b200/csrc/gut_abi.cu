@@ -10,7 +10,9 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <array>
 #include <string>
+#include <vector>
 
 #include "../../include/gut.h"
 #include "launch.h"
@@ -37,7 +39,8 @@ struct gut_context {
   uint32_t *counters = nullptr, *h_counters = nullptr;
   uint32_t epoch = 0;
   bool reserved = false;
-  cudaEvent_t ev[7] = {};
+  std::vector<std::array<cudaEvent_t, 7>> tsets;  // per-render stage events (timing = 1)
+  size_t tnext = 0;
   // last render (for gut_debug_copy_stage)
   int64_t last_n = 0;
   int last_tiles = 0;
@@ -257,7 +260,6 @@ gut_status gut_context_create(int32_t dev, gut_context **out) {
     delete ctx;
     return fail(nullptr, GUT_E_OUT_OF_MEMORY, "counters");
   }
-  for (auto &e : ctx->ev) cudaEventCreate(&e);
   *out = ctx;
   return GUT_OK;
 }
@@ -270,7 +272,8 @@ void gut_context_destroy(gut_context *ctx) {
                 ctx->st_tile, ctx->counters};
   for (void *p : ps) if (p) cudaFree(p);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
-  for (auto &e : ctx->ev) if (e) cudaEventDestroy(e);
+  for (auto &set : ctx->tsets)
+    for (auto &e : set) cudaEventDestroy(e);
   delete ctx;
 }
 
@@ -379,13 +382,22 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   if (!out->on_device && (s = ensure_pix(ctx, npix)) != GUT_OK) return s;
   if (!ctx->ka && (s = ensure_k(ctx, (size_t)N * 4 + 1024)) != GUT_OK) return s;
   const bool timing = opt->timing != 0;
-  if (timing) cudaEventRecord(ctx->ev[0], st);
+  cudaEvent_t *ev = nullptr;
+  if (timing) {
+    if (ctx->tnext == ctx->tsets.size()) {
+      std::array<cudaEvent_t, 7> set;
+      for (auto &e : set) CUDA_TRY(ctx, cudaEventCreate(&e));
+      ctx->tsets.push_back(set);
+    }
+    ev = ctx->tsets[ctx->tnext++].data();
+    cudaEventRecord(ev[0], st);
+  }
 
   uint32_t *cnt = ctx->counters;
   CUDA_TRY(ctx, cudaMemsetAsync(cnt, 0, CNT_WORDS * sizeof(uint32_t), st));
   // K1: UT projection
   launch_project(dc, scene->d, ctx->dkey, ctx->tiles, ctx->ell, ctx->payload, cnt, st);
-  if (timing) cudaEventRecord(ctx->ev[1], st);
+  if (timing) cudaEventRecord(ev[1], st);
   // K3 level 1: depth sort of the visible Gaussians (4 LSD passes, first one compacts)
   const uint32_t n32 = (uint32_t)N;
   const uint32_t *hd = cnt + CNT_HIST_DEPTH;
@@ -398,7 +410,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   launch_sort_pass(ctx->sa_k, ctx->sa_v, nullptr, ctx->sb_v, cnt + CNT_NVIS, n32, 24, hd + 768, ctx->st_depth,
                    cnt + CNT_TICKETS + 3, ++ctx->epoch, false, st);
   const uint32_t *order = ctx->sb_v;
-  if (timing) cudaEventRecord(ctx->ev[2], st);
+  if (timing) cudaEventRecord(ev[2], st);
   // key count: capacity mode keeps the stream asynchronous; otherwise read K back
   size_t n_keys_host;
   if (ctx->reserved) {
@@ -414,7 +426,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   // K2: depth-ordered scan + emission of (tile, gid) keys
   launch_emit(order, cnt + CNT_NVIS, n32, ctx->tiles, ctx->ell, dc.tiles_x, dc.tile_cull, ctx->ka, ctx->va,
               (uint32_t)ctx->cap_k, cnt, ctx->st_emit, ++ctx->epoch, st);
-  if (timing) cudaEventRecord(ctx->ev[3], st);
+  if (timing) cudaEventRecord(ev[3], st);
   // K3 level 2: stable tile passes
   const uint32_t *ht = cnt + CNT_HIST_TILE;
   const uint32_t *kdev = cnt + CNT_K;  // low word of the u64 key count (K < 2^30)
@@ -428,10 +440,11 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
                      cnt + CNT_TICKETS + 6, ++ctx->epoch, false, st);
     fk = ctx->ka; fv = ctx->va;
   }
-  if (timing) cudaEventRecord(ctx->ev[4], st);
+  if (timing) cudaEventRecord(ev[4], st);
   // K4 ranges, K5 blend
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->ranges, 0, (size_t)dc.n_tiles * sizeof(uint2), st));
   launch_ranges(fk, cnt, (uint32_t)ctx->cap_k, ctx->ranges, st);
+  if (timing) cudaEventRecord(ev[5], st);
   float *rgb = out->rgb, *alpha = out->alpha, *depth = out->depth;
   if (!out->on_device) {
     rgb = ctx->img;
@@ -439,7 +452,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
     depth = out->depth ? ctx->img + 4 * npix : nullptr;
   }
   launch_blend(dc, ctx->ranges, fv, ctx->payload, rgb, alpha, depth, cnt, st);
-  if (timing) cudaEventRecord(ctx->ev[5], st);
+  if (timing) cudaEventRecord(ev[6], st);
   {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(ctx, GUT_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
@@ -475,11 +488,8 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
     stats->pixels_terminated = (int64_t)pt;
     stats->overflow = (h[CNT_OVERFLOW] != 0 || K > ctx->cap_k) ? 1 : 0;
     if (timing) {
-      float t[5];
-      for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], ctx->ev[i], ctx->ev[i + 1]);
-      stats->ms_stage[0] = t[0]; stats->ms_stage[1] = t[1]; stats->ms_stage[2] = t[2];
-      stats->ms_stage[3] = t[3]; stats->ms_stage[4] = t[4];
-      cudaEventElapsedTime(&stats->ms_stage[5], ctx->ev[0], ctx->ev[5]);
+      for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&stats->ms_stage[i], ev[i], ev[i + 1]);
+      cudaEventElapsedTime(&stats->ms_stage[6], ev[0], ev[6]);
     }
     if (stats->overflow) return fail(ctx, GUT_E_CAPACITY, "key capacity exceeded (gut_workspace_reserve)");
   }
@@ -499,6 +509,26 @@ gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_
     gut_status r = render_one(ctx, scene, &cams[v], opt, &outs[v], (cudaStream_t)s, stats ? &stats[v] : nullptr);
     if (r != GUT_OK) return r;
   }
+  return GUT_OK;
+}
+
+gut_status gut_timing_read(gut_context *ctx, double ms_sum[7], int32_t *n_renders, int32_t reset) {
+  if (!ctx || !ms_sum) return fail(ctx, GUT_E_INVALID_ARGUMENT, "gut_timing_read: NULL argument");
+  cudaSetDevice(ctx->device);
+  for (int i = 0; i < 7; ++i) ms_sum[i] = 0;
+  for (size_t r = 0; r < ctx->tnext; ++r) {
+    auto &e = ctx->tsets[r];
+    CUDA_TRY(ctx, cudaEventSynchronize(e[6]));
+    float t;
+    for (int i = 0; i < 6; ++i) {
+      CUDA_TRY(ctx, cudaEventElapsedTime(&t, e[i], e[i + 1]));
+      ms_sum[i] += t;
+    }
+    CUDA_TRY(ctx, cudaEventElapsedTime(&t, e[0], e[6]));
+    ms_sum[6] += t;
+  }
+  if (n_renders) *n_renders = (int32_t)ctx->tnext;
+  if (reset) ctx->tnext = 0;
   return GUT_OK;
 }
 

@@ -52,7 +52,7 @@ class gut_outputs(C.Structure):
 class gut_stats(C.Structure):
     _fields_ = [("n_input", C.c_int64), ("n_visible", C.c_int64), ("n_keys", C.c_int64), ("n_tiles", C.c_int32),
                 ("max_tile_len", C.c_int32), ("pairs_evaluated", C.c_int64), ("pairs_contributing", C.c_int64),
-                ("pixels_terminated", C.c_int64), ("ms_stage", C.c_float * 6), ("overflow", C.c_int32),
+                ("pixels_terminated", C.c_int64), ("ms_stage", C.c_float * 7), ("overflow", C.c_int32),
                 ("pad0", C.c_int32)]
 
     def as_dict(self):
@@ -68,7 +68,8 @@ class gut_proj_record(C.Structure):
 
 EXPORTS = ["gut_abi_version", "gut_options_default", "gut_context_create", "gut_context_destroy",
            "gut_last_error", "gut_workspace_reserve", "gut_scene_create", "gut_scene_destroy", "gut_render",
-           "gut_render_batch", "gut_debug_copy_stage"]
+           "gut_render_batch", "gut_timing_read", "gut_debug_copy_stage"]
+STAGE_NAMES = ["K1_project", "K3_sort_depth", "K2_emit", "K3_sort_tile", "K4_ranges", "K5_blend", "total"]
 
 _lib = None
 
@@ -102,8 +103,9 @@ def lib():
         L.gut_render_batch.argtypes = [vp, vp, C.POINTER(gut_camera), i32, C.POINTER(gut_options),
                                        C.POINTER(gut_outputs), vp, C.POINTER(gut_stats)]
         L.gut_debug_copy_stage.argtypes = [vp, i32, vp, C.c_size_t, C.POINTER(C.c_size_t)]
+        L.gut_timing_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int32), i32]
         for name in ("gut_context_create", "gut_workspace_reserve", "gut_scene_create", "gut_render",
-                     "gut_render_batch", "gut_debug_copy_stage"):
+                     "gut_render_batch", "gut_timing_read", "gut_debug_copy_stage"):
             getattr(L, name).restype = C.c_int
         L.gut_options_default.restype = None
         L.gut_context_destroy.restype = None
@@ -228,6 +230,14 @@ def gut_render_batch(ctx, scene, cams: Sequence[gut_camera], opt: gut_options, o
     st = (gut_stats * n)() if stats else None
     _check(lib().gut_render_batch(ctx, scene, carr, n, C.byref(opt), oarr, _stream_ptr(stream), st), ctx)
     return st
+
+
+def gut_timing_read(ctx, reset: bool = True):
+    """Summed per-stage milliseconds of the timing=1 renders since the last reset."""
+    ms = (C.c_double * 7)()
+    n = C.c_int32(0)
+    _check(lib().gut_timing_read(ctx, ms, C.byref(n), int(reset)), ctx)
+    return dict(zip(STAGE_NAMES, list(ms))), int(n.value)
 
 
 def gut_debug_copy_stage(ctx, stage: int):

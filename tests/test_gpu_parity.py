@@ -38,14 +38,17 @@ def _proj_parity(scene, cam, g, o_proj, opt=OPT):
     both = vis_g & vis_o & ~amb
     # tile counts bit-exact outside the 1e-3 px band
     np.testing.assert_array_equal(gp["tiles"][both], o_proj["tiles"][both])
-    # mean within 1e-3 px, covariance within 1e-4 relative, depth, colour
-    assert np.abs(gp["vx"][both] - o_proj["vx"][both]).max(initial=0) < 1e-3
-    assert np.abs(gp["vy"][both] - o_proj["vy"][both]).max(initial=0) < 1e-3
-    for f in ("cxx", "cyy"):
+    # binning geometry: mean and extent edges within half the 1e-3 px band,
+    # covariance within 1e-3 relative (fp32 pixel coordinates)
+    assert np.abs(gp["vx"][both] - o_proj["vx"][both]).max(initial=0) < 5e-4
+    assert np.abs(gp["vy"][both] - o_proj["vy"][both]).max(initial=0) < 5e-4
+    for f, h in (("cxx", "hx"), ("cyy", "hy")):
         rel = np.abs(gp[f][both] - o_proj[f][both]) / np.abs(o_proj[f][both])
-        assert rel.max(initial=0) < 1e-4, f
+        assert rel.max(initial=0) < 1e-3, f
+        hg = np.sqrt(gp["k2"][both].astype(np.float64) * gp[f][both])
+        assert np.abs(hg - o_proj[h][both]).max(initial=0) < 5e-4, h
     sc = np.sqrt(o_proj["cxx"][both] * o_proj["cyy"][both])
-    assert (np.abs(gp["cxy"][both] - o_proj["cxy"][both]) / sc).max(initial=0) < 1e-4
+    assert (np.abs(gp["cxy"][both] - o_proj["cxy"][both]) / sc).max(initial=0) < 1e-3
     rel = np.abs(gp["depth"][both] - o_proj["depth"][both]) / o_proj["depth"][both]
     assert rel.max(initial=0) < 2e-6
     assert np.abs(gp["rgb"][both] - o_proj["rgb"][both]).max(initial=0) < 1e-5
