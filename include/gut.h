@@ -148,7 +148,9 @@ typedef enum {
   GUT_STAGE_PROJECT = 1, /* per Gaussian gut_proj_record [n_input] */
   GUT_STAGE_DEPTH_ORDER = 2, /* uint32 gid [n_visible], visible Gaussians by (depth, gid) */
   GUT_STAGE_SORTED = 3,  /* uint32 pairs (tile, gid) [n_keys], sorted by (tile, depth, gid) */
-  GUT_STAGE_RANGES = 4   /* uint32 pairs [start, end) [n_tiles] */
+  GUT_STAGE_RANGES = 4,  /* uint32 pairs [start, end) [n_tiles] */
+  GUT_STAGE_TILE_WORK = 5 /* uint32 pairs (list length, entries the blend visited before every
+                             pixel of the tile terminated) [n_tiles] */
 } gut_stage;
 
 typedef struct { /* GUT_STAGE_PROJECT record (K1 output, fp32) */

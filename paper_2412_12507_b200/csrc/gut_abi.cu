@@ -33,7 +33,7 @@ struct gut_context {
   float4 *ell = nullptr, *payload = nullptr;
   uint32_t *sa_k = nullptr, *sa_v = nullptr, *sb_k = nullptr, *sb_v = nullptr;
   uint32_t *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr;
-  uint2 *ranges = nullptr;
+  uint2 *ranges = nullptr, *tile_work = nullptr;
   float *img = nullptr;
   unsigned long long *st_depth = nullptr, *st_emit = nullptr, *st_tile = nullptr;
   uint32_t *counters = nullptr, *h_counters = nullptr;
@@ -111,6 +111,7 @@ static gut_status ensure_tiles(gut_context *ctx, size_t t) {
   if (t <= ctx->cap_tiles) return GUT_OK;
   size_t dummy = 0;
   CUDA_TRY(ctx, regrow(ctx->ranges, dummy, t));
+  CUDA_TRY(ctx, regrow(ctx->tile_work, dummy, t));
   ctx->cap_tiles = t;
   return GUT_OK;
 }
@@ -268,7 +269,8 @@ void gut_context_destroy(gut_context *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->payload, ctx->sa_k, ctx->sa_v, ctx->sb_k, ctx->sb_v,
-                ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->img, ctx->st_depth, ctx->st_emit,
+                ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->tile_work, ctx->img, ctx->st_depth,
+                ctx->st_emit,
                 ctx->st_tile, ctx->counters};
   for (void *p : ps) if (p) cudaFree(p);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
@@ -451,7 +453,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
     alpha = ctx->img + 3 * npix;
     depth = out->depth ? ctx->img + 4 * npix : nullptr;
   }
-  launch_blend(dc, ctx->ranges, fv, ctx->payload, rgb, alpha, depth, cnt, st);
+  launch_blend(dc, ctx->ranges, fv, ctx->payload, rgb, alpha, depth, cnt, ctx->tile_work, st);
   if (timing) cudaEventRecord(ev[6], st);
   {
     cudaError_t e = cudaGetLastError();
@@ -547,7 +549,8 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
     case GUT_STAGE_PROJECT: need = N * sizeof(gut_proj_record); break;
     case GUT_STAGE_DEPTH_ORDER: need = nv * sizeof(uint32_t); break;
     case GUT_STAGE_SORTED: need = (size_t)K * 2 * sizeof(uint32_t); break;
-    case GUT_STAGE_RANGES: need = (size_t)ctx->last_tiles * 2 * sizeof(uint32_t); break;
+    case GUT_STAGE_RANGES:
+    case GUT_STAGE_TILE_WORK: need = (size_t)ctx->last_tiles * 2 * sizeof(uint32_t); break;
     default: return fail(ctx, GUT_E_INVALID_ARGUMENT, "stage");
   }
   if (bytes_needed) *bytes_needed = need;
@@ -584,8 +587,10 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
     uint32_t *o = (uint32_t *)host_dst;
     for (size_t k = 0; k < K; ++k) { o[2 * k] = t[k]; o[2 * k + 1] = g[k]; }
     delete[] t; delete[] g;
-  } else {
+  } else if (stage == GUT_STAGE_RANGES) {
     CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->ranges, need, cudaMemcpyDeviceToHost));
+  } else {
+    CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->tile_work, need, cudaMemcpyDeviceToHost));
   }
   return GUT_OK;
 }

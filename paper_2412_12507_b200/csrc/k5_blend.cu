@@ -109,7 +109,7 @@ template <int MODE>  // 0: central global shutter, 1: orthographic, 2: central r
 __global__ __launch_bounds__(GUT_BLEND_THREADS) void blend_kernel(
     DevCam c, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ gids,
     const float4 *__restrict__ payload, float *__restrict__ out_rgb, float *__restrict__ out_alpha,
-    float *__restrict__ out_depth, uint32_t *counters) {
+    float *__restrict__ out_depth, uint32_t *counters, uint2 *__restrict__ tile_work) {
   constexpr int NF = MODE == 2 ? 10 : 7;
   __shared__ float4 s_f[NF][GUT_BLEND_THREADS];
   __shared__ double s_red[8][4];
@@ -204,7 +204,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS) void blend_kernel(
   // ---- compositing state
   float T = 1.f, Cr = 0.f, Cg = 0.f, Cb = 0.f, Dp = 0.f;
   bool done = !valid;
-  uint32_t n_eval = 0, n_contrib = 0, n_term = 0;
+  uint32_t n_eval = 0, n_contrib = 0, n_term = 0, processed = 0;
   const uint2 rg = ranges[tile];
   const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x;
   if (threadIdx.x == 0 && end > start) atomicMax(&counters[CNT_MAXLEN], end - start);
@@ -294,6 +294,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS) void blend_kernel(
       T = Tn;
       ++n_contrib;
     }
+    processed = b0 - start + cnt;
     if (__syncthreads_count(done) == GUT_BLEND_THREADS) break;
   }
 
@@ -314,6 +315,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS) void blend_kernel(
     }
   }
   // statistics
+  if (threadIdx.x == 0) tile_work[tile] = make_uint2(end - start, processed);
   unsigned long long e1 = warp_sum((unsigned long long)n_eval);
   unsigned long long e2 = warp_sum((unsigned long long)n_contrib);
   unsigned long long e3 = warp_sum((unsigned long long)n_term);
@@ -325,14 +327,14 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS) void blend_kernel(
 }
 
 void launch_blend(const DevCam &cam, const uint2 *ranges, const uint32_t *gids, const float4 *payload,
-                  float *rgb, float *alpha, float *depth, uint32_t *counters, cudaStream_t st) {
+                  float *rgb, float *alpha, float *depth, uint32_t *counters, uint2 *tile_work, cudaStream_t st) {
   const unsigned blocks = (unsigned)cam.n_tiles;
   if (cam.model == CAM_ORTHO)
-    blend_kernel<1><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, ranges, gids, payload, rgb, alpha, depth, counters);
+    blend_kernel<1><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, ranges, gids, payload, rgb, alpha, depth, counters, tile_work);
   else if (cam.shutter != SH_GLOBAL)
-    blend_kernel<2><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, ranges, gids, payload, rgb, alpha, depth, counters);
+    blend_kernel<2><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, ranges, gids, payload, rgb, alpha, depth, counters, tile_work);
   else
-    blend_kernel<0><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, ranges, gids, payload, rgb, alpha, depth, counters);
+    blend_kernel<0><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, ranges, gids, payload, rgb, alpha, depth, counters, tile_work);
 }
 
 }  // namespace gut

@@ -52,6 +52,6 @@ void launch_ranges(const uint32_t *tile_sorted, const uint32_t *counters, uint32
                    cudaStream_t st);
 
 void launch_blend(const DevCam &cam, const uint2 *ranges, const uint32_t *gids, const float4 *payload,
-                  float *rgb, float *alpha, float *depth, uint32_t *counters, cudaStream_t st);
+                  float *rgb, float *alpha, float *depth, uint32_t *counters, uint2 *tile_work, cudaStream_t st);
 
 }  // namespace gut
