@@ -8,6 +8,7 @@
 // the slerp axis-angle, UT weights from alpha/beta/kappa).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <array>
@@ -37,6 +38,16 @@ struct gut_context {
   float *img = nullptr;
   unsigned long long *st_depth = nullptr, *st_emit = nullptr, *st_tile = nullptr;
   uint32_t *counters = nullptr, *h_counters = nullptr;
+  // K5: ray LUT (cached per intrinsics for global shutter), blend work plan
+  float4 *pix = nullptr;
+  TileAnchor *anchors = nullptr;
+  uint32_t *seg_base = nullptr, *tile_done = nullptr, *items = nullptr, *items_pre = nullptr;
+  float *prod = nullptr, *part_t = nullptr;
+  float4 *part_c = nullptr;
+  size_t cap_items = 0;
+  bool lut_valid = false;
+  double lut_key[20] = {};
+  int blend_seg = 1024;
   uint32_t epoch = 0;
   bool reserved = false;
   std::vector<std::array<cudaEvent_t, 7>> tsets;  // per-render stage events (timing = 1)
@@ -112,7 +123,26 @@ static gut_status ensure_tiles(gut_context *ctx, size_t t) {
   size_t dummy = 0;
   CUDA_TRY(ctx, regrow(ctx->ranges, dummy, t));
   CUDA_TRY(ctx, regrow(ctx->tile_work, dummy, t));
+  CUDA_TRY(ctx, regrow(ctx->pix, dummy, t * GUT_BLEND_THREADS));
+  CUDA_TRY(ctx, regrow(ctx->anchors, dummy, t));
+  CUDA_TRY(ctx, regrow(ctx->seg_base, dummy, t));
+  CUDA_TRY(ctx, regrow(ctx->tile_done, dummy, t));
+  CUDA_TRY(ctx, cudaMemset(ctx->tile_done, 0, t * sizeof(uint32_t)));
+  ctx->lut_valid = false;
   ctx->cap_tiles = t;
+  return GUT_OK;
+}
+
+// blend work items: at most n_tiles + K / seg + 1 (tile, segment) pairs
+static gut_status ensure_items(gut_context *ctx, size_t items) {
+  if (items <= ctx->cap_items) return GUT_OK;
+  size_t c = items + items / 8 + 64, dummy = 0;
+  CUDA_TRY(ctx, regrow(ctx->items, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->items_pre, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->prod, dummy, c * GUT_BLEND_THREADS));
+  CUDA_TRY(ctx, regrow(ctx->part_c, dummy, c * GUT_BLEND_THREADS));
+  CUDA_TRY(ctx, regrow(ctx->part_t, dummy, c * GUT_BLEND_THREADS));
+  ctx->cap_items = c;
   return GUT_OK;
 }
 
@@ -256,6 +286,10 @@ gut_status gut_context_create(int32_t dev, gut_context **out) {
   gut_context *ctx = new (std::nothrow) gut_context();
   if (!ctx) return fail(nullptr, GUT_E_OUT_OF_MEMORY, "context");
   ctx->device = dev;
+  if (const char *e = getenv("GUT_BLEND_SEG")) {  // tuning knob: list entries per blend work item
+    int v = atoi(e);
+    if (v >= 256 && v % 256 == 0) ctx->blend_seg = v;
+  }
   if (cudaMalloc((void **)&ctx->counters, CNT_WORDS * sizeof(uint32_t)) != cudaSuccess ||
       cudaMallocHost((void **)&ctx->h_counters, CNT_WORDS * sizeof(uint32_t)) != cudaSuccess) {
     delete ctx;
@@ -270,8 +304,8 @@ void gut_context_destroy(gut_context *ctx) {
   cudaSetDevice(ctx->device);
   void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->payload, ctx->sa_k, ctx->sa_v, ctx->sb_k, ctx->sb_v,
                 ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->tile_work, ctx->img, ctx->st_depth,
-                ctx->st_emit,
-                ctx->st_tile, ctx->counters};
+                ctx->st_emit, ctx->st_tile, ctx->counters, ctx->pix, ctx->anchors, ctx->seg_base,
+                ctx->tile_done, ctx->items, ctx->items_pre, ctx->prod, ctx->part_c, ctx->part_t};
   for (void *p : ps) if (p) cudaFree(p);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
   for (auto &set : ctx->tsets)
@@ -453,7 +487,32 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
     alpha = ctx->img + 3 * npix;
     depth = out->depth ? ctx->img + 4 * npix : nullptr;
   }
-  launch_blend(dc, ctx->ranges, fv, ctx->payload, rgb, alpha, depth, cnt, ctx->tile_work, st);
+  // a5: pixel rays relative to per-tile anchors — a function of the intrinsics
+  // only for global shutter (built once per intrinsics), per view for RS
+  {
+    double key[20] = {(double)dc.model, (double)dc.width, (double)dc.height, dc.fx, dc.fy, dc.cx, dc.cy,
+                      dc.k[0], dc.k[1], dc.k[2], dc.k[3], dc.k[4], dc.k[5], dc.p[0], dc.p[1], dc.fov,
+                      (double)dc.shutter, 0, 0, 0};
+    const bool cacheable = dc.shutter == GUT_SHUTTER_GLOBAL;
+    if (!cacheable || !ctx->lut_valid || memcmp(key, ctx->lut_key, sizeof(key)) != 0) {
+      launch_rays(dc, ctx->pix, ctx->anchors, st);
+      memcpy(ctx->lut_key, key, sizeof(key));
+      ctx->lut_valid = cacheable;
+    }
+  }
+  const size_t max_items = (size_t)dc.n_tiles + ctx->cap_k / (size_t)ctx->blend_seg + 2;
+  if ((s = ensure_items(ctx, max_items)) != GUT_OK) return s;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->tile_work, 0, (size_t)dc.n_tiles * sizeof(uint2), st));
+  launch_plan(ctx->ranges, dc.n_tiles, ctx->blend_seg, ctx->items, ctx->items_pre, ctx->seg_base, cnt, st);
+  BlendBufs bb;
+  bb.ranges = ctx->ranges; bb.gids = fv; bb.payload = ctx->payload; bb.pix = ctx->pix; bb.anchors = ctx->anchors;
+  bb.items = ctx->items; bb.items_pre = ctx->items_pre; bb.seg_base = ctx->seg_base;
+  bb.prod = ctx->prod; bb.part_c = ctx->part_c; bb.part_t = ctx->part_t; bb.tile_done = ctx->tile_done;
+  bb.tile_work = ctx->tile_work; bb.seg = ctx->blend_seg;
+  bb.max_items = (uint32_t)max_items;
+  bb.max_pre = (uint32_t)(ctx->cap_k / (size_t)ctx->blend_seg + 1);
+  bb.rgb = rgb; bb.alpha = alpha; bb.depth = depth; bb.counters = cnt;
+  launch_blend(dc, bb, st);
   if (timing) cudaEventRecord(ev[6], st);
   {
     cudaError_t e = cudaGetLastError();

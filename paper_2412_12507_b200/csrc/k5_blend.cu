@@ -7,18 +7,28 @@
 // response at tau_max is exp(-omega^2/2), omega^2 = ||o_g x d_g||^2/||d_g||^2
 // (Supp. B, L506).  Order = the tile's global depth order (L208).
 //
-// One CTA per 16x16 tile, one pixel per thread, warps on 8x4 pixel blocks.
-// Precision design: the cross product o_g x d_g
-// cancels catastrophically in fp32 for small, distant Gaussians, so every
-// pixel ray is written relative to a per-tile anchor ray (D, O) as
+// Precision: o_g x d_g cancels catastrophically
+// in fp32 for small, distant Gaussians, so every pixel ray is written relative
+// to a per-tile anchor ray (D, O) as
 //   d' = D + a T1 + b T2  (central cameras; a, b = tangent-plane offsets),
 //   o  = O + a T1 + b T2  (orthographic),   o = O + beta dc  (rolling shutter),
 // and per (tile, entry) the large, cancelling part c0 = o_g x (M D) is formed
-// in fp64 while staging the entry into shared memory.  What remains per
-// (pixel, entry) pair is fp32 and small:
+// in fp64 while the entry is staged into shared memory.  Per (pixel, entry):
 //   n = c0 + a P + b Q [+ beta (h + a PU + b QV)],  e = e0 + a U + b V
 //   omega^2 = |n|^2 / |e|^2,   reject before MUFU if |n|^2 > k^2 |e|^2
 // with k^2 = 2 ln(sigma / alpha_min) (alpha >= alpha_min <=> omega^2 <= k^2).
+//
+// Load balance: tile lists are split into segments of `seg` entries; every
+// (tile, segment) is one CTA.  Front-to-back blending needs the transmittance
+// at the segment start, so a first pass computes each non-final segment's
+// transmittance product P_s (cut to 0 once below T_min: termination then
+// happens no later than that segment); the blend pass starts segment s at
+// T = prod_{s'<s} P_s' and runs the exact per-pixel loop with termination.
+// When the product of the earlier segments is >= T_min no earlier entry can
+// have terminated the pixel (T is monotone), so the result equals the
+// sequential loop up to fp32 rounding of the products.  The last segment CTA
+// to finish a tile (atomic counter) sums the partial results in segment order
+// (deterministic) and writes the pixels.
 #include "launch.h"
 
 namespace gut {
@@ -105,41 +115,41 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-template <int MODE>  // 0: central global shutter, 1: orthographic, 2: central rolling shutter
-__global__ __launch_bounds__(GUT_BLEND_THREADS) void blend_kernel(
-    DevCam c, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ gids,
-    const float4 *__restrict__ payload, float *__restrict__ out_rgb, float *__restrict__ out_alpha,
-    float *__restrict__ out_depth, uint32_t *counters, uint2 *__restrict__ tile_work) {
-  constexpr int NF = MODE == 2 ? 10 : 7;
-  __shared__ float4 s_f[NF][GUT_BLEND_THREADS];
-  __shared__ double s_red[8][4];
-  __shared__ double s_anchor[13];  // D(3) O(3) T1(3) T2(3) t_anchor
-  __shared__ int s_nvalid;
+// thread -> pixel of a 16x16 tile: warps on 8x4 pixel blocks (coherent ballots)
+__device__ __forceinline__ void tile_pixel(int tile, int tiles_x, int &px, int &py) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  px = (tile % tiles_x) * GUT_TILE + (w & 1) * 8 + (lane & 7);
+  py = (tile / tiles_x) * GUT_TILE + (w >> 1) * 4 + (lane >> 3);
+}
 
+// ---------------------------------------------------------------- rays (a5)
+// Per tile: fp64 rays of its pixels, anchor = mean valid direction (central)
+// or mean valid origin (orthographic); per pixel the fp32 offsets (a, b), the
+// distance factor snorm = |d'| (0 marks an invalid pixel) and, for rolling
+// shutter, beta = t_pixel - t_anchor.  MODE 0/1: camera frame (depends on the
+// intrinsics only, cached by the host); MODE 2: world frame (per view).
+template <int MODE>
+__global__ __launch_bounds__(GUT_BLEND_THREADS) void rays_kernel(DevCam c, float4 *__restrict__ pix,
+                                                                 TileAnchor *__restrict__ anchors) {
+  __shared__ double s_red[8][4];
+  __shared__ double s_a[13];
   const int tile = blockIdx.x;
   const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int px = tx * GUT_TILE + (w & 1) * 8 + (lane & 7);
-  const int py = ty * GUT_TILE + (w >> 1) * 4 + (lane >> 3);
+  int px, py;
+  tile_pixel(tile, c.tiles_x, px, py);
   const bool inside = px < c.width && py < c.height;
   const double u = px + 0.5, v = py + 0.5;
-
-  // ---- per-pixel ray in fp64 (PAPER L116 r(tau) = o + tau d; reading R17 time)
   d3 dcam = mkd(0, 0, 1), ocam = mkd(0, 0, 0);
   bool valid = inside && unproject(c, u, v, dcam, ocam);
   const double tp = pixel_time(c, u, v);
-  d3 dw = mkd(0, 0, 0);
-  if (valid) {
-    if (MODE == 2) {
-      double Rt[9], Rw[9];
-      rodrigues_d(mkd(c.phi_axis[0], c.phi_axis[1], c.phi_axis[2]), tp * c.phi_angle, Rt);
-      matmul3(c.R0, Rt, Rw);
-      dw = mv(Rw, dcam);
-    } else if (MODE == 0) {
-      dw = mv(c.R0, dcam);
-    }
+  d3 dw = dcam;
+  if (MODE == 2 && valid) {
+    double Rt[9], Rw[9];
+    rodrigues_d(mkd(c.phi_axis[0], c.phi_axis[1], c.phi_axis[2]), tp * c.phi_angle, Rt);
+    matmul3(c.R0, Rt, Rw);
+    dw = mv(Rw, dcam);
   }
-  // ---- tile anchor: mean valid direction (central) / mean valid origin (ortho)
   d3 red = MODE == 1 ? ocam : dw;
   if (!valid) red = mkd(0, 0, 0);
   double rx = warp_sum(red.x), ry = warp_sum(red.y), rz = warp_sum(red.z);
@@ -150,74 +160,179 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS) void blend_kernel(
     d3 s = mkd(0, 0, 0);
     double cnt = 0;
     for (int k = 0; k < 8; ++k) { s = s + mkd(s_red[k][0], s_red[k][1], s_red[k][2]); cnt += s_red[k][3]; }
-    s_nvalid = (int)cnt;
     d3 D, O, T1, T2;
     double ta = 0;
     if (MODE == 1) {
-      d3 m = (cnt > 0 ? 1.0 / cnt : 0.0) * s;
-      O = mkd(c.c0[0], c.c0[1], c.c0[2]) + mv(c.R0, m);
-      D = mv(c.R0, mkd(0, 0, 1));
-      T1 = mv(c.R0, mkd(1, 0, 0));
-      T2 = mv(c.R0, mkd(0, 1, 0));
-      s_anchor[12] = 0;
-      // store the mean camera-frame offset in T-slots' spare: reuse s_red
-      s_red[0][0] = m.x; s_red[0][1] = m.y;
+      O = (cnt > 0 ? 1.0 / cnt : 0.0) * s;  // mean camera-frame origin offset
+      D = mkd(0, 0, 1); T1 = mkd(1, 0, 0); T2 = mkd(0, 1, 0);
     } else {
       D = cnt > 0 ? normalize_d(s) : mkd(0, 0, 1);
       d3 h = fabs(D.x) < 0.6 ? mkd(1, 0, 0) : (fabs(D.y) < 0.6 ? mkd(0, 1, 0) : mkd(0, 0, 1));
       T1 = normalize_d(h - dot(h, D) * D);
       T2 = cross(D, T1);
+      O = mkd(c.c0[0], c.c0[1], c.c0[2]);
       if (MODE == 2) {
         double uc = fmin(fmax(tx * GUT_TILE + 8.0, 0.5), c.width - 0.5);
         double vc = fmin(fmax(ty * GUT_TILE + 8.0, 0.5), c.height - 0.5);
         ta = pixel_time(c, uc, vc);
+        O = mkd(c.c0[0] + ta * c.dc[0], c.c0[1] + ta * c.dc[1], c.c0[2] + ta * c.dc[2]);
       }
-      O = mkd(c.c0[0] + ta * c.dc[0], c.c0[1] + ta * c.dc[1], c.c0[2] + ta * c.dc[2]);
     }
-    s_anchor[0] = D.x; s_anchor[1] = D.y; s_anchor[2] = D.z;
-    s_anchor[3] = O.x; s_anchor[4] = O.y; s_anchor[5] = O.z;
-    s_anchor[6] = T1.x; s_anchor[7] = T1.y; s_anchor[8] = T1.z;
-    s_anchor[9] = T2.x; s_anchor[10] = T2.y; s_anchor[11] = T2.z;
-    s_anchor[12] = ta;
+    double vals[13] = {D.x, D.y, D.z, T1.x, T1.y, T1.z, T2.x, T2.y, T2.z, O.x, O.y, O.z, ta};
+    for (int k = 0; k < 13; ++k) s_a[k] = vals[k];
+    TileAnchor A;
+    for (int k = 0; k < 3; ++k) { A.D[k] = vals[k]; A.T1[k] = vals[3 + k]; A.T2[k] = vals[6 + k]; A.O[k] = vals[9 + k]; }
+    A.ta = ta; A.pad[0] = A.pad[1] = A.pad[2] = 0;
+    anchors[tile] = A;
   }
   __syncthreads();
-  const d3 D = mkd(s_anchor[0], s_anchor[1], s_anchor[2]);
-  const d3 O = mkd(s_anchor[3], s_anchor[4], s_anchor[5]);
-  const d3 T1 = mkd(s_anchor[6], s_anchor[7], s_anchor[8]);
-  const d3 T2 = mkd(s_anchor[9], s_anchor[10], s_anchor[11]);
-  const f3 T1f = tof(T1), T2f = tof(T2);
-  float a = 0.f, b = 0.f, beta = 0.f, snorm = 1.f;
+  float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
   if (valid) {
+    const d3 D = mkd(s_a[0], s_a[1], s_a[2]), T1 = mkd(s_a[3], s_a[4], s_a[5]), T2 = mkd(s_a[6], s_a[7], s_a[8]);
     if (MODE == 1) {
-      a = (float)(ocam.x - s_red[0][0]);
-      b = (float)(ocam.y - s_red[0][1]);
+      out = make_float4((float)(ocam.x - s_a[9]), (float)(ocam.y - s_a[10]), 1.f, 0.f);
     } else {
-      double den = dot(dw, D);
-      a = (float)(dot(dw, T1) / den);
-      b = (float)(dot(dw, T2) / den);
-      snorm = (float)(1.0 / den);
-      if (!(den > 0)) valid = false;
-      if (MODE == 2) beta = (float)(tp - s_anchor[12]);
+      const double den = dot(dw, D);
+      if (den > 0) {
+        out.x = (float)(dot(dw, T1) / den);
+        out.y = (float)(dot(dw, T2) / den);
+        out.z = (float)(1.0 / den);
+        out.w = MODE == 2 ? (float)(tp - s_a[12]) : 0.f;
+      }
     }
   }
+  pix[(size_t)tile * GUT_BLEND_THREADS + threadIdx.x] = out;
+}
 
-  // ---- compositing state
-  float T = 1.f, Cr = 0.f, Cg = 0.f, Cb = 0.f, Dp = 0.f;
-  bool done = !valid;
-  uint32_t n_eval = 0, n_contrib = 0, n_term = 0, processed = 0;
-  const uint2 rg = ranges[tile];
-  const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x;
-  if (threadIdx.x == 0 && end > start) atomicMax(&counters[CNT_MAXLEN], end - start);
+void launch_rays(const DevCam &cam, float4 *pix, TileAnchor *anchors, cudaStream_t st) {
+  const unsigned blocks = (unsigned)cam.n_tiles;
+  if (cam.model == CAM_ORTHO) rays_kernel<1><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, pix, anchors);
+  else if (cam.shutter != SH_GLOBAL) rays_kernel<2><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, pix, anchors);
+  else rays_kernel<0><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, pix, anchors);
+}
+
+// ---------------------------------------------------------------- plan
+__global__ __launch_bounds__(1024) void plan_kernel(const uint2 *__restrict__ ranges, int n_tiles, int seg,
+                                                    uint32_t *__restrict__ items, uint32_t *__restrict__ items_pre,
+                                                    uint32_t *__restrict__ seg_base, uint32_t *counters) {
+  __shared__ uint32_t s_w[2][32];
+  const int per = (n_tiles + 1023) / 1024;
+  const int t0 = threadIdx.x * per, t1 = min(t0 + per, n_tiles);
+  uint32_t sa = 0, sb = 0;
+  for (int t = t0; t < t1; ++t) {
+    const uint2 r = ranges[t];
+    const uint32_t len = r.y > r.x ? r.y - r.x : 0;
+    const uint32_t S = len == 0 ? 1 : (len + seg - 1) / seg;
+    sa += S;
+    sb += S - 1;
+  }
+  // block exclusive scan of (sa, sb)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t xa = sa, xb = sb;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t ya = __shfl_up_sync(0xffffffffu, xa, o), yb = __shfl_up_sync(0xffffffffu, xb, o);
+    if (lane >= o) { xa += ya; xb += yb; }
+  }
+  if (lane == 31) { s_w[0][w] = xa; s_w[1][w] = xb; }
+  __syncthreads();
+  if (w == 0) {
+    uint32_t ya = s_w[0][lane], yb = s_w[1][lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t za = __shfl_up_sync(0xffffffffu, ya, o), zb = __shfl_up_sync(0xffffffffu, yb, o);
+      if (lane >= o) { ya += za; yb += zb; }
+    }
+    s_w[0][lane] = ya; s_w[1][lane] = yb;
+  }
+  __syncthreads();
+  uint32_t oa = (w > 0 ? s_w[0][w - 1] : 0) + xa - sa;
+  uint32_t ob = (w > 0 ? s_w[1][w - 1] : 0) + xb - sb;
+  for (int t = t0; t < t1; ++t) {
+    const uint2 r = ranges[t];
+    const uint32_t len = r.y > r.x ? r.y - r.x : 0;
+    const uint32_t S = len == 0 ? 1 : (len + seg - 1) / seg;
+    seg_base[t] = oa;
+    for (uint32_t s = 0; s < S; ++s) items[oa + s] = (uint32_t)t | (s << 16);
+    for (uint32_t s = 0; s + 1 < S; ++s) items_pre[ob + s] = (uint32_t)t | (s << 16);
+    oa += S;
+    ob += S - 1;
+  }
+  if (threadIdx.x == 1023) {
+    counters[CNT_NITEMS] = oa;
+    counters[CNT_NPRE] = ob;
+  }
+}
+
+void launch_plan(const uint2 *ranges, int n_tiles, int seg, uint32_t *items, uint32_t *items_pre,
+                 uint32_t *seg_base, uint32_t *counters, cudaStream_t st) {
+  plan_kernel<<<1, 1024, 0, st>>>(ranges, n_tiles, seg, items, items_pre, seg_base, counters);
+}
+
+// ---------------------------------------------------------------- blend
+// PASS 0: transmittance product of a non-final segment; PASS 1: blend.
+template <int MODE, int PASS>
+__global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, BlendBufs B) {
+  constexpr int NF = MODE == 2 ? 10 : 7;
+  constexpr int NT = GUT_BLEND_THREADS;
+  __shared__ float4 s_f[NF * NT];
+  __shared__ int s_last;
+
+  const uint32_t n_items = B.counters[PASS == 0 ? CNT_NPRE : CNT_NITEMS];
+  const uint32_t item_idx = blockIdx.x;
+  if (item_idx >= n_items) return;
+  const uint32_t item = (PASS == 0 ? B.items_pre : B.items)[item_idx];
+  const int tile = (int)(item & 0xFFFFu), s = (int)(item >> 16);
+  const uint2 rg = B.ranges[tile];
+  const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x, len = end - start;
+  const int S = len == 0 ? 1 : (int)((len + B.seg - 1) / B.seg);
+  const uint32_t s0 = start + (uint32_t)s * B.seg, s1 = min(s0 + (uint32_t)B.seg, end);
+  const int tid = threadIdx.x;
+  int px, py;
+  tile_pixel(tile, c.tiles_x, px, py);
+  const bool inside = px < c.width && py < c.height;
+
+  // ---- pixel ray (LUT) and the tile anchor in the world frame (fp64)
+  const float4 pl = B.pix[(size_t)tile * NT + tid];
+  const float a = pl.x, b = pl.y, snorm = pl.z, beta = pl.w;
+  const bool valid = inside && snorm > 0.f;
+  const TileAnchor &A = B.anchors[tile];
+  d3 D, T1, T2, O;
+  if (MODE == 2) {
+    D = mkd(A.D[0], A.D[1], A.D[2]); T1 = mkd(A.T1[0], A.T1[1], A.T1[2]);
+    T2 = mkd(A.T2[0], A.T2[1], A.T2[2]); O = mkd(A.O[0], A.O[1], A.O[2]);
+  } else {
+    D = mv(c.R0, mkd(A.D[0], A.D[1], A.D[2]));
+    T1 = mv(c.R0, mkd(A.T1[0], A.T1[1], A.T1[2]));
+    T2 = mv(c.R0, mkd(A.T2[0], A.T2[1], A.T2[2]));
+    O = mkd(c.c0[0], c.c0[1], c.c0[2]);
+    if (MODE == 1) O = O + mv(c.R0, mkd(A.O[0], A.O[1], A.O[2]));
+  }
+  const f3 T1f = tof(T1), T2f = tof(T2);
   const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
 
-  for (uint32_t b0 = start; b0 < end; b0 += GUT_BLEND_THREADS) {
-    const uint32_t cnt = min((uint32_t)GUT_BLEND_THREADS, end - b0);
+  // ---- transmittance at the segment start
+  float T = 1.f;
+  if (PASS == 1 && s > 0 && valid) {
+    const uint32_t first = item_idx - (uint32_t)s;  // items of a tile are contiguous
+    for (int q = 0; q < s; ++q) T *= __ldcg(&B.prod[(size_t)(first + q) * NT + tid]);
+  }
+  const bool active = valid && T >= c.t_min;
+  bool done = !active;
+  float Cr = 0.f, Cg = 0.f, Cb = 0.f, Dp = 0.f;
+  uint32_t n_eval = 0, n_contrib = 0, n_term = 0;
+  if (PASS == 1 && s == 0 && tid == 0 && len > 0) atomicMax(&B.counters[CNT_MAXLEN], len);
+
+  uint32_t processed = 0;
+  const float alpha_min = c.alpha_min, alpha_max = c.alpha_max, t_min = c.t_min;
+  for (uint32_t b0 = s0; b0 < s1; b0 += NT) {
+    const uint32_t cnt = min((uint32_t)NT, s1 - b0);
     __syncthreads();
-    if (threadIdx.x < cnt) {
+    if ((uint32_t)tid < cnt) {
       // ---- stage one list entry: fp64 for the cancelling part, fp32 for the rest
-      const uint32_t g = __ldg(&gids[b0 + threadIdx.x]);
-      const float4 p0 = __ldg(&payload[4 * g]), p1 = __ldg(&payload[4 * g + 1]);
-      const float4 p2 = __ldg(&payload[4 * g + 2]), p3 = __ldg(&payload[4 * g + 3]);
+      const uint32_t g = __ldg(&B.gids[b0 + tid]);
+      const float4 p0 = __ldg(&B.payload[4 * g]), p1 = __ldg(&B.payload[4 * g + 1]);
+      const float4 p2 = __ldg(&B.payload[4 * g + 2]), p3 = __ldg(&B.payload[4 * g + 3]);
       const float M[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
       const double Md[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
       const d3 og = mv(Md, O - mkd(p0.x, p0.y, p0.z));
@@ -233,108 +348,153 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS) void blend_kernel(
       } else {
         P = cross(ogf, U); Q = cross(ogf, V); gu = dot(ogf, U); gv = dot(ogf, V);
       }
-      const float k2 = 2.f * logf(p0.w / c.alpha_min);
+      const float k2 = 2.f * logf(p0.w / alpha_min);
       const float l2s = log2f(p0.w);
-      const int t = threadIdx.x;
-      s_f[0][t] = make_float4((float)c0.x, (float)c0.y, (float)c0.z, k2);
-      s_f[1][t] = make_float4(P.x, P.y, P.z, Q.x);
-      s_f[2][t] = make_float4(Q.y, Q.z, e0.x, e0.y);
-      s_f[3][t] = make_float4(e0.z, U.x, U.y, U.z);
-      s_f[4][t] = make_float4(V.x, V.y, V.z, l2s);
-      s_f[5][t] = make_float4((float)g0, gu, gv, 0.f);
-      s_f[6][t] = make_float4(p3.y, p3.z, p3.w, 0.f);
+      s_f[0 * NT + tid] = make_float4((float)c0.x, (float)c0.y, (float)c0.z, k2);
+      s_f[1 * NT + tid] = make_float4(P.x, P.y, P.z, Q.x);
+      s_f[2 * NT + tid] = make_float4(Q.y, Q.z, e0.x, e0.y);
+      s_f[3 * NT + tid] = make_float4(e0.z, U.x, U.y, U.z);
+      s_f[4 * NT + tid] = make_float4(V.x, V.y, V.z, l2s);
+      s_f[5 * NT + tid] = make_float4((float)g0, gu, gv, 0.f);
+      s_f[6 * NT + tid] = make_float4(p3.y, p3.z, p3.w, 0.f);
       if (MODE == 2) {
         const f3 m = mv(M, dcw);
         const f3 h = cross(m, e0), PU = cross(m, U), QV = cross(m, V);
-        s_f[NF - 3][t] = make_float4(h.x, h.y, h.z, dot(m, e0));
-        s_f[NF - 2][t] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
-        s_f[NF - 1][t] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
+        s_f[(NF - 3) * NT + tid] = make_float4(h.x, h.y, h.z, dot(m, e0));
+        s_f[(NF - 2) * NT + tid] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
+        s_f[(NF - 1) * NT + tid] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
       }
     }
     __syncthreads();
-    for (uint32_t k = 0; k < cnt; ++k) {
-      if (done) break;
-      ++n_eval;
-      const float4 f0 = s_f[0][k], f1 = s_f[1][k], f2 = s_f[2][k], f3v = s_f[3][k], f4 = s_f[4][k];
-      float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
-      float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
-      float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
-      if (MODE == 2) {
-        const float4 h = s_f[NF - 3][k], pu = s_f[NF - 2][k], qv = s_f[NF - 1][k];
-        nx = fmaf(beta, fmaf(a, pu.x, fmaf(b, qv.x, h.x)), nx);
-        ny = fmaf(beta, fmaf(a, pu.y, fmaf(b, qv.y, h.y)), ny);
-        nz = fmaf(beta, fmaf(a, pu.z, fmaf(b, qv.z, h.z)), nz);
+    if (!done) {
+      const float4 *__restrict__ sf = s_f;
+      uint32_t k = 0;
+      for (; k < cnt; ++k) {
+        const float4 f0 = sf[k], f1 = sf[NT + k], f2 = sf[2 * NT + k], f3v = sf[3 * NT + k], f4 = sf[4 * NT + k];
+        float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
+        float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
+        float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
+        if (MODE == 2) {
+          const float4 h = sf[(NF - 3) * NT + k], pu = sf[(NF - 2) * NT + k], qv = sf[(NF - 1) * NT + k];
+          nx = fmaf(beta, fmaf(a, pu.x, fmaf(b, qv.x, h.x)), nx);
+          ny = fmaf(beta, fmaf(a, pu.y, fmaf(b, qv.y, h.y)), ny);
+          nz = fmaf(beta, fmaf(a, pu.z, fmaf(b, qv.z, h.z)), nz);
+        }
+        const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
+        const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
+        const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
+        const float N = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
+        const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
+        if (N > f0.w * Dd) continue;  // omega^2 > k^2  <=>  alpha < alpha_min
+        const float rD = __frcp_rn(Dd);
+        const float w2 = N * rD;
+        const float al = fminf(alpha_max, exp2f(fmaf(-0.72134752044448170f, w2, f4.w)));
+        if (!(al >= alpha_min)) continue;
+        const float4 f5 = sf[5 * NT + k];
+        float gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
+        if (MODE == 2) {
+          const float4 h = sf[(NF - 3) * NT + k], pu = sf[(NF - 2) * NT + k], qv = sf[(NF - 1) * NT + k];
+          gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
+        }
+        const float tau = -gg * rD * snorm;
+        if (!(tau > 0.f)) continue;  // reading R24
+        const float Tn = T * (1.f - al);
+        if (Tn < t_min) {
+          done = true;
+          n_term = 1;
+          if (PASS == 0) T = 0.f;
+          ++k;
+          break;
+        }
+        if (PASS == 1) {
+          const float4 f6 = sf[6 * NT + k];
+          const float wgt = al * T;
+          Cr = fmaf(wgt, f6.x, Cr);
+          Cg = fmaf(wgt, f6.y, Cg);
+          Cb = fmaf(wgt, f6.z, Cb);
+          Dp = fmaf(wgt, tau, Dp);
+          ++n_contrib;
+        }
+        T = Tn;
       }
-      const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
-      const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
-      const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
-      const float N = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
-      const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
-      if (N > f0.w * Dd) continue;  // omega^2 > k^2  <=>  alpha < alpha_min
-      const float rD = __frcp_rn(Dd);
-      const float w2 = N * rD;
-      const float al = fminf(c.alpha_max, exp2f(fmaf(-0.72134752044448170f, w2, f4.w)));
-      if (!(al >= c.alpha_min)) continue;
-      const float4 f5 = s_f[5][k];
-      float gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
-      if (MODE == 2) {
-        const float4 h = s_f[NF - 3][k], pu = s_f[NF - 2][k], qv = s_f[NF - 1][k];
-        gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
-      }
-      const float tau = -gg * rD * snorm;
-      if (!(tau > 0.f)) continue;  // reading R24
-      const float Tn = T * (1.f - al);
-      if (Tn < c.t_min) { done = true; n_term = 1; break; }
-      const float4 f6 = s_f[6][k];
-      const float wgt = al * T;
-      Cr = fmaf(wgt, f6.x, Cr);
-      Cg = fmaf(wgt, f6.y, Cg);
-      Cb = fmaf(wgt, f6.z, Cb);
-      Dp = fmaf(wgt, tau, Dp);
-      T = Tn;
-      ++n_contrib;
+      n_eval += k;
     }
-    processed = b0 - start + cnt;
-    if (__syncthreads_count(done) == GUT_BLEND_THREADS) break;
+    processed = b0 - s0 + cnt;
+    if (__syncthreads_count(done) == NT) break;
   }
 
-  if (inside) {
-    const size_t pix = (size_t)py * c.width + px;
-    if (valid) {
-      out_rgb[3 * pix] = Cr + T * c.bg[0];
-      out_rgb[3 * pix + 1] = Cg + T * c.bg[1];
-      out_rgb[3 * pix + 2] = Cb + T * c.bg[2];
-      out_alpha[pix] = 1.f - T;
-      if (out_depth) out_depth[pix] = Dp;
-    } else {
-      out_rgb[3 * pix] = c.bg[0];
-      out_rgb[3 * pix + 1] = c.bg[1];
-      out_rgb[3 * pix + 2] = c.bg[2];
-      out_alpha[pix] = 0.f;
-      if (out_depth) out_depth[pix] = 0.f;
+  if (PASS == 0) {
+    B.prod[(size_t)(B.seg_base[tile] + s) * NT + tid] = T;
+    return;
+  }
+  // ---- statistics
+  if (tid == 0) {
+    atomicAdd(&B.tile_work[tile].y, processed);
+    if (s == 0) B.tile_work[tile].x = len;
+  }
+  {
+    const int lane = tid & 31;
+    unsigned long long e1 = warp_sum((unsigned long long)n_eval);
+    unsigned long long e2 = warp_sum((unsigned long long)n_contrib);
+    unsigned long long e3 = warp_sum((unsigned long long)n_term);
+    if (lane == 0 && (e1 | e2 | e3)) {
+      atomicAdd(reinterpret_cast<unsigned long long *>(&B.counters[CNT_PAIRS_EVAL]), e1);
+      atomicAdd(reinterpret_cast<unsigned long long *>(&B.counters[CNT_PAIRS_CONTRIB]), e2);
+      atomicAdd(reinterpret_cast<unsigned long long *>(&B.counters[CNT_TERMINATED]), e3);
     }
   }
-  // statistics
-  if (threadIdx.x == 0) tile_work[tile] = make_uint2(end - start, processed);
-  unsigned long long e1 = warp_sum((unsigned long long)n_eval);
-  unsigned long long e2 = warp_sum((unsigned long long)n_contrib);
-  unsigned long long e3 = warp_sum((unsigned long long)n_term);
-  if (lane == 0 && (e1 | e2 | e3)) {
-    atomicAdd(reinterpret_cast<unsigned long long *>(&counters[CNT_PAIRS_EVAL]), e1);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&counters[CNT_PAIRS_CONTRIB]), e2);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&counters[CNT_TERMINATED]), e3);
+  // ---- outputs (single segment) or partials + deterministic in-order combine
+  float Tf = T;
+  if (S > 1) {
+    const size_t j = (size_t)item_idx * NT + tid;
+    B.part_c[j] = make_float4(Cr, Cg, Cb, Dp);
+    B.part_t[j] = active ? T : -1.f;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&B.tile_done[tile], 1u) == (uint32_t)(S - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const uint32_t first = item_idx - (uint32_t)s;
+    Cr = Cg = Cb = Dp = 0.f;
+    Tf = 1.f;
+    for (int q = 0; q < S; ++q) {
+      const size_t jj = (size_t)(first + q) * NT + tid;
+      const float4 pc = __ldcg(&B.part_c[jj]);
+      const float pt = __ldcg(&B.part_t[jj]);
+      Cr += pc.x; Cg += pc.y; Cb += pc.z; Dp += pc.w;
+      if (pt >= 0.f) Tf = pt;
+    }
+    if (tid == 0) B.tile_done[tile] = 0;
+  }
+  if (inside) {
+    const size_t p = (size_t)py * c.width + px;
+    if (valid) {
+      B.rgb[3 * p] = Cr + Tf * c.bg[0];
+      B.rgb[3 * p + 1] = Cg + Tf * c.bg[1];
+      B.rgb[3 * p + 2] = Cb + Tf * c.bg[2];
+      B.alpha[p] = 1.f - Tf;
+      if (B.depth) B.depth[p] = Dp;
+    } else {
+      B.rgb[3 * p] = c.bg[0];
+      B.rgb[3 * p + 1] = c.bg[1];
+      B.rgb[3 * p + 2] = c.bg[2];
+      B.alpha[p] = 0.f;
+      if (B.depth) B.depth[p] = 0.f;
+    }
   }
 }
 
-void launch_blend(const DevCam &cam, const uint2 *ranges, const uint32_t *gids, const float4 *payload,
-                  float *rgb, float *alpha, float *depth, uint32_t *counters, uint2 *tile_work, cudaStream_t st) {
-  const unsigned blocks = (unsigned)cam.n_tiles;
-  if (cam.model == CAM_ORTHO)
-    blend_kernel<1><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, ranges, gids, payload, rgb, alpha, depth, counters, tile_work);
-  else if (cam.shutter != SH_GLOBAL)
-    blend_kernel<2><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, ranges, gids, payload, rgb, alpha, depth, counters, tile_work);
-  else
-    blend_kernel<0><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, ranges, gids, payload, rgb, alpha, depth, counters, tile_work);
+template <int MODE>
+static void blend_mode(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
+  if (b.max_pre > 0) blend_kernel<MODE, 0><<<b.max_pre, GUT_BLEND_THREADS, 0, st>>>(cam, b);
+  blend_kernel<MODE, 1><<<b.max_items, GUT_BLEND_THREADS, 0, st>>>(cam, b);
+}
+
+void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
+  if (cam.model == CAM_ORTHO) blend_mode<1>(cam, b, st);
+  else if (cam.shutter != SH_GLOBAL) blend_mode<2>(cam, b, st);
+  else blend_mode<0>(cam, b, st);
 }
 
 }  // namespace gut

@@ -25,6 +25,8 @@ enum : int {
   CNT_PAIRS_CONTRIB = 20,  // u64
   CNT_TERMINATED = 22,     // u64
   CNT_MAXLEN = 24,
+  CNT_NITEMS = 26,         // blend work items (tile, segment)
+  CNT_NPRE = 27,           // transmittance-prefix work items
   CNT_HIST_DEPTH = 32,     // 4 x 256
   CNT_HIST_TILE = 32 + 1024,  // 2 x 256
   CNT_WORDS = 32 + 1024 + 512
@@ -51,7 +53,37 @@ void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper,
 void launch_ranges(const uint32_t *tile_sorted, const uint32_t *counters, uint32_t cap_k, uint2 *ranges,
                    cudaStream_t st);
 
-void launch_blend(const DevCam &cam, const uint2 *ranges, const uint32_t *gids, const float4 *payload,
-                  float *rgb, float *alpha, float *depth, uint32_t *counters, uint2 *tile_work, cudaStream_t st);
+// Per-tile ray anchor (fp64).  Global shutter: camera frame, a function of the
+// intrinsics only (cached).  Rolling shutter: world frame, per view.
+struct TileAnchor {
+  double D[3], T1[3], T2[3], O[3], ta, pad[3];
+};
+
+// per-pixel (a, b, snorm, beta) relative to the tile anchor + per-tile anchors
+void launch_rays(const DevCam &cam, float4 *pix, TileAnchor *anchors, cudaStream_t st);
+
+// blend work plan: tiles split into segments of `seg` list entries
+void launch_plan(const uint2 *ranges, int n_tiles, int seg, uint32_t *items, uint32_t *items_pre,
+                 uint32_t *seg_base, uint32_t *counters, cudaStream_t st);
+
+struct BlendBufs {
+  const uint2 *ranges;
+  const uint32_t *gids;
+  const float4 *payload;
+  const float4 *pix;
+  const TileAnchor *anchors;
+  const uint32_t *items, *items_pre, *seg_base;
+  float *prod;       // per (item, pixel) transmittance product of a segment
+  float4 *part_c;    // per (item, pixel) partial colour + depth
+  float *part_t;     // per (item, pixel) transmittance at segment end (-1 inactive)
+  uint32_t *tile_done;
+  uint2 *tile_work;
+  int seg;
+  uint32_t max_items, max_pre;
+  float *rgb, *alpha, *depth;
+  uint32_t *counters;
+};
+
+void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st);
 
 }  // namespace gut
