@@ -112,6 +112,113 @@ __device__ __forceinline__ bool project_sigma(const DevCam &c, f3 y, f3 w, float
   return true;
 }
 
+// ---- fp64 twin of the projection for Gaussians whose sigma points land far
+// from the principal point: fp32 pixel coordinates carry ~eps*|v| absolute
+// error, which above ~2048 px would exceed half the 1e-3 px binning band.
+__device__ bool project_cam_d(const DevCam &c, d3 x, double &du, double &dv) {
+  switch (c.model) {
+    case CAM_PINHOLE:
+      if (!(x.z > (double)c.near_plane)) return false;
+      du = c.fx * (x.x / x.z); dv = c.fy * (x.y / x.z);
+      return true;
+    case CAM_ORTHO:
+      if (!(x.z > (double)c.near_plane)) return false;
+      du = c.fx * x.x; dv = c.fy * x.y;
+      return true;
+    case CAM_OPENCV: {
+      if (!(x.z > (double)c.near_plane)) return false;
+      double xn = x.x / x.z, yn = x.y / x.z, r2 = xn * xn + yn * yn;
+      if (c.fov > 0 && !(r2 <= c.fov * c.fov)) return false;
+      double num = 1 + r2 * (c.k[0] + r2 * (c.k[1] + r2 * c.k[2]));
+      double den = 1 + r2 * (c.k[3] + r2 * (c.k[4] + r2 * c.k[5]));
+      double a = num / den;
+      double xd = xn * a + 2 * c.p[0] * xn * yn + c.p[1] * (r2 + 2 * xn * xn);
+      double yd = yn * a + c.p[0] * (r2 + 2 * yn * yn) + 2 * c.p[1] * xn * yn;
+      du = c.fx * xd; dv = c.fy * yd;
+      return true;
+    }
+    case CAM_FISHEYE: {
+      double nrm = sqrt(x.x * x.x + x.y * x.y + x.z * x.z);
+      if (!(nrm > (double)c.near_plane)) return false;
+      double rho = sqrt(x.x * x.x + x.y * x.y);
+      double th = atan2(rho, x.z);
+      if (!(th <= (double)c.fovf)) return false;  // same threshold value as the fp32 path
+      if (rho == 0) { du = 0; dv = 0; return true; }
+      double t2 = th * th;
+      double td = th * (1 + t2 * (c.k[0] + t2 * (c.k[1] + t2 * (c.k[2] + t2 * c.k[3]))));
+      du = c.fx * (td * x.x / rho); dv = c.fy * (td * x.y / rho);
+      return true;
+    }
+  }
+  return false;
+}
+
+__device__ __forceinline__ double shutter_coord_d(const DevCam &c, double du, double dv) {
+  double r;
+  switch (c.shutter) {
+    case SH_T2B: r = (dv + c.cy) / c.height; break;
+    case SH_B2T: r = 1.0 - (dv + c.cy) / c.height; break;
+    case SH_L2R: r = (du + c.cx) / c.width; break;
+    case SH_R2L: r = 1.0 - (du + c.cx) / c.width; break;
+    default: return 0.0;
+  }
+  return fmin(fmax(r, 0.0), 1.0);
+}
+
+__device__ bool project_sigma_d(const DevCam &c, d3 y, d3 w, double &du, double &dv) {
+  if (c.shutter == SH_GLOBAL) return project_cam_d(c, y, du, dv);
+  const d3 ax = mkd(c.phi_axis[0], c.phi_axis[1], c.phi_axis[2]);
+  auto at = [&](double t) {
+    double Rt[9];
+    rodrigues_d(ax, t * c.phi_angle, Rt);
+    return mtv(Rt, y - t * w);
+  };
+  double t0 = 0.5, u0, v0;
+  if (!project_cam_d(c, at(t0), u0, v0)) return false;
+  double f0 = shutter_coord_d(c, u0, v0) - t0;
+  double t1 = t0 + f0, u1, v1;
+  if (!project_cam_d(c, at(t1), u1, v1)) return false;
+  double f1 = shutter_coord_d(c, u1, v1) - t1;
+  for (int it = 0; it < c.rs_max_iter; ++it) {
+    if (hypot(u1 - u0, v1 - v0) < (double)c.rs_tol_px) break;
+    double den = f1 - f0;
+    double t2 = fabs(den) > 1e-15 ? t1 - f1 * (t1 - t0) / den : t1 + f1;
+    t2 = fmin(fmax(t2, 0.0), 1.0);
+    t0 = t1; u0 = u1; v0 = v1; f0 = f1; t1 = t2;
+    if (!project_cam_d(c, at(t1), u1, v1)) return false;
+    f1 = shutter_coord_d(c, u1, v1) - t1;
+  }
+  du = u1; dv = v1;
+  return true;
+}
+
+// Eq. 9-10 in fp64 from the fp64 camera-frame centre and fp32 R, s
+__device__ __noinline__ bool ut_fp64(const DevCam &c, d3 y0d, const float *R, float4 sc, float &vx, float &vy,
+                                     float &cxx, float &cxy, float &cyy) {
+  const d3 w = mtv(c.R0, mkd(c.dc[0], c.dc[1], c.dc[2]));
+  const double sj[3] = {sc.x, sc.y, sc.z};
+  double du[7], dv[7];
+  bool ok = project_sigma_d(c, y0d, w, du[0], dv[0]);
+  for (int j = 0; j < 3 && ok; ++j) {
+    const d3 L = ((double)c.gamma * sj[j]) * mkd(R[j], R[3 + j], R[6 + j]);
+    const d3 Lc = mtv(c.R0, L);
+    ok = ok && project_sigma_d(c, y0d + Lc, w, du[1 + j], dv[1 + j]);
+    ok = ok && project_sigma_d(c, y0d - Lc, w, du[4 + j], dv[4 + j]);
+  }
+  if (!ok) return false;
+  double mx = c.wmu0 * du[0], my = c.wmu0 * dv[0];
+  for (int k = 1; k < 7; ++k) { mx += (double)c.wmui * du[k]; my += (double)c.wmui * dv[k]; }
+  double sxx = 0, sxy = 0, syy = 0;
+  for (int k = 0; k < 7; ++k) {
+    const double wk = k == 0 ? (double)c.wsig0 : (double)c.wsigi;
+    const double ax = du[k] - mx, ay = dv[k] - my;
+    sxx += wk * ax * ax; sxy += wk * ax * ay; syy += wk * ay * ay;
+  }
+  vx = (float)mx; vy = (float)my;
+  cxx = (float)(sxx + c.dilation); cxy = (float)sxy; cyy = (float)(syy + c.dilation);
+  return true;
+}
+
 // 3DGS real SH basis up to degree DEG (reading R19), colour = max(sum + 0.5, 0)
 template <int DEG>
 __device__ __forceinline__ f3 sh_colour(const float4 *sh, int64_t n, int64_t i, f3 d) {
@@ -146,7 +253,7 @@ __device__ __forceinline__ f3 sh_colour(const float4 *sh, int64_t n, int64_t i, 
 }
 
 template <int DEG>
-__global__ __launch_bounds__(256) void project_kernel(DevCam c, SceneDev s, uint32_t *__restrict__ dkey,
+__global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, uint32_t *__restrict__ dkey,
                                                       uint32_t *__restrict__ tiles, float4 *__restrict__ ell,
                                                       float4 *__restrict__ payload, uint32_t *counters) {
   __shared__ uint32_t s_hist[4][256];
@@ -204,6 +311,10 @@ __global__ __launch_bounds__(256) void project_kernel(DevCam c, SceneDev s, uint
       cxx += c.wsigi * sxx + c.dilation;
       cxy += c.wsigi * sxy;
       cyy += c.wsigi * syy + c.dilation;
+      float mag = 0.f;
+#pragma unroll
+      for (int k = 0; k < 7; ++k) mag = fmaxf(mag, fmaxf(fabsf(du[k]), fabsf(dv[k])));
+      if (mag > 2048.f) ok = ut_fp64(c, y0d, R, sc, vx, vy, cxx, cxy, cyy);
       float det = cxx * cyy - cxy * cxy;
       ok = cxx > 0.f && cyy > 0.f && det > 0.f && isfinite(det);
       // opacity-aware extent level (Alg. 1 l.3, reading R11)

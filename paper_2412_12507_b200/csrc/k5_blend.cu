@@ -273,7 +273,7 @@ void launch_plan(const uint2 *ranges, int n_tiles, int seg, uint32_t *items, uin
 // PASS 0: transmittance product of a non-final segment; PASS 1: blend.
 template <int MODE, int PASS>
 __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, BlendBufs B) {
-  constexpr int NF = MODE == 2 ? 10 : 7;
+  constexpr int NF = MODE == 2 ? 11 : 8;
   constexpr int NT = GUT_BLEND_THREADS;
   __shared__ float4 s_f[NF * NT];
   __shared__ int s_last;
@@ -296,6 +296,25 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
   const float4 pl = B.pix[(size_t)tile * NT + tid];
   const float a = pl.x, b = pl.y, snorm = pl.z, beta = pl.w;
   const bool valid = inside && snorm > 0.f;
+  const int lane = tid & 31;
+  // warp pixel box in (a, b) for the conservative warp cull
+  float ac, bc, ra, rb;
+  {
+    float amin = valid ? a : 3e38f, amax = valid ? a : -3e38f;
+    float bmin = valid ? b : 3e38f, bmax = valid ? b : -3e38f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      amin = fminf(amin, __shfl_xor_sync(0xffffffffu, amin, o));
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      bmin = fminf(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+      bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+    }
+    if (amin > amax) { amin = amax = 0.f; bmin = bmax = 0.f; }  // no valid pixel: warp is done anyway
+    ac = 0.5f * (amin + amax);
+    bc = 0.5f * (bmin + bmax);
+    ra = 0.5f * (amax - amin) + 1e-7f * (fabsf(amin) + fabsf(amax));
+    rb = 0.5f * (bmax - bmin) + 1e-7f * (fabsf(bmin) + fabsf(bmax));
+  }
   const TileAnchor &A = B.anchors[tile];
   d3 D, T1, T2, O;
   if (MODE == 2) {
@@ -357,6 +376,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
       s_f[4 * NT + tid] = make_float4(V.x, V.y, V.z, l2s);
       s_f[5 * NT + tid] = make_float4((float)g0, gu, gv, 0.f);
       s_f[6 * NT + tid] = make_float4(p3.y, p3.z, p3.w, 0.f);
+      s_f[7 * NT + tid] = make_float4(sqrtf(dot(P, P)), sqrtf(dot(Q, Q)), sqrtf(dot(U, U)), sqrtf(dot(V, V)));
       if (MODE == 2) {
         const f3 m = mv(M, dcw);
         const f3 h = cross(m, e0), PU = cross(m, U), QV = cross(m, V);
@@ -366,10 +386,40 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
       }
     }
     __syncthreads();
-    if (!done) {
+    if (!__all_sync(0xffffffffu, done)) {
       const float4 *__restrict__ sf = s_f;
-      uint32_t k = 0;
-      for (; k < cnt; ++k) {
+      for (uint32_t r0 = 0; r0 < cnt; r0 += 32) {
+        // ---- per-warp conservative cull: lane j tests entry r0 + j against the
+        // warp's pixel box (a in ac +- ra, b in bc +- rb).  For every pixel of
+        // the box |n| >= |n(ac,bc)| - ra|P| - rb|Q| and |e| <= |e(ac,bc)| +
+        // ra|U| + rb|V| (triangle inequality), so omega^2 > k^2 for the whole
+        // box if (|n0| - dn)^2 > k^2 (|e0| + de)^2; 1e-3 relative margin for
+        // fp32 rounding.  Rolling shutter: no warp cull (every entry tested).
+        bool maybe = false;
+        const uint32_t kc = r0 + (uint32_t)lane;
+        if (kc < cnt) {
+          if (MODE == 2) {
+            maybe = true;
+          } else {
+            const float4 f0 = sf[kc], f1 = sf[NT + kc], f2 = sf[2 * NT + kc], f3v = sf[3 * NT + kc];
+            const float4 f4 = sf[4 * NT + kc], f7 = sf[7 * NT + kc];
+            const float nx = fmaf(ac, f1.x, fmaf(bc, f1.w, f0.x));
+            const float ny = fmaf(ac, f1.y, fmaf(bc, f2.x, f0.y));
+            const float nz = fmaf(ac, f1.z, fmaf(bc, f2.y, f0.z));
+            const float ex = fmaf(ac, f3v.y, fmaf(bc, f4.x, f2.z));
+            const float ey = fmaf(ac, f3v.z, fmaf(bc, f4.y, f2.w));
+            const float ez = fmaf(ac, f3v.w, fmaf(bc, f4.z, f3v.x));
+            const float lo = sqrtf(fmaf(nx, nx, fmaf(ny, ny, nz * nz))) - fmaf(ra, f7.x, rb * f7.y);
+            const float hi = sqrtf(fmaf(ex, ex, fmaf(ey, ey, ez * ez))) + fmaf(ra, f7.z, rb * f7.w);
+            maybe = !(lo > 0.f && lo * lo > 1.001f * f0.w * (hi * hi));
+          }
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, maybe);
+        while (m) {
+        const uint32_t k = r0 + (uint32_t)(__ffs(m) - 1);
+        m &= m - 1;
+        if (done) continue;
+        ++n_eval;
         const float4 f0 = sf[k], f1 = sf[NT + k], f2 = sf[2 * NT + k], f3v = sf[3 * NT + k], f4 = sf[4 * NT + k];
         float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
         float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
@@ -403,8 +453,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
           done = true;
           n_term = 1;
           if (PASS == 0) T = 0.f;
-          ++k;
-          break;
+          continue;
         }
         if (PASS == 1) {
           const float4 f6 = sf[6 * NT + k];
@@ -416,8 +465,9 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
           ++n_contrib;
         }
         T = Tn;
+        }
+        if (__all_sync(0xffffffffu, done)) break;
       }
-      n_eval += k;
     }
     processed = b0 - s0 + cnt;
     if (__syncthreads_count(done) == NT) break;
@@ -433,7 +483,6 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
     if (s == 0) B.tile_work[tile].x = len;
   }
   {
-    const int lane = tid & 31;
     unsigned long long e1 = warp_sum((unsigned long long)n_eval);
     unsigned long long e2 = warp_sum((unsigned long long)n_contrib);
     unsigned long long e3 = warp_sum((unsigned long long)n_term);
