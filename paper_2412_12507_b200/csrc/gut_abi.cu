@@ -32,6 +32,8 @@ struct gut_context {
   size_t cap_n = 0, cap_k = 0, cap_tiles = 0, cap_pix = 0;
   uint32_t *dkey = nullptr, *tiles = nullptr;
   float4 *ell = nullptr, *payload = nullptr;
+  double2 *ell64 = nullptr;
+  uint32_t *deferred = nullptr;
   uint32_t *sa_k = nullptr, *sa_v = nullptr, *sb_k = nullptr, *sb_v = nullptr;
   uint32_t *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr;
   uint2 *ranges = nullptr, *tile_work = nullptr;
@@ -88,6 +90,8 @@ static gut_status ensure_n(gut_context *ctx, size_t n) {
   CUDA_TRY(ctx, regrow(ctx->dkey, dummy, c));
   CUDA_TRY(ctx, regrow(ctx->tiles, dummy, c));
   CUDA_TRY(ctx, regrow(ctx->ell, dummy, 2 * c));
+  CUDA_TRY(ctx, regrow(ctx->ell64, dummy, 3 * c));
+  CUDA_TRY(ctx, regrow(ctx->deferred, dummy, c));
   CUDA_TRY(ctx, regrow(ctx->payload, dummy, 4 * c));
   CUDA_TRY(ctx, regrow(ctx->sa_k, dummy, c));
   CUDA_TRY(ctx, regrow(ctx->sa_v, dummy, c));
@@ -302,7 +306,8 @@ gut_status gut_context_create(int32_t dev, gut_context **out) {
 void gut_context_destroy(gut_context *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->payload, ctx->sa_k, ctx->sa_v, ctx->sb_k, ctx->sb_v,
+  void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->deferred, ctx->payload, ctx->sa_k, ctx->sa_v,
+                ctx->sb_k, ctx->sb_v,
                 ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->tile_work, ctx->img, ctx->st_depth,
                 ctx->st_emit, ctx->st_tile, ctx->counters, ctx->pix, ctx->anchors, ctx->seg_base,
                 ctx->tile_done, ctx->items, ctx->items_pre, ctx->prod, ctx->part_c, ctx->part_t};
@@ -432,7 +437,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   uint32_t *cnt = ctx->counters;
   CUDA_TRY(ctx, cudaMemsetAsync(cnt, 0, CNT_WORDS * sizeof(uint32_t), st));
   // K1: UT projection
-  launch_project(dc, scene->d, ctx->dkey, ctx->tiles, ctx->ell, ctx->payload, cnt, st);
+  launch_project(dc, scene->d, ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->payload, cnt, ctx->deferred, st);
   if (timing) cudaEventRecord(ev[1], st);
   // K3 level 1: depth sort of the visible Gaussians (4 LSD passes, first one compacts)
   const uint32_t n32 = (uint32_t)N;
@@ -460,7 +465,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
     n_keys_host = (size_t)K;
   }
   // K2: depth-ordered scan + emission of (tile, gid) keys
-  launch_emit(order, cnt + CNT_NVIS, n32, ctx->tiles, ctx->ell, dc.tiles_x, dc.tile_cull, ctx->ka, ctx->va,
+  launch_emit(order, cnt + CNT_NVIS, n32, ctx->tiles, ctx->ell, ctx->ell64, dc.tiles_x, dc.tile_cull, ctx->ka, ctx->va,
               (uint32_t)ctx->cap_k, cnt, ctx->st_emit, ++ctx->epoch, st);
   if (timing) cudaEventRecord(ev[3], st);
   // K3 level 2: stable tile passes
@@ -627,7 +632,7 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
       r[i].tiles = tl[i];
       if (!tl[i]) continue;
       float4 a = el[2 * i], b = el[2 * i + 1], p3 = pl[4 * i + 3];
-      r[i].vx = a.x; r[i].vy = a.y; r[i].cxx = a.z; r[i].cxy = a.w; r[i].cyy = b.x; r[i].k2 = b.y;
+      r[i].vx = a.x; r[i].vy = a.y; r[i].cxx = a.z; r[i].cxy = a.w; r[i].cyy = b.x; r[i].k2 = fabsf(b.y);
       memcpy(&r[i].depth, &dk[i], 4);
       r[i].rgb[0] = p3.y; r[i].rgb[1] = p3.z; r[i].rgb[2] = p3.w;
       uint32_t r0, r1;

@@ -104,40 +104,52 @@ __host__ __device__ __forceinline__ void matmul3(const T *A, const T *B, T *C) {
 // edge nearest to it.  Tiles whose closed x-range meets that extent are kept.
 // K1 (counting) and K2 (emission) call this same function, so counts and
 // emitted keys agree bit for bit.
-struct Ell {
-  float vx, vy, cxx, cxy, cyy, k2;
+// Precision: fp32 for ordinary Gaussians; "wide" Gaussians (sigma points more
+// than 2048 px from the principal point, e.g. edge-on splats grazing the near
+// plane) run the UT and this test in fp64 (EllT<double>), because fp32 pixel
+// coordinates there have an ulp above the 1e-3 px binning band.
+template <class Real>
+struct EllT {
+  Real vx, vy, cxx, cxy, cyy, k2;
   int x0, y0, x1, y1;  // clamped tile rectangle
 };
+using Ell = EllT<float>;
+using EllD = EllT<double>;
 
-__device__ __forceinline__ void row_span(const Ell &e, int ty, int tile_cull, int &lo, int &hi) {
+template <class Real>
+__device__ __forceinline__ void row_span(const EllT<Real> &e, int ty, int tile_cull, int &lo, int &hi) {
   if (tile_cull == 0) { lo = e.x0; hi = e.x1; return; }
-  float hy = sqrtf(e.k2 * e.cyy);
-  float a = fmaxf((float)(GUT_TILE * ty) - e.vy, -hy);
-  float b = fminf((float)(GUT_TILE * ty + GUT_TILE) - e.vy, hy);
+  const Real zero = 0, tile = GUT_TILE;
+  Real hy = sqrt(e.k2 * e.cyy);
+  Real a = fmax((Real)(GUT_TILE * ty) - e.vy, -hy);
+  Real b = fmin((Real)(GUT_TILE * ty + GUT_TILE) - e.vy, hy);
   if (a > b) { lo = 1; hi = 0; return; }
-  float hx = sqrtf(e.k2 * e.cxx);
-  float ystar = e.cxy * sqrtf(e.k2 / e.cxx);  // dy of the rightmost point (leftmost at -ystar)
-  float slope = e.cxy / e.cyy;
-  float cond = fmaxf(e.cxx - e.cxy * slope, 0.f);  // det / cyy
-  float xr, xl;
+  Real hx = sqrt(e.k2 * e.cxx);
+  Real ystar = e.cxy * sqrt(e.k2 / e.cxx);  // dy of the rightmost point (leftmost at -ystar)
+  Real slope = e.cxy / e.cyy;
+  Real cond = fmax(e.cxx - e.cxy * slope, zero);  // det / cyy
+  Real xr, xl;
   if (ystar >= a && ystar <= b) xr = hx;
   else {
-    float yy = ystar < a ? a : b;
-    xr = slope * yy + sqrtf(fmaxf(cond * (e.k2 - yy * yy / e.cyy), 0.f));
+    Real yy = ystar < a ? a : b;
+    xr = slope * yy + sqrt(fmax(cond * (e.k2 - yy * yy / e.cyy), zero));
   }
   if (-ystar >= a && -ystar <= b) xl = -hx;
   else {
-    float yy = -ystar < a ? a : b;
-    xl = slope * yy - sqrtf(fmaxf(cond * (e.k2 - yy * yy / e.cyy), 0.f));
+    Real yy = -ystar < a ? a : b;
+    xl = slope * yy - sqrt(fmax(cond * (e.k2 - yy * yy / e.cyy), zero));
   }
-  float XL = e.vx + xl, XR = e.vx + xr;
-  int l = (int)ceilf(XL * (1.f / GUT_TILE)) - 1;
-  int h = (int)floorf(XR * (1.f / GUT_TILE));
+  Real XL = e.vx + xl, XR = e.vx + xr;
+  XL = fmin(fmax(XL, (Real)-1e7), (Real)1e7);
+  XR = fmin(fmax(XR, (Real)-1e7), (Real)1e7);
+  int l = (int)ceil(XL / tile) - 1;
+  int h = (int)floor(XR / tile);
   lo = max(l, e.x0);
   hi = min(h, e.x1);
 }
 
-__device__ __forceinline__ int ell_tile_count(const Ell &e, int tile_cull) {
+template <class Real>
+__device__ __forceinline__ int ell_tile_count(const EllT<Real> &e, int tile_cull) {
   if (tile_cull == 0) return (e.x1 - e.x0 + 1) * (e.y1 - e.y0 + 1);
   int n = 0;
   for (int ty = e.y0; ty <= e.y1; ++ty) {

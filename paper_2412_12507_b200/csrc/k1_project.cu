@@ -165,7 +165,8 @@ __device__ __forceinline__ double shutter_coord_d(const DevCam &c, double du, do
   return fmin(fmax(r, 0.0), 1.0);
 }
 
-__device__ bool project_sigma_d(const DevCam &c, d3 y, d3 w, double &du, double &dv) {
+__device__ bool project_sigma_d(const DevCam &c, d3 y, d3 w, double &du, double &dv, double &t_out) {
+  t_out = 0.0;
   if (c.shutter == SH_GLOBAL) return project_cam_d(c, y, du, dv);
   const d3 ax = mkd(c.phi_axis[0], c.phi_axis[1], c.phi_axis[2]);
   auto at = [&](double t) {
@@ -188,34 +189,7 @@ __device__ bool project_sigma_d(const DevCam &c, d3 y, d3 w, double &du, double 
     if (!project_cam_d(c, at(t1), u1, v1)) return false;
     f1 = shutter_coord_d(c, u1, v1) - t1;
   }
-  du = u1; dv = v1;
-  return true;
-}
-
-// Eq. 9-10 in fp64 from the fp64 camera-frame centre and fp32 R, s
-__device__ __noinline__ bool ut_fp64(const DevCam &c, d3 y0d, const float *R, float4 sc, float &vx, float &vy,
-                                     float &cxx, float &cxy, float &cyy) {
-  const d3 w = mtv(c.R0, mkd(c.dc[0], c.dc[1], c.dc[2]));
-  const double sj[3] = {sc.x, sc.y, sc.z};
-  double du[7], dv[7];
-  bool ok = project_sigma_d(c, y0d, w, du[0], dv[0]);
-  for (int j = 0; j < 3 && ok; ++j) {
-    const d3 L = ((double)c.gamma * sj[j]) * mkd(R[j], R[3 + j], R[6 + j]);
-    const d3 Lc = mtv(c.R0, L);
-    ok = ok && project_sigma_d(c, y0d + Lc, w, du[1 + j], dv[1 + j]);
-    ok = ok && project_sigma_d(c, y0d - Lc, w, du[4 + j], dv[4 + j]);
-  }
-  if (!ok) return false;
-  double mx = c.wmu0 * du[0], my = c.wmu0 * dv[0];
-  for (int k = 1; k < 7; ++k) { mx += (double)c.wmui * du[k]; my += (double)c.wmui * dv[k]; }
-  double sxx = 0, sxy = 0, syy = 0;
-  for (int k = 0; k < 7; ++k) {
-    const double wk = k == 0 ? (double)c.wsig0 : (double)c.wsigi;
-    const double ax = du[k] - mx, ay = dv[k] - my;
-    sxx += wk * ax * ax; sxy += wk * ax * ay; syy += wk * ay * ay;
-  }
-  vx = (float)mx; vy = (float)my;
-  cxx = (float)(sxx + c.dilation); cxy = (float)sxy; cyy = (float)(syy + c.dilation);
+  du = u1; dv = v1; t_out = t1;
   return true;
 }
 
@@ -252,127 +226,62 @@ __device__ __forceinline__ f3 sh_colour(const float4 *sh, int64_t n, int64_t i, 
   return mk(fmaxf(r, 0.f), fmaxf(g, 0.f), fmaxf(b, 0.f));
 }
 
+// ---- shared tail of both K1 kernels: depth key, SH colour, blend payload,
+// packed ellipse record.  Returns the depth key.
 template <int DEG>
-__global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, uint32_t *__restrict__ dkey,
-                                                      uint32_t *__restrict__ tiles, float4 *__restrict__ ell,
-                                                      float4 *__restrict__ payload, uint32_t *counters) {
-  __shared__ uint32_t s_hist[4][256];
-  __shared__ unsigned long long s_k[8];
-  __shared__ uint32_t s_nv[8];
-  for (int j = threadIdx.x; j < 1024; j += 256) (&s_hist[0][0])[j] = 0;
-  __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
-  uint32_t my_tiles = 0, key = GUT_CULLED_KEY;
-  if (i < s.n) {
-    float4 po = __ldg(&s.pos_opa[i]), ro = __ldg(&s.rot[i]), sc = __ldg(&s.scale[i]);
-    float qn2 = ro.x * ro.x + ro.y * ro.y + ro.z * ro.z + ro.w * ro.w;
-    bool ok = isfinite(po.x) && isfinite(po.y) && isfinite(po.z) && isfinite(qn2) && qn2 > 0.f &&
-              sc.x > 0.f && sc.y > 0.f && sc.z > 0.f && isfinite(sc.x) && isfinite(sc.y) &&
-              isfinite(sc.z) && po.w > c.alpha_min && isfinite(po.w);
-    float du[7], dv[7], tt[7];
-    f3 y0;
-    d3 y0d;
-    float R[9];
-    f3 wv = mk(0.f, 0.f, 0.f);
-    if (ok) {
-      // O1: R(q) from the normalised quaternion (w,x,y,z), Eq. 2
-      float inv = 1.f / sqrtf(qn2);
-      float w = ro.x * inv, x = ro.y * inv, y = ro.z * inv, z = ro.w * inv;
-      R[0] = 1.f - 2.f * (y * y + z * z); R[1] = 2.f * (x * y - w * z); R[2] = 2.f * (x * z + w * y);
-      R[3] = 2.f * (x * y + w * z); R[4] = 1.f - 2.f * (x * x + z * z); R[5] = 2.f * (y * z - w * x);
-      R[6] = 2.f * (x * z - w * y); R[7] = 2.f * (y * z + w * x); R[8] = 1.f - 2.f * (x * x + y * y);
-      // camera-frame centre in fp64, sigma offsets gamma s_j R[:,j] rotated in fp32 (Eq. 6)
-      y0d = mtv(c.R0, mkd(po.x, po.y, po.z) - mkd(c.c0[0], c.c0[1], c.c0[2]));
-      y0 = tof(y0d);
-      wv = mtv(c.R0f, mk(c.dcf[0], c.dcf[1], c.dcf[2]));
-      float sj[3] = {sc.x, sc.y, sc.z};
-      ok = project_sigma(c, y0, wv, du[0], dv[0], tt[0]);
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        f3 L = (c.gamma * sj[j]) * mk(R[j], R[3 + j], R[6 + j]);
-        f3 Lc = mtv(c.R0f, L);
-        ok = ok && project_sigma(c, y0 + Lc, wv, du[1 + j], dv[1 + j], tt[1 + j]);
-        ok = ok && project_sigma(c, y0 - Lc, wv, du[4 + j], dv[4 + j], tt[4 + j]);
-      }
-    }
-    float vx = 0, vy = 0, cxx = 0, cxy = 0, cyy = 0, k2 = 0;
-    if (ok) {
-      // Eq. 9-10, then + dilation (reading R10)
-      vx = c.wmu0 * du[0] + c.wmui * (((du[1] + du[4]) + (du[2] + du[5])) + (du[3] + du[6]));
-      vy = c.wmu0 * dv[0] + c.wmui * (((dv[1] + dv[4]) + (dv[2] + dv[5])) + (dv[3] + dv[6]));
-      float ex = du[0] - vx, ey = dv[0] - vy;
-      cxx = c.wsig0 * ex * ex; cxy = c.wsig0 * ex * ey; cyy = c.wsig0 * ey * ey;
-      float sxx = 0, sxy = 0, syy = 0;
-#pragma unroll
-      for (int k = 1; k < 7; ++k) {
-        float ax = du[k] - vx, ay = dv[k] - vy;
-        sxx += ax * ax; sxy += ax * ay; syy += ay * ay;
-      }
-      cxx += c.wsigi * sxx + c.dilation;
-      cxy += c.wsigi * sxy;
-      cyy += c.wsigi * syy + c.dilation;
-      float mag = 0.f;
-#pragma unroll
-      for (int k = 0; k < 7; ++k) mag = fmaxf(mag, fmaxf(fabsf(du[k]), fabsf(dv[k])));
-      if (mag > 2048.f) ok = ut_fp64(c, y0d, R, sc, vx, vy, cxx, cxy, cyy);
-      float det = cxx * cyy - cxy * cxy;
-      ok = cxx > 0.f && cyy > 0.f && det > 0.f && isfinite(det);
-      // opacity-aware extent level (Alg. 1 l.3, reading R11)
-      k2 = 2.f * logf(po.w / c.alpha_min);
-      ok = ok && k2 > 0.f;
-    }
-    Ell e;
-    if (ok) {
-      float hx = sqrtf(k2 * cxx), hy = sqrtf(k2 * cyy);
-      e.vx = vx + c.cxf; e.vy = vy + c.cyf;
-      e.cxx = cxx; e.cxy = cxy; e.cyy = cyy; e.k2 = k2;
-      float fx0 = floorf(fminf(fmaxf((e.vx - hx) * (1.f / GUT_TILE), -1e6f), 1e6f));
-      float fx1 = floorf(fminf(fmaxf((e.vx + hx) * (1.f / GUT_TILE), -1e6f), 1e6f));
-      float fy0 = floorf(fminf(fmaxf((e.vy - hy) * (1.f / GUT_TILE), -1e6f), 1e6f));
-      float fy1 = floorf(fminf(fmaxf((e.vy + hy) * (1.f / GUT_TILE), -1e6f), 1e6f));
-      e.x0 = max((int)fx0, 0); e.x1 = min((int)fx1, c.tiles_x - 1);
-      e.y0 = max((int)fy0, 0); e.y1 = min((int)fy1, c.tiles_y - 1);
-      ok = e.x0 <= e.x1 && e.y0 <= e.y1;
-      if (ok) {
-        my_tiles = (uint32_t)ell_tile_count(e, c.tile_cull);
-        ok = my_tiles > 0;
-      }
-    }
-    if (ok) {
-      // depth key (reading R13): camera-frame distance of mu at its own time t0
-      double t0 = tt[0];
-      d3 dcw = mkd(c.dc[0], c.dc[1], c.dc[2]);
-      d3 yc = y0d - t0 * mtv(c.R0, dcw);
-      float depth = (float)sqrt(dot(yc, yc));
-      key = __float_as_uint(depth);
-      // colour (reading R18): SH at d = normalize(mu - c(t0))
-      d3 dw = mkd(po.x, po.y, po.z) - (mkd(c.c0[0], c.c0[1], c.c0[2]) + t0 * dcw);
-      double nd = sqrt(dot(dw, dw));
-      f3 dir = tof((1.0 / nd) * dw);
-      f3 rgb = sh_colour<DEG>(s.sh, s.n, i, dir);
-      ell[2 * i] = make_float4(e.vx, e.vy, e.cxx, e.cxy);
-      ell[2 * i + 1] = make_float4(e.cyy, e.k2, __uint_as_float((uint32_t)e.x0 | ((uint32_t)e.y0 << 16)),
-                                   __uint_as_float((uint32_t)e.x1 | ((uint32_t)e.y1 << 16)));
-      // blend payload: mu, sigma, M = diag(1/s) R^T (Eq. 11 o_g = M (o - mu)), rgb
-      float is0 = 1.f / sc.x, is1 = 1.f / sc.y, is2 = 1.f / sc.z;
-      payload[4 * i] = po;
-      payload[4 * i + 1] = make_float4(R[0] * is0, R[3] * is0, R[6] * is0, R[1] * is1);
-      payload[4 * i + 2] = make_float4(R[4] * is1, R[7] * is1, R[2] * is2, R[5] * is2);
-      payload[4 * i + 3] = make_float4(R[8] * is2, rgb.x, rgb.y, rgb.z);
-    } else {
-      my_tiles = 0;
-      key = GUT_CULLED_KEY;
-    }
-    dkey[i] = key;
-    tiles[i] = my_tiles;
-  }
+__device__ __forceinline__ uint32_t finish_gaussian(const DevCam &c, const SceneDev &s, int64_t i, float4 po,
+                                                    float4 sc, const float *R, d3 y0d, double t0, float4 e0,
+                                                    float4 e1, float4 *__restrict__ ell,
+                                                    float4 *__restrict__ payload) {
+  // depth key (reading R13): camera-frame distance of mu at its own time t0
+  const d3 dcw = mkd(c.dc[0], c.dc[1], c.dc[2]);
+  const d3 yc = y0d - t0 * mtv(c.R0, dcw);
+  const float depth = (float)sqrt(dot(yc, yc));
+  // colour (reading R18): SH at d = normalize(mu - c(t0))
+  const d3 dw = mkd(po.x, po.y, po.z) - (mkd(c.c0[0], c.c0[1], c.c0[2]) + t0 * dcw);
+  const double nd = sqrt(dot(dw, dw));
+  const f3 rgb = sh_colour<DEG>(s.sh, s.n, i, tof((1.0 / nd) * dw));
+  ell[2 * i] = e0;
+  ell[2 * i + 1] = e1;
+  // blend payload: mu, sigma, M = diag(1/s) R^T (Eq. 11 o_g = M (o - mu)), rgb
+  const float is0 = 1.f / sc.x, is1 = 1.f / sc.y, is2 = 1.f / sc.z;
+  payload[4 * i] = po;
+  payload[4 * i + 1] = make_float4(R[0] * is0, R[3] * is0, R[6] * is0, R[1] * is1);
+  payload[4 * i + 2] = make_float4(R[4] * is1, R[7] * is1, R[2] * is2, R[5] * is2);
+  payload[4 * i + 3] = make_float4(R[8] * is2, rgb.x, rgb.y, rgb.z);
+  return __float_as_uint(depth);
+}
+
+__device__ __forceinline__ bool load_gaussian(const DevCam &c, const SceneDev &s, int64_t i, float4 &po, float4 &sc,
+                                              float *R) {
+  po = __ldg(&s.pos_opa[i]);
+  const float4 ro = __ldg(&s.rot[i]);
+  sc = __ldg(&s.scale[i]);
+  const float qn2 = ro.x * ro.x + ro.y * ro.y + ro.z * ro.z + ro.w * ro.w;
+  const bool ok = isfinite(po.x) && isfinite(po.y) && isfinite(po.z) && isfinite(qn2) && qn2 > 0.f &&
+                  sc.x > 0.f && sc.y > 0.f && sc.z > 0.f && isfinite(sc.x) && isfinite(sc.y) &&
+                  isfinite(sc.z) && po.w > c.alpha_min && isfinite(po.w);
+  if (!ok) return false;
+  // O1: R(q) from the normalised quaternion (w,x,y,z), Eq. 2
+  const float inv = 1.f / sqrtf(qn2);
+  const float w = ro.x * inv, x = ro.y * inv, y = ro.z * inv, z = ro.w * inv;
+  R[0] = 1.f - 2.f * (y * y + z * z); R[1] = 2.f * (x * y - w * z); R[2] = 2.f * (x * z + w * y);
+  R[3] = 2.f * (x * y + w * z); R[4] = 1.f - 2.f * (x * x + z * z); R[5] = 2.f * (y * z - w * x);
+  R[6] = 2.f * (x * z - w * y); R[7] = 2.f * (y * z + w * x); R[8] = 1.f - 2.f * (x * x + y * y);
+  return true;
+}
+
+__device__ __forceinline__ uint32_t pack_rect(int x, int y) { return (uint32_t)x | ((uint32_t)y << 16); }
+
+// block-aggregated visible count, key total and depth-digit histograms
+__device__ __forceinline__ void k1_block_totals(uint32_t my_tiles, uint32_t key, uint32_t (*s_hist)[256],
+                                                unsigned long long *s_k, uint32_t *s_nv, uint32_t *counters) {
   if (my_tiles) {
     atomicAdd(&s_hist[0][key & 255u], 1u);
     atomicAdd(&s_hist[1][(key >> 8) & 255u], 1u);
     atomicAdd(&s_hist[2][(key >> 16) & 255u], 1u);
     atomicAdd(&s_hist[3][key >> 24], 1u);
   }
-  // block totals: visible count and K
   unsigned long long kk = my_tiles;
   uint32_t nv = my_tiles ? 1u : 0u;
 #pragma unroll
@@ -392,8 +301,192 @@ __global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, u
     }
   }
   for (int j = threadIdx.x; j < 1024; j += 256) {
-    uint32_t v = (&s_hist[0][0])[j];
+    const uint32_t v = (&s_hist[0][0])[j];
     if (v) atomicAdd(&counters[CNT_HIST_DEPTH + j], v);
+  }
+}
+
+// ---- K1 main (fp32): one thread per Gaussian
+template <int DEG>
+__global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, uint32_t *__restrict__ dkey,
+                                                         uint32_t *__restrict__ tiles, float4 *__restrict__ ell,
+                                                         float4 *__restrict__ payload, uint32_t *counters,
+                                                         uint32_t *__restrict__ deferred) {
+  __shared__ uint32_t s_hist[4][256];
+  __shared__ unsigned long long s_k[8];
+  __shared__ uint32_t s_nv[8];
+  for (int j = threadIdx.x; j < 1024; j += 256) (&s_hist[0][0])[j] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  uint32_t my_tiles = 0, key = GUT_CULLED_KEY;
+  if (i < s.n) {
+    float4 po, sc;
+    float R[9];
+    bool ok = load_gaussian(c, s, i, po, sc, R);
+    bool wide = false;
+    float du[7], dv[7], tt[7];
+    d3 y0d = mkd(0, 0, 0);
+    if (ok) {
+      // camera-frame centre in fp64, sigma offsets gamma s_j R[:,j] rotated in fp32 (Eq. 6)
+      y0d = mtv(c.R0, mkd(po.x, po.y, po.z) - mkd(c.c0[0], c.c0[1], c.c0[2]));
+      const f3 y0 = tof(y0d);
+      const f3 wv = mtv(c.R0f, mk(c.dcf[0], c.dcf[1], c.dcf[2]));
+      const float sj[3] = {sc.x, sc.y, sc.z};
+      ok = project_sigma(c, y0, wv, du[0], dv[0], tt[0]);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const f3 L = (c.gamma * sj[j]) * mk(R[j], R[3 + j], R[6 + j]);
+        const f3 Lc = mtv(c.R0f, L);
+        ok = ok && project_sigma(c, y0 + Lc, wv, du[1 + j], dv[1 + j], tt[1 + j]);
+        ok = ok && project_sigma(c, y0 - Lc, wv, du[4 + j], dv[4 + j], tt[4 + j]);
+      }
+    }
+    float vx = 0, vy = 0, cxx = 0, cxy = 0, cyy = 0, k2 = 0;
+    if (ok) {
+      float mag = 0.f;
+#pragma unroll
+      for (int k = 0; k < 7; ++k) mag = fmaxf(mag, fmaxf(fabsf(du[k]), fabsf(dv[k])));
+      if (mag > 2048.f) {  // far sigma points: redo this Gaussian in fp64 (project_wide_kernel)
+        wide = true;
+        ok = false;
+      }
+    }
+    if (ok) {
+      // Eq. 9-10, then + dilation (reading R10)
+      vx = c.wmu0 * du[0] + c.wmui * (((du[1] + du[4]) + (du[2] + du[5])) + (du[3] + du[6]));
+      vy = c.wmu0 * dv[0] + c.wmui * (((dv[1] + dv[4]) + (dv[2] + dv[5])) + (dv[3] + dv[6]));
+      const float ex = du[0] - vx, ey = dv[0] - vy;
+      cxx = c.wsig0 * ex * ex; cxy = c.wsig0 * ex * ey; cyy = c.wsig0 * ey * ey;
+      float sxx = 0, sxy = 0, syy = 0;
+#pragma unroll
+      for (int k = 1; k < 7; ++k) {
+        const float ax = du[k] - vx, ay = dv[k] - vy;
+        sxx += ax * ax; sxy += ax * ay; syy += ay * ay;
+      }
+      cxx += c.wsigi * sxx + c.dilation;
+      cxy += c.wsigi * sxy;
+      cyy += c.wsigi * syy + c.dilation;
+      const float det = cxx * cyy - cxy * cxy;
+      ok = cxx > 0.f && cyy > 0.f && det > 0.f && isfinite(det);
+      // opacity-aware extent level (Alg. 1 l.3, reading R11)
+      k2 = 2.f * logf(po.w / c.alpha_min);
+      ok = ok && k2 > 0.f;
+    }
+    Ell e;
+    if (ok) {
+      const float hx = sqrtf(k2 * cxx), hy = sqrtf(k2 * cyy);
+      e.vx = vx + c.cxf; e.vy = vy + c.cyf;
+      e.cxx = cxx; e.cxy = cxy; e.cyy = cyy; e.k2 = k2;
+      const float fx0 = floorf(fminf(fmaxf((e.vx - hx) * (1.f / GUT_TILE), -1e6f), 1e6f));
+      const float fx1 = floorf(fminf(fmaxf((e.vx + hx) * (1.f / GUT_TILE), -1e6f), 1e6f));
+      const float fy0 = floorf(fminf(fmaxf((e.vy - hy) * (1.f / GUT_TILE), -1e6f), 1e6f));
+      const float fy1 = floorf(fminf(fmaxf((e.vy + hy) * (1.f / GUT_TILE), -1e6f), 1e6f));
+      e.x0 = max((int)fx0, 0); e.x1 = min((int)fx1, c.tiles_x - 1);
+      e.y0 = max((int)fy0, 0); e.y1 = min((int)fy1, c.tiles_y - 1);
+      ok = e.x0 <= e.x1 && e.y0 <= e.y1;
+      if (ok) {
+        my_tiles = (uint32_t)ell_tile_count(e, c.tile_cull);
+        ok = my_tiles > 0;
+      }
+    }
+    if (ok) {
+      key = finish_gaussian<DEG>(c, s, i, po, sc, R, y0d, (double)tt[0],
+                                 make_float4(e.vx, e.vy, e.cxx, e.cxy),
+                                 make_float4(e.cyy, e.k2, __uint_as_float(pack_rect(e.x0, e.y0)),
+                                             __uint_as_float(pack_rect(e.x1, e.y1))),
+                                 ell, payload);
+    } else {
+      my_tiles = 0;
+      key = GUT_CULLED_KEY;
+    }
+    dkey[i] = key;
+    tiles[i] = my_tiles;
+    if (wide) deferred[atomicAdd(&counters[CNT_NDEFER], 1u)] = (uint32_t)i;
+  }
+  k1_block_totals(my_tiles, key, s_hist, s_k, s_nv, counters);
+}
+
+// ---- K1 wide (fp64 UT + fp64 ellipse) for the deferred Gaussians.  The packed
+// record stores -k2 as a flag; K2 then reads the fp64 ellipse from ell64.
+template <int DEG>
+__global__ __launch_bounds__(256) void project_wide_kernel(DevCam c, SceneDev s, uint32_t *__restrict__ dkey,
+                                                           uint32_t *__restrict__ tiles, float4 *__restrict__ ell,
+                                                           double2 *__restrict__ ell64,
+                                                           float4 *__restrict__ payload, uint32_t *counters,
+                                                           const uint32_t *__restrict__ deferred) {
+  __shared__ uint32_t s_hist[4][256];
+  __shared__ unsigned long long s_k[8];
+  __shared__ uint32_t s_nv[8];
+  const uint32_t nd = counters[CNT_NDEFER];
+  for (uint32_t base = blockIdx.x * 256; base < nd; base += gridDim.x * 256) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < 1024; j += 256) (&s_hist[0][0])[j] = 0;
+    __syncthreads();
+    uint32_t my_tiles = 0, key = GUT_CULLED_KEY;
+    const uint32_t q = base + threadIdx.x;
+    if (q < nd) {
+      const int64_t i = deferred[q];
+      float4 po, sc;
+      float R[9];
+      bool ok = load_gaussian(c, s, i, po, sc, R);
+      const d3 y0d = mtv(c.R0, mkd(po.x, po.y, po.z) - mkd(c.c0[0], c.c0[1], c.c0[2]));
+      const d3 w = mtv(c.R0, mkd(c.dc[0], c.dc[1], c.dc[2]));
+      const double sj[3] = {sc.x, sc.y, sc.z};
+      double du[7], dv[7], t0 = 0, tdummy;
+      ok = ok && project_sigma_d(c, y0d, w, du[0], dv[0], t0);
+      for (int j = 0; j < 3 && ok; ++j) {
+        const d3 Lc = mtv(c.R0, ((double)c.gamma * sj[j]) * mkd(R[j], R[3 + j], R[6 + j]));
+        ok = ok && project_sigma_d(c, y0d + Lc, w, du[1 + j], dv[1 + j], tdummy);
+        ok = ok && project_sigma_d(c, y0d - Lc, w, du[4 + j], dv[4 + j], tdummy);
+      }
+      EllD e;
+      if (ok) {
+        double mx = (double)c.wmu0 * du[0], my = (double)c.wmu0 * dv[0];
+        for (int k = 1; k < 7; ++k) { mx += (double)c.wmui * du[k]; my += (double)c.wmui * dv[k]; }
+        double sxx = 0, sxy = 0, syy = 0;
+        for (int k = 0; k < 7; ++k) {
+          const double wk = k == 0 ? (double)c.wsig0 : (double)c.wsigi;
+          const double ax = du[k] - mx, ay = dv[k] - my;
+          sxx += wk * ax * ax; sxy += wk * ax * ay; syy += wk * ay * ay;
+        }
+        e.cxx = sxx + c.dilation; e.cxy = sxy; e.cyy = syy + c.dilation;
+        const double det = e.cxx * e.cyy - e.cxy * e.cxy;
+        const float k2f = 2.f * logf(po.w / c.alpha_min);  // same value as the fp32 path / K5
+        e.k2 = k2f;
+        ok = e.cxx > 0 && e.cyy > 0 && det > 0 && isfinite(det) && k2f > 0.f;
+        if (ok) {
+          e.vx = mx + c.cx; e.vy = my + c.cy;
+          const double hx = sqrt(e.k2 * e.cxx), hy = sqrt(e.k2 * e.cyy);
+          const double fx0 = floor(fmin(fmax((e.vx - hx) / GUT_TILE, -1e9), 1e9));
+          const double fx1 = floor(fmin(fmax((e.vx + hx) / GUT_TILE, -1e9), 1e9));
+          const double fy0 = floor(fmin(fmax((e.vy - hy) / GUT_TILE, -1e9), 1e9));
+          const double fy1 = floor(fmin(fmax((e.vy + hy) / GUT_TILE, -1e9), 1e9));
+          e.x0 = (int)fmax(fx0, 0.0); e.x1 = (int)fmin(fx1, (double)(c.tiles_x - 1));
+          e.y0 = (int)fmax(fy0, 0.0); e.y1 = (int)fmin(fy1, (double)(c.tiles_y - 1));
+          ok = e.x0 <= e.x1 && e.y0 <= e.y1;
+          if (ok) {
+            my_tiles = (uint32_t)ell_tile_count(e, c.tile_cull);
+            ok = my_tiles > 0;
+          }
+        }
+      }
+      if (ok) {
+        ell64[3 * i] = make_double2(e.vx, e.vy);
+        ell64[3 * i + 1] = make_double2(e.cxx, e.cxy);
+        ell64[3 * i + 2] = make_double2(e.cyy, e.k2);
+        key = finish_gaussian<DEG>(c, s, i, po, sc, R, y0d, t0,
+                                   make_float4((float)e.vx, (float)e.vy, (float)e.cxx, (float)e.cxy),
+                                   make_float4((float)e.cyy, -(float)e.k2, __uint_as_float(pack_rect(e.x0, e.y0)),
+                                               __uint_as_float(pack_rect(e.x1, e.y1))),
+                                   ell, payload);
+      } else {
+        my_tiles = 0;
+        key = GUT_CULLED_KEY;
+      }
+      dkey[i] = key;
+      tiles[i] = my_tiles;
+    }
+    k1_block_totals(my_tiles, key, s_hist, s_k, s_nv, counters);
   }
 }
 
@@ -421,15 +514,29 @@ void launch_pack_scene(const float *means, const float *rots, const float *scale
   pack_scene_kernel<<<(unsigned)blocks, 256, 0, st>>>(means, rots, scales, opac, sh, s);
 }
 
+
 void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32_t *tiles, float4 *ell,
-                    float4 *payload, uint32_t *counters, cudaStream_t st) {
+                    double2 *ell64, float4 *payload, uint32_t *counters, uint32_t *deferred, cudaStream_t st) {
   if (s.n == 0) return;
-  unsigned blocks = (unsigned)((s.n + 255) / 256);
+  const unsigned blocks = (unsigned)((s.n + 255) / 256);
+  const unsigned wblocks = 32;  // grid-stride over the (few) deferred Gaussians
   switch (s.sh_degree) {
-    case 0: project_kernel<0><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters); break;
-    case 1: project_kernel<1><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters); break;
-    case 2: project_kernel<2><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters); break;
-    default: project_kernel<3><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters); break;
+    case 0:
+      project_kernel<0><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      project_wide_kernel<0><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
+      break;
+    case 1:
+      project_kernel<1><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      project_wide_kernel<1><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
+      break;
+    case 2:
+      project_kernel<2><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      project_wide_kernel<2><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
+      break;
+    default:
+      project_kernel<3><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      project_wide_kernel<3><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
+      break;
   }
 }
 

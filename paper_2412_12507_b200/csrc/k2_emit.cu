@@ -21,7 +21,8 @@ namespace gut {
 
 __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
     const uint32_t *__restrict__ order, const uint32_t *n_vis_p, const uint32_t *__restrict__ tiles,
-    const float4 *__restrict__ ell, int tiles_x, int tile_cull, uint32_t *__restrict__ out_tile,
+    const float4 *__restrict__ ell, const double2 *__restrict__ ell64, int tiles_x, int tile_cull,
+    uint32_t *__restrict__ out_tile,
     uint32_t *__restrict__ out_gid, uint32_t cap_k, uint32_t *counters, unsigned long long *status,
     uint32_t epoch) {
   __shared__ uint32_t s_incl[GUT_EMIT_PART];
@@ -93,12 +94,27 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
     uint32_t r0 = __float_as_uint(b.z), r1 = __float_as_uint(b.w);
     el.x0 = (int)(r0 & 0xFFFF); el.y0 = (int)(r0 >> 16); el.x1 = (int)(r1 & 0xFFFF); el.y1 = (int)(r1 >> 16);
     uint32_t tile = 0;
-    for (int ty = el.y0; ty <= el.y1; ++ty) {
-      int l, h;
-      row_span(el, ty, tile_cull, l, h);
-      uint32_t cnt = (uint32_t)max(h - l + 1, 0);
-      if (j < cnt) { tile = (uint32_t)(ty * tiles_x + l + (int)j); break; }
-      j -= cnt;
+    if (el.k2 >= 0.f) {
+      for (int ty = el.y0; ty <= el.y1; ++ty) {
+        int l, h;
+        row_span(el, ty, tile_cull, l, h);
+        uint32_t cnt = (uint32_t)max(h - l + 1, 0);
+        if (j < cnt) { tile = (uint32_t)(ty * tiles_x + l + (int)j); break; }
+        j -= cnt;
+      }
+    } else {  // "wide" Gaussian: fp64 ellipse written by the fp64 K1 kernel
+      const uint32_t g = s_gid[lo];
+      const double2 q0 = ell64[3 * g], q1 = ell64[3 * g + 1], q2 = ell64[3 * g + 2];
+      EllD ed;
+      ed.vx = q0.x; ed.vy = q0.y; ed.cxx = q1.x; ed.cxy = q1.y; ed.cyy = q2.x; ed.k2 = q2.y;
+      ed.x0 = el.x0; ed.y0 = el.y0; ed.x1 = el.x1; ed.y1 = el.y1;
+      for (int ty = ed.y0; ty <= ed.y1; ++ty) {
+        int l, h;
+        row_span(ed, ty, tile_cull, l, h);
+        uint32_t cnt = (uint32_t)max(h - l + 1, 0);
+        if (j < cnt) { tile = (uint32_t)(ty * tiles_x + l + (int)j); break; }
+        j -= cnt;
+      }
     }
     uint32_t pos = prefix + e;
     if (pos < cap_k) {
@@ -129,12 +145,13 @@ __global__ void ranges_kernel(const uint32_t *__restrict__ tile_sorted, const ui
 }
 
 void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper, const uint32_t *tiles,
-                 const float4 *ell, int tiles_x, int tile_cull, uint32_t *out_tile, uint32_t *out_gid,
+                 const float4 *ell, const double2 *ell64, int tiles_x, int tile_cull, uint32_t *out_tile,
+                 uint32_t *out_gid,
                  uint32_t cap_k, uint32_t *counters, unsigned long long *status, uint32_t epoch,
                  cudaStream_t st) {
   if (n_upper == 0) return;
   unsigned blocks = (n_upper + GUT_EMIT_PART - 1) / GUT_EMIT_PART;
-  emit_kernel<<<blocks, GUT_EMIT_THREADS, 0, st>>>(order, n_vis, tiles, ell, tiles_x, tile_cull, out_tile, out_gid,
+  emit_kernel<<<blocks, GUT_EMIT_THREADS, 0, st>>>(order, n_vis, tiles, ell, ell64, tiles_x, tile_cull, out_tile, out_gid,
                                                    cap_k, counters, status, epoch);
 }
 

@@ -334,7 +334,15 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
   float T = 1.f;
   if (PASS == 1 && s > 0 && valid) {
     const uint32_t first = item_idx - (uint32_t)s;  // items of a tile are contiguous
-    for (int q = 0; q < s; ++q) T *= __ldcg(&B.prod[(size_t)(first + q) * NT + tid]);
+    int q = 0;
+    for (; q + 8 <= s; q += 8) {  // 8 independent loads in flight, product in segment order
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(&B.prod[(size_t)(first + q + u) * NT + tid]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) T *= v[u];
+    }
+    for (; q < s; ++q) T *= __ldcg(&B.prod[(size_t)(first + q) * NT + tid]);
   }
   const bool active = valid && T >= c.t_min;
   bool done = !active;

@@ -27,6 +27,7 @@ enum : int {
   CNT_MAXLEN = 24,
   CNT_NITEMS = 26,         // blend work items (tile, segment)
   CNT_NPRE = 27,           // transmittance-prefix work items
+  CNT_NDEFER = 28,         // Gaussians deferred to the fp64 K1 kernel
   CNT_HIST_DEPTH = 32,     // 4 x 256
   CNT_HIST_TILE = 32 + 1024,  // 2 x 256
   CNT_WORDS = 32 + 1024 + 512
@@ -35,8 +36,10 @@ enum : int {
 void launch_pack_scene(const float *means, const float *rots, const float *scales, const float *opac,
                        const float *sh, SceneDev s, cudaStream_t st);
 
+// K1 (fp32) followed by the fp64 kernel for the deferred "wide" Gaussians;
+// ell64 [3 x double2 per Gaussian] holds their fp64 ellipse (record k2 < 0)
 void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32_t *tiles, float4 *ell,
-                    float4 *payload, uint32_t *counters, cudaStream_t st);
+                    double2 *ell64, float4 *payload, uint32_t *counters, uint32_t *deferred, cudaStream_t st);
 
 // one onesweep LSD pass over 8-bit digit `shift`; first = keys only, value = index,
 // items equal to GUT_CULLED_KEY dropped.  n_dev: device count (nullable, then n_host).
@@ -46,7 +49,7 @@ void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t
                       bool first, cudaStream_t st);
 
 void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper, const uint32_t *tiles,
-                 const float4 *ell, int tiles_x, int tile_cull, uint32_t *out_tile, uint32_t *out_gid,
+                 const float4 *ell, const double2 *ell64, int tiles_x, int tile_cull, uint32_t *out_tile, uint32_t *out_gid,
                  uint32_t cap_k, uint32_t *counters, unsigned long long *status, uint32_t epoch,
                  cudaStream_t st);
 

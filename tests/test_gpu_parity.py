@@ -40,13 +40,16 @@ def _proj_parity(scene, cam, g, o_proj, opt=OPT):
     np.testing.assert_array_equal(gp["tiles"][both], o_proj["tiles"][both])
     # binning geometry: mean and extent edges within half the 1e-3 px band,
     # covariance within 1e-3 relative (fp32 pixel coordinates)
-    assert np.abs(gp["vx"][both] - o_proj["vx"][both]).max(initial=0) < 5e-4
-    assert np.abs(gp["vy"][both] - o_proj["vy"][both]).max(initial=0) < 5e-4
+    # (the debug record is fp32: add its own representation error, 2 ulp, for
+    # the "wide" Gaussians whose fp64 ellipse sits far from the image)
+    for v in ("vx", "vy"):
+        tol = 5e-4 + 2 * np.spacing(np.abs(gp[v][both]).astype(np.float32)).astype(np.float64)
+        assert np.all(np.abs(gp[v][both] - o_proj[v][both]) < tol), v
     for f, h in (("cxx", "hx"), ("cyy", "hy")):
         rel = np.abs(gp[f][both] - o_proj[f][both]) / np.abs(o_proj[f][both])
         assert rel.max(initial=0) < 1e-3, f
         hg = np.sqrt(gp["k2"][both].astype(np.float64) * gp[f][both])
-        assert np.abs(hg - o_proj[h][both]).max(initial=0) < 5e-4, h
+        assert np.all(np.abs(hg - o_proj[h][both]) < 5e-4 + 4e-7 * o_proj[h][both]), h
     sc = np.sqrt(o_proj["cxx"][both] * o_proj["cyy"][both])
     assert (np.abs(gp["cxy"][both] - o_proj["cxy"][both]) / sc).max(initial=0) < 1e-3
     rel = np.abs(gp["depth"][both] - o_proj["depth"][both]) / o_proj["depth"][both]
