@@ -43,8 +43,9 @@ struct gut_context {
   // K5: ray LUT (cached per intrinsics for global shutter), blend work plan
   float4 *pix = nullptr;
   TileAnchor *anchors = nullptr;
-  uint32_t *seg_base = nullptr, *tile_done = nullptr, *items = nullptr, *items_pre = nullptr;
-  float *prod = nullptr, *part_t = nullptr;
+  uint32_t *seg_base = nullptr, *tile_done = nullptr;
+  unsigned long long *bstatus = nullptr;
+  float *part_t = nullptr;
   float4 *part_c = nullptr;
   size_t cap_items = 0;
   bool lut_valid = false;
@@ -141,9 +142,8 @@ static gut_status ensure_tiles(gut_context *ctx, size_t t) {
 static gut_status ensure_items(gut_context *ctx, size_t items) {
   if (items <= ctx->cap_items) return GUT_OK;
   size_t c = items + items / 8 + 64, dummy = 0;
-  CUDA_TRY(ctx, regrow(ctx->items, dummy, c));
-  CUDA_TRY(ctx, regrow(ctx->items_pre, dummy, c));
-  CUDA_TRY(ctx, regrow(ctx->prod, dummy, c * GUT_BLEND_THREADS));
+  CUDA_TRY(ctx, regrow(ctx->bstatus, dummy, c * GUT_BLEND_THREADS));
+  CUDA_TRY(ctx, cudaMemset(ctx->bstatus, 0, c * GUT_BLEND_THREADS * sizeof(unsigned long long)));
   CUDA_TRY(ctx, regrow(ctx->part_c, dummy, c * GUT_BLEND_THREADS));
   CUDA_TRY(ctx, regrow(ctx->part_t, dummy, c * GUT_BLEND_THREADS));
   ctx->cap_items = c;
@@ -310,7 +310,7 @@ void gut_context_destroy(gut_context *ctx) {
                 ctx->sb_k, ctx->sb_v,
                 ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->tile_work, ctx->img, ctx->st_depth,
                 ctx->st_emit, ctx->st_tile, ctx->counters, ctx->pix, ctx->anchors, ctx->seg_base,
-                ctx->tile_done, ctx->items, ctx->items_pre, ctx->prod, ctx->part_c, ctx->part_t};
+                ctx->tile_done, ctx->bstatus, ctx->part_c, ctx->part_t};
   for (void *p : ps) if (p) cudaFree(p);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
   for (auto &set : ctx->tsets)
@@ -508,14 +508,20 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   const size_t max_items = (size_t)dc.n_tiles + ctx->cap_k / (size_t)ctx->blend_seg + 2;
   if ((s = ensure_items(ctx, max_items)) != GUT_OK) return s;
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->tile_work, 0, (size_t)dc.n_tiles * sizeof(uint2), st));
-  launch_plan(ctx->ranges, dc.n_tiles, ctx->blend_seg, ctx->items, ctx->items_pre, ctx->seg_base, cnt, st);
+  launch_plan(ctx->ranges, dc.n_tiles, ctx->blend_seg, ctx->seg_base, cnt, st);
+  // blend look-back epochs live in 22 bits: clear the status words on wrap
+  uint32_t bepoch = ++ctx->epoch;
+  if ((bepoch & 0x3FFFFFu) == 0) {
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->bstatus, 0, ctx->cap_items * GUT_BLEND_THREADS * sizeof(unsigned long long), st));
+    bepoch = ++ctx->epoch;
+  }
   BlendBufs bb;
   bb.ranges = ctx->ranges; bb.gids = fv; bb.payload = ctx->payload; bb.pix = ctx->pix; bb.anchors = ctx->anchors;
-  bb.items = ctx->items; bb.items_pre = ctx->items_pre; bb.seg_base = ctx->seg_base;
-  bb.prod = ctx->prod; bb.part_c = ctx->part_c; bb.part_t = ctx->part_t; bb.tile_done = ctx->tile_done;
-  bb.tile_work = ctx->tile_work; bb.seg = ctx->blend_seg;
+  bb.seg_base = ctx->seg_base; bb.status = ctx->bstatus;
+  bb.part_c = ctx->part_c; bb.part_t = ctx->part_t; bb.tile_done = ctx->tile_done;
+  bb.tile_work = ctx->tile_work; bb.seg = ctx->blend_seg; bb.n_tiles = dc.n_tiles;
   bb.max_items = (uint32_t)max_items;
-  bb.max_pre = (uint32_t)(ctx->cap_k / (size_t)ctx->blend_seg + 1);
+  bb.epoch = bepoch;
   bb.rgb = rgb; bb.alpha = alpha; bb.depth = depth; bb.counters = cnt;
   launch_blend(dc, bb, st);
   if (timing) cudaEventRecord(ev[6], st);

@@ -369,7 +369,8 @@ __global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, u
       const float det = cxx * cyy - cxy * cxy;
       ok = cxx > 0.f && cyy > 0.f && det > 0.f && isfinite(det);
       // opacity-aware extent level (Alg. 1 l.3, reading R11)
-      k2 = 2.f * logf(po.w / c.alpha_min);
+      // k2 = 2 ln(sigma/alpha_min) via log1p: accurate when sigma is near alpha_min
+      k2 = 2.f * log1pf((po.w - c.alpha_min) / c.alpha_min);
       ok = ok && k2 > 0.f;
     }
     Ell e;
@@ -451,7 +452,7 @@ __global__ __launch_bounds__(256) void project_wide_kernel(DevCam c, SceneDev s,
         }
         e.cxx = sxx + c.dilation; e.cxy = sxy; e.cyy = syy + c.dilation;
         const double det = e.cxx * e.cyy - e.cxy * e.cxy;
-        const float k2f = 2.f * logf(po.w / c.alpha_min);  // same value as the fp32 path / K5
+        const float k2f = 2.f * log1pf((po.w - c.alpha_min) / c.alpha_min);  // same value as the fp32 path / K5
         e.k2 = k2f;
         ok = e.cxx > 0 && e.cyy > 0 && det > 0 && isfinite(det) && k2f > 0.f;
         if (ok) {

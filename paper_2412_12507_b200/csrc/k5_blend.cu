@@ -19,16 +19,20 @@
 // with k^2 = 2 ln(sigma / alpha_min) (alpha >= alpha_min <=> omega^2 <= k^2).
 //
 // Load balance: tile lists are split into segments of `seg` entries; every
-// (tile, segment) is one CTA.  Front-to-back blending needs the transmittance
-// at the segment start, so a first pass computes each non-final segment's
-// transmittance product P_s (cut to 0 once below T_min: termination then
-// happens no later than that segment); the blend pass starts segment s at
-// T = prod_{s'<s} P_s' and runs the exact per-pixel loop with termination.
-// When the product of the earlier segments is >= T_min no earlier entry can
-// have terminated the pixel (T is monotone), so the result equals the
-// sequential loop up to fp32 rounding of the products.  The last segment CTA
-// to finish a tile (atomic counter) sums the partial results in segment order
-// (deterministic) and writes the pixels.
+// (tile, segment) is one CTA, all running concurrently.  Front-to-back
+// blending is associative ((C1,T1) over (C2,T2) = (C1 + T1 C2, T1 T2)) except
+// for the termination rule, so each segment first runs speculatively from
+// T = 1 (exact for segment 0), publishes its per-pixel transmittance product
+// P_s and resolves the product of its predecessors T_pre by decoupled
+// look-back.  If the pixel survives the segment (no local termination and
+// T_pre P_s >= T_min) no entry of the segment can have terminated it in the
+// sequential loop (T is monotone) and its exact contribution is T_pre times
+// the speculative sums; otherwise the segment is re-run from T_pre with the
+// termination rule (each pixel re-runs at most the one segment where it
+// terminates).  Products travel as fixed-point -log2 sums so prefixes are
+// bitwise deterministic.  The last segment CTA of a tile (atomic counter)
+// sums the partial results in segment order (deterministic) and writes the
+// pixels.
 #include "launch.h"
 
 namespace gut {
@@ -212,146 +216,95 @@ void launch_rays(const DevCam &cam, float4 *pix, TileAnchor *anchors, cudaStream
 }
 
 // ---------------------------------------------------------------- plan
+// Per tile: S_t = max(1, ceil(len / seg)) segments; slots are numbered
+// tile-major (seg_base[t] + s).  Work order: all (t, 0) first, then the deeper
+// segments (t, s >= 1) tile-major; a CTA maps its ticket to (t, s).
 __global__ __launch_bounds__(1024) void plan_kernel(const uint2 *__restrict__ ranges, int n_tiles, int seg,
-                                                    uint32_t *__restrict__ items, uint32_t *__restrict__ items_pre,
                                                     uint32_t *__restrict__ seg_base, uint32_t *counters) {
-  __shared__ uint32_t s_w[2][32];
+  __shared__ uint32_t s_w[32];
   const int per = (n_tiles + 1023) / 1024;
   const int t0 = threadIdx.x * per, t1 = min(t0 + per, n_tiles);
-  uint32_t sa = 0, sb = 0;
+  uint32_t sa = 0;
   for (int t = t0; t < t1; ++t) {
     const uint2 r = ranges[t];
     const uint32_t len = r.y > r.x ? r.y - r.x : 0;
-    const uint32_t S = len == 0 ? 1 : (len + seg - 1) / seg;
-    sa += S;
-    sb += S - 1;
+    sa += len == 0 ? 1 : (len + seg - 1) / seg;
   }
-  // block exclusive scan of (sa, sb)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t xa = sa, xb = sb;
+  uint32_t xa = sa;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    uint32_t ya = __shfl_up_sync(0xffffffffu, xa, o), yb = __shfl_up_sync(0xffffffffu, xb, o);
-    if (lane >= o) { xa += ya; xb += yb; }
+    const uint32_t ya = __shfl_up_sync(0xffffffffu, xa, o);
+    if (lane >= o) xa += ya;
   }
-  if (lane == 31) { s_w[0][w] = xa; s_w[1][w] = xb; }
+  if (lane == 31) s_w[w] = xa;
   __syncthreads();
   if (w == 0) {
-    uint32_t ya = s_w[0][lane], yb = s_w[1][lane];
+    uint32_t ya = s_w[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      uint32_t za = __shfl_up_sync(0xffffffffu, ya, o), zb = __shfl_up_sync(0xffffffffu, yb, o);
-      if (lane >= o) { ya += za; yb += zb; }
+      const uint32_t za = __shfl_up_sync(0xffffffffu, ya, o);
+      if (lane >= o) ya += za;
     }
-    s_w[0][lane] = ya; s_w[1][lane] = yb;
+    s_w[lane] = ya;
   }
   __syncthreads();
-  uint32_t oa = (w > 0 ? s_w[0][w - 1] : 0) + xa - sa;
-  uint32_t ob = (w > 0 ? s_w[1][w - 1] : 0) + xb - sb;
+  uint32_t oa = (w > 0 ? s_w[w - 1] : 0) + xa - sa;
   for (int t = t0; t < t1; ++t) {
     const uint2 r = ranges[t];
     const uint32_t len = r.y > r.x ? r.y - r.x : 0;
-    const uint32_t S = len == 0 ? 1 : (len + seg - 1) / seg;
     seg_base[t] = oa;
-    for (uint32_t s = 0; s < S; ++s) items[oa + s] = (uint32_t)t | (s << 16);
-    for (uint32_t s = 0; s + 1 < S; ++s) items_pre[ob + s] = (uint32_t)t | (s << 16);
-    oa += S;
-    ob += S - 1;
+    oa += len == 0 ? 1 : (len + seg - 1) / seg;
   }
-  if (threadIdx.x == 1023) {
-    counters[CNT_NITEMS] = oa;
-    counters[CNT_NPRE] = ob;
-  }
+  if (threadIdx.x == 1023) counters[CNT_NITEMS] = oa;
 }
 
-void launch_plan(const uint2 *ranges, int n_tiles, int seg, uint32_t *items, uint32_t *items_pre,
-                 uint32_t *seg_base, uint32_t *counters, cudaStream_t st) {
-  plan_kernel<<<1, 1024, 0, st>>>(ranges, n_tiles, seg, items, items_pre, seg_base, counters);
+void launch_plan(const uint2 *ranges, int n_tiles, int seg, uint32_t *seg_base, uint32_t *counters,
+                 cudaStream_t st) {
+  plan_kernel<<<1, 1024, 0, st>>>(ranges, n_tiles, seg, seg_base, counters);
 }
 
 // ---------------------------------------------------------------- blend
-// PASS 0: transmittance product of a non-final segment; PASS 1: blend.
-template <int MODE, int PASS>
-__global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, BlendBufs B) {
+// Transmittance products travel between segments as fixed-point -log2 sums
+// (integer addition is associative, so prefixes are bitwise deterministic
+// whatever the look-back walk): L = round(-log2(P) 2^32), saturated at 2^36
+// (T = 2^-16 < T_min: "dead").  Status word: [63:62] flag (1 aggregate,
+// 2 inclusive), [61:40] epoch, [39:0] L.
+#define GUT_L_ONE 4294967296.0
+#define GUT_L_DEAD (16ull << 32)
+
+__device__ __forceinline__ unsigned long long l_of(float P) {
+  if (!(P > 0.f)) return GUT_L_DEAD;
+  const double l = -log2((double)P) * GUT_L_ONE;
+  return l >= (double)GUT_L_DEAD ? GUT_L_DEAD : (unsigned long long)llrint(l);
+}
+__device__ __forceinline__ float t_of(unsigned long long L) {
+  return L >= GUT_L_DEAD ? 0.f : (float)exp2(-(double)L / GUT_L_ONE);
+}
+__device__ __forceinline__ unsigned long long st_word(uint32_t flag, uint32_t epoch, unsigned long long L) {
+  return ((unsigned long long)flag << 62) | ((unsigned long long)(epoch & 0x3FFFFFu) << 40) | L;
+}
+
+// One pass over the segment [s0, s1): staging + warp cull + exact per-pixel
+// loop starting at transmittance T_start for active pixels.  Termination rule
+// (reading R21): stop before an entry would take T below T_min.
+template <int MODE>
+__device__ __forceinline__ void segment_pass(const DevCam &c, const BlendBufs &B, float4 *s_f, uint32_t s0,
+                                             uint32_t s1, const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f,
+                                             float a, float b, float beta, float snorm, float ac, float bc, float ra,
+                                             float rb, bool active, float T_start, float &Cr, float &Cg, float &Cb,
+                                             float &Dp, float &T, bool &term, uint32_t &n_eval, uint32_t &n_contrib,
+                                             uint32_t &processed) {
   constexpr int NF = MODE == 2 ? 11 : 8;
   constexpr int NT = GUT_BLEND_THREADS;
-  __shared__ float4 s_f[NF * NT];
-  __shared__ int s_last;
-
-  const uint32_t n_items = B.counters[PASS == 0 ? CNT_NPRE : CNT_NITEMS];
-  const uint32_t item_idx = blockIdx.x;
-  if (item_idx >= n_items) return;
-  const uint32_t item = (PASS == 0 ? B.items_pre : B.items)[item_idx];
-  const int tile = (int)(item & 0xFFFFu), s = (int)(item >> 16);
-  const uint2 rg = B.ranges[tile];
-  const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x, len = end - start;
-  const int S = len == 0 ? 1 : (int)((len + B.seg - 1) / B.seg);
-  const uint32_t s0 = start + (uint32_t)s * B.seg, s1 = min(s0 + (uint32_t)B.seg, end);
-  const int tid = threadIdx.x;
-  int px, py;
-  tile_pixel(tile, c.tiles_x, px, py);
-  const bool inside = px < c.width && py < c.height;
-
-  // ---- pixel ray (LUT) and the tile anchor in the world frame (fp64)
-  const float4 pl = B.pix[(size_t)tile * NT + tid];
-  const float a = pl.x, b = pl.y, snorm = pl.z, beta = pl.w;
-  const bool valid = inside && snorm > 0.f;
-  const int lane = tid & 31;
-  // warp pixel box in (a, b) for the conservative warp cull
-  float ac, bc, ra, rb;
-  {
-    float amin = valid ? a : 3e38f, amax = valid ? a : -3e38f;
-    float bmin = valid ? b : 3e38f, bmax = valid ? b : -3e38f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      amin = fminf(amin, __shfl_xor_sync(0xffffffffu, amin, o));
-      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-      bmin = fminf(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
-      bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
-    }
-    if (amin > amax) { amin = amax = 0.f; bmin = bmax = 0.f; }  // no valid pixel: warp is done anyway
-    ac = 0.5f * (amin + amax);
-    bc = 0.5f * (bmin + bmax);
-    ra = 0.5f * (amax - amin) + 1e-7f * (fabsf(amin) + fabsf(amax));
-    rb = 0.5f * (bmax - bmin) + 1e-7f * (fabsf(bmin) + fabsf(bmax));
-  }
-  const TileAnchor &A = B.anchors[tile];
-  d3 D, T1, T2, O;
-  if (MODE == 2) {
-    D = mkd(A.D[0], A.D[1], A.D[2]); T1 = mkd(A.T1[0], A.T1[1], A.T1[2]);
-    T2 = mkd(A.T2[0], A.T2[1], A.T2[2]); O = mkd(A.O[0], A.O[1], A.O[2]);
-  } else {
-    D = mv(c.R0, mkd(A.D[0], A.D[1], A.D[2]));
-    T1 = mv(c.R0, mkd(A.T1[0], A.T1[1], A.T1[2]));
-    T2 = mv(c.R0, mkd(A.T2[0], A.T2[1], A.T2[2]));
-    O = mkd(c.c0[0], c.c0[1], c.c0[2]);
-    if (MODE == 1) O = O + mv(c.R0, mkd(A.O[0], A.O[1], A.O[2]));
-  }
-  const f3 T1f = tof(T1), T2f = tof(T2);
-  const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
-
-  // ---- transmittance at the segment start
-  float T = 1.f;
-  if (PASS == 1 && s > 0 && valid) {
-    const uint32_t first = item_idx - (uint32_t)s;  // items of a tile are contiguous
-    int q = 0;
-    for (; q + 8 <= s; q += 8) {  // 8 independent loads in flight, product in segment order
-      float v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcg(&B.prod[(size_t)(first + q + u) * NT + tid]);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) T *= v[u];
-    }
-    for (; q < s; ++q) T *= __ldcg(&B.prod[(size_t)(first + q) * NT + tid]);
-  }
-  const bool active = valid && T >= c.t_min;
-  bool done = !active;
-  float Cr = 0.f, Cg = 0.f, Cb = 0.f, Dp = 0.f;
-  uint32_t n_eval = 0, n_contrib = 0, n_term = 0;
-  if (PASS == 1 && s == 0 && tid == 0 && len > 0) atomicMax(&B.counters[CNT_MAXLEN], len);
-
-  uint32_t processed = 0;
+  const int tid = threadIdx.x, lane = tid & 31;
   const float alpha_min = c.alpha_min, alpha_max = c.alpha_max, t_min = c.t_min;
+  const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
+  T = T_start;
+  Cr = Cg = Cb = Dp = 0.f;
+  term = false;
+  bool done = !active;
+  processed = 0;
   for (uint32_t b0 = s0; b0 < s1; b0 += NT) {
     const uint32_t cnt = min((uint32_t)NT, s1 - b0);
     __syncthreads();
@@ -375,7 +328,8 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
       } else {
         P = cross(ogf, U); Q = cross(ogf, V); gu = dot(ogf, U); gv = dot(ogf, V);
       }
-      const float k2 = 2.f * logf(p0.w / alpha_min);
+      // k^2 = 2 ln(sigma/alpha_min) via log1p (accurate for sigma near alpha_min)
+      const float k2 = 2.f * log1pf((p0.w - alpha_min) / alpha_min);
       const float l2s = log2f(p0.w);
       s_f[0 * NT + tid] = make_float4((float)c0.x, (float)c0.y, (float)c0.z, k2);
       s_f[1 * NT + tid] = make_float4(P.x, P.y, P.z, Q.x);
@@ -424,46 +378,44 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
         }
         uint32_t m = __ballot_sync(0xffffffffu, maybe);
         while (m) {
-        const uint32_t k = r0 + (uint32_t)(__ffs(m) - 1);
-        m &= m - 1;
-        if (done) continue;
-        ++n_eval;
-        const float4 f0 = sf[k], f1 = sf[NT + k], f2 = sf[2 * NT + k], f3v = sf[3 * NT + k], f4 = sf[4 * NT + k];
-        float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
-        float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
-        float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
-        if (MODE == 2) {
-          const float4 h = sf[(NF - 3) * NT + k], pu = sf[(NF - 2) * NT + k], qv = sf[(NF - 1) * NT + k];
-          nx = fmaf(beta, fmaf(a, pu.x, fmaf(b, qv.x, h.x)), nx);
-          ny = fmaf(beta, fmaf(a, pu.y, fmaf(b, qv.y, h.y)), ny);
-          nz = fmaf(beta, fmaf(a, pu.z, fmaf(b, qv.z, h.z)), nz);
-        }
-        const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
-        const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
-        const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
-        const float N = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
-        const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
-        if (N > f0.w * Dd) continue;  // omega^2 > k^2  <=>  alpha < alpha_min
-        const float rD = __frcp_rn(Dd);
-        const float w2 = N * rD;
-        const float al = fminf(alpha_max, exp2f(fmaf(-0.72134752044448170f, w2, f4.w)));
-        if (!(al >= alpha_min)) continue;
-        const float4 f5 = sf[5 * NT + k];
-        float gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
-        if (MODE == 2) {
-          const float4 h = sf[(NF - 3) * NT + k], pu = sf[(NF - 2) * NT + k], qv = sf[(NF - 1) * NT + k];
-          gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
-        }
-        const float tau = -gg * rD * snorm;
-        if (!(tau > 0.f)) continue;  // reading R24
-        const float Tn = T * (1.f - al);
-        if (Tn < t_min) {
-          done = true;
-          n_term = 1;
-          if (PASS == 0) T = 0.f;
-          continue;
-        }
-        if (PASS == 1) {
+          const uint32_t k = r0 + (uint32_t)(__ffs(m) - 1);
+          m &= m - 1;
+          if (done) continue;
+          ++n_eval;
+          const float4 f0 = sf[k], f1 = sf[NT + k], f2 = sf[2 * NT + k], f3v = sf[3 * NT + k], f4 = sf[4 * NT + k];
+          float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
+          float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
+          float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
+          if (MODE == 2) {
+            const float4 h = sf[(NF - 3) * NT + k], pu = sf[(NF - 2) * NT + k], qv = sf[(NF - 1) * NT + k];
+            nx = fmaf(beta, fmaf(a, pu.x, fmaf(b, qv.x, h.x)), nx);
+            ny = fmaf(beta, fmaf(a, pu.y, fmaf(b, qv.y, h.y)), ny);
+            nz = fmaf(beta, fmaf(a, pu.z, fmaf(b, qv.z, h.z)), nz);
+          }
+          const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
+          const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
+          const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
+          const float N = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
+          const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
+          if (N > f0.w * Dd) continue;  // omega^2 > k^2  <=>  alpha < alpha_min
+          const float rD = __frcp_rn(Dd);
+          const float w2 = N * rD;
+          const float al = fminf(alpha_max, exp2f(fmaf(-0.72134752044448170f, w2, f4.w)));
+          if (!(al >= alpha_min)) continue;
+          const float4 f5 = sf[5 * NT + k];
+          float gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
+          if (MODE == 2) {
+            const float4 h = sf[(NF - 3) * NT + k], pu = sf[(NF - 2) * NT + k], qv = sf[(NF - 1) * NT + k];
+            gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
+          }
+          const float tau = -gg * rD * snorm;
+          if (!(tau > 0.f)) continue;  // reading R24
+          const float Tn = T * (1.f - al);
+          if (Tn < t_min) {
+            done = true;
+            term = true;
+            continue;
+          }
           const float4 f6 = sf[6 * NT + k];
           const float wgt = al * T;
           Cr = fmaf(wgt, f6.x, Cr);
@@ -471,8 +423,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
           Cb = fmaf(wgt, f6.z, Cb);
           Dp = fmaf(wgt, tau, Dp);
           ++n_contrib;
-        }
-        T = Tn;
+          T = Tn;
         }
         if (__all_sync(0xffffffffu, done)) break;
       }
@@ -480,11 +431,139 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
     processed = b0 - s0 + cnt;
     if (__syncthreads_count(done) == NT) break;
   }
+}
 
-  if (PASS == 0) {
-    B.prod[(size_t)(B.seg_base[tile] + s) * NT + tid] = T;
-    return;
+template <int MODE>
+__global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, BlendBufs B) {
+  constexpr int NF = MODE == 2 ? 11 : 8;
+  constexpr int NT = GUT_BLEND_THREADS;
+  __shared__ float4 s_f[NF * NT];
+  __shared__ uint32_t s_ticket;
+  __shared__ int s_last;
+
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) s_ticket = atomicAdd(&B.counters[CNT_TICKET_BLEND], 1u);
+  __syncthreads();
+  const uint32_t ticket = s_ticket;
+  if (ticket >= B.counters[CNT_NITEMS]) return;
+  // ---- ticket -> (tile, segment): all segment-0 items first, then the rest tile-major
+  int tile, s;
+  if (ticket < (uint32_t)B.n_tiles) {
+    tile = (int)ticket;
+    s = 0;
+  } else {
+    const uint32_t q = ticket - (uint32_t)B.n_tiles;
+    int lo = 0, hi = B.n_tiles - 1;  // last t with seg_base[t] - t <= q
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (B.seg_base[mid] - (uint32_t)mid <= q) lo = mid; else hi = mid - 1;
+    }
+    tile = lo;
+    s = 1 + (int)(q - (B.seg_base[lo] - (uint32_t)lo));
   }
+  const uint2 rg = B.ranges[tile];
+  const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x, len = end - start;
+  const int S = len == 0 ? 1 : (int)((len + B.seg - 1) / B.seg);
+  const uint32_t s0 = start + (uint32_t)s * B.seg, s1 = min(s0 + (uint32_t)B.seg, end);
+  const uint32_t slot = B.seg_base[tile] + (uint32_t)s;
+  int px, py;
+  tile_pixel(tile, c.tiles_x, px, py);
+  const bool inside = px < c.width && py < c.height;
+
+  // ---- pixel ray (LUT) and the tile anchor in the world frame (fp64)
+  const float4 pl = B.pix[(size_t)tile * NT + tid];
+  const float a = pl.x, b = pl.y, snorm = pl.z, beta = pl.w;
+  const bool valid = inside && snorm > 0.f;
+  const TileAnchor &A = B.anchors[tile];
+  d3 D, T1, T2, O;
+  if (MODE == 2) {
+    D = mkd(A.D[0], A.D[1], A.D[2]); T1 = mkd(A.T1[0], A.T1[1], A.T1[2]);
+    T2 = mkd(A.T2[0], A.T2[1], A.T2[2]); O = mkd(A.O[0], A.O[1], A.O[2]);
+  } else {
+    D = mv(c.R0, mkd(A.D[0], A.D[1], A.D[2]));
+    T1 = mv(c.R0, mkd(A.T1[0], A.T1[1], A.T1[2]));
+    T2 = mv(c.R0, mkd(A.T2[0], A.T2[1], A.T2[2]));
+    O = mkd(c.c0[0], c.c0[1], c.c0[2]);
+    if (MODE == 1) O = O + mv(c.R0, mkd(A.O[0], A.O[1], A.O[2]));
+  }
+  const f3 T1f = tof(T1), T2f = tof(T2);
+  // warp pixel box in (a, b) for the conservative warp cull
+  float ac, bc, ra, rb;
+  {
+    float amin = valid ? a : 3e38f, amax = valid ? a : -3e38f;
+    float bmin = valid ? b : 3e38f, bmax = valid ? b : -3e38f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      amin = fminf(amin, __shfl_xor_sync(0xffffffffu, amin, o));
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      bmin = fminf(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+      bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+    }
+    if (amin > amax) { amin = amax = 0.f; bmin = bmax = 0.f; }  // no valid pixel: the warp is idle
+    ac = 0.5f * (amin + amax);
+    bc = 0.5f * (bmin + bmax);
+    ra = 0.5f * (amax - amin) + 1e-7f * (fabsf(amin) + fabsf(amax));
+    rb = 0.5f * (bmax - bmin) + 1e-7f * (fabsf(bmin) + fabsf(bmax));
+  }
+  if (s == 0 && tid == 0 && len > 0) atomicMax(&B.counters[CNT_MAXLEN], len);
+  unsigned long long *stat = B.status + (size_t)slot * NT + tid;
+
+  // ---- predecessor peek: pixels already known dead are skipped (same result)
+  bool run = valid;
+  if (s > 0 && valid) {
+    const unsigned long long wv = ld_relaxed(stat - NT);
+    if ((uint32_t)(wv >> 62) == 2u && (uint32_t)((wv >> 40) & 0x3FFFFFu) == (B.epoch & 0x3FFFFFu) &&
+        t_of(wv & ((1ull << 40) - 1)) < c.t_min)
+      run = false;
+  }
+  // ---- speculative pass: transmittance from 1 (exact for segment 0)
+  float Cr, Cg, Cb, Dp, Tsp;
+  bool term;
+  uint32_t n_eval = 0, n_contrib = 0, processed = 0, n_term = 0;
+  segment_pass<MODE>(c, B, s_f, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, run, 1.f, Cr, Cg,
+                     Cb, Dp, Tsp, term, n_eval, n_contrib, processed);
+  const unsigned long long Ls = term ? GUT_L_DEAD : l_of(Tsp);
+  float T_pre = 1.f;
+  bool alive_in = valid;
+  if (S > 1) {
+    unsigned long long Lpre = 0;
+    if (s == 0) {
+      if (valid) st_relaxed(stat, st_word(2, B.epoch, Ls));
+    } else if (valid) {
+      st_relaxed(stat, st_word(1, B.epoch, Ls));
+      // decoupled look-back over this pixel's earlier segments (integer sums)
+      for (int j = s - 1;; --j) {
+        const unsigned long long wv = ld_relaxed(stat - (size_t)(s - j) * NT);
+        const uint32_t flag = (uint32_t)(wv >> 62);
+        if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (B.epoch & 0x3FFFFFu)) { ++j; continue; }
+        Lpre += wv & ((1ull << 40) - 1);
+        if (Lpre >= GUT_L_DEAD) { Lpre = GUT_L_DEAD; break; }
+        if (flag == 2) break;
+      }
+      const unsigned long long Lin = Lpre + Ls >= GUT_L_DEAD ? GUT_L_DEAD : Lpre + Ls;
+      st_relaxed(stat, st_word(2, B.epoch, Lin));
+    }
+    T_pre = t_of(Lpre);
+    alive_in = valid && T_pre >= c.t_min;
+  }
+  // ---- exact result: scale the speculative sums, or redo the segment from T_pre
+  const bool redo = alive_in && s > 0 && (term || T_pre * Tsp < c.t_min);
+  float T_end = Tsp;
+  if (s > 0 && alive_in && !redo) {
+    Cr *= T_pre; Cg *= T_pre; Cb *= T_pre; Dp *= T_pre;
+    T_end = T_pre * Tsp;
+  }
+  if (__syncthreads_or(redo)) {
+    float r0, r1, r2, r3, rT;
+    bool rterm;
+    uint32_t e2 = 0, c2 = 0, p2 = 0;
+    segment_pass<MODE>(c, B, s_f, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, redo, T_pre, r0, r1,
+                       r2, r3, rT, rterm, e2, c2, p2);
+    if (redo) { Cr = r0; Cg = r1; Cb = r2; Dp = r3; T_end = rT; term = rterm; }
+    processed += p2;
+  }
+  n_term = (alive_in && term) ? 1u : 0u;
+
   // ---- statistics
   if (tid == 0) {
     atomicAdd(&B.tile_work[tile].y, processed);
@@ -501,18 +580,18 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
     }
   }
   // ---- outputs (single segment) or partials + deterministic in-order combine
-  float Tf = T;
+  float Tf = T_end;
   if (S > 1) {
-    const size_t j = (size_t)item_idx * NT + tid;
-    B.part_c[j] = make_float4(Cr, Cg, Cb, Dp);
-    B.part_t[j] = active ? T : -1.f;
+    const size_t j = (size_t)slot * NT + tid;
+    B.part_c[j] = alive_in ? make_float4(Cr, Cg, Cb, Dp) : make_float4(0.f, 0.f, 0.f, 0.f);
+    B.part_t[j] = alive_in ? T_end : -1.f;
     __threadfence();
     __syncthreads();
     if (tid == 0) s_last = atomicAdd(&B.tile_done[tile], 1u) == (uint32_t)(S - 1);
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    const uint32_t first = item_idx - (uint32_t)s;
+    const uint32_t first = B.seg_base[tile];
     Cr = Cg = Cb = Dp = 0.f;
     Tf = 1.f;
     for (int q = 0; q < S; ++q) {
@@ -542,16 +621,10 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
   }
 }
 
-template <int MODE>
-static void blend_mode(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
-  if (b.max_pre > 0) blend_kernel<MODE, 0><<<b.max_pre, GUT_BLEND_THREADS, 0, st>>>(cam, b);
-  blend_kernel<MODE, 1><<<b.max_items, GUT_BLEND_THREADS, 0, st>>>(cam, b);
-}
-
 void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
-  if (cam.model == CAM_ORTHO) blend_mode<1>(cam, b, st);
-  else if (cam.shutter != SH_GLOBAL) blend_mode<2>(cam, b, st);
-  else blend_mode<0>(cam, b, st);
+  if (cam.model == CAM_ORTHO) blend_kernel<1><<<b.max_items, GUT_BLEND_THREADS, 0, st>>>(cam, b);
+  else if (cam.shutter != SH_GLOBAL) blend_kernel<2><<<b.max_items, GUT_BLEND_THREADS, 0, st>>>(cam, b);
+  else blend_kernel<0><<<b.max_items, GUT_BLEND_THREADS, 0, st>>>(cam, b);
 }
 
 }  // namespace gut

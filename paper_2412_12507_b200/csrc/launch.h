@@ -28,6 +28,7 @@ enum : int {
   CNT_NITEMS = 26,         // blend work items (tile, segment)
   CNT_NPRE = 27,           // transmittance-prefix work items
   CNT_NDEFER = 28,         // Gaussians deferred to the fp64 K1 kernel
+  CNT_TICKET_BLEND = 29,   // blend work-item tickets
   CNT_HIST_DEPTH = 32,     // 4 x 256
   CNT_HIST_TILE = 32 + 1024,  // 2 x 256
   CNT_WORDS = 32 + 1024 + 512
@@ -66,8 +67,8 @@ struct TileAnchor {
 void launch_rays(const DevCam &cam, float4 *pix, TileAnchor *anchors, cudaStream_t st);
 
 // blend work plan: tiles split into segments of `seg` list entries
-void launch_plan(const uint2 *ranges, int n_tiles, int seg, uint32_t *items, uint32_t *items_pre,
-                 uint32_t *seg_base, uint32_t *counters, cudaStream_t st);
+void launch_plan(const uint2 *ranges, int n_tiles, int seg, uint32_t *seg_base, uint32_t *counters,
+                 cudaStream_t st);
 
 struct BlendBufs {
   const uint2 *ranges;
@@ -75,14 +76,14 @@ struct BlendBufs {
   const float4 *payload;
   const float4 *pix;
   const TileAnchor *anchors;
-  const uint32_t *items, *items_pre, *seg_base;
-  float *prod;       // per (item, pixel) transmittance product of a segment
-  float4 *part_c;    // per (item, pixel) partial colour + depth
-  float *part_t;     // per (item, pixel) transmittance at segment end (-1 inactive)
+  const uint32_t *seg_base;     // per tile: first (tile, segment) slot, tile-major
+  unsigned long long *status;   // per (slot, pixel) look-back word (flag | epoch | -log2 T)
+  float4 *part_c;    // per (slot, pixel) partial colour + depth
+  float *part_t;     // per (slot, pixel) transmittance at segment end (-1 inactive)
   uint32_t *tile_done;
   uint2 *tile_work;
-  int seg;
-  uint32_t max_items, max_pre;
+  int seg, n_tiles;
+  uint32_t max_items, epoch;
   float *rgb, *alpha, *depth;
   uint32_t *counters;
 };
