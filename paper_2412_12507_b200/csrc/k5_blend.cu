@@ -285,41 +285,53 @@ __device__ __forceinline__ unsigned long long st_word(uint32_t flag, uint32_t ep
   return ((unsigned long long)flag << 62) | ((unsigned long long)(epoch & 0x3FFFFFu) << 40) | L;
 }
 
-// One pass over the segment [s0, s1): staging + warp cull + exact per-pixel
-// loop starting at transmittance T_start for active pixels.  Termination rule
+// Per-warp table of staged list entries (32 per chunk).  MODE 0/1: the
+// quadratic forms of F = |n|^2 - k^2 |e|^2 and D = |e|^2 in the lane's pixel
+// offset (da, db) from the warp box centre; MODE 2 (rolling shutter, beta
+// varies per row): the raw anchored vectors.
+template <int MODE> struct WarpTbl { static constexpr int NF = 5; };
+template <> struct WarpTbl<2> { static constexpr int NF = 11; };
+
+// One pass of ONE WARP over the segment [s0, s1): no CTA barriers.  Each chunk
+// of 32 entries is staged by the 32 lanes (one entry each: fp64 for the
+// cancelling part), culled against the warp's pixel box in registers, and the
+// surviving entries are evaluated by every lane in list order.  The warp leaves
+// the list as soon as all its pixels have terminated.  Termination rule
 // (reading R21): stop before an entry would take T below T_min.
 template <int MODE>
-__device__ __forceinline__ void segment_pass(const DevCam &c, const BlendBufs &B, float4 *s_f, uint32_t s0,
-                                             uint32_t s1, const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f,
-                                             float a, float b, float beta, float snorm, float ac, float bc, float ra,
-                                             float rb, bool active, float T_start, float &Cr, float &Cg, float &Cb,
-                                             float &Dp, float &T, bool &term, uint32_t &n_eval, uint32_t &n_contrib,
-                                             uint32_t &processed) {
-  constexpr int NF = MODE == 2 ? 11 : 8;
-  constexpr int NT = GUT_BLEND_THREADS;
-  const int tid = threadIdx.x, lane = tid & 31;
+__device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, float4 *__restrict__ wt,
+                                          uint32_t s0, uint32_t s1, const d3 &D, const d3 &O, const f3 &T1f,
+                                          const f3 &T2f, float a, float b, float beta, float snorm, float ac, float bc,
+                                          float ra, float rb, bool active, float T_start, float &Cr, float &Cg,
+                                          float &Cb, float &Dp, float &T, bool &term, uint32_t &n_eval,
+                                          uint32_t &n_contrib, uint32_t &processed) {
+  constexpr int NF = WarpTbl<MODE>::NF;
+  const int lane = threadIdx.x & 31;
   const float alpha_min = c.alpha_min, alpha_max = c.alpha_max, t_min = c.t_min;
   const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
+  const float da = a - ac, db = b - bc;
   T = T_start;
   Cr = Cg = Cb = Dp = 0.f;
   term = false;
   bool done = !active;
   processed = 0;
-  for (uint32_t b0 = s0; b0 < s1; b0 += NT) {
-    const uint32_t cnt = min((uint32_t)NT, s1 - b0);
-    __syncthreads();
-    if ((uint32_t)tid < cnt) {
-      // ---- stage one list entry: fp64 for the cancelling part, fp32 for the rest
-      const uint32_t g = __ldg(&B.gids[b0 + tid]);
+  for (uint32_t b0 = s0; b0 < s1; b0 += 32) {
+    if (__all_sync(0xffffffffu, done)) break;
+    processed = min(b0 + 32, s1) - s0;
+    const uint32_t kk = b0 + (uint32_t)lane;
+    bool maybe = false;
+    if (kk < s1) {
+      // ---- stage entry kk: fp64 for the cancelling part, fp32 for the rest
+      const uint32_t g = __ldg(&B.gids[kk]);
       const float4 p0 = __ldg(&B.payload[4 * g]), p1 = __ldg(&B.payload[4 * g + 1]);
       const float4 p2 = __ldg(&B.payload[4 * g + 2]), p3 = __ldg(&B.payload[4 * g + 3]);
       const float M[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
       const double Md[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
       const d3 og = mv(Md, O - mkd(p0.x, p0.y, p0.z));
       const d3 e0d = mv(Md, D);
-      const d3 c0 = cross(og, e0d);
+      const d3 c0d = cross(og, e0d);
       const double g0 = dot(og, e0d);
-      const f3 ogf = tof(og), e0 = tof(e0d);
+      const f3 ogf = tof(og), e0 = tof(e0d), c0 = tof(c0d);
       f3 U = mv(M, T1f), V = mv(M, T2f), P, Q;
       float gu, gv;
       if (MODE == 1) {
@@ -331,113 +343,121 @@ __device__ __forceinline__ void segment_pass(const DevCam &c, const BlendBufs &B
       // k^2 = 2 ln(sigma/alpha_min) via log1p (accurate for sigma near alpha_min)
       const float k2 = 2.f * log1pf((p0.w - alpha_min) / alpha_min);
       const float l2s = log2f(p0.w);
-      s_f[0 * NT + tid] = make_float4((float)c0.x, (float)c0.y, (float)c0.z, k2);
-      s_f[1 * NT + tid] = make_float4(P.x, P.y, P.z, Q.x);
-      s_f[2 * NT + tid] = make_float4(Q.y, Q.z, e0.x, e0.y);
-      s_f[3 * NT + tid] = make_float4(e0.z, U.x, U.y, U.z);
-      s_f[4 * NT + tid] = make_float4(V.x, V.y, V.z, l2s);
-      s_f[5 * NT + tid] = make_float4((float)g0, gu, gv, 0.f);
-      s_f[6 * NT + tid] = make_float4(p3.y, p3.z, p3.w, 0.f);
-      s_f[7 * NT + tid] = make_float4(sqrtf(dot(P, P)), sqrtf(dot(Q, Q)), sqrtf(dot(U, U)), sqrtf(dot(V, V)));
+      // ---- conservative cull against the warp's pixel box (a in ac +- ra,
+      // b in bc +- rb): |n| >= |n(ac,bc)| - ra|P| - rb|Q|, |e| <= |e(ac,bc)| +
+      // ra|U| + rb|V| (triangle inequality); omega^2 > k^2 on the whole box if
+      // (|n0| - dn)^2 > k^2 (|e0| + de)^2 (1e-3 margin for fp32 rounding).
+      // Rolling shutter: every entry is kept.
+      const f3 n0 = c0 + ac * P + bc * Q;
+      const f3 e0c = e0 + ac * U + bc * V;
       if (MODE == 2) {
-        const f3 m = mv(M, dcw);
-        const f3 h = cross(m, e0), PU = cross(m, U), QV = cross(m, V);
-        s_f[(NF - 3) * NT + tid] = make_float4(h.x, h.y, h.z, dot(m, e0));
-        s_f[(NF - 2) * NT + tid] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
-        s_f[(NF - 1) * NT + tid] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
+        maybe = true;
+      } else {
+        const float lo = sqrtf(dot(n0, n0)) - (ra * sqrtf(dot(P, P)) + rb * sqrtf(dot(Q, Q)));
+        const float hi = sqrtf(dot(e0c, e0c)) + (ra * sqrtf(dot(U, U)) + rb * sqrtf(dot(V, V)));
+        maybe = !(lo > 0.f && lo * lo > 1.001f * k2 * (hi * hi));
+      }
+      if (maybe) {
+        float4 *t = wt + lane * NF;
+        if (MODE == 2) {
+          const f3 m = mv(M, dcw);
+          const f3 h = cross(m, e0), PU = cross(m, U), QV = cross(m, V);
+          t[0] = make_float4(c0.x, c0.y, c0.z, k2);
+          t[1] = make_float4(P.x, P.y, P.z, Q.x);
+          t[2] = make_float4(Q.y, Q.z, e0.x, e0.y);
+          t[3] = make_float4(e0.z, U.x, U.y, U.z);
+          t[4] = make_float4(V.x, V.y, V.z, l2s);
+          t[5] = make_float4((float)g0, gu, gv, 0.f);
+          t[6] = make_float4(p3.y, p3.z, p3.w, 0.f);
+          t[7] = make_float4(h.x, h.y, h.z, dot(m, e0));
+          t[8] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
+          t[9] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
+        } else {
+          // quadratic forms in the pixel offset (da, db) from the box centre
+          const float N0 = dot(n0, n0), Na = 2.f * dot(n0, P), Nb = 2.f * dot(n0, Q);
+          const float Naa = dot(P, P), Nab = 2.f * dot(P, Q), Nbb = dot(Q, Q);
+          const float D0 = dot(e0c, e0c), Da = 2.f * dot(e0c, U), Db = 2.f * dot(e0c, V);
+          const float Daa = dot(U, U), Dab = 2.f * dot(U, V), Dbb = dot(V, V);
+          const float gc = (float)g0 + ac * gu + bc * gv;
+          t[0] = make_float4(fmaf(-k2, D0, N0), fmaf(-k2, Da, Na), fmaf(-k2, Db, Nb), fmaf(-k2, Daa, Naa));
+          t[1] = make_float4(fmaf(-k2, Dab, Nab), fmaf(-k2, Dbb, Nbb), k2, l2s);
+          t[2] = make_float4(D0, Da, Db, Daa);
+          t[3] = make_float4(Dab, Dbb, gc, gu);
+          t[4] = make_float4(gv, p3.y, p3.z, p3.w);
+        }
       }
     }
-    __syncthreads();
-    if (!__all_sync(0xffffffffu, done)) {
-      const float4 *__restrict__ sf = s_f;
-      for (uint32_t r0 = 0; r0 < cnt; r0 += 32) {
-        // ---- per-warp conservative cull: lane j tests entry r0 + j against the
-        // warp's pixel box (a in ac +- ra, b in bc +- rb).  For every pixel of
-        // the box |n| >= |n(ac,bc)| - ra|P| - rb|Q| and |e| <= |e(ac,bc)| +
-        // ra|U| + rb|V| (triangle inequality), so omega^2 > k^2 for the whole
-        // box if (|n0| - dn)^2 > k^2 (|e0| + de)^2; 1e-3 relative margin for
-        // fp32 rounding.  Rolling shutter: no warp cull (every entry tested).
-        bool maybe = false;
-        const uint32_t kc = r0 + (uint32_t)lane;
-        if (kc < cnt) {
-          if (MODE == 2) {
-            maybe = true;
-          } else {
-            const float4 f0 = sf[kc], f1 = sf[NT + kc], f2 = sf[2 * NT + kc], f3v = sf[3 * NT + kc];
-            const float4 f4 = sf[4 * NT + kc], f7 = sf[7 * NT + kc];
-            const float nx = fmaf(ac, f1.x, fmaf(bc, f1.w, f0.x));
-            const float ny = fmaf(ac, f1.y, fmaf(bc, f2.x, f0.y));
-            const float nz = fmaf(ac, f1.z, fmaf(bc, f2.y, f0.z));
-            const float ex = fmaf(ac, f3v.y, fmaf(bc, f4.x, f2.z));
-            const float ey = fmaf(ac, f3v.z, fmaf(bc, f4.y, f2.w));
-            const float ez = fmaf(ac, f3v.w, fmaf(bc, f4.z, f3v.x));
-            const float lo = sqrtf(fmaf(nx, nx, fmaf(ny, ny, nz * nz))) - fmaf(ra, f7.x, rb * f7.y);
-            const float hi = sqrtf(fmaf(ex, ex, fmaf(ey, ey, ez * ez))) + fmaf(ra, f7.z, rb * f7.w);
-            maybe = !(lo > 0.f && lo * lo > 1.001f * f0.w * (hi * hi));
-          }
-        }
-        uint32_t m = __ballot_sync(0xffffffffu, maybe);
-        while (m) {
-          const uint32_t k = r0 + (uint32_t)(__ffs(m) - 1);
-          m &= m - 1;
-          if (done) continue;
-          ++n_eval;
-          const float4 f0 = sf[k], f1 = sf[NT + k], f2 = sf[2 * NT + k], f3v = sf[3 * NT + k], f4 = sf[4 * NT + k];
-          float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
-          float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
-          float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
-          if (MODE == 2) {
-            const float4 h = sf[(NF - 3) * NT + k], pu = sf[(NF - 2) * NT + k], qv = sf[(NF - 1) * NT + k];
-            nx = fmaf(beta, fmaf(a, pu.x, fmaf(b, qv.x, h.x)), nx);
-            ny = fmaf(beta, fmaf(a, pu.y, fmaf(b, qv.y, h.y)), ny);
-            nz = fmaf(beta, fmaf(a, pu.z, fmaf(b, qv.z, h.z)), nz);
-          }
-          const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
-          const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
-          const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
-          const float N = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
-          const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
-          if (N > f0.w * Dd) continue;  // omega^2 > k^2  <=>  alpha < alpha_min
-          const float rD = __frcp_rn(Dd);
-          const float w2 = N * rD;
-          const float al = fminf(alpha_max, exp2f(fmaf(-0.72134752044448170f, w2, f4.w)));
-          if (!(al >= alpha_min)) continue;
-          const float4 f5 = sf[5 * NT + k];
-          float gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
-          if (MODE == 2) {
-            const float4 h = sf[(NF - 3) * NT + k], pu = sf[(NF - 2) * NT + k], qv = sf[(NF - 1) * NT + k];
-            gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
-          }
-          const float tau = -gg * rD * snorm;
-          if (!(tau > 0.f)) continue;  // reading R24
-          const float Tn = T * (1.f - al);
-          if (Tn < t_min) {
-            done = true;
-            term = true;
-            continue;
-          }
-          const float4 f6 = sf[6 * NT + k];
-          const float wgt = al * T;
-          Cr = fmaf(wgt, f6.x, Cr);
-          Cg = fmaf(wgt, f6.y, Cg);
-          Cb = fmaf(wgt, f6.z, Cb);
-          Dp = fmaf(wgt, tau, Dp);
-          ++n_contrib;
-          T = Tn;
-        }
-        if (__all_sync(0xffffffffu, done)) break;
+    uint32_t m = __ballot_sync(0xffffffffu, maybe);
+    __syncwarp();
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      if (done) continue;
+      ++n_eval;
+      const float4 *t = wt + j * NF;
+      float w2, rD, gg, k2;
+      if (MODE == 2) {
+        const float4 f0 = t[0], f1 = t[1], f2 = t[2], f3v = t[3], f4 = t[4];
+        const float4 h = t[7], pu = t[8], qv = t[9];
+        float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
+        float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
+        float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
+        nx = fmaf(beta, fmaf(a, pu.x, fmaf(b, qv.x, h.x)), nx);
+        ny = fmaf(beta, fmaf(a, pu.y, fmaf(b, qv.y, h.y)), ny);
+        nz = fmaf(beta, fmaf(a, pu.z, fmaf(b, qv.z, h.z)), nz);
+        const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
+        const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
+        const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
+        const float N = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
+        const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
+        k2 = f0.w;
+        if (N > k2 * Dd) continue;  // omega^2 > k^2  <=>  alpha < alpha_min
+        rD = __frcp_rn(Dd);
+        w2 = N * rD;
+        const float4 f5 = t[5];
+        gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
+        gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
+      } else {
+        const float4 f0 = t[0], f1 = t[1];
+        // F = N - k^2 D <= 0  <=>  omega^2 <= k^2  <=>  alpha >= alpha_min
+        const float F = fmaf(da, fmaf(f0.w, da, fmaf(f1.x, db, f0.y)), fmaf(db, fmaf(f1.y, db, f0.z), f0.x));
+        if (F > 0.f) continue;
+        const float4 f2 = t[2], f3v = t[3];
+        const float Dd = fmaf(da, fmaf(f2.w, da, fmaf(f3v.x, db, f2.y)), fmaf(db, fmaf(f3v.y, db, f2.z), f2.x));
+        k2 = f1.z;
+        rD = __frcp_rn(Dd);
+        w2 = fmaxf(fmaf(k2, Dd, F), 0.f) * rD;
+        gg = fmaf(da, f3v.w, fmaf(db, t[4].x, f3v.z));
       }
+      const float l2s = MODE == 2 ? t[4].w : t[1].w;
+      const float al = fminf(alpha_max, exp2f(fmaf(-0.72134752044448170f, w2, l2s)));
+      if (!(al >= alpha_min)) continue;
+      const float tau = -gg * rD * snorm;
+      if (!(tau > 0.f)) continue;  // reading R24
+      const float Tn = T * (1.f - al);
+      if (Tn < t_min) {
+        done = true;
+        term = true;
+        continue;
+      }
+      const float4 cc = MODE == 2 ? t[6] : make_float4(t[4].y, t[4].z, t[4].w, 0.f);
+      const float wgt = al * T;
+      Cr = fmaf(wgt, cc.x, Cr);
+      Cg = fmaf(wgt, cc.y, Cg);
+      Cb = fmaf(wgt, cc.z, Cb);
+      Dp = fmaf(wgt, tau, Dp);
+      ++n_contrib;
+      T = Tn;
     }
-    processed = b0 - s0 + cnt;
-    if (__syncthreads_count(done) == NT) break;
+    __syncwarp();
   }
 }
 
 template <int MODE>
 __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, BlendBufs B) {
-  constexpr int NF = MODE == 2 ? 11 : 8;
+  constexpr int NF = WarpTbl<MODE>::NF;
   constexpr int NT = GUT_BLEND_THREADS;
-  __shared__ float4 s_f[NF * NT];
+  __shared__ float4 s_wt[(NT / 32) * 32 * NF];
   __shared__ uint32_t s_ticket;
   __shared__ int s_last;
 
@@ -520,7 +540,8 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
   float Cr, Cg, Cb, Dp, Tsp;
   bool term;
   uint32_t n_eval = 0, n_contrib = 0, processed = 0, n_term = 0;
-  segment_pass<MODE>(c, B, s_f, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, run, 1.f, Cr, Cg,
+  float4 *wt = s_wt + (tid >> 5) * 32 * NF;
+  warp_pass<MODE>(c, B, wt, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, run, 1.f, Cr, Cg,
                      Cb, Dp, Tsp, term, n_eval, n_contrib, processed);
   const unsigned long long Ls = term ? GUT_L_DEAD : l_of(Tsp);
   float T_pre = 1.f;
@@ -553,11 +574,11 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
     Cr *= T_pre; Cg *= T_pre; Cb *= T_pre; Dp *= T_pre;
     T_end = T_pre * Tsp;
   }
-  if (__syncthreads_or(redo)) {
+  if (__any_sync(0xffffffffu, redo)) {
     float r0, r1, r2, r3, rT;
     bool rterm;
     uint32_t e2 = 0, c2 = 0, p2 = 0;
-    segment_pass<MODE>(c, B, s_f, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, redo, T_pre, r0, r1,
+    warp_pass<MODE>(c, B, wt, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, redo, T_pre, r0, r1,
                        r2, r3, rT, rterm, e2, c2, p2);
     if (redo) { Cr = r0; Cg = r1; Cb = r2; Dp = r3; T_end = rT; term = rterm; }
     processed += p2;
