@@ -50,7 +50,7 @@ struct gut_context {
   size_t cap_items = 0;
   bool lut_valid = false;
   double lut_key[20] = {};
-  int blend_seg = 1024;
+  int blend_seg = 4096;
   uint32_t epoch = 0;
   bool reserved = false;
   std::vector<std::array<cudaEvent_t, 7>> tsets;  // per-render stage events (timing = 1)

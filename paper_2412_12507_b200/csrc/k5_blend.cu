@@ -289,7 +289,18 @@ __device__ __forceinline__ unsigned long long st_word(uint32_t flag, uint32_t ep
 // quadratic forms of F = |n|^2 - k^2 |e|^2 and D = |e|^2 in the lane's pixel
 // offset (da, db) from the warp box centre; MODE 2 (rolling shutter, beta
 // varies per row): the raw anchored vectors.
-template <int MODE> struct WarpTbl { static constexpr int NF = 5; };
+template <int MODE> struct WarpTbl { static constexpr int NF = 6; };
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 template <> struct WarpTbl<2> { static constexpr int NF = 11; };
 
 // One pass of ONE WARP over the segment [s0, s1): no CTA barriers.  Each chunk
@@ -299,17 +310,18 @@ template <> struct WarpTbl<2> { static constexpr int NF = 11; };
 // the list as soon as all its pixels have terminated.  Termination rule
 // (reading R21): stop before an entry would take T below T_min.
 template <int MODE>
-__device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, float4 *__restrict__ wt,
-                                          uint32_t s0, uint32_t s1, const d3 &D, const d3 &O, const f3 &T1f,
-                                          const f3 &T2f, float a, float b, float beta, float snorm, float ac, float bc,
-                                          float ra, float rb, bool active, float T_start, float &Cr, float &Cg,
-                                          float &Cb, float &Dp, float &T, bool &term, uint32_t &n_eval,
-                                          uint32_t &n_contrib, uint32_t &processed) {
+__device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, uint32_t s0, uint32_t s1,
+                                          const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f, float a, float b,
+                                          float beta, float snorm, float ac, float bc, float ra, float rb, bool active,
+                                          float T_start, float &Cr, float &Cg, float &Cb, float &Dp, float &T,
+                                          bool &term, uint32_t &n_eval, uint32_t &n_contrib, uint32_t &processed) {
   constexpr int NF = WarpTbl<MODE>::NF;
+  // per-warp entry table (function-scope shared array: one per CTA)
+  __shared__ float4 s_wt[(GUT_BLEND_THREADS / 32) * 32 * NF];
+  float4 *__restrict__ wt = s_wt + (threadIdx.x >> 5) * 32 * NF;
   const int lane = threadIdx.x & 31;
   const float alpha_min = c.alpha_min, alpha_max = c.alpha_max, t_min = c.t_min;
   const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
-  const float da = a - ac, db = b - bc;
   T = T_start;
   Cr = Cg = Cb = Dp = 0.f;
   term = false;
@@ -373,17 +385,35 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, f
           t[8] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
           t[9] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
         } else {
-          // quadratic forms in the pixel offset (da, db) from the box centre
-          const float N0 = dot(n0, n0), Na = 2.f * dot(n0, P), Nb = 2.f * dot(n0, Q);
-          const float Naa = dot(P, P), Nab = 2.f * dot(P, Q), Nbb = dot(Q, Q);
-          const float D0 = dot(e0c, e0c), Da = 2.f * dot(e0c, U), Db = 2.f * dot(e0c, V);
+          // Quadratic forms of F = |n|^2 - k^2 |e|^2 and D = |e|^2 in the pixel
+          // offset (da, db) from an expansion point (a*, b*): the box point
+          // nearest the Gaussian (minimiser of |n|^2, clamped to the box), so
+          // the coefficients' rounding stays relative to the values at the
+          // pixels (expanding about the box centre would cost eps * omega_c^2
+          // for Gaussians far smaller than the box).
+          const float pp = dot(P, P), pq = dot(P, Q), qq = dot(Q, Q);
+          const float np = dot(n0, P), nq = dot(n0, Q);
+          const float det = fmaf(pp, qq, -pq * pq);
+          float xa = 0.f, xb = 0.f;
+          if (det > 1e-30f * pp * qq && det > 0.f) {
+            const float id = 1.f / det;
+            xa = (pq * nq - qq * np) * id;
+            xb = (pq * np - pp * nq) * id;
+          }
+          const float as = ac + fminf(fmaxf(xa, -ra), ra), bs = bc + fminf(fmaxf(xb, -rb), rb);
+          const f3 ns = c0 + as * P + bs * Q;
+          const f3 es = e0 + as * U + bs * V;
+          const float N0 = dot(ns, ns), Na = 2.f * dot(ns, P), Nb = 2.f * dot(ns, Q);
+          const float Nab = 2.f * pq;
+          const float D0 = dot(es, es), Da = 2.f * dot(es, U), Db = 2.f * dot(es, V);
           const float Daa = dot(U, U), Dab = 2.f * dot(U, V), Dbb = dot(V, V);
-          const float gc = (float)g0 + ac * gu + bc * gv;
-          t[0] = make_float4(fmaf(-k2, D0, N0), fmaf(-k2, Da, Na), fmaf(-k2, Db, Nb), fmaf(-k2, Daa, Naa));
-          t[1] = make_float4(fmaf(-k2, Dab, Nab), fmaf(-k2, Dbb, Nbb), k2, l2s);
+          const float gs = (float)g0 + as * gu + bs * gv;
+          t[0] = make_float4(fmaf(-k2, D0, N0), fmaf(-k2, Da, Na), fmaf(-k2, Db, Nb), fmaf(-k2, Daa, pp));
+          t[1] = make_float4(fmaf(-k2, Dab, Nab), fmaf(-k2, Dbb, qq), as, bs);
           t[2] = make_float4(D0, Da, Db, Daa);
-          t[3] = make_float4(Dab, Dbb, gc, gu);
-          t[4] = make_float4(gv, p3.y, p3.z, p3.w);
+          t[3] = make_float4(Dab, Dbb, gs, gu);
+          t[4] = make_float4(gv, k2, l2s, 0.f);
+          t[5] = make_float4(p3.y, p3.z, p3.w, 0.f);
         }
       }
     }
@@ -412,25 +442,27 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, f
         const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
         k2 = f0.w;
         if (N > k2 * Dd) continue;  // omega^2 > k^2  <=>  alpha < alpha_min
-        rD = __frcp_rn(Dd);
+        rD = rcp_approx(Dd);
         w2 = N * rD;
         const float4 f5 = t[5];
         gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
         gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
       } else {
         const float4 f0 = t[0], f1 = t[1];
+        const float da = a - f1.z, db = b - f1.w;
         // F = N - k^2 D <= 0  <=>  omega^2 <= k^2  <=>  alpha >= alpha_min
         const float F = fmaf(da, fmaf(f0.w, da, fmaf(f1.x, db, f0.y)), fmaf(db, fmaf(f1.y, db, f0.z), f0.x));
         if (F > 0.f) continue;
-        const float4 f2 = t[2], f3v = t[3];
+        const float4 f2 = t[2], f3v = t[3], f4 = t[4];
         const float Dd = fmaf(da, fmaf(f2.w, da, fmaf(f3v.x, db, f2.y)), fmaf(db, fmaf(f3v.y, db, f2.z), f2.x));
-        k2 = f1.z;
-        rD = __frcp_rn(Dd);
+        k2 = f4.y;
+        rD = rcp_approx(Dd);
         w2 = fmaxf(fmaf(k2, Dd, F), 0.f) * rD;
-        gg = fmaf(da, f3v.w, fmaf(db, t[4].x, f3v.z));
+        gg = fmaf(da, f3v.w, fmaf(db, f4.x, f3v.z));
       }
-      const float l2s = MODE == 2 ? t[4].w : t[1].w;
-      const float al = fminf(alpha_max, exp2f(fmaf(-0.72134752044448170f, w2, l2s)));
+      const float l2s = MODE == 2 ? t[4].w : t[4].z;
+      // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
+      const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, l2s)));
       if (!(al >= alpha_min)) continue;
       const float tau = -gg * rD * snorm;
       if (!(tau > 0.f)) continue;  // reading R24
@@ -440,7 +472,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, f
         term = true;
         continue;
       }
-      const float4 cc = MODE == 2 ? t[6] : make_float4(t[4].y, t[4].z, t[4].w, 0.f);
+      const float4 cc = MODE == 2 ? t[6] : t[5];
       const float wgt = al * T;
       Cr = fmaf(wgt, cc.x, Cr);
       Cg = fmaf(wgt, cc.y, Cg);
@@ -457,7 +489,6 @@ template <int MODE>
 __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, BlendBufs B) {
   constexpr int NF = WarpTbl<MODE>::NF;
   constexpr int NT = GUT_BLEND_THREADS;
-  __shared__ float4 s_wt[(NT / 32) * 32 * NF];
   __shared__ uint32_t s_ticket;
   __shared__ int s_last;
 
@@ -540,8 +571,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
   float Cr, Cg, Cb, Dp, Tsp;
   bool term;
   uint32_t n_eval = 0, n_contrib = 0, processed = 0, n_term = 0;
-  float4 *wt = s_wt + (tid >> 5) * 32 * NF;
-  warp_pass<MODE>(c, B, wt, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, run, 1.f, Cr, Cg,
+  warp_pass<MODE>(c, B, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, run, 1.f, Cr, Cg,
                      Cb, Dp, Tsp, term, n_eval, n_contrib, processed);
   const unsigned long long Ls = term ? GUT_L_DEAD : l_of(Tsp);
   float T_pre = 1.f;
@@ -578,7 +608,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
     float r0, r1, r2, r3, rT;
     bool rterm;
     uint32_t e2 = 0, c2 = 0, p2 = 0;
-    warp_pass<MODE>(c, B, wt, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, redo, T_pre, r0, r1,
+    warp_pass<MODE>(c, B, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, redo, T_pre, r0, r1,
                        r2, r3, rT, rterm, e2, c2, p2);
     if (redo) { Cr = r0; Cg = r1; Cb = r2; Dp = r3; T_end = rT; term = rterm; }
     processed += p2;
