@@ -296,6 +296,13 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -316,27 +323,52 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
                                           float T_start, float &Cr, float &Cg, float &Cb, float &Dp, float &T,
                                           bool &term, uint32_t &n_eval, uint32_t &n_contrib, uint32_t &processed) {
   constexpr int NF = WarpTbl<MODE>::NF;
-  // per-warp entry table (function-scope shared array: one per CTA)
-  __shared__ float4 s_wt[(GUT_BLEND_THREADS / 32) * 32 * NF];
-  float4 *__restrict__ wt = s_wt + (threadIdx.x >> 5) * 32 * NF;
+  // dynamic shared memory: [raw payload double buffer: 8 warps x 2 x 32 x 4]
+  // [per-warp entry table: 8 warps x 32 x NF]
+  extern __shared__ float4 s_dyn[];
+  constexpr int RAW = (GUT_BLEND_THREADS / 32) * 2 * 32 * 4;
+  float4 *__restrict__ wt = s_dyn + RAW + (threadIdx.x >> 5) * 32 * NF;
   const int lane = threadIdx.x & 31;
   const float alpha_min = c.alpha_min, alpha_max = c.alpha_max, t_min = c.t_min;
   const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
+  // raw payload of the warp's current / next chunk (cp.async double buffer)
+  float4 *__restrict__ raw = s_dyn + (threadIdx.x >> 5) * 2 * 32 * 4;
   T = T_start;
   Cr = Cg = Cb = Dp = 0.f;
   term = false;
   bool done = !active;
   processed = 0;
-  for (uint32_t b0 = s0; b0 < s1; b0 += 32) {
+  if (__all_sync(0xffffffffu, done) || s0 >= s1) return;
+  // gathers run one chunk ahead (cp.async), Gaussian ids two chunks ahead
+  uint32_t gnext = s0 + lane < s1 ? __ldg(&B.gids[s0 + lane]) : 0u;
+  if (s0 + lane < s1) {
+    float4 *dst = raw + lane * 4;
+    for (int q = 0; q < 4; ++q) cp_async16(dst + q, &B.payload[4 * gnext + q]);
+  }
+  cp_async_commit();
+  gnext = s0 + 32 + lane < s1 ? __ldg(&B.gids[s0 + 32 + lane]) : 0u;
+  int buf = 0;
+  for (uint32_t b0 = s0; b0 < s1; b0 += 32, buf ^= 1) {
     if (__all_sync(0xffffffffu, done)) break;
+    if (b0 + 32 < s1) {  // prefetch the next chunk
+      if (b0 + 32 + lane < s1) {
+        float4 *dst = raw + ((buf ^ 1) * 32 + lane) * 4;
+        for (int q = 0; q < 4; ++q) cp_async16(dst + q, &B.payload[4 * gnext + q]);
+      }
+      cp_async_commit();
+      gnext = b0 + 64 + lane < s1 ? __ldg(&B.gids[b0 + 64 + lane]) : 0u;
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
     processed = min(b0 + 32, s1) - s0;
     const uint32_t kk = b0 + (uint32_t)lane;
     bool maybe = false;
     if (kk < s1) {
       // ---- stage entry kk: fp64 for the cancelling part, fp32 for the rest
-      const uint32_t g = __ldg(&B.gids[kk]);
-      const float4 p0 = __ldg(&B.payload[4 * g]), p1 = __ldg(&B.payload[4 * g + 1]);
-      const float4 p2 = __ldg(&B.payload[4 * g + 2]), p3 = __ldg(&B.payload[4 * g + 3]);
+      const float4 *src = raw + (buf * 32 + lane) * 4;
+      const float4 p0 = src[0], p1 = src[1], p2 = src[2], p3 = src[3];
       const float M[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
       const double Md[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
       const d3 og = mv(Md, O - mkd(p0.x, p0.y, p0.z));
@@ -483,6 +515,8 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
     }
     __syncwarp();
   }
+  cp_async_wait<0>();  // a warp leaving early must not leave copies in flight
+  __syncwarp();
 }
 
 template <int MODE>
@@ -672,10 +706,22 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
   }
 }
 
+template <int MODE>
+static void blend_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
+  constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_THREADS / 32) * 2 * 32 * 4 +
+                                            (GUT_BLEND_THREADS / 32) * 32 * WarpTbl<MODE>::NF);
+  static bool configured = false;  // per template instance; the attribute is per device function
+  if (!configured) {
+    cudaFuncSetAttribute(blend_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  blend_kernel<MODE><<<b.max_items, GUT_BLEND_THREADS, smem, st>>>(cam, b);
+}
+
 void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
-  if (cam.model == CAM_ORTHO) blend_kernel<1><<<b.max_items, GUT_BLEND_THREADS, 0, st>>>(cam, b);
-  else if (cam.shutter != SH_GLOBAL) blend_kernel<2><<<b.max_items, GUT_BLEND_THREADS, 0, st>>>(cam, b);
-  else blend_kernel<0><<<b.max_items, GUT_BLEND_THREADS, 0, st>>>(cam, b);
+  if (cam.model == CAM_ORTHO) blend_launch<1>(cam, b, st);
+  else if (cam.shutter != SH_GLOBAL) blend_launch<2>(cam, b, st);
+  else blend_launch<0>(cam, b, st);
 }
 
 }  // namespace gut
