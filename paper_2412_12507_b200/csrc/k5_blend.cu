@@ -285,167 +285,195 @@ __device__ __forceinline__ unsigned long long st_word(uint32_t flag, uint32_t ep
   return ((unsigned long long)flag << 62) | ((unsigned long long)(epoch & 0x3FFFFFu) << 40) | L;
 }
 
-// Per-warp table of staged list entries (32 per chunk).  MODE 0/1: the
-// quadratic forms of F = |n|^2 - k^2 |e|^2 and D = |e|^2 in the lane's pixel
-// offset (da, db) from the warp box centre; MODE 2 (rolling shutter, beta
-// varies per row): the raw anchored vectors.
-template <int MODE> struct WarpTbl { static constexpr int NF = 6; };
+// ---- shared-memory layout of a blend CTA (dynamic, float4 units)
+//   ctrl : ready[8] claim[8] pos[8] (ints)                  8 float4
+//   ring : 8 slots x 32 entries x SF float4 (staged entries, shared by the warps)
+//   tbl  : 8 warps x 32 x NF float4 (per-warp quadratic forms, MODE 0/1)
+// A list chunk (32 consecutive entries) is staged ONCE per CTA, by whichever
+// warp needs it first, into ring slot chunk % 8; a slot is reused only after
+// every live warp has consumed its previous chunk.  No CTA-wide barrier: warps
+// drift up to 8 chunks apart and leave as soon as their pixels terminate.
+#define GUT_RING 8
+template <int MODE> struct BlendLayout {
+  static constexpr int SF = 8;  // staged entry: c0 k2 | P Qx | Qyz e0xy | e0z U | V l2s | g | rgb | norms
+  static constexpr int NF = 6;  // per-warp quadratic form
+};
+template <> struct BlendLayout<2> {
+  static constexpr int SF = 11;  // + h | PU | QV (rolling shutter, read directly)
+  static constexpr int NF = 0;
+};
+template <int MODE>
+constexpr size_t blend_smem_bytes() {
+  return sizeof(float4) * (8 + GUT_RING * 32 * BlendLayout<MODE>::SF +
+                           (GUT_BLEND_THREADS / 32) * 32 * BlendLayout<MODE>::NF);
+}
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-template <> struct WarpTbl<2> { static constexpr int NF = 11; };
+__device__ __forceinline__ int ld_vol(const int *p) { return *(const volatile int *)p; }
+__device__ __forceinline__ void st_vol(int *p, int v) { *(volatile int *)p = v; }
 
-// One pass of ONE WARP over the segment [s0, s1): no CTA barriers.  Each chunk
-// of 32 entries is staged by the 32 lanes (one entry each: fp64 for the
-// cancelling part), culled against the warp's pixel box in registers, and the
-// surviving entries are evaluated by every lane in list order.  The warp leaves
-// the list as soon as all its pixels have terminated.  Termination rule
-// (reading R21): stop before an entry would take T below T_min.
+// stage one list entry into the ring: fp64 for the cancelling part c0 =
+// o_g x (M D), fp32 for the rest (the anchored form of Eq. 11)
+template <int MODE>
+__device__ __forceinline__ void stage_entry(const DevCam &c, const BlendBufs &B, uint32_t k, const d3 &D, const d3 &O,
+                                            const f3 &T1f, const f3 &T2f, float4 *__restrict__ dst) {
+  const uint32_t g = __ldg(&B.gids[k]);
+  const float4 p0 = __ldg(&B.payload[4 * g]), p1 = __ldg(&B.payload[4 * g + 1]);
+  const float4 p2 = __ldg(&B.payload[4 * g + 2]), p3 = __ldg(&B.payload[4 * g + 3]);
+  const float M[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
+  const double Md[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
+  const d3 og = mv(Md, O - mkd(p0.x, p0.y, p0.z));
+  const d3 e0d = mv(Md, D);
+  const d3 c0 = cross(og, e0d);
+  const double g0 = dot(og, e0d);
+  const f3 ogf = tof(og), e0 = tof(e0d);
+  f3 U = mv(M, T1f), V = mv(M, T2f), P, Q;
+  float gu, gv;
+  if (MODE == 1) {
+    P = cross(U, e0); Q = cross(V, e0); gu = dot(U, e0); gv = dot(V, e0);
+    U = mk(0, 0, 0); V = mk(0, 0, 0);
+  } else {
+    P = cross(ogf, U); Q = cross(ogf, V); gu = dot(ogf, U); gv = dot(ogf, V);
+  }
+  // k^2 = 2 ln(sigma/alpha_min) via log1p (accurate for sigma near alpha_min)
+  const float k2 = 2.f * log1pf((p0.w - c.alpha_min) / c.alpha_min);
+  dst[0] = make_float4((float)c0.x, (float)c0.y, (float)c0.z, k2);
+  dst[1] = make_float4(P.x, P.y, P.z, Q.x);
+  dst[2] = make_float4(Q.y, Q.z, e0.x, e0.y);
+  dst[3] = make_float4(e0.z, U.x, U.y, U.z);
+  dst[4] = make_float4(V.x, V.y, V.z, log2f(p0.w));
+  dst[5] = make_float4((float)g0, gu, gv, 0.f);
+  dst[6] = make_float4(p3.y, p3.z, p3.w, 0.f);
+  dst[7] = make_float4(sqrtf(dot(P, P)), sqrtf(dot(Q, Q)), sqrtf(dot(U, U)), sqrtf(dot(V, V)));
+  if (MODE == 2) {
+    const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
+    const f3 m = mv(M, dcw);
+    const f3 h = cross(m, e0), PU = cross(m, U), QV = cross(m, V);
+    dst[8] = make_float4(h.x, h.y, h.z, dot(m, e0));
+    dst[9] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
+    dst[10] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
+  }
+}
+
+// reset the ring control block (by the whole CTA, followed by a barrier)
+__device__ __forceinline__ void ring_reset(int *ctrl) {
+  if (threadIdx.x < GUT_RING) {
+    ctrl[threadIdx.x] = -1;                        // ready: chunk id staged in the slot
+    ctrl[GUT_RING + threadIdx.x] = (int)threadIdx.x - GUT_RING;  // claim: chunk id claimed
+  }
+  if (threadIdx.x < GUT_BLEND_THREADS / 32) ctrl[2 * GUT_RING + threadIdx.x] = 0;  // pos: next chunk per warp
+}
+
+// One pass of ONE WARP over the segment [s0, s1), starting at transmittance
+// T_start for its active pixels.  Termination rule (reading R21): stop before
+// an entry would take T below T_min.
 template <int MODE>
 __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, uint32_t s0, uint32_t s1,
                                           const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f, float a, float b,
                                           float beta, float snorm, float ac, float bc, float ra, float rb, bool active,
                                           float T_start, float &Cr, float &Cg, float &Cb, float &Dp, float &T,
                                           bool &term, uint32_t &n_eval, uint32_t &n_contrib, uint32_t &processed) {
-  constexpr int NF = WarpTbl<MODE>::NF;
-  // dynamic shared memory: [raw payload double buffer: 8 warps x 2 x 32 x 4]
-  // [per-warp entry table: 8 warps x 32 x NF]
+  constexpr int SF = BlendLayout<MODE>::SF, NF = BlendLayout<MODE>::NF;
   extern __shared__ float4 s_dyn[];
-  constexpr int RAW = (GUT_BLEND_THREADS / 32) * 2 * 32 * 4;
-  float4 *__restrict__ wt = s_dyn + RAW + (threadIdx.x >> 5) * 32 * NF;
-  const int lane = threadIdx.x & 31;
+  int *ctrl = reinterpret_cast<int *>(s_dyn);
+  int *ready = ctrl, *claim = ctrl + GUT_RING, *pos = ctrl + 2 * GUT_RING;
+  float4 *__restrict__ ring = s_dyn + 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4 *__restrict__ wt = ring + GUT_RING * 32 * SF + warp * 32 * (NF > 0 ? NF : 1);
   const float alpha_min = c.alpha_min, alpha_max = c.alpha_max, t_min = c.t_min;
-  const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
-  // raw payload of the warp's current / next chunk (cp.async double buffer)
-  float4 *__restrict__ raw = s_dyn + (threadIdx.x >> 5) * 2 * 32 * 4;
   T = T_start;
   Cr = Cg = Cb = Dp = 0.f;
   term = false;
   bool done = !active;
   processed = 0;
-  if (__all_sync(0xffffffffu, done) || s0 >= s1) return;
-  // gathers run one chunk ahead (cp.async), Gaussian ids two chunks ahead
-  uint32_t gnext = s0 + lane < s1 ? __ldg(&B.gids[s0 + lane]) : 0u;
-  if (s0 + lane < s1) {
-    float4 *dst = raw + lane * 4;
-    for (int q = 0; q < 4; ++q) cp_async16(dst + q, &B.payload[4 * gnext + q]);
-  }
-  cp_async_commit();
-  gnext = s0 + 32 + lane < s1 ? __ldg(&B.gids[s0 + 32 + lane]) : 0u;
-  int buf = 0;
-  for (uint32_t b0 = s0; b0 < s1; b0 += 32, buf ^= 1) {
+  const int nchunks = s1 > s0 ? (int)((s1 - s0 + 31) / 32) : 0;
+  for (int ch = 0; ch < nchunks; ++ch) {
     if (__all_sync(0xffffffffu, done)) break;
-    if (b0 + 32 < s1) {  // prefetch the next chunk
-      if (b0 + 32 + lane < s1) {
-        float4 *dst = raw + ((buf ^ 1) * 32 + lane) * 4;
-        for (int q = 0; q < 4; ++q) cp_async16(dst + q, &B.payload[4 * gnext + q]);
+    const uint32_t b0 = s0 + 32u * (uint32_t)ch;
+    const int slot = ch & (GUT_RING - 1);
+    // ---- acquire chunk ch: stage it if nobody has, else wait for it
+    while (true) {
+      if (ld_vol(&ready[slot]) == ch) break;
+      int mine = 0;
+      if (lane == 0 && ld_vol(&claim[slot]) == ch - GUT_RING) {
+        int mn = 0x7FFFFFFF;
+#pragma unroll
+        for (int w = 0; w < GUT_BLEND_THREADS / 32; ++w) mn = min(mn, ld_vol(&pos[w]));
+        if (mn > ch - GUT_RING && atomicCAS(&claim[slot], ch - GUT_RING, ch) == ch - GUT_RING) mine = 1;
       }
-      cp_async_commit();
-      gnext = b0 + 64 + lane < s1 ? __ldg(&B.gids[b0 + 64 + lane]) : 0u;
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+      if (__shfl_sync(0xffffffffu, mine, 0)) {
+        if (b0 + lane < s1) stage_entry<MODE>(c, B, b0 + lane, D, O, T1f, T2f, ring + (slot * 32 + lane) * SF);
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) st_vol(&ready[slot], ch);
+        break;
+      }
+      __nanosleep(32);
     }
-    __syncwarp();
+    __threadfence_block();
     processed = min(b0 + 32, s1) - s0;
-    const uint32_t kk = b0 + (uint32_t)lane;
+    const float4 *__restrict__ rs = ring + slot * 32 * SF;
+    // ---- conservative cull of entry b0 + lane against the warp's pixel box
+    // (a in ac +- ra, b in bc +- rb): |n| >= |n(ac,bc)| - ra|P| - rb|Q|, |e| <=
+    // |e(ac,bc)| + ra|U| + rb|V| (triangle inequality), so omega^2 > k^2 on the
+    // box if (|n0| - dn)^2 > k^2 (|e0| + de)^2 (1e-3 margin for fp32 rounding).
+    // Rolling shutter: every entry is kept.
     bool maybe = false;
-    if (kk < s1) {
-      // ---- stage entry kk: fp64 for the cancelling part, fp32 for the rest
-      const float4 *src = raw + (buf * 32 + lane) * 4;
-      const float4 p0 = src[0], p1 = src[1], p2 = src[2], p3 = src[3];
-      const float M[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
-      const double Md[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
-      const d3 og = mv(Md, O - mkd(p0.x, p0.y, p0.z));
-      const d3 e0d = mv(Md, D);
-      const d3 c0d = cross(og, e0d);
-      const double g0 = dot(og, e0d);
-      const f3 ogf = tof(og), e0 = tof(e0d), c0 = tof(c0d);
-      f3 U = mv(M, T1f), V = mv(M, T2f), P, Q;
-      float gu, gv;
-      if (MODE == 1) {
-        P = cross(U, e0); Q = cross(V, e0); gu = dot(U, e0); gv = dot(V, e0);
-        U = mk(0, 0, 0); V = mk(0, 0, 0);
-      } else {
-        P = cross(ogf, U); Q = cross(ogf, V); gu = dot(ogf, U); gv = dot(ogf, V);
-      }
-      // k^2 = 2 ln(sigma/alpha_min) via log1p (accurate for sigma near alpha_min)
-      const float k2 = 2.f * log1pf((p0.w - alpha_min) / alpha_min);
-      const float l2s = log2f(p0.w);
-      // ---- conservative cull against the warp's pixel box (a in ac +- ra,
-      // b in bc +- rb): |n| >= |n(ac,bc)| - ra|P| - rb|Q|, |e| <= |e(ac,bc)| +
-      // ra|U| + rb|V| (triangle inequality); omega^2 > k^2 on the whole box if
-      // (|n0| - dn)^2 > k^2 (|e0| + de)^2 (1e-3 margin for fp32 rounding).
-      // Rolling shutter: every entry is kept.
-      const f3 n0 = c0 + ac * P + bc * Q;
-      const f3 e0c = e0 + ac * U + bc * V;
-      if (MODE == 2) {
-        maybe = true;
-      } else {
-        const float lo = sqrtf(dot(n0, n0)) - (ra * sqrtf(dot(P, P)) + rb * sqrtf(dot(Q, Q)));
-        const float hi = sqrtf(dot(e0c, e0c)) + (ra * sqrtf(dot(U, U)) + rb * sqrtf(dot(V, V)));
-        maybe = !(lo > 0.f && lo * lo > 1.001f * k2 * (hi * hi));
-      }
-      if (maybe) {
-        float4 *t = wt + lane * NF;
+    {
+      if (b0 + lane < s1) {
         if (MODE == 2) {
-          const f3 m = mv(M, dcw);
-          const f3 h = cross(m, e0), PU = cross(m, U), QV = cross(m, V);
-          t[0] = make_float4(c0.x, c0.y, c0.z, k2);
-          t[1] = make_float4(P.x, P.y, P.z, Q.x);
-          t[2] = make_float4(Q.y, Q.z, e0.x, e0.y);
-          t[3] = make_float4(e0.z, U.x, U.y, U.z);
-          t[4] = make_float4(V.x, V.y, V.z, l2s);
-          t[5] = make_float4((float)g0, gu, gv, 0.f);
-          t[6] = make_float4(p3.y, p3.z, p3.w, 0.f);
-          t[7] = make_float4(h.x, h.y, h.z, dot(m, e0));
-          t[8] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
-          t[9] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
+          maybe = true;
         } else {
-          // Quadratic forms of F = |n|^2 - k^2 |e|^2 and D = |e|^2 in the pixel
-          // offset (da, db) from an expansion point (a*, b*): the box point
-          // nearest the Gaussian (minimiser of |n|^2, clamped to the box), so
-          // the coefficients' rounding stays relative to the values at the
-          // pixels (expanding about the box centre would cost eps * omega_c^2
-          // for Gaussians far smaller than the box).
-          const float pp = dot(P, P), pq = dot(P, Q), qq = dot(Q, Q);
-          const float np = dot(n0, P), nq = dot(n0, Q);
-          const float det = fmaf(pp, qq, -pq * pq);
-          float xa = 0.f, xb = 0.f;
-          if (det > 1e-30f * pp * qq && det > 0.f) {
-            const float id = 1.f / det;
-            xa = (pq * nq - qq * np) * id;
-            xb = (pq * np - pp * nq) * id;
+          const float4 *e = rs + lane * SF;
+          const float4 f0 = e[0], f1 = e[1], f2 = e[2], f3v = e[3], f4 = e[4], f7 = e[7];
+          const f3 c0 = mk(f0.x, f0.y, f0.z), P = mk(f1.x, f1.y, f1.z), Q = mk(f1.w, f2.x, f2.y);
+          const f3 e0 = mk(f2.z, f2.w, f3v.x), U = mk(f3v.y, f3v.z, f3v.w), V = mk(f4.x, f4.y, f4.z);
+          const float k2 = f0.w;
+          const f3 n0 = c0 + ac * P + bc * Q;
+          const f3 e0c = e0 + ac * U + bc * V;
+          const float lo = sqrtf(dot(n0, n0)) - fmaf(ra, f7.x, rb * f7.y);
+          const float hi = sqrtf(dot(e0c, e0c)) + fmaf(ra, f7.z, rb * f7.w);
+          maybe = !(lo > 0.f && lo * lo > 1.001f * k2 * (hi * hi));
+          if (maybe) {
+            // Quadratic forms of F = |n|^2 - k^2 |e|^2 and D = |e|^2 in the pixel
+            // offset (da, db) from the box point (a*, b*) nearest the Gaussian
+            // (minimiser of |n|^2, clamped to the box): the coefficients' rounding
+            // stays relative to the values at the pixels (expanding about the box
+            // centre would cost eps * omega_c^2 for Gaussians far smaller than it).
+            const float pp = dot(P, P), pq = dot(P, Q), qq = dot(Q, Q);
+            const float np = dot(n0, P), nq = dot(n0, Q);
+            const float det = fmaf(pp, qq, -pq * pq);
+            float xa = 0.f, xb = 0.f;
+            if (det > 1e-30f * pp * qq && det > 0.f) {
+              const float id = 1.f / det;
+              xa = (pq * nq - qq * np) * id;
+              xb = (pq * np - pp * nq) * id;
+            }
+            const float as = ac + fminf(fmaxf(xa, -ra), ra), bs = bc + fminf(fmaxf(xb, -rb), rb);
+            const f3 ns = c0 + as * P + bs * Q;
+            const f3 es = e0 + as * U + bs * V;
+            const float N0 = dot(ns, ns), Na = 2.f * dot(ns, P), Nb = 2.f * dot(ns, Q);
+            const float D0 = dot(es, es), Da = 2.f * dot(es, U), Db = 2.f * dot(es, V);
+            const float Daa = dot(U, U), Dab = 2.f * dot(U, V), Dbb = dot(V, V);
+            const float4 f5 = e[5];
+            const float gs = f5.x + as * f5.y + bs * f5.z;
+            float4 *t = wt + lane * NF;
+            t[0] = make_float4(fmaf(-k2, D0, N0), fmaf(-k2, Da, Na), fmaf(-k2, Db, Nb), fmaf(-k2, Daa, pp));
+            t[1] = make_float4(fmaf(-k2, Dab, 2.f * pq), fmaf(-k2, Dbb, qq), as, bs);
+            t[2] = make_float4(D0, Da, Db, Daa);
+            t[3] = make_float4(Dab, Dbb, gs, f5.y);
+            t[4] = make_float4(f5.z, k2, f4.w, 0.f);
+            t[5] = e[6];
           }
-          const float as = ac + fminf(fmaxf(xa, -ra), ra), bs = bc + fminf(fmaxf(xb, -rb), rb);
-          const f3 ns = c0 + as * P + bs * Q;
-          const f3 es = e0 + as * U + bs * V;
-          const float N0 = dot(ns, ns), Na = 2.f * dot(ns, P), Nb = 2.f * dot(ns, Q);
-          const float Nab = 2.f * pq;
-          const float D0 = dot(es, es), Da = 2.f * dot(es, U), Db = 2.f * dot(es, V);
-          const float Daa = dot(U, U), Dab = 2.f * dot(U, V), Dbb = dot(V, V);
-          const float gs = (float)g0 + as * gu + bs * gv;
-          t[0] = make_float4(fmaf(-k2, D0, N0), fmaf(-k2, Da, Na), fmaf(-k2, Db, Nb), fmaf(-k2, Daa, pp));
-          t[1] = make_float4(fmaf(-k2, Dab, Nab), fmaf(-k2, Dbb, qq), as, bs);
-          t[2] = make_float4(D0, Da, Db, Daa);
-          t[3] = make_float4(Dab, Dbb, gs, gu);
-          t[4] = make_float4(gv, k2, l2s, 0.f);
-          t[5] = make_float4(p3.y, p3.z, p3.w, 0.f);
         }
       }
     }
@@ -456,11 +484,12 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
       m &= m - 1;
       if (done) continue;
       ++n_eval;
-      const float4 *t = wt + j * NF;
-      float w2, rD, gg, k2;
+      float w2, rD, gg, k2, l2s;
+      float4 cc;
       if (MODE == 2) {
+        const float4 *t = rs + j * SF;
         const float4 f0 = t[0], f1 = t[1], f2 = t[2], f3v = t[3], f4 = t[4];
-        const float4 h = t[7], pu = t[8], qv = t[9];
+        const float4 h = t[8], pu = t[9], qv = t[10];
         float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
         float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
         float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
@@ -479,7 +508,10 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
         const float4 f5 = t[5];
         gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
         gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
+        l2s = f4.w;
+        cc = t[6];
       } else {
+        const float4 *t = wt + j * NF;
         const float4 f0 = t[0], f1 = t[1];
         const float da = a - f1.z, db = b - f1.w;
         // F = N - k^2 D <= 0  <=>  omega^2 <= k^2  <=>  alpha >= alpha_min
@@ -491,8 +523,9 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
         rD = rcp_approx(Dd);
         w2 = fmaxf(fmaf(k2, Dd, F), 0.f) * rD;
         gg = fmaf(da, f3v.w, fmaf(db, f4.x, f3v.z));
+        l2s = f4.z;
+        cc = t[5];
       }
-      const float l2s = MODE == 2 ? t[4].w : t[4].z;
       // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
       const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, l2s)));
       if (!(al >= alpha_min)) continue;
@@ -504,7 +537,6 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
         term = true;
         continue;
       }
-      const float4 cc = MODE == 2 ? t[6] : t[5];
       const float wgt = al * T;
       Cr = fmaf(wgt, cc.x, Cr);
       Cg = fmaf(wgt, cc.y, Cg);
@@ -514,14 +546,14 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
       T = Tn;
     }
     __syncwarp();
+    if (lane == 0) st_vol(&pos[warp], ch + 1);  // chunk consumed: its slot may be reused
   }
-  cp_async_wait<0>();  // a warp leaving early must not leave copies in flight
   __syncwarp();
+  if (lane == 0) st_vol(&pos[warp], 0x7FFFFFFF);  // this warp needs no further chunks
 }
 
 template <int MODE>
 __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, BlendBufs B) {
-  constexpr int NF = WarpTbl<MODE>::NF;
   constexpr int NT = GUT_BLEND_THREADS;
   __shared__ uint32_t s_ticket;
   __shared__ int s_last;
@@ -602,6 +634,10 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
       run = false;
   }
   // ---- speculative pass: transmittance from 1 (exact for segment 0)
+  extern __shared__ float4 s_dyn[];
+  int *ctrl = reinterpret_cast<int *>(s_dyn);
+  ring_reset(ctrl);
+  __syncthreads();
   float Cr, Cg, Cb, Dp, Tsp;
   bool term;
   uint32_t n_eval = 0, n_contrib = 0, processed = 0, n_term = 0;
@@ -638,7 +674,9 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
     Cr *= T_pre; Cg *= T_pre; Cb *= T_pre; Dp *= T_pre;
     T_end = T_pre * Tsp;
   }
-  if (__any_sync(0xffffffffu, redo)) {
+  if (__syncthreads_or(redo)) {  // every warp has left pass 1: the ring can be reset
+    ring_reset(ctrl);
+    __syncthreads();
     float r0, r1, r2, r3, rT;
     bool rterm;
     uint32_t e2 = 0, c2 = 0, p2 = 0;
@@ -708,8 +746,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
 
 template <int MODE>
 static void blend_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
-  constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_THREADS / 32) * 2 * 32 * 4 +
-                                            (GUT_BLEND_THREADS / 32) * 32 * WarpTbl<MODE>::NF);
+  constexpr size_t smem = blend_smem_bytes<MODE>();
   static bool configured = false;  // per template instance; the attribute is per device function
   if (!configured) {
     cudaFuncSetAttribute(blend_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
