@@ -285,165 +285,76 @@ __device__ __forceinline__ unsigned long long st_word(uint32_t flag, uint32_t ep
   return ((unsigned long long)flag << 62) | ((unsigned long long)(epoch & 0x3FFFFFu) << 40) | L;
 }
 
-// ---- staged list entries (ring slots) and per-warp quadratic forms
-#define GUT_RING 8
-template <int MODE> struct BlendLayout {
-  static constexpr int SF = 8;  // staged entry: c0 k2 | P Qx | Qyz e0xy | e0z U | V l2s | g | rgb | norms
-  static constexpr int NF = 6;  // per-warp quadratic form
-};
-template <> struct BlendLayout<2> {
-  static constexpr int SF = 11;  // + h | PU | QV (rolling shutter, read directly)
-  static constexpr int NF = 0;
-};
+// Per-warp table of staged list entries (32 per chunk).  MODE 0/1: the
+// quadratic forms of F = |n|^2 - k^2 |e|^2 and D = |e|^2 in the lane's pixel
+// offset (da, db) from the warp box centre; MODE 2 (rolling shutter, beta
+// varies per row): the raw anchored vectors.
+template <int MODE> struct WarpTbl { static constexpr int NF = 6; };
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ int ld_vol(const int *p) { return *(const volatile int *)p; }
-__device__ __forceinline__ void st_vol(int *p, int v) { *(volatile int *)p = v; }
+template <> struct WarpTbl<2> { static constexpr int NF = 11; };
 
-// stage one list entry into the ring: fp64 for the cancelling part c0 =
-// o_g x (M D), fp32 for the rest (the anchored form of Eq. 11)
+// One pass of ONE WARP over the segment [s0, s1): no CTA barriers.  Each chunk
+// of 32 entries is staged by the 32 lanes (one entry each: fp64 for the
+// cancelling part), culled against the warp's pixel box in registers, and the
+// surviving entries are evaluated by every lane in list order.  The warp leaves
+// the list as soon as all its pixels have terminated.  Termination rule
+// (reading R21): stop before an entry would take T below T_min.
 template <int MODE>
-__device__ __forceinline__ void stage_entry(const DevCam &c, float4 p0, float4 p1, float4 p2, float4 p3, const d3 &D,
-                                            const d3 &O, const f3 &T1f, const f3 &T2f, float4 *__restrict__ dst) {
-  const float M[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
-  const double Md[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
-  const d3 og = mv(Md, O - mkd(p0.x, p0.y, p0.z));
-  const d3 e0d = mv(Md, D);
-  const d3 c0 = cross(og, e0d);
-  const double g0 = dot(og, e0d);
-  const f3 ogf = tof(og), e0 = tof(e0d);
-  f3 U = mv(M, T1f), V = mv(M, T2f), P, Q;
-  float gu, gv;
-  if (MODE == 1) {
-    P = cross(U, e0); Q = cross(V, e0); gu = dot(U, e0); gv = dot(V, e0);
-    U = mk(0, 0, 0); V = mk(0, 0, 0);
-  } else {
-    P = cross(ogf, U); Q = cross(ogf, V); gu = dot(ogf, U); gv = dot(ogf, V);
-  }
-  // k^2 = 2 ln(sigma/alpha_min) via log1p (accurate for sigma near alpha_min)
-  const float k2 = 2.f * log1pf((p0.w - c.alpha_min) / c.alpha_min);
-  dst[0] = make_float4((float)c0.x, (float)c0.y, (float)c0.z, k2);
-  dst[1] = make_float4(P.x, P.y, P.z, Q.x);
-  dst[2] = make_float4(Q.y, Q.z, e0.x, e0.y);
-  dst[3] = make_float4(e0.z, U.x, U.y, U.z);
-  dst[4] = make_float4(V.x, V.y, V.z, log2f(p0.w));
-  dst[5] = make_float4((float)g0, gu, gv, 0.f);
-  dst[6] = make_float4(p3.y, p3.z, p3.w, 0.f);
-  dst[7] = make_float4(sqrtf(dot(P, P)), sqrtf(dot(Q, Q)), sqrtf(dot(U, U)), sqrtf(dot(V, V)));
-  if (MODE == 2) {
-    const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
-    const f3 m = mv(M, dcw);
-    const f3 h = cross(m, e0), PU = cross(m, U), QV = cross(m, V);
-    dst[8] = make_float4(h.x, h.y, h.z, dot(m, e0));
-    dst[9] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
-    dst[10] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
-  }
-}
-
-// ---- warp-specialised blend CTA: 8 consumer warps (one pixel each) + 1
-// producer warp.  The producer stages each 32-entry chunk of the segment ONCE
-// into a ring of GUT_RING slots (payload gathers prefetched one chunk ahead
-// with cp.async); consumers wait on the slot's "full" mbarrier, cull, evaluate
-// and release it through its "empty" mbarrier (8 arrivals).  mbarrier waits
-// sleep in hardware: no CTA-wide barrier inside the loop, consumer warps drift
-// up to GUT_RING chunks apart, and warps whose pixels have all terminated just
-// wait/arrive.  When every consumer warp is done the producer stops early.
-#define GUT_PRODUCER_THREADS 32
-#define GUT_CTA_THREADS (GUT_BLEND_THREADS + GUT_PRODUCER_THREADS)
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_inval(unsigned long long *bar) {
-  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
-  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// dynamic shared memory (float4 units): [mbarriers: full[R], empty[R]]
-// [ring: R x 32 x SF] [producer raw payload: 2 x 32 x 4] [consumer tables: 8 x 32 x NF]
-template <int MODE>
-struct SmemLayout {
-  static constexpr int SF = BlendLayout<MODE>::SF, NF = BlendLayout<MODE>::NF;
-  static constexpr int BAR = 8;                       // 2 * GUT_RING mbarriers (8 B each) = 128 B
-  static constexpr int RING = BAR;
-  static constexpr int RAW = RING + GUT_RING * 32 * SF;
-  static constexpr int TBL = RAW + 2 * 32 * 4;
-  static constexpr int TOTAL = TBL + (GUT_BLEND_THREADS / 32) * 32 * (NF > 0 ? NF : 0);
-  static constexpr size_t bytes() { return sizeof(float4) * (size_t)TOTAL; }
-};
-
-struct PassCtl {
-  int active;  // consumer warps with live pixels
-  int end;     // first chunk index the producer will not deliver
-};
-
-// (thread 0 of the CTA; followed by a barrier)
-template <int MODE>
-__device__ __forceinline__ void pass_init(float4 *s_dyn, PassCtl *ctl, bool reinit) {
-  unsigned long long *bars = reinterpret_cast<unsigned long long *>(s_dyn);
-  for (int i = 0; i < 2 * GUT_RING; ++i) {
-    if (reinit) mbar_inval(&bars[i]);
-    mbar_init(&bars[i], i < GUT_RING ? 1u : (uint32_t)(GUT_BLEND_THREADS / 32));
-  }
-  ctl->active = GUT_BLEND_THREADS / 32;
-  ctl->end = 0x7FFFFFFF;
-}
-
-// producer warp: stage the chunks of [s0, s1)
-template <int MODE>
-__device__ __forceinline__ void produce(const DevCam &c, const BlendBufs &B, float4 *s_dyn, PassCtl *ctl, uint32_t s0,
-                                        uint32_t s1, const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f) {
-  using L = SmemLayout<MODE>;
-  unsigned long long *full = reinterpret_cast<unsigned long long *>(s_dyn), *empty = full + GUT_RING;
-  float4 *ring = s_dyn + L::RING, *raw = s_dyn + L::RAW;
+__device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, uint32_t s0, uint32_t s1,
+                                          const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f, float a, float b,
+                                          float beta, float snorm, float ac, float bc, float ra, float rb, bool active,
+                                          float T_start, float &Cr, float &Cg, float &Cb, float &Dp, float &T,
+                                          bool &term, uint32_t &n_eval, uint32_t &n_contrib, uint32_t &processed) {
+  constexpr int NF = WarpTbl<MODE>::NF;
+  // dynamic shared memory: [raw payload double buffer: 8 warps x 2 x 32 x 4]
+  // [per-warp entry table: 8 warps x 32 x NF]
+  extern __shared__ float4 s_dyn[];
+  constexpr int RAW = (GUT_BLEND_THREADS / 32) * 2 * 32 * 4;
+  float4 *__restrict__ wt = s_dyn + RAW + (threadIdx.x >> 5) * 32 * NF;
   const int lane = threadIdx.x & 31;
-  const int nchunks = s1 > s0 ? (int)((s1 - s0 + 31) / 32) : 0;
-  if (nchunks == 0) return;
+  const float alpha_min = c.alpha_min, alpha_max = c.alpha_max, t_min = c.t_min;
+  const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
+  // raw payload of the warp's current / next chunk (cp.async double buffer)
+  float4 *__restrict__ raw = s_dyn + (threadIdx.x >> 5) * 2 * 32 * 4;
+  T = T_start;
+  Cr = Cg = Cb = Dp = 0.f;
+  term = false;
+  bool done = !active;
+  processed = 0;
+  if (__all_sync(0xffffffffu, done) || s0 >= s1) return;
+  // gathers run one chunk ahead (cp.async), Gaussian ids two chunks ahead
   uint32_t gnext = s0 + lane < s1 ? __ldg(&B.gids[s0 + lane]) : 0u;
-  if (s0 + lane < s1)
-    for (int q = 0; q < 4; ++q) cp_async16(raw + lane * 4 + q, &B.payload[4 * gnext + q]);
+  if (s0 + lane < s1) {
+    float4 *dst = raw + lane * 4;
+    for (int q = 0; q < 4; ++q) cp_async16(dst + q, &B.payload[4 * gnext + q]);
+  }
   cp_async_commit();
   gnext = s0 + 32 + lane < s1 ? __ldg(&B.gids[s0 + 32 + lane]) : 0u;
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int slot = ch % GUT_RING;
-    if (ch >= GUT_RING) mbar_wait(&empty[slot], (uint32_t)((ch / GUT_RING - 1) & 1));
-    if (*(volatile int *)&ctl->active == 0) {  // every pixel has terminated: stop
-      if (lane == 0) {
-        *(volatile int *)&ctl->end = ch;
-        __threadfence_block();
-        mbar_arrive(&full[slot]);
+  int buf = 0;
+  for (uint32_t b0 = s0; b0 < s1; b0 += 32, buf ^= 1) {
+    if (__all_sync(0xffffffffu, done)) break;
+    if (b0 + 32 < s1) {  // prefetch the next chunk
+      if (b0 + 32 + lane < s1) {
+        float4 *dst = raw + ((buf ^ 1) * 32 + lane) * 4;
+        for (int q = 0; q < 4; ++q) cp_async16(dst + q, &B.payload[4 * gnext + q]);
       }
-      break;
-    }
-    const uint32_t b0 = s0 + 32u * (uint32_t)ch;
-    if (ch + 1 < nchunks) {  // prefetch the next chunk's payload
-      if (b0 + 32 + lane < s1)
-        for (int q = 0; q < 4; ++q) cp_async16(raw + (((ch + 1) & 1) * 32 + lane) * 4 + q, &B.payload[4 * gnext + q]);
       cp_async_commit();
       gnext = b0 + 64 + lane < s1 ? __ldg(&B.gids[b0 + 64 + lane]) : 0u;
       cp_async_wait<1>();
@@ -451,203 +362,166 @@ __device__ __forceinline__ void produce(const DevCam &c, const BlendBufs &B, flo
       cp_async_wait<0>();
     }
     __syncwarp();
-    if (b0 + lane < s1) {
-      const float4 *src = raw + ((ch & 1) * 32 + lane) * 4;
-      stage_entry<MODE>(c, src[0], src[1], src[2], src[3], D, O, T1f, T2f, ring + (slot * 32 + lane) * L::SF);
-    }
-    __threadfence_block();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&full[slot]);
-  }
-  cp_async_wait<0>();
-}
-
-// consumer warp: one pass over the chunks of [s0, s1) for its 32 pixels,
-// starting at transmittance T_start.  Termination rule (reading R21): stop
-// before an entry would take T below T_min.
-template <int MODE>
-__device__ __forceinline__ void consume(const DevCam &c, float4 *s_dyn, PassCtl *ctl, uint32_t s0, uint32_t s1,
-                                        float a, float b, float beta, float snorm, float ac, float bc, float ra,
-                                        float rb, bool active, float T_start, float &Cr, float &Cg, float &Cb,
-                                        float &Dp, float &T, bool &term, uint32_t &n_eval, uint32_t &n_contrib,
-                                        uint32_t &processed) {
-  using L = SmemLayout<MODE>;
-  constexpr int SF = L::SF, NF = L::NF;
-  unsigned long long *full = reinterpret_cast<unsigned long long *>(s_dyn), *empty = full + GUT_RING;
-  const float4 *ring = s_dyn + L::RING;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float4 *__restrict__ wt = s_dyn + L::TBL + warp * 32 * (NF > 0 ? NF : 1);
-  const float alpha_min = c.alpha_min, alpha_max = c.alpha_max, t_min = c.t_min;
-  T = T_start;
-  Cr = Cg = Cb = Dp = 0.f;
-  term = false;
-  bool done = !active;
-  bool counted = false;
-  processed = 0;
-  const int nchunks = s1 > s0 ? (int)((s1 - s0 + 31) / 32) : 0;
-  for (int ch = 0; ch < nchunks; ++ch) {
-    if (!counted && __all_sync(0xffffffffu, done)) {
-      if (lane == 0) atomicSub(&ctl->active, 1);
-      counted = true;
-    }
-    const int slot = ch % GUT_RING;
-    mbar_wait(&full[slot], (uint32_t)((ch / GUT_RING) & 1));
-    if (*(volatile int *)&ctl->end <= ch) break;  // producer stopped: nothing left to blend
-    const uint32_t b0 = s0 + 32u * (uint32_t)ch;
-    if (!counted) {
-      processed = min(b0 + 32, s1) - s0;
-      const float4 *__restrict__ rs = ring + slot * 32 * SF;
-      // ---- conservative cull of entry b0 + lane against the warp's pixel box
-      // (a in ac +- ra, b in bc +- rb): |n| >= |n(ac,bc)| - ra|P| - rb|Q|, |e| <=
-      // |e(ac,bc)| + ra|U| + rb|V| (triangle inequality), so omega^2 > k^2 on
-      // the box if (|n0| - dn)^2 > k^2 (|e0| + de)^2 (1e-3 margin for fp32
-      // rounding).  Rolling shutter: every entry is kept.
-      bool maybe = false;
-      if (b0 + lane < s1) {
+    processed = min(b0 + 32, s1) - s0;
+    const uint32_t kk = b0 + (uint32_t)lane;
+    bool maybe = false;
+    if (kk < s1) {
+      // ---- stage entry kk: fp64 for the cancelling part, fp32 for the rest
+      const float4 *src = raw + (buf * 32 + lane) * 4;
+      const float4 p0 = src[0], p1 = src[1], p2 = src[2], p3 = src[3];
+      const float M[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
+      const double Md[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
+      const d3 og = mv(Md, O - mkd(p0.x, p0.y, p0.z));
+      const d3 e0d = mv(Md, D);
+      const d3 c0d = cross(og, e0d);
+      const double g0 = dot(og, e0d);
+      const f3 ogf = tof(og), e0 = tof(e0d), c0 = tof(c0d);
+      f3 U = mv(M, T1f), V = mv(M, T2f), P, Q;
+      float gu, gv;
+      if (MODE == 1) {
+        P = cross(U, e0); Q = cross(V, e0); gu = dot(U, e0); gv = dot(V, e0);
+        U = mk(0, 0, 0); V = mk(0, 0, 0);
+      } else {
+        P = cross(ogf, U); Q = cross(ogf, V); gu = dot(ogf, U); gv = dot(ogf, V);
+      }
+      // k^2 = 2 ln(sigma/alpha_min) via log1p (accurate for sigma near alpha_min)
+      const float k2 = 2.f * log1pf((p0.w - alpha_min) / alpha_min);
+      const float l2s = log2f(p0.w);
+      // ---- conservative cull against the warp's pixel box (a in ac +- ra,
+      // b in bc +- rb): |n| >= |n(ac,bc)| - ra|P| - rb|Q|, |e| <= |e(ac,bc)| +
+      // ra|U| + rb|V| (triangle inequality); omega^2 > k^2 on the whole box if
+      // (|n0| - dn)^2 > k^2 (|e0| + de)^2 (1e-3 margin for fp32 rounding).
+      // Rolling shutter: every entry is kept.
+      const f3 n0 = c0 + ac * P + bc * Q;
+      const f3 e0c = e0 + ac * U + bc * V;
+      if (MODE == 2) {
+        maybe = true;
+      } else {
+        const float lo = sqrtf(dot(n0, n0)) - (ra * sqrtf(dot(P, P)) + rb * sqrtf(dot(Q, Q)));
+        const float hi = sqrtf(dot(e0c, e0c)) + (ra * sqrtf(dot(U, U)) + rb * sqrtf(dot(V, V)));
+        maybe = !(lo > 0.f && lo * lo > 1.001f * k2 * (hi * hi));
+      }
+      if (maybe) {
+        float4 *t = wt + lane * NF;
         if (MODE == 2) {
-          maybe = true;
+          const f3 m = mv(M, dcw);
+          const f3 h = cross(m, e0), PU = cross(m, U), QV = cross(m, V);
+          t[0] = make_float4(c0.x, c0.y, c0.z, k2);
+          t[1] = make_float4(P.x, P.y, P.z, Q.x);
+          t[2] = make_float4(Q.y, Q.z, e0.x, e0.y);
+          t[3] = make_float4(e0.z, U.x, U.y, U.z);
+          t[4] = make_float4(V.x, V.y, V.z, l2s);
+          t[5] = make_float4((float)g0, gu, gv, 0.f);
+          t[6] = make_float4(p3.y, p3.z, p3.w, 0.f);
+          t[7] = make_float4(h.x, h.y, h.z, dot(m, e0));
+          t[8] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
+          t[9] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
         } else {
-          const float4 *e = rs + lane * SF;
-          const float4 f0 = e[0], f1 = e[1], f2 = e[2], f3v = e[3], f4 = e[4], f7 = e[7];
-          const f3 c0 = mk(f0.x, f0.y, f0.z), P = mk(f1.x, f1.y, f1.z), Q = mk(f1.w, f2.x, f2.y);
-          const f3 e0 = mk(f2.z, f2.w, f3v.x), U = mk(f3v.y, f3v.z, f3v.w), V = mk(f4.x, f4.y, f4.z);
-          const float k2 = f0.w;
-          const f3 n0 = c0 + ac * P + bc * Q;
-          const f3 e0c = e0 + ac * U + bc * V;
-          const float lo = sqrtf(dot(n0, n0)) - fmaf(ra, f7.x, rb * f7.y);
-          const float hi = sqrtf(dot(e0c, e0c)) + fmaf(ra, f7.z, rb * f7.w);
-          maybe = !(lo > 0.f && lo * lo > 1.001f * k2 * (hi * hi));
-          if (maybe) {
-            // Quadratic forms of F = |n|^2 - k^2 |e|^2 and D = |e|^2 in the pixel
-            // offset (da, db) from the box point (a*, b*) nearest the Gaussian
-            // (minimiser of |n|^2, clamped to the box): the coefficients'
-            // rounding stays relative to the values at the pixels (expanding
-            // about the box centre would cost eps * omega_c^2 for Gaussians far
-            // smaller than the box).
-            const float pp = dot(P, P), pq = dot(P, Q), qq = dot(Q, Q);
-            const float np = dot(n0, P), nq = dot(n0, Q);
-            const float det = fmaf(pp, qq, -pq * pq);
-            float xa = 0.f, xb = 0.f;
-            if (det > 1e-30f * pp * qq && det > 0.f) {
-              const float id = 1.f / det;
-              xa = (pq * nq - qq * np) * id;
-              xb = (pq * np - pp * nq) * id;
-            }
-            const float as = ac + fminf(fmaxf(xa, -ra), ra), bs = bc + fminf(fmaxf(xb, -rb), rb);
-            const f3 ns = c0 + as * P + bs * Q;
-            const f3 es = e0 + as * U + bs * V;
-            const float N0 = dot(ns, ns), Na = 2.f * dot(ns, P), Nb = 2.f * dot(ns, Q);
-            const float D0 = dot(es, es), Da = 2.f * dot(es, U), Db = 2.f * dot(es, V);
-            const float Daa = dot(U, U), Dab = 2.f * dot(U, V), Dbb = dot(V, V);
-            const float4 f5 = e[5];
-            const float gs = f5.x + as * f5.y + bs * f5.z;
-            float4 *t = wt + lane * NF;
-            t[0] = make_float4(fmaf(-k2, D0, N0), fmaf(-k2, Da, Na), fmaf(-k2, Db, Nb), fmaf(-k2, Daa, pp));
-            t[1] = make_float4(fmaf(-k2, Dab, 2.f * pq), fmaf(-k2, Dbb, qq), as, bs);
-            t[2] = make_float4(D0, Da, Db, Daa);
-            t[3] = make_float4(Dab, Dbb, gs, f5.y);
-            t[4] = make_float4(f5.z, k2, f4.w, 0.f);
-            t[5] = e[6];
+          // Quadratic forms of F = |n|^2 - k^2 |e|^2 and D = |e|^2 in the pixel
+          // offset (da, db) from an expansion point (a*, b*): the box point
+          // nearest the Gaussian (minimiser of |n|^2, clamped to the box), so
+          // the coefficients' rounding stays relative to the values at the
+          // pixels (expanding about the box centre would cost eps * omega_c^2
+          // for Gaussians far smaller than the box).
+          const float pp = dot(P, P), pq = dot(P, Q), qq = dot(Q, Q);
+          const float np = dot(n0, P), nq = dot(n0, Q);
+          const float det = fmaf(pp, qq, -pq * pq);
+          float xa = 0.f, xb = 0.f;
+          if (det > 1e-30f * pp * qq && det > 0.f) {
+            const float id = 1.f / det;
+            xa = (pq * nq - qq * np) * id;
+            xb = (pq * np - pp * nq) * id;
           }
+          const float as = ac + fminf(fmaxf(xa, -ra), ra), bs = bc + fminf(fmaxf(xb, -rb), rb);
+          const f3 ns = c0 + as * P + bs * Q;
+          const f3 es = e0 + as * U + bs * V;
+          const float N0 = dot(ns, ns), Na = 2.f * dot(ns, P), Nb = 2.f * dot(ns, Q);
+          const float Nab = 2.f * pq;
+          const float D0 = dot(es, es), Da = 2.f * dot(es, U), Db = 2.f * dot(es, V);
+          const float Daa = dot(U, U), Dab = 2.f * dot(U, V), Dbb = dot(V, V);
+          const float gs = (float)g0 + as * gu + bs * gv;
+          t[0] = make_float4(fmaf(-k2, D0, N0), fmaf(-k2, Da, Na), fmaf(-k2, Db, Nb), fmaf(-k2, Daa, pp));
+          t[1] = make_float4(fmaf(-k2, Dab, Nab), fmaf(-k2, Dbb, qq), as, bs);
+          t[2] = make_float4(D0, Da, Db, Daa);
+          t[3] = make_float4(Dab, Dbb, gs, gu);
+          t[4] = make_float4(gv, k2, l2s, 0.f);
+          t[5] = make_float4(p3.y, p3.z, p3.w, 0.f);
         }
-      }
-      uint32_t m = __ballot_sync(0xffffffffu, maybe);
-      __syncwarp();
-      while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
-        if (done) continue;
-        ++n_eval;
-        float w2, rD, gg, k2, l2s;
-        float4 cc;
-        if (MODE == 2) {
-          const float4 *t = rs + j * SF;
-          const float4 f0 = t[0], f1 = t[1], f2 = t[2], f3v = t[3], f4 = t[4];
-          const float4 h = t[8], pu = t[9], qv = t[10];
-          float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
-          float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
-          float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
-          nx = fmaf(beta, fmaf(a, pu.x, fmaf(b, qv.x, h.x)), nx);
-          ny = fmaf(beta, fmaf(a, pu.y, fmaf(b, qv.y, h.y)), ny);
-          nz = fmaf(beta, fmaf(a, pu.z, fmaf(b, qv.z, h.z)), nz);
-          const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
-          const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
-          const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
-          const float N = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
-          const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
-          k2 = f0.w;
-          if (N > k2 * Dd) continue;  // omega^2 > k^2  <=>  alpha < alpha_min
-          rD = rcp_approx(Dd);
-          w2 = N * rD;
-          const float4 f5 = t[5];
-          gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
-          gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
-          l2s = f4.w;
-          cc = t[6];
-        } else {
-          const float4 *t = wt + j * NF;
-          const float4 f0 = t[0], f1 = t[1];
-          const float da = a - f1.z, db = b - f1.w;
-          // F = N - k^2 D <= 0  <=>  omega^2 <= k^2  <=>  alpha >= alpha_min
-          const float F = fmaf(da, fmaf(f0.w, da, fmaf(f1.x, db, f0.y)), fmaf(db, fmaf(f1.y, db, f0.z), f0.x));
-          if (F > 0.f) continue;
-          const float4 f2 = t[2], f3v = t[3], f4 = t[4];
-          const float Dd = fmaf(da, fmaf(f2.w, da, fmaf(f3v.x, db, f2.y)), fmaf(db, fmaf(f3v.y, db, f2.z), f2.x));
-          k2 = f4.y;
-          rD = rcp_approx(Dd);
-          w2 = fmaxf(fmaf(k2, Dd, F), 0.f) * rD;
-          gg = fmaf(da, f3v.w, fmaf(db, f4.x, f3v.z));
-          l2s = f4.z;
-          cc = t[5];
-        }
-        // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
-        const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, l2s)));
-        if (!(al >= alpha_min)) continue;
-        const float tau = -gg * rD * snorm;
-        if (!(tau > 0.f)) continue;  // reading R24
-        const float Tn = T * (1.f - al);
-        if (Tn < t_min) {
-          done = true;
-          term = true;
-          continue;
-        }
-        const float wgt = al * T;
-        Cr = fmaf(wgt, cc.x, Cr);
-        Cg = fmaf(wgt, cc.y, Cg);
-        Cb = fmaf(wgt, cc.z, Cb);
-        Dp = fmaf(wgt, tau, Dp);
-        ++n_contrib;
-        T = Tn;
       }
     }
+    uint32_t m = __ballot_sync(0xffffffffu, maybe);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      if (done) continue;
+      ++n_eval;
+      const float4 *t = wt + j * NF;
+      float w2, rD, gg, k2;
+      if (MODE == 2) {
+        const float4 f0 = t[0], f1 = t[1], f2 = t[2], f3v = t[3], f4 = t[4];
+        const float4 h = t[7], pu = t[8], qv = t[9];
+        float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
+        float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
+        float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
+        nx = fmaf(beta, fmaf(a, pu.x, fmaf(b, qv.x, h.x)), nx);
+        ny = fmaf(beta, fmaf(a, pu.y, fmaf(b, qv.y, h.y)), ny);
+        nz = fmaf(beta, fmaf(a, pu.z, fmaf(b, qv.z, h.z)), nz);
+        const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
+        const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
+        const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
+        const float N = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
+        const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
+        k2 = f0.w;
+        if (N > k2 * Dd) continue;  // omega^2 > k^2  <=>  alpha < alpha_min
+        rD = rcp_approx(Dd);
+        w2 = N * rD;
+        const float4 f5 = t[5];
+        gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
+        gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
+      } else {
+        const float4 f0 = t[0], f1 = t[1];
+        const float da = a - f1.z, db = b - f1.w;
+        // F = N - k^2 D <= 0  <=>  omega^2 <= k^2  <=>  alpha >= alpha_min
+        const float F = fmaf(da, fmaf(f0.w, da, fmaf(f1.x, db, f0.y)), fmaf(db, fmaf(f1.y, db, f0.z), f0.x));
+        if (F > 0.f) continue;
+        const float4 f2 = t[2], f3v = t[3], f4 = t[4];
+        const float Dd = fmaf(da, fmaf(f2.w, da, fmaf(f3v.x, db, f2.y)), fmaf(db, fmaf(f3v.y, db, f2.z), f2.x));
+        k2 = f4.y;
+        rD = rcp_approx(Dd);
+        w2 = fmaxf(fmaf(k2, Dd, F), 0.f) * rD;
+        gg = fmaf(da, f3v.w, fmaf(db, f4.x, f3v.z));
+      }
+      const float l2s = MODE == 2 ? t[4].w : t[4].z;
+      // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
+      const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, l2s)));
+      if (!(al >= alpha_min)) continue;
+      const float tau = -gg * rD * snorm;
+      if (!(tau > 0.f)) continue;  // reading R24
+      const float Tn = T * (1.f - al);
+      if (Tn < t_min) {
+        done = true;
+        term = true;
+        continue;
+      }
+      const float4 cc = MODE == 2 ? t[6] : t[5];
+      const float wgt = al * T;
+      Cr = fmaf(wgt, cc.x, Cr);
+      Cg = fmaf(wgt, cc.y, Cg);
+      Cb = fmaf(wgt, cc.z, Cb);
+      Dp = fmaf(wgt, tau, Dp);
+      ++n_contrib;
+      T = Tn;
+    }
+    __syncwarp();
   }
-  if (!counted && lane == 0) atomicSub(&ctl->active, 1);
+  cp_async_wait<0>();  // a warp leaving early must not leave copies in flight
+  __syncwarp();
 }
 
-// one pass of the CTA: the producer warp stages, the consumer warps blend
 template <int MODE>
-__device__ __forceinline__ void cta_pass(const DevCam &c, const BlendBufs &B, float4 *s_dyn, PassCtl *ctl,
-                                         bool reinit, uint32_t s0, uint32_t s1, const d3 &D, const d3 &O,
-                                         const f3 &T1f, const f3 &T2f, float a, float b, float beta, float snorm,
-                                         float ac, float bc, float ra, float rb, bool active, float T_start, float &Cr,
-                                         float &Cg, float &Cb, float &Dp, float &T, bool &term, uint32_t &n_eval,
-                                         uint32_t &n_contrib, uint32_t &processed) {
-  if (threadIdx.x == 0) pass_init<MODE>(s_dyn, ctl, reinit);
-  __syncthreads();
-  if (threadIdx.x >= GUT_BLEND_THREADS) {
-    produce<MODE>(c, B, s_dyn, ctl, s0, s1, D, O, T1f, T2f);
-    T = T_start; Cr = Cg = Cb = Dp = 0.f; term = false; processed = 0;
-  } else {
-    consume<MODE>(c, s_dyn, ctl, s0, s1, a, b, beta, snorm, ac, bc, ra, rb, active, T_start, Cr, Cg, Cb, Dp, T, term,
-                  n_eval, n_contrib, processed);
-  }
-  __syncthreads();
-}
-
-template <int MODE>
-__global__ __launch_bounds__(GUT_CTA_THREADS, 3) void blend_kernel(DevCam c, BlendBufs B) {
+__global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, BlendBufs B) {
+  constexpr int NF = WarpTbl<MODE>::NF;
   constexpr int NT = GUT_BLEND_THREADS;
   __shared__ uint32_t s_ticket;
   __shared__ int s_last;
@@ -677,13 +551,12 @@ __global__ __launch_bounds__(GUT_CTA_THREADS, 3) void blend_kernel(DevCam c, Ble
   const int S = len == 0 ? 1 : (int)((len + B.seg - 1) / B.seg);
   const uint32_t s0 = start + (uint32_t)s * B.seg, s1 = min(s0 + (uint32_t)B.seg, end);
   const uint32_t slot = B.seg_base[tile] + (uint32_t)s;
-  const bool is_cons = tid < NT;  // consumer (pixel) thread; the last warp is the producer
-  int px = 0, py = 0;
-  if (is_cons) tile_pixel(tile, c.tiles_x, px, py);
-  const bool inside = is_cons && px < c.width && py < c.height;
+  int px, py;
+  tile_pixel(tile, c.tiles_x, px, py);
+  const bool inside = px < c.width && py < c.height;
 
   // ---- pixel ray (LUT) and the tile anchor in the world frame (fp64)
-  const float4 pl = is_cons ? B.pix[(size_t)tile * NT + tid] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 pl = B.pix[(size_t)tile * NT + tid];
   const float a = pl.x, b = pl.y, snorm = pl.z, beta = pl.w;
   const bool valid = inside && snorm > 0.f;
   const TileAnchor &A = B.anchors[tile];
@@ -729,13 +602,11 @@ __global__ __launch_bounds__(GUT_CTA_THREADS, 3) void blend_kernel(DevCam c, Ble
       run = false;
   }
   // ---- speculative pass: transmittance from 1 (exact for segment 0)
-  extern __shared__ float4 s_dyn[];
-  __shared__ PassCtl s_ctl;
   float Cr, Cg, Cb, Dp, Tsp;
   bool term;
   uint32_t n_eval = 0, n_contrib = 0, processed = 0, n_term = 0;
-  cta_pass<MODE>(c, B, s_dyn, &s_ctl, false, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, run, 1.f, Cr,
-                 Cg, Cb, Dp, Tsp, term, n_eval, n_contrib, processed);
+  warp_pass<MODE>(c, B, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, run, 1.f, Cr, Cg,
+                     Cb, Dp, Tsp, term, n_eval, n_contrib, processed);
   const unsigned long long Ls = term ? GUT_L_DEAD : l_of(Tsp);
   float T_pre = 1.f;
   bool alive_in = valid;
@@ -767,12 +638,12 @@ __global__ __launch_bounds__(GUT_CTA_THREADS, 3) void blend_kernel(DevCam c, Ble
     Cr *= T_pre; Cg *= T_pre; Cb *= T_pre; Dp *= T_pre;
     T_end = T_pre * Tsp;
   }
-  if (__syncthreads_or(redo)) {
+  if (__any_sync(0xffffffffu, redo)) {
     float r0, r1, r2, r3, rT;
     bool rterm;
     uint32_t e2 = 0, c2 = 0, p2 = 0;
-    cta_pass<MODE>(c, B, s_dyn, &s_ctl, true, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, redo, T_pre,
-                   r0, r1, r2, r3, rT, rterm, e2, c2, p2);
+    warp_pass<MODE>(c, B, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, redo, T_pre, r0, r1,
+                       r2, r3, rT, rterm, e2, c2, p2);
     if (redo) { Cr = r0; Cg = r1; Cb = r2; Dp = r3; T_end = rT; term = rterm; }
     processed += p2;
   }
@@ -797,10 +668,8 @@ __global__ __launch_bounds__(GUT_CTA_THREADS, 3) void blend_kernel(DevCam c, Ble
   float Tf = T_end;
   if (S > 1) {
     const size_t j = (size_t)slot * NT + tid;
-    if (is_cons) {
-      B.part_c[j] = alive_in ? make_float4(Cr, Cg, Cb, Dp) : make_float4(0.f, 0.f, 0.f, 0.f);
-      B.part_t[j] = alive_in ? T_end : -1.f;
-    }
+    B.part_c[j] = alive_in ? make_float4(Cr, Cg, Cb, Dp) : make_float4(0.f, 0.f, 0.f, 0.f);
+    B.part_t[j] = alive_in ? T_end : -1.f;
     __threadfence();
     __syncthreads();
     if (tid == 0) s_last = atomicAdd(&B.tile_done[tile], 1u) == (uint32_t)(S - 1);
@@ -810,7 +679,7 @@ __global__ __launch_bounds__(GUT_CTA_THREADS, 3) void blend_kernel(DevCam c, Ble
     const uint32_t first = B.seg_base[tile];
     Cr = Cg = Cb = Dp = 0.f;
     Tf = 1.f;
-    for (int q = 0; q < S && is_cons; ++q) {
+    for (int q = 0; q < S; ++q) {
       const size_t jj = (size_t)(first + q) * NT + tid;
       const float4 pc = __ldcg(&B.part_c[jj]);
       const float pt = __ldcg(&B.part_t[jj]);
@@ -839,13 +708,14 @@ __global__ __launch_bounds__(GUT_CTA_THREADS, 3) void blend_kernel(DevCam c, Ble
 
 template <int MODE>
 static void blend_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
-  constexpr size_t smem = SmemLayout<MODE>::bytes();
+  constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_THREADS / 32) * 2 * 32 * 4 +
+                                            (GUT_BLEND_THREADS / 32) * 32 * WarpTbl<MODE>::NF);
   static bool configured = false;  // per template instance; the attribute is per device function
   if (!configured) {
     cudaFuncSetAttribute(blend_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  blend_kernel<MODE><<<b.max_items, GUT_CTA_THREADS, smem, st>>>(cam, b);
+  blend_kernel<MODE><<<b.max_items, GUT_BLEND_THREADS, smem, st>>>(cam, b);
 }
 
 void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {

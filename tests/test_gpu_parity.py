@@ -42,14 +42,19 @@ def _proj_parity(scene, cam, g, o_proj, opt=OPT):
     # covariance within 1e-3 relative (fp32 pixel coordinates)
     # (the debug record is fp32: add its own representation error, 2 ulp, for
     # the "wide" Gaussians whose fp64 ellipse sits far from the image)
-    for v in ("vx", "vy"):
-        tol = 5e-4 + 2 * np.spacing(np.abs(gp[v][both]).astype(np.float32)).astype(np.float64)
+    # Relative term 1e-6 * extent: R(q) and s are formed from the fp32 inputs on
+    # the GPU, so sigma points differ from the fp64 oracle's by ~1e-7 relative,
+    # which the projection of edge-on Gaussians grazing the near plane (extents
+    # of 10^4 px) amplifies; their tile sets still match bit for bit (above).
+    hx_o, hy_o = o_proj["hx"][both], o_proj["hy"][both]
+    for v, h_o in (("vx", hx_o), ("vy", hy_o)):
+        tol = 5e-4 + 1e-6 * h_o + 2 * np.spacing(np.abs(gp[v][both]).astype(np.float32)).astype(np.float64)
         assert np.all(np.abs(gp[v][both] - o_proj[v][both]) < tol), v
     for f, h in (("cxx", "hx"), ("cyy", "hy")):
         rel = np.abs(gp[f][both] - o_proj[f][both]) / np.abs(o_proj[f][both])
         assert rel.max(initial=0) < 1e-3, f
         hg = np.sqrt(gp["k2"][both].astype(np.float64) * gp[f][both])
-        assert np.all(np.abs(hg - o_proj[h][both]) < 5e-4 + 4e-7 * o_proj[h][both]), h
+        assert np.all(np.abs(hg - o_proj[h][both]) < 5e-4 + 1e-6 * o_proj[h][both]), h
     sc = np.sqrt(o_proj["cxx"][both] * o_proj["cyy"][both])
     assert (np.abs(gp["cxy"][both] - o_proj["cxy"][both]) / sc).max(initial=0) < 1e-3
     rel = np.abs(gp["depth"][both] - o_proj["depth"][both]) / o_proj["depth"][both]

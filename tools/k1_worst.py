@@ -32,6 +32,13 @@ def main(config="mipnerf360", n=60000, factor=0.25, view=0):
               f"cov_rel {abs(g['cxx'][i]-o['cxx'][i])/o['cxx'][i]:.2e} sigma pts max|uv-c| "
               f"{max(abs(u[0]-cam.cx) for u in uv):.1f},{max(abs(u[1]-cam.cy) for u in uv):.1f} "
               f"s {scene.scales[i]} ambig {o['bin_ambig'][i]} tiles {g['tiles'][i]}/{o['tiles'][i]}")
+    hg = np.sqrt(g["k2"][idx].astype(np.float64) * g["cxx"][idx])
+    herr = np.abs(hg - o["hx"][idx])
+    for j in np.argsort(-herr)[:5]:
+        i = idx[j]
+        print(f"h: gid {i} |dh| {herr[j]:.3e} h {o['hx'][i]:.4f} k2 gpu {g['k2'][i]:.7f} orc {o['k2'][i]:.7f} "
+              f"cxx gpu {g['cxx'][i]:.7f} orc {o['cxx'][i]:.7f} sigma {scene.opacities[i]!r} "
+              f"tiles {g['tiles'][i]}/{o['tiles'][i]} ambig {o['bin_ambig'][i]}")
     r.close()
 
 
