@@ -149,8 +149,14 @@ typedef enum {
   GUT_STAGE_DEPTH_ORDER = 2, /* uint32 gid [n_visible], visible Gaussians by (depth, gid) */
   GUT_STAGE_SORTED = 3,  /* uint32 pairs (tile, gid) [n_keys], sorted by (tile, depth, gid) */
   GUT_STAGE_RANGES = 4,  /* uint32 pairs [start, end) [n_tiles] */
-  GUT_STAGE_TILE_WORK = 5 /* uint32 pairs (list length, entries the blend visited before every
-                             pixel of the tile terminated) [n_tiles] */
+  GUT_STAGE_TILE_WORK = 5, /* uint32 pairs (list length, list entries the blend visited summed
+                             over the tile's eight 8x4 pixel blocks, speculation and re-runs
+                             included) [n_tiles] */
+  GUT_STAGE_BLEND_TRACE = 6 /* uint32 x8 per blend work unit (segment slot, 8x4 pixel block):
+                               (tile | segment << 16 | block << 29, SM id, start ns, end ns,
+                               entries visited, pairs evaluated, pairs contributing, re-ran);
+                               all zero for units that did not run; only with env
+                               GUT_BLEND_TRACE=1 */
 } gut_stage;
 
 typedef struct { /* GUT_STAGE_PROJECT record (K1 output, fp32) */

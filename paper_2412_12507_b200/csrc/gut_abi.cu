@@ -37,20 +37,24 @@ struct gut_context {
   uint32_t *sa_k = nullptr, *sa_v = nullptr, *sb_k = nullptr, *sb_v = nullptr;
   uint32_t *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr;
   uint2 *ranges = nullptr, *tile_work = nullptr;
+  uint4 *trace = nullptr;  // K5 per-work-item trace (env GUT_BLEND_TRACE=1, diagnostics only)
+  size_t cap_trace = 0, last_items = 0;
+  bool trace_on = false;
   float *img = nullptr;
   unsigned long long *st_depth = nullptr, *st_emit = nullptr, *st_tile = nullptr;
   uint32_t *counters = nullptr, *h_counters = nullptr;
   // K5: ray LUT (cached per intrinsics for global shutter), blend work plan
   float4 *pix = nullptr;
   TileAnchor *anchors = nullptr;
-  uint32_t *seg_base = nullptr, *tile_done = nullptr;
+  uint32_t *seg_base = nullptr, *granted = nullptr, *next_s = nullptr, *unit_done = nullptr;
+  uint32_t *q1 = nullptr, *q2 = nullptr;  // blend work queues (k5_blend.cu)
   unsigned long long *bstatus = nullptr;
   float *part_t = nullptr;
   float4 *part_c = nullptr;
   size_t cap_items = 0;
   bool lut_valid = false;
   double lut_key[20] = {};
-  int blend_seg = 4096;
+  int blend_seg = 2048, blend_window = 2;  // K5 segment length and speculation window (tools/seg_sweep.sh)
   uint32_t epoch = 0;
   bool reserved = false;
   std::vector<std::array<cudaEvent_t, 7>> tsets;  // per-render stage events (timing = 1)
@@ -131,8 +135,9 @@ static gut_status ensure_tiles(gut_context *ctx, size_t t) {
   CUDA_TRY(ctx, regrow(ctx->pix, dummy, t * GUT_BLEND_THREADS));
   CUDA_TRY(ctx, regrow(ctx->anchors, dummy, t));
   CUDA_TRY(ctx, regrow(ctx->seg_base, dummy, t));
-  CUDA_TRY(ctx, regrow(ctx->tile_done, dummy, t));
-  CUDA_TRY(ctx, cudaMemset(ctx->tile_done, 0, t * sizeof(uint32_t)));
+  CUDA_TRY(ctx, regrow(ctx->granted, dummy, t * GUT_BLEND_WARPS));
+  CUDA_TRY(ctx, regrow(ctx->next_s, dummy, t * GUT_BLEND_WARPS));
+  CUDA_TRY(ctx, regrow(ctx->unit_done, dummy, t * GUT_BLEND_WARPS));
   ctx->lut_valid = false;
   ctx->cap_tiles = t;
   return GUT_OK;
@@ -146,6 +151,12 @@ static gut_status ensure_items(gut_context *ctx, size_t items) {
   CUDA_TRY(ctx, cudaMemset(ctx->bstatus, 0, c * GUT_BLEND_THREADS * sizeof(unsigned long long)));
   CUDA_TRY(ctx, regrow(ctx->part_c, dummy, c * GUT_BLEND_THREADS));
   CUDA_TRY(ctx, regrow(ctx->part_t, dummy, c * GUT_BLEND_THREADS));
+  CUDA_TRY(ctx, regrow(ctx->q1, dummy, c * GUT_BLEND_WARPS));
+  // queue 2: every grant plus one outstanding ticket per resident warp; the
+  // consumers re-zero the slots they take (tickets past the last grant find 0)
+  const size_t q2n = c * GUT_BLEND_WARPS + GUT_BLEND_Q2_SLACK;
+  CUDA_TRY(ctx, regrow(ctx->q2, dummy, q2n));
+  CUDA_TRY(ctx, cudaMemset(ctx->q2, 0, q2n * sizeof(uint32_t)));
   ctx->cap_items = c;
   return GUT_OK;
 }
@@ -290,9 +301,14 @@ gut_status gut_context_create(int32_t dev, gut_context **out) {
   gut_context *ctx = new (std::nothrow) gut_context();
   if (!ctx) return fail(nullptr, GUT_E_OUT_OF_MEMORY, "context");
   ctx->device = dev;
+  if (const char *e = getenv("GUT_BLEND_TRACE")) ctx->trace_on = atoi(e) != 0;
   if (const char *e = getenv("GUT_BLEND_SEG")) {  // tuning knob: list entries per blend work item
     int v = atoi(e);
     if (v >= 256 && v % 256 == 0) ctx->blend_seg = v;
+  }
+  if (const char *e = getenv("GUT_BLEND_WINDOW")) {  // tuning knob: speculative segments in flight per tile
+    int v = atoi(e);
+    if (v >= 1 && v <= 1 << 20) ctx->blend_window = v;
   }
   if (cudaMalloc((void **)&ctx->counters, CNT_WORDS * sizeof(uint32_t)) != cudaSuccess ||
       cudaMallocHost((void **)&ctx->h_counters, CNT_WORDS * sizeof(uint32_t)) != cudaSuccess) {
@@ -309,8 +325,8 @@ void gut_context_destroy(gut_context *ctx) {
   void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->deferred, ctx->payload, ctx->sa_k, ctx->sa_v,
                 ctx->sb_k, ctx->sb_v,
                 ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->tile_work, ctx->img, ctx->st_depth,
-                ctx->st_emit, ctx->st_tile, ctx->counters, ctx->pix, ctx->anchors, ctx->seg_base,
-                ctx->tile_done, ctx->bstatus, ctx->part_c, ctx->part_t};
+                ctx->st_emit, ctx->st_tile, ctx->counters, ctx->pix, ctx->anchors, ctx->seg_base, ctx->granted, ctx->next_s, ctx->q1, ctx->q2,
+                ctx->unit_done, ctx->bstatus, ctx->part_c, ctx->part_t, ctx->trace};
   for (void *p : ps) if (p) cudaFree(p);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
   for (auto &set : ctx->tsets)
@@ -508,7 +524,8 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   const size_t max_items = (size_t)dc.n_tiles + ctx->cap_k / (size_t)ctx->blend_seg + 2;
   if ((s = ensure_items(ctx, max_items)) != GUT_OK) return s;
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->tile_work, 0, (size_t)dc.n_tiles * sizeof(uint2), st));
-  launch_plan(ctx->ranges, dc.n_tiles, ctx->blend_seg, ctx->seg_base, cnt, st);
+  launch_plan(ctx->ranges, dc.n_tiles, ctx->blend_seg, ctx->blend_window, ctx->seg_base, ctx->granted, ctx->next_s,
+              ctx->unit_done, ctx->q1, cnt, st);
   // blend look-back epochs live in 22 bits: clear the status words on wrap
   uint32_t bepoch = ++ctx->epoch;
   if ((bepoch & 0x3FFFFFu) == 0) {
@@ -517,10 +534,22 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   }
   BlendBufs bb;
   bb.ranges = ctx->ranges; bb.gids = fv; bb.payload = ctx->payload; bb.pix = ctx->pix; bb.anchors = ctx->anchors;
-  bb.seg_base = ctx->seg_base; bb.status = ctx->bstatus;
-  bb.part_c = ctx->part_c; bb.part_t = ctx->part_t; bb.tile_done = ctx->tile_done;
-  bb.tile_work = ctx->tile_work; bb.seg = ctx->blend_seg; bb.n_tiles = dc.n_tiles;
-  bb.max_items = (uint32_t)max_items;
+  bb.seg_base = ctx->seg_base; bb.granted = ctx->granted; bb.next_s = ctx->next_s; bb.unit_done = ctx->unit_done;
+  bb.q1 = ctx->q1; bb.q2 = ctx->q2;
+  bb.status = ctx->bstatus;
+  bb.part_c = ctx->part_c; bb.part_t = ctx->part_t;
+  bb.tile_work = ctx->tile_work; bb.seg = ctx->blend_seg; bb.window = ctx->blend_window; bb.n_tiles = dc.n_tiles;
+  bb.trace = nullptr;
+  if (ctx->trace_on) {
+    if (ctx->cap_trace < max_items) {
+      size_t dummy = 0;
+      CUDA_TRY(ctx, regrow(ctx->trace, dummy, 2 * GUT_BLEND_WARPS * max_items));
+      ctx->cap_trace = max_items;
+    }
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->trace, 0, 2 * GUT_BLEND_WARPS * max_items * sizeof(uint4), st));
+    bb.trace = ctx->trace;
+    ctx->last_items = max_items;
+  }
   bb.epoch = bepoch;
   bb.rgb = rgb; bb.alpha = alpha; bb.depth = depth; bb.counters = cnt;
   launch_blend(dc, bb, st);
@@ -621,6 +650,7 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
     case GUT_STAGE_SORTED: need = (size_t)K * 2 * sizeof(uint32_t); break;
     case GUT_STAGE_RANGES:
     case GUT_STAGE_TILE_WORK: need = (size_t)ctx->last_tiles * 2 * sizeof(uint32_t); break;
+    case GUT_STAGE_BLEND_TRACE: need = ctx->trace ? 2 * GUT_BLEND_WARPS * ctx->last_items * sizeof(uint4) : 0; break;
     default: return fail(ctx, GUT_E_INVALID_ARGUMENT, "stage");
   }
   if (bytes_needed) *bytes_needed = need;
@@ -659,6 +689,8 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
     delete[] t; delete[] g;
   } else if (stage == GUT_STAGE_RANGES) {
     CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->ranges, need, cudaMemcpyDeviceToHost));
+  } else if (stage == GUT_STAGE_BLEND_TRACE) {
+    CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->trace, need, cudaMemcpyDeviceToHost));
   } else {
     CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->tile_work, need, cudaMemcpyDeviceToHost));
   }

@@ -243,9 +243,11 @@ __device__ __forceinline__ uint32_t finish_gaussian(const DevCam &c, const Scene
   const f3 rgb = sh_colour<DEG>(s.sh, s.n, i, tof((1.0 / nd) * dw));
   ell[2 * i] = e0;
   ell[2 * i + 1] = e1;
-  // blend payload: mu, sigma, M = diag(1/s) R^T (Eq. 11 o_g = M (o - mu)), rgb
+  // blend payload: mu, k^2 = 2 ln(sigma / alpha_min) (the ellipse record's
+  // value; K5 derives log2 sigma from it), M = diag(1/s) R^T (Eq. 11
+  // o_g = M (o - mu)), rgb
   const float is0 = 1.f / sc.x, is1 = 1.f / sc.y, is2 = 1.f / sc.z;
-  payload[4 * i] = po;
+  payload[4 * i] = make_float4(po.x, po.y, po.z, fabsf(e1.y));
   payload[4 * i + 1] = make_float4(R[0] * is0, R[3] * is0, R[6] * is0, R[1] * is1);
   payload[4 * i + 2] = make_float4(R[4] * is1, R[7] * is1, R[2] * is2, R[5] * is2);
   payload[4 * i + 3] = make_float4(R[8] * is2, rgb.x, rgb.y, rgb.z);

@@ -119,9 +119,8 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-// thread -> pixel of a 16x16 tile: warps on 8x4 pixel blocks (coherent ballots)
-__device__ __forceinline__ void tile_pixel(int tile, int tiles_x, int &px, int &py) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// (warp block w, lane) -> pixel of a 16x16 tile: 8x4 pixel blocks (coherent ballots)
+__device__ __forceinline__ void tile_pixel(int tile, int tiles_x, int w, int lane, int &px, int &py) {
   px = (tile % tiles_x) * GUT_TILE + (w & 1) * 8 + (lane & 7);
   py = (tile / tiles_x) * GUT_TILE + (w >> 1) * 4 + (lane >> 3);
 }
@@ -141,7 +140,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS) void rays_kernel(DevCam c, float
   const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int px, py;
-  tile_pixel(tile, c.tiles_x, px, py);
+  tile_pixel(tile, c.tiles_x, w, lane, px, py);
   const bool inside = px < c.width && py < c.height;
   const double u = px + 0.5, v = py + 0.5;
   d3 dcam = mkd(0, 0, 1), ocam = mkd(0, 0, 0);
@@ -217,51 +216,99 @@ void launch_rays(const DevCam &cam, float4 *pix, TileAnchor *anchors, cudaStream
 
 // ---------------------------------------------------------------- plan
 // Per tile: S_t = max(1, ceil(len / seg)) segments; slots are numbered
-// tile-major (seg_base[t] + s).  Work order: all (t, 0) first, then the deeper
-// segments (t, s >= 1) tile-major; a CTA maps its ticket to (t, s).
-__global__ __launch_bounds__(1024) void plan_kernel(const uint2 *__restrict__ ranges, int n_tiles, int seg,
-                                                    uint32_t *__restrict__ seg_base, uint32_t *counters) {
+// tile-major (seg_base[t] + s).  The unit of work is one warp's 8x4 pixel
+// block of a tile (unit u = 8 t + w) over one segment: warps never wait for
+// each other.  Per unit, min(S_t, window) segments are granted up front
+// (queue 1, tiles in decreasing list length = longest chains first); a
+// completing segment s with pixels still alive grants further segments
+// (queue 2, served first).  The segment index is assigned when a warp takes a
+// unit from a queue (next_s[u]++), so a unit's segments start in order and
+// the look-back only ever waits on segments that are already running.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *s_w, uint32_t &total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t y = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += z;
+    }
+    s_w[lane] = y;
+  }
+  __syncthreads();
+  const uint32_t r = (w > 0 ? s_w[w - 1] : 0) + x - v;
+  total = s_w[31];
+  __syncthreads();
+  return r;
+}
+
+// queue-1 order bucket: decreasing list length (log scale, 1024 buckets)
+__device__ __forceinline__ uint32_t len_bucket(uint32_t len) {
+  const uint32_t key = len == 0 ? 0u : min(1023u, (uint32_t)(log2f((float)len) * 60.f) + 1u);
+  return 1023u - key;
+}
+
+__global__ __launch_bounds__(1024) void plan_kernel(const uint2 *__restrict__ ranges, int n_tiles, int seg, int window,
+                                                    uint32_t *__restrict__ seg_base, uint32_t *__restrict__ granted,
+                                                    uint32_t *__restrict__ next_s, uint32_t *__restrict__ unit_done,
+                                                    uint32_t *__restrict__ q1, uint32_t *counters) {
   __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_hist[1024];
   const int per = (n_tiles + 1023) / 1024;
-  const int t0 = threadIdx.x * per, t1 = min(t0 + per, n_tiles);
+  const int t0 = min((int)threadIdx.x * per, n_tiles), t1 = min(t0 + per, n_tiles);
+  s_hist[threadIdx.x] = 0;
   uint32_t sa = 0;
   for (int t = t0; t < t1; ++t) {
     const uint2 r = ranges[t];
     const uint32_t len = r.y > r.x ? r.y - r.x : 0;
     sa += len == 0 ? 1 : (len + seg - 1) / seg;
   }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t xa = sa;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t ya = __shfl_up_sync(0xffffffffu, xa, o);
-    if (lane >= o) xa += ya;
-  }
-  if (lane == 31) s_w[w] = xa;
-  __syncthreads();
-  if (w == 0) {
-    uint32_t ya = s_w[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t za = __shfl_up_sync(0xffffffffu, ya, o);
-      if (lane >= o) ya += za;
-    }
-    s_w[lane] = ya;
-  }
-  __syncthreads();
-  uint32_t oa = (w > 0 ? s_w[w - 1] : 0) + xa - sa;
+  uint32_t n_slots;
+  uint32_t oa = block_excl_scan(sa, s_w, n_slots);  // (its barriers also order the s_hist reset)
   for (int t = t0; t < t1; ++t) {
     const uint2 r = ranges[t];
     const uint32_t len = r.y > r.x ? r.y - r.x : 0;
+    const uint32_t S = len == 0 ? 1 : (len + seg - 1) / seg;
+    const uint32_t g = min(S, (uint32_t)window);
     seg_base[t] = oa;
-    oa += len == 0 ? 1 : (len + seg - 1) / seg;
+    oa += S;
+    for (int w = 0; w < GUT_BLEND_WARPS; ++w) {
+      granted[GUT_BLEND_WARPS * t + w] = g;
+      next_s[GUT_BLEND_WARPS * t + w] = 0;
+      unit_done[GUT_BLEND_WARPS * t + w] = 0;
+    }
+    atomicAdd(&s_hist[len_bucket(len)], g * GUT_BLEND_WARPS);
   }
-  if (threadIdx.x == 1023) counters[CNT_NITEMS] = oa;
+  __syncthreads();
+  uint32_t n_init;
+  const uint32_t off = block_excl_scan(s_hist[threadIdx.x], s_w, n_init);
+  s_hist[threadIdx.x] = off;
+  __syncthreads();
+  for (int t = t0; t < t1; ++t) {
+    const uint2 r = ranges[t];
+    const uint32_t len = r.y > r.x ? r.y - r.x : 0;
+    const uint32_t S = len == 0 ? 1 : (len + seg - 1) / seg;
+    const uint32_t g = min(S, (uint32_t)window);
+    const uint32_t pos = atomicAdd(&s_hist[len_bucket(len)], g * GUT_BLEND_WARPS);
+    for (uint32_t k = 0; k < g * GUT_BLEND_WARPS; ++k) q1[pos + k] = GUT_BLEND_WARPS * (uint32_t)t + k % GUT_BLEND_WARPS;
+  }
+  if (threadIdx.x == 0) {
+    counters[CNT_NITEMS] = n_slots;
+    counters[CNT_Q_NINIT] = n_init;
+  }
 }
 
-void launch_plan(const uint2 *ranges, int n_tiles, int seg, uint32_t *seg_base, uint32_t *counters,
-                 cudaStream_t st) {
-  plan_kernel<<<1, 1024, 0, st>>>(ranges, n_tiles, seg, seg_base, counters);
+void launch_plan(const uint2 *ranges, int n_tiles, int seg, int window, uint32_t *seg_base, uint32_t *granted,
+                 uint32_t *next_s, uint32_t *unit_done, uint32_t *q1, uint32_t *counters, cudaStream_t st) {
+  plan_kernel<<<1, 1024, 0, st>>>(ranges, n_tiles, seg, window, seg_base, granted, next_s, unit_done, q1, counters);
 }
 
 // ---------------------------------------------------------------- blend
@@ -285,6 +332,25 @@ __device__ __forceinline__ unsigned long long st_word(uint32_t flag, uint32_t ep
   return ((unsigned long long)flag << 62) | ((unsigned long long)(epoch & 0x3FFFFFu) << 40) | L;
 }
 
+// True if the pixel is certainly dead before segment s: the published
+// products of some of its predecessors (aggregates back to the first
+// inclusive word, at most 4) already multiply below 2^-16 < T_min.  Any
+// subset of the prefix factors bounds the prefix from above, so words not yet
+// published are simply skipped.
+__device__ __forceinline__ bool pred_dead(const unsigned long long *stat, int s, uint32_t epoch) {
+  unsigned long long L = 0;
+  const int jmax = min(s, 4);
+  for (int j = 1; j <= jmax; ++j) {
+    const unsigned long long wv = ld_relaxed(stat - (size_t)j * GUT_BLEND_THREADS);
+    const uint32_t flag = (uint32_t)(wv >> 62);
+    if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (epoch & 0x3FFFFFu)) continue;
+    L += wv & ((1ull << 40) - 1);
+    if (L >= GUT_L_DEAD) return true;
+    if (flag == 2) break;
+  }
+  return false;
+}
+
 // Per-warp table of staged list entries (32 per chunk).  MODE 0/1: the
 // quadratic forms of F = |n|^2 - k^2 |e|^2 and D = |e|^2 in the lane's pixel
 // offset (da, db) from the warp box centre; MODE 2 (rolling shutter, beta
@@ -303,6 +369,11 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -321,15 +392,18 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
                                           const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f, float a, float b,
                                           float beta, float snorm, float ac, float bc, float ra, float rb, bool active,
                                           float T_start, float &Cr, float &Cg, float &Cb, float &Dp, float &T,
-                                          bool &term, uint32_t &n_eval, uint32_t &n_contrib, uint32_t &processed) {
+                                          bool &term, uint32_t &n_eval, uint32_t &n_contrib, uint32_t &processed,
+                                          const unsigned long long *poll_stat, int poll_s) {
   constexpr int NF = WarpTbl<MODE>::NF;
   // dynamic shared memory: [raw payload double buffer: 8 warps x 2 x 32 x 4]
   // [per-warp entry table: 8 warps x 32 x NF]
   extern __shared__ float4 s_dyn[];
   constexpr int RAW = (GUT_BLEND_THREADS / 32) * 2 * 32 * 4;
   float4 *__restrict__ wt = s_dyn + RAW + (threadIdx.x >> 5) * 32 * NF;
+  const uint32_t wt_s = (uint32_t)__cvta_generic_to_shared(wt);
   const int lane = threadIdx.x & 31;
   const float alpha_min = c.alpha_min, alpha_max = c.alpha_max, t_min = c.t_min;
+  const float l2amin = log2f(alpha_min);
   const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
   // raw payload of the warp's current / next chunk (cp.async double buffer)
   float4 *__restrict__ raw = s_dyn + (threadIdx.x >> 5) * 2 * 32 * 4;
@@ -349,6 +423,12 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   gnext = s0 + 32 + lane < s1 ? __ldg(&B.gids[s0 + 32 + lane]) : 0u;
   int buf = 0;
   for (uint32_t b0 = s0; b0 < s1; b0 += 32, buf ^= 1) {
+    // speculative pass of a later segment: every 2 chunks, drop pixels whose
+    // predecessors have meanwhile published a dead prefix (Ls := dead, exact)
+    if (poll_stat && ((b0 - s0) & 63u) == 32u && !done && pred_dead(poll_stat, poll_s, B.epoch)) {
+      done = true;
+      term = true;
+    }
     if (__all_sync(0xffffffffu, done)) break;
     if (b0 + 32 < s1) {  // prefetch the next chunk
       if (b0 + 32 + lane < s1) {
@@ -384,9 +464,9 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
       } else {
         P = cross(ogf, U); Q = cross(ogf, V); gu = dot(ogf, U); gv = dot(ogf, V);
       }
-      // k^2 = 2 ln(sigma/alpha_min) via log1p (accurate for sigma near alpha_min)
-      const float k2 = 2.f * log1pf((p0.w - alpha_min) / alpha_min);
-      const float l2s = log2f(p0.w);
+      // k^2 = 2 ln(sigma/alpha_min) (K1, via log1p); log2 sigma = k^2 / (2 ln 2) + log2 alpha_min
+      const float k2 = p0.w;
+      const float l2s = fmaf(k2, 0.72134752044448170f, l2amin);
       // ---- conservative cull against the warp's pixel box (a in ac +- ra,
       // b in bc +- rb): |n| >= |n(ac,bc)| - ra|P| - rb|Q|, |e| <= |e(ac,bc)| +
       // ra|U| + rb|V| (triangle inequality); omega^2 > k^2 on the whole box if
@@ -440,25 +520,42 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           const float D0 = dot(es, es), Da = 2.f * dot(es, U), Db = 2.f * dot(es, V);
           const float Daa = dot(U, U), Dab = 2.f * dot(U, V), Dbb = dot(V, V);
           const float gs = (float)g0 + as * gu + bs * gv;
-          t[0] = make_float4(fmaf(-k2, D0, N0), fmaf(-k2, Da, Na), fmaf(-k2, Db, Nb), fmaf(-k2, Daa, pp));
-          t[1] = make_float4(fmaf(-k2, Dab, Nab), fmaf(-k2, Dbb, qq), as, bs);
-          t[2] = make_float4(D0, Da, Db, Daa);
-          t[3] = make_float4(Dab, Dbb, gs, gu);
-          t[4] = make_float4(gv, k2, l2s, 0.f);
-          t[5] = make_float4(p3.y, p3.z, p3.w, 0.f);
+          const float F0 = fmaf(-k2, D0, N0), Fa = fmaf(-k2, Da, Na), Fb = fmaf(-k2, Db, Nb);
+          const float Faa = fmaf(-k2, Daa, pp), Fab = fmaf(-k2, Dab, Nab), Fbb = fmaf(-k2, Dbb, qq);
+          // second, tighter cull: a lower bound of the quadratic F over the box
+          // (offsets da in [la, ha], db in [lb, hb] from (a*, b*)) as the sum of
+          // the exact 1-D minima of the a- and b-parts and the worst cross term;
+          // margin 1e-4 of the terms' magnitude for fp32 rounding
+          const float la = ac - ra - as, ha = ac + ra - as, lb = bc - rb - bs, hb = bc + rb - bs;
+          const float A = fmaxf(-la, ha), Bm = fmaxf(-lb, hb);
+          const float xa_ = Faa > 0.f ? fminf(fmaxf(-0.5f * Fa / Faa, la), ha) : (Fa > 0.f ? la : ha);
+          const float xb_ = Fbb > 0.f ? fminf(fmaxf(-0.5f * Fb / Fbb, lb), hb) : (Fb > 0.f ? lb : hb);
+          const float ma = fminf(xa_ * fmaf(Faa, xa_, Fa), fminf(la * fmaf(Faa, la, Fa), ha * fmaf(Faa, ha, Fa)));
+          const float mb = fminf(xb_ * fmaf(Fbb, xb_, Fb), fminf(lb * fmaf(Fbb, lb, Fb), hb * fmaf(Fbb, hb, Fb)));
+          const float mab = fabsf(Fab) * A * Bm;
+          const float mag = fabsf(F0) + fabsf(Fa) * A + fabsf(Fb) * Bm + (fabsf(Faa) * A + fabsf(Fab) * Bm) * A +
+                            fabsf(Fbb) * Bm * Bm;
+          maybe = !(F0 + ma + mb - mab > 1e-4f * mag);
+          if (maybe) {
+            t[0] = make_float4(F0, Fa, Fb, Faa);
+            t[1] = make_float4(Fab, Fbb, as, bs);
+            t[2] = make_float4(D0, Da, Db, Daa);
+            t[3] = make_float4(Dab, Dbb, gs, gu);
+            t[4] = make_float4(gv, k2, l2s, 0.f);
+            t[5] = make_float4(p3.y, p3.z, p3.w, 0.f);
+          }
         }
       }
     }
     uint32_t m = __ballot_sync(0xffffffffu, maybe);
     __syncwarp();
-    while (m) {
-      const int j = __ffs(m) - 1;
-      m &= m - 1;
-      if (done) continue;
-      ++n_eval;
-      const float4 *t = wt + j * NF;
-      float w2, rD, gg, k2;
-      if (MODE == 2) {
+    if (MODE == 2) {
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        if (done) continue;
+        ++n_eval;
+        const float4 *t = wt + j * NF;
         const float4 f0 = t[0], f1 = t[1], f2 = t[2], f3v = t[3], f4 = t[4];
         const float4 h = t[7], pu = t[8], qv = t[9];
         float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
@@ -472,46 +569,70 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
         const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
         const float N = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
         const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
-        k2 = f0.w;
+        const float k2 = f0.w;
         if (N > k2 * Dd) continue;  // omega^2 > k^2  <=>  alpha < alpha_min
-        rD = rcp_approx(Dd);
-        w2 = N * rD;
+        const float rD = rcp_approx(Dd);
+        const float w2 = N * rD;
         const float4 f5 = t[5];
-        gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
+        float gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
         gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
-      } else {
-        const float4 f0 = t[0], f1 = t[1];
+        // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
+        const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, f4.w)));
+        if (!(al >= alpha_min)) continue;
+        const float tau = -gg * rD * snorm;
+        if (!(tau > 0.f)) continue;  // reading R24
+        const float Tn = T * (1.f - al);
+        if (Tn < t_min) {
+          done = true;
+          term = true;
+          continue;
+        }
+        const float4 cc = t[6];
+        const float wgt = al * T;
+        Cr = fmaf(wgt, cc.x, Cr);
+        Cg = fmaf(wgt, cc.y, Cg);
+        Cb = fmaf(wgt, cc.z, Cb);
+        Dp = fmaf(wgt, tau, Dp);
+        ++n_contrib;
+        T = Tn;
+      }
+    } else {
+      // one iteration per surviving entry; lanes predicated, the body skipped
+      // (warp-uniform branch) when no lane's pixel is inside the footprint
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t ta = wt_s + (uint32_t)j * (NF * 16);
+        const float4 f0 = lds128(ta), f1 = lds128(ta + 16);
+        n_eval += done ? 0u : 1u;
         const float da = a - f1.z, db = b - f1.w;
         // F = N - k^2 D <= 0  <=>  omega^2 <= k^2  <=>  alpha >= alpha_min
         const float F = fmaf(da, fmaf(f0.w, da, fmaf(f1.x, db, f0.y)), fmaf(db, fmaf(f1.y, db, f0.z), f0.x));
-        if (F > 0.f) continue;
-        const float4 f2 = t[2], f3v = t[3], f4 = t[4];
+        const bool hit = !done && F <= 0.f;
+        if (!__any_sync(0xffffffffu, hit)) continue;
+        const float4 f2 = lds128(ta + 32), f3v = lds128(ta + 48), f4 = lds128(ta + 64);
         const float Dd = fmaf(da, fmaf(f2.w, da, fmaf(f3v.x, db, f2.y)), fmaf(db, fmaf(f3v.y, db, f2.z), f2.x));
-        k2 = f4.y;
-        rD = rcp_approx(Dd);
-        w2 = fmaxf(fmaf(k2, Dd, F), 0.f) * rD;
-        gg = fmaf(da, f3v.w, fmaf(db, f4.x, f3v.z));
+        const float rD = rcp_approx(Dd);
+        const float w2 = fmaxf(fmaf(f4.y, Dd, F), 0.f) * rD;
+        const float gg = fmaf(da, f3v.w, fmaf(db, f4.x, f3v.z));
+        // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
+        const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, f4.z)));
+        const float tau = -gg * rD * snorm;
+        const float Tn = T * (1.f - al);
+        const bool ok = hit && al >= alpha_min && tau > 0.f;  // reading R24: tau > 0
+        const bool dead = ok && Tn < t_min;
+        if (dead) { done = true; term = true; }
+        if (ok && !dead) {
+          const float4 cc = lds128(ta + 80);
+          const float wgt = al * T;
+          Cr = fmaf(wgt, cc.x, Cr);
+          Cg = fmaf(wgt, cc.y, Cg);
+          Cb = fmaf(wgt, cc.z, Cb);
+          Dp = fmaf(wgt, tau, Dp);
+          ++n_contrib;
+          T = Tn;
+        }
       }
-      const float l2s = MODE == 2 ? t[4].w : t[4].z;
-      // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
-      const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, l2s)));
-      if (!(al >= alpha_min)) continue;
-      const float tau = -gg * rD * snorm;
-      if (!(tau > 0.f)) continue;  // reading R24
-      const float Tn = T * (1.f - al);
-      if (Tn < t_min) {
-        done = true;
-        term = true;
-        continue;
-      }
-      const float4 cc = MODE == 2 ? t[6] : t[5];
-      const float wgt = al * T;
-      Cr = fmaf(wgt, cc.x, Cr);
-      Cg = fmaf(wgt, cc.y, Cg);
-      Cb = fmaf(wgt, cc.z, Cb);
-      Dp = fmaf(wgt, tau, Dp);
-      ++n_contrib;
-      T = Tn;
     }
     __syncwarp();
   }
@@ -519,189 +640,287 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   __syncwarp();
 }
 
+// Work queue (lane 0 of a warp).  Queue 2 (granted successors of running
+// chains) is served before queue 1 (initial grants).  Both hand out tickets
+// with one atomicAdd (no CAS retry storms among thousands of warps); a warp
+// holding a queue-2 ticket whose slot is not yet written waits on that slot
+// alone (backoff), and leaves once every unit has been written.  The segment
+// index is assigned here, in hand-out order per unit.
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ bool fetch_work(const BlendBufs &B, int &unit, int &s) {
+  uint32_t *cnt = B.counters;
+  const uint32_t n_init = cnt[CNT_Q_NINIT];
+  const uint32_t n_units = (uint32_t)B.n_tiles * GUT_BLEND_WARPS;
+  for (;;) {
+    const bool q1_empty = ld_volatile_u32(&cnt[CNT_Q_HEAD1]) >= n_init;
+    if (q1_empty || ld_volatile_u32(&cnt[CNT_Q_HEAD2]) < ld_volatile_u32(&cnt[CNT_Q_ALLOC2])) {
+      const uint32_t t2 = atomicAdd(&cnt[CNT_Q_HEAD2], 1u);
+      uint32_t u1;
+      for (int k = 0; (u1 = ld_volatile_u32(&B.q2[t2])) == 0; ++k) {
+        if ((k & 7) == 7 && ld_volatile_u32(&cnt[CNT_Q_FINISHED]) >= n_units) return false;
+        __nanosleep(k < 4 ? 64 : 512);
+      }
+      B.q2[t2] = 0;  // slot reusable by the next render
+      unit = (int)(u1 - 1);
+      s = (int)atomicAdd(&B.next_s[unit], 1u);
+      return true;
+    }
+    const uint32_t h1 = atomicAdd(&cnt[CNT_Q_HEAD1], 1u);
+    if (h1 < n_init) {
+      unit = (int)B.q1[h1];
+      s = (int)atomicAdd(&B.next_s[unit], 1u);
+      return true;
+    }
+  }
+}
+
+// Persistent CTAs (as many as fit), each warp looping independently over
+// work units (tile, warp block, segment) taken from the queues.  Per unit:
+// the lane's pixel, the speculative pass, the look-back, the redo, then either
+// the pixel write (single-segment tile) or the partials, the successor grants
+// and, in the warp completing the unit's last granted segment, the in-order
+// combine.  No CTA-wide barriers: a warp whose pixels finish early moves on.
 template <int MODE>
 __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, BlendBufs B) {
-  constexpr int NF = WarpTbl<MODE>::NF;
   constexpr int NT = GUT_BLEND_THREADS;
-  __shared__ uint32_t s_ticket;
-  __shared__ int s_last;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  uint32_t n_eval_acc = 0, n_contrib_acc = 0, n_term_acc = 0;
 
-  const int tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) s_ticket = atomicAdd(&B.counters[CNT_TICKET_BLEND], 1u);
-  __syncthreads();
-  const uint32_t ticket = s_ticket;
-  if (ticket >= B.counters[CNT_NITEMS]) return;
-  // ---- ticket -> (tile, segment): all segment-0 items first, then the rest tile-major
-  int tile, s;
-  if (ticket < (uint32_t)B.n_tiles) {
-    tile = (int)ticket;
-    s = 0;
-  } else {
-    const uint32_t q = ticket - (uint32_t)B.n_tiles;
-    int lo = 0, hi = B.n_tiles - 1;  // last t with seg_base[t] - t <= q
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (B.seg_base[mid] - (uint32_t)mid <= q) lo = mid; else hi = mid - 1;
+  for (;;) {
+    int unit = -1, s = 0;
+    if (lane == 0 && !fetch_work(B, unit, s)) unit = -1;
+    unit = __shfl_sync(FULL, unit, 0);
+    s = __shfl_sync(FULL, s, 0);
+    if (unit < 0) break;
+    const int tile = unit / GUT_BLEND_WARPS, w = unit % GUT_BLEND_WARPS;
+    unsigned long long t_begin = 0;
+    if (B.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+
+    const uint2 rg = B.ranges[tile];
+    const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x, len = end - start;
+    const int S = len == 0 ? 1 : (int)((len + B.seg - 1) / B.seg);
+    const uint32_t s0 = start + (uint32_t)s * B.seg, s1 = min(s0 + (uint32_t)B.seg, end);
+    const uint32_t slot = B.seg_base[tile] + (uint32_t)s;
+    const int pidx = w * 32 + lane;  // pixel of the tile (LUT, status and partial index)
+    int px, py;
+    tile_pixel(tile, c.tiles_x, w, lane, px, py);
+    const bool inside = px < c.width && py < c.height;
+
+    // ---- pixel ray (LUT) and the tile anchor in the world frame (fp64)
+    const float4 pl = B.pix[(size_t)tile * NT + pidx];
+    const float a = pl.x, b = pl.y, snorm = pl.z, beta = pl.w;
+    const bool valid = inside && snorm > 0.f;
+    const TileAnchor &A = B.anchors[tile];
+    d3 D, T1, T2, O;
+    if (MODE == 2) {
+      D = mkd(A.D[0], A.D[1], A.D[2]); T1 = mkd(A.T1[0], A.T1[1], A.T1[2]);
+      T2 = mkd(A.T2[0], A.T2[1], A.T2[2]); O = mkd(A.O[0], A.O[1], A.O[2]);
+    } else {
+      D = mv(c.R0, mkd(A.D[0], A.D[1], A.D[2]));
+      T1 = mv(c.R0, mkd(A.T1[0], A.T1[1], A.T1[2]));
+      T2 = mv(c.R0, mkd(A.T2[0], A.T2[1], A.T2[2]));
+      O = mkd(c.c0[0], c.c0[1], c.c0[2]);
+      if (MODE == 1) O = O + mv(c.R0, mkd(A.O[0], A.O[1], A.O[2]));
     }
-    tile = lo;
-    s = 1 + (int)(q - (B.seg_base[lo] - (uint32_t)lo));
-  }
-  const uint2 rg = B.ranges[tile];
-  const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x, len = end - start;
-  const int S = len == 0 ? 1 : (int)((len + B.seg - 1) / B.seg);
-  const uint32_t s0 = start + (uint32_t)s * B.seg, s1 = min(s0 + (uint32_t)B.seg, end);
-  const uint32_t slot = B.seg_base[tile] + (uint32_t)s;
-  int px, py;
-  tile_pixel(tile, c.tiles_x, px, py);
-  const bool inside = px < c.width && py < c.height;
-
-  // ---- pixel ray (LUT) and the tile anchor in the world frame (fp64)
-  const float4 pl = B.pix[(size_t)tile * NT + tid];
-  const float a = pl.x, b = pl.y, snorm = pl.z, beta = pl.w;
-  const bool valid = inside && snorm > 0.f;
-  const TileAnchor &A = B.anchors[tile];
-  d3 D, T1, T2, O;
-  if (MODE == 2) {
-    D = mkd(A.D[0], A.D[1], A.D[2]); T1 = mkd(A.T1[0], A.T1[1], A.T1[2]);
-    T2 = mkd(A.T2[0], A.T2[1], A.T2[2]); O = mkd(A.O[0], A.O[1], A.O[2]);
-  } else {
-    D = mv(c.R0, mkd(A.D[0], A.D[1], A.D[2]));
-    T1 = mv(c.R0, mkd(A.T1[0], A.T1[1], A.T1[2]));
-    T2 = mv(c.R0, mkd(A.T2[0], A.T2[1], A.T2[2]));
-    O = mkd(c.c0[0], c.c0[1], c.c0[2]);
-    if (MODE == 1) O = O + mv(c.R0, mkd(A.O[0], A.O[1], A.O[2]));
-  }
-  const f3 T1f = tof(T1), T2f = tof(T2);
-  // warp pixel box in (a, b) for the conservative warp cull
-  float ac, bc, ra, rb;
-  {
-    float amin = valid ? a : 3e38f, amax = valid ? a : -3e38f;
-    float bmin = valid ? b : 3e38f, bmax = valid ? b : -3e38f;
+    const f3 T1f = tof(T1), T2f = tof(T2);
+    // warp pixel box in (a, b) for the conservative warp cull
+    float ac, bc, ra, rb;
+    {
+      float amin = valid ? a : 3e38f, amax = valid ? a : -3e38f;
+      float bmin = valid ? b : 3e38f, bmax = valid ? b : -3e38f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      amin = fminf(amin, __shfl_xor_sync(0xffffffffu, amin, o));
-      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-      bmin = fminf(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
-      bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
-    }
-    if (amin > amax) { amin = amax = 0.f; bmin = bmax = 0.f; }  // no valid pixel: the warp is idle
-    ac = 0.5f * (amin + amax);
-    bc = 0.5f * (bmin + bmax);
-    ra = 0.5f * (amax - amin) + 1e-7f * (fabsf(amin) + fabsf(amax));
-    rb = 0.5f * (bmax - bmin) + 1e-7f * (fabsf(bmin) + fabsf(bmax));
-  }
-  if (s == 0 && tid == 0 && len > 0) atomicMax(&B.counters[CNT_MAXLEN], len);
-  unsigned long long *stat = B.status + (size_t)slot * NT + tid;
-
-  // ---- predecessor peek: pixels already known dead are skipped (same result)
-  bool run = valid;
-  if (s > 0 && valid) {
-    const unsigned long long wv = ld_relaxed(stat - NT);
-    if ((uint32_t)(wv >> 62) == 2u && (uint32_t)((wv >> 40) & 0x3FFFFFu) == (B.epoch & 0x3FFFFFu) &&
-        t_of(wv & ((1ull << 40) - 1)) < c.t_min)
-      run = false;
-  }
-  // ---- speculative pass: transmittance from 1 (exact for segment 0)
-  float Cr, Cg, Cb, Dp, Tsp;
-  bool term;
-  uint32_t n_eval = 0, n_contrib = 0, processed = 0, n_term = 0;
-  warp_pass<MODE>(c, B, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, run, 1.f, Cr, Cg,
-                     Cb, Dp, Tsp, term, n_eval, n_contrib, processed);
-  const unsigned long long Ls = term ? GUT_L_DEAD : l_of(Tsp);
-  float T_pre = 1.f;
-  bool alive_in = valid;
-  if (S > 1) {
-    unsigned long long Lpre = 0;
-    if (s == 0) {
-      if (valid) st_relaxed(stat, st_word(2, B.epoch, Ls));
-    } else if (valid) {
-      st_relaxed(stat, st_word(1, B.epoch, Ls));
-      // decoupled look-back over this pixel's earlier segments (integer sums)
-      for (int j = s - 1;; --j) {
-        const unsigned long long wv = ld_relaxed(stat - (size_t)(s - j) * NT);
-        const uint32_t flag = (uint32_t)(wv >> 62);
-        if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (B.epoch & 0x3FFFFFu)) { ++j; continue; }
-        Lpre += wv & ((1ull << 40) - 1);
-        if (Lpre >= GUT_L_DEAD) { Lpre = GUT_L_DEAD; break; }
-        if (flag == 2) break;
+      for (int o = 16; o > 0; o >>= 1) {
+        amin = fminf(amin, __shfl_xor_sync(FULL, amin, o));
+        amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, o));
+        bmin = fminf(bmin, __shfl_xor_sync(FULL, bmin, o));
+        bmax = fmaxf(bmax, __shfl_xor_sync(FULL, bmax, o));
       }
-      const unsigned long long Lin = Lpre + Ls >= GUT_L_DEAD ? GUT_L_DEAD : Lpre + Ls;
-      st_relaxed(stat, st_word(2, B.epoch, Lin));
+      if (amin > amax) { amin = amax = 0.f; bmin = bmax = 0.f; }  // no valid pixel: the warp is idle
+      ac = 0.5f * (amin + amax);
+      bc = 0.5f * (bmin + bmax);
+      ra = 0.5f * (amax - amin) + 1e-7f * (fabsf(amin) + fabsf(amax));
+      rb = 0.5f * (bmax - bmin) + 1e-7f * (fabsf(bmin) + fabsf(bmax));
     }
-    T_pre = t_of(Lpre);
-    alive_in = valid && T_pre >= c.t_min;
-  }
-  // ---- exact result: scale the speculative sums, or redo the segment from T_pre
-  const bool redo = alive_in && s > 0 && (term || T_pre * Tsp < c.t_min);
-  float T_end = Tsp;
-  if (s > 0 && alive_in && !redo) {
-    Cr *= T_pre; Cg *= T_pre; Cb *= T_pre; Dp *= T_pre;
-    T_end = T_pre * Tsp;
-  }
-  if (__any_sync(0xffffffffu, redo)) {
-    float r0, r1, r2, r3, rT;
-    bool rterm;
-    uint32_t e2 = 0, c2 = 0, p2 = 0;
-    warp_pass<MODE>(c, B, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, redo, T_pre, r0, r1,
-                       r2, r3, rT, rterm, e2, c2, p2);
-    if (redo) { Cr = r0; Cg = r1; Cb = r2; Dp = r3; T_end = rT; term = rterm; }
-    processed += p2;
-  }
-  n_term = (alive_in && term) ? 1u : 0u;
+    if (s == 0 && w == 0 && lane == 0 && len > 0) atomicMax(&B.counters[CNT_MAXLEN], len);
+    unsigned long long *stat = B.status + (size_t)slot * NT + pidx;
 
-  // ---- statistics
-  if (tid == 0) {
-    atomicAdd(&B.tile_work[tile].y, processed);
-    if (s == 0) B.tile_work[tile].x = len;
+    // ---- predecessor peek: pixels already known dead are skipped (same result)
+    bool run = valid;
+    if (s > 0 && valid && pred_dead(stat, s, B.epoch)) run = false;
+    // ---- speculative pass: transmittance from 1 (exact for segment 0)
+    float Cr, Cg, Cb, Dp, Tsp;
+    bool term;
+    uint32_t n_eval = 0, n_contrib = 0, processed = 0;
+    warp_pass<MODE>(c, B, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, run, 1.f, Cr, Cg,
+                    Cb, Dp, Tsp, term, n_eval, n_contrib, processed, s > 0 ? stat : nullptr, s);
+    const unsigned long long Ls = (term || (valid && !run)) ? GUT_L_DEAD : l_of(Tsp);
+    float T_pre = 1.f;
+    bool alive_in = valid;
+    if (S > 1) {
+      unsigned long long Lpre = 0;
+      if (s == 0) {
+        if (valid) st_relaxed(stat, st_word(2, B.epoch, Ls));
+      } else if (valid) {
+        st_relaxed(stat, st_word(1, B.epoch, Ls));
+        // decoupled look-back over this pixel's earlier segments (integer sums)
+        for (int j = s - 1;; --j) {
+          const unsigned long long wv = ld_relaxed(stat - (size_t)(s - j) * NT);
+          const uint32_t flag = (uint32_t)(wv >> 62);
+          if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (B.epoch & 0x3FFFFFu)) {
+            __nanosleep(256);  // predecessor still running: yield issue slots to the SM's other warps
+            ++j;
+            continue;
+          }
+          Lpre += wv & ((1ull << 40) - 1);
+          if (Lpre >= GUT_L_DEAD) { Lpre = GUT_L_DEAD; break; }
+          if (flag == 2) break;
+        }
+        const unsigned long long Lin = Lpre + Ls >= GUT_L_DEAD ? GUT_L_DEAD : Lpre + Ls;
+        st_relaxed(stat, st_word(2, B.epoch, Lin));
+      }
+      T_pre = t_of(Lpre);
+      alive_in = valid && T_pre >= c.t_min;
+    }
+    // ---- exact result: scale the speculative sums, or redo the segment from T_pre
+    const bool redo = alive_in && s > 0 && (term || T_pre * Tsp < c.t_min);
+    float T_end = Tsp;
+    if (s > 0 && alive_in && !redo) {
+      Cr *= T_pre; Cg *= T_pre; Cb *= T_pre; Dp *= T_pre;
+      T_end = T_pre * Tsp;
+    }
+    const bool wredo = __any_sync(FULL, redo);
+    if (wredo) {
+      float r0, r1, r2, r3, rT;
+      bool rterm;
+      uint32_t e2 = 0, c2 = 0, p2 = 0;
+      warp_pass<MODE>(c, B, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, redo, T_pre, r0, r1,
+                      r2, r3, rT, rterm, e2, c2, p2, nullptr, 0);
+      if (redo) { Cr = r0; Cg = r1; Cb = r2; Dp = r3; T_end = rT; term = rterm; }
+      processed += p2;
+    }
+    n_eval_acc += n_eval;
+    n_contrib_acc += n_contrib;
+    n_term_acc += (alive_in && term) ? 1u : 0u;
+    if (lane == 0) {
+      atomicAdd(&B.tile_work[tile].y, processed);
+      if (s == 0 && w == 0) B.tile_work[tile].x = len;
+    }
+    if (B.trace) {
+      const uint32_t e1 = warp_sum(n_eval), e2 = warp_sum(n_contrib);
+      if (lane == 0) {
+        unsigned long long t_end;
+        uint32_t smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        const size_t ti = 2 * ((size_t)slot * GUT_BLEND_WARPS + w);
+        B.trace[ti] = make_uint4((uint32_t)tile | ((uint32_t)s << 16) | ((uint32_t)w << 29), smid,
+                                 (uint32_t)t_begin, (uint32_t)t_end);
+        B.trace[ti + 1] = make_uint4(processed, e1, e2, wredo ? 1u : 0u);
+      }
+    }
+
+    // ---- outputs: single segment -> pixels; else partials, successor grants,
+    // and the in-order combine by the warp completing the unit's last granted segment
+    float Tf = T_end;
+    bool write = true;
+    if (S > 1) {
+      const size_t j = (size_t)slot * NT + pidx;
+      B.part_c[j] = alive_in ? make_float4(Cr, Cg, Cb, Dp) : make_float4(0.f, 0.f, 0.f, 0.f);
+      B.part_t[j] = alive_in ? T_end : -1.f;
+      const bool alive_out = alive_in && !term && T_end >= c.t_min;
+      float tmax = alive_out ? T_end : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(FULL, tmax, o));
+      __threadfence();  // partials visible before the completion count
+      __syncwarp();
+      uint32_t nseg = 0;
+      if (lane == 0) {
+        if (tmax > 0.f) {
+          // grant segments up to s + max(window, the depth the slowest pixel of
+          // the block still needs at its decay so far) (queue 2)
+          int ahead = B.window;
+          const float n_done = (float)((uint32_t)(s + 1) * (uint32_t)B.seg);
+          const float decay = -__logf(tmax);  // over n_done entries
+          if (decay < 1e-3f * n_done / (float)B.seg) {
+            ahead = S;
+          } else {
+            const float rem = n_done * __logf(tmax / c.t_min) / decay;
+            ahead = max(ahead, (int)fminf(rem / (float)B.seg + 1.f, (float)S));
+          }
+          const uint32_t target = (uint32_t)min(S, s + 1 + ahead);
+          uint32_t g = ld_volatile_u32(&B.granted[unit]);
+          while (g < target) {
+            const uint32_t prev = atomicCAS(&B.granted[unit], g, target);
+            if (prev == g) {
+              const uint32_t n = target - g, pos = atomicAdd(&B.counters[CNT_Q_ALLOC2], n);
+              for (uint32_t k = 0; k < n; ++k) atomicExch(&B.q2[pos + k], (uint32_t)unit + 1u);
+              break;
+            }
+            g = prev;
+          }
+        }
+        __threadfence();
+        const uint32_t d = atomicAdd(&B.unit_done[unit], 1u) + 1u;
+        __threadfence();
+        const uint32_t g = ld_volatile_u32(&B.granted[unit]);
+        nseg = d == g ? g : 0u;
+      }
+      nseg = __shfl_sync(FULL, nseg, 0);
+      write = nseg != 0;
+      if (write) {
+        __threadfence();
+        const uint32_t first = B.seg_base[tile];
+        Cr = Cg = Cb = Dp = 0.f;
+        Tf = 1.f;
+#pragma unroll 8
+        for (uint32_t q = 0; q < nseg; ++q) {  // (unrolled: loads in flight, sums in order)
+          const size_t jj = (size_t)(first + q) * NT + pidx;
+          const float4 pc = __ldcg(&B.part_c[jj]);
+          const float pt = __ldcg(&B.part_t[jj]);
+          Cr += pc.x; Cg += pc.y; Cb += pc.z; Dp += pc.w;
+          if (pt >= 0.f) Tf = pt;
+        }
+      }
+    }
+    if (write) {
+      if (inside) {
+        const size_t p = (size_t)py * c.width + px;
+        if (valid) {
+          B.rgb[3 * p] = Cr + Tf * c.bg[0];
+          B.rgb[3 * p + 1] = Cg + Tf * c.bg[1];
+          B.rgb[3 * p + 2] = Cb + Tf * c.bg[2];
+          B.alpha[p] = 1.f - Tf;
+          if (B.depth) B.depth[p] = Dp;
+        } else {
+          B.rgb[3 * p] = c.bg[0];
+          B.rgb[3 * p + 1] = c.bg[1];
+          B.rgb[3 * p + 2] = c.bg[2];
+          B.alpha[p] = 0.f;
+          if (B.depth) B.depth[p] = 0.f;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicAdd(&B.counters[CNT_Q_FINISHED], 1u);
+      }
+    }
   }
+  // ---- statistics (once per warp)
   {
-    unsigned long long e1 = warp_sum((unsigned long long)n_eval);
-    unsigned long long e2 = warp_sum((unsigned long long)n_contrib);
-    unsigned long long e3 = warp_sum((unsigned long long)n_term);
+    const unsigned long long e1 = warp_sum((unsigned long long)n_eval_acc);
+    const unsigned long long e2 = warp_sum((unsigned long long)n_contrib_acc);
+    const unsigned long long e3 = warp_sum((unsigned long long)n_term_acc);
     if (lane == 0 && (e1 | e2 | e3)) {
       atomicAdd(reinterpret_cast<unsigned long long *>(&B.counters[CNT_PAIRS_EVAL]), e1);
       atomicAdd(reinterpret_cast<unsigned long long *>(&B.counters[CNT_PAIRS_CONTRIB]), e2);
       atomicAdd(reinterpret_cast<unsigned long long *>(&B.counters[CNT_TERMINATED]), e3);
-    }
-  }
-  // ---- outputs (single segment) or partials + deterministic in-order combine
-  float Tf = T_end;
-  if (S > 1) {
-    const size_t j = (size_t)slot * NT + tid;
-    B.part_c[j] = alive_in ? make_float4(Cr, Cg, Cb, Dp) : make_float4(0.f, 0.f, 0.f, 0.f);
-    B.part_t[j] = alive_in ? T_end : -1.f;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&B.tile_done[tile], 1u) == (uint32_t)(S - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const uint32_t first = B.seg_base[tile];
-    Cr = Cg = Cb = Dp = 0.f;
-    Tf = 1.f;
-    for (int q = 0; q < S; ++q) {
-      const size_t jj = (size_t)(first + q) * NT + tid;
-      const float4 pc = __ldcg(&B.part_c[jj]);
-      const float pt = __ldcg(&B.part_t[jj]);
-      Cr += pc.x; Cg += pc.y; Cb += pc.z; Dp += pc.w;
-      if (pt >= 0.f) Tf = pt;
-    }
-    if (tid == 0) B.tile_done[tile] = 0;
-  }
-  if (inside) {
-    const size_t p = (size_t)py * c.width + px;
-    if (valid) {
-      B.rgb[3 * p] = Cr + Tf * c.bg[0];
-      B.rgb[3 * p + 1] = Cg + Tf * c.bg[1];
-      B.rgb[3 * p + 2] = Cb + Tf * c.bg[2];
-      B.alpha[p] = 1.f - Tf;
-      if (B.depth) B.depth[p] = Dp;
-    } else {
-      B.rgb[3 * p] = c.bg[0];
-      B.rgb[3 * p + 1] = c.bg[1];
-      B.rgb[3 * p + 2] = c.bg[2];
-      B.alpha[p] = 0.f;
-      if (B.depth) B.depth[p] = 0.f;
     }
   }
 }
@@ -710,12 +929,16 @@ template <int MODE>
 static void blend_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
   constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_THREADS / 32) * 2 * 32 * 4 +
                                             (GUT_BLEND_THREADS / 32) * 32 * WarpTbl<MODE>::NF);
-  static bool configured = false;  // per template instance; the attribute is per device function
-  if (!configured) {
+  static int grid = 0;  // per template instance: persistent CTAs = SMs x resident CTAs per SM
+  if (!grid) {
     cudaFuncSetAttribute(blend_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, blend_kernel<MODE>, GUT_BLEND_THREADS, smem);
+    grid = max(1, sms) * max(1, per);
   }
-  blend_kernel<MODE><<<b.max_items, GUT_BLEND_THREADS, smem, st>>>(cam, b);
+  blend_kernel<MODE><<<grid, GUT_BLEND_THREADS, smem, st>>>(cam, b);
 }
 
 void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {

@@ -25,13 +25,17 @@ enum : int {
   CNT_PAIRS_CONTRIB = 20,  // u64
   CNT_TERMINATED = 22,     // u64
   CNT_MAXLEN = 24,
-  CNT_NITEMS = 26,         // blend work items (tile, segment)
+  CNT_NITEMS = 26,         // blend segment slots (sum over tiles of S_t)
   CNT_NPRE = 27,           // transmittance-prefix work items
   CNT_NDEFER = 28,         // Gaussians deferred to the fp64 K1 kernel
-  CNT_TICKET_BLEND = 29,   // blend work-item tickets
-  CNT_HIST_DEPTH = 32,     // 4 x 256
-  CNT_HIST_TILE = 32 + 1024,  // 2 x 256
-  CNT_WORDS = 32 + 1024 + 512
+  CNT_Q_NINIT = 32,        // blend work queue: initial grants (queue 1 length)
+  CNT_Q_HEAD1 = 33,        //   next queue-1 entry
+  CNT_Q_HEAD2 = 34,        //   next queue-2 (granted successor) entry
+  CNT_Q_ALLOC2 = 35,       //   queue-2 entries allocated
+  CNT_Q_FINISHED = 36,     //   units (8 per tile) whose pixels are written
+  CNT_HIST_DEPTH = 64,     // 4 x 256
+  CNT_HIST_TILE = 64 + 1024,  // 2 x 256
+  CNT_WORDS = 64 + 1024 + 512
 };
 
 void launch_pack_scene(const float *means, const float *rots, const float *scales, const float *opac,
@@ -66,9 +70,11 @@ struct TileAnchor {
 // per-pixel (a, b, snorm, beta) relative to the tile anchor + per-tile anchors
 void launch_rays(const DevCam &cam, float4 *pix, TileAnchor *anchors, cudaStream_t st);
 
-// blend work plan: tiles split into segments of `seg` list entries
-void launch_plan(const uint2 *ranges, int n_tiles, int seg, uint32_t *seg_base, uint32_t *counters,
-                 cudaStream_t st);
+// blend work plan (see k5_blend.cu): segment slots (seg_base), per-tile
+// grant/dispatch/completion counters, queue 1 = the first min(S_t, window)
+// segment grants of every tile, longest tiles first
+void launch_plan(const uint2 *ranges, int n_tiles, int seg, int window, uint32_t *seg_base, uint32_t *granted,
+                 uint32_t *next_s, uint32_t *unit_done, uint32_t *q1, uint32_t *counters, cudaStream_t st);
 
 struct BlendBufs {
   const uint2 *ranges;
@@ -77,16 +83,24 @@ struct BlendBufs {
   const float4 *pix;
   const TileAnchor *anchors;
   const uint32_t *seg_base;     // per tile: first (tile, segment) slot, tile-major
+  uint32_t *granted;            // per unit (8 tile + warp block): segments granted so far
+  uint32_t *next_s;             // per unit: next segment index to hand out
+  uint32_t *unit_done;          // per unit: segments completed
+  const uint32_t *q1;           // queue 1: unit ids (initial grants, longest tiles first)
+  uint32_t *q2;                 // queue 2: unit id + 1 per granted successor (0 = empty slot)
   unsigned long long *status;   // per (slot, pixel) look-back word (flag | epoch | -log2 T)
   float4 *part_c;    // per (slot, pixel) partial colour + depth
   float *part_t;     // per (slot, pixel) transmittance at segment end (-1 inactive)
-  uint32_t *tile_done;
   uint2 *tile_work;
-  int seg, n_tiles;
-  uint32_t max_items, epoch;
+  uint4 *trace;  // optional (GUT_BLEND_TRACE=1): per (slot, warp block) 2 x uint4 (see GUT_STAGE_BLEND_TRACE)
+  int seg, window, n_tiles;
+  uint32_t epoch;
   float *rgb, *alpha, *depth;
   uint32_t *counters;
 };
+
+// queue-2 slots beyond the grants: one ticket per resident blend warp (>= 148 SMs x 64 warps)
+#define GUT_BLEND_Q2_SLACK (1u << 16)
 
 void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st);
 
