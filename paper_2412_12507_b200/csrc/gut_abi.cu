@@ -46,7 +46,7 @@ struct gut_context {
   // K5: ray LUT (cached per intrinsics for global shutter), blend work plan
   float4 *pix = nullptr;
   TileAnchor *anchors = nullptr;
-  uint32_t *seg_base = nullptr, *granted = nullptr, *next_s = nullptr, *unit_done = nullptr;
+  uint32_t *seg_base = nullptr, *unit_ctr = nullptr;  // unit_ctr: 3 x n_units (extra grants, next_s, done)
   uint32_t *q1 = nullptr, *q2 = nullptr;  // blend work queues (k5_blend.cu)
   unsigned long long *bstatus = nullptr;
   float *part_t = nullptr;
@@ -97,7 +97,7 @@ static gut_status ensure_n(gut_context *ctx, size_t n) {
   CUDA_TRY(ctx, regrow(ctx->ell, dummy, 2 * c));
   CUDA_TRY(ctx, regrow(ctx->ell64, dummy, 3 * c));
   CUDA_TRY(ctx, regrow(ctx->deferred, dummy, c));
-  CUDA_TRY(ctx, regrow(ctx->payload, dummy, 4 * c));
+  CUDA_TRY(ctx, regrow(ctx->payload, dummy, (size_t)GUT_PAYLOAD_F4 * c));
   CUDA_TRY(ctx, regrow(ctx->sa_k, dummy, c));
   CUDA_TRY(ctx, regrow(ctx->sa_v, dummy, c));
   CUDA_TRY(ctx, regrow(ctx->sb_k, dummy, c));
@@ -135,9 +135,7 @@ static gut_status ensure_tiles(gut_context *ctx, size_t t) {
   CUDA_TRY(ctx, regrow(ctx->pix, dummy, t * GUT_BLEND_THREADS));
   CUDA_TRY(ctx, regrow(ctx->anchors, dummy, t));
   CUDA_TRY(ctx, regrow(ctx->seg_base, dummy, t));
-  CUDA_TRY(ctx, regrow(ctx->granted, dummy, t * GUT_BLEND_WARPS));
-  CUDA_TRY(ctx, regrow(ctx->next_s, dummy, t * GUT_BLEND_WARPS));
-  CUDA_TRY(ctx, regrow(ctx->unit_done, dummy, t * GUT_BLEND_WARPS));
+  CUDA_TRY(ctx, regrow(ctx->unit_ctr, dummy, 3 * t * GUT_BLEND_WARPS));
   ctx->lut_valid = false;
   ctx->cap_tiles = t;
   return GUT_OK;
@@ -325,8 +323,8 @@ void gut_context_destroy(gut_context *ctx) {
   void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->deferred, ctx->payload, ctx->sa_k, ctx->sa_v,
                 ctx->sb_k, ctx->sb_v,
                 ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->tile_work, ctx->img, ctx->st_depth,
-                ctx->st_emit, ctx->st_tile, ctx->counters, ctx->pix, ctx->anchors, ctx->seg_base, ctx->granted, ctx->next_s, ctx->q1, ctx->q2,
-                ctx->unit_done, ctx->bstatus, ctx->part_c, ctx->part_t, ctx->trace};
+                ctx->st_emit, ctx->st_tile, ctx->counters, ctx->pix, ctx->anchors, ctx->seg_base, ctx->unit_ctr, ctx->q1, ctx->q2,
+                ctx->bstatus, ctx->part_c, ctx->part_t, ctx->trace};
   for (void *p : ps) if (p) cudaFree(p);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
   for (auto &set : ctx->tsets)
@@ -524,8 +522,9 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   const size_t max_items = (size_t)dc.n_tiles + ctx->cap_k / (size_t)ctx->blend_seg + 2;
   if ((s = ensure_items(ctx, max_items)) != GUT_OK) return s;
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->tile_work, 0, (size_t)dc.n_tiles * sizeof(uint2), st));
-  launch_plan(ctx->ranges, dc.n_tiles, ctx->blend_seg, ctx->blend_window, ctx->seg_base, ctx->granted, ctx->next_s,
-              ctx->unit_done, ctx->q1, cnt, st);
+  const size_t n_units = (size_t)dc.n_tiles * GUT_BLEND_WARPS;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->unit_ctr, 0, 3 * n_units * sizeof(uint32_t), st));
+  launch_plan(ctx->ranges, dc.n_tiles, ctx->blend_seg, ctx->blend_window, ctx->seg_base, ctx->q1, cnt, st);
   // blend look-back epochs live in 22 bits: clear the status words on wrap
   uint32_t bepoch = ++ctx->epoch;
   if ((bepoch & 0x3FFFFFu) == 0) {
@@ -534,7 +533,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   }
   BlendBufs bb;
   bb.ranges = ctx->ranges; bb.gids = fv; bb.payload = ctx->payload; bb.pix = ctx->pix; bb.anchors = ctx->anchors;
-  bb.seg_base = ctx->seg_base; bb.granted = ctx->granted; bb.next_s = ctx->next_s; bb.unit_done = ctx->unit_done;
+  bb.seg_base = ctx->seg_base; bb.granted = ctx->unit_ctr; bb.next_s = ctx->unit_ctr + n_units; bb.unit_done = ctx->unit_ctr + 2 * n_units;
   bb.q1 = ctx->q1; bb.q2 = ctx->q2;
   bb.status = ctx->bstatus;
   bb.part_c = ctx->part_c; bb.part_t = ctx->part_t;
@@ -657,20 +656,20 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
   if (!host_dst || bytes < need) return GUT_OK;
   if (stage == GUT_STAGE_PROJECT) {
     uint32_t *tl = new uint32_t[N + 1], *dk = new uint32_t[N + 1];
-    float4 *el = new float4[2 * N + 1], *pl = new float4[4 * N + 1];
+    float4 *el = new float4[2 * N + 1], *pl = new float4[GUT_PAYLOAD_F4 * N + 1];
     cudaMemcpy(tl, ctx->tiles, N * 4, cudaMemcpyDeviceToHost);
     cudaMemcpy(dk, ctx->dkey, N * 4, cudaMemcpyDeviceToHost);
     cudaMemcpy(el, ctx->ell, N * 32, cudaMemcpyDeviceToHost);
-    cudaMemcpy(pl, ctx->payload, N * 64, cudaMemcpyDeviceToHost);
+    cudaMemcpy(pl, ctx->payload, N * GUT_PAYLOAD_F4 * sizeof(float4), cudaMemcpyDeviceToHost);
     gut_proj_record *r = (gut_proj_record *)host_dst;
     for (size_t i = 0; i < N; ++i) {
       memset(&r[i], 0, sizeof(r[i]));
       r[i].tiles = tl[i];
       if (!tl[i]) continue;
-      float4 a = el[2 * i], b = el[2 * i + 1], p3 = pl[4 * i + 3];
+      float4 a = el[2 * i], b = el[2 * i + 1], p4 = pl[GUT_PAYLOAD_F4 * i + 4];
       r[i].vx = a.x; r[i].vy = a.y; r[i].cxx = a.z; r[i].cxy = a.w; r[i].cyy = b.x; r[i].k2 = fabsf(b.y);
       memcpy(&r[i].depth, &dk[i], 4);
-      r[i].rgb[0] = p3.y; r[i].rgb[1] = p3.z; r[i].rgb[2] = p3.w;
+      r[i].rgb[0] = p4.x; r[i].rgb[1] = p4.y; r[i].rgb[2] = p4.z;
       uint32_t r0, r1;
       memcpy(&r0, &b.z, 4);
       memcpy(&r1, &b.w, 4);

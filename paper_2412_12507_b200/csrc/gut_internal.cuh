@@ -7,6 +7,7 @@
 #define GUT_TILE 16
 #define GUT_BLEND_THREADS 256
 #define GUT_BLEND_WARPS (GUT_BLEND_THREADS / 32)  // K5 work units per tile (8x4 pixel blocks)
+#define GUT_PAYLOAD_F4 5  // K1 -> K5 blend payload per Gaussian, in float4 (k1_project.cu finish_gaussian)
 #define GUT_SORT_THREADS 256
 #define GUT_SORT_ITEMS 16
 #define GUT_SORT_PART (GUT_SORT_THREADS * GUT_SORT_ITEMS)  // 4096 keys per onesweep partition

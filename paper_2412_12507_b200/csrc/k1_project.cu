@@ -243,14 +243,20 @@ __device__ __forceinline__ uint32_t finish_gaussian(const DevCam &c, const Scene
   const f3 rgb = sh_colour<DEG>(s.sh, s.n, i, tof((1.0 / nd) * dw));
   ell[2 * i] = e0;
   ell[2 * i + 1] = e1;
-  // blend payload: mu, k^2 = 2 ln(sigma / alpha_min) (the ellipse record's
-  // value; K5 derives log2 sigma from it), M = diag(1/s) R^T (Eq. 11
-  // o_g = M (o - mu)), rgb
+  // blend payload (80 B): w0 = c(0) - mu in fp64 (K5 forms the cancelling
+  // o_g x d_g = cof(M) (w x d) from it, see k5_blend.cu), k^2 = 2 ln(sigma /
+  // alpha_min) (the ellipse record's value; K5 derives log2 sigma from it),
+  // M = diag(1/s) R^T (Eq. 11 o_g = M (o - mu)), rgb
   const float is0 = 1.f / sc.x, is1 = 1.f / sc.y, is2 = 1.f / sc.z;
-  payload[4 * i] = make_float4(po.x, po.y, po.z, fabsf(e1.y));
-  payload[4 * i + 1] = make_float4(R[0] * is0, R[3] * is0, R[6] * is0, R[1] * is1);
-  payload[4 * i + 2] = make_float4(R[4] * is1, R[7] * is1, R[2] * is2, R[5] * is2);
-  payload[4 * i + 3] = make_float4(R[8] * is2, rgb.x, rgb.y, rgb.z);
+  const d3 w0 = mkd(c.c0[0], c.c0[1], c.c0[2]) - mkd(po.x, po.y, po.z);
+  const unsigned long long wz = (unsigned long long)__double_as_longlong(w0.z);
+  float4 *pl = payload + (size_t)GUT_PAYLOAD_F4 * i;
+  reinterpret_cast<double2 *>(pl)[0] = make_double2(w0.x, w0.y);
+  pl[1] = make_float4(__int_as_float((int)(uint32_t)wz), __int_as_float((int)(uint32_t)(wz >> 32)), fabsf(e1.y),
+                      R[0] * is0);
+  pl[2] = make_float4(R[3] * is0, R[6] * is0, R[1] * is1, R[4] * is1);
+  pl[3] = make_float4(R[7] * is1, R[2] * is2, R[5] * is2, R[8] * is2);
+  pl[4] = make_float4(rgb.x, rgb.y, rgb.z, 0.f);
   return __float_as_uint(depth);
 }
 

@@ -256,59 +256,94 @@ __device__ __forceinline__ uint32_t len_bucket(uint32_t len) {
   return 1023u - key;
 }
 
-__global__ __launch_bounds__(1024) void plan_kernel(const uint2 *__restrict__ ranges, int n_tiles, int seg, int window,
-                                                    uint32_t *__restrict__ seg_base, uint32_t *__restrict__ granted,
-                                                    uint32_t *__restrict__ next_s, uint32_t *__restrict__ unit_done,
-                                                    uint32_t *__restrict__ q1, uint32_t *counters) {
+// Three small kernels: (a) per tile S_t into seg_base and the bucket
+// histogram of the initial grants (warp-aggregated atomics), (b) one CTA
+// scans both in place (8 contiguous tiles per thread), (c) per tile its
+// position in its bucket (warp-aggregated atomics) and the queue-1 entries.
+// The per-unit counters are zeroed by the host (memset) before the blend.
+__device__ __forceinline__ void tile_plan(const uint2 *ranges, int t, int seg, int window, uint32_t &S, uint32_t &g,
+                                          uint32_t &bk) {
+  const uint2 r = ranges[t];
+  const uint32_t len = r.y > r.x ? r.y - r.x : 0;
+  S = len == 0 ? 1 : (len + seg - 1) / seg;
+  g = min(S, (uint32_t)window) * GUT_BLEND_WARPS;
+  bk = len_bucket(len);
+}
+
+__global__ __launch_bounds__(256) void plan_count_kernel(const uint2 *__restrict__ ranges, int n_tiles, int seg,
+                                                         int window, uint32_t *__restrict__ seg_base,
+                                                         uint32_t *counters) {
+  const int t = blockIdx.x * 256 + threadIdx.x;
+  uint32_t S = 0, g = 0, bk = 0xFFFFFFFFu;
+  if (t < n_tiles) {
+    tile_plan(ranges, t, seg, window, S, g, bk);
+    seg_base[t] = S;
+  }
+  const uint32_t peers = __match_any_sync(0xffffffffu, bk);
+  const uint32_t gsum = __reduce_add_sync(peers, g);
+  if (t < n_tiles && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counters[CNT_PLAN_HIST + bk], gsum);
+}
+
+__global__ __launch_bounds__(1024) void plan_scan_kernel(int n_tiles, uint32_t *__restrict__ seg_base,
+                                                         uint32_t *counters) {
   __shared__ uint32_t s_w[32];
-  __shared__ uint32_t s_hist[1024];
-  const int per = (n_tiles + 1023) / 1024;
-  const int t0 = min((int)threadIdx.x * per, n_tiles), t1 = min(t0 + per, n_tiles);
-  s_hist[threadIdx.x] = 0;
-  uint32_t sa = 0;
-  for (int t = t0; t < t1; ++t) {
-    const uint2 r = ranges[t];
-    const uint32_t len = r.y > r.x ? r.y - r.x : 0;
-    sa += len == 0 ? 1 : (len + seg - 1) / seg;
-  }
-  uint32_t n_slots;
-  uint32_t oa = block_excl_scan(sa, s_w, n_slots);  // (its barriers also order the s_hist reset)
-  for (int t = t0; t < t1; ++t) {
-    const uint2 r = ranges[t];
-    const uint32_t len = r.y > r.x ? r.y - r.x : 0;
-    const uint32_t S = len == 0 ? 1 : (len + seg - 1) / seg;
-    const uint32_t g = min(S, (uint32_t)window);
-    seg_base[t] = oa;
-    oa += S;
-    for (int w = 0; w < GUT_BLEND_WARPS; ++w) {
-      granted[GUT_BLEND_WARPS * t + w] = g;
-      next_s[GUT_BLEND_WARPS * t + w] = 0;
-      unit_done[GUT_BLEND_WARPS * t + w] = 0;
+  const int tid = threadIdx.x;
+  uint32_t run = 0;
+  for (int base = 0; base < n_tiles; base += 1024 * 8) {
+    const int t0 = base + tid * 8;
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = t0 + k < n_tiles ? seg_base[t0 + k] : 0u;
+      sum += v[k];
     }
-    atomicAdd(&s_hist[len_bucket(len)], g * GUT_BLEND_WARPS);
+    uint32_t total;
+    uint32_t off = run + block_excl_scan(sum, s_w, total);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (t0 + k < n_tiles) seg_base[t0 + k] = off;
+      off += v[k];
+    }
+    run += total;
   }
-  __syncthreads();
   uint32_t n_init;
-  const uint32_t off = block_excl_scan(s_hist[threadIdx.x], s_w, n_init);
-  s_hist[threadIdx.x] = off;
-  __syncthreads();
-  for (int t = t0; t < t1; ++t) {
-    const uint2 r = ranges[t];
-    const uint32_t len = r.y > r.x ? r.y - r.x : 0;
-    const uint32_t S = len == 0 ? 1 : (len + seg - 1) / seg;
-    const uint32_t g = min(S, (uint32_t)window);
-    const uint32_t pos = atomicAdd(&s_hist[len_bucket(len)], g * GUT_BLEND_WARPS);
-    for (uint32_t k = 0; k < g * GUT_BLEND_WARPS; ++k) q1[pos + k] = GUT_BLEND_WARPS * (uint32_t)t + k % GUT_BLEND_WARPS;
-  }
-  if (threadIdx.x == 0) {
-    counters[CNT_NITEMS] = n_slots;
+  const uint32_t h = counters[CNT_PLAN_HIST + tid];
+  const uint32_t boff = block_excl_scan(h, s_w, n_init);
+  counters[CNT_PLAN_HIST + tid] = boff;
+  if (tid == 0) {
+    counters[CNT_NITEMS] = run;
     counters[CNT_Q_NINIT] = n_init;
   }
 }
 
-void launch_plan(const uint2 *ranges, int n_tiles, int seg, int window, uint32_t *seg_base, uint32_t *granted,
-                 uint32_t *next_s, uint32_t *unit_done, uint32_t *q1, uint32_t *counters, cudaStream_t st) {
-  plan_kernel<<<1, 1024, 0, st>>>(ranges, n_tiles, seg, window, seg_base, granted, next_s, unit_done, q1, counters);
+__global__ __launch_bounds__(256) void plan_fill_kernel(const uint2 *__restrict__ ranges, int n_tiles, int seg,
+                                                        int window, uint32_t *__restrict__ q1, uint32_t *counters) {
+  const int t = blockIdx.x * 256 + threadIdx.x, lane = threadIdx.x & 31;
+  uint32_t S = 0, g = 0, bk = 0xFFFFFFFFu;
+  if (t < n_tiles) tile_plan(ranges, t, seg, window, S, g, bk);
+  const uint32_t peers = __match_any_sync(0xffffffffu, bk);
+  const int leader = __ffs(peers) - 1;
+  // exclusive prefix of g among this lane's peers (g is the same for equal buckets
+  // unless S < window; sum explicitly)
+  uint32_t pre = 0, gsum = 0;
+  for (uint32_t m = peers; m; m &= m - 1) {
+    const int l = __ffs(m) - 1;
+    const uint32_t gl = __shfl_sync(peers, g, l);
+    gsum += gl;
+    if (l < lane) pre += gl;
+  }
+  uint32_t pos = 0;
+  if (t < n_tiles && lane == leader) pos = atomicAdd(&counters[CNT_PLAN_HIST + bk], gsum);
+  pos = __shfl_sync(peers, pos, leader) + pre;
+  for (uint32_t k = 0; k < g; ++k) q1[pos + k] = GUT_BLEND_WARPS * (uint32_t)t + k % GUT_BLEND_WARPS;
+}
+
+void launch_plan(const uint2 *ranges, int n_tiles, int seg, int window, uint32_t *seg_base, uint32_t *q1,
+                 uint32_t *counters, cudaStream_t st) {
+  const unsigned blocks = (unsigned)((n_tiles + 255) / 256);
+  plan_count_kernel<<<blocks, 256, 0, st>>>(ranges, n_tiles, seg, window, seg_base, counters);
+  plan_scan_kernel<<<1, 1024, 0, st>>>(n_tiles, seg_base, counters);
+  plan_fill_kernel<<<blocks, 256, 0, st>>>(ranges, n_tiles, seg, window, q1, counters);
 }
 
 // ---------------------------------------------------------------- blend
@@ -395,10 +430,11 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
                                           bool &term, uint32_t &n_eval, uint32_t &n_contrib, uint32_t &processed,
                                           const unsigned long long *poll_stat, int poll_s) {
   constexpr int NF = WarpTbl<MODE>::NF;
-  // dynamic shared memory: [raw payload double buffer: 8 warps x 2 x 32 x 4]
+  // dynamic shared memory: [raw payload double buffer: 8 warps x 2 x 32 x 5]
   // [per-warp entry table: 8 warps x 32 x NF]
   extern __shared__ float4 s_dyn[];
-  constexpr int RAW = (GUT_BLEND_THREADS / 32) * 2 * 32 * 4;
+  constexpr int PF = GUT_PAYLOAD_F4;
+  constexpr int RAW = (GUT_BLEND_THREADS / 32) * 2 * 32 * PF;
   float4 *__restrict__ wt = s_dyn + RAW + (threadIdx.x >> 5) * 32 * NF;
   const uint32_t wt_s = (uint32_t)__cvta_generic_to_shared(wt);
   const int lane = threadIdx.x & 31;
@@ -406,7 +442,10 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   const float l2amin = log2f(alpha_min);
   const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
   // raw payload of the warp's current / next chunk (cp.async double buffer)
-  float4 *__restrict__ raw = s_dyn + (threadIdx.x >> 5) * 2 * 32 * 4;
+  float4 *__restrict__ raw = s_dyn + (threadIdx.x >> 5) * 2 * 32 * PF;
+  // the item's anchor: dO = O - c(0) (payload w0 = c(0) - mu), D in fp32
+  const d3 dO = O - mkd(c.c0[0], c.c0[1], c.c0[2]);
+  const f3 Df = tof(D);
   T = T_start;
   Cr = Cg = Cb = Dp = 0.f;
   term = false;
@@ -416,8 +455,8 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   // gathers run one chunk ahead (cp.async), Gaussian ids two chunks ahead
   uint32_t gnext = s0 + lane < s1 ? __ldg(&B.gids[s0 + lane]) : 0u;
   if (s0 + lane < s1) {
-    float4 *dst = raw + lane * 4;
-    for (int q = 0; q < 4; ++q) cp_async16(dst + q, &B.payload[4 * gnext + q]);
+    float4 *dst = raw + lane * PF;
+    for (int q = 0; q < PF; ++q) cp_async16(dst + q, &B.payload[(size_t)PF * gnext + q]);
   }
   cp_async_commit();
   gnext = s0 + 32 + lane < s1 ? __ldg(&B.gids[s0 + 32 + lane]) : 0u;
@@ -432,8 +471,8 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
     if (__all_sync(0xffffffffu, done)) break;
     if (b0 + 32 < s1) {  // prefetch the next chunk
       if (b0 + 32 + lane < s1) {
-        float4 *dst = raw + ((buf ^ 1) * 32 + lane) * 4;
-        for (int q = 0; q < 4; ++q) cp_async16(dst + q, &B.payload[4 * gnext + q]);
+        float4 *dst = raw + ((buf ^ 1) * 32 + lane) * PF;
+        for (int q = 0; q < PF; ++q) cp_async16(dst + q, &B.payload[(size_t)PF * gnext + q]);
       }
       cp_async_commit();
       gnext = b0 + 64 + lane < s1 ? __ldg(&B.gids[b0 + 64 + lane]) : 0u;
@@ -446,16 +485,25 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
     const uint32_t kk = b0 + (uint32_t)lane;
     bool maybe = false;
     if (kk < s1) {
-      // ---- stage entry kk: fp64 for the cancelling part, fp32 for the rest
-      const float4 *src = raw + (buf * 32 + lane) * 4;
-      const float4 p0 = src[0], p1 = src[1], p2 = src[2], p3 = src[3];
-      const float M[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
-      const double Md[9] = {p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w, p3.x};
-      const d3 og = mv(Md, O - mkd(p0.x, p0.y, p0.z));
-      const d3 e0d = mv(Md, D);
-      const d3 c0d = cross(og, e0d);
-      const double g0 = dot(og, e0d);
-      const f3 ogf = tof(og), e0 = tof(e0d), c0 = tof(c0d);
+      // ---- stage entry kk.  The cancelling part c0 = o_g x d_g (o_g = M w,
+      // d_g = M D, w = O - mu) uses (M a) x (M b) = cof(M) (a x b) with
+      // cof(M) = det(M) M^-T = diag(s_i^2 det M) M for M = diag(1/s) R^T:
+      // only w x D is formed in fp64 (the small vector), the rest in fp32.
+      const float4 *src = raw + (buf * 32 + lane) * PF;
+      const double2 wxy = *reinterpret_cast<const double2 *>(src);
+      const float4 p1 = src[1], p2 = src[2], p3 = src[3], p4 = src[4];
+      const d3 w = mkd(wxy.x, wxy.y, __hiloint2double(__float_as_int(p1.y), __float_as_int(p1.x))) + dO;
+      const f3 x = tof(cross(w, D));
+      const float M[9] = {p1.w, p2.x, p2.y, p2.z, p2.w, p3.x, p3.y, p3.z, p3.w};
+      // row norms |M_i|^2 = 1/s_i^2; lambda_i = s_i^2 det M = sqrt(n0 n1 n2) / n_i
+      const float rn0 = fmaf(M[0], M[0], fmaf(M[1], M[1], M[2] * M[2]));
+      const float rn1 = fmaf(M[3], M[3], fmaf(M[4], M[4], M[5] * M[5]));
+      const float rn2 = fmaf(M[6], M[6], fmaf(M[7], M[7], M[8] * M[8]));
+      const float dM = sqrtf(rn0 * rn1 * rn2);
+      const f3 Mx = mv(M, x);
+      const f3 c0 = mk(Mx.x * (dM / rn0), Mx.y * (dM / rn1), Mx.z * (dM / rn2));
+      const f3 ogf = mv(M, tof(w)), e0 = mv(M, Df);
+      const float g0 = dot(ogf, e0);
       f3 U = mv(M, T1f), V = mv(M, T2f), P, Q;
       float gu, gv;
       if (MODE == 1) {
@@ -465,7 +513,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
         P = cross(ogf, U); Q = cross(ogf, V); gu = dot(ogf, U); gv = dot(ogf, V);
       }
       // k^2 = 2 ln(sigma/alpha_min) (K1, via log1p); log2 sigma = k^2 / (2 ln 2) + log2 alpha_min
-      const float k2 = p0.w;
+      const float k2 = p1.z;
       const float l2s = fmaf(k2, 0.72134752044448170f, l2amin);
       // ---- conservative cull against the warp's pixel box (a in ac +- ra,
       // b in bc +- rb): |n| >= |n(ac,bc)| - ra|P| - rb|Q|, |e| <= |e(ac,bc)| +
@@ -491,8 +539,8 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           t[2] = make_float4(Q.y, Q.z, e0.x, e0.y);
           t[3] = make_float4(e0.z, U.x, U.y, U.z);
           t[4] = make_float4(V.x, V.y, V.z, l2s);
-          t[5] = make_float4((float)g0, gu, gv, 0.f);
-          t[6] = make_float4(p3.y, p3.z, p3.w, 0.f);
+          t[5] = make_float4(g0, gu, gv, 0.f);
+          t[6] = make_float4(p4.x, p4.y, p4.z, 0.f);
           t[7] = make_float4(h.x, h.y, h.z, dot(m, e0));
           t[8] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
           t[9] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
@@ -519,7 +567,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           const float Nab = 2.f * pq;
           const float D0 = dot(es, es), Da = 2.f * dot(es, U), Db = 2.f * dot(es, V);
           const float Daa = dot(U, U), Dab = 2.f * dot(U, V), Dbb = dot(V, V);
-          const float gs = (float)g0 + as * gu + bs * gv;
+          const float gs = g0 + as * gu + bs * gv;
           const float F0 = fmaf(-k2, D0, N0), Fa = fmaf(-k2, Da, Na), Fb = fmaf(-k2, Db, Nb);
           const float Faa = fmaf(-k2, Daa, pp), Fab = fmaf(-k2, Dab, Nab), Fbb = fmaf(-k2, Dbb, qq);
           // second, tighter cull: a lower bound of the quadratic F over the box
@@ -542,7 +590,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
             t[2] = make_float4(D0, Da, Db, Daa);
             t[3] = make_float4(Dab, Dbb, gs, gu);
             t[4] = make_float4(gv, k2, l2s, 0.f);
-            t[5] = make_float4(p3.y, p3.z, p3.w, 0.f);
+            t[5] = make_float4(p4.x, p4.y, p4.z, 0.f);
           }
         }
       }
@@ -658,12 +706,17 @@ __device__ bool fetch_work(const BlendBufs &B, int &unit, int &s) {
   const uint32_t n_units = (uint32_t)B.n_tiles * GUT_BLEND_WARPS;
   for (;;) {
     const bool q1_empty = ld_volatile_u32(&cnt[CNT_Q_HEAD1]) >= n_init;
-    if (q1_empty || ld_volatile_u32(&cnt[CNT_Q_HEAD2]) < ld_volatile_u32(&cnt[CNT_Q_ALLOC2])) {
+    const uint32_t h2 = ld_volatile_u32(&cnt[CNT_Q_HEAD2]), a2 = ld_volatile_u32(&cnt[CNT_Q_ALLOC2]);
+    // nothing left to hand out and enough warps already waiting for future
+    // grants: leave (a warp never leaves holding a ticket, so every granted
+    // slot keeps a consumer; idle warps would only burn issue slots)
+    if (q1_empty && h2 >= a2 + GUT_BLEND_MAX_WAITERS) return false;
+    if (q1_empty || h2 < a2) {
       const uint32_t t2 = atomicAdd(&cnt[CNT_Q_HEAD2], 1u);
       uint32_t u1;
       for (int k = 0; (u1 = ld_volatile_u32(&B.q2[t2])) == 0; ++k) {
-        if ((k & 7) == 7 && ld_volatile_u32(&cnt[CNT_Q_FINISHED]) >= n_units) return false;
-        __nanosleep(k < 4 ? 64 : 512);
+        if ((k & 3) == 3 && ld_volatile_u32(&cnt[CNT_Q_FINISHED]) >= n_units) return false;
+        __nanosleep(k < 2 ? 128 : (k < 6 ? 512 : 2048));
       }
       B.q2[t2] = 0;  // slot reusable by the next render
       unit = (int)(u1 - 1);
@@ -840,6 +893,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
       __threadfence();  // partials visible before the completion count
       __syncwarp();
       uint32_t nseg = 0;
+      const uint32_t g0 = (uint32_t)min(S, B.window);
       if (lane == 0) {
         if (tmax > 0.f) {
           // grant segments up to s + max(window, the depth the slowest pixel of
@@ -853,7 +907,8 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
             const float rem = n_done * __logf(tmax / c.t_min) / decay;
             ahead = max(ahead, (int)fminf(rem / (float)B.seg + 1.f, (float)S));
           }
-          const uint32_t target = (uint32_t)min(S, s + 1 + ahead);
+          // granted = g0 + extra (g0 = the up-front grants, extra zeroed per render)
+          const uint32_t target = (uint32_t)min(S, s + 1 + ahead) - g0;
           uint32_t g = ld_volatile_u32(&B.granted[unit]);
           while (g < target) {
             const uint32_t prev = atomicCAS(&B.granted[unit], g, target);
@@ -868,7 +923,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
         __threadfence();
         const uint32_t d = atomicAdd(&B.unit_done[unit], 1u) + 1u;
         __threadfence();
-        const uint32_t g = ld_volatile_u32(&B.granted[unit]);
+        const uint32_t g = g0 + ld_volatile_u32(&B.granted[unit]);
         nseg = d == g ? g : 0u;
       }
       nseg = __shfl_sync(FULL, nseg, 0);
@@ -927,7 +982,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
 
 template <int MODE>
 static void blend_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
-  constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_THREADS / 32) * 2 * 32 * 4 +
+  constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_THREADS / 32) * 2 * 32 * GUT_PAYLOAD_F4 +
                                             (GUT_BLEND_THREADS / 32) * 32 * WarpTbl<MODE>::NF);
   static int grid = 0;  // per template instance: persistent CTAs = SMs x resident CTAs per SM
   if (!grid) {

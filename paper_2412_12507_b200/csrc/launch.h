@@ -35,7 +35,8 @@ enum : int {
   CNT_Q_FINISHED = 36,     //   units (8 per tile) whose pixels are written
   CNT_HIST_DEPTH = 64,     // 4 x 256
   CNT_HIST_TILE = 64 + 1024,  // 2 x 256
-  CNT_WORDS = 64 + 1024 + 512
+  CNT_PLAN_HIST = 64 + 1024 + 512,  // 1024 blend queue-1 buckets
+  CNT_WORDS = 64 + 1024 + 512 + 1024
 };
 
 void launch_pack_scene(const float *means, const float *rots, const float *scales, const float *opac,
@@ -70,11 +71,12 @@ struct TileAnchor {
 // per-pixel (a, b, snorm, beta) relative to the tile anchor + per-tile anchors
 void launch_rays(const DevCam &cam, float4 *pix, TileAnchor *anchors, cudaStream_t st);
 
-// blend work plan (see k5_blend.cu): segment slots (seg_base), per-tile
-// grant/dispatch/completion counters, queue 1 = the first min(S_t, window)
-// segment grants of every tile, longest tiles first
-void launch_plan(const uint2 *ranges, int n_tiles, int seg, int window, uint32_t *seg_base, uint32_t *granted,
-                 uint32_t *next_s, uint32_t *unit_done, uint32_t *q1, uint32_t *counters, cudaStream_t st);
+// blend work plan (see k5_blend.cu): segment slots (seg_base) and queue 1 =
+// the first min(S_t, window) segment grants of every unit, longest tiles
+// first.  The per-unit counters (extra grants, next segment, completed) are
+// zeroed by the host before the blend.
+void launch_plan(const uint2 *ranges, int n_tiles, int seg, int window, uint32_t *seg_base, uint32_t *q1,
+                 uint32_t *counters, cudaStream_t st);
 
 struct BlendBufs {
   const uint2 *ranges;
@@ -83,7 +85,7 @@ struct BlendBufs {
   const float4 *pix;
   const TileAnchor *anchors;
   const uint32_t *seg_base;     // per tile: first (tile, segment) slot, tile-major
-  uint32_t *granted;            // per unit (8 tile + warp block): segments granted so far
+  uint32_t *granted;            // per unit (8 tile + warp block): grants beyond the first min(S, window)
   uint32_t *next_s;             // per unit: next segment index to hand out
   uint32_t *unit_done;          // per unit: segments completed
   const uint32_t *q1;           // queue 1: unit ids (initial grants, longest tiles first)
@@ -101,6 +103,8 @@ struct BlendBufs {
 
 // queue-2 slots beyond the grants: one ticket per resident blend warp (>= 148 SMs x 64 warps)
 #define GUT_BLEND_Q2_SLACK (1u << 16)
+// blend warps allowed to wait for future grants once queue 1 is drained
+#define GUT_BLEND_MAX_WAITERS 768u
 
 void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st);
 

@@ -18,7 +18,7 @@ def analyse(tr, ranges, tx, seg, label):
     used = tr[:, 3] != 0
     tr = tr[used].astype(np.int64)
     proc, nev, ncon, nredo = tr[:, 4], tr[:, 5], tr[:, 6], tr[:, 7]
-    tile, s = tr[:, 0] & 0xFFFF, tr[:, 0] >> 16
+    tile, s = tr[:, 0] & 0xFFFF, (tr[:, 0] >> 16) & 0x1FFF
     t0 = tr[:, 2].min()
     b, e = tr[:, 2] - t0, tr[:, 3] - t0
     span = e.max()
@@ -33,12 +33,12 @@ def analyse(tr, ranges, tx, seg, label):
         lo, hi = span * q / 10, span * (q + 1) / 10
         ov = np.clip(np.minimum(e, hi) - np.maximum(b, lo), 0, None).sum()
         prof.append(ov / (hi - lo))
-    print(f"{label}: items {len(tr)} span {span / 1e3:.1f} us, peak concurrency {peak}, "
+    print(f"{label}: units {len(tr)} span {span / 1e3:.1f} us, peak concurrency {peak} warps, "
           f"sum dur {dur.sum() / 1e3:.0f} us -> packed span {dur.sum() / peak / 1e3:.1f} us")
     print("  mean concurrency per 10% slice:", " ".join(f"{p:.0f}" for p in prof))
     print("  item dur pct 50/90/99/max [us]:", (np.percentile(dur, [50, 90, 99]) / 1e3).round(1), dur.max() / 1e3)
     print(f"  totals: warp-entries visited {proc.sum()} pairs eval {nev.sum()} contrib {ncon.sum()} "
-          f"redo warps {nredo.sum()};  ns per warp-entry {dur.sum() * 8 / max(proc.sum(), 1):.1f} (CTA-time x 8 warps)")
+          f"redo warps {nredo.sum()};  ns per warp-entry {dur.sum() / max(proc.sum(), 1):.1f} (warp-time)")
     s0 = s == 0
     print(f"  s=0 items: {s0.sum()} dur {dur[s0].sum() / 1e3:.0f} us visited {proc[s0].sum()} eval {nev[s0].sum()}; "
           f"s>0 items: {(~s0).sum()} dur {dur[~s0].sum() / 1e3:.0f} us visited {proc[~s0].sum()} eval {nev[~s0].sum()} "
