@@ -416,20 +416,28 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 template <> struct WarpTbl<2> { static constexpr int NF = 11; };
 
+// The NP pixels of one lane (GUT_BLEND_NP): ray offsets in, running blend state out.
+template <int NP> struct LanePx {
+  float a[NP], b[NP], beta[NP], snorm[NP];
+  float Cr[NP], Cg[NP], Cb[NP], Dp[NP], T[NP];
+  bool done[NP], term[NP];
+};
+
 // One pass of ONE WARP over the segment [s0, s1): no CTA barriers.  Each chunk
 // of 32 entries is staged by the 32 lanes (one entry each: fp64 for the
 // cancelling part), culled against the warp's pixel box in registers, and the
-// surviving entries are evaluated by every lane in list order.  The warp leaves
-// the list as soon as all its pixels have terminated.  Termination rule
-// (reading R21): stop before an entry would take T below T_min.
-template <int MODE>
+// surviving entries are evaluated by every lane, for each of its NP pixels, in
+// list order.  The warp leaves the list as soon as all its pixels have
+// terminated.  Termination rule (reading R21): stop before an entry would take
+// T below T_min.  The caller sets L.a/b/beta/snorm, L.T (start), L.done
+// (= inactive) and L.term = false; the colour sums start at 0 here.
+template <int MODE, int NP>
 __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, uint32_t s0, uint32_t s1,
-                                          const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f, float a, float b,
-                                          float beta, float snorm, float ac, float bc, float ra, float rb, bool active,
-                                          float T_start, float &Cr, float &Cg, float &Cb, float &Dp, float &T,
-                                          bool &term, uint32_t &n_eval, uint32_t &n_contrib, uint32_t &processed,
-                                          const unsigned long long *poll_stat, int poll_s) {
+                                          const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f, float ac, float bc,
+                                          float ra, float rb, LanePx<NP> &L, uint32_t &n_eval, uint32_t &n_contrib,
+                                          uint32_t &processed, const unsigned long long *poll_stat, int poll_s) {
   constexpr int NF = WarpTbl<MODE>::NF;
+  constexpr unsigned FULL = 0xffffffffu;
   // dynamic shared memory: [raw payload double buffer: 8 warps x 2 x 32 x 5]
   // [per-warp entry table: 8 warps x 32 x NF]
   extern __shared__ float4 s_dyn[];
@@ -446,12 +454,14 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   // the item's anchor: dO = O - c(0) (payload w0 = c(0) - mu), D in fp32
   const d3 dO = O - mkd(c.c0[0], c.c0[1], c.c0[2]);
   const f3 Df = tof(D);
-  T = T_start;
-  Cr = Cg = Cb = Dp = 0.f;
-  term = false;
-  bool done = !active;
+  bool all_done = true;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    L.Cr[k] = L.Cg[k] = L.Cb[k] = L.Dp[k] = 0.f;
+    all_done = all_done && L.done[k];
+  }
   processed = 0;
-  if (__all_sync(0xffffffffu, done) || s0 >= s1) return;
+  if (__all_sync(FULL, all_done) || s0 >= s1) return;
   // gathers run one chunk ahead (cp.async), Gaussian ids two chunks ahead
   uint32_t gnext = s0 + lane < s1 ? __ldg(&B.gids[s0 + lane]) : 0u;
   if (s0 + lane < s1) {
@@ -464,11 +474,15 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   for (uint32_t b0 = s0; b0 < s1; b0 += 32, buf ^= 1) {
     // speculative pass of a later segment: every 2 chunks, drop pixels whose
     // predecessors have meanwhile published a dead prefix (Ls := dead, exact)
-    if (poll_stat && ((b0 - s0) & 63u) == 32u && !done && pred_dead(poll_stat, poll_s, B.epoch)) {
-      done = true;
-      term = true;
+    if (poll_stat && ((b0 - s0) & 63u) == 32u) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        if (!L.done[k] && pred_dead(poll_stat + 64 * k, poll_s, B.epoch)) L.done[k] = L.term[k] = true;
     }
-    if (__all_sync(0xffffffffu, done)) break;
+    all_done = true;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) all_done = all_done && L.done[k];
+    if (__all_sync(FULL, all_done)) break;
     if (b0 + 32 < s1) {  // prefetch the next chunk
       if (b0 + 32 + lane < s1) {
         float4 *dst = raw + ((buf ^ 1) * 32 + lane) * PF;
@@ -595,90 +609,104 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
         }
       }
     }
-    uint32_t m = __ballot_sync(0xffffffffu, maybe);
+    uint32_t m = __ballot_sync(FULL, maybe);
     __syncwarp();
-    if (MODE == 2) {
-      while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
-        if (done) continue;
-        ++n_eval;
-        const float4 *t = wt + j * NF;
-        const float4 f0 = t[0], f1 = t[1], f2 = t[2], f3v = t[3], f4 = t[4];
-        const float4 h = t[7], pu = t[8], qv = t[9];
-        float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
-        float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
-        float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
-        nx = fmaf(beta, fmaf(a, pu.x, fmaf(b, qv.x, h.x)), nx);
-        ny = fmaf(beta, fmaf(a, pu.y, fmaf(b, qv.y, h.y)), ny);
-        nz = fmaf(beta, fmaf(a, pu.z, fmaf(b, qv.z, h.z)), nz);
-        const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
-        const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
-        const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
-        const float N = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
-        const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
-        const float k2 = f0.w;
-        if (N > k2 * Dd) continue;  // omega^2 > k^2  <=>  alpha < alpha_min
-        const float rD = rcp_approx(Dd);
-        const float w2 = N * rD;
-        const float4 f5 = t[5];
-        float gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
-        gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
-        // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
-        const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, f4.w)));
-        if (!(al >= alpha_min)) continue;
-        const float tau = -gg * rD * snorm;
-        if (!(tau > 0.f)) continue;  // reading R24
-        const float Tn = T * (1.f - al);
-        if (Tn < t_min) {
-          done = true;
-          term = true;
-          continue;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t ta = wt_s + (uint32_t)j * (NF * 16);
+      if (MODE == 2) {
+        const float4 f0 = lds128(ta), f1 = lds128(ta + 16), f2 = lds128(ta + 32), f3v = lds128(ta + 48),
+                     f4 = lds128(ta + 64), f5 = lds128(ta + 80);
+        const float4 h = lds128(ta + 112), pu = lds128(ta + 128), qv = lds128(ta + 144);
+        float N[NP], Dd[NP];
+        bool hit[NP], any = false;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const float a = L.a[k], b = L.b[k], beta = L.beta[k];
+          float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
+          float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
+          float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
+          nx = fmaf(beta, fmaf(a, pu.x, fmaf(b, qv.x, h.x)), nx);
+          ny = fmaf(beta, fmaf(a, pu.y, fmaf(b, qv.y, h.y)), ny);
+          nz = fmaf(beta, fmaf(a, pu.z, fmaf(b, qv.z, h.z)), nz);
+          const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
+          const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
+          const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
+          N[k] = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
+          Dd[k] = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
+          n_eval += L.done[k] ? 0u : 1u;
+          // omega^2 <= k^2  <=>  alpha >= alpha_min
+          hit[k] = !L.done[k] && N[k] <= f0.w * Dd[k];
+          any = any || hit[k];
         }
-        const float4 cc = t[6];
-        const float wgt = al * T;
-        Cr = fmaf(wgt, cc.x, Cr);
-        Cg = fmaf(wgt, cc.y, Cg);
-        Cb = fmaf(wgt, cc.z, Cb);
-        Dp = fmaf(wgt, tau, Dp);
-        ++n_contrib;
-        T = Tn;
-      }
-    } else {
-      // one iteration per surviving entry; lanes predicated, the body skipped
-      // (warp-uniform branch) when no lane's pixel is inside the footprint
-      while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
-        const uint32_t ta = wt_s + (uint32_t)j * (NF * 16);
+        if (!__any_sync(FULL, any)) continue;
+        const float4 cc = lds128(ta + 96);
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const float a = L.a[k], b = L.b[k], beta = L.beta[k];
+          const float rD = rcp_approx(Dd[k]);
+          const float w2 = N[k] * rD;
+          float gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
+          gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
+          // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
+          const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, f4.w)));
+          const float tau = -gg * rD * L.snorm[k];
+          const float Tn = L.T[k] * (1.f - al);
+          const bool ok = hit[k] && al >= alpha_min && tau > 0.f;  // reading R24: tau > 0
+          const bool dead = ok && Tn < t_min;
+          if (dead) { L.done[k] = true; L.term[k] = true; }
+          if (ok && !dead) {
+            const float wgt = al * L.T[k];
+            L.Cr[k] = fmaf(wgt, cc.x, L.Cr[k]);
+            L.Cg[k] = fmaf(wgt, cc.y, L.Cg[k]);
+            L.Cb[k] = fmaf(wgt, cc.z, L.Cb[k]);
+            L.Dp[k] = fmaf(wgt, tau, L.Dp[k]);
+            ++n_contrib;
+            L.T[k] = Tn;
+          }
+        }
+      } else {
+        // lanes predicated, the body skipped (warp-uniform branch) when no
+        // pixel of the warp is inside the footprint
         const float4 f0 = lds128(ta), f1 = lds128(ta + 16);
-        n_eval += done ? 0u : 1u;
-        const float da = a - f1.z, db = b - f1.w;
-        // F = N - k^2 D <= 0  <=>  omega^2 <= k^2  <=>  alpha >= alpha_min
-        const float F = fmaf(da, fmaf(f0.w, da, fmaf(f1.x, db, f0.y)), fmaf(db, fmaf(f1.y, db, f0.z), f0.x));
-        const bool hit = !done && F <= 0.f;
-        if (!__any_sync(0xffffffffu, hit)) continue;
-        const float4 f2 = lds128(ta + 32), f3v = lds128(ta + 48), f4 = lds128(ta + 64);
-        const float Dd = fmaf(da, fmaf(f2.w, da, fmaf(f3v.x, db, f2.y)), fmaf(db, fmaf(f3v.y, db, f2.z), f2.x));
-        const float rD = rcp_approx(Dd);
-        const float w2 = fmaxf(fmaf(f4.y, Dd, F), 0.f) * rD;
-        const float gg = fmaf(da, f3v.w, fmaf(db, f4.x, f3v.z));
-        // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
-        const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, f4.z)));
-        const float tau = -gg * rD * snorm;
-        const float Tn = T * (1.f - al);
-        const bool ok = hit && al >= alpha_min && tau > 0.f;  // reading R24: tau > 0
-        const bool dead = ok && Tn < t_min;
-        if (dead) { done = true; term = true; }
-        if (ok && !dead) {
-          const float4 cc = lds128(ta + 80);
-          const float wgt = al * T;
-          Cr = fmaf(wgt, cc.x, Cr);
-          Cg = fmaf(wgt, cc.y, Cg);
-          Cb = fmaf(wgt, cc.z, Cb);
-          Dp = fmaf(wgt, tau, Dp);
-          ++n_contrib;
-          T = Tn;
+        float F[NP], da[NP], db[NP];
+        bool hit[NP], any = false;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          da[k] = L.a[k] - f1.z;
+          db[k] = L.b[k] - f1.w;
+          // F = N - k^2 D <= 0  <=>  omega^2 <= k^2  <=>  alpha >= alpha_min
+          F[k] = fmaf(da[k], fmaf(f0.w, da[k], fmaf(f1.x, db[k], f0.y)), fmaf(db[k], fmaf(f1.y, db[k], f0.z), f0.x));
+          n_eval += L.done[k] ? 0u : 1u;
+          hit[k] = !L.done[k] && F[k] <= 0.f;
+          any = any || hit[k];
+        }
+        if (!__any_sync(FULL, any)) continue;
+        const float4 f2 = lds128(ta + 32), f3v = lds128(ta + 48), f4 = lds128(ta + 64), cc = lds128(ta + 80);
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const float Dd = fmaf(da[k], fmaf(f2.w, da[k], fmaf(f3v.x, db[k], f2.y)),
+                                fmaf(db[k], fmaf(f3v.y, db[k], f2.z), f2.x));
+          const float rD = rcp_approx(Dd);
+          const float w2 = fmaxf(fmaf(f4.y, Dd, F[k]), 0.f) * rD;
+          const float gg = fmaf(da[k], f3v.w, fmaf(db[k], f4.x, f3v.z));
+          // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
+          const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, f4.z)));
+          const float tau = -gg * rD * L.snorm[k];
+          const float Tn = L.T[k] * (1.f - al);
+          const bool ok = hit[k] && al >= alpha_min && tau > 0.f;  // reading R24: tau > 0
+          const bool dead = ok && Tn < t_min;
+          if (dead) { L.done[k] = true; L.term[k] = true; }
+          if (ok && !dead) {
+            const float wgt = al * L.T[k];
+            L.Cr[k] = fmaf(wgt, cc.x, L.Cr[k]);
+            L.Cg[k] = fmaf(wgt, cc.y, L.Cg[k]);
+            L.Cb[k] = fmaf(wgt, cc.z, L.Cb[k]);
+            L.Dp[k] = fmaf(wgt, tau, L.Dp[k]);
+            ++n_contrib;
+            L.T[k] = Tn;
+          }
         }
       }
     }
@@ -733,14 +761,15 @@ __device__ bool fetch_work(const BlendBufs &B, int &unit, int &s) {
 }
 
 // Persistent CTAs (as many as fit), each warp looping independently over
-// work units (tile, warp block, segment) taken from the queues.  Per unit:
-// the lane's pixel, the speculative pass, the look-back, the redo, then either
-// the pixel write (single-segment tile) or the partials, the successor grants
-// and, in the warp completing the unit's last granted segment, the in-order
-// combine.  No CTA-wide barriers: a warp whose pixels finish early moves on.
+// work units (tile, 8x8 pixel block, segment) taken from the queues; a lane
+// owns NP = 2 pixels of the block (rows r and r + 4).  Per unit: the pixels,
+// the speculative pass, the look-back, the redo, then either the pixel write
+// (single-segment tile) or the partials, the successor grants and, in the
+// warp completing the unit's last granted segment, the in-order combine.  No
+// CTA-wide barriers: a warp whose pixels finish early moves on.
 template <int MODE>
-__global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, BlendBufs B) {
-  constexpr int NT = GUT_BLEND_THREADS;
+__global__ __launch_bounds__(GUT_BLEND_THREADS, GUT_BLEND_CTAS) void blend_kernel(DevCam c, BlendBufs B) {
+  constexpr int NT = GUT_BLEND_THREADS, NP = GUT_BLEND_NP;
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   uint32_t n_eval_acc = 0, n_contrib_acc = 0, n_term_acc = 0;
@@ -760,15 +789,25 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
     const int S = len == 0 ? 1 : (int)((len + B.seg - 1) / B.seg);
     const uint32_t s0 = start + (uint32_t)s * B.seg, s1 = min(s0 + (uint32_t)B.seg, end);
     const uint32_t slot = B.seg_base[tile] + (uint32_t)s;
-    const int pidx = w * 32 + lane;  // pixel of the tile (LUT, status and partial index)
-    int px, py;
-    tile_pixel(tile, c.tiles_x, w, lane, px, py);
-    const bool inside = px < c.width && py < c.height;
-
-    // ---- pixel ray (LUT) and the tile anchor in the world frame (fp64)
-    const float4 pl = B.pix[(size_t)tile * NT + pidx];
-    const float a = pl.x, b = pl.y, snorm = pl.z, beta = pl.w;
-    const bool valid = inside && snorm > 0.f;
+    // pixel k of the lane = lane of the 8x4 LUT block w8 (rays_kernel layout)
+    const int pidx0 = (((w & 1) | ((w >> 1) << 2)) << 5) + lane;  // + 64 k
+    LanePx<NP> L;
+    bool valid[NP], inside[NP];
+    int px[NP], py[NP];
+    float amin = 3e38f, amax = -3e38f, bmin = 3e38f, bmax = -3e38f;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      tile_pixel(tile, c.tiles_x, ((w & 1) | (((w >> 1) * 2 + k) << 1)), lane, px[k], py[k]);
+      inside[k] = px[k] < c.width && py[k] < c.height;
+      const float4 pl = B.pix[(size_t)tile * NT + pidx0 + 64 * k];
+      L.a[k] = pl.x; L.b[k] = pl.y; L.snorm[k] = pl.z; L.beta[k] = pl.w;
+      valid[k] = inside[k] && pl.z > 0.f;
+      if (valid[k]) {
+        amin = fminf(amin, pl.x); amax = fmaxf(amax, pl.x);
+        bmin = fminf(bmin, pl.y); bmax = fmaxf(bmax, pl.y);
+      }
+    }
+    // ---- the tile anchor in the world frame (fp64)
     const TileAnchor &A = B.anchors[tile];
     d3 D, T1, T2, O;
     if (MODE == 2) {
@@ -785,8 +824,6 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
     // warp pixel box in (a, b) for the conservative warp cull
     float ac, bc, ra, rb;
     {
-      float amin = valid ? a : 3e38f, amax = valid ? a : -3e38f;
-      float bmin = valid ? b : 3e38f, bmax = valid ? b : -3e38f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         amin = fminf(amin, __shfl_xor_sync(FULL, amin, o));
@@ -801,65 +838,88 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
       rb = 0.5f * (bmax - bmin) + 1e-7f * (fabsf(bmin) + fabsf(bmax));
     }
     if (s == 0 && w == 0 && lane == 0 && len > 0) atomicMax(&B.counters[CNT_MAXLEN], len);
-    unsigned long long *stat = B.status + (size_t)slot * NT + pidx;
+    unsigned long long *stat = B.status + (size_t)slot * NT + pidx0;  // pixel k: + 64 k
 
-    // ---- predecessor peek: pixels already known dead are skipped (same result)
-    bool run = valid;
-    if (s > 0 && valid && pred_dead(stat, s, B.epoch)) run = false;
-    // ---- speculative pass: transmittance from 1 (exact for segment 0)
-    float Cr, Cg, Cb, Dp, Tsp;
-    bool term;
+    // ---- predecessor peek (pixels already known dead are skipped: same result),
+    // then the speculative pass: transmittance from 1 (exact for segment 0)
+    bool run[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      run[k] = valid[k] && !(s > 0 && pred_dead(stat + 64 * k, s, B.epoch));
+      L.done[k] = !run[k];
+      L.term[k] = false;
+      L.T[k] = 1.f;
+    }
     uint32_t n_eval = 0, n_contrib = 0, processed = 0;
-    warp_pass<MODE>(c, B, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, run, 1.f, Cr, Cg,
-                    Cb, Dp, Tsp, term, n_eval, n_contrib, processed, s > 0 ? stat : nullptr, s);
-    const unsigned long long Ls = (term || (valid && !run)) ? GUT_L_DEAD : l_of(Tsp);
-    float T_pre = 1.f;
-    bool alive_in = valid;
-    if (S > 1) {
-      unsigned long long Lpre = 0;
-      if (s == 0) {
-        if (valid) st_relaxed(stat, st_word(2, B.epoch, Ls));
-      } else if (valid) {
-        st_relaxed(stat, st_word(1, B.epoch, Ls));
-        // decoupled look-back over this pixel's earlier segments (integer sums)
-        for (int j = s - 1;; --j) {
-          const unsigned long long wv = ld_relaxed(stat - (size_t)(s - j) * NT);
-          const uint32_t flag = (uint32_t)(wv >> 62);
-          if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (B.epoch & 0x3FFFFFu)) {
-            __nanosleep(256);  // predecessor still running: yield issue slots to the SM's other warps
-            ++j;
-            continue;
+    warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, L, n_eval, n_contrib, processed,
+                        s > 0 ? stat : nullptr, s);
+    float T_pre[NP], T_end[NP];
+    bool alive_in[NP], redo[NP], any_redo = false;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const unsigned long long Ls = (L.term[k] || (valid[k] && !run[k])) ? GUT_L_DEAD : l_of(L.T[k]);
+      T_pre[k] = 1.f;
+      alive_in[k] = valid[k];
+      if (S > 1 && valid[k]) {
+        unsigned long long *st = stat + 64 * k;
+        unsigned long long Lpre = 0;
+        if (s == 0) {
+          st_relaxed(st, st_word(2, B.epoch, Ls));
+        } else {
+          st_relaxed(st, st_word(1, B.epoch, Ls));
+          // decoupled look-back over this pixel's earlier segments (integer sums)
+          for (int j = s - 1;; --j) {
+            const unsigned long long wv = ld_relaxed(st - (size_t)(s - j) * NT);
+            const uint32_t flag = (uint32_t)(wv >> 62);
+            if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (B.epoch & 0x3FFFFFu)) {
+              __nanosleep(256);  // predecessor still running: yield issue slots to the SM's other warps
+              ++j;
+              continue;
+            }
+            Lpre += wv & ((1ull << 40) - 1);
+            if (Lpre >= GUT_L_DEAD) { Lpre = GUT_L_DEAD; break; }
+            if (flag == 2) break;
           }
-          Lpre += wv & ((1ull << 40) - 1);
-          if (Lpre >= GUT_L_DEAD) { Lpre = GUT_L_DEAD; break; }
-          if (flag == 2) break;
+          const unsigned long long Lin = Lpre + Ls >= GUT_L_DEAD ? GUT_L_DEAD : Lpre + Ls;
+          st_relaxed(st, st_word(2, B.epoch, Lin));
         }
-        const unsigned long long Lin = Lpre + Ls >= GUT_L_DEAD ? GUT_L_DEAD : Lpre + Ls;
-        st_relaxed(stat, st_word(2, B.epoch, Lin));
+        T_pre[k] = t_of(Lpre);
+        alive_in[k] = T_pre[k] >= c.t_min;
       }
-      T_pre = t_of(Lpre);
-      alive_in = valid && T_pre >= c.t_min;
+      // ---- exact result: scale the speculative sums, or redo the segment from T_pre
+      redo[k] = alive_in[k] && s > 0 && (L.term[k] || T_pre[k] * L.T[k] < c.t_min);
+      any_redo = any_redo || redo[k];
+      T_end[k] = L.T[k];
+      if (s > 0 && alive_in[k] && !redo[k]) {
+        L.Cr[k] *= T_pre[k]; L.Cg[k] *= T_pre[k]; L.Cb[k] *= T_pre[k]; L.Dp[k] *= T_pre[k];
+        T_end[k] = T_pre[k] * L.T[k];
+      }
     }
-    // ---- exact result: scale the speculative sums, or redo the segment from T_pre
-    const bool redo = alive_in && s > 0 && (term || T_pre * Tsp < c.t_min);
-    float T_end = Tsp;
-    if (s > 0 && alive_in && !redo) {
-      Cr *= T_pre; Cg *= T_pre; Cb *= T_pre; Dp *= T_pre;
-      T_end = T_pre * Tsp;
-    }
-    const bool wredo = __any_sync(FULL, redo);
+    const bool wredo = __any_sync(FULL, any_redo);
     if (wredo) {
-      float r0, r1, r2, r3, rT;
-      bool rterm;
+      LanePx<NP> R;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        R.a[k] = L.a[k]; R.b[k] = L.b[k]; R.beta[k] = L.beta[k]; R.snorm[k] = L.snorm[k];
+        R.T[k] = T_pre[k];
+        R.done[k] = !redo[k];
+        R.term[k] = false;
+      }
       uint32_t e2 = 0, c2 = 0, p2 = 0;
-      warp_pass<MODE>(c, B, s0, s1, D, O, T1f, T2f, a, b, beta, snorm, ac, bc, ra, rb, redo, T_pre, r0, r1,
-                      r2, r3, rT, rterm, e2, c2, p2, nullptr, 0);
-      if (redo) { Cr = r0; Cg = r1; Cb = r2; Dp = r3; T_end = rT; term = rterm; }
+      warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, R, e2, c2, p2, nullptr, 0);
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        if (redo[k]) {
+          L.Cr[k] = R.Cr[k]; L.Cg[k] = R.Cg[k]; L.Cb[k] = R.Cb[k]; L.Dp[k] = R.Dp[k];
+          T_end[k] = R.T[k];
+          L.term[k] = R.term[k];
+        }
       processed += p2;
     }
     n_eval_acc += n_eval;
     n_contrib_acc += n_contrib;
-    n_term_acc += (alive_in && term) ? 1u : 0u;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) n_term_acc += (alive_in[k] && L.term[k]) ? 1u : 0u;
     if (lane == 0) {
       atomicAdd(&B.tile_work[tile].y, processed);
       if (s == 0 && w == 0) B.tile_work[tile].x = len;
@@ -880,14 +940,20 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
 
     // ---- outputs: single segment -> pixels; else partials, successor grants,
     // and the in-order combine by the warp completing the unit's last granted segment
-    float Tf = T_end;
+    float Tf[NP];
     bool write = true;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) Tf[k] = T_end[k];
     if (S > 1) {
-      const size_t j = (size_t)slot * NT + pidx;
-      B.part_c[j] = alive_in ? make_float4(Cr, Cg, Cb, Dp) : make_float4(0.f, 0.f, 0.f, 0.f);
-      B.part_t[j] = alive_in ? T_end : -1.f;
-      const bool alive_out = alive_in && !term && T_end >= c.t_min;
-      float tmax = alive_out ? T_end : 0.f;
+      float tmax = 0.f;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const size_t j = (size_t)slot * NT + pidx0 + 64 * k;
+        B.part_c[j] = alive_in[k] ? make_float4(L.Cr[k], L.Cg[k], L.Cb[k], L.Dp[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        B.part_t[j] = alive_in[k] ? T_end[k] : -1.f;
+        const bool alive_out = alive_in[k] && !L.term[k] && T_end[k] >= c.t_min;
+        if (alive_out) tmax = fmaxf(tmax, T_end[k]);
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(FULL, tmax, o));
       __threadfence();  // partials visible before the completion count
@@ -931,27 +997,32 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, 3) void blend_kernel(DevCam c, B
       if (write) {
         __threadfence();
         const uint32_t first = B.seg_base[tile];
-        Cr = Cg = Cb = Dp = 0.f;
-        Tf = 1.f;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          float Cr = 0.f, Cg = 0.f, Cb = 0.f, Dp = 0.f, T = 1.f;
 #pragma unroll 8
-        for (uint32_t q = 0; q < nseg; ++q) {  // (unrolled: loads in flight, sums in order)
-          const size_t jj = (size_t)(first + q) * NT + pidx;
-          const float4 pc = __ldcg(&B.part_c[jj]);
-          const float pt = __ldcg(&B.part_t[jj]);
-          Cr += pc.x; Cg += pc.y; Cb += pc.z; Dp += pc.w;
-          if (pt >= 0.f) Tf = pt;
+          for (uint32_t q = 0; q < nseg; ++q) {  // (unrolled: loads in flight, sums in order)
+            const size_t jj = (size_t)(first + q) * NT + pidx0 + 64 * k;
+            const float4 pc = __ldcg(&B.part_c[jj]);
+            const float pt = __ldcg(&B.part_t[jj]);
+            Cr += pc.x; Cg += pc.y; Cb += pc.z; Dp += pc.w;
+            if (pt >= 0.f) T = pt;
+          }
+          L.Cr[k] = Cr; L.Cg[k] = Cg; L.Cb[k] = Cb; L.Dp[k] = Dp; Tf[k] = T;
         }
       }
     }
     if (write) {
-      if (inside) {
-        const size_t p = (size_t)py * c.width + px;
-        if (valid) {
-          B.rgb[3 * p] = Cr + Tf * c.bg[0];
-          B.rgb[3 * p + 1] = Cg + Tf * c.bg[1];
-          B.rgb[3 * p + 2] = Cb + Tf * c.bg[2];
-          B.alpha[p] = 1.f - Tf;
-          if (B.depth) B.depth[p] = Dp;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        if (!inside[k]) continue;
+        const size_t p = (size_t)py[k] * c.width + px[k];
+        if (valid[k]) {
+          B.rgb[3 * p] = L.Cr[k] + Tf[k] * c.bg[0];
+          B.rgb[3 * p + 1] = L.Cg[k] + Tf[k] * c.bg[1];
+          B.rgb[3 * p + 2] = L.Cb[k] + Tf[k] * c.bg[2];
+          B.alpha[p] = 1.f - Tf[k];
+          if (B.depth) B.depth[p] = L.Dp[k];
         } else {
           B.rgb[3 * p] = c.bg[0];
           B.rgb[3 * p + 1] = c.bg[1];

@@ -17,8 +17,8 @@ def L(p): return next(i+1 for i,l in enumerate(src) if p in l)
 bounds=[("warp_pass head",L("__device__ __forceinline__ void warp_pass"),L("      // ---- stage entry kk")),
 ("staging",L("      // ---- stage entry kk"),L("      // ---- conservative cull against")),
 ("cull1",L("      // ---- conservative cull against"),L("      if (maybe) {")),
-("table+cull2",L("      if (maybe) {"),L("    uint32_t m = __ballot_sync(0xffffffffu, maybe);")),
-("fine",L("    uint32_t m = __ballot_sync(0xffffffffu, maybe);"),L("  cp_async_wait<0>();  // a warp leaving")),
+("table+cull2",L("      if (maybe) {"),L("    uint32_t m = __ballot_sync(FULL, maybe);")),
+("fine",L("    uint32_t m = __ballot_sync(FULL, maybe);"),L("  cp_async_wait<0>();  // a warp leaving")),
 ("fetch",L("__device__ bool fetch_work"),L("// Persistent CTAs")),
 ("kernel",L("// Persistent CTAs"),L("    // ---- predecessor peek")),
 ("peek+pass",L("    // ---- predecessor peek"),L("        // decoupled look-back")),
