@@ -367,12 +367,12 @@ __device__ __forceinline__ unsigned long long st_word(uint32_t flag, uint32_t ep
   return ((unsigned long long)flag << 62) | ((unsigned long long)(epoch & 0x3FFFFFu) << 40) | L;
 }
 
-// True if the pixel is certainly dead before segment s: the published
-// products of some of its predecessors (aggregates back to the first
-// inclusive word, at most 4) already multiply below 2^-16 < T_min.  Any
-// subset of the prefix factors bounds the prefix from above, so words not yet
-// published are simply skipped.
-__device__ __forceinline__ bool pred_dead(const unsigned long long *stat, int s, uint32_t epoch) {
+// Upper bound of the pixel's prefix transmittance before segment s, as a
+// fixed-point -log2 sum: the published products of some of its predecessors
+// (aggregates back to the first inclusive word, at most 4).  Any subset of
+// the prefix factors bounds the prefix from above, so words not yet published
+// are simply skipped (0 = no information).
+__device__ __forceinline__ unsigned long long pred_L(const unsigned long long *stat, int s, uint32_t epoch) {
   unsigned long long L = 0;
   const int jmax = min(s, 4);
   for (int j = 1; j <= jmax; ++j) {
@@ -380,11 +380,25 @@ __device__ __forceinline__ bool pred_dead(const unsigned long long *stat, int s,
     const uint32_t flag = (uint32_t)(wv >> 62);
     if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (epoch & 0x3FFFFFu)) continue;
     L += wv & ((1ull << 40) - 1);
-    if (L >= GUT_L_DEAD) return true;
+    if (L >= GUT_L_DEAD) return GUT_L_DEAD;
     if (flag == 2) break;
   }
-  return false;
+  return L;
 }
+__device__ __forceinline__ bool pred_dead(const unsigned long long *stat, int s, uint32_t epoch) {
+  return pred_L(stat, s, epoch) >= GUT_L_DEAD;
+}
+
+// Redo checkpoints of a speculative pass: the lane's pixel state after every
+// `seg / GUT_CK` entries, recorded while the pixel is live, so a re-run from
+// the exact prefix T_pre resumes at the last checkpoint the exact sequence
+// certainly reached (T_pre T_c >= T_min) instead of at the segment start.
+#define GUT_CK 8
+template <int NP> struct Checkpoints {
+  float4 C[GUT_CK][NP];
+  float T[GUT_CK][NP];
+  int n[NP];
+};
 
 // Per-warp table of staged list entries (32 per chunk).  MODE 0/1: the
 // quadratic forms of F = |n|^2 - k^2 |e|^2 and D = |e|^2 in the lane's pixel
@@ -435,7 +449,8 @@ template <int MODE, int NP>
 __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, uint32_t s0, uint32_t s1,
                                           const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f, float ac, float bc,
                                           float ra, float rb, LanePx<NP> &L, uint32_t &n_eval, uint32_t &n_contrib,
-                                          uint32_t &processed, const unsigned long long *poll_stat, int poll_s) {
+                                          uint32_t &processed, const unsigned long long *poll_stat, int poll_s,
+                                          Checkpoints<NP> *ck, uint32_t ck_step) {
   constexpr int NF = WarpTbl<MODE>::NF;
   constexpr unsigned FULL = 0xffffffffu;
   // dynamic shared memory: [raw payload double buffer: 8 warps x 2 x 32 x 5]
@@ -457,8 +472,8 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   bool all_done = true;
 #pragma unroll
   for (int k = 0; k < NP; ++k) {
-    L.Cr[k] = L.Cg[k] = L.Cb[k] = L.Dp[k] = 0.f;
     all_done = all_done && L.done[k];
+    if (ck) ck->n[k] = 0;
   }
   processed = 0;
   if (__all_sync(FULL, all_done) || s0 >= s1) return;
@@ -472,12 +487,27 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   gnext = s0 + 32 + lane < s1 ? __ldg(&B.gids[s0 + 32 + lane]) : 0u;
   int buf = 0;
   for (uint32_t b0 = s0; b0 < s1; b0 += 32, buf ^= 1) {
-    // speculative pass of a later segment: every 2 chunks, drop pixels whose
-    // predecessors have meanwhile published a dead prefix (Ls := dead, exact)
+    // speculative pass of a later segment: every 2 chunks, stop pixels whose
+    // exact sequence has certainly terminated by now: T_spec times the bound of
+    // the published prefix below T_min (Ls := dead, exact; a re-run resolves it)
     if (poll_stat && ((b0 - s0) & 63u) == 32u) {
 #pragma unroll
       for (int k = 0; k < NP; ++k)
-        if (!L.done[k] && pred_dead(poll_stat + 64 * k, poll_s, B.epoch)) L.done[k] = L.term[k] = true;
+        if (!L.done[k]) {
+          const unsigned long long Lb = pred_L(poll_stat + 64 * k, poll_s, B.epoch);
+          if (Lb >= GUT_L_DEAD || L.T[k] * exp2f(-(float)Lb * 2.3283064365386963e-10f) < t_min)
+            L.done[k] = L.term[k] = true;
+        }
+    }
+    if (ck && b0 > s0 && (b0 - s0) % ck_step == 0u) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        if (!L.done[k]) {
+          const int c = (int)((b0 - s0) / ck_step) - 1;
+          ck->C[c][k] = make_float4(L.Cr[k], L.Cg[k], L.Cb[k], L.Dp[k]);
+          ck->T[c][k] = L.T[k];
+          ck->n[k] = c + 1;
+        }
     }
     all_done = true;
 #pragma unroll
@@ -611,6 +641,12 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
     }
     uint32_t m = __ballot_sync(FULL, maybe);
     __syncwarp();
+    {  // statistics: pairs (live pixel, surviving entry) of this chunk
+      uint32_t live = 0;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) live += L.done[k] ? 0u : 1u;
+      n_eval += live * (uint32_t)__popc(m);
+    }
     while (m) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
@@ -635,7 +671,6 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
           N[k] = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
           Dd[k] = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
-          n_eval += L.done[k] ? 0u : 1u;
           // omega^2 <= k^2  <=>  alpha >= alpha_min
           hit[k] = !L.done[k] && N[k] <= f0.w * Dd[k];
           any = any || hit[k];
@@ -678,7 +713,6 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           db[k] = L.b[k] - f1.w;
           // F = N - k^2 D <= 0  <=>  omega^2 <= k^2  <=>  alpha >= alpha_min
           F[k] = fmaf(da[k], fmaf(f0.w, da[k], fmaf(f1.x, db[k], f0.y)), fmaf(db[k], fmaf(f1.y, db[k], f0.z), f0.x));
-          n_eval += L.done[k] ? 0u : 1u;
           hit[k] = !L.done[k] && F[k] <= 0.f;
           any = any || hit[k];
         }
@@ -726,6 +760,17 @@ __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t *p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 
 __device__ bool fetch_work(const BlendBufs &B, int &unit, int &s) {
@@ -849,10 +894,13 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, GUT_BLEND_CTAS) void blend_kerne
       L.done[k] = !run[k];
       L.term[k] = false;
       L.T[k] = 1.f;
+      L.Cr[k] = L.Cg[k] = L.Cb[k] = L.Dp[k] = 0.f;
     }
     uint32_t n_eval = 0, n_contrib = 0, processed = 0;
+    Checkpoints<NP> ck;
+    const uint32_t ck_step = max(32u, ((uint32_t)B.seg / GUT_CK) & ~31u);
     warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, L, n_eval, n_contrib, processed,
-                        s > 0 ? stat : nullptr, s);
+                        s > 0 ? stat : nullptr, s, s > 0 ? &ck : nullptr, ck_step);
     float T_pre[NP], T_end[NP];
     bool alive_in[NP], redo[NP], any_redo = false;
 #pragma unroll
@@ -897,16 +945,37 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, GUT_BLEND_CTAS) void blend_kerne
     }
     const bool wredo = __any_sync(FULL, any_redo);
     if (wredo) {
+      // resume point: the latest checkpoint every re-running pixel of the warp
+      // certainly reached in the exact sequence (T_pre T_c >= T_min)
+      int cres = GUT_CK;
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        if (redo[k]) {
+          int ck_k = -1;
+          for (int q = ck.n[k] - 1; q >= 0; --q)
+            if (T_pre[k] * ck.T[q][k] >= c.t_min) { ck_k = q; break; }
+          cres = min(cres, ck_k);
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cres = min(cres, __shfl_xor_sync(FULL, cres, o));
       LanePx<NP> R;
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         R.a[k] = L.a[k]; R.b[k] = L.b[k]; R.beta[k] = L.beta[k]; R.snorm[k] = L.snorm[k];
-        R.T[k] = T_pre[k];
         R.done[k] = !redo[k];
         R.term[k] = false;
+        if (cres >= 0 && redo[k]) {
+          const float4 cc = ck.C[cres][k];
+          R.Cr[k] = T_pre[k] * cc.x; R.Cg[k] = T_pre[k] * cc.y; R.Cb[k] = T_pre[k] * cc.z; R.Dp[k] = T_pre[k] * cc.w;
+          R.T[k] = T_pre[k] * ck.T[cres][k];
+        } else {
+          R.Cr[k] = R.Cg[k] = R.Cb[k] = R.Dp[k] = 0.f;
+          R.T[k] = T_pre[k];
+        }
       }
       uint32_t e2 = 0, c2 = 0, p2 = 0;
-      warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, R, e2, c2, p2, nullptr, 0);
+      const uint32_t r0 = cres >= 0 ? s0 + (uint32_t)(cres + 1) * ck_step : s0;
+      warp_pass<MODE, NP>(c, B, r0, s1, D, O, T1f, T2f, ac, bc, ra, rb, R, e2, c2, p2, nullptr, 0, nullptr, 0);
 #pragma unroll
       for (int k = 0; k < NP; ++k)
         if (redo[k]) {
@@ -956,8 +1025,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, GUT_BLEND_CTAS) void blend_kerne
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(FULL, tmax, o));
-      __threadfence();  // partials visible before the completion count
-      __syncwarp();
+      __syncwarp();  // the lanes' partials are ordered before lane 0's release below
       uint32_t nseg = 0;
       const uint32_t g0 = (uint32_t)min(S, B.window);
       if (lane == 0) {
@@ -986,16 +1054,16 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, GUT_BLEND_CTAS) void blend_kerne
             g = prev;
           }
         }
-        __threadfence();
-        const uint32_t d = atomicAdd(&B.unit_done[unit], 1u) + 1u;
-        __threadfence();
-        const uint32_t g = g0 + ld_volatile_u32(&B.granted[unit]);
+        // completion count with acq_rel: releases this segment's partials and
+        // grants, acquires those of every segment counted before it
+        const uint32_t d = atom_add_acq_rel(&B.unit_done[unit], 1u) + 1u;
+        const uint32_t g = g0 + ld_acquire_u32(&B.granted[unit]);
         nseg = d == g ? g : 0u;
       }
       nseg = __shfl_sync(FULL, nseg, 0);
       write = nseg != 0;
       if (write) {
-        __threadfence();
+        __syncwarp();  // lane 0's acquire orders the other lanes' loads (L2 reads, __ldcg)
         const uint32_t first = B.seg_base[tile];
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
@@ -1031,11 +1099,7 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, GUT_BLEND_CTAS) void blend_kerne
           if (B.depth) B.depth[p] = 0.f;
         }
       }
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        atomicAdd(&B.counters[CNT_Q_FINISHED], 1u);
-      }
+      if (lane == 0) atomicAdd(&B.counters[CNT_Q_FINISHED], 1u);  // termination count only (no data)
     }
   }
   // ---- statistics (once per warp)
