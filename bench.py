@@ -321,7 +321,7 @@ def run_ours(args):
     rl = roofline(stage_ms, work, peaks, clk)
     dom = max(rl, key=lambda k: rl[k]["ms"])
     d = rl[dom]
-    launches_per_render = 2 + 4 + 1 + (2 if n_tiles > 256 else 1) + 1 + 4  # K1+wide, 4 depth, emit, tile passes, ranges, plan (3) + blend
+    launches_per_render = 2 + 4 + 3 + (2 if n_tiles > 256 else 1) + 1 + 4  # K1+wide, 4 depth, emit (count, scan, emit), tile passes, ranges, plan (3) + blend
     total_views = world * args.steps
     fps = total_views / (ms_max * 1e-3)
     line = {

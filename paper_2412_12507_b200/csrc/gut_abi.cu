@@ -480,7 +480,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   }
   // K2: depth-ordered scan + emission of (tile, gid) keys
   launch_emit(order, cnt + CNT_NVIS, n32, ctx->tiles, ctx->ell, ctx->ell64, dc.tiles_x, dc.tile_cull, ctx->ka, ctx->va,
-              (uint32_t)ctx->cap_k, cnt, ctx->st_emit, ++ctx->epoch, st);
+              (uint32_t)ctx->cap_k, cnt, reinterpret_cast<uint32_t *>(ctx->st_emit), st);
   if (timing) cudaEventRecord(ev[3], st);
   // K3 level 2: stable tile passes
   const uint32_t *ht = cnt + CNT_HIST_TILE;
@@ -664,7 +664,8 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
     gut_proj_record *r = (gut_proj_record *)host_dst;
     for (size_t i = 0; i < N; ++i) {
       memset(&r[i], 0, sizeof(r[i]));
-      r[i].tiles = tl[i];
+      // tile code (gut_internal.cuh ell_tile_code) -> tile count
+      r[i].tiles = (tl[i] >> 31) ? (tl[i] & 0x7FFFFFFFu) : (uint32_t)__builtin_popcount(tl[i] & 0x1FFu);
       if (!tl[i]) continue;
       float4 a = el[2 * i], b = el[2 * i + 1], p4 = pl[GUT_PAYLOAD_F4 * i + 4];
       r[i].vx = a.x; r[i].vy = a.y; r[i].cxx = a.z; r[i].cxy = a.w; r[i].cyy = b.x; r[i].k2 = fabsf(b.y);

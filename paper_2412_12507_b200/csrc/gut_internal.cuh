@@ -120,34 +120,50 @@ struct EllT {
 using Ell = EllT<float>;
 using EllD = EllT<double>;
 
+// fp32: MUFU square root / reciprocal (relative error ~2^-22, far inside the
+// 1e-3 px binning band; K1 and K2 share them, so counts still match keys)
+__device__ __forceinline__ float rs_sqrt(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ double rs_sqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float rs_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ double rs_rcp(double x) { return 1.0 / x; }
+
 template <class Real>
 __device__ __forceinline__ void row_span(const EllT<Real> &e, int ty, int tile_cull, int &lo, int &hi) {
   if (tile_cull == 0) { lo = e.x0; hi = e.x1; return; }
-  const Real zero = 0, tile = GUT_TILE;
-  Real hy = sqrt(e.k2 * e.cyy);
+  const Real zero = 0, itile = (Real)(1.0 / GUT_TILE);
+  Real hy = rs_sqrt(e.k2 * e.cyy);
   Real a = fmax((Real)(GUT_TILE * ty) - e.vy, -hy);
   Real b = fmin((Real)(GUT_TILE * ty + GUT_TILE) - e.vy, hy);
   if (a > b) { lo = 1; hi = 0; return; }
-  Real hx = sqrt(e.k2 * e.cxx);
-  Real ystar = e.cxy * sqrt(e.k2 / e.cxx);  // dy of the rightmost point (leftmost at -ystar)
-  Real slope = e.cxy / e.cyy;
+  const Real icxx = rs_rcp(e.cxx), icyy = rs_rcp(e.cyy);
+  Real hx = rs_sqrt(e.k2 * e.cxx);
+  Real ystar = e.cxy * rs_sqrt(e.k2 * icxx);  // dy of the rightmost point (leftmost at -ystar)
+  Real slope = e.cxy * icyy;
   Real cond = fmax(e.cxx - e.cxy * slope, zero);  // det / cyy
   Real xr, xl;
   if (ystar >= a && ystar <= b) xr = hx;
   else {
     Real yy = ystar < a ? a : b;
-    xr = slope * yy + sqrt(fmax(cond * (e.k2 - yy * yy / e.cyy), zero));
+    xr = slope * yy + rs_sqrt(fmax(cond * (e.k2 - yy * yy * icyy), zero));
   }
   if (-ystar >= a && -ystar <= b) xl = -hx;
   else {
     Real yy = -ystar < a ? a : b;
-    xl = slope * yy - sqrt(fmax(cond * (e.k2 - yy * yy / e.cyy), zero));
+    xl = slope * yy - rs_sqrt(fmax(cond * (e.k2 - yy * yy * icyy), zero));
   }
   Real XL = e.vx + xl, XR = e.vx + xr;
   XL = fmin(fmax(XL, (Real)-1e7), (Real)1e7);
   XR = fmin(fmax(XR, (Real)-1e7), (Real)1e7);
-  int l = (int)ceil(XL / tile) - 1;
-  int h = (int)floor(XR / tile);
+  int l = (int)ceil(XL * itile) - 1;
+  int h = (int)floor(XR * itile);
   lo = max(l, e.x0);
   hi = min(h, e.x1);
 }
@@ -162,6 +178,30 @@ __device__ __forceinline__ int ell_tile_count(const EllT<Real> &e, int tile_cull
     n += max(hi - lo + 1, 0);
   }
   return n;
+}
+
+// K1 -> K2 tile code per Gaussian: 0 = culled; bit 31 clear: tile rectangle
+// of at most 3x3 tiles, bits 0-8 = hit mask (row-major over the rectangle),
+// bits 9-19 = x0, bits 20-30 = y0; bit 31 set: bits 0-30 = tile count (K2
+// walks the rows of the ellipse record).  Counts and masks come from the same
+// row_span() calls, so K2 emits exactly the counted keys.
+template <class Real>
+__device__ __forceinline__ uint32_t ell_tile_code(const EllT<Real> &e, int tile_cull) {
+  const int w = e.x1 - e.x0 + 1, h = e.y1 - e.y0 + 1;
+  if (w <= 3 && h <= 3 && e.x0 < 2048 && e.y0 < 2048) {
+    uint32_t mask = 0;
+    for (int r = 0; r < h; ++r) {
+      int lo, hi;
+      row_span(e, e.y0 + r, tile_cull, lo, hi);
+      for (int x = lo; x <= hi; ++x) mask |= 1u << (3 * r + (x - e.x0));
+    }
+    return mask ? (mask | ((uint32_t)e.x0 << 9) | ((uint32_t)e.y0 << 20)) : 0u;
+  }
+  const int n = ell_tile_count(e, tile_cull);
+  return n > 0 ? (0x80000000u | (uint32_t)min(n, 0x7FFFFFFF)) : 0u;
+}
+__device__ __forceinline__ uint32_t code_count(uint32_t code) {
+  return (code >> 31) ? (code & 0x7FFFFFFFu) : (uint32_t)__popc(code & 0x1FFu);
 }
 
 __device__ __forceinline__ Ell load_ell(const float4 *ell, uint32_t g) {

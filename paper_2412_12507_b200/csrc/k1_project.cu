@@ -326,7 +326,7 @@ __global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, u
   for (int j = threadIdx.x; j < 1024; j += 256) (&s_hist[0][0])[j] = 0;
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
-  uint32_t my_tiles = 0, key = GUT_CULLED_KEY;
+  uint32_t my_code = 0, key = GUT_CULLED_KEY;  // my_code: tile code (gut_internal.cuh)
   if (i < s.n) {
     float4 po, sc;
     float R[9];
@@ -394,8 +394,8 @@ __global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, u
       e.y0 = max((int)fy0, 0); e.y1 = min((int)fy1, c.tiles_y - 1);
       ok = e.x0 <= e.x1 && e.y0 <= e.y1;
       if (ok) {
-        my_tiles = (uint32_t)ell_tile_count(e, c.tile_cull);
-        ok = my_tiles > 0;
+        my_code = ell_tile_code(e, c.tile_cull);
+        ok = my_code != 0;
       }
     }
     if (ok) {
@@ -405,14 +405,14 @@ __global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, u
                                              __uint_as_float(pack_rect(e.x1, e.y1))),
                                  ell, payload);
     } else {
-      my_tiles = 0;
+      my_code = 0;
       key = GUT_CULLED_KEY;
     }
     dkey[i] = key;
-    tiles[i] = my_tiles;
+    tiles[i] = my_code;
     if (wide) deferred[atomicAdd(&counters[CNT_NDEFER], 1u)] = (uint32_t)i;
   }
-  k1_block_totals(my_tiles, key, s_hist, s_k, s_nv, counters);
+  k1_block_totals(code_count(my_code), key, s_hist, s_k, s_nv, counters);
 }
 
 // ---- K1 wide (fp64 UT + fp64 ellipse) for the deferred Gaussians.  The packed
@@ -431,7 +431,7 @@ __global__ __launch_bounds__(256) void project_wide_kernel(DevCam c, SceneDev s,
     __syncthreads();
     for (int j = threadIdx.x; j < 1024; j += 256) (&s_hist[0][0])[j] = 0;
     __syncthreads();
-    uint32_t my_tiles = 0, key = GUT_CULLED_KEY;
+    uint32_t my_code = 0, key = GUT_CULLED_KEY;  // my_code: tile code (gut_internal.cuh)
     const uint32_t q = base + threadIdx.x;
     if (q < nd) {
       const int64_t i = deferred[q];
@@ -474,8 +474,8 @@ __global__ __launch_bounds__(256) void project_wide_kernel(DevCam c, SceneDev s,
           e.y0 = (int)fmax(fy0, 0.0); e.y1 = (int)fmin(fy1, (double)(c.tiles_y - 1));
           ok = e.x0 <= e.x1 && e.y0 <= e.y1;
           if (ok) {
-            my_tiles = (uint32_t)ell_tile_count(e, c.tile_cull);
-            ok = my_tiles > 0;
+            my_code = ell_tile_code(e, c.tile_cull);
+            ok = my_code != 0;
           }
         }
       }
@@ -489,13 +489,13 @@ __global__ __launch_bounds__(256) void project_wide_kernel(DevCam c, SceneDev s,
                                                __uint_as_float(pack_rect(e.x1, e.y1))),
                                    ell, payload);
       } else {
-        my_tiles = 0;
+        my_code = 0;
         key = GUT_CULLED_KEY;
       }
       dkey[i] = key;
-      tiles[i] = my_tiles;
+      tiles[i] = my_code;
     }
-    k1_block_totals(my_tiles, key, s_hist, s_k, s_nv, counters);
+    k1_block_totals(code_count(my_code), key, s_hist, s_k, s_nv, counters);
   }
 }
 

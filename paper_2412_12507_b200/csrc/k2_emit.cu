@@ -19,117 +19,222 @@
 
 namespace gut {
 
+// block-wide exclusive scan of two values at once (256 threads)
+__device__ __forceinline__ void block_scan2(uint32_t x, uint32_t y, uint32_t *s_tmp, uint32_t &ex, uint32_t &ey,
+                                            uint32_t &tx, uint32_t &ty) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t a = x, b = y;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t pa = __shfl_up_sync(0xffffffffu, a, o), pb = __shfl_up_sync(0xffffffffu, b, o);
+    if (lane >= o) { a += pa; b += pb; }
+  }
+  if (lane == 31) { s_tmp[w] = a; s_tmp[8 + w] = b; }
+  __syncthreads();
+  uint32_t wa = 0, wb = 0;
+  tx = ty = 0;
+#pragma unroll
+  for (int ww = 0; ww < GUT_EMIT_THREADS / 32; ++ww) {
+    const uint32_t va = s_tmp[ww], vb = s_tmp[8 + ww];
+    if (ww < w) { wa += va; wb += vb; }
+    tx += va; ty += vb;
+  }
+  ex = wa + a - x;
+  ey = wb + b - y;
+  __syncthreads();  // s_tmp reusable
+}
+
+// A CTA owns GUT_EMIT_PART consecutive Gaussians (depth order); its first
+// key slot comes from emit_count_kernel + emit_scan_kernel (per-partition key
+// totals, scanned), so no CTA waits on another.  K2 reads only the 4-byte
+// tile code per Gaussian (gut_internal.cuh ell_tile_code): a Gaussian whose
+// tile rectangle is at most 3x3 emits its keys straight from the hit mask;
+// the others ("big", a few percent) are expanded one at a time by a warp: a
+// lane per tile row computes the span with row_span() (the function K1
+// counted with), a warp scan places the rows, and the keys are written by
+// consecutive lanes.
+__device__ __forceinline__ void emit_key(uint32_t pos, uint32_t tile, uint32_t g, uint32_t cap_k, uint32_t *out_tile,
+                                         uint32_t *out_gid, uint32_t (*s_hist)[256], uint32_t *counters) {
+  if (pos < cap_k) {
+    out_tile[pos] = tile;
+    out_gid[pos] = g;
+    atomicAdd(&s_hist[0][tile & 255u], 1u);
+    atomicAdd(&s_hist[1][(tile >> 8) & 255u], 1u);
+  } else {
+    counters[CNT_OVERFLOW] = 1u;
+  }
+}
+
 __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
     const uint32_t *__restrict__ order, const uint32_t *n_vis_p, const uint32_t *__restrict__ tiles,
     const float4 *__restrict__ ell, const double2 *__restrict__ ell64, int tiles_x, int tile_cull,
-    uint32_t *__restrict__ out_tile,
-    uint32_t *__restrict__ out_gid, uint32_t cap_k, uint32_t *counters, unsigned long long *status,
-    uint32_t epoch) {
-  __shared__ uint32_t s_incl[GUT_EMIT_PART];
-  __shared__ uint32_t s_gid[GUT_EMIT_PART];
-  __shared__ float4 s_e0[GUT_EMIT_PART];  // vx, vy, cxx, cxy
-  __shared__ float4 s_e1[GUT_EMIT_PART];  // cyy, k2, rect0, rect1
+    uint32_t *__restrict__ out_tile, uint32_t *__restrict__ out_gid, uint32_t cap_k, uint32_t *counters,
+    const uint32_t *__restrict__ part_off) {
+  constexpr unsigned FULL = 0xffffffffu;
   __shared__ uint32_t s_hist[2][256];
   __shared__ uint32_t s_tmp[16];
-  __shared__ uint32_t s_part, s_prefix;
 
   const uint32_t n = *n_vis_p;
-  if (threadIdx.x == 0) s_part = atomicAdd(&counters[CNT_TICKETS + 4], 1u);
-  for (int j = threadIdx.x; j < 512; j += GUT_EMIT_THREADS) (&s_hist[0][0])[j] = 0;
-  __syncthreads();
-  const uint32_t part = s_part;
-  const uint32_t base = part * GUT_EMIT_PART;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t base = blockIdx.x * GUT_EMIT_PART;
   if (base >= n) return;
+  const uint32_t prefix = __ldg(&part_off[blockIdx.x]);
+  for (int j = tid; j < 512; j += GUT_EMIT_THREADS) (&s_hist[0][0])[j] = 0;
 
-  // load 4 consecutive Gaussians per thread, thread-local inclusive scan
-  uint32_t c[GUT_EMIT_ITEMS], acc = 0;
+  // ---- codes and counts (4 consecutive Gaussians per thread), block scan
+  uint32_t g[GUT_EMIT_ITEMS], code[GUT_EMIT_ITEMS], sc = 0;
 #pragma unroll
   for (int j = 0; j < GUT_EMIT_ITEMS; ++j) {
-    uint32_t li = threadIdx.x * GUT_EMIT_ITEMS + j, gi = base + li;
-    uint32_t g = 0, cnt = 0;
+    const uint32_t gi = base + tid * GUT_EMIT_ITEMS + j;
+    g[j] = 0;
+    code[j] = 0;
     if (gi < n) {
-      g = __ldg(&order[gi]);
-      cnt = __ldg(&tiles[g]);
-      s_e0[li] = __ldg(&ell[2 * g]);
-      s_e1[li] = __ldg(&ell[2 * g + 1]);
+      g[j] = __ldg(&order[gi]);
+      code[j] = __ldg(&tiles[g[j]]);
     }
-    s_gid[li] = g;
-    acc += cnt;
-    c[j] = acc;
+    sc += code_count(code[j]);
   }
-  // block exclusive scan of per-thread sums
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t x = acc;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_tmp[w] = x;
-  __syncthreads();
-  uint32_t wpre = 0, total = 0;
-  for (int ww = 0; ww < GUT_EMIT_THREADS / 32; ++ww) {
-    if (ww < w) wpre += s_tmp[ww];
-    total += s_tmp[ww];
-  }
-  const uint32_t texcl = wpre + x - acc;
-#pragma unroll
-  for (int j = 0; j < GUT_EMIT_ITEMS; ++j) s_incl[threadIdx.x * GUT_EMIT_ITEMS + j] = texcl + c[j];
-  if (threadIdx.x == 0) s_prefix = lookback(status, 1, (int)part, 0, total, epoch);
-  __syncthreads();
-  const uint32_t prefix = s_prefix;
+  uint32_t ex, ey, total, ty_;
+  block_scan2(sc, 0u, s_tmp, ex, ey, total, ty_);  // (its barriers also order the s_hist reset)
 
-  // one output slot per thread per round
-  for (uint32_t e = threadIdx.x; e < total; e += GUT_EMIT_THREADS) {
-    // Gaussian owning slot e: first li with s_incl[li] > e
-    int lo = 0, hi = GUT_EMIT_PART - 1;
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (s_incl[mid] > e) hi = mid; else lo = mid + 1;
-    }
-    uint32_t j = e - (lo > 0 ? s_incl[lo - 1] : 0u);
-    float4 a = s_e0[lo], b = s_e1[lo];
-    Ell el;
-    el.vx = a.x; el.vy = a.y; el.cxx = a.z; el.cxy = a.w; el.cyy = b.x; el.k2 = b.y;
-    uint32_t r0 = __float_as_uint(b.z), r1 = __float_as_uint(b.w);
-    el.x0 = (int)(r0 & 0xFFFF); el.y0 = (int)(r0 >> 16); el.x1 = (int)(r1 & 0xFFFF); el.y1 = (int)(r1 >> 16);
-    uint32_t tile = 0;
-    if (el.k2 >= 0.f) {
-      for (int ty = el.y0; ty <= el.y1; ++ty) {
-        int l, h;
-        row_span(el, ty, tile_cull, l, h);
-        uint32_t cnt = (uint32_t)max(h - l + 1, 0);
-        if (j < cnt) { tile = (uint32_t)(ty * tiles_x + l + (int)j); break; }
-        j -= cnt;
+  // ---- small Gaussians: keys from the mask, row-major
+  uint32_t pos = prefix + ex;
+  bool big[GUT_EMIT_ITEMS];
+  uint32_t bpos[GUT_EMIT_ITEMS];
+#pragma unroll
+  for (int j = 0; j < GUT_EMIT_ITEMS; ++j) {
+    big[j] = (code[j] >> 31) != 0u;
+    bpos[j] = pos;
+    if (!big[j] && code[j]) {
+      const uint32_t x0 = (code[j] >> 9) & 0x7FFu, y0 = (code[j] >> 20) & 0x7FFu;
+      for (uint32_t m = code[j] & 0x1FFu; m; m &= m - 1) {
+        const uint32_t b = (uint32_t)(__ffs(m) - 1);
+        const uint32_t tile = (y0 + b / 3u) * (uint32_t)tiles_x + x0 + b % 3u;
+        emit_key(pos++, tile, g[j], cap_k, out_tile, out_gid, s_hist, counters);
       }
-    } else {  // "wide" Gaussian: fp64 ellipse written by the fp64 K1 kernel
-      const uint32_t g = s_gid[lo];
-      const double2 q0 = ell64[3 * g], q1 = ell64[3 * g + 1], q2 = ell64[3 * g + 2];
-      EllD ed;
-      ed.vx = q0.x; ed.vy = q0.y; ed.cxx = q1.x; ed.cxy = q1.y; ed.cyy = q2.x; ed.k2 = q2.y;
-      ed.x0 = el.x0; ed.y0 = el.y0; ed.x1 = el.x1; ed.y1 = el.y1;
-      for (int ty = ed.y0; ty <= ed.y1; ++ty) {
-        int l, h;
-        row_span(ed, ty, tile_cull, l, h);
-        uint32_t cnt = (uint32_t)max(h - l + 1, 0);
-        if (j < cnt) { tile = (uint32_t)(ty * tiles_x + l + (int)j); break; }
-        j -= cnt;
-      }
-    }
-    uint32_t pos = prefix + e;
-    if (pos < cap_k) {
-      out_tile[pos] = tile;
-      out_gid[pos] = s_gid[lo];
-      atomicAdd(&s_hist[0][tile & 255u], 1u);
-      atomicAdd(&s_hist[1][(tile >> 8) & 255u], 1u);
     } else {
-      counters[CNT_OVERFLOW] = 1u;
+      pos += code_count(code[j]);
+    }
+  }
+  // ---- big Gaussians: one warp each, a lane per tile row
+#pragma unroll
+  for (int j = 0; j < GUT_EMIT_ITEMS; ++j) {
+    for (uint32_t bm = __ballot_sync(FULL, big[j]); bm; bm &= bm - 1) {
+      const int src = __ffs(bm) - 1;
+      const uint32_t gg = __shfl_sync(FULL, g[j], src);
+      uint32_t kpos = __shfl_sync(FULL, bpos[j], src);
+      const float4 a = __ldg(&ell[2 * gg]), b = __ldg(&ell[2 * gg + 1]);
+      const uint32_t r0w = __float_as_uint(b.z), r1w = __float_as_uint(b.w);
+      const int x0 = (int)(r0w & 0xFFFF), y0 = (int)(r0w >> 16), x1 = (int)(r1w & 0xFFFF), y1 = (int)(r1w >> 16);
+      const bool wide = b.y < 0.f;
+      Ell el;
+      EllD ed;
+      if (!wide) {
+        el.vx = a.x; el.vy = a.y; el.cxx = a.z; el.cxy = a.w; el.cyy = b.x; el.k2 = b.y;
+        el.x0 = x0; el.y0 = y0; el.x1 = x1; el.y1 = y1;
+      } else {  // "wide" Gaussian: fp64 ellipse written by the fp64 K1 kernel
+        const double2 q0 = ell64[3 * gg], q1 = ell64[3 * gg + 1], q2 = ell64[3 * gg + 2];
+        ed.vx = q0.x; ed.vy = q0.y; ed.cxx = q1.x; ed.cxy = q1.y; ed.cyy = q2.x; ed.k2 = q2.y;
+        ed.x0 = x0; ed.y0 = y0; ed.x1 = x1; ed.y1 = y1;
+      }
+      for (int rb = y0; rb <= y1; rb += 32) {
+        const int ty = rb + lane;
+        int l = 0, h = -1;
+        if (ty <= y1) {
+          if (!wide) row_span(el, ty, tile_cull, l, h);
+          else row_span(ed, ty, tile_cull, l, h);
+        }
+        const uint32_t cnt = (uint32_t)max(h - l + 1, 0);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const uint32_t tot = __shfl_sync(FULL, incl, 31);
+        for (uint32_t e0 = 0; e0 < tot; e0 += 32) {  // warp-uniform trip count (full-mask shuffles)
+          const uint32_t e = e0 + (uint32_t)lane;
+          int lo = 0;  // first row (lane) with incl > e
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t v = __shfl_sync(FULL, incl, lo + step - 1);
+            if (v <= e) lo += step;
+          }
+          const uint32_t ex_lo = __shfl_sync(FULL, incl - cnt, lo);
+          const int l_lo = __shfl_sync(FULL, l, lo);
+          if (e < tot) {
+            const uint32_t tile = (uint32_t)(rb + lo) * (uint32_t)tiles_x + (uint32_t)l_lo + (e - ex_lo);
+            emit_key(kpos + e, tile, gg, cap_k, out_tile, out_gid, s_hist, counters);
+          }
+        }
+        kpos += tot;
+      }
     }
   }
   __syncthreads();
-  for (int jj = threadIdx.x; jj < 512; jj += GUT_EMIT_THREADS) {
-    uint32_t v = (&s_hist[0][0])[jj];
+  for (int jj = tid; jj < 512; jj += GUT_EMIT_THREADS) {
+    const uint32_t v = (&s_hist[0][0])[jj];
     if (v) atomicAdd(&counters[CNT_HIST_TILE + jj], v);
+  }
+}
+
+// per-partition key totals (the emit's partition prefixes after the scan)
+__global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_count_kernel(const uint32_t *__restrict__ order,
+                                                                      const uint32_t *n_vis_p,
+                                                                      const uint32_t *__restrict__ tiles,
+                                                                      uint32_t *__restrict__ part_off) {
+  __shared__ uint32_t s_w[GUT_EMIT_THREADS / 32];
+  const uint32_t n = *n_vis_p, base = blockIdx.x * GUT_EMIT_PART;
+  if (base >= n) return;
+  uint32_t sum = 0;
+#pragma unroll
+  for (int j = 0; j < GUT_EMIT_ITEMS; ++j) {
+    const uint32_t gi = base + j * GUT_EMIT_THREADS + threadIdx.x;
+    if (gi < n) sum += code_count(__ldg(&tiles[__ldg(&order[gi])]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < GUT_EMIT_THREADS / 32; ++w) t += s_w[w];
+    part_off[blockIdx.x] = t;
+  }
+}
+
+// exclusive scan of the partition totals in place (one CTA; partitions past
+// n_vis hold stale values but are never read)
+__global__ __launch_bounds__(1024) void emit_scan_kernel(const uint32_t *n_vis_p, uint32_t *__restrict__ part_off) {
+  __shared__ uint32_t s_w[32];
+  const uint32_t n = *n_vis_p, np = (n + GUT_EMIT_PART - 1) / GUT_EMIT_PART;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t run = 0;
+  for (uint32_t b0 = 0; b0 < np; b0 += 1024) {
+    const uint32_t i = b0 + threadIdx.x;
+    const uint32_t v = i < np ? part_off[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t y = s_w[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += z;
+      }
+      s_w[lane] = y;
+    }
+    __syncthreads();
+    const uint32_t ex = run + (w > 0 ? s_w[w - 1] : 0u) + x - v;
+    if (i < np) part_off[i] = ex;
+    run += s_w[31];
+    __syncthreads();
   }
 }
 
@@ -146,13 +251,13 @@ __global__ void ranges_kernel(const uint32_t *__restrict__ tile_sorted, const ui
 
 void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper, const uint32_t *tiles,
                  const float4 *ell, const double2 *ell64, int tiles_x, int tile_cull, uint32_t *out_tile,
-                 uint32_t *out_gid,
-                 uint32_t cap_k, uint32_t *counters, unsigned long long *status, uint32_t epoch,
-                 cudaStream_t st) {
+                 uint32_t *out_gid, uint32_t cap_k, uint32_t *counters, uint32_t *part_off, cudaStream_t st) {
   if (n_upper == 0) return;
   unsigned blocks = (n_upper + GUT_EMIT_PART - 1) / GUT_EMIT_PART;
+  emit_count_kernel<<<blocks, GUT_EMIT_THREADS, 0, st>>>(order, n_vis, tiles, part_off);
+  emit_scan_kernel<<<1, 1024, 0, st>>>(n_vis, part_off);
   emit_kernel<<<blocks, GUT_EMIT_THREADS, 0, st>>>(order, n_vis, tiles, ell, ell64, tiles_x, tile_cull, out_tile, out_gid,
-                                                   cap_k, counters, status, epoch);
+                                                   cap_k, counters, part_off);
 }
 
 void launch_ranges(const uint32_t *tile_sorted, const uint32_t *counters, uint32_t cap_k, uint2 *ranges,

@@ -54,10 +54,11 @@ void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t
                       const uint32_t *hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch,
                       bool first, cudaStream_t st);
 
+// K2: per-partition key totals, their scan, then the emission (part_off:
+// one uint32 per GUT_EMIT_PART Gaussians of the upper bound n_upper)
 void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper, const uint32_t *tiles,
-                 const float4 *ell, const double2 *ell64, int tiles_x, int tile_cull, uint32_t *out_tile, uint32_t *out_gid,
-                 uint32_t cap_k, uint32_t *counters, unsigned long long *status, uint32_t epoch,
-                 cudaStream_t st);
+                 const float4 *ell, const double2 *ell64, int tiles_x, int tile_cull, uint32_t *out_tile,
+                 uint32_t *out_gid, uint32_t cap_k, uint32_t *counters, uint32_t *part_off, cudaStream_t st);
 
 void launch_ranges(const uint32_t *tile_sorted, const uint32_t *counters, uint32_t cap_k, uint2 *ranges,
                    cudaStream_t st);
