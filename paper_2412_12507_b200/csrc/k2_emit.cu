@@ -73,9 +73,12 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ uint32_t s_hist[2][256];
   __shared__ uint32_t s_tmp[16];
+  __shared__ uint2 s_big[GUT_EMIT_PART];  // (Gaussian, first key slot) of the CTA's big Gaussians
+  __shared__ uint32_t s_nbig;
 
   const uint32_t n = *n_vis_p;
   const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) s_nbig = 0;
   const uint32_t base = blockIdx.x * GUT_EMIT_PART;
   if (base >= n) return;
   const uint32_t prefix = __ldg(&part_off[blockIdx.x]);
@@ -116,13 +119,18 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
       pos += code_count(code[j]);
     }
   }
-  // ---- big Gaussians: one warp each, a lane per tile row
+  // ---- big Gaussians: collected per CTA (depth order clusters them in a few
+  // threads), then one warp each, round-robin over the warps, a lane per tile row
 #pragma unroll
-  for (int j = 0; j < GUT_EMIT_ITEMS; ++j) {
-    for (uint32_t bm = __ballot_sync(FULL, big[j]); bm; bm &= bm - 1) {
-      const int src = __ffs(bm) - 1;
-      const uint32_t gg = __shfl_sync(FULL, g[j], src);
-      uint32_t kpos = __shfl_sync(FULL, bpos[j], src);
+  for (int j = 0; j < GUT_EMIT_ITEMS; ++j)
+    if (big[j]) s_big[atomicAdd(&s_nbig, 1u)] = make_uint2(g[j], bpos[j]);
+  __syncthreads();
+  const uint32_t nbig = s_nbig;
+  for (uint32_t bi = (uint32_t)(tid >> 5); bi < nbig; bi += GUT_EMIT_THREADS / 32) {
+    {
+      const uint2 bg = s_big[bi];
+      const uint32_t gg = bg.x;
+      uint32_t kpos = bg.y;
       const float4 a = __ldg(&ell[2 * gg]), b = __ldg(&ell[2 * gg + 1]);
       const uint32_t r0w = __float_as_uint(b.z), r1w = __float_as_uint(b.w);
       const int x0 = (int)(r0w & 0xFFFF), y0 = (int)(r0w >> 16), x1 = (int)(r1w & 0xFFFF), y1 = (int)(r1w >> 16);
