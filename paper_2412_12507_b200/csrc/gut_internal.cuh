@@ -10,8 +10,8 @@
 #define GUT_BLEND_WARPS (GUT_BLEND_THREADS / (32 * GUT_BLEND_NP))  // K5 work units per tile (8x8 pixel blocks)
 #define GUT_BLEND_CTAS 2  // K5 resident CTAs per SM (register budget 65536 / (256 x 2) = 128)
 #define GUT_PAYLOAD_F4 5  // K1 -> K5 blend payload per Gaussian, in float4 (k1_project.cu finish_gaussian)
-#define GUT_SORT_THREADS 256
-#define GUT_SORT_ITEMS 16
+#define GUT_SORT_THREADS 512
+#define GUT_SORT_ITEMS 8
 #define GUT_SORT_PART (GUT_SORT_THREADS * GUT_SORT_ITEMS)  // 4096 keys per onesweep partition
 #define GUT_EMIT_THREADS 256
 #define GUT_EMIT_ITEMS 4

@@ -25,32 +25,30 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-// exclusive block scan of one value per thread (256 threads); returns exclusive, *total
-__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t *s_tmp, uint32_t *total) {
+// exclusive scans over the 256 digits of two values at once: threads 0..255
+// (warps 0-7) hold digit values, every thread of the CTA calls (barriers)
+__device__ __forceinline__ void digit_scan2(uint32_t a, uint32_t b, uint32_t *s_tmp, uint32_t &ea, uint32_t &eb,
+                                            uint32_t &tb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t x = v;
+  uint32_t x = a, y = b;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+    const uint32_t px = __shfl_up_sync(0xffffffffu, x, o), py = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) { x += px; y += py; }
   }
-  if (lane == 31) s_tmp[w] = x;
+  if (lane == 31 && w < 8) { s_tmp[w] = x; s_tmp[8 + w] = y; }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    uint32_t t = threadIdx.x < 8 ? s_tmp[threadIdx.x] : 0;
+  uint32_t wa = 0, wb = 0;
+  tb = 0;
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
-    }
-    if (threadIdx.x < 8) s_tmp[8 + threadIdx.x] = t;  // inclusive warp prefix
+  for (int ww = 0; ww < 8; ++ww) {
+    const uint32_t va = s_tmp[ww], vb = s_tmp[8 + ww];
+    if (ww < w) { wa += va; wb += vb; }
+    tb += vb;
   }
+  ea = wa + x - a;
+  eb = wb + y - b;
   __syncthreads();
-  uint32_t wpre = w > 0 ? s_tmp[8 + w - 1] : 0;
-  if (total) *total = s_tmp[15];
-  uint32_t r = wpre + x - v;
-  __syncthreads();
-  return r;
 }
 
 template <bool FIRST>
@@ -59,9 +57,10 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     uint32_t *__restrict__ vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
     const uint32_t *__restrict__ hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch) {
   constexpr int W = GUT_SORT_THREADS / 32;
+  static_assert(GUT_SORT_THREADS >= 256, "one thread per digit");
   __shared__ uint32_t s_keys[GUT_SORT_PART];
   __shared__ uint32_t s_vals[GUT_SORT_PART];
-  __shared__ uint32_t s_wcnt[W][256];
+  __shared__ uint16_t s_wcnt[W][256];  // per-warp digit counts, then exclusive over warps (< 4096)
   __shared__ uint32_t s_goff[256];
   __shared__ uint32_t s_loff[256];
   __shared__ uint32_t s_tmp[16];
@@ -78,7 +77,7 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt = lanemask_lt();
   uint32_t key[GUT_SORT_ITEMS], val[GUT_SORT_ITEMS], rank[GUT_SORT_ITEMS];
-  // warp w owns the contiguous sub-range [base + w*512, base + (w+1)*512)
+  // warp w owns the contiguous sub-range [base + w*32*ITEMS, base + (w+1)*32*ITEMS)
 #pragma unroll
   for (int j = 0; j < GUT_SORT_ITEMS; ++j) {
     uint32_t idx = base + w * (32 * GUT_SORT_ITEMS) + j * 32 + lane;
@@ -87,8 +86,7 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     if (FIRST) val[j] = idx;
     else val[j] = in ? __ldg(&vals_in[idx]) : 0u;
     if (!FIRST && !in) key[j] = 0xFFFFFFFFu;
-    // validity travels in rank's top bit until ranking
-    rank[j] = (in && (!FIRST || key[j] != GUT_CULLED_KEY)) ? 1u : 0u;
+    rank[j] = (in && (!FIRST || key[j] != GUT_CULLED_KEY)) ? 1u : 0u;  // validity until ranked
   }
   // stable per-warp ranking, rounds in sequence order
 #pragma unroll
@@ -99,29 +97,31 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     const uint32_t before = __popc(peers & lt);
     uint32_t prev = valid ? s_wcnt[w][d] : 0u;
     __syncwarp();
-    if (valid && before == 0) s_wcnt[w][d] = prev + __popc(peers);
+    if (valid && before == 0) s_wcnt[w][d] = (uint16_t)(prev + __popc(peers));
     __syncwarp();
     rank[j] = valid ? (prev + before) : 0xFFFFFFFFu;
   }
   __syncthreads();
-  // per-digit: exclusive over warps, partition total
-  const uint32_t dgt = threadIdx.x;  // 256 threads = 256 digits
-  uint32_t tot = 0;
+  // per digit (threads 0..255): exclusive over warps, partition total, look-back
+  uint32_t tot = 0, gpre = 0, hv = 0;
+  if (threadIdx.x < 256) {
+    const uint32_t dgt = threadIdx.x;
 #pragma unroll
-  for (int ww = 0; ww < W; ++ww) {
-    uint32_t c = s_wcnt[ww][dgt];
-    s_wcnt[ww][dgt] = tot;
-    tot += c;
+    for (int ww = 0; ww < W; ++ww) {
+      const uint32_t c = s_wcnt[ww][dgt];
+      s_wcnt[ww][dgt] = (uint16_t)tot;
+      tot += c;
+    }
+    gpre = lookback(status, 256, (int)part, (int)dgt, tot, epoch);
+    hv = __ldg(&hist[dgt]);
   }
-  // publish + decoupled look-back for this digit
-  const uint32_t gpre = lookback(status, 256, (int)part, (int)dgt, tot, epoch);
   // global digit start (exclusive scan of the pass histogram) and local digit start
-  uint32_t hsum;
-  const uint32_t hex = block_excl_scan256(__ldg(&hist[dgt]), s_tmp, &hsum);
-  uint32_t ltotal;
-  const uint32_t lex = block_excl_scan256(tot, s_tmp, &ltotal);
-  s_goff[dgt] = hex + gpre;
-  s_loff[dgt] = lex;
+  uint32_t hex, lex, ltotal;
+  digit_scan2(hv, tot, s_tmp, hex, lex, ltotal);
+  if (threadIdx.x < 256) {
+    s_goff[threadIdx.x] = hex + gpre;
+    s_loff[threadIdx.x] = lex;
+  }
   __syncthreads();
   // scatter into shared memory in digit order
 #pragma unroll
