@@ -23,6 +23,11 @@ HEADERS = ["gut_internal.cuh", "launch.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
+# tuning experiments only: extra -D flags and an alternative output (see gut.py GUT_LIB)
+FLAGS += os.environ.get("GUT_EXTRA_FLAGS", "").split()
+if os.environ.get("GUT_LIB_OUT"):
+    OUT = os.environ["GUT_LIB_OUT"]
+    OBJ = OUT + ".objs"
 
 
 def _newest_input() -> float:

@@ -132,7 +132,7 @@ static gut_status ensure_tiles(gut_context *ctx, size_t t) {
   size_t dummy = 0;
   CUDA_TRY(ctx, regrow(ctx->ranges, dummy, t));
   CUDA_TRY(ctx, regrow(ctx->tile_work, dummy, t));
-  CUDA_TRY(ctx, regrow(ctx->pix, dummy, t * GUT_BLEND_THREADS));
+  CUDA_TRY(ctx, regrow(ctx->pix, dummy, t * GUT_TILE_PX));
   CUDA_TRY(ctx, regrow(ctx->anchors, dummy, t));
   CUDA_TRY(ctx, regrow(ctx->seg_base, dummy, t));
   CUDA_TRY(ctx, regrow(ctx->unit_ctr, dummy, 3 * t * GUT_BLEND_WARPS));
@@ -145,10 +145,10 @@ static gut_status ensure_tiles(gut_context *ctx, size_t t) {
 static gut_status ensure_items(gut_context *ctx, size_t items) {
   if (items <= ctx->cap_items) return GUT_OK;
   size_t c = items + items / 8 + 64, dummy = 0;
-  CUDA_TRY(ctx, regrow(ctx->bstatus, dummy, c * GUT_BLEND_THREADS));
-  CUDA_TRY(ctx, cudaMemset(ctx->bstatus, 0, c * GUT_BLEND_THREADS * sizeof(unsigned long long)));
-  CUDA_TRY(ctx, regrow(ctx->part_c, dummy, c * GUT_BLEND_THREADS));
-  CUDA_TRY(ctx, regrow(ctx->part_t, dummy, c * GUT_BLEND_THREADS));
+  CUDA_TRY(ctx, regrow(ctx->bstatus, dummy, c * GUT_TILE_PX));
+  CUDA_TRY(ctx, cudaMemset(ctx->bstatus, 0, c * GUT_TILE_PX * sizeof(unsigned long long)));
+  CUDA_TRY(ctx, regrow(ctx->part_c, dummy, c * GUT_TILE_PX));
+  CUDA_TRY(ctx, regrow(ctx->part_t, dummy, c * GUT_TILE_PX));
   CUDA_TRY(ctx, regrow(ctx->q1, dummy, c * GUT_BLEND_WARPS));
   // queue 2: every grant plus one outstanding ticket per resident warp; the
   // consumers re-zero the slots they take (tickets past the last grant find 0)
@@ -528,7 +528,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   // blend look-back epochs live in 22 bits: clear the status words on wrap
   uint32_t bepoch = ++ctx->epoch;
   if ((bepoch & 0x3FFFFFu) == 0) {
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->bstatus, 0, ctx->cap_items * GUT_BLEND_THREADS * sizeof(unsigned long long), st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->bstatus, 0, ctx->cap_items * GUT_TILE_PX * sizeof(unsigned long long), st));
     bepoch = ++ctx->epoch;
   }
   BlendBufs bb;

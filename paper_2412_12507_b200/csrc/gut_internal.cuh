@@ -5,10 +5,15 @@
 #include <stdint.h>
 
 #define GUT_TILE 16
-#define GUT_BLEND_THREADS 256
+#define GUT_TILE_PX (GUT_TILE * GUT_TILE)  // pixels per tile (ray LUT, look-back status, partials)
 #define GUT_BLEND_NP 2  // K5 pixels per lane
-#define GUT_BLEND_WARPS (GUT_BLEND_THREADS / (32 * GUT_BLEND_NP))  // K5 work units per tile (8x8 pixel blocks)
+#define GUT_BLEND_WARPS (GUT_TILE_PX / (32 * GUT_BLEND_NP))  // K5 work units per tile (8x8 pixel blocks)
+#ifndef GUT_BLEND_CTA
+#define GUT_BLEND_CTA 256  // K5 threads per CTA (independent warps; sized for the register budget)
+#endif
+#ifndef GUT_BLEND_CTAS
 #define GUT_BLEND_CTAS 2  // K5 resident CTAs per SM (register budget 65536 / (256 x 2) = 128)
+#endif
 #define GUT_PAYLOAD_F4 5  // K1 -> K5 blend payload per Gaussian, in float4 (k1_project.cu finish_gaussian)
 #define GUT_SORT_THREADS 512
 #define GUT_SORT_ITEMS 8

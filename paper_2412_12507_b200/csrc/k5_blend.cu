@@ -132,7 +132,7 @@ __device__ __forceinline__ void tile_pixel(int tile, int tiles_x, int w, int lan
 // shutter, beta = t_pixel - t_anchor.  MODE 0/1: camera frame (depends on the
 // intrinsics only, cached by the host); MODE 2: world frame (per view).
 template <int MODE>
-__global__ __launch_bounds__(GUT_BLEND_THREADS) void rays_kernel(DevCam c, float4 *__restrict__ pix,
+__global__ __launch_bounds__(GUT_TILE_PX) void rays_kernel(DevCam c, float4 *__restrict__ pix,
                                                                  TileAnchor *__restrict__ anchors) {
   __shared__ double s_red[8][4];
   __shared__ double s_a[13];
@@ -204,14 +204,14 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS) void rays_kernel(DevCam c, float
       }
     }
   }
-  pix[(size_t)tile * GUT_BLEND_THREADS + threadIdx.x] = out;
+  pix[(size_t)tile * GUT_TILE_PX + threadIdx.x] = out;
 }
 
 void launch_rays(const DevCam &cam, float4 *pix, TileAnchor *anchors, cudaStream_t st) {
   const unsigned blocks = (unsigned)cam.n_tiles;
-  if (cam.model == CAM_ORTHO) rays_kernel<1><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, pix, anchors);
-  else if (cam.shutter != SH_GLOBAL) rays_kernel<2><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, pix, anchors);
-  else rays_kernel<0><<<blocks, GUT_BLEND_THREADS, 0, st>>>(cam, pix, anchors);
+  if (cam.model == CAM_ORTHO) rays_kernel<1><<<blocks, GUT_TILE_PX, 0, st>>>(cam, pix, anchors);
+  else if (cam.shutter != SH_GLOBAL) rays_kernel<2><<<blocks, GUT_TILE_PX, 0, st>>>(cam, pix, anchors);
+  else rays_kernel<0><<<blocks, GUT_TILE_PX, 0, st>>>(cam, pix, anchors);
 }
 
 // ---------------------------------------------------------------- plan
@@ -376,7 +376,7 @@ __device__ __forceinline__ unsigned long long pred_L(const unsigned long long *s
   unsigned long long L = 0;
   const int jmax = min(s, 4);
   for (int j = 1; j <= jmax; ++j) {
-    const unsigned long long wv = ld_relaxed(stat - (size_t)j * GUT_BLEND_THREADS);
+    const unsigned long long wv = ld_relaxed(stat - (size_t)j * GUT_TILE_PX);
     const uint32_t flag = (uint32_t)(wv >> 62);
     if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (epoch & 0x3FFFFFu)) continue;
     L += wv & ((1ull << 40) - 1);
@@ -457,7 +457,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   // [per-warp entry table: 8 warps x 32 x NF]
   extern __shared__ float4 s_dyn[];
   constexpr int PF = GUT_PAYLOAD_F4;
-  constexpr int RAW = (GUT_BLEND_THREADS / 32) * 2 * 32 * PF;
+  constexpr int RAW = (GUT_BLEND_CTA / 32) * 2 * 32 * PF;
   float4 *__restrict__ wt = s_dyn + RAW + (threadIdx.x >> 5) * 32 * NF;
   const uint32_t wt_s = (uint32_t)__cvta_generic_to_shared(wt);
   const int lane = threadIdx.x & 31;
@@ -813,8 +813,8 @@ __device__ bool fetch_work(const BlendBufs &B, int &unit, int &s) {
 // warp completing the unit's last granted segment, the in-order combine.  No
 // CTA-wide barriers: a warp whose pixels finish early moves on.
 template <int MODE>
-__global__ __launch_bounds__(GUT_BLEND_THREADS, GUT_BLEND_CTAS) void blend_kernel(DevCam c, BlendBufs B) {
-  constexpr int NT = GUT_BLEND_THREADS, NP = GUT_BLEND_NP;
+__global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(DevCam c, BlendBufs B) {
+  constexpr int NT = GUT_TILE_PX, NP = GUT_BLEND_NP;
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   uint32_t n_eval_acc = 0, n_contrib_acc = 0, n_term_acc = 0;
@@ -1117,18 +1117,18 @@ __global__ __launch_bounds__(GUT_BLEND_THREADS, GUT_BLEND_CTAS) void blend_kerne
 
 template <int MODE>
 static void blend_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
-  constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_THREADS / 32) * 2 * 32 * GUT_PAYLOAD_F4 +
-                                            (GUT_BLEND_THREADS / 32) * 32 * WarpTbl<MODE>::NF);
+  constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_CTA / 32) * 2 * 32 * GUT_PAYLOAD_F4 +
+                                            (GUT_BLEND_CTA / 32) * 32 * WarpTbl<MODE>::NF);
   static int grid = 0;  // per template instance: persistent CTAs = SMs x resident CTAs per SM
   if (!grid) {
     cudaFuncSetAttribute(blend_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, blend_kernel<MODE>, GUT_BLEND_THREADS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, blend_kernel<MODE>, GUT_BLEND_CTA, smem);
     grid = max(1, sms) * max(1, per);
   }
-  blend_kernel<MODE><<<grid, GUT_BLEND_THREADS, smem, st>>>(cam, b);
+  blend_kernel<MODE><<<grid, GUT_BLEND_CTA, smem, st>>>(cam, b);
 }
 
 void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {

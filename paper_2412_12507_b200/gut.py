@@ -12,7 +12,7 @@ import os
 from typing import Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgut.so")
+LIB_PATH = os.environ.get("GUT_LIB") or os.path.join(_HERE, "libgut.so")  # GUT_LIB: tuning experiments only
 
 GUT_OK = 0
 STATUS = {0: "GUT_OK", 1: "GUT_E_INVALID_ARGUMENT", 2: "GUT_E_UNSUPPORTED", 3: "GUT_E_OUT_OF_MEMORY",
