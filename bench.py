@@ -105,9 +105,9 @@ def algorithmic_work(n, nv, k, tiles, pixels, pe, pc, sh_chunks=12):
     """Algorithmic bytes / FLOPs per launch of each kernel.
     n: Gaussians, nv: visible, k: keys, pe/pc: evaluated / contributing pairs."""
     return {
-        "K1_project": ("hbm", 48 * n + 8 * n + nv * (16 * sh_chunks + 32 + 64)),
+        "K1_project": ("hbm", 48 * n + 8 * n + nv * (16 * sh_chunks + 32 + 80)),
         "K3_sort_depth": ("hbm", 4 * n + 8 * nv + 3 * 16 * nv - 4 * nv),
-        "K2_emit": ("hbm", 4 * nv + 4 * nv + 32 * nv + 8 * k),
+        "K2_emit": ("hbm", 4 * nv + 4 * nv + 8 * k),  # depth order + tile code per visible, (tile, gid) per key
         "K3_sort_tile": ("hbm", (32 if tiles > 256 else 16) * k),
         "K4_ranges": ("hbm", 4 * k + 8 * tiles),
         # FP32 work of Eq. 11 in the anchored form: 36 FLOP to the reject test per
