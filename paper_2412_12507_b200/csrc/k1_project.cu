@@ -17,6 +17,29 @@
 
 namespace gut {
 
+// atan2(y, x) for y >= 0: octant reduction + odd minimax polynomial for atan
+// on [0, 1] (fitted here; max abs error 9e-8 in fp32, ~ CUDA's atan2f, at a
+// third of its instructions).  Only the fisheye projection (theta) uses it.
+__device__ __forceinline__ float atan2_pos(float y, float x) {
+  const float ax = fabsf(x);
+  const float mx = fmaxf(y, ax), mn = fminf(y, ax);
+  const float a = mx > 0.f ? mn * __frcp_rn(mx) : 0.f;
+  const float u = a * a;
+  float p = 0.0024561970494687557f;
+  p = fmaf(p, u, -0.014399108476936817f);
+  p = fmaf(p, u, 0.039777275174856186f);
+  p = fmaf(p, u, -0.07234489917755127f);
+  p = fmaf(p, u, 0.10498751699924469f);
+  p = fmaf(p, u, -0.141611710190773f);
+  p = fmaf(p, u, 0.19985897839069366f);
+  p = fmaf(p, u, -0.33332595229148865f);
+  p = fmaf(p, u, 0.9999998807907104f);
+  float t = p * a;
+  if (y > ax) t = 1.5707963267948966f - t;
+  if (x < 0.f) t = 3.141592653589793f - t;
+  return t;
+}
+
 __device__ __forceinline__ bool project_cam_f(const DevCam &c, f3 x, float &du, float &dv) {
   // returns pixel offsets from the principal point (du, dv); validity first
   switch (c.model) {
@@ -46,15 +69,16 @@ __device__ __forceinline__ bool project_cam_f(const DevCam &c, f3 x, float &du, 
       return true;
     }
     case CAM_FISHEYE: {
-      float nrm = sqrtf(x.x * x.x + x.y * x.y + x.z * x.z);
-      if (!(nrm > c.near_plane)) return false;
-      float rho = sqrtf(x.x * x.x + x.y * x.y);
-      float th = atan2f(rho, x.z);
+      const float rho2 = x.x * x.x + x.y * x.y;
+      // |x| > near, squared (near * |near| keeps a negative near always true)
+      if (!(rho2 + x.z * x.z > c.near_plane * fabsf(c.near_plane))) return false;
+      const float rho = sqrtf(rho2);
+      const float th = atan2_pos(rho, x.z);
       if (!(th <= c.fovf)) return false;
       if (rho == 0.f) { du = 0.f; dv = 0.f; return true; }
       float t2 = th * th;
       float td = th * (1.f + t2 * (c.kf[0] + t2 * (c.kf[1] + t2 * (c.kf[2] + t2 * c.kf[3]))));
-      float s = td / rho;
+      float s = td * __frcp_rn(rho);
       du = c.fxf * (s * x.x);
       dv = c.fyf * (s * x.y);
       return true;
@@ -194,18 +218,14 @@ __device__ bool project_sigma_d(const DevCam &c, d3 y, d3 w, double &du, double 
 }
 
 // 3DGS real SH basis up to degree DEG (reading R19), colour = max(sum + 0.5, 0)
-// (coefficients: float4 chunk c at base[c * stride]; global SoA or the
-// kernel's shared-memory prefetch)
-template <int DEG> struct ShChunks { static constexpr int NC = (DEG + 1) * (DEG + 1), CH = (3 * NC + 3) / 4; };
-
 template <int DEG>
-__device__ __forceinline__ f3 sh_colour(const float4 *base, int64_t stride, f3 d) {
-  constexpr int NC = ShChunks<DEG>::NC;
-  constexpr int CH = ShChunks<DEG>::CH;
+__device__ __forceinline__ f3 sh_colour(const float4 *sh, int64_t n, int64_t i, f3 d) {
+  constexpr int NC = (DEG + 1) * (DEG + 1);
+  constexpr int CH = (3 * NC + 3) / 4;
   float f[CH * 4];
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
-    float4 v = base[(int64_t)c * stride];
+    float4 v = __ldg(&sh[(int64_t)c * n + i]);
     f[4 * c] = v.x; f[4 * c + 1] = v.y; f[4 * c + 2] = v.z; f[4 * c + 3] = v.w;
   }
   float Y[16];
@@ -236,8 +256,7 @@ template <int DEG>
 __device__ __forceinline__ uint32_t finish_gaussian(const DevCam &c, const SceneDev &s, int64_t i, float4 po,
                                                     float4 sc, const float *R, d3 y0d, double t0, float4 e0,
                                                     float4 e1, float4 *__restrict__ ell,
-                                                    float4 *__restrict__ payload, const float4 *sh_base,
-                                                    int64_t sh_stride) {
+                                                    float4 *__restrict__ payload) {
   // depth key (reading R13): camera-frame distance of mu at its own time t0
   const d3 dcw = mkd(c.dc[0], c.dc[1], c.dc[2]);
   const d3 yc = y0d - t0 * mtv(c.R0, dcw);
@@ -245,7 +264,7 @@ __device__ __forceinline__ uint32_t finish_gaussian(const DevCam &c, const Scene
   // colour (reading R18): SH at d = normalize(mu - c(t0))
   const d3 dw = mkd(po.x, po.y, po.z) - (mkd(c.c0[0], c.c0[1], c.c0[2]) + t0 * dcw);
   const double nd = sqrt(dot(dw, dw));
-  const f3 rgb = sh_colour<DEG>(sh_base, sh_stride, tof((1.0 / nd) * dw));
+  const f3 rgb = sh_colour<DEG>(s.sh, s.n, i, tof((1.0 / nd) * dw));
   ell[2 * i] = e0;
   ell[2 * i + 1] = e1;
   // blend payload (80 B): w0 = c(0) - mu in fp64 (K5 forms the cancelling
@@ -328,7 +347,6 @@ __global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, u
   __shared__ uint32_t s_hist[4][256];
   __shared__ unsigned long long s_k[8];
   __shared__ uint32_t s_nv[8];
-  extern __shared__ float4 s_sh[];  // SH prefetch: chunk c of thread t at s_sh[c * 256 + t]
   for (int j = threadIdx.x; j < 1024; j += 256) (&s_hist[0][0])[j] = 0;
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
@@ -340,24 +358,9 @@ __global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, u
     bool wide = false;
     float du[7], dv[7], tt[7];
     d3 y0d = mkd(0, 0, 0);
-    bool pref = false;
     if (ok) {
       // camera-frame centre in fp64, sigma offsets gamma s_j R[:,j] rotated in fp32 (Eq. 6)
       y0d = mtv(c.R0, mkd(po.x, po.y, po.z) - mkd(c.c0[0], c.c0[1], c.c0[2]));
-      // likely visible (centre in front / inside the field of view + 20 deg):
-      // start the SH loads now so they overlap the UT (a miss just loads later)
-      const double r2 = dot(y0d, y0d);
-      pref = c.model == CAM_FISHEYE ? (r2 > 0.0 && y0d.z > cos(fmin(c.fov + 0.35, 3.14159)) * sqrt(r2))
-                                    : y0d.z > 0.0;
-      if (pref) {
-#pragma unroll
-        for (int q = 0; q < ShChunks<DEG>::CH; ++q) {
-          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&s_sh[q * 256 + threadIdx.x]);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(&s.sh[(int64_t)q * s.n + i])
-                       : "memory");
-        }
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
       const f3 y0 = tof(y0d);
       const f3 wv = mtv(c.R0f, mk(c.dcf[0], c.dcf[1], c.dcf[2]));
       const float sj[3] = {sc.x, sc.y, sc.z};
@@ -419,13 +422,12 @@ __global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, u
         ok = my_code != 0;
       }
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");  // (own chunks only: no barrier needed)
     if (ok) {
       key = finish_gaussian<DEG>(c, s, i, po, sc, R, y0d, (double)tt[0],
                                  make_float4(e.vx, e.vy, e.cxx, e.cxy),
                                  make_float4(e.cyy, e.k2, __uint_as_float(pack_rect(e.x0, e.y0)),
                                              __uint_as_float(pack_rect(e.x1, e.y1))),
-                                 ell, payload, pref ? s_sh + threadIdx.x : s.sh + i, pref ? 256 : s.n);
+                                 ell, payload);
     } else {
       my_code = 0;
       key = GUT_CULLED_KEY;
@@ -509,7 +511,7 @@ __global__ __launch_bounds__(256) void project_wide_kernel(DevCam c, SceneDev s,
                                    make_float4((float)e.vx, (float)e.vy, (float)e.cxx, (float)e.cxy),
                                    make_float4((float)e.cyy, -(float)e.k2, __uint_as_float(pack_rect(e.x0, e.y0)),
                                                __uint_as_float(pack_rect(e.x1, e.y1))),
-                                   ell, payload, s.sh + i, s.n);
+                                   ell, payload);
       } else {
         my_code = 0;
         key = GUT_CULLED_KEY;
@@ -551,29 +553,21 @@ void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32
   if (s.n == 0) return;
   const unsigned blocks = (unsigned)((s.n + 255) / 256);
   const unsigned wblocks = 32;  // grid-stride over the (few) deferred Gaussians
-  static bool configured = false;
-  if (!configured) {  // SH prefetch buffers (48 KB at degree 3) exceed the static shared-memory limit
-    cudaFuncSetAttribute(project_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 16 * ShChunks<0>::CH);
-    cudaFuncSetAttribute(project_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 16 * ShChunks<1>::CH);
-    cudaFuncSetAttribute(project_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 16 * ShChunks<2>::CH);
-    cudaFuncSetAttribute(project_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 16 * ShChunks<3>::CH);
-    configured = true;
-  }
   switch (s.sh_degree) {
     case 0:
-      project_kernel<0><<<blocks, 256, 256 * 16 * ShChunks<0>::CH, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      project_kernel<0><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
       project_wide_kernel<0><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
       break;
     case 1:
-      project_kernel<1><<<blocks, 256, 256 * 16 * ShChunks<1>::CH, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      project_kernel<1><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
       project_wide_kernel<1><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
       break;
     case 2:
-      project_kernel<2><<<blocks, 256, 256 * 16 * ShChunks<2>::CH, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      project_kernel<2><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
       project_wide_kernel<2><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
       break;
     default:
-      project_kernel<3><<<blocks, 256, 256 * 16 * ShChunks<3>::CH, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      project_kernel<3><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
       project_wide_kernel<3><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
       break;
   }
