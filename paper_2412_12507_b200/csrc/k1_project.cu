@@ -340,7 +340,10 @@ __device__ __forceinline__ void k1_block_totals(uint32_t my_tiles, uint32_t key,
 
 // ---- K1 main (fp32): one thread per Gaussian
 template <int DEG>
-__global__ __launch_bounds__(256, 3) void project_kernel(DevCam c, SceneDev s, uint32_t *__restrict__ dkey,
+#ifndef GUT_K1_CTAS
+#define GUT_K1_CTAS 4  // 64 registers: 32 warps per SM (measured best)
+#endif
+__global__ __launch_bounds__(256, GUT_K1_CTAS) void project_kernel(DevCam c, SceneDev s, uint32_t *__restrict__ dkey,
                                                          uint32_t *__restrict__ tiles, float4 *__restrict__ ell,
                                                          float4 *__restrict__ payload, uint32_t *counters,
                                                          uint32_t *__restrict__ deferred) {
