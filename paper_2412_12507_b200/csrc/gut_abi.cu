@@ -487,19 +487,19 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   const uint32_t *kdev = cnt + CNT_K;  // low word of the u64 key count (K < 2^30)
   const uint32_t nk = (uint32_t)n_keys_host;
   const uint32_t *fk, *fv;
+  // (K4 ranges fused into the final tile pass)
+  launch_ranges_init(ctx->ranges, dc.n_tiles, st);
+  const bool two = dc.n_tiles > 256;
   launch_sort_pass(ctx->ka, ctx->va, ctx->kb, ctx->vb, kdev, nk, 0, ht, ctx->st_tile, cnt + CNT_TICKETS + 5,
-                   ++ctx->epoch, false, st);
+                   ++ctx->epoch, false, st, two ? nullptr : ctx->ranges);
   fk = ctx->kb; fv = ctx->vb;
-  if (dc.n_tiles > 256) {
+  if (two) {
     launch_sort_pass(ctx->kb, ctx->vb, ctx->ka, ctx->va, kdev, nk, 8, ht + 256, ctx->st_tile,
-                     cnt + CNT_TICKETS + 6, ++ctx->epoch, false, st);
+                     cnt + CNT_TICKETS + 6, ++ctx->epoch, false, st, ctx->ranges);
     fk = ctx->ka; fv = ctx->va;
   }
   if (timing) cudaEventRecord(ev[4], st);
-  // K4 ranges, K5 blend
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->ranges, 0, (size_t)dc.n_tiles * sizeof(uint2), st));
-  launch_ranges(fk, cnt, (uint32_t)ctx->cap_k, ctx->ranges, st);
-  if (timing) cudaEventRecord(ev[5], st);
+  if (timing) cudaEventRecord(ev[5], st);  // K4: fused (stage time ~0)
   float *rgb = out->rgb, *alpha = out->alpha, *depth = out->depth;
   if (!out->on_device) {
     rgb = ctx->img;
@@ -689,6 +689,9 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
     delete[] t; delete[] g;
   } else if (stage == GUT_STAGE_RANGES) {
     CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->ranges, need, cudaMemcpyDeviceToHost));
+    uint32_t *r = (uint32_t *)host_dst;  // empty tiles: (UINT_MAX, 0) on the device -> (0, 0)
+    for (size_t t = 0; t < need / 8; ++t)
+      if (r[2 * t + 1] <= r[2 * t]) r[2 * t] = r[2 * t + 1] = 0;
   } else if (stage == GUT_STAGE_BLEND_TRACE) {
     CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->trace, need, cudaMemcpyDeviceToHost));
   } else {

@@ -1,20 +1,16 @@
-// k2_emit.cu — K2 (scan + key emission, the paper's "Duplicate") and K4
-// (tile ranges), sm_100a.
+// k2_emit.cu — K2 (scan + key emission, the paper's "Duplicate"), sm_100a.
+// (K4, the tile ranges, is fused into the final tile pass: k3_sort.cu.)
 //
 // K2 walks the visible Gaussians in depth order (output of the depth passes
-// of K3).  A CTA owns 1024 consecutive Gaussians: it scans their tile counts,
-// gets its global key offset by decoupled look-back, then emits its keys with
-// one OUTPUT slot per thread (slot -> Gaussian by binary search in the local
-// scan, -> tile by walking the Gaussian's tile-row spans), so the writes of
-// (tile id, Gaussian id) are coalesced and large Gaussians do not serialise a
-// thread.  Row spans come from row_span(), the same function K1 counted with,
-// so counts and emitted keys agree bit for bit.  Because emission follows
-// depth order and the tile passes are stable, equal-tile keys stay ordered by
-// (depth, index) — the tie rule of PAPER L208 / DESIGN.md R13.
+// of K3) in partitions of 1024: per-partition key totals and their scan give
+// every partition its first key slot; the emission then reads one 4-byte tile
+// code per Gaussian (K1, gut_internal.cuh ell_tile_code): small Gaussians
+// (tile rectangle <= 3x3) emit straight from the hit mask, big ones are
+// expanded row by row by a warp with row_span(), the function K1 counted
+// with, so counts and emitted keys agree bit for bit.  Because emission
+// follows depth order and the tile passes are stable, equal-tile keys stay
+// ordered by (depth, index) — the tie rule of PAPER L208 / DESIGN.md R13.
 // K2 also builds the two 8-bit digit histograms of the tile ids.
-//
-// K4 marks [start, end) of every tile in the sorted key array (Alg. 1's
-// tiles, "same tiling ... as 3DGS").
 #include "launch.h"
 
 namespace gut {
@@ -246,17 +242,6 @@ __global__ __launch_bounds__(1024) void emit_scan_kernel(const uint32_t *n_vis_p
   }
 }
 
-__global__ void ranges_kernel(const uint32_t *__restrict__ tile_sorted, const uint32_t *counters, uint32_t cap_k,
-                              uint2 *__restrict__ ranges) {
-  const unsigned long long Kfull = *reinterpret_cast<const unsigned long long *>(&counters[CNT_K]);
-  const uint32_t K = (uint32_t)min(Kfull, (unsigned long long)cap_k);
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
-    uint32_t t = tile_sorted[k];
-    if (k == 0 || tile_sorted[k - 1] != t) ranges[t].x = k;
-    if (k == K - 1 || tile_sorted[k + 1] != t) ranges[t].y = k + 1;
-  }
-}
-
 void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper, const uint32_t *tiles,
                  const float4 *ell, const double2 *ell64, int tiles_x, int tile_cull, uint32_t *out_tile,
                  uint32_t *out_gid, uint32_t cap_k, uint32_t *counters, uint32_t *part_off, cudaStream_t st) {
@@ -266,11 +251,6 @@ void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper,
   emit_scan_kernel<<<1, 1024, 0, st>>>(n_vis, part_off);
   emit_kernel<<<blocks, GUT_EMIT_THREADS, 0, st>>>(order, n_vis, tiles, ell, ell64, tiles_x, tile_cull, out_tile, out_gid,
                                                    cap_k, counters, part_off);
-}
-
-void launch_ranges(const uint32_t *tile_sorted, const uint32_t *counters, uint32_t cap_k, uint2 *ranges,
-                   cudaStream_t st) {
-  ranges_kernel<<<148 * 8, 256, 0, st>>>(tile_sorted, counters, cap_k, ranges);
 }
 
 }  // namespace gut

@@ -58,7 +58,8 @@ template <bool FIRST>
 __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, uint32_t *__restrict__ keys_out,
     uint32_t *__restrict__ vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
-    const uint32_t *__restrict__ hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch) {
+    const uint32_t *__restrict__ hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch,
+    uint2 *__restrict__ ranges) {
   constexpr int W = GUT_SORT_THREADS / 32;
   static_assert(GUT_SORT_THREADS >= 256, "one thread per digit");
   __shared__ uint32_t s_keys[GUT_SORT_PART];
@@ -155,21 +156,38 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     const uint32_t o = s_goff[d] + (p - s_loff[d]);
     if (keys_out) keys_out[o] = k;
     vals_out[o] = s_vals[p];
+    if (ranges) {
+      // K4 fused into the final tile pass: a tile's keys are contiguous in this
+      // CTA's run (the input is ordered by the lower digits) and in the output,
+      // so the min / max over CTAs of their first / last positions is its range
+      if (p == 0 || s_keys[p - 1] != k) atomicMin(&ranges[k].x, o);
+      if (p + 1 == ltotal || s_keys[p + 1] != k) atomicMax(&ranges[k].y, o + 1);
+    }
   }
+}
+
+// empty ranges (start UINT_MAX, end 0) before the final tile pass fills them
+__global__ void ranges_init_kernel(uint2 *__restrict__ ranges, int n_tiles) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n_tiles) ranges[t] = make_uint2(0xFFFFFFFFu, 0u);
+}
+
+void launch_ranges_init(uint2 *ranges, int n_tiles, cudaStream_t st) {
+  ranges_init_kernel<<<(n_tiles + 255) / 256, 256, 0, st>>>(ranges, n_tiles);
 }
 
 void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                       uint32_t *vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
                       const uint32_t *hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch,
-                      bool first, cudaStream_t st) {
+                      bool first, cudaStream_t st, uint2 *ranges) {
   if (n_host == 0) return;
   unsigned blocks = (n_host + GUT_SORT_PART - 1) / GUT_SORT_PART;
   if (first)
     onesweep_kernel<true><<<blocks, GUT_SORT_THREADS, 0, st>>>(keys_in, vals_in, keys_out, vals_out, n_dev,
-                                                               n_host, shift, hist, status, ticket, epoch);
+                                                               n_host, shift, hist, status, ticket, epoch, ranges);
   else
     onesweep_kernel<false><<<blocks, GUT_SORT_THREADS, 0, st>>>(keys_in, vals_in, keys_out, vals_out, n_dev,
-                                                                n_host, shift, hist, status, ticket, epoch);
+                                                                n_host, shift, hist, status, ticket, epoch, ranges);
 }
 
 }  // namespace gut

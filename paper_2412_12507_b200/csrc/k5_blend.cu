@@ -829,8 +829,8 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     unsigned long long t_begin = 0;
     if (B.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
 
-    const uint2 rg = B.ranges[tile];
-    const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x, len = end - start;
+    const uint2 rg = B.ranges[tile];  // empty tile: (UINT_MAX, 0)
+    const uint32_t start = rg.y > rg.x ? rg.x : 0u, end = rg.y > rg.x ? rg.y : 0u, len = end - start;
     const int S = len == 0 ? 1 : (int)((len + B.seg - 1) / B.seg);
     const uint32_t s0 = start + (uint32_t)s * B.seg, s1 = min(s0 + (uint32_t)B.seg, end);
     const uint32_t slot = B.seg_base[tile] + (uint32_t)s;

@@ -52,7 +52,9 @@ void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32
 void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                       uint32_t *vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
                       const uint32_t *hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch,
-                      bool first, cudaStream_t st);
+                      bool first, cudaStream_t st, uint2 *ranges = nullptr);
+// K4 fused into the final tile pass (ranges != nullptr there): ranges start empty
+void launch_ranges_init(uint2 *ranges, int n_tiles, cudaStream_t st);
 
 // K2: per-partition key totals, their scan, then the emission (part_off:
 // one uint32 per GUT_EMIT_PART Gaussians of the upper bound n_upper)
@@ -60,8 +62,7 @@ void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper,
                  const float4 *ell, const double2 *ell64, int tiles_x, int tile_cull, uint32_t *out_tile,
                  uint32_t *out_gid, uint32_t cap_k, uint32_t *counters, uint32_t *part_off, cudaStream_t st);
 
-void launch_ranges(const uint32_t *tile_sorted, const uint32_t *counters, uint32_t cap_k, uint2 *ranges,
-                   cudaStream_t st);
+
 
 // Per-tile ray anchor (fp64).  Global shutter: camera frame, a function of the
 // intrinsics only (cached).  Rolling shutter: world frame, per view.
