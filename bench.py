@@ -137,6 +137,26 @@ def roofline(stage_ms, work, peaks, clocks):
     return out
 
 
+# ncu kernel names of the stages (profiles/<tag>_traffic.json, tools/profile_round.sh)
+NCU_NAMES = {"K5_blend": "blend_kernel<0>", "K1_project": "project_kernel<3>"}
+
+
+def load_traffic(stage):
+    """dram read + write bytes per launch of the stage's kernel from the newest
+    committed `ncu --set full` capture (profiles/*_traffic.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), key=os.path.getmtime)
+    for f in reversed(files):
+        try:
+            d = json.load(open(f))
+            v = d["bytes_per_launch"].get(NCU_NAMES.get(stage, ""))
+            if v:
+                return float(v), os.path.relpath(f, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = {"hbm_gbs": 6650.0, "hbm_source": "fallback (B200_PROFILING.md)"}
@@ -335,6 +355,7 @@ def run_ours(args):
     rl = roofline(stage_ms, work, peaks, clk)
     dom = max(rl, key=lambda k: rl[k]["ms"])
     d = rl[dom]
+    traffic, traffic_src = load_traffic(dom)
     launches_per_render = 2 + 4 + 3 + (2 if n_tiles > 256 else 1) + 1 + 4  # K1+wide, 4 depth, emit (count, scan, emit), tile passes, ranges, plan (3) + blend
     total_views = world * args.steps
     fps = total_views / (ms_max * 1e-3)
@@ -355,7 +376,7 @@ def run_ours(args):
                         "contexts on two streams alternate frames (copy of frame i overlaps render of i+1)"},
         "gpu_launches": launches_per_render * args.steps,
         "roofline": {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
-                     "unit": d["unit"], "frac": d["frac"], "traffic": None,
+                     "unit": d["unit"], "frac": d["frac"], "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": peaks["hbm_source"] if d["bound"] == "hbm" else peaks["fp32_source"]},
         "roofline_all": rl,
         "workload_stats": {"n": N, "n_visible_mean": mean_nv, "keys_mean": mean_k, "kappa": mean_k / max(mean_nv, 1),

@@ -1,8 +1,12 @@
 """Summarise ncu artefacts (launch list CSV + `--set full` report) into a
 markdown table for profiles/.  Runs here (no GPU): ncu -i reads the report.
 
-    python tools/ncu_summary.py gpurun_out/launches.csv gpurun_out/full.ncu-rep > profiles/rN_summary.md
+    python tools/ncu_summary.py gpurun_out/launches.csv gpurun_out/full.ncu-rep [traffic.json] > profiles/rN_summary.md
+
+traffic.json (optional): per kernel, dram__bytes_read.sum + dram__bytes_write.sum
+of its launch in the `--set full` capture (bench.py's roofline "traffic").
 """
+import json
 import collections
 import csv
 import io
@@ -67,6 +71,7 @@ def full(path):
 
 def main():
     lc, fr = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None
+    tj = sys.argv[3] if len(sys.argv) > 3 else None
     tot, cnt = launches(lc)
     total = sum(tot.values())
     print("## Launch list (ncu `gpu__time_duration.sum`, cold-cache, serialised)\n")
@@ -95,6 +100,12 @@ def main():
                 else:
                     vals.append(f"{v:.1f}")
             print(f"| {d['kernel']} | " + " | ".join(vals) + " |")
+        if tj:
+            traffic = {}
+            for d in full(fr):
+                if d.get("dram_read") is not None and d.get("dram_write") is not None:
+                    traffic.setdefault(d["kernel"], d["dram_read"] + d["dram_write"])
+            json.dump({"source": f"ncu --set full ({fr})", "bytes_per_launch": traffic}, open(tj, "w"), indent=1)
 
 
 if __name__ == "__main__":
