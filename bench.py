@@ -356,7 +356,7 @@ def run_ours(args):
     dom = max(rl, key=lambda k: rl[k]["ms"])
     d = rl[dom]
     traffic, traffic_src = load_traffic(dom)
-    launches_per_render = 2 + 4 + 3 + (2 if n_tiles > 256 else 1) + 1 + 4  # K1+wide, 4 depth, emit (count, scan, emit), tile passes, ranges, plan (3) + blend
+    launches_per_render = 2 + 4 + 4 + (2 if n_tiles > 256 else 1) + 1 + 4  # K1+wide, 4 depth, emit (count, scan, emit, big), tile passes, ranges init, plan (3) + blend
     total_views = world * args.steps
     fps = total_views / (ms_max * 1e-3)
     line = {

@@ -34,6 +34,7 @@ struct gut_context {
   float4 *ell = nullptr, *payload = nullptr;
   double2 *ell64 = nullptr;
   uint32_t *deferred = nullptr;
+  uint2 *big_list = nullptr;  // K2: (Gaussian, first key slot) of the big Gaussians
   uint32_t *sa_k = nullptr, *sa_v = nullptr, *sb_k = nullptr, *sb_v = nullptr;
   uint32_t *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr;
   uint2 *ranges = nullptr, *tile_work = nullptr;
@@ -97,6 +98,7 @@ static gut_status ensure_n(gut_context *ctx, size_t n) {
   CUDA_TRY(ctx, regrow(ctx->ell, dummy, 2 * c));
   CUDA_TRY(ctx, regrow(ctx->ell64, dummy, 3 * c));
   CUDA_TRY(ctx, regrow(ctx->deferred, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->big_list, dummy, c));
   CUDA_TRY(ctx, regrow(ctx->payload, dummy, (size_t)GUT_PAYLOAD_F4 * c));
   CUDA_TRY(ctx, regrow(ctx->sa_k, dummy, c));
   CUDA_TRY(ctx, regrow(ctx->sa_v, dummy, c));
@@ -320,7 +322,7 @@ gut_status gut_context_create(int32_t dev, gut_context **out) {
 void gut_context_destroy(gut_context *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->deferred, ctx->payload, ctx->sa_k, ctx->sa_v,
+  void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->deferred, ctx->big_list, ctx->payload, ctx->sa_k, ctx->sa_v,
                 ctx->sb_k, ctx->sb_v,
                 ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->tile_work, ctx->img, ctx->st_depth,
                 ctx->st_emit, ctx->st_tile, ctx->counters, ctx->pix, ctx->anchors, ctx->seg_base, ctx->unit_ctr, ctx->q1, ctx->q2,
@@ -480,7 +482,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   }
   // K2: depth-ordered scan + emission of (tile, gid) keys
   launch_emit(order, cnt + CNT_NVIS, n32, ctx->tiles, ctx->ell, ctx->ell64, dc.tiles_x, dc.tile_cull, ctx->ka, ctx->va,
-              (uint32_t)ctx->cap_k, cnt, reinterpret_cast<uint32_t *>(ctx->st_emit), st);
+              (uint32_t)ctx->cap_k, cnt, reinterpret_cast<uint32_t *>(ctx->st_emit), ctx->big_list, st);
   if (timing) cudaEventRecord(ev[3], st);
   // K3 level 2: stable tile passes
   const uint32_t *ht = cnt + CNT_HIST_TILE;

@@ -45,10 +45,8 @@ __device__ __forceinline__ void block_scan2(uint32_t x, uint32_t y, uint32_t *s_
 // totals, scanned), so no CTA waits on another.  K2 reads only the 4-byte
 // tile code per Gaussian (gut_internal.cuh ell_tile_code): a Gaussian whose
 // tile rectangle is at most 3x3 emits its keys straight from the hit mask;
-// the others ("big", a few percent) are expanded one at a time by a warp: a
-// lane per tile row computes the span with row_span() (the function K1
-// counted with), a warp scan places the rows, and the keys are written by
-// consecutive lanes.
+// the others ("big", a few percent, clustered at the front of the depth
+// order) go to a global list that emit_big_kernel expands over the whole GPU.
 __device__ __forceinline__ void emit_key(uint32_t pos, uint32_t tile, uint32_t g, uint32_t cap_k, uint32_t *out_tile,
                                          uint32_t *out_gid, uint32_t (*s_hist)[256], uint32_t *counters) {
   if (pos < cap_k) {
@@ -65,16 +63,13 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
     const uint32_t *__restrict__ order, const uint32_t *n_vis_p, const uint32_t *__restrict__ tiles,
     const float4 *__restrict__ ell, const double2 *__restrict__ ell64, int tiles_x, int tile_cull,
     uint32_t *__restrict__ out_tile, uint32_t *__restrict__ out_gid, uint32_t cap_k, uint32_t *counters,
-    const uint32_t *__restrict__ part_off) {
+    const uint32_t *__restrict__ part_off, uint2 *__restrict__ big_list) {
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ uint32_t s_hist[2][256];
   __shared__ uint32_t s_tmp[16];
-  __shared__ uint2 s_big[GUT_EMIT_PART];  // (Gaussian, first key slot) of the CTA's big Gaussians
-  __shared__ uint32_t s_nbig;
 
   const uint32_t n = *n_vis_p;
   const int tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) s_nbig = 0;
   const uint32_t base = blockIdx.x * GUT_EMIT_PART;
   if (base >= n) return;
   const uint32_t prefix = __ldg(&part_off[blockIdx.x]);
@@ -115,64 +110,87 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
       pos += code_count(code[j]);
     }
   }
-  // ---- big Gaussians: collected per CTA (depth order clusters them in a few
-  // threads), then one warp each, round-robin over the warps, a lane per tile row
+  // ---- big Gaussians: appended to a global list (depth order clusters them in
+  // the first partitions) and expanded by emit_big_kernel over the whole GPU
 #pragma unroll
-  for (int j = 0; j < GUT_EMIT_ITEMS; ++j)
-    if (big[j]) s_big[atomicAdd(&s_nbig, 1u)] = make_uint2(g[j], bpos[j]);
+  for (int j = 0; j < GUT_EMIT_ITEMS; ++j) {
+    const uint32_t bm = __ballot_sync(FULL, big[j]);
+    if (!bm) continue;
+    uint32_t slot = 0;
+    if (lane == __ffs(bm) - 1) slot = atomicAdd(&counters[CNT_NBIG], (uint32_t)__popc(bm));
+    slot = __shfl_sync(FULL, slot, __ffs(bm) - 1) + (uint32_t)__popc(bm & ((1u << lane) - 1u));
+    if (big[j]) big_list[slot] = make_uint2(g[j], bpos[j]);
+  }
   __syncthreads();
-  const uint32_t nbig = s_nbig;
-  for (uint32_t bi = (uint32_t)(tid >> 5); bi < nbig; bi += GUT_EMIT_THREADS / 32) {
-    {
-      const uint2 bg = s_big[bi];
-      const uint32_t gg = bg.x;
-      uint32_t kpos = bg.y;
-      const float4 a = __ldg(&ell[2 * gg]), b = __ldg(&ell[2 * gg + 1]);
-      const uint32_t r0w = __float_as_uint(b.z), r1w = __float_as_uint(b.w);
-      const int x0 = (int)(r0w & 0xFFFF), y0 = (int)(r0w >> 16), x1 = (int)(r1w & 0xFFFF), y1 = (int)(r1w >> 16);
-      const bool wide = b.y < 0.f;
-      Ell el;
-      EllD ed;
-      if (!wide) {
-        el.vx = a.x; el.vy = a.y; el.cxx = a.z; el.cxy = a.w; el.cyy = b.x; el.k2 = b.y;
-        el.x0 = x0; el.y0 = y0; el.x1 = x1; el.y1 = y1;
-      } else {  // "wide" Gaussian: fp64 ellipse written by the fp64 K1 kernel
-        const double2 q0 = ell64[3 * gg], q1 = ell64[3 * gg + 1], q2 = ell64[3 * gg + 2];
-        ed.vx = q0.x; ed.vy = q0.y; ed.cxx = q1.x; ed.cxy = q1.y; ed.cyy = q2.x; ed.k2 = q2.y;
-        ed.x0 = x0; ed.y0 = y0; ed.x1 = x1; ed.y1 = y1;
+  for (int jj = tid; jj < 512; jj += GUT_EMIT_THREADS) {
+    const uint32_t v = (&s_hist[0][0])[jj];
+    if (v) atomicAdd(&counters[CNT_HIST_TILE + jj], v);
+  }
+}
+
+// big Gaussians (tile rectangle > 3x3): one warp each, grid-stride over the
+// list, a lane per tile row (row_span), a warp scan places the rows, the keys
+// are written by consecutive lanes
+__global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_big_kernel(
+    const uint2 *__restrict__ big_list, const float4 *__restrict__ ell, const double2 *__restrict__ ell64,
+    int tiles_x, int tile_cull, uint32_t *__restrict__ out_tile, uint32_t *__restrict__ out_gid, uint32_t cap_k,
+    uint32_t *counters) {
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ uint32_t s_hist[2][256];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int j = tid; j < 512; j += GUT_EMIT_THREADS) (&s_hist[0][0])[j] = 0;
+  __syncthreads();
+  const uint32_t nbig = counters[CNT_NBIG];
+  const uint32_t wstride = gridDim.x * (GUT_EMIT_THREADS / 32);
+  for (uint32_t bi = blockIdx.x * (GUT_EMIT_THREADS / 32) + (uint32_t)(tid >> 5); bi < nbig; bi += wstride) {
+    const uint2 bg = big_list[bi];
+    const uint32_t gg = bg.x;
+    uint32_t kpos = bg.y;
+    const float4 a = __ldg(&ell[2 * gg]), b = __ldg(&ell[2 * gg + 1]);
+    const uint32_t r0w = __float_as_uint(b.z), r1w = __float_as_uint(b.w);
+    const int x0 = (int)(r0w & 0xFFFF), y0 = (int)(r0w >> 16), x1 = (int)(r1w & 0xFFFF), y1 = (int)(r1w >> 16);
+    const bool wide = b.y < 0.f;
+    Ell el;
+    EllD ed;
+    if (!wide) {
+      el.vx = a.x; el.vy = a.y; el.cxx = a.z; el.cxy = a.w; el.cyy = b.x; el.k2 = b.y;
+      el.x0 = x0; el.y0 = y0; el.x1 = x1; el.y1 = y1;
+    } else {  // "wide" Gaussian: fp64 ellipse written by the fp64 K1 kernel
+      const double2 q0 = ell64[3 * gg], q1 = ell64[3 * gg + 1], q2 = ell64[3 * gg + 2];
+      ed.vx = q0.x; ed.vy = q0.y; ed.cxx = q1.x; ed.cxy = q1.y; ed.cyy = q2.x; ed.k2 = q2.y;
+      ed.x0 = x0; ed.y0 = y0; ed.x1 = x1; ed.y1 = y1;
+    }
+    for (int rb = y0; rb <= y1; rb += 32) {
+      const int ty = rb + lane;
+      int l = 0, h = -1;
+      if (ty <= y1) {
+        if (!wide) row_span(el, ty, tile_cull, l, h);
+        else row_span(ed, ty, tile_cull, l, h);
       }
-      for (int rb = y0; rb <= y1; rb += 32) {
-        const int ty = rb + lane;
-        int l = 0, h = -1;
-        if (ty <= y1) {
-          if (!wide) row_span(el, ty, tile_cull, l, h);
-          else row_span(ed, ty, tile_cull, l, h);
-        }
-        const uint32_t cnt = (uint32_t)max(h - l + 1, 0);
-        uint32_t incl = cnt;
+      const uint32_t cnt = (uint32_t)max(h - l + 1, 0);
+      uint32_t incl = cnt;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(FULL, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const uint32_t tot = __shfl_sync(FULL, incl, 31);
-        for (uint32_t e0 = 0; e0 < tot; e0 += 32) {  // warp-uniform trip count (full-mask shuffles)
-          const uint32_t e = e0 + (uint32_t)lane;
-          int lo = 0;  // first row (lane) with incl > e
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1) {
-            const uint32_t v = __shfl_sync(FULL, incl, lo + step - 1);
-            if (v <= e) lo += step;
-          }
-          const uint32_t ex_lo = __shfl_sync(FULL, incl - cnt, lo);
-          const int l_lo = __shfl_sync(FULL, l, lo);
-          if (e < tot) {
-            const uint32_t tile = (uint32_t)(rb + lo) * (uint32_t)tiles_x + (uint32_t)l_lo + (e - ex_lo);
-            emit_key(kpos + e, tile, gg, cap_k, out_tile, out_gid, s_hist, counters);
-          }
-        }
-        kpos += tot;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
       }
+      const uint32_t tot = __shfl_sync(FULL, incl, 31);
+      for (uint32_t e0 = 0; e0 < tot; e0 += 32) {  // warp-uniform trip count (full-mask shuffles)
+        const uint32_t e = e0 + (uint32_t)lane;
+        int lo = 0;  // first row (lane) with incl > e
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const uint32_t v = __shfl_sync(FULL, incl, lo + step - 1);
+          if (v <= e) lo += step;
+        }
+        const uint32_t ex_lo = __shfl_sync(FULL, incl - cnt, lo);
+        const int l_lo = __shfl_sync(FULL, l, lo);
+        if (e < tot) {
+          const uint32_t tile = (uint32_t)(rb + lo) * (uint32_t)tiles_x + (uint32_t)l_lo + (e - ex_lo);
+          emit_key(kpos + e, tile, gg, cap_k, out_tile, out_gid, s_hist, counters);
+        }
+      }
+      kpos += tot;
     }
   }
   __syncthreads();
@@ -244,13 +262,16 @@ __global__ __launch_bounds__(1024) void emit_scan_kernel(const uint32_t *n_vis_p
 
 void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper, const uint32_t *tiles,
                  const float4 *ell, const double2 *ell64, int tiles_x, int tile_cull, uint32_t *out_tile,
-                 uint32_t *out_gid, uint32_t cap_k, uint32_t *counters, uint32_t *part_off, cudaStream_t st) {
+                 uint32_t *out_gid, uint32_t cap_k, uint32_t *counters, uint32_t *part_off, uint2 *big_list,
+                 cudaStream_t st) {
   if (n_upper == 0) return;
   unsigned blocks = (n_upper + GUT_EMIT_PART - 1) / GUT_EMIT_PART;
   emit_count_kernel<<<blocks, GUT_EMIT_THREADS, 0, st>>>(order, n_vis, tiles, part_off);
   emit_scan_kernel<<<1, 1024, 0, st>>>(n_vis, part_off);
   emit_kernel<<<blocks, GUT_EMIT_THREADS, 0, st>>>(order, n_vis, tiles, ell, ell64, tiles_x, tile_cull, out_tile, out_gid,
-                                                   cap_k, counters, part_off);
+                                                   cap_k, counters, part_off, big_list);
+  emit_big_kernel<<<148 * 4, GUT_EMIT_THREADS, 0, st>>>(big_list, ell, ell64, tiles_x, tile_cull, out_tile, out_gid,
+                                                        cap_k, counters);
 }
 
 }  // namespace gut

@@ -33,6 +33,7 @@ enum : int {
   CNT_Q_HEAD2 = 34,        //   next queue-2 (granted successor) entry
   CNT_Q_ALLOC2 = 35,       //   queue-2 entries allocated
   CNT_Q_FINISHED = 36,     //   units (8 per tile) whose pixels are written
+  CNT_NBIG = 37,           // K2: Gaussians in the big list (tile rectangle > 3x3)
   CNT_HIST_DEPTH = 64,     // 4 x 256
   CNT_HIST_TILE = 64 + 1024,  // 2 x 256
   CNT_PLAN_HIST = 64 + 1024 + 512,  // 1024 blend queue-1 buckets
@@ -60,7 +61,8 @@ void launch_ranges_init(uint2 *ranges, int n_tiles, cudaStream_t st);
 // one uint32 per GUT_EMIT_PART Gaussians of the upper bound n_upper)
 void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper, const uint32_t *tiles,
                  const float4 *ell, const double2 *ell64, int tiles_x, int tile_cull, uint32_t *out_tile,
-                 uint32_t *out_gid, uint32_t cap_k, uint32_t *counters, uint32_t *part_off, cudaStream_t st);
+                 uint32_t *out_gid, uint32_t cap_k, uint32_t *counters, uint32_t *part_off, uint2 *big_list,
+                 cudaStream_t st);
 
 
 
