@@ -308,7 +308,7 @@ gut_status gut_context_create(int32_t dev, gut_context **out) {
   }
   if (const char *e = getenv("GUT_BLEND_WINDOW")) {  // tuning knob: speculative segments in flight per tile
     int v = atoi(e);
-    if (v >= 1 && v <= 1 << 20) ctx->blend_window = v;
+    if (v >= 1 && v <= 255) ctx->blend_window = v;  // (queue-1 entries carry the segment in 8 bits)
   }
   if (cudaMalloc((void **)&ctx->counters, CNT_WORDS * sizeof(uint32_t)) != cudaSuccess ||
       cudaMallocHost((void **)&ctx->h_counters, CNT_WORDS * sizeof(uint32_t)) != cudaSuccess) {

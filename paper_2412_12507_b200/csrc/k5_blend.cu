@@ -335,7 +335,9 @@ __global__ __launch_bounds__(256) void plan_fill_kernel(const uint2 *__restrict_
   uint32_t pos = 0;
   if (t < n_tiles && lane == leader) pos = atomicAdd(&counters[CNT_PLAN_HIST + bk], gsum);
   pos = __shfl_sync(peers, pos, leader) + pre;
-  for (uint32_t k = 0; k < g; ++k) q1[pos + k] = GUT_BLEND_WARPS * (uint32_t)t + k % GUT_BLEND_WARPS;
+  // entry = unit | segment << 24 (a unit's first segments in order)
+  for (uint32_t k = 0; k < g; ++k)
+    q1[pos + k] = (GUT_BLEND_WARPS * (uint32_t)t + k % GUT_BLEND_WARPS) | ((k / GUT_BLEND_WARPS) << 24);
 }
 
 void launch_plan(const uint2 *ranges, int n_tiles, int seg, int window, uint32_t *seg_base, uint32_t *q1,
@@ -773,13 +775,13 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t *p, uint32_t v) {
   return old;
 }
 
-__device__ bool fetch_work(const BlendBufs &B, int &unit, int &s) {
+__device__ bool fetch_work(const BlendBufs &B, uint32_t n_init, int &unit, int &s) {
   uint32_t *cnt = B.counters;
-  const uint32_t n_init = cnt[CNT_Q_NINIT];
   const uint32_t n_units = (uint32_t)B.n_tiles * GUT_BLEND_WARPS;
   for (;;) {
-    const bool q1_empty = ld_volatile_u32(&cnt[CNT_Q_HEAD1]) >= n_init;
+    const uint32_t hd1 = ld_volatile_u32(&cnt[CNT_Q_HEAD1]);
     const uint32_t h2 = ld_volatile_u32(&cnt[CNT_Q_HEAD2]), a2 = ld_volatile_u32(&cnt[CNT_Q_ALLOC2]);
+    const bool q1_empty = hd1 >= n_init;
     // nothing left to hand out and enough warps already waiting for future
     // grants: leave (a warp never leaves holding a ticket, so every granted
     // slot keeps a consumer; idle warps would only burn issue slots)
@@ -793,13 +795,18 @@ __device__ bool fetch_work(const BlendBufs &B, int &unit, int &s) {
       }
       B.q2[t2] = 0;  // slot reusable by the next render
       unit = (int)(u1 - 1);
-      s = (int)atomicAdd(&B.next_s[unit], 1u);
+      // granted successors follow the unit's first min(S, window) segments
+      const uint2 rg = B.ranges[unit / GUT_BLEND_WARPS];
+      const uint32_t len = rg.y > rg.x ? rg.y - rg.x : 0u;
+      const uint32_t S = len == 0 ? 1u : (len + B.seg - 1) / B.seg;
+      s = (int)(min(S, (uint32_t)B.window) + atomicAdd(&B.next_s[unit], 1u));
       return true;
     }
     const uint32_t h1 = atomicAdd(&cnt[CNT_Q_HEAD1], 1u);
     if (h1 < n_init) {
-      unit = (int)B.q1[h1];
-      s = (int)atomicAdd(&B.next_s[unit], 1u);
+      const uint32_t e = B.q1[h1];  // unit | segment << 24 (plan_fill_kernel)
+      unit = (int)(e & 0xFFFFFFu);
+      s = (int)(e >> 24);
       return true;
     }
   }
@@ -818,10 +825,11 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   uint32_t n_eval_acc = 0, n_contrib_acc = 0, n_term_acc = 0;
+  const uint32_t n_init = B.counters[CNT_Q_NINIT];
 
   for (;;) {
     int unit = -1, s = 0;
-    if (lane == 0 && !fetch_work(B, unit, s)) unit = -1;
+    if (lane == 0 && !fetch_work(B, n_init, unit, s)) unit = -1;
     unit = __shfl_sync(FULL, unit, 0);
     s = __shfl_sync(FULL, s, 0);
     if (unit < 0) break;
