@@ -11,7 +11,9 @@ rank r renders view (s * N + r) mod 256 at step s (weak scaling in views).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Prints ONE JSON line (rank 0).  value = frames/s over all ranks with the
-scene resident in HBM (device-timed with CUDA events, max over ranks);
+scene resident in HBM (device-timed with CUDA events, max over ranks; 3
+frames in flight per GPU on separate contexts/streams, --inflight 1 for
+strictly sequential frames; single_stream = one frame at a time);
 e2e = the same metric through the C ABI with HOST output buffers (device->host
 copy of RGB/alpha/depth inside the timed region, camera struct in by value).
 --impl reference times the fp64 CPU oracle (the paper's algorithm written out)
@@ -46,6 +48,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--inflight", type=int, default=3, help="frames in flight (contexts x streams) in the timed region")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-tiles", type=int, default=512, help="tiles in the oracle's bounded sample")
     p.add_argument("--n", type=int, default=None, help="override N (debug only; the default is the config)")
@@ -289,30 +292,64 @@ def run_ours(args):
     torch.cuda.synchronize()
     P.barrier()
     torch.cuda.synchronize()
+    timed_views = [P.view_of(args.warmup + s, rank, world, nv) for s in range(args.steps)]
+    # per-stage breakdown: the timed views rendered one after another on one
+    # stream with the library's stage events (gut_timing_read)
+    for v in timed_views:
+        gut.gut_render(ctx, scene, cams[v], topt, out_dev, stream=stream, stats=False)
+    torch.cuda.synchronize()
+    stage_sum, n_timed = gut.gut_timing_read(ctx, reset=True)
+    stage_ms = {k: v / max(n_timed, 1) for k, v in stage_sum.items()}
+    # timed region: `inflight` frames in flight, contexts (own workspaces, shared
+    # read-only scene) on their own streams taking the views in turn, so one
+    # frame's kernel tails overlap the next frame's first kernels
+    lanes_d = [(ctx, stream, out_dev)]
+    extra = []
+    for _ in range(args.inflight - 1):
+        c2 = gut.gut_context_create(local)
+        gut.gut_workspace_reserve(c2, int(kmax * 1.02) + 65536, N, W, H)
+        st2 = torch.cuda.Stream(device=dev)
+        bufs = (torch.empty((H, W, 3), device=dev), torch.empty((H, W), device=dev), torch.empty((H, W), device=dev))
+        extra.append((c2, bufs))
+        lanes_d.append((c2, st2, gut.gut_outputs(bufs[0].data_ptr(), bufs[1].data_ptr(), bufs[2].data_ptr(), 1, 0)))
+    for i, (c_, st_, o_) in enumerate(lanes_d):  # warm every context
+        for s in range(2):
+            gut.gut_render(c_, scene, cams[P.view_of(s + i, rank, world, nv)], gopt, o_, stream=st_, stats=False)
+    torch.cuda.synchronize()
+    P.barrier()
+    torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    timed_views = [P.view_of(args.warmup + s, rank, world, nv) for s in range(args.steps)]
     ev0.record(stream)
-    for v in timed_views:
-        gut.gut_render(ctx, scene, cams[v], topt, out_dev, stream=stream, stats=False)
+    for c_, st_, o_ in lanes_d[1:]:
+        st_.wait_event(ev0)
+    for i, v in enumerate(timed_views):
+        c_, st_, o_ = lanes_d[i % len(lanes_d)]
+        gut.gut_render(c_, scene, cams[v], gopt, o_, stream=st_, stats=False)
+    for c_, st_, o_ in lanes_d[1:]:
+        j = torch.cuda.Event()
+        j.record(st_)
+        stream.wait_event(j)
     ev1.record(stream)
     torch.cuda.synchronize()
     P.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     ms_max = P.max_over_ranks(ms, device=dev)
-    stage_sum, n_timed = gut.gut_timing_read(ctx, reset=True)
-    stage_ms = {k: v / max(n_timed, 1) for k, v in stage_sum.items()}
+    for c2, _ in extra:
+        gut.gut_context_destroy(c2)
     # e2e: host (pinned) outputs through the same C-ABI call; D2H inside the timed
     # region.  Two contexts on two streams alternate frames so the copy of one
     # frame overlaps the render of the next (the scene is shared read-only).
-    ctx2 = gut.gut_context_create(local)
-    gut.gut_workspace_reserve(ctx2, int(kmax * 1.02) + 65536, N, W, H)
-    stream2 = torch.cuda.Stream(device=dev)
+    e2e_ctx = [(ctx, stream)]
+    for _ in range(max(2, args.inflight) - 1):
+        c2 = gut.gut_context_create(local)
+        gut.gut_workspace_reserve(c2, int(kmax * 1.02) + 65536, N, W, H)
+        e2e_ctx.append((c2, torch.cuda.Stream(device=dev)))
     lanes = []
-    for c_, st_ in ((ctx, stream), (ctx2, stream2)):
+    for c_, st_ in e2e_ctx:
         hr = torch.empty((H, W, 3), pin_memory=True)
         ha = torch.empty((H, W), pin_memory=True)
         hd = torch.empty((H, W), pin_memory=True)
@@ -325,19 +362,22 @@ def run_ours(args):
     torch.cuda.synchronize()
     P.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    j0 = torch.cuda.Event()
     e0.record(stream)
-    stream2.wait_event(e0)
+    for _, st_, _, _ in lanes[1:]:
+        st_.wait_event(e0)
     for s in range(e2e_steps):
         v = P.view_of(e2e_first + 2 + s, rank, world, nv)
-        c_, st_, o_, _ = lanes[s % 2]
+        c_, st_, o_, _ = lanes[s % len(lanes)]
         gut.gut_render(c_, scene, cams[v], gopt, o_, stream=st_, stats=False)
-    j0.record(stream2)
-    stream.wait_event(j0)
+    for _, st_, _, _ in lanes[1:]:
+        j0 = torch.cuda.Event()
+        j0.record(st_)
+        stream.wait_event(j0)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = P.max_over_ranks(e0.elapsed_time(e1), device=dev)
-    gut.gut_context_destroy(ctx2)
+    for c2, _ in e2e_ctx[1:]:
+        gut.gut_context_destroy(c2)
     # per-view statistics of the timed views (deterministic renders) gathered to rank 0
     rows = [[v, per_view[v]["n_visible"], per_view[v]["n_keys"], per_view[v]["pairs_evaluated"],
              per_view[v]["pairs_contributing"], per_view[v]["max_tile_len"]] for v in timed_views]
@@ -365,15 +405,19 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "views_per_step": world, "parallelism": f"views sharded over {world} GPU(s), "
                    "scene replicated", "l2": "inputs larger than L2 (720 MB resident scene; 41 MB output/view)",
-                   "capacity_mode": True, "reserved_keys": int(kmax * 1.02) + 65536},
+                   "capacity_mode": True, "reserved_keys": int(kmax * 1.02) + 65536,
+                   "frames_in_flight": args.inflight,
+                   "ms_stage_note": "ms_stage: the same views one at a time on one stream (library stage events)"},
         "mpix_per_s": fps * npix / 1e6,
+        "single_stream": {"frames_per_s": world * 1e3 / stage_ms["total"], "ms_per_frame": stage_ms["total"],
+                          "what": "one frame at a time on one stream (per-frame latency; library stage events)"},
         "ms_stage": stage_ms,
         "clocks": clk,
         "e2e": {"value": world * e2e_steps / (e2e_ms * 1e-3), "unit": "frames/s", "h2d_bytes_per_step": 240,
                 "d2h_bytes_per_step": npix * 5 * 4,
                 "what": "gut_render with host (pinned) output buffers: RGB+alpha+depth copied device->host each "
-                        "step; camera struct (240 B) passed by value; scene resident (uploaded once); two "
-                        "contexts on two streams alternate frames (copy of frame i overlaps render of i+1)"},
+                        "step; camera struct (240 B) passed by value; scene resident (uploaded once); "
+                        "frames in flight on separate contexts/streams (copies overlap later renders)"},
         "gpu_launches": launches_per_render * args.steps,
         "roofline": {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                      "unit": d["unit"], "frac": d["frac"], "traffic": traffic, "traffic_source": traffic_src,
