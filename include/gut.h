@@ -156,7 +156,9 @@ typedef enum {
                                (tile | segment << 16 | block << 29, SM id, start ns, end ns,
                                entries visited, pairs evaluated, pairs contributing, re-ran);
                                all zero for units that did not run; only with env
-                               GUT_BLEND_TRACE=1 */
+                               GUT_BLEND_TRACE=1 */,
+  GUT_STAGE_COUNTERS = 7    /* uint32[64]: the render's device counters (diagnostics; layout
+                               internal, see csrc/launch.h CNT_*) */
 } gut_stage;
 
 typedef struct { /* GUT_STAGE_PROJECT record (K1 output, fp32) */

@@ -219,6 +219,7 @@ static gut_status build_cam(gut_context *ctx, const gut_camera *cam, const gut_o
   c.p[0] = cam->p[0]; c.p[1] = cam->p[1];
   c.fov = cam->model == GUT_CAM_FISHEYE ? cam->fov_limit : (cam->fov_limit > 0 ? cam->fov_limit : 0);
   c.fxf = (float)c.fx; c.fyf = (float)c.fy; c.cxf = (float)c.cx; c.cyf = (float)c.cy;
+  c.inv_wf = 1.f / (float)c.width; c.inv_hf = 1.f / (float)c.height;
   c.pf[0] = (float)c.p[0]; c.pf[1] = (float)c.p[1]; c.fovf = (float)c.fov;
   // pose: R0 from the normalised t=0 quaternion; slerp axis-angle of q0^-1 q1
   double q0[4], q1[4];
@@ -652,6 +653,7 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
     case GUT_STAGE_RANGES:
     case GUT_STAGE_TILE_WORK: need = (size_t)ctx->last_tiles * 2 * sizeof(uint32_t); break;
     case GUT_STAGE_BLEND_TRACE: need = ctx->trace ? 2 * GUT_BLEND_WARPS * ctx->last_items * sizeof(uint4) : 0; break;
+    case GUT_STAGE_COUNTERS: need = 64 * sizeof(uint32_t); break;
     default: return fail(ctx, GUT_E_INVALID_ARGUMENT, "stage");
   }
   if (bytes_needed) *bytes_needed = need;
@@ -694,6 +696,8 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
     uint32_t *r = (uint32_t *)host_dst;  // empty tiles: (UINT_MAX, 0) on the device -> (0, 0)
     for (size_t t = 0; t < need / 8; ++t)
       if (r[2 * t + 1] <= r[2 * t]) r[2 * t] = r[2 * t + 1] = 0;
+  } else if (stage == GUT_STAGE_COUNTERS) {
+    CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->counters, need, cudaMemcpyDeviceToHost));
   } else if (stage == GUT_STAGE_BLEND_TRACE) {
     CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->trace, need, cudaMemcpyDeviceToHost));
   } else {

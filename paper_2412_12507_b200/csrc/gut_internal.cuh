@@ -35,6 +35,7 @@ struct DevCam {
   // intrinsics (fp64 master copy; fp32 copies for K1)
   double fx, fy, cx, cy, k[6], p[2], fov;
   float fxf, fyf, cxf, cyf, kf[6], pf[2], fovf;
+  float inv_wf, inv_hf;  // 1 / width, 1 / height (rolling-shutter row time)
   // pose: R0 = camera->world at t=0 (row-major), c0 = centre at t=0,
   // dc = c1 - c0, phi = axis-angle (body frame) of R0^T R1 (slerp = R0 Exp(t phi))
   double R0[9], c0[3], dc[3], phi_axis[3], phi_angle;
@@ -83,18 +84,34 @@ __host__ __device__ __forceinline__ V mtv(const M *m, V v) {
 }
 
 // Rodrigues: R = I + sin(a) [u]x + (1 - cos(a)) [u]x^2, row-major (fp32)
+// (rolling-shutter rotations are tiny: |angle| ~ readout x angular rate; the
+// Taylor branch is exact to the precision and avoids the sincos range reduction)
 __device__ __forceinline__ void rodrigues(f3 u, float ang, float R[9]) {
-  float s, c;
-  sincosf(ang, &s, &c);
-  float t = 1.f - c;
+  float s, c, t;
+  if (fabsf(ang) < 0.03f) {
+    const float a2 = ang * ang;
+    s = ang * (1.f - a2 * (1.f / 6.f) * (1.f - a2 * 0.05f));
+    t = 0.5f * a2 * (1.f - a2 * (1.f / 12.f));  // 1 - cos without cancellation
+    c = 1.f - t;
+  } else {
+    sincosf(ang, &s, &c);
+    t = 1.f - c;
+  }
   R[0] = c + t * u.x * u.x;       R[1] = t * u.x * u.y - s * u.z; R[2] = t * u.x * u.z + s * u.y;
   R[3] = t * u.x * u.y + s * u.z; R[4] = c + t * u.y * u.y;       R[5] = t * u.y * u.z - s * u.x;
   R[6] = t * u.x * u.z - s * u.y; R[7] = t * u.y * u.z + s * u.x; R[8] = c + t * u.z * u.z;
 }
 __device__ __forceinline__ void rodrigues_d(d3 u, double ang, double R[9]) {
-  double s, c;
-  sincos(ang, &s, &c);
-  double t = 1.0 - c;
+  double s, c, t;
+  if (fabs(ang) < 0.01) {
+    const double a2 = ang * ang;
+    s = ang * (1.0 - a2 / 6.0 * (1.0 - a2 / 20.0 * (1.0 - a2 / 42.0)));
+    t = 0.5 * a2 * (1.0 - a2 / 12.0 * (1.0 - a2 / 30.0 * (1.0 - a2 / 56.0)));
+    c = 1.0 - t;
+  } else {
+    sincos(ang, &s, &c);
+    t = 1.0 - c;
+  }
   R[0] = c + t * u.x * u.x;       R[1] = t * u.x * u.y - s * u.z; R[2] = t * u.x * u.z + s * u.y;
   R[3] = t * u.x * u.y + s * u.z; R[4] = c + t * u.y * u.y;       R[5] = t * u.y * u.z - s * u.x;
   R[6] = t * u.x * u.z - s * u.y; R[7] = t * u.y * u.z + s * u.x; R[8] = c + t * u.z * u.z;

@@ -45,8 +45,9 @@ __device__ __forceinline__ bool project_cam_f(const DevCam &c, f3 x, float &du, 
   switch (c.model) {
     case CAM_PINHOLE: {
       if (!(x.z > c.near_plane)) return false;
-      du = c.fxf * (x.x / x.z);
-      dv = c.fyf * (x.y / x.z);
+      const float rz = __frcp_rn(x.z);
+      du = c.fxf * (x.x * rz);
+      dv = c.fyf * (x.y * rz);
       return true;
     }
     case CAM_ORTHO: {
@@ -57,11 +58,12 @@ __device__ __forceinline__ bool project_cam_f(const DevCam &c, f3 x, float &du, 
     }
     case CAM_OPENCV: {
       if (!(x.z > c.near_plane)) return false;
-      float xn = x.x / x.z, yn = x.y / x.z, r2 = xn * xn + yn * yn;
+      const float rz = __frcp_rn(x.z);
+      float xn = x.x * rz, yn = x.y * rz, r2 = xn * xn + yn * yn;
       if (c.fovf > 0.f && !(r2 <= c.fovf * c.fovf)) return false;
       float num = 1.f + r2 * (c.kf[0] + r2 * (c.kf[1] + r2 * c.kf[2]));
       float den = 1.f + r2 * (c.kf[3] + r2 * (c.kf[4] + r2 * c.kf[5]));
-      float a = num / den;
+      float a = num * __frcp_rn(den);
       float xd = xn * a + 2.f * c.pf[0] * xn * yn + c.pf[1] * (r2 + 2.f * xn * xn);
       float yd = yn * a + c.pf[0] * (r2 + 2.f * yn * yn) + 2.f * c.pf[1] * xn * yn;
       du = c.fxf * xd;
@@ -90,10 +92,10 @@ __device__ __forceinline__ bool project_cam_f(const DevCam &c, f3 x, float &du, 
 __device__ __forceinline__ float shutter_coord(const DevCam &c, float du, float dv) {
   float r;
   switch (c.shutter) {
-    case SH_T2B: r = (dv + c.cyf) / (float)c.height; break;
-    case SH_B2T: r = 1.f - (dv + c.cyf) / (float)c.height; break;
-    case SH_L2R: r = (du + c.cxf) / (float)c.width; break;
-    case SH_R2L: r = 1.f - (du + c.cxf) / (float)c.width; break;
+    case SH_T2B: r = (dv + c.cyf) * c.inv_hf; break;
+    case SH_B2T: r = 1.f - (dv + c.cyf) * c.inv_hf; break;
+    case SH_L2R: r = (du + c.cxf) * c.inv_wf; break;
+    case SH_R2L: r = 1.f - (du + c.cxf) * c.inv_wf; break;
     default: return 0.f;
   }
   return fminf(fmaxf(r, 0.f), 1.f);
@@ -123,10 +125,15 @@ __device__ __forceinline__ bool project_sigma(const DevCam &c, f3 y, f3 w, float
   float t1 = t0 + f0, u1, v1;
   if (!project_cam_f(c, cam_point_at(c, y, w, t1), u1, v1)) return false;
   float f1 = shutter_coord(c, u1, v1) - t1;
+  // stop when the pixel moved less than the tolerance -- or than fp32 can
+  // resolve at this pixel position (4 ulps), beyond which steps are noise -- or
+  // when the time no longer changes
+  const float tol2 = c.rs_tol_px * c.rs_tol_px;
   for (int it = 0; it < c.rs_max_iter; ++it) {
-    if (hypotf(u1 - u0, v1 - v0) < c.rs_tol_px) break;
+    const float ddu = u1 - u0, ddv = v1 - v0, ulp4 = 4.8e-7f * (fabsf(u1) + fabsf(v1));
+    if (ddu * ddu + ddv * ddv < fmaxf(tol2, ulp4 * ulp4) || t1 == t0) break;
     float den = f1 - f0;
-    float t2 = fabsf(den) > 1e-12f ? t1 - f1 * (t1 - t0) / den : t1 + f1;
+    float t2 = fabsf(den) > 1e-12f ? t1 - f1 * (t1 - t0) * __frcp_rn(den) : t1 + f1;
     t2 = fminf(fmaxf(t2, 0.f), 1.f);
     t0 = t1; u0 = u1; v0 = v1; f0 = f1; t1 = t2;
     if (!project_cam_f(c, cam_point_at(c, y, w, t1), u1, v1)) return false;
@@ -555,7 +562,7 @@ void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32
                     double2 *ell64, float4 *payload, uint32_t *counters, uint32_t *deferred, cudaStream_t st) {
   if (s.n == 0) return;
   const unsigned blocks = (unsigned)((s.n + 255) / 256);
-  const unsigned wblocks = 32;  // grid-stride over the (few) deferred Gaussians
+  const unsigned wblocks = 148 * 4;  // grid-stride over the deferred Gaussians (count known on the device only)
   switch (s.sh_degree) {
     case 0:
       project_kernel<0><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);

@@ -20,7 +20,7 @@ STATUS = {0: "GUT_OK", 1: "GUT_E_INVALID_ARGUMENT", 2: "GUT_E_UNSUPPORTED", 3: "
 MODELS = {"pinhole": 0, "opencv": 1, "fisheye": 2, "ortho": 3}
 SHUTTERS = {"global": 0, "top_to_bottom": 1, "left_to_right": 2, "bottom_to_top": 3, "right_to_left": 4}
 STAGE_PROJECT, STAGE_DEPTH_ORDER, STAGE_SORTED, STAGE_RANGES, STAGE_TILE_WORK = 1, 2, 3, 4, 5
-STAGE_BLEND_TRACE = 6
+STAGE_BLEND_TRACE, STAGE_COUNTERS = 6, 7
 
 
 class gut_camera(C.Structure):
