@@ -23,7 +23,7 @@ def gpu_render(scene, cam, opt=None, reserve=None, timing=False):
     torch.cuda.synchronize()
     out = dict(rgb=rgb.cpu().numpy(), alpha=alpha.cpu().numpy(), depth=depth.cpu().numpy(), stats=st.as_dict(),
                proj=r.stage(gut.STAGE_PROJECT), sorted=r.stage(gut.STAGE_SORTED), ranges=r.stage(gut.STAGE_RANGES),
-               order=r.stage(gut.STAGE_DEPTH_ORDER))
+               order=r.stage(gut.STAGE_DEPTH_ORDER), counters=r.stage(gut.STAGE_COUNTERS))
     r.close()
     return out
 
