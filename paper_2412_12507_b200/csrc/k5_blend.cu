@@ -425,6 +425,16 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -545,9 +555,10 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
       const float rn0 = fmaf(M[0], M[0], fmaf(M[1], M[1], M[2] * M[2]));
       const float rn1 = fmaf(M[3], M[3], fmaf(M[4], M[4], M[5] * M[5]));
       const float rn2 = fmaf(M[6], M[6], fmaf(M[7], M[7], M[8] * M[8]));
-      const float dM = sqrtf(rn0 * rn1 * rn2);
+      // (MUFU rsqrt / rcp: relative error ~2^-22 in the row scales, harmless)
+      const float r012 = rn0 * rn1 * rn2, dM = r012 * rsqrt_approx(r012);
       const f3 Mx = mv(M, x);
-      const f3 c0 = mk(Mx.x * (dM / rn0), Mx.y * (dM / rn1), Mx.z * (dM / rn2));
+      const f3 c0 = mk(Mx.x * (dM * rcp_approx(rn0)), Mx.y * (dM * rcp_approx(rn1)), Mx.z * (dM * rcp_approx(rn2)));
       const f3 ogf = mv(M, tof(w)), e0 = mv(M, Df);
       const float g0 = dot(ogf, e0);
       f3 U = mv(M, T1f), V = mv(M, T2f), P, Q;
@@ -571,8 +582,9 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
       if (MODE == 2) {
         maybe = true;
       } else {
-        const float lo = sqrtf(dot(n0, n0)) - (ra * sqrtf(dot(P, P)) + rb * sqrtf(dot(Q, Q)));
-        const float hi = sqrtf(dot(e0c, e0c)) + (ra * sqrtf(dot(U, U)) + rb * sqrtf(dot(V, V)));
+        // (MUFU square roots: 2^-22 relative, inside the 1e-3 margin below)
+        const float lo = sqrt_approx(dot(n0, n0)) - (ra * sqrt_approx(dot(P, P)) + rb * sqrt_approx(dot(Q, Q)));
+        const float hi = sqrt_approx(dot(e0c, e0c)) + (ra * sqrt_approx(dot(U, U)) + rb * sqrt_approx(dot(V, V)));
         maybe = !(lo > 0.f && lo * lo > 1.001f * k2 * (hi * hi));
       }
       if (maybe) {
@@ -602,7 +614,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           const float det = fmaf(pp, qq, -pq * pq);
           float xa = 0.f, xb = 0.f;
           if (det > 1e-30f * pp * qq && det > 0.f) {
-            const float id = 1.f / det;
+            const float id = rcp_approx(det);  // (expansion point only)
             xa = (pq * nq - qq * np) * id;
             xb = (pq * np - pp * nq) * id;
           }
@@ -622,8 +634,10 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           // margin 1e-4 of the terms' magnitude for fp32 rounding
           const float la = ac - ra - as, ha = ac + ra - as, lb = bc - rb - bs, hb = bc + rb - bs;
           const float A = fmaxf(-la, ha), Bm = fmaxf(-lb, hb);
-          const float xa_ = Faa > 0.f ? fminf(fmaxf(-0.5f * Fa / Faa, la), ha) : (Fa > 0.f ? la : ha);
-          const float xb_ = Fbb > 0.f ? fminf(fmaxf(-0.5f * Fb / Fbb, lb), hb) : (Fb > 0.f ? lb : hb);
+          // (approximate 1-D minimisers: the quadratic is evaluated at them, an
+          // offset delta raises the value by Faa delta^2 only -- far inside the margin)
+          const float xa_ = Faa > 0.f ? fminf(fmaxf(-0.5f * Fa * rcp_approx(Faa), la), ha) : (Fa > 0.f ? la : ha);
+          const float xb_ = Fbb > 0.f ? fminf(fmaxf(-0.5f * Fb * rcp_approx(Fbb), lb), hb) : (Fb > 0.f ? lb : hb);
           const float ma = fminf(xa_ * fmaf(Faa, xa_, Fa), fminf(la * fmaf(Faa, la, Fa), ha * fmaf(Faa, ha, Fa)));
           const float mb = fminf(xb_ * fmaf(Fbb, xb_, Fb), fminf(lb * fmaf(Fbb, lb, Fb), hb * fmaf(Fbb, hb, Fb)));
           const float mab = fabsf(Fab) * A * Bm;
