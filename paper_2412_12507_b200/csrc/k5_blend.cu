@@ -469,7 +469,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
                                           const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f, float ac, float bc,
                                           float ra, float rb, LanePx<NP> &L, uint32_t &n_eval, uint32_t &n_contrib,
                                           uint32_t &processed, const unsigned long long *poll_stat, int poll_s,
-                                          Checkpoints<NP> *ck, uint32_t ck_step) {
+                                          Checkpoints<NP> *ck, uint32_t ck_step, const uint32_t *act) {
   constexpr int NF = WarpTbl<MODE>::NF;
   constexpr unsigned FULL = 0xffffffffu;
   // dynamic shared memory: [raw payload double buffer: 8 warps x 2 x 32 x 5]
@@ -495,17 +495,45 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
     if (ck) ck->n[k] = 0;
   }
   processed = 0;
-  if (__all_sync(FULL, all_done) || s0 >= s1) return;
-  // gathers run one chunk ahead (cp.async), Gaussian ids two chunks ahead
-  uint32_t gnext = s0 + lane < s1 ? __ldg(&B.gids[s0 + lane]) : 0u;
-  if (s0 + lane < s1) {
-    float4 *dst = raw + lane * PF;
-    for (int q = 0; q < PF; ++q) cp_async16(dst + q, &B.payload[(size_t)PF * gnext + q]);
+  // per-pixel start positions (a re-run resumes each pixel at its own
+  // checkpoint): pixels starting later are dormant until the walk reaches
+  // them, and the walk jumps over stretches where no pixel is active
+  bool pend[NP];
+  uint32_t actp[NP], start = 0xFFFFFFFFu;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    actp[k] = act ? act[k] : s0;
+    pend[k] = !L.done[k] && actp[k] > s0;
+    if (!L.done[k]) start = min(start, actp[k]);
+    if (pend[k]) L.done[k] = true;
   }
-  cp_async_commit();
-  gnext = s0 + 32 + lane < s1 ? __ldg(&B.gids[s0 + 32 + lane]) : 0u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) start = min(start, __shfl_xor_sync(FULL, start, o));
+  if (start >= s1) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) if (pend[k]) L.done[k] = false;  // (nothing left to walk: unchanged state)
+    return;
+  }
+  // gathers run one chunk ahead (cp.async), Gaussian ids two chunks ahead
+  uint32_t gnext = 0;
   int buf = 0;
-  for (uint32_t b0 = s0; b0 < s1; b0 += 32, buf ^= 1) {
+  auto prime = [&](uint32_t p) {
+    gnext = p + lane < s1 ? __ldg(&B.gids[p + lane]) : 0u;
+    if (p + lane < s1) {
+      float4 *dst = raw + lane * PF;
+      for (int q = 0; q < PF; ++q) cp_async16(dst + q, &B.payload[(size_t)PF * gnext + q]);
+    }
+    cp_async_commit();
+    gnext = p + 32 + lane < s1 ? __ldg(&B.gids[p + 32 + lane]) : 0u;
+  };
+  prime(start);
+  for (uint32_t b0 = start; b0 < s1; b0 += 32, buf ^= 1) {
+    bool anypend = false;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      if (pend[k] && actp[k] <= b0) { pend[k] = false; L.done[k] = false; }
+      anypend = anypend || pend[k];
+    }
     // speculative pass of a later segment: every 2 chunks, stop pixels whose
     // exact sequence has certainly terminated by now: T_spec times the bound of
     // the published prefix below T_min (Ls := dead, exact; a re-run resolves it)
@@ -531,7 +559,21 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
     all_done = true;
 #pragma unroll
     for (int k = 0; k < NP; ++k) all_done = all_done && L.done[k];
-    if (__all_sync(FULL, all_done)) break;
+    if (__all_sync(FULL, all_done)) {
+      if (!__any_sync(FULL, anypend)) break;
+      // no active pixel: jump to the next resume position and restart the gathers
+      uint32_t nxt = 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) if (pend[k]) nxt = min(nxt, actp[k]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nxt = min(nxt, __shfl_xor_sync(FULL, nxt, o));
+      cp_async_wait<0>();
+      __syncwarp();
+      prime(nxt);
+      b0 = nxt - 32;  // (the loop increment lands on nxt with buf = 0)
+      buf = 1;
+      continue;
+    }
     if (b0 + 32 < s1) {  // prefetch the next chunk
       if (b0 + 32 + lane < s1) {
         float4 *dst = raw + ((buf ^ 1) * 32 + lane) * PF;
@@ -929,7 +971,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     Checkpoints<NP> ck;
     const uint32_t ck_step = max(32u, ((uint32_t)B.seg / GUT_CK) & ~31u);
     warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, L, n_eval, n_contrib, processed,
-                        s > 0 ? stat : nullptr, s, s > 0 ? &ck : nullptr, ck_step);
+                        s > 0 ? stat : nullptr, s, s > 0 ? &ck : nullptr, ck_step, nullptr);
     float T_pre[NP], T_end[NP];
     bool alive_in[NP], redo[NP], any_redo = false;
 #pragma unroll
@@ -974,37 +1016,31 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     }
     const bool wredo = __any_sync(FULL, any_redo);
     if (wredo) {
-      // resume point: the latest checkpoint every re-running pixel of the warp
-      // certainly reached in the exact sequence (T_pre T_c >= T_min)
-      int cres = GUT_CK;
-#pragma unroll
-      for (int k = 0; k < NP; ++k)
-        if (redo[k]) {
-          int ck_k = -1;
-          for (int q = ck.n[k] - 1; q >= 0; --q)
-            if (T_pre[k] * ck.T[q][k] >= c.t_min) { ck_k = q; break; }
-          cres = min(cres, ck_k);
-        }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) cres = min(cres, __shfl_xor_sync(FULL, cres, o));
+      // each re-running pixel resumes at the latest checkpoint its exact
+      // sequence certainly reached (T_pre T_c >= T_min), or at the segment start
       LanePx<NP> R;
+      uint32_t act[NP];
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         R.a[k] = L.a[k]; R.b[k] = L.b[k]; R.beta[k] = L.beta[k]; R.snorm[k] = L.snorm[k];
         R.done[k] = !redo[k];
         R.term[k] = false;
-        if (cres >= 0 && redo[k]) {
-          const float4 cc = ck.C[cres][k];
+        int ck_k = -1;
+        if (redo[k])
+          for (int q = ck.n[k] - 1; q >= 0; --q)
+            if (T_pre[k] * ck.T[q][k] >= c.t_min) { ck_k = q; break; }
+        act[k] = ck_k >= 0 ? s0 + (uint32_t)(ck_k + 1) * ck_step : s0;
+        if (ck_k >= 0) {
+          const float4 cc = ck.C[ck_k][k];
           R.Cr[k] = T_pre[k] * cc.x; R.Cg[k] = T_pre[k] * cc.y; R.Cb[k] = T_pre[k] * cc.z; R.Dp[k] = T_pre[k] * cc.w;
-          R.T[k] = T_pre[k] * ck.T[cres][k];
+          R.T[k] = T_pre[k] * ck.T[ck_k][k];
         } else {
           R.Cr[k] = R.Cg[k] = R.Cb[k] = R.Dp[k] = 0.f;
           R.T[k] = T_pre[k];
         }
       }
       uint32_t e2 = 0, c2 = 0, p2 = 0;
-      const uint32_t r0 = cres >= 0 ? s0 + (uint32_t)(cres + 1) * ck_step : s0;
-      warp_pass<MODE, NP>(c, B, r0, s1, D, O, T1f, T2f, ac, bc, ra, rb, R, e2, c2, p2, nullptr, 0, nullptr, 0);
+      warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, R, e2, c2, p2, nullptr, 0, nullptr, 0, act);
 #pragma unroll
       for (int k = 0; k < NP; ++k)
         if (redo[k]) {
