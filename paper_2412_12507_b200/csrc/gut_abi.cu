@@ -55,7 +55,7 @@ struct gut_context {
   size_t cap_items = 0;
   bool lut_valid = false;
   double lut_key[20] = {};
-  int blend_seg = 2048, blend_window = 2;  // K5 segment length and speculation window (tools/seg_sweep.sh)
+  int blend_seg = 1536, blend_window = 2;  // K5 segment length and speculation window (tools/seg_sweep.sh)
   uint32_t epoch = 0;
   bool reserved = false;
   std::vector<std::array<cudaEvent_t, 7>> tsets;  // per-render stage events (timing = 1)
