@@ -570,12 +570,141 @@ static void load_gauss(const float *means, const float *rots, const float *scale
   if (proj) for (int a = 0; a < 3; ++a) g->rgb[a] = proj[i].rgb[a];
 }
 
+/* ----------------------------------------------------------------------
+ * O6' — per-ray hit order of "Ours (sorted)" (§4.3; reading R28).
+ * "storing the per-ray k-farthest hit particles (typically using k = 16) in a
+ * buffer.  The closest hits which cannot be stored in the buffer are
+ * incrementally alpha-blended until the transmittance of the blended part
+ * vanishes."  Hits (alpha >= alpha_min, tau_max > 0) arrive in the tile's
+ * global depth order (O4).  While at most k hits are pending they are stored;
+ * a further hit makes k + 1 pending hits and the closest of them (smallest
+ * tau_max, ties: earlier in the stream) is alpha-blended -- so the buffer
+ * always holds the k farthest pending hits.  At the end of the stream the
+ * buffer is blended near to far.  Blending is Eq. 5 with the termination rule
+ * R21 (a hit that would take T below T_min stops the ray unblended).
+ * k = -1: every hit blended in exact tau_max order (the order 3DGRT's tracer
+ * collects); k = 0: stream order (= O6, "Ours").
+ * ---------------------------------------------------------------------- */
+typedef struct { double tau, alpha, rgb[3]; int32_t pos; } orc_hit;
+
+static int dbl_cmp(const void *a, const void *b) {
+  double x = *(const double *)a, y = *(const double *)b;
+  return x < y ? -1 : (x > y);
+}
+
+static int hit_cmp(const void *a, const void *b) {
+  const orc_hit *x = (const orc_hit *)a, *y = (const orc_hit *)b;
+  if (x->tau != y->tau) return x->tau < y->tau ? -1 : 1;
+  return x->pos < y->pos ? -1 : (x->pos > y->pos);
+}
+
+/* Eq. 5 step for one hit; returns 1 if the ray terminates (hit not blended) */
+static int blend_hit(const orc_hit *h, double t_min, double C[3], double *T, double *D, double *min_term_gap) {
+  double Tn = *T * (1.0 - h->alpha);
+  double tg = fabs(Tn - t_min);
+  if (min_term_gap && tg < *min_term_gap) *min_term_gap = tg;
+  if (Tn < t_min) return 1;
+  for (int c = 0; c < 3; ++c) C[c] += h->alpha * *T * h->rgb[c];
+  *D += h->alpha * *T * h->tau;
+  *T = Tn;
+  return 0;
+}
+
+int32_t orc_kbuffer_blend(const double *tau, const double *alpha, const double *rgb, int32_t n, int32_t k,
+                          double t_min, double C[3], double *T_out, double *D_out, int32_t *n_blended,
+                          double *min_term_gap) {
+  double T = 1.0, D = 0.0;
+  int32_t nb = 0, consumed = n, dead = 0;
+  C[0] = C[1] = C[2] = 0.0;
+  orc_hit *buf = (orc_hit *)malloc(sizeof(orc_hit) * (size_t)(n > 0 ? n : 1));
+  int32_t m = 0;
+  for (int32_t i = 0; i < n && !dead; ++i) {
+    orc_hit h = {tau[i], alpha[i], {rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]}, i};
+    if (k == 0) {                       /* stream order */
+      dead = blend_hit(&h, t_min, C, &T, &D, min_term_gap);
+      if (dead) consumed = i + 1; else ++nb;
+      continue;
+    }
+    buf[m++] = h;
+    if (k > 0 && m > k) {               /* k + 1 pending: blend the closest */
+      int32_t j = 0;
+      for (int32_t q = 1; q < m; ++q) if (hit_cmp(&buf[q], &buf[j]) < 0) j = q;
+      orc_hit c = buf[j];
+      buf[j] = buf[--m];
+      dead = blend_hit(&c, t_min, C, &T, &D, min_term_gap);
+      if (dead) consumed = i + 1; else ++nb;
+    }
+  }
+  if (!dead && k != 0) {                /* end of stream: the pending hits near to far */
+    qsort(buf, (size_t)m, sizeof(orc_hit), hit_cmp);
+    for (int32_t j = 0; j < m; ++j) {
+      if (blend_hit(&buf[j], t_min, C, &T, &D, min_term_gap)) break;
+      ++nb;
+    }
+  }
+  free(buf);
+  *T_out = T;
+  *D_out = D;
+  if (n_blended) *n_blended = nb;
+  return consumed;
+}
+
+/* one pixel of "Ours (sorted)": the hit stream of the tile list, then O6' */
+static void composite_pixel_sorted(const orc_gauss *G, const int32_t *gids, int32_t a, int32_t b,
+                                   const double *depth_of, const double o[3], const double d[3],
+                                   const orc_options *opt, double C[3], double *T_out, double *Dp,
+                                   orc_pixdiag *dg) {
+  int32_t n = 0, cap = b > a ? b - a : 1;
+  double *tau = (double *)malloc(sizeof(double) * (size_t)cap);
+  double *al = (double *)malloc(sizeof(double) * (size_t)cap);
+  double *rgb = (double *)malloc(sizeof(double) * 3 * (size_t)cap);
+  double *dk = (double *)malloc(sizeof(double) * (size_t)cap);
+  for (int32_t k = a; k < b; ++k) {
+    const orc_gauss *g = &G[gids[k]];
+    double t, w2 = orc_max_response(g->mu, g->R, g->s, o, d, &t);
+    double x = g->sig * exp(-0.5 * w2);
+    if (x > opt->alpha_max) x = opt->alpha_max;
+    if (dg) {
+      dg->visited++;
+      double gap = fabs(x - opt->alpha_min);
+      if (gap < dg->min_alpha_gap) dg->min_alpha_gap = gap;
+    }
+    if (x < opt->alpha_min) continue;
+    if (!(t > 0.0)) continue;            /* reading R24 */
+    tau[n] = t; al[n] = x;
+    for (int c = 0; c < 3; ++c) rgb[3 * n + c] = g->rgb[c];
+    dk[n] = depth_of ? depth_of[gids[k]] : 0;
+    ++n;
+  }
+  int32_t nb = 0;
+  double tg = 1e300;
+  int32_t used = orc_kbuffer_blend(tau, al, rgb, n, opt->kbuffer, opt->t_min, C, T_out, Dp, &nb, &tg);
+  if (dg) {
+    dg->contributed = nb;
+    dg->terminated = nb < n;   /* every hit is blended unless the ray terminates */
+    if (tg < dg->min_term_gap) dg->min_term_gap = tg;
+    /* order ambiguity over the hits that reached the buffer: stream (depth key)
+     * neighbours and tau_max neighbours */
+    for (int32_t i = 1; i < used; ++i) {
+      double rg = fabs(dk[i] - dk[i - 1]) / fmax(dk[i], dk[i - 1]);
+      if (rg < dg->min_order_gap) dg->min_order_gap = rg;
+    }
+    qsort(tau, (size_t)used, sizeof(double), dbl_cmp);
+    for (int32_t i = 1; i < used; ++i) {
+      double rg = fabs(tau[i] - tau[i - 1]) / fmax(fabs(tau[i]), fabs(tau[i - 1]));
+      if (rg < dg->min_tau_gap) dg->min_tau_gap = rg;
+    }
+  }
+  free(tau); free(al); free(rgb); free(dk);
+}
+
 /* one pixel: Eq. 5 front to back with alpha_i = sigma_i rho_i(o + tau_max d)
  * (P:L121), alpha clamp / skip / termination per readings R20-R21 */
 static void composite_pixel(const orc_gauss *G, const int32_t *gids, int32_t a, int32_t b,
                             const double *depth_of, const double o[3], const double d[3],
                             const orc_options *opt, double C[3], double *T_out, double *Dp,
                             orc_pixdiag *dg) {
+  if (opt->kbuffer != 0) { composite_pixel_sorted(G, gids, a, b, depth_of, o, d, opt, C, T_out, Dp, dg); return; }
   double T = 1.0;
   C[0] = C[1] = C[2] = 0; *Dp = 0;
   double prev_depth = -1;
@@ -637,7 +766,7 @@ void orc_composite(const float *means, const float *rots, const float *scales, c
         int64_t pix = (int64_t)py * cam->width + px;
         orc_pixdiag dg;
         memset(&dg, 0, sizeof(dg));
-        dg.min_alpha_gap = dg.min_term_gap = dg.min_order_gap = 1e300;
+        dg.min_alpha_gap = dg.min_term_gap = dg.min_order_gap = dg.min_tau_gap = 1e300;
         double ro[3], rd[3], C[3], T, Dp;
         if (!orc_pixel_ray(cam, px + 0.5, py + 0.5, ro, rd)) {
           /* invalid pixel: RGB = bg, alpha = 0, depth = 0 (O5) */

@@ -43,7 +43,9 @@ typedef struct {
   double alpha_min, alpha_max, t_min, dilation, near_plane;
   double bg[3];
   int32_t tile_cull;      /* 0 AABB, 1 ellipse-tile */
-  int32_t pad;
+  int32_t kbuffer;        /* O6 hit order: 0 = the tile's global depth order ("Ours");
+                             k >= 1 = per-ray MLAB k-buffer ("Ours (sorted)");
+                             -1 = exact per-ray tau_max sort (the 3DGRT order) */
 } orc_options;
 
 /* cull reasons (0 = visible) */
@@ -74,6 +76,8 @@ typedef struct {
   double min_order_gap;    /* min relative depth gap between consecutive contributing entries */
   int32_t amb_bin;         /* a binning-ambiguous pair could change this pixel */
   int32_t amb_cull;        /* a cull-ambiguous Gaussian could change this pixel */
+  double min_tau_gap;      /* kbuffer != 0: min relative tau_max gap between two hits adjacent
+                              in tau order (an fp32 tau could swap them) */
 } orc_pixdiag;
 
 /* ---- O1 ---- */
@@ -101,6 +105,13 @@ int64_t orc_tile_lists(const orc_proj *proj, int64_t n, const orc_camera *cam, c
 /* ---- O5 ---- */
 int  orc_pixel_ray(const orc_camera *cam, double u, double v, double o[3], double d[3]);
 /* ---- O6 ---- */
+/* Per-ray re-ordering of one pixel's hit stream: hits in stream
+ * order (tau_max, alpha, rgb), k = kbuffer option (>= 1 MLAB k-buffer, -1
+ * exact tau sort, 0 stream order); Eq. 5 with the termination rule R21. */
+/* Returns the number of stream hits consumed before termination (n if none). */
+int32_t orc_kbuffer_blend(const double *tau, const double *alpha, const double *rgb, int32_t n, int32_t k,
+                          double t_min, double C[3], double *T_out, double *D_out, int32_t *n_blended,
+                          double *min_term_gap);
 double orc_max_response(const double mu[3], const double R[9], const double s[3], const double o[3],
                         const double d[3], double *tau);
 void orc_composite(const float *means, const float *rots, const float *scales, const float *opac,

@@ -47,7 +47,7 @@ class OrcOptions(C.Structure):
     _fields_ = [("ut_alpha", C.c_double), ("ut_beta", C.c_double), ("ut_kappa", C.c_double),
                 ("alpha_min", C.c_double), ("alpha_max", C.c_double), ("t_min", C.c_double),
                 ("dilation", C.c_double), ("near_plane", C.c_double), ("bg", C.c_double * 3),
-                ("tile_cull", C.c_int32), ("pad", C.c_int32)]
+                ("tile_cull", C.c_int32), ("kbuffer", C.c_int32)]
 
 
 class OrcProj(C.Structure):
@@ -61,7 +61,8 @@ class OrcProj(C.Structure):
 class OrcPixDiag(C.Structure):
     _fields_ = [("visited", C.c_int32), ("contributed", C.c_int32), ("terminated", C.c_int32),
                 ("invalid", C.c_int32), ("min_alpha_gap", C.c_double), ("min_term_gap", C.c_double),
-                ("min_order_gap", C.c_double), ("amb_bin", C.c_int32), ("amb_cull", C.c_int32)]
+                ("min_order_gap", C.c_double), ("amb_bin", C.c_int32), ("amb_cull", C.c_int32),
+                ("min_tau_gap", C.c_double)]
 
 
 PROJ_DTYPE = np.dtype([("reason", "<i4"), ("tiles", "<i4"), ("rect", "<i4", 4), ("cull_ambig", "<i4"),
@@ -70,7 +71,8 @@ PROJ_DTYPE = np.dtype([("reason", "<i4"), ("tiles", "<i4"), ("rect", "<i4", 4), 
                        ("hx", "<f8"), ("hy", "<f8"), ("depth", "<f8"), ("t0", "<f8"), ("rgb", "<f8", 3)])
 DIAG_DTYPE = np.dtype([("visited", "<i4"), ("contributed", "<i4"), ("terminated", "<i4"),
                        ("invalid", "<i4"), ("min_alpha_gap", "<f8"), ("min_term_gap", "<f8"),
-                       ("min_order_gap", "<f8"), ("amb_bin", "<i4"), ("amb_cull", "<i4")])
+                       ("min_order_gap", "<f8"), ("amb_bin", "<i4"), ("amb_cull", "<i4"),
+                       ("min_tau_gap", "<f8")])
 assert PROJ_DTYPE.itemsize == C.sizeof(OrcProj)
 assert DIAG_DTYPE.itemsize == C.sizeof(OrcPixDiag)
 
@@ -108,6 +110,8 @@ def lib():
         L.orc_mark_ambiguity.argtypes = [fp, fp, fp, fp, C.c_void_p, C.c_int64, C.POINTER(OrcCamera),
                                          C.POINTER(OrcOptions), C.c_double, ip, C.c_int32, C.c_void_p]
         L.orc_threads.restype = C.c_int
+        L.orc_kbuffer_blend.argtypes = [dp, dp, dp, C.c_int32, C.c_int32, C.c_double, dp, dp, dp, ip, dp]
+        L.orc_kbuffer_blend.restype = C.c_int32
         _lib = L
     return _lib
 
@@ -150,6 +154,7 @@ def options(opt) -> OrcOptions:
     for i in range(3):
         o.bg[i] = opt.background[i]
     o.tile_cull = int(opt.tile_cull)
+    o.kbuffer = int(getattr(opt, "kbuffer", 0))
     return o
 
 
@@ -264,6 +269,20 @@ def max_response(mu, R, s, o, d):
     tau = np.zeros(1)
     w2 = lib().orc_max_response(_dp(mu), _dp(R), _dp(s), _dp(o), _dp(d), _dp(tau))
     return float(w2), float(tau[0])
+
+
+def kbuffer_blend(tau, alpha, rgb, k, t_min):
+    """O6' on one hit stream: returns (C[3], T, D, n_blended,
+    n_consumed).  k >= 1 MLAB k-buffer, -1 exact tau sort, 0 stream order."""
+    tau = np.ascontiguousarray(tau, np.float64)
+    alpha = np.ascontiguousarray(alpha, np.float64)
+    rgb = np.ascontiguousarray(rgb, np.float64).reshape(-1)
+    n = tau.size
+    Cc, T, D, tg = np.zeros(3), np.zeros(1), np.zeros(1), np.full(1, 1e300)
+    nb = C.c_int32(0)
+    used = lib().orc_kbuffer_blend(_dp(tau), _dp(alpha), _dp(rgb), n, int(k), float(t_min), _dp(Cc), _dp(T),
+                                   _dp(D), C.byref(nb), _dp(tg))
+    return Cc, float(T[0]), float(D[0]), int(nb.value), int(used)
 
 
 def composite(scene, proj, gids, ranges, cam, opt, tile_subset=None):

@@ -1,0 +1,185 @@
+"""Pins for O6' — the per-ray hit order of "Ours (sorted)" (PAPER L205-212,
+§4.3: MLAB k-buffer; reading R28 in DESIGN.md):
+
+* hand-derived worked streams (tests/golden/kbuffer.json, alpha = 1/2 so each
+  blended hit's weight names its rank) for k = 0, 1, 2, -1 and a termination
+  inside the final flush;
+* k >= hits  ==  exact per-ray tau_max sort, where the sort is a numpy
+  argsort + a plain Eq. 5 loop written here (SPEC acceptance 5);
+* an independent MLAB simulation with a binary heap (heapq) on random streams;
+* full pipeline: k >= hits per pixel == k = -1 bit for bit; a scene whose
+  Gaussians are separated in depth (no per-ray inversions) gives identical
+  images for k = 16 and k = 0; conservation rgb == alpha when every
+  colour is 1; mean error vs the exact sort non-increasing in k.
+"""
+import heapq
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import scenegen as S
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_kbuffer_golden(orc):
+    g = json.load(open(os.path.join(GOLD, "kbuffer.json")))
+    for c in g["cases"]:
+        Cc, T, D, nb, used = orc.kbuffer_blend(c["tau"], c["alpha"], c["rgb"], c["k"], c.get("t_min", 1e-4))
+        assert Cc == pytest.approx(c["C"], abs=1e-15), c["_why"]
+        assert T == pytest.approx(c["T"], abs=1e-15), c["_why"]
+        assert D == pytest.approx(c["D"], abs=1e-15), c["_why"]
+
+
+def _exact_sorted(tau, alpha, rgb, t_min):
+    """Eq. 5 over the hits sorted by tau (ties: stream position), R21 stop."""
+    order = np.argsort(np.asarray(tau), kind="stable")
+    Cc, T, D = np.zeros(3), 1.0, 0.0
+    for i in order:
+        Tn = T * (1.0 - alpha[i])
+        if Tn < t_min:
+            break
+        Cc += alpha[i] * T * rgb[i]
+        D += alpha[i] * T * tau[i]
+        T = Tn
+    return Cc, T, D
+
+
+def _mlab_heap(tau, alpha, rgb, k, t_min):
+    """The §4.3 text with a min-heap of pending hits keyed (tau, position)."""
+    heap, Cc, T, D = [], np.zeros(3), 1.0, 0.0
+
+    def blend(i):
+        nonlocal T, D
+        Tn = T * (1.0 - alpha[i])
+        if Tn < t_min:
+            return True
+        Cc[:] += alpha[i] * T * rgb[i]
+        D += alpha[i] * T * tau[i]
+        T = Tn
+        return False
+
+    for i in range(len(tau)):
+        heapq.heappush(heap, (tau[i], i))
+        if len(heap) > k:
+            if blend(heapq.heappop(heap)[1]):
+                return Cc, T, D
+    while heap:
+        if blend(heapq.heappop(heap)[1]):
+            break
+    return Cc, T, D
+
+
+def _random_stream(rng, n):
+    # depth-ordered stream with local inversions (what a tile's global order gives)
+    base = np.sort(rng.uniform(1, 10, n))
+    tau = base + rng.normal(0, 0.4, n)
+    tau = np.where(tau > 0, tau, 0.01)
+    alpha = rng.uniform(1 / 255, 0.99, n) ** 2
+    rgb = rng.uniform(0, 1, (n, 3))
+    return tau, alpha, rgb
+
+
+def test_kbuffer_large_k_is_exact_sort(orc):
+    rng = np.random.default_rng(5)
+    for trial in range(200):
+        n = int(rng.integers(0, 40))
+        tau, alpha, rgb = _random_stream(rng, n)
+        t_min = 1e-4 if trial % 2 else 1e-9
+        ref = _exact_sorted(tau, alpha, rgb, t_min)
+        for k in (n, n + 3, -1):
+            if k == 0:
+                continue
+            Cc, T, D, nb, used = orc.kbuffer_blend(tau, alpha, rgb, k, t_min)
+            np.testing.assert_allclose(Cc, ref[0], rtol=0, atol=1e-13)
+            assert T == pytest.approx(ref[1], abs=1e-15) and D == pytest.approx(ref[2], abs=1e-12)
+
+
+def test_kbuffer_vs_heap_simulation(orc):
+    rng = np.random.default_rng(6)
+    for trial in range(300):
+        n = int(rng.integers(1, 60))
+        tau, alpha, rgb = _random_stream(rng, n)
+        k = int(rng.choice([1, 2, 3, 4, 8, 16]))
+        t_min = 1e-4
+        ref = _mlab_heap(tau, alpha, rgb, k, t_min)
+        Cc, T, D, nb, used = orc.kbuffer_blend(tau, alpha, rgb, k, t_min)
+        np.testing.assert_allclose(Cc, ref[0], rtol=0, atol=1e-14)
+        assert T == ref[1] and D == pytest.approx(ref[2], abs=1e-13)
+
+
+def test_kbuffer_k0_is_stream_order(orc):
+    rng = np.random.default_rng(7)
+    for _ in range(50):
+        tau, alpha, rgb = _random_stream(rng, 30)
+        Cc, T, D, nb, used = orc.kbuffer_blend(tau, alpha, rgb, 0, 1e-4)
+        ref = _exact_sorted(np.arange(30.0), alpha, rgb, 1e-4)  # stream order = sort by position
+        np.testing.assert_allclose(Cc, ref[0], atol=1e-14)
+        assert T == pytest.approx(ref[1], abs=1e-15)
+
+
+# ---------------------------------------------------------------- full pipeline
+def _opt(k, **kw):
+    return S.RenderOptions(kbuffer=k, **kw)
+
+
+@pytest.mark.parametrize("variant", ["pinhole", "fisheye", "rs"])
+def test_pipeline_large_k_equals_exact(orc, variant):
+    scene, cam = S.tiny(3, variant, n=64)
+    ex = orc.render(scene, cam, _opt(-1), ambiguity=False)
+    big = orc.render(scene, cam, _opt(4096), ambiguity=False)
+    assert int(ex["diag"]["visited"].max()) < 4096
+    assert np.array_equal(ex["rgb"], big["rgb"]) and np.array_equal(ex["alpha"], big["alpha"])
+    assert np.array_equal(ex["depth"], big["depth"])
+
+
+def test_pipeline_depth_separated_scene_order_free(orc):
+    """Gaussians whose hit intervals along every ray are disjoint in depth:
+    the tile order is already the per-ray order, so k = 16 == k = 0."""
+    rng = np.random.default_rng(8)
+    n = 24
+    z = 2.0 + np.arange(n, dtype=np.float64)
+    xy = rng.uniform(-0.3, 0.3, (n, 2))
+    means = np.column_stack([xy, z])
+    q = rng.standard_normal((n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    s = rng.uniform(0.01, 0.05, (n, 3))  # 3.33 sigma < 0.17 << the 1.0 spacing
+    sh = np.zeros((n, 1, 3))
+    sh[:, 0, :] = rng.uniform(-1.5, 1.5, (n, 3))
+    scene = S._pack(means, q, s, rng.uniform(0.3, 0.99, n), sh, 0)
+    _, cam = S.tiny(0, "pinhole", n=1)
+    a = orc.render(scene, cam, _opt(0), ambiguity=False)
+    b = orc.render(scene, cam, _opt(16), ambiguity=False)
+    c = orc.render(scene, cam, _opt(1), ambiguity=False)
+    assert a["alpha"].max() > 0.5
+    for x in (b, c):
+        assert np.array_equal(a["rgb"], x["rgb"]) and np.array_equal(a["alpha"], x["alpha"])
+        assert np.array_equal(a["depth"], x["depth"])
+
+
+@pytest.mark.parametrize("k", [1, 4, 16, -1])
+def test_pipeline_conservation(orc, k):
+    scene, cam = S.tiny(4, "pinhole", n=64)
+    scene.sh[:, 0, :] = (1.0 - 0.5) / 0.28209479177387814  # colour exactly 1 after SH + 0.5
+    o = orc.render(scene, cam, _opt(k), ambiguity=False)
+    np.testing.assert_allclose(o["rgb"], np.repeat(o["alpha"][..., None], 3, -1), atol=2e-7)
+    assert o["alpha"].min() >= 0 and o["alpha"].max() <= 1
+
+
+def test_pipeline_error_nonincreasing_in_k(orc):
+    """the k-buffer's error against the exact per-ray sort shrinks as
+    k grows (mean over pixels of 6 random overlapping scenes)."""
+    errs = {k: 0.0 for k in (0, 1, 2, 4, 8, 16)}
+    for seed in range(6):
+        scene, cam = S.tiny(10 + seed, "pinhole", n=160)
+        scene.scales[:] *= 2.0  # overlapping in depth -> per-ray inversions
+        ex = orc.render(scene, cam, _opt(-1), ambiguity=False)["rgb"]
+        for k in errs:
+            errs[k] += float(np.abs(orc.render(scene, cam, _opt(k), ambiguity=False)["rgb"] - ex).mean())
+    ks = sorted(errs)  # k = 0 (the global tile order) first
+    assert errs[1] > 0, "scenes have no per-ray inversions"
+    for a, b in zip(ks, ks[1:]):
+        assert errs[b] <= errs[a] * (1 + 1e-9), errs
