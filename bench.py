@@ -148,7 +148,7 @@ def load_traffic(stage):
     """dram read + write bytes per launch of the stage's kernel from the newest
     committed `ncu --set full` capture (profiles/*_traffic.json), or None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))  # by name: r1 < r1v2 < r1v3 < r2 ...)
     for f in reversed(files):
         try:
             d = json.load(open(f))
