@@ -117,6 +117,13 @@ typedef struct {
   int32_t tile_cull;                 /* 0 = AABB, 1 = ellipse-tile (default) */
   float background[3];               /* composited with the final T (R22) */
   int32_t timing;                    /* 1: record per-stage CUDA-event times (adds events) */
+  int32_t kbuffer;                   /* hit order of the compositing (reading R28):
+                                        0 = the tile's global depth order ("Ours", default);
+                                        k in {1, 2, 4, 8, 16} = "Ours (sorted)": a per-ray MLAB
+                                        k-buffer holding the k farthest pending hits by tau_max,
+                                        the closest of k + 1 pending hits alpha-blended, the rest
+                                        blended near to far at the end of the list (paper: k = 16).
+                                        Other values: GUT_E_INVALID_ARGUMENT. */
 } gut_options;
 
 /* Outputs, HWC: rgb [H][W][3], alpha [H][W] (= 1 - T_final), depth [H][W]

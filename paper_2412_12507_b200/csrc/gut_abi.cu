@@ -206,6 +206,8 @@ static gut_status build_cam(gut_context *ctx, const gut_camera *cam, const gut_o
   if (!(o->cov2d_dilation >= 0) || !(o->near_plane >= 0)) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.cov2d_dilation/near_plane");
   if (o->rs_max_iterations < 0 || !(o->rs_tolerance_px >= 0)) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.rs_*");
   if (o->tile_cull != 0 && o->tile_cull != 1) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.tile_cull");
+  if (!(o->kbuffer == 0 || o->kbuffer == 1 || o->kbuffer == 2 || o->kbuffer == 4 || o->kbuffer == 8 || o->kbuffer == 16))
+    return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.kbuffer (0, 1, 2, 4, 8 or 16)");
 
   memset(&c, 0, sizeof(c));
   c.model = cam->model; c.width = cam->width; c.height = cam->height; c.shutter = cam->shutter;
@@ -214,6 +216,7 @@ static gut_status build_cam(gut_context *ctx, const gut_camera *cam, const gut_o
   if ((int64_t)c.tiles_x * c.tiles_y > 65536) return fail(ctx, GUT_E_UNSUPPORTED, "camera: more than 65536 tiles");
   c.n_tiles = c.tiles_x * c.tiles_y;
   c.tile_cull = o->tile_cull;
+  c.kbuf = o->kbuffer;
   c.fx = cam->fx; c.fy = cam->fy; c.cx = cam->cx; c.cy = cam->cy;
   for (int i = 0; i < 6; ++i) { c.k[i] = cam->k[i]; c.kf[i] = (float)cam->k[i]; }
   c.p[0] = cam->p[0]; c.p[1] = cam->p[1];
@@ -522,12 +525,17 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
       ctx->lut_valid = cacheable;
     }
   }
-  const size_t max_items = (size_t)dc.n_tiles + ctx->cap_k / (size_t)ctx->blend_seg + 2;
+  // (k-buffer: one item per tile but twice the units per tile -> q1 needs 2 x n_tiles x GUT_BLEND_WARPS)
+  const size_t max_items = dc.kbuf > 0 ? 2 * (size_t)dc.n_tiles + 2
+                                       : (size_t)dc.n_tiles + ctx->cap_k / (size_t)ctx->blend_seg + 2;
   if ((s = ensure_items(ctx, max_items)) != GUT_OK) return s;
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->tile_work, 0, (size_t)dc.n_tiles * sizeof(uint2), st));
   const size_t n_units = (size_t)dc.n_tiles * GUT_BLEND_WARPS;
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->unit_ctr, 0, 3 * n_units * sizeof(uint32_t), st));
-  launch_plan(ctx->ranges, dc.n_tiles, ctx->blend_seg, ctx->blend_window, ctx->seg_base, ctx->q1, cnt, st);
+  if (dc.kbuf > 0)  // one segment per tile (the buffer state runs along the whole list), 8x4 units
+    launch_plan(ctx->ranges, dc.n_tiles, 1 << 30, 1, ctx->seg_base, ctx->q1, cnt, st, GUT_KBUF_UNITS);
+  else
+    launch_plan(ctx->ranges, dc.n_tiles, ctx->blend_seg, ctx->blend_window, ctx->seg_base, ctx->q1, cnt, st);
   // blend look-back epochs live in 22 bits: clear the status words on wrap
   uint32_t bepoch = ++ctx->epoch;
   if ((bepoch & 0x3FFFFFu) == 0) {
@@ -554,7 +562,8 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   }
   bb.epoch = bepoch;
   bb.rgb = rgb; bb.alpha = alpha; bb.depth = depth; bb.counters = cnt;
-  launch_blend(dc, bb, st);
+  if (dc.kbuf > 0) launch_blend_kbuf(dc, bb, st);
+  else launch_blend(dc, bb, st);
   if (timing) cudaEventRecord(ev[6], st);
   {
     cudaError_t e = cudaGetLastError();

@@ -8,6 +8,7 @@
 #define GUT_TILE_PX (GUT_TILE * GUT_TILE)  // pixels per tile (ray LUT, look-back status, partials)
 #define GUT_BLEND_NP 2  // K5 pixels per lane
 #define GUT_BLEND_WARPS (GUT_TILE_PX / (32 * GUT_BLEND_NP))  // K5 work units per tile (8x8 pixel blocks)
+#define GUT_KBUF_UNITS (GUT_TILE_PX / 32)  // K5 k-buffer variant: work units per tile (8x4 blocks, 1 pixel per lane)
 #ifndef GUT_BLEND_CTA
 #define GUT_BLEND_CTA 256  // K5 threads per CTA (independent warps; sized for the register budget)
 #endif
@@ -47,6 +48,7 @@ struct DevCam {
   float rs_tol_px;
   int rs_max_iter;
   float bg[3];
+  int kbuf;  // 0 = "Ours" (tile order); 1..16 = "Ours (sorted)" per-ray k-buffer size
 };
 
 // ---------------------------------------------------------------- small math

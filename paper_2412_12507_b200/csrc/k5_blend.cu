@@ -261,22 +261,22 @@ __device__ __forceinline__ uint32_t len_bucket(uint32_t len) {
 // scans both in place (8 contiguous tiles per thread), (c) per tile its
 // position in its bucket (warp-aggregated atomics) and the queue-1 entries.
 // The per-unit counters are zeroed by the host (memset) before the blend.
-__device__ __forceinline__ void tile_plan(const uint2 *ranges, int t, int seg, int window, uint32_t &S, uint32_t &g,
-                                          uint32_t &bk) {
+__device__ __forceinline__ void tile_plan(const uint2 *ranges, int t, int seg, int window, int upt, uint32_t &S,
+                                          uint32_t &g, uint32_t &bk) {
   const uint2 r = ranges[t];
   const uint32_t len = r.y > r.x ? r.y - r.x : 0;
   S = len == 0 ? 1 : (len + seg - 1) / seg;
-  g = min(S, (uint32_t)window) * GUT_BLEND_WARPS;
+  g = min(S, (uint32_t)window) * (uint32_t)upt;
   bk = len_bucket(len);
 }
 
 __global__ __launch_bounds__(256) void plan_count_kernel(const uint2 *__restrict__ ranges, int n_tiles, int seg,
-                                                         int window, uint32_t *__restrict__ seg_base,
+                                                         int window, int upt, uint32_t *__restrict__ seg_base,
                                                          uint32_t *counters) {
   const int t = blockIdx.x * 256 + threadIdx.x;
   uint32_t S = 0, g = 0, bk = 0xFFFFFFFFu;
   if (t < n_tiles) {
-    tile_plan(ranges, t, seg, window, S, g, bk);
+    tile_plan(ranges, t, seg, window, upt, S, g, bk);
     seg_base[t] = S;
   }
   const uint32_t peers = __match_any_sync(0xffffffffu, bk);
@@ -317,10 +317,11 @@ __global__ __launch_bounds__(1024) void plan_scan_kernel(int n_tiles, uint32_t *
 }
 
 __global__ __launch_bounds__(256) void plan_fill_kernel(const uint2 *__restrict__ ranges, int n_tiles, int seg,
-                                                        int window, uint32_t *__restrict__ q1, uint32_t *counters) {
+                                                        int window, int upt, uint32_t *__restrict__ q1,
+                                                        uint32_t *counters) {
   const int t = blockIdx.x * 256 + threadIdx.x, lane = threadIdx.x & 31;
   uint32_t S = 0, g = 0, bk = 0xFFFFFFFFu;
-  if (t < n_tiles) tile_plan(ranges, t, seg, window, S, g, bk);
+  if (t < n_tiles) tile_plan(ranges, t, seg, window, upt, S, g, bk);
   const uint32_t peers = __match_any_sync(0xffffffffu, bk);
   const int leader = __ffs(peers) - 1;
   // exclusive prefix of g among this lane's peers (g is the same for equal buckets
@@ -336,16 +337,16 @@ __global__ __launch_bounds__(256) void plan_fill_kernel(const uint2 *__restrict_
   if (t < n_tiles && lane == leader) pos = atomicAdd(&counters[CNT_PLAN_HIST + bk], gsum);
   pos = __shfl_sync(peers, pos, leader) + pre;
   // entry = unit | segment << 24 (a unit's first segments in order)
-  for (uint32_t k = 0; k < g; ++k)
-    q1[pos + k] = (GUT_BLEND_WARPS * (uint32_t)t + k % GUT_BLEND_WARPS) | ((k / GUT_BLEND_WARPS) << 24);
+  const uint32_t u = (uint32_t)upt;
+  for (uint32_t k = 0; k < g; ++k) q1[pos + k] = (u * (uint32_t)t + k % u) | ((k / u) << 24);
 }
 
 void launch_plan(const uint2 *ranges, int n_tiles, int seg, int window, uint32_t *seg_base, uint32_t *q1,
-                 uint32_t *counters, cudaStream_t st) {
+                 uint32_t *counters, cudaStream_t st, int upt) {
   const unsigned blocks = (unsigned)((n_tiles + 255) / 256);
-  plan_count_kernel<<<blocks, 256, 0, st>>>(ranges, n_tiles, seg, window, seg_base, counters);
+  plan_count_kernel<<<blocks, 256, 0, st>>>(ranges, n_tiles, seg, window, upt, seg_base, counters);
   plan_scan_kernel<<<1, 1024, 0, st>>>(n_tiles, seg_base, counters);
-  plan_fill_kernel<<<blocks, 256, 0, st>>>(ranges, n_tiles, seg, window, q1, counters);
+  plan_fill_kernel<<<blocks, 256, 0, st>>>(ranges, n_tiles, seg, window, upt, q1, counters);
 }
 
 // ---------------------------------------------------------------- blend
@@ -456,6 +457,57 @@ template <int NP> struct LanePx {
   bool done[NP], term[NP];
 };
 
+// "Ours (sorted)" (reading R28): the lane's per-ray MLAB
+// k-buffer -- the KB farthest pending hits (tau_max, alpha, Gaussian id),
+// ascending in tau; empty slots hold tau = -inf and sit at the bottom.
+template <int KB> struct KBuf {
+  float t[KB > 0 ? KB : 1], a[KB > 0 ? KB : 1];
+  uint32_t g[KB > 0 ? KB : 1];
+};
+
+// Eq. 5 step of one hit leaving the k-buffer (termination rule R21); the
+// colour is gathered from the K1 payload (rgb in the fifth float4).
+template <int NP>
+__device__ __forceinline__ void kb_blend(LanePx<NP> &L, int k, float tau, float al, uint32_t gid,
+                                         const float4 *__restrict__ payload, float t_min, uint32_t &n_contrib) {
+  const float Tn = L.T[k] * (1.f - al);
+  if (Tn < t_min) {
+    L.done[k] = true;
+    L.term[k] = true;
+    return;
+  }
+  const float4 cc = __ldg(&payload[(size_t)GUT_PAYLOAD_F4 * gid + 4]);
+  const float wgt = al * L.T[k];
+  L.Cr[k] = fmaf(wgt, cc.x, L.Cr[k]);
+  L.Cg[k] = fmaf(wgt, cc.y, L.Cg[k]);
+  L.Cb[k] = fmaf(wgt, cc.z, L.Cb[k]);
+  L.Dp[k] = fmaf(wgt, tau, L.Dp[k]);
+  L.T[k] = Tn;
+  ++n_contrib;
+}
+
+// A hit enters the k-buffer: of the KB + 1 pending hits the closest leaves
+// (register insertion chain, static indices only) and is blended.
+template <int KB, int NP>
+__device__ __forceinline__ void kb_insert(KBuf<KB> &kb, LanePx<NP> &L, int k, float tau, float al, uint32_t gid,
+                                          const float4 *__restrict__ payload, float t_min, uint32_t &n_contrib) {
+  const bool sw = tau < kb.t[0];
+  const float pt = sw ? tau : kb.t[0], pa = sw ? al : kb.a[0];
+  const uint32_t pg = sw ? gid : kb.g[0];
+  float mt = sw ? kb.t[0] : tau, ma = sw ? kb.a[0] : al;
+  uint32_t mg = sw ? kb.g[0] : gid;
+#pragma unroll
+  for (int i = 1; i < KB; ++i) {
+    const bool lo = mt < kb.t[i];
+    const float ti = kb.t[i], ai = kb.a[i];
+    const uint32_t gi = kb.g[i];
+    kb.t[i - 1] = lo ? mt : ti; kb.a[i - 1] = lo ? ma : ai; kb.g[i - 1] = lo ? mg : gi;
+    mt = lo ? ti : mt; ma = lo ? ai : ma; mg = lo ? gi : mg;
+  }
+  kb.t[KB - 1] = mt; kb.a[KB - 1] = ma; kb.g[KB - 1] = mg;
+  if (pt > -INFINITY) kb_blend<NP>(L, k, pt, pa, pg, payload, t_min, n_contrib);
+}
+
 // One pass of ONE WARP over the segment [s0, s1): no CTA barriers.  Each chunk
 // of 32 entries is staged by the 32 lanes (one entry each: fp64 for the
 // cancelling part), culled against the warp's pixel box in registers, and the
@@ -464,12 +516,13 @@ template <int NP> struct LanePx {
 // terminated.  Termination rule (reading R21): stop before an entry would take
 // T below T_min.  The caller sets L.a/b/beta/snorm, L.T (start), L.done
 // (= inactive) and L.term = false; the colour sums start at 0 here.
-template <int MODE, int NP>
+template <int MODE, int NP, int KB = 0>
 __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, uint32_t s0, uint32_t s1,
                                           const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f, float ac, float bc,
                                           float ra, float rb, LanePx<NP> &L, uint32_t &n_eval, uint32_t &n_contrib,
                                           uint32_t &processed, const unsigned long long *poll_stat, int poll_s,
-                                          Checkpoints<NP> *ck, uint32_t ck_step, const uint32_t *act) {
+                                          Checkpoints<NP> *ck, uint32_t ck_step, const uint32_t *act,
+                                          KBuf<KB> *kb = nullptr) {
   constexpr int NF = WarpTbl<MODE>::NF;
   constexpr unsigned FULL = 0xffffffffu;
   // dynamic shared memory: [raw payload double buffer: 8 warps x 2 x 32 x 5]
@@ -647,7 +700,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           t[3] = make_float4(e0.z, U.x, U.y, U.z);
           t[4] = make_float4(V.x, V.y, V.z, l2s);
           t[5] = make_float4(g0, gu, gv, 0.f);
-          t[6] = make_float4(p4.x, p4.y, p4.z, 0.f);
+          t[6] = make_float4(p4.x, p4.y, p4.z, KB > 0 ? __uint_as_float(__ldg(&B.gids[kk])) : 0.f);
           t[7] = make_float4(h.x, h.y, h.z, dot(m, e0));
           t[8] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
           t[9] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
@@ -699,7 +752,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
             t[2] = make_float4(D0, Da, Db, Daa);
             t[3] = make_float4(Dab, Dbb, gs, gu);
             t[4] = make_float4(gv, k2, l2s, 0.f);
-            t[5] = make_float4(p4.x, p4.y, p4.z, 0.f);
+            t[5] = make_float4(p4.x, p4.y, p4.z, KB > 0 ? __uint_as_float(__ldg(&B.gids[kk])) : 0.f);
           }
         }
       }
@@ -754,6 +807,10 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           const float tau = -gg * rD * L.snorm[k];
           const float Tn = L.T[k] * (1.f - al);
           const bool ok = hit[k] && al >= alpha_min && tau > 0.f;  // reading R24: tau > 0
+          if (KB > 0) {  // "Ours (sorted)": the hit enters the per-ray k-buffer
+            if (ok) kb_insert<KB, NP>(*kb, L, k, tau, al, __float_as_uint(cc.w), B.payload, t_min, n_contrib);
+            continue;
+          }
           const bool dead = ok && Tn < t_min;
           if (dead) { L.done[k] = true; L.term[k] = true; }
           if (ok && !dead) {
@@ -795,6 +852,10 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           const float tau = -gg * rD * L.snorm[k];
           const float Tn = L.T[k] * (1.f - al);
           const bool ok = hit[k] && al >= alpha_min && tau > 0.f;  // reading R24: tau > 0
+          if (KB > 0) {  // "Ours (sorted)": the hit enters the per-ray k-buffer
+            if (ok) kb_insert<KB, NP>(*kb, L, k, tau, al, __float_as_uint(cc.w), B.payload, t_min, n_contrib);
+            continue;
+          }
           const bool dead = ok && Tn < t_min;
           if (dead) { L.done[k] = true; L.term[k] = true; }
           if (ok && !dead) {
@@ -1200,6 +1261,162 @@ void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
   if (cam.model == CAM_ORTHO) blend_launch<1>(cam, b, st);
   else if (cam.shutter != SH_GLOBAL) blend_launch<2>(cam, b, st);
   else blend_launch<0>(cam, b, st);
+}
+
+// ---------------------------------------------------------------- "Ours (sorted)"
+// PAPER L205-212 (reading R28): per-ray MLAB k-buffer of KB hits.  The buffer
+// carries state along the whole list, so a ray's list cannot be split into
+// independently composited segments: the unit of work is one warp on one 8x4
+// pixel block (one pixel per lane, the buffer in registers) over its tile's
+// whole list, taken from queue 1 (tiles in decreasing list length).  The
+// staging, the two-stage warp cull and the per-pixel Eq. 11 evaluation are
+// those of the global-order kernel; an evaluated hit (alpha >= alpha_min,
+// tau_max > 0) enters the buffer and the closest of the KB + 1 pending hits
+// is blended; at the end of the list the buffer is blended near to far.
+template <int MODE, int KB>
+__global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kbuf_kernel(DevCam c, BlendBufs B) {
+  constexpr int NT = GUT_TILE_PX;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  uint32_t n_eval_acc = 0, n_contrib_acc = 0, n_term_acc = 0;
+  const uint32_t n_init = B.counters[CNT_Q_NINIT];
+  for (;;) {
+    uint32_t h = 0;
+    if (lane == 0) h = atomicAdd(&B.counters[CNT_Q_HEAD1], 1u);
+    h = __shfl_sync(FULL, h, 0);
+    if (h >= n_init) break;
+    const int unit = (int)(B.q1[h] & 0xFFFFFFu);
+    const int tile = unit / GUT_KBUF_UNITS, w = unit % GUT_KBUF_UNITS;
+    const uint2 rg = B.ranges[tile];
+    const uint32_t start = rg.y > rg.x ? rg.x : 0u, end = rg.y > rg.x ? rg.y : 0u;
+    int px, py;
+    tile_pixel(tile, c.tiles_x, w, lane, px, py);  // = rays_kernel's thread w * 32 + lane
+    const bool inside = px < c.width && py < c.height;
+    const float4 pl = B.pix[(size_t)tile * NT + w * 32 + lane];
+    LanePx<1> L;
+    L.a[0] = pl.x; L.b[0] = pl.y; L.snorm[0] = pl.z; L.beta[0] = pl.w;
+    const bool valid = inside && pl.z > 0.f;
+    float amin = valid ? pl.x : 3e38f, amax = valid ? pl.x : -3e38f;
+    float bmin = valid ? pl.y : 3e38f, bmax = valid ? pl.y : -3e38f;
+    const TileAnchor &A = B.anchors[tile];
+    d3 D, T1, T2, O;
+    if (MODE == 2) {
+      D = mkd(A.D[0], A.D[1], A.D[2]); T1 = mkd(A.T1[0], A.T1[1], A.T1[2]);
+      T2 = mkd(A.T2[0], A.T2[1], A.T2[2]); O = mkd(A.O[0], A.O[1], A.O[2]);
+    } else {
+      D = mv(c.R0, mkd(A.D[0], A.D[1], A.D[2]));
+      T1 = mv(c.R0, mkd(A.T1[0], A.T1[1], A.T1[2]));
+      T2 = mv(c.R0, mkd(A.T2[0], A.T2[1], A.T2[2]));
+      O = mkd(c.c0[0], c.c0[1], c.c0[2]);
+      if (MODE == 1) O = O + mv(c.R0, mkd(A.O[0], A.O[1], A.O[2]));
+    }
+    const f3 T1f = tof(T1), T2f = tof(T2);
+    float ac, bc, ra, rb;
+    {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        amin = fminf(amin, __shfl_xor_sync(FULL, amin, o));
+        amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, o));
+        bmin = fminf(bmin, __shfl_xor_sync(FULL, bmin, o));
+        bmax = fmaxf(bmax, __shfl_xor_sync(FULL, bmax, o));
+      }
+      if (amin > amax) { amin = amax = 0.f; bmin = bmax = 0.f; }
+      ac = 0.5f * (amin + amax);
+      bc = 0.5f * (bmin + bmax);
+      ra = 0.5f * (amax - amin) + 1e-7f * (fabsf(amin) + fabsf(amax));
+      rb = 0.5f * (bmax - bmin) + 1e-7f * (fabsf(bmin) + fabsf(bmax));
+    }
+    if (w == 0 && lane == 0 && end > start) atomicMax(&B.counters[CNT_MAXLEN], end - start);
+    L.done[0] = !valid;
+    L.term[0] = false;
+    L.T[0] = 1.f;
+    L.Cr[0] = L.Cg[0] = L.Cb[0] = L.Dp[0] = 0.f;
+    KBuf<KB> kb;
+#pragma unroll
+    for (int i = 0; i < KB; ++i) { kb.t[i] = -INFINITY; kb.a[i] = 0.f; kb.g[i] = 0u; }
+    uint32_t n_eval = 0, n_contrib = 0, processed = 0;
+    warp_pass<MODE, 1, KB>(c, B, start, end, D, O, T1f, T2f, ac, bc, ra, rb, L, n_eval, n_contrib, processed,
+                           nullptr, 0, nullptr, 0, nullptr, &kb);
+    // end of the list: the pending hits near to far (colours gathered up front)
+    if (!L.done[0]) {
+      float4 cc[KB];
+#pragma unroll
+      for (int i = 0; i < KB; ++i)
+        cc[i] = kb.t[i] > -INFINITY ? __ldg(&B.payload[(size_t)GUT_PAYLOAD_F4 * kb.g[i] + 4])
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < KB; ++i) {
+        if (L.done[0] || !(kb.t[i] > -INFINITY)) continue;
+        const float Tn = L.T[0] * (1.f - kb.a[i]);
+        if (Tn < c.t_min) { L.done[0] = L.term[0] = true; continue; }
+        const float wgt = kb.a[i] * L.T[0];
+        L.Cr[0] = fmaf(wgt, cc[i].x, L.Cr[0]);
+        L.Cg[0] = fmaf(wgt, cc[i].y, L.Cg[0]);
+        L.Cb[0] = fmaf(wgt, cc[i].z, L.Cb[0]);
+        L.Dp[0] = fmaf(wgt, kb.t[i], L.Dp[0]);
+        L.T[0] = Tn;
+        ++n_contrib;
+      }
+    }
+    n_eval_acc += n_eval;
+    n_contrib_acc += n_contrib;
+    n_term_acc += (valid && L.term[0]) ? 1u : 0u;
+    if (lane == 0) {
+      atomicAdd(&B.tile_work[tile].y, processed);
+      if (w == 0) B.tile_work[tile].x = end - start;
+    }
+    if (inside) {
+      const size_t p = (size_t)py * c.width + px;
+      const float Tf = valid ? L.T[0] : 1.f;
+      B.rgb[3 * p] = (valid ? L.Cr[0] : 0.f) + Tf * c.bg[0];
+      B.rgb[3 * p + 1] = (valid ? L.Cg[0] : 0.f) + Tf * c.bg[1];
+      B.rgb[3 * p + 2] = (valid ? L.Cb[0] : 0.f) + Tf * c.bg[2];
+      B.alpha[p] = 1.f - Tf;
+      if (B.depth) B.depth[p] = valid ? L.Dp[0] : 0.f;
+    }
+  }
+  const unsigned long long e1 = warp_sum((unsigned long long)n_eval_acc);
+  const unsigned long long e2 = warp_sum((unsigned long long)n_contrib_acc);
+  const unsigned long long e3 = warp_sum((unsigned long long)n_term_acc);
+  if (lane == 0 && (e1 | e2 | e3)) {
+    atomicAdd(reinterpret_cast<unsigned long long *>(&B.counters[CNT_PAIRS_EVAL]), e1);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&B.counters[CNT_PAIRS_CONTRIB]), e2);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&B.counters[CNT_TERMINATED]), e3);
+  }
+}
+
+template <int MODE, int KB>
+static void blend_kbuf_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
+  constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_CTA / 32) * 2 * 32 * GUT_PAYLOAD_F4 +
+                                            (GUT_BLEND_CTA / 32) * 32 * WarpTbl<MODE>::NF);
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(blend_kbuf_kernel<MODE, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, blend_kbuf_kernel<MODE, KB>, GUT_BLEND_CTA, smem);
+    grid = max(1, sms) * max(1, per);
+  }
+  blend_kbuf_kernel<MODE, KB><<<grid, GUT_BLEND_CTA, smem, st>>>(cam, b);
+}
+
+template <int KB>
+static void blend_kbuf_modes(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
+  if (cam.model == CAM_ORTHO) blend_kbuf_launch<1, KB>(cam, b, st);
+  else if (cam.shutter != SH_GLOBAL) blend_kbuf_launch<2, KB>(cam, b, st);
+  else blend_kbuf_launch<0, KB>(cam, b, st);
+}
+
+void launch_blend_kbuf(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
+  switch (cam.kbuf) {
+    case 1: blend_kbuf_modes<1>(cam, b, st); break;
+    case 2: blend_kbuf_modes<2>(cam, b, st); break;
+    case 4: blend_kbuf_modes<4>(cam, b, st); break;
+    case 8: blend_kbuf_modes<8>(cam, b, st); break;
+    case 16: blend_kbuf_modes<16>(cam, b, st); break;
+    default: break;  // validated by the ABI
+  }
 }
 
 }  // namespace gut

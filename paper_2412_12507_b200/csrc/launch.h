@@ -79,8 +79,9 @@ void launch_rays(const DevCam &cam, float4 *pix, TileAnchor *anchors, cudaStream
 // the first min(S_t, window) segment grants of every unit, longest tiles
 // first.  The per-unit counters (extra grants, next segment, completed) are
 // zeroed by the host before the blend.
+// upt = work units per tile (GUT_BLEND_WARPS 8x8 blocks; GUT_KBUF_UNITS 8x4 blocks for the k-buffer)
 void launch_plan(const uint2 *ranges, int n_tiles, int seg, int window, uint32_t *seg_base, uint32_t *q1,
-                 uint32_t *counters, cudaStream_t st);
+                 uint32_t *counters, cudaStream_t st, int upt = GUT_BLEND_WARPS);
 
 struct BlendBufs {
   const uint2 *ranges;
@@ -111,5 +112,8 @@ struct BlendBufs {
 #define GUT_BLEND_MAX_WAITERS 768u
 
 void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st);
+// "Ours (sorted)": per-ray MLAB k-buffer of cam.kbuf hits (1, 2, 4, 8, 16), queue 1
+// planned with GUT_KBUF_UNITS units per tile and one segment per tile
+void launch_blend_kbuf(const DevCam &cam, const BlendBufs &b, cudaStream_t st);
 
 }  // namespace gut
