@@ -5,7 +5,13 @@ composites the GPU's own sorted lists) and end to end, tiny variants, ragged
 images, reduced large configs, and the full-size bench frame on sampled tiles.
 
 Extra ambiguity band: two hits whose tau_max differ by less than TAU_BAND
-(relative) may swap places in the buffer (the GPU's tau is fp32)."""
+(relative) may swap places in the buffer.  The GPU's tau is fp32 from the
+tile-anchored quadratic forms (a few ulps, ~5e-7 relative); the
+band is 4x that.  A swap inside the band would change RGB by
+~T alpha_i alpha_j |c_i - c_j| >> 2e-4, so green strict pixels also confirm
+the band.  On pixels excluded only by the tau band the output alpha
+(= 1 - prod(1 - alpha_i), order-free unless the ray terminated) is still
+checked."""
 import dataclasses
 
 import numpy as np
@@ -16,7 +22,7 @@ from gpu_common import TOL_RGB, assert_images_close, gpu_lists, gpu_render, pixe
 
 pytestmark = pytest.mark.gpu
 
-TAU_BAND = 1e-5
+TAU_BAND = 2e-6
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -38,6 +44,18 @@ def _isolated(scene, cam, g, opt, max_excluded=0.01, label=""):
                                max_excluded=max_excluded)
 
 
+def _alpha_on_tau_band(g, o, sel=None):
+    """Pixels excluded only by the tau band, ray not terminated: alpha is order-free."""
+    d = o["diag"]
+    m = pixel_mask(d) & (d["min_tau_gap"] <= TAU_BAND) & (d["terminated"] == 0)
+    if sel is not None:
+        m &= sel
+    if m.any():
+        e = float(np.abs(g["alpha"] - o["alpha"])[m].max())
+        print(f"  tau-band pixels {int(m.sum())}: alpha {e:.2e}")
+        assert e <= TOL_RGB
+
+
 def _full(scene, cam, opt, max_excluded=0.01, label=""):
     from oracle import oracle as O
     g = gpu_render(scene, cam, opt)
@@ -45,6 +63,7 @@ def _full(scene, cam, opt, max_excluded=0.01, label=""):
     o = O.render(scene, cam, opt)
     m = pixel_mask(o["diag"]) & (o["diag"]["min_tau_gap"] > TAU_BAND)
     assert_images_close(g, o, m, f"kbuf e2e {label}", max_excluded=max_excluded)
+    _alpha_on_tau_band(g, o)
     T = 1 - g["alpha"]
     assert np.all(np.isfinite(g["rgb"])) and np.all(T >= 0) and np.all(T <= 1)
     return g, o
@@ -102,9 +121,12 @@ def test_full_size_sampled_tiles_kbuffer():
         x0, y0 = (t % tx) * 16, (t // tx) * 16
         mask[y0:y0 + 16, x0:x0 + 16] = True
     inband = mask.sum()
+    _alpha_on_tau_band(g, o, mask)
     mask &= pixel_mask(o["diag"]) & (o["diag"]["min_tau_gap"] > TAU_BAND)
+    # the 8 longest lists are the dense object cluster (~10^5 entries, hundreds of
+    # hits per ray): many pixels hold two hits within 2e-6 in tau
     print(f"full-size kbuf: strict pixels {mask.sum()} of {inband}")
-    assert mask.sum() > 0.85 * inband
+    assert mask.sum() > 0.6 * inband
     e_rgb = np.abs(g["rgb"] - o["rgb"]).max(-1)[mask].max()
     e_a = np.abs(g["alpha"] - o["alpha"])[mask].max()
     print(f"full-size sampled (k=16): rgb {e_rgb:.2e} alpha {e_a:.2e}")
