@@ -37,6 +37,19 @@ static void mtv3(const double M[9], const double v[3], double r[3]) {
   for (int i = 0; i < 3; ++i) r[i] = M[i] * v[0] + M[3 + i] * v[1] + M[6 + i] * v[2];
 }
 
+/* Supp. A, reading R29: generalized Gaussian of degree n,
+ * rho = exp(-(1/2) lambda_n d^n) with d^2 the Mahalanobis distance and
+ * lambda_n = r^2 / r^n, r = 3 (the response at d = r equals the Gaussian's
+ * exp(-r^2/2); n = 2 is the Gaussian, Eq. 1).  The printed formula omits the
+ * 1/2, which contradicts "the same kernel response at a given distance r as
+ * the reference Gaussian kernel"; we keep it (SPEC S:L59 reads the same). */
+double orc_kernel_lambda(int32_t n) { return pow(3.0, 2.0 - (double)n); }
+
+double orc_kernel_response(double d2, int32_t n) {
+  if (n == 2) return exp(-0.5 * d2);
+  return exp(-0.5 * orc_kernel_lambda(n) * pow(d2, 0.5 * (double)n));
+}
+
 int orc_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
@@ -377,7 +390,10 @@ static void preprocess_one(const float *means, const float *rots, const float *s
   double det = cxx * cyy - cxy * cxy;
   if (!(cxx > 0 && cyy > 0 && det > 0) || !isfinite(det)) { p->reason = ORC_CULL_COV; return; }
   /* O3.3-4: opacity-aware extent (Alg. 1 line 3; reading R11) */
+  /* alpha >= alpha_min  <=>  omega^2 <= k2 (Alg. 1 l.3); degree n
+   * kernel (Supp. A, reading R29): (1/2) lambda_n omega^n <= ln(sigma/alpha_min) */
   p->k2 = 2.0 * log(sig / o->alpha_min);
+  if (o->kernel_degree != 2) p->k2 = pow(p->k2 / orc_kernel_lambda(o->kernel_degree), 2.0 / o->kernel_degree);
   p->hx = sqrt(p->k2 * cxx);
   p->hy = sqrt(p->k2 * cyy);
   /* O3.5: rectangle (Alg. 1 line 5) clamped to the tile grid */
@@ -662,7 +678,7 @@ static void composite_pixel_sorted(const orc_gauss *G, const int32_t *gids, int3
   for (int32_t k = a; k < b; ++k) {
     const orc_gauss *g = &G[gids[k]];
     double t, w2 = orc_max_response(g->mu, g->R, g->s, o, d, &t);
-    double x = g->sig * exp(-0.5 * w2);
+    double x = g->sig * orc_kernel_response(w2, opt->kernel_degree);
     if (x > opt->alpha_max) x = opt->alpha_max;
     if (dg) {
       dg->visited++;
@@ -711,7 +727,7 @@ static void composite_pixel(const orc_gauss *G, const int32_t *gids, int32_t a, 
   for (int32_t k = a; k < b; ++k) {
     const orc_gauss *g = &G[gids[k]];
     double tau, w2 = orc_max_response(g->mu, g->R, g->s, o, d, &tau);
-    double al = g->sig * exp(-0.5 * w2);
+    double al = g->sig * orc_kernel_response(w2, opt->kernel_degree);
     if (al > opt->alpha_max) al = opt->alpha_max;
     if (dg) {
       dg->visited++;
@@ -870,7 +886,7 @@ void orc_mark_ambiguity(const float *means, const float *rots, const float *scal
             double ro[3], rd[3], tau;
             if (!orc_pixel_ray(cam, px + 0.5, py + 0.5, ro, rd)) continue;
             double w2 = orc_max_response(g.mu, g.R, g.s, ro, rd, &tau);
-            double al = g.sig * exp(-0.5 * w2);
+            double al = g.sig * orc_kernel_response(w2, o->kernel_degree);
             if (al >= o->alpha_min - alpha_eps) {
               if (is_cull) diag[(int64_t)py * cam->width + px].amb_cull = 1;
               else diag[(int64_t)py * cam->width + px].amb_bin = 1;

@@ -46,6 +46,8 @@ typedef struct {
   int32_t kbuffer;        /* O6 hit order: 0 = the tile's global depth order ("Ours");
                              k >= 1 = per-ray MLAB k-buffer ("Ours (sorted)");
                              -1 = exact per-ray tau_max sort (the 3DGRT order) */
+  int32_t kernel_degree;  /* Supp. A generalized Gaussian degree n (2 = Gaussian, Eq. 1) */
+  int32_t pad;
 } orc_options;
 
 /* cull reasons (0 = visible) */
@@ -130,6 +132,9 @@ void orc_mark_ambiguity(const float *means, const float *rots, const float *scal
                         double alpha_eps, const int32_t *tile_subset, int32_t n_subset,
                         orc_pixdiag *diag);
 int  orc_threads(void);
+/* Supp. A: lambda_n = 3^(2-n); response exp(-lambda_n (d^2)^(n/2) / 2) (reading R29) */
+double orc_kernel_lambda(int32_t n);
+double orc_kernel_response(double d2, int32_t n);
 
 #ifdef __cplusplus
 }

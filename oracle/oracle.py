@@ -47,7 +47,8 @@ class OrcOptions(C.Structure):
     _fields_ = [("ut_alpha", C.c_double), ("ut_beta", C.c_double), ("ut_kappa", C.c_double),
                 ("alpha_min", C.c_double), ("alpha_max", C.c_double), ("t_min", C.c_double),
                 ("dilation", C.c_double), ("near_plane", C.c_double), ("bg", C.c_double * 3),
-                ("tile_cull", C.c_int32), ("kbuffer", C.c_int32)]
+                ("tile_cull", C.c_int32), ("kbuffer", C.c_int32),
+                ("kernel_degree", C.c_int32), ("pad", C.c_int32)]
 
 
 class OrcProj(C.Structure):
@@ -112,6 +113,10 @@ def lib():
         L.orc_threads.restype = C.c_int
         L.orc_kbuffer_blend.argtypes = [dp, dp, dp, C.c_int32, C.c_int32, C.c_double, dp, dp, dp, ip, dp]
         L.orc_kbuffer_blend.restype = C.c_int32
+        L.orc_kernel_lambda.argtypes = [C.c_int32]
+        L.orc_kernel_lambda.restype = C.c_double
+        L.orc_kernel_response.argtypes = [C.c_double, C.c_int32]
+        L.orc_kernel_response.restype = C.c_double
         _lib = L
     return _lib
 
@@ -155,6 +160,7 @@ def options(opt) -> OrcOptions:
         o.bg[i] = opt.background[i]
     o.tile_cull = int(opt.tile_cull)
     o.kbuffer = int(getattr(opt, "kbuffer", 0))
+    o.kernel_degree = int(getattr(opt, "kernel_degree", 2))
     return o
 
 
@@ -269,6 +275,15 @@ def max_response(mu, R, s, o, d):
     tau = np.zeros(1)
     w2 = lib().orc_max_response(_dp(mu), _dp(R), _dp(s), _dp(o), _dp(d), _dp(tau))
     return float(w2), float(tau[0])
+
+
+def kernel_response(d2, n):
+    """Supp. A generalized Gaussian response at Mahalanobis^2 distance d2."""
+    return float(lib().orc_kernel_response(float(d2), int(n)))
+
+
+def kernel_lambda(n):
+    return float(lib().orc_kernel_lambda(int(n)))
 
 
 def kbuffer_blend(tau, alpha, rgb, k, t_min):

@@ -76,6 +76,7 @@ class RenderOptions:
     rs_tolerance_px: float = float(np.float32(1e-4))
     tile_cull: int = 1             # 0 = AABB, 1 = ellipse-tile (StopThePop-style)
     kbuffer: int = 0               # 0 = "Ours" (tile depth order); k >= 1 = "Ours (sorted)" MLAB k-buffer
+    kernel_degree: int = 2         # Supp. A generalized Gaussian degree n (2 = Gaussian)
     background: Tuple[float, float, float] = (0.0, 0.0, 0.0)
 
 
