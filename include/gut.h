@@ -124,6 +124,11 @@ typedef struct {
                                         the closest of k + 1 pending hits alpha-blended, the rest
                                         blended near to far at the end of the list (paper: k = 16).
                                         Other values: GUT_E_INVALID_ARGUMENT. */
+  int32_t kernel_degree;             /* generalized Gaussian kernel of degree n (Supp. A, P:L458-462,
+                                        reading R29): rho = exp(-lambda_n d^n / 2), lambda_n = 3^(2-n),
+                                        d = Mahalanobis distance; 2 = the Gaussian (default); 1..8
+                                        accepted, else GUT_E_INVALID_ARGUMENT.  Changes the extent
+                                        level (Alg. 1) and the Eq. 11 response. */
 } gut_options;
 
 /* Outputs, HWC: rgb [H][W][3], alpha [H][W] (= 1 - T_final), depth [H][W]

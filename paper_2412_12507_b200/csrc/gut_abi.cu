@@ -208,6 +208,8 @@ static gut_status build_cam(gut_context *ctx, const gut_camera *cam, const gut_o
   if (o->tile_cull != 0 && o->tile_cull != 1) return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.tile_cull");
   if (!(o->kbuffer == 0 || o->kbuffer == 1 || o->kbuffer == 2 || o->kbuffer == 4 || o->kbuffer == 8 || o->kbuffer == 16))
     return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.kbuffer (0, 1, 2, 4, 8 or 16)");
+  if (o->kernel_degree < 1 || o->kernel_degree > 8)
+    return fail(ctx, GUT_E_INVALID_ARGUMENT, "options.kernel_degree (1..8)");
 
   memset(&c, 0, sizeof(c));
   c.model = cam->model; c.width = cam->width; c.height = cam->height; c.shutter = cam->shutter;
@@ -217,6 +219,8 @@ static gut_status build_cam(gut_context *ctx, const gut_camera *cam, const gut_o
   c.n_tiles = c.tiles_x * c.tiles_y;
   c.tile_cull = o->tile_cull;
   c.kbuf = o->kbuffer;
+  c.kdeg = o->kernel_degree;
+  c.klam = (float)pow(3.0, 2.0 - (double)o->kernel_degree);  // Supp. A: lambda_n = r^2 / r^n, r = 3
   c.fx = cam->fx; c.fy = cam->fy; c.cx = cam->cx; c.cy = cam->cy;
   for (int i = 0; i < 6; ++i) { c.k[i] = cam->k[i]; c.kf[i] = (float)cam->k[i]; }
   c.p[0] = cam->p[0]; c.p[1] = cam->p[1];
@@ -288,6 +292,7 @@ void gut_options_default(gut_options *o) {
   o->rs_max_iterations = 8;
   o->rs_tolerance_px = 1e-4f;
   o->tile_cull = 1;
+  o->kernel_degree = 2;
 }
 
 gut_status gut_context_create(int32_t dev, gut_context **out) {

@@ -49,6 +49,8 @@ struct DevCam {
   int rs_max_iter;
   float bg[3];
   int kbuf;  // 0 = "Ours" (tile order); 1..16 = "Ours (sorted)" per-ray k-buffer size
+  int kdeg;     // Supp. A generalized Gaussian degree n (2 = Gaussian)
+  float klam;   // lambda_n = 3^(2 - n)
 };
 
 // ---------------------------------------------------------------- small math

@@ -287,8 +287,17 @@ __device__ __forceinline__ uint32_t finish_gaussian(const DevCam &c, const Scene
                       R[0] * is0);
   pl[2] = make_float4(R[3] * is0, R[6] * is0, R[1] * is1, R[4] * is1);
   pl[3] = make_float4(R[7] * is1, R[2] * is2, R[5] * is2, R[8] * is2);
-  pl[4] = make_float4(rgb.x, rgb.y, rgb.z, 0.f);
+  pl[4] = make_float4(rgb.x, rgb.y, rgb.z, log2f(po.w));  // log2 sigma: K5's alpha for kernel degree != 2
   return __float_as_uint(depth);
+}
+
+// Opacity-aware extent level (Alg. 1 l.3): alpha >= alpha_min <=>
+// omega^2 <= k2, k2 = 2 ln(sigma / alpha_min) (via log1p: accurate when sigma is
+// near alpha_min); generalized kernel of degree n (Supp. A, reading R29):
+// (1/2) lambda_n omega^n <= ln(sigma / alpha_min) -> k2 = (k2_2 / lambda_n)^(2/n)
+__device__ __forceinline__ float extent_level(const DevCam &c, float sigma) {
+  const float k2 = 2.f * log1pf((sigma - c.alpha_min) / c.alpha_min);
+  return c.kdeg == 2 ? k2 : powf(k2 / c.klam, 2.f / (float)c.kdeg);
 }
 
 __device__ __forceinline__ bool load_gaussian(const DevCam &c, const SceneDev &s, int64_t i, float4 &po, float4 &sc,
@@ -412,7 +421,7 @@ __global__ __launch_bounds__(256, GUT_K1_CTAS) void project_kernel(DevCam c, Sce
       ok = cxx > 0.f && cyy > 0.f && det > 0.f && isfinite(det);
       // opacity-aware extent level (Alg. 1 l.3, reading R11)
       // k2 = 2 ln(sigma/alpha_min) via log1p: accurate when sigma is near alpha_min
-      k2 = 2.f * log1pf((po.w - c.alpha_min) / c.alpha_min);
+      k2 = extent_level(c, po.w);
       ok = ok && k2 > 0.f;
     }
     Ell e;
@@ -494,7 +503,7 @@ __global__ __launch_bounds__(256) void project_wide_kernel(DevCam c, SceneDev s,
         }
         e.cxx = sxx + c.dilation; e.cxy = sxy; e.cyy = syy + c.dilation;
         const double det = e.cxx * e.cyy - e.cxy * e.cxy;
-        const float k2f = 2.f * log1pf((po.w - c.alpha_min) / c.alpha_min);  // same value as the fp32 path / K5
+        const float k2f = extent_level(c, po.w);  // same value as the fp32 path / K5
         e.k2 = k2f;
         ok = e.cxx > 0 && e.cyy > 0 && det > 0 && isfinite(det) && k2f > 0.f;
         if (ok) {

@@ -421,6 +421,15 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// log2 of alpha / ... : log2 sigma - omega^2 / (2 ln 2) (Gaussian, Eq. 11 response);
+// degree n: log2 sigma - lambda_n (omega^2)^(n/2) / (2 ln 2) (MUFU lg2 / ex2)
+__device__ __forceinline__ float kernel_arg(bool gen, float kgl, float khn, float w2, float l2s) {
+  if (!gen) return fmaf(-0.72134752044448170f, w2, l2s);
+  float lw, p;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lw) : "f"(w2));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p) : "f"(khn * lw));
+  return fmaf(kgl, p, l2s);
+}
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
@@ -535,6 +544,9 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   const int lane = threadIdx.x & 31;
   const float alpha_min = c.alpha_min, alpha_max = c.alpha_max, t_min = c.t_min;
   const float l2amin = log2f(alpha_min);
+  // kernel degree n (Supp. A): log2 alpha = log2 sigma - lambda_n omega^n / (2 ln 2)
+  const bool gen = c.kdeg != 2;
+  const float kgl = -0.72134752044448170f * c.klam, khn = 0.5f * (float)c.kdeg;
   const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
   // raw payload of the warp's current / next chunk (cp.async double buffer)
   float4 *__restrict__ raw = s_dyn + (threadIdx.x >> 5) * 2 * 32 * PF;
@@ -673,7 +685,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
       }
       // k^2 = 2 ln(sigma/alpha_min) (K1, via log1p); log2 sigma = k^2 / (2 ln 2) + log2 alpha_min
       const float k2 = p1.z;
-      const float l2s = fmaf(k2, 0.72134752044448170f, l2amin);
+      const float l2s = c.kdeg == 2 ? fmaf(k2, 0.72134752044448170f, l2amin) : p4.w;  // (p4.w = log2 sigma from K1)
       // ---- conservative cull against the warp's pixel box (a in ac +- ra,
       // b in bc +- rb): |n| >= |n(ac,bc)| - ra|P| - rb|Q|, |e| <= |e(ac,bc)| +
       // ra|U| + rb|V| (triangle inequality); omega^2 > k^2 on the whole box if
@@ -803,7 +815,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           float gg = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
           gg = fmaf(beta, fmaf(a, pu.w, fmaf(b, qv.w, h.w)), gg);
           // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
-          const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, f4.w)));
+          const float al = fminf(alpha_max, ex2_approx(kernel_arg(gen, kgl, khn, w2, f4.w)));
           const float tau = -gg * rD * L.snorm[k];
           const float Tn = L.T[k] * (1.f - al);
           const bool ok = hit[k] && al >= alpha_min && tau > 0.f;  // reading R24: tau > 0
@@ -848,7 +860,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           const float w2 = fmaxf(fmaf(f4.y, Dd, F[k]), 0.f) * rD;
           const float gg = fmaf(da[k], f3v.w, fmaf(db[k], f4.x, f3v.z));
           // MUFU ex2 / rcp (rel. error < 2^-21): alpha = sigma exp(-omega^2 / 2)
-          const float al = fminf(alpha_max, ex2_approx(fmaf(-0.72134752044448170f, w2, f4.z)));
+          const float al = fminf(alpha_max, ex2_approx(kernel_arg(gen, kgl, khn, w2, f4.z)));
           const float tau = -gg * rD * L.snorm[k];
           const float Tn = L.T[k] * (1.f - al);
           const bool ok = hit[k] && al >= alpha_min && tau > 0.f;  // reading R24: tau > 0

@@ -42,7 +42,8 @@ class gut_options(C.Structure):
                 ("ut_kappa", C.c_float), ("alpha_min", C.c_float), ("alpha_max", C.c_float),
                 ("transmittance_min", C.c_float), ("cov2d_dilation", C.c_float), ("near_plane", C.c_float),
                 ("rs_max_iterations", C.c_int32), ("rs_tolerance_px", C.c_float), ("tile_cull", C.c_int32),
-                ("background", C.c_float * 3), ("timing", C.c_int32), ("kbuffer", C.c_int32)]
+                ("background", C.c_float * 3), ("timing", C.c_int32), ("kbuffer", C.c_int32),
+                ("kernel_degree", C.c_int32)]
 
 
 class gut_outputs(C.Structure):
@@ -154,6 +155,7 @@ def make_options(opt=None, timing: bool = False) -> gut_options:
         for i in range(3):
             o.background[i] = opt.background[i]
         o.kbuffer = int(getattr(opt, "kbuffer", 0))
+        o.kernel_degree = int(getattr(opt, "kernel_degree", 2))
     o.timing = int(timing)
     return o
 
