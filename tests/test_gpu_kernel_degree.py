@@ -20,7 +20,7 @@ def _cuda():
     build.build()
 
 
-@pytest.mark.parametrize("n", [1, 3, 4, 5, 8])
+@pytest.mark.parametrize("n", [3, 4, 5, 8])  # the degrees of Table 4
 @pytest.mark.parametrize("variant", S.TINY_VARIANTS)
 def test_tiny_degree(variant, n):
     scene, cam = S.tiny(2, variant, n=96)
