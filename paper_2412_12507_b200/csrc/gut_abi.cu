@@ -47,7 +47,7 @@ struct gut_context {
   // K5: ray LUT (cached per intrinsics for global shutter), blend work plan
   float4 *pix = nullptr;
   TileAnchor *anchors = nullptr;
-  uint32_t *seg_base = nullptr, *unit_ctr = nullptr;  // unit_ctr: 3 x n_units (extra grants, next_s, done)
+  uint32_t *seg_base = nullptr, *unit_ctr = nullptr;  // unit_ctr: 4 x n_units (extra grants, next_s, done, q1 taken)
   uint32_t *q1 = nullptr, *q2 = nullptr;  // blend work queues (k5_blend.cu)
   unsigned long long *bstatus = nullptr;
   float *part_t = nullptr;
@@ -137,7 +137,7 @@ static gut_status ensure_tiles(gut_context *ctx, size_t t) {
   CUDA_TRY(ctx, regrow(ctx->pix, dummy, t * GUT_TILE_PX));
   CUDA_TRY(ctx, regrow(ctx->anchors, dummy, t));
   CUDA_TRY(ctx, regrow(ctx->seg_base, dummy, t));
-  CUDA_TRY(ctx, regrow(ctx->unit_ctr, dummy, 3 * t * GUT_BLEND_WARPS));
+  CUDA_TRY(ctx, regrow(ctx->unit_ctr, dummy, 4 * t * GUT_BLEND_WARPS));
   ctx->lut_valid = false;
   ctx->cap_tiles = t;
   return GUT_OK;
@@ -536,7 +536,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   if ((s = ensure_items(ctx, max_items)) != GUT_OK) return s;
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->tile_work, 0, (size_t)dc.n_tiles * sizeof(uint2), st));
   const size_t n_units = (size_t)dc.n_tiles * GUT_BLEND_WARPS;
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->unit_ctr, 0, 3 * n_units * sizeof(uint32_t), st));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->unit_ctr, 0, 4 * n_units * sizeof(uint32_t), st));
   if (dc.kbuf > 0)  // one segment per tile (the buffer state runs along the whole list), 8x4 units
     launch_plan(ctx->ranges, dc.n_tiles, 1 << 30, 1, ctx->seg_base, ctx->q1, cnt, st, GUT_KBUF_UNITS);
   else
@@ -550,6 +550,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   BlendBufs bb;
   bb.ranges = ctx->ranges; bb.gids = fv; bb.payload = ctx->payload; bb.pix = ctx->pix; bb.anchors = ctx->anchors;
   bb.seg_base = ctx->seg_base; bb.granted = ctx->unit_ctr; bb.next_s = ctx->unit_ctr + n_units; bb.unit_done = ctx->unit_ctr + 2 * n_units;
+  bb.q1_taken = ctx->unit_ctr + 3 * n_units;
   bb.q1 = ctx->q1; bb.q2 = ctx->q2;
   bb.status = ctx->bstatus;
   bb.part_c = ctx->part_c; bb.part_t = ctx->part_t;

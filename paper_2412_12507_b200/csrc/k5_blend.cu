@@ -943,6 +943,7 @@ __device__ bool fetch_work(const BlendBufs &B, uint32_t n_init, int &unit, int &
       const uint32_t e = B.q1[h1];  // unit | segment << 24 (plan_fill_kernel)
       unit = (int)(e & 0xFFFFFFu);
       s = (int)(e >> 24);
+      atomicAdd(&B.q1_taken[unit], 1u);  // (successor grants wait for this: see the grant below)
       return true;
     }
   }
@@ -1167,7 +1168,14 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
       uint32_t nseg = 0;
       const uint32_t g0 = (uint32_t)min(S, B.window);
       if (lane == 0) {
-        if (tmax > 0.f) {
+        // Successors (queue 2, segments >= g0) are granted only once all of the
+        // unit's initial queue-1 segments have been taken by running warps: a
+        // successor's look-back then never waits on a segment still sitting in
+        // queue 1 (which, with queue 2 served first, could starve when few warps
+        // are resident, e.g. next to another frame's kernels).  A completion
+        // that sees an initial segment not yet taken skips granting: that
+        // segment's own completion sees every initial segment taken and grants.
+        if (tmax > 0.f && ld_volatile_u32(&B.q1_taken[unit]) >= g0) {
           // grant segments up to s + max(window, the depth the slowest pixel of
           // the block still needs at its decay so far) (queue 2)
           int ahead = B.window;

@@ -93,6 +93,7 @@ struct BlendBufs {
   uint32_t *granted;            // per unit (8 tile + warp block): grants beyond the first min(S, window)
   uint32_t *next_s;             // per unit: next segment index to hand out
   uint32_t *unit_done;          // per unit: segments completed
+  uint32_t *q1_taken;           // per unit: queue-1 (initial) segments taken by a warp
   const uint32_t *q1;           // queue 1: unit ids (initial grants, longest tiles first)
   uint32_t *q2;                 // queue 2: unit id + 1 per granted successor (0 = empty slot)
   unsigned long long *status;   // per (slot, pixel) look-back word (flag | epoch | -log2 T)
