@@ -897,3 +897,155 @@ void orc_mark_ambiguity(const float *means, const float *rots, const float *scal
   }
   free(in_sub);
 }
+
+/* ======================================================================
+ * O7 — backward pass of the compositing and the 3D response (Supp. B,
+ * P:L494-513; "avoids propagating gradients through the projection", P:L202:
+ * the UT / binning is not differentiated, reading R30).  Scalar loss
+ * L = sum_px g_rgb . rgb + g_alpha alpha + g_depth depth with the given
+ * per-pixel upstream gradients; "Ours" order (kbuffer = 0), degree-2 kernel.
+ * Plain fp64 chain rule, written out per hit:
+ *   Eq. 5: w_i = alpha_i T_i, C = sum w_i c_i, D = sum w_i tau_i, T_f = prod(1 - alpha_i)
+ *   dL/dc_i = w_i g_rgb;  dL/dtau_i = w_i g_depth
+ *   dL/dalpha_i = T_i (c_i.g_rgb + tau_i g_depth) - S_i / (1 - alpha_i),
+ *     S_i = sum_{j>i} w_j (c_j.g_rgb + tau_j g_depth) + T_f (bg.g_rgb - g_alpha)
+ *   alpha = min(alpha_max, sigma rho), rho = exp(-omega^2/2)  (clamped: no gradient)
+ *   Eq. 11 with o_g = M (o - mu), d_g = M d, M = S^-1 R^T, x_g = o_g + tau d_g:
+ *     d omega^2 / d o_g = 2 x_g,  d omega^2 / d d_g = 2 tau x_g,
+ *     d tau / d o_g = -d_g / |d_g|^2,  d tau / d d_g = -(x_g + tau d_g) / |d_g|^2
+ *   dL/dmu = -M^T dL/do_g;  dL/dM = dL/do_g (o - mu)^T + dL/dd_g d^T
+ *   M_ij = R_ji / s_i: dL/ds_i = -(1/s_i) sum_j dL/dM_ij M_ij, dL/dR_ji = dL/dM_ij / s_i
+ *   R(q^), q^ = q/|q| (Eq. 2): dL/dq = (I - q^ q^T) dL/dq^ / |q|
+ *   colour c = max(0, sum_k sh_k Y_k(dir) + 1/2) at the forward's direction
+ *   (reading R18, held constant): dL/dsh_k = dL/dc Y_k where c > 0.
+ * ====================================================================== */
+typedef struct { int32_t gid; double al, rho, T, tau, g; int clamped; } orc_bhit;
+
+int64_t orc_backward(const float *means, const float *rots, const float *scales, const float *opac,
+                     const float *sh, int32_t sh_degree, int64_t n, const orc_camera *cam,
+                     const orc_options *o, const float *g_rgb, const float *g_alpha, const float *g_depth,
+                     double *d_means, double *d_rots, double *d_scales, double *d_opac, double *d_sh,
+                     double *d_rgb, double *loss) {
+  int tx_n = (cam->width + TILE - 1) / TILE, ty_n = (cam->height + TILE - 1) / TILE, nt = tx_n * ty_n;
+  int nc = (sh_degree + 1) * (sh_degree + 1);
+  orc_proj *proj = (orc_proj *)malloc(sizeof(orc_proj) * (size_t)(n > 0 ? n : 1));
+  orc_preprocess(means, rots, scales, opac, sh, sh_degree, n, cam, o, proj);
+  int32_t *ranges = (int32_t *)calloc((size_t)nt * 2, sizeof(int32_t));
+  int64_t K = orc_tile_lists(proj, n, cam, o, means, scales, NULL, NULL, 0, NULL);
+  int32_t *tiles = (int32_t *)malloc(sizeof(int32_t) * (size_t)(K > 0 ? K : 1));
+  int32_t *gids = (int32_t *)malloc(sizeof(int32_t) * (size_t)(K > 0 ? K : 1));
+  orc_tile_lists(proj, n, cam, o, means, scales, tiles, gids, K, ranges);
+  orc_gauss *G = (orc_gauss *)malloc(sizeof(orc_gauss) * (size_t)(n > 0 ? n : 1));
+  double *gM = (double *)calloc((size_t)(n > 0 ? n : 1) * 9, sizeof(double));
+  for (int64_t i = 0; i < n; ++i) load_gauss(means, rots, scales, opac, proj, i, &G[i]);
+  memset(d_means, 0, sizeof(double) * 3 * (size_t)n); memset(d_rots, 0, sizeof(double) * 4 * (size_t)n);
+  memset(d_scales, 0, sizeof(double) * 3 * (size_t)n); memset(d_opac, 0, sizeof(double) * (size_t)n);
+  memset(d_sh, 0, sizeof(double) * 3 * (size_t)nc * (size_t)n); memset(d_rgb, 0, sizeof(double) * 3 * (size_t)n);
+  orc_bhit *hits = (orc_bhit *)malloc(sizeof(orc_bhit) * (size_t)(K > 0 ? K : 1));
+  double Lsum = 0.0;  /* the forward loss in fp64 (finite-difference pins) */
+  for (int t = 0; t < nt; ++t) {
+    int tx = t % tx_n, ty = t / tx_n;
+    for (int py = ty * TILE; py < ty * TILE + TILE && py < cam->height; ++py)
+      for (int px = tx * TILE; px < tx * TILE + TILE && px < cam->width; ++px) {
+        int64_t pix = (int64_t)py * cam->width + px;
+        double ro[3], rd[3];
+        if (!orc_pixel_ray(cam, px + 0.5, py + 0.5, ro, rd)) continue;
+        const double gc[3] = {g_rgb[3 * pix], g_rgb[3 * pix + 1], g_rgb[3 * pix + 2]};
+        const double ga = g_alpha[pix], gdp = g_depth[pix];
+        /* forward walk (= O6, kbuffer 0) recording the blended hits */
+        double T = 1.0;
+        int m = 0;
+        for (int32_t k = ranges[2 * t]; k < ranges[2 * t + 1]; ++k) {
+          const orc_gauss *g = &G[gids[k]];
+          double tau, w2 = orc_max_response(g->mu, g->R, g->s, ro, rd, &tau);
+          double rho = exp(-0.5 * w2), al = g->sig * rho;
+          int clamped = al > o->alpha_max;
+          if (clamped) al = o->alpha_max;
+          if (al < o->alpha_min || !(tau > 0.0)) continue;
+          double Tn = T * (1.0 - al);
+          if (Tn < o->t_min) break;
+          orc_bhit h = {gids[k], al, rho, T, tau, 0.0, clamped};
+          h.g = g->rgb[0] * gc[0] + g->rgb[1] * gc[1] + g->rgb[2] * gc[2] + tau * gdp;
+          hits[m++] = h;
+          T = Tn;
+        }
+        double S = T * (o->bg[0] * gc[0] + o->bg[1] * gc[1] + o->bg[2] * gc[2] - ga);
+        for (int q = 0; q < m; ++q) S += hits[q].al * hits[q].T * hits[q].g;
+        Lsum += S + ga;  /* = rgb.g_rgb + depth g_depth + alpha g_alpha (alpha = 1 - T_f) */
+        /* backward, front to back with the running suffix S_i */
+        for (int q = 0; q < m; ++q) {
+          const orc_bhit *h = &hits[q];
+          const orc_gauss *g = &G[h->gid];
+          const double w = h->al * h->T;
+          S -= w * h->g;                               /* S_i = sum over j > i (+ T_f term) */
+          const double dal = h->T * h->g - S / (1.0 - h->al);
+          for (int c = 0; c < 3; ++c) d_rgb[3 * h->gid + c] += w * gc[c];
+          const double dtau = w * gdp;
+          double dw2 = 0.0;
+          if (!h->clamped) {
+            d_opac[h->gid] += h->rho * dal;
+            dw2 = -0.5 * g->sig * h->rho * dal;
+          }
+          /* Eq. 11 chain */
+          double om[3] = {ro[0] - g->mu[0], ro[1] - g->mu[1], ro[2] - g->mu[2]}, og[3], dg[3];
+          mtv3(g->R, om, og);
+          mtv3(g->R, rd, dg);
+          for (int a = 0; a < 3; ++a) { og[a] /= g->s[a]; dg[a] /= g->s[a]; }
+          const double dd = dot3(dg, dg), tau = -dot3(og, dg) / dd;
+          double xg[3], go[3], gd[3];
+          for (int a = 0; a < 3; ++a) xg[a] = og[a] + tau * dg[a];
+          for (int a = 0; a < 3; ++a) {
+            go[a] = dw2 * 2.0 * xg[a] - dtau * dg[a] / dd;
+            gd[a] = dw2 * 2.0 * tau * xg[a] - dtau * (xg[a] + tau * dg[a]) / dd;
+          }
+          /* M = S^-1 R^T: M_ij = R_ji / s_i;  dL/dmu = -M^T go */
+          for (int j = 0; j < 3; ++j) {
+            double acc = 0;
+            for (int i = 0; i < 3; ++i) acc += (g->R[3 * j + i] / g->s[i]) * go[i];
+            d_means[3 * h->gid + j] -= acc;
+          }
+          for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) gM[9 * (size_t)h->gid + 3 * i + j] += go[i] * om[j] + gd[i] * rd[j];
+        }
+      }
+  }
+  /* per Gaussian: M -> (s, R) -> q; colour -> SH */
+  for (int64_t i = 0; i < n; ++i) {
+    const orc_gauss *g = &G[i];
+    const double *gm = &gM[9 * (size_t)i];
+    double gR[9];  /* dL/dR_ji = dL/dM_ij / s_i */
+    for (int a = 0; a < 3; ++a) {
+      double acc = 0;
+      for (int j = 0; j < 3; ++j) acc += gm[3 * a + j] * (g->R[3 * j + a] / g->s[a]);
+      d_scales[3 * i + a] = -acc / g->s[a];
+      for (int j = 0; j < 3; ++j) gR[3 * j + a] = gm[3 * a + j] / g->s[a];
+    }
+    double qn = sqrt((double)rots[4 * i] * rots[4 * i] + (double)rots[4 * i + 1] * rots[4 * i + 1] +
+                     (double)rots[4 * i + 2] * rots[4 * i + 2] + (double)rots[4 * i + 3] * rots[4 * i + 3]);
+    if (qn > 0) {
+      double w = rots[4 * i] / qn, x = rots[4 * i + 1] / qn, y = rots[4 * i + 2] / qn, z = rots[4 * i + 3] / qn;
+      const double dRw[9] = {0, -2 * z, 2 * y, 2 * z, 0, -2 * x, -2 * y, 2 * x, 0};
+      const double dRx[9] = {0, 2 * y, 2 * z, 2 * y, -4 * x, -2 * w, 2 * z, 2 * w, -4 * x};
+      const double dRy[9] = {-4 * y, 2 * x, 2 * w, 2 * x, 0, 2 * z, -2 * w, 2 * z, -4 * y};
+      const double dRz[9] = {-4 * z, -2 * w, 2 * x, 2 * w, -4 * z, 2 * y, 2 * x, 2 * y, 0};
+      double gq[4] = {0, 0, 0, 0};
+      for (int k = 0; k < 9; ++k) { gq[0] += gR[k] * dRw[k]; gq[1] += gR[k] * dRx[k]; gq[2] += gR[k] * dRy[k]; gq[3] += gR[k] * dRz[k]; }
+      const double qh[4] = {w, x, y, z}, pr = gq[0] * w + gq[1] * x + gq[2] * y + gq[3] * z;
+      for (int k = 0; k < 4; ++k) d_rots[4 * i + k] = (gq[k] - qh[k] * pr) / qn;
+    }
+    /* SH: the forward's direction (reading R18) and clamp */
+    if (proj[i].reason != ORC_OK) continue;
+    double Rc[9], cc[3], dd[3], Y[16];
+    orc_pose_at(cam, proj[i].t0, Rc, cc);
+    for (int a = 0; a < 3; ++a) dd[a] = g->mu[a] - cc[a];
+    double nd = sqrt(dot3(dd, dd)), dir[3] = {dd[0] / nd, dd[1] / nd, dd[2] / nd};
+    orc_sh_basis(dir, Y);
+    for (int ch = 0; ch < 3; ++ch) {
+      if (!(proj[i].rgb[ch] > 0)) continue;
+      for (int b = 0; b < nc; ++b) d_sh[(i * nc + b) * 3 + ch] = d_rgb[3 * i + ch] * Y[b];
+    }
+  }
+  free(hits); free(gM); free(G); free(gids); free(tiles); free(ranges); free(proj);
+  if (loss) *loss = Lsum;
+  return K;
+}

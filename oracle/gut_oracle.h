@@ -132,6 +132,15 @@ void orc_mark_ambiguity(const float *means, const float *rots, const float *scal
                         double alpha_eps, const int32_t *tile_subset, int32_t n_subset,
                         orc_pixdiag *diag);
 int  orc_threads(void);
+/* ---- O7 (backward, Supp. B; "Ours" order, degree 2, reading R30) ----
+ * upstream g_rgb [H][W][3], g_alpha [H][W], g_depth [H][W] (fp32);
+ * outputs (fp64): d_means [n][3], d_rots [n][4], d_scales [n][3], d_opac [n],
+ * d_sh [n][(d+1)^2][3], d_rgb [n][3] (gradient of the view's colour). Returns K. */
+int64_t orc_backward(const float *means, const float *rots, const float *scales, const float *opac,
+                     const float *sh, int32_t sh_degree, int64_t n, const orc_camera *cam,
+                     const orc_options *o, const float *g_rgb, const float *g_alpha, const float *g_depth,
+                     double *d_means, double *d_rots, double *d_scales, double *d_opac, double *d_sh,
+                     double *d_rgb, double *loss);
 /* Supp. A: lambda_n = 3^(2-n); response exp(-lambda_n (d^2)^(n/2) / 2) (reading R29) */
 double orc_kernel_lambda(int32_t n);
 double orc_kernel_response(double d2, int32_t n);

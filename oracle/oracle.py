@@ -113,6 +113,9 @@ def lib():
         L.orc_threads.restype = C.c_int
         L.orc_kbuffer_blend.argtypes = [dp, dp, dp, C.c_int32, C.c_int32, C.c_double, dp, dp, dp, ip, dp]
         L.orc_kbuffer_blend.restype = C.c_int32
+        L.orc_backward.argtypes = [fp, fp, fp, fp, fp, C.c_int32, C.c_int64, C.POINTER(OrcCamera),
+                                   C.POINTER(OrcOptions), fp, fp, fp, dp, dp, dp, dp, dp, dp, dp]
+        L.orc_backward.restype = C.c_int64
         L.orc_kernel_lambda.argtypes = [C.c_int32]
         L.orc_kernel_lambda.restype = C.c_double
         L.orc_kernel_response.argtypes = [C.c_double, C.c_int32]
@@ -342,6 +345,25 @@ def render(scene, cam, opt, brute=False, tile_subset=None, ambiguity=True, alpha
                                  C.byref(oo), float(alpha_eps), None if sub is None else _ip(sub),
                                  0 if sub is None else sub.size, diag.ctypes.data)
     return dict(rgb=rgb, alpha=alpha, depth=depth, diag=diag.reshape(H, W), proj=proj, n_keys=int(K.value))
+
+
+def backward(scene, cam, opt, g_rgb, g_alpha, g_depth):
+    """O7: gradients of L = sum(g_rgb rgb + g_alpha alpha + g_depth depth) with
+    respect to the scene parameters (fp64 dict)."""
+    m, r, s, o, sh = _scene_arrays(scene)
+    n, nc = scene.count, (scene.sh_degree + 1) ** 2
+    out = {k: np.zeros(sz) for k, sz in (("means", (n, 3)), ("rotations", (n, 4)), ("scales", (n, 3)),
+                                          ("opacities", (n,)), ("sh", (n, nc, 3)), ("rgb", (n, 3)))}
+    gr = np.ascontiguousarray(g_rgb, np.float32)
+    ga = np.ascontiguousarray(g_alpha, np.float32)
+    gd = np.ascontiguousarray(g_depth, np.float32)
+    oc, oo = camera(cam), options(opt)
+    loss = np.zeros(1)
+    lib().orc_backward(_fp(m), _fp(r), _fp(s), _fp(o), _fp(sh), scene.sh_degree, n, C.byref(oc), C.byref(oo),
+                       _fp(gr), _fp(ga), _fp(gd), _dp(out["means"]), _dp(out["rotations"]), _dp(out["scales"]),
+                       _dp(out["opacities"]), _dp(out["sh"]), _dp(out["rgb"]), _dp(loss))
+    out["loss"] = float(loss[0])
+    return out
 
 
 def threads() -> int:
