@@ -210,6 +210,37 @@ void gut_scene_destroy(gut_context *ctx, gut_scene *scene);
 gut_status gut_render(gut_context *ctx, const gut_scene *scene, const gut_camera *cam,
                       const gut_options *opt, const gut_outputs *out, gut_stream s, gut_stats *stats);
 
+/* Gradients of a scalar loss with respect to the scene (device buffers, fp32,
+ * written -- not accumulated -- by gut_render_backward). */
+typedef struct {
+  float *means;      /* [count][3] */
+  float *rotations;  /* [count][4] w.r.t. the raw (unnormalised) input quaternion */
+  float *scales;     /* [count][3] */
+  float *opacities;  /* [count] */
+  float *sh;         /* [count][(sh_degree+1)^2][3] */
+  float *rgb;        /* nullable: [count][3] gradient of the view's SH colour */
+} gut_gradients;
+
+/* Backward pass (PAPER Supp. B, L494-513; reading R30) of the LAST gut_render
+ * on this context, which must have been called with the same scene, camera
+ * and options and device outputs: L = sum over pixels of grad_rgb . rgb +
+ * grad_alpha alpha + grad_depth depth.  Gradients flow through the Eq. 5
+ * compositing and the Eq. 11 3D response to mu, q, s, sigma and (through the
+ * colour, view direction held constant) the SH coefficients; the UT
+ * projection and the binning are not differentiated.
+ * rgb/alpha/depth: the forward's device outputs ([H][W][3], [H][W], [H][W]);
+ * grad_rgb [H][W][3] required, grad_alpha / grad_depth nullable (zero); depth
+ * is required when grad_depth is given.  All pointers device memory on the
+ * context's device; asynchronous on s.  Per-Gaussian sums use fp32 atomics
+ * (reproducible to rounding, not bitwise).  Supported: global-shutter
+ * PINHOLE / OPENCV / FISHEYE, kbuffer 0, kernel_degree 2; otherwise
+ * GUT_E_UNSUPPORTED.  A camera / options mismatch with the last render:
+ * GUT_E_INVALID_ARGUMENT. */
+gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const gut_camera *cam,
+                               const gut_options *opt, const float *rgb, const float *alpha,
+                               const float *depth, const float *grad_rgb, const float *grad_alpha,
+                               const float *grad_depth, const gut_gradients *grads, gut_stream s);
+
 /* Renders n_views views in order (outs[i] for cams[i]); stats nullable [n_views]. */
 gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_camera *cams,
                             int32_t n_views, const gut_options *opt, const gut_outputs *outs,

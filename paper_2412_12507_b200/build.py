@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libgut.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["k1_project.cu", "k3_sort.cu", "k2_emit.cu", "k5_blend.cu", "gut_abi.cu"]
+SOURCES = ["k1_project.cu", "k3_sort.cu", "k2_emit.cu", "k5_blend.cu", "k6_backward.cu", "gut_abi.cu"]
 HEADERS = ["gut_internal.cuh", "launch.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -64,6 +64,10 @@ struct gut_context {
   int64_t last_n = 0;
   int last_tiles = 0;
   const uint32_t *last_order = nullptr, *last_keys = nullptr, *last_vals = nullptr;
+  DevCam last_cam;                    // (gut_render_backward: must match)
+  const gut_scene *last_scene = nullptr;
+  float *gacc = nullptr;              // K6 accumulators (16 per Gaussian)
+  size_t cap_gacc = 0;
 };
 
 static thread_local std::string g_err;
@@ -335,7 +339,7 @@ void gut_context_destroy(gut_context *ctx) {
                 ctx->sb_k, ctx->sb_v,
                 ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->tile_work, ctx->img, ctx->st_depth,
                 ctx->st_emit, ctx->st_tile, ctx->counters, ctx->pix, ctx->anchors, ctx->seg_base, ctx->unit_ctr, ctx->q1, ctx->q2,
-                ctx->bstatus, ctx->part_c, ctx->part_t, ctx->trace};
+                ctx->bstatus, ctx->part_c, ctx->part_t, ctx->trace, ctx->gacc};
   for (void *p : ps) if (p) cudaFree(p);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
   for (auto &set : ctx->tsets)
@@ -584,6 +588,8 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   ctx->last_n = N;
   ctx->last_tiles = dc.n_tiles;
   ctx->last_order = order;
+  ctx->last_cam = dc;
+  ctx->last_scene = scene;
   ctx->last_keys = fk;
   ctx->last_vals = fv;
   if (stats) {
@@ -617,6 +623,44 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
 gut_status gut_render(gut_context *ctx, const gut_scene *scene, const gut_camera *cam, const gut_options *opt,
                       const gut_outputs *out, gut_stream s, gut_stats *stats) {
   return render_one(ctx, scene, cam, opt, out, (cudaStream_t)s, stats);
+}
+
+gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const gut_camera *cam,
+                               const gut_options *opt, const float *rgb, const float *alpha, const float *depth,
+                               const float *grad_rgb, const float *grad_alpha, const float *grad_depth,
+                               const gut_gradients *grads, gut_stream s) {
+  if (!ctx) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "ctx: NULL");
+  if (!scene || !grads) return fail(ctx, GUT_E_INVALID_ARGUMENT, "scene / grads: NULL");
+  if (!rgb || !alpha || !grad_rgb) return fail(ctx, GUT_E_INVALID_ARGUMENT, "rgb / alpha / grad_rgb: NULL");
+  if (grad_depth && !depth) return fail(ctx, GUT_E_INVALID_ARGUMENT, "grad_depth needs the forward depth");
+  if (!grads->means || !grads->rotations || !grads->scales || !grads->opacities || !grads->sh)
+    return fail(ctx, GUT_E_INVALID_ARGUMENT, "grads: NULL buffer");
+  DevCam dc;
+  gut_status st_ = build_cam(ctx, cam, opt, dc);
+  if (st_ != GUT_OK) return st_;
+  if (dc.shutter != GUT_SHUTTER_GLOBAL || dc.model == CAM_ORTHO || dc.kbuf != 0 || dc.kdeg != 2)
+    return fail(ctx, GUT_E_UNSUPPORTED, "backward: global-shutter PINHOLE/OPENCV/FISHEYE, kbuffer 0, degree 2 only");
+  if (ctx->last_scene != scene || memcmp(&ctx->last_cam, &dc, sizeof(DevCam)) != 0)
+    return fail(ctx, GUT_E_INVALID_ARGUMENT, "backward: scene / camera / options differ from the last render");
+  cudaSetDevice(ctx->device);
+  const int64_t N = scene->d.n;
+  if (ctx->cap_gacc < (size_t)N) {
+    if (ctx->gacc) cudaFree(ctx->gacc);
+    ctx->gacc = nullptr;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->gacc, (size_t)16 * (N > 0 ? N : 1) * sizeof(float)));
+    ctx->cap_gacc = (size_t)N;
+  }
+  BwdBufs b;
+  b.ranges = ctx->ranges; b.gids = ctx->last_vals; b.payload = ctx->payload; b.pix = ctx->pix;
+  b.anchors = ctx->anchors; b.tiles = ctx->tiles;
+  b.rgb = rgb; b.alpha = alpha; b.depth = depth; b.g_rgb = grad_rgb; b.g_alpha = grad_alpha; b.g_depth = grad_depth;
+  b.acc = ctx->gacc;
+  b.d_means = grads->means; b.d_rots = grads->rotations; b.d_scales = grads->scales; b.d_opac = grads->opacities;
+  b.d_sh = grads->sh; b.d_rgb = grads->rgb;
+  launch_backward(dc, scene->d, b, (cudaStream_t)s);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, GUT_E_CUDA, std::string("backward launch: ") + cudaGetErrorString(e));
+  return GUT_OK;
 }
 
 gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_camera *cams, int32_t n_views,

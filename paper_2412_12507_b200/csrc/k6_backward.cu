@@ -1,0 +1,262 @@
+// k6_backward.cu — K6: backward pass of the compositing and the 3D response
+// (PAPER Supp. B, L494-513; reading R30: the UT / binning is not
+// differentiated; the colour's view direction is held constant).
+//
+// Scalar loss L = sum_px g_rgb.rgb + g_alpha alpha + g_depth depth.  Per pixel,
+// front to back over the tile's list (the forward's order and hit rules):
+//   w_i = alpha_i T_i,  g_i = c_i.g_rgb + tau_i g_depth,
+//   dL/dalpha_i = T_i g_i - S_i / (1 - alpha_i),  S_i = G - sum_{j<=i} w_j g_j,
+//   G = rgb.g_rgb + depth g_depth - T_f g_alpha  (from the forward's outputs),
+//   dL/dc_i = w_i g_rgb,  dL/dtau_i = w_i g_depth,
+//   alpha = min(alpha_max, sigma exp(-omega^2/2)).
+// Eq. 11 in canonical space with the pixel ray d' = D + a T1 + b T2 (tile
+// anchor, as in K5; tau_world = tau' |d'|), o_g = M (o - mu), d_g = M d',
+// n = o_g x d_g (the cofactor form, accurate), x_g = (d_g x n) / |d_g|^2:
+//   dL/do_g = 2 dL/domega^2 x_g - (dL/dtau' / |d_g|^2) d_g
+//   dL/dM   = dL/do_g (M^-1 x_g)^T - (dL/dtau' / |d_g|^2) x_g d'^T
+//   dL/dmu  = -M^T dL/do_g
+// (o - mu = M^-1 x_g - tau' d' removes the cancelling (o - mu) term).  Per
+// list entry the 32 lanes' contributions are summed with warp shuffles and
+// added to per-Gaussian fp32 accumulators with atomics (summation order not
+// fixed: results reproducible to fp32 rounding, not bitwise).  A per-Gaussian
+// kernel then maps dL/dM -> (s, R) -> q and dL/dc -> SH.
+#include "launch.h"
+
+namespace gut {
+
+namespace {
+
+constexpr int BW_NF = 10;  // float4 per staged entry
+
+__device__ __forceinline__ float ex2f_(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <class T>
+__device__ __forceinline__ T wsum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace
+
+// One CTA per tile, 8 warps = the tile's 8x4 pixel blocks (one pixel per lane,
+// rays_kernel's layout); every warp walks the whole list in chunks of 32.
+__global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
+  __shared__ float4 s_tbl[8][32 * BW_NF];
+  const int tile = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr unsigned FULL = 0xffffffffu;
+  float4 *tbl = s_tbl[w];
+  int px, py;
+  px = (tile % c.tiles_x) * GUT_TILE + (w & 1) * 8 + (lane & 7);
+  py = (tile / c.tiles_x) * GUT_TILE + (w >> 1) * 4 + (lane >> 3);
+  const bool inside = px < c.width && py < c.height;
+  const float4 pl = B.pix[(size_t)tile * GUT_TILE_PX + w * 32 + lane];
+  const float a = pl.x, b = pl.y, snorm = pl.z;
+  bool done = !(inside && snorm > 0.f);
+  // per-pixel upstream gradients and the forward's outputs
+  float gr = 0.f, gg = 0.f, gb = 0.f, gA = 0.f, gD = 0.f, Gtot = 0.f;
+  if (!done) {
+    const size_t p = (size_t)py * c.width + px;
+    gr = B.g_rgb[3 * p]; gg = B.g_rgb[3 * p + 1]; gb = B.g_rgb[3 * p + 2];
+    gA = B.g_alpha ? B.g_alpha[p] : 0.f;
+    gD = B.g_depth ? B.g_depth[p] : 0.f;
+    const float Tf = 1.f - B.alpha[p];
+    Gtot = B.rgb[3 * p] * gr + B.rgb[3 * p + 1] * gg + B.rgb[3 * p + 2] * gb + (B.depth ? B.depth[p] * gD : 0.f) -
+           Tf * gA;
+  }
+  // tile anchor (camera frame) -> world
+  const TileAnchor &A = B.anchors[tile];
+  const d3 D = mv(c.R0, mkd(A.D[0], A.D[1], A.D[2]));
+  const d3 T1 = mv(c.R0, mkd(A.T1[0], A.T1[1], A.T1[2]));
+  const d3 T2 = mv(c.R0, mkd(A.T2[0], A.T2[1], A.T2[2]));
+  const f3 Df = tof(D), T1f = tof(T1), T2f = tof(T2);
+  const f3 dpw = Df + a * T1f + b * T2f;  // d' (world, |d'| = snorm)
+  const uint2 rg = B.ranges[tile];
+  const uint32_t start = rg.y > rg.x ? rg.x : 0u, end = rg.y > rg.x ? rg.y : 0u;
+  const float l2amin = log2f(c.alpha_min);
+  float T = 1.f, Gpre = 0.f;
+  for (uint32_t b0 = start; b0 < end; b0 += 32) {
+    if (__all_sync(FULL, done)) break;
+    const uint32_t kk = b0 + lane;
+    __syncwarp();
+    if (kk < end) {
+      const uint32_t gid = B.gids[kk];
+      const float4 *src = B.payload + (size_t)GUT_PAYLOAD_F4 * gid;
+      const double2 wxy = *reinterpret_cast<const double2 *>(src);
+      const float4 p1 = src[1], p2 = src[2], p3 = src[3], p4 = src[4];
+      const d3 wv = mkd(wxy.x, wxy.y, __hiloint2double(__float_as_int(p1.y), __float_as_int(p1.x)));
+      const f3 x = tof(cross(wv, D));
+      const float M[9] = {p1.w, p2.x, p2.y, p2.z, p2.w, p3.x, p3.y, p3.z, p3.w};
+      const float rn0 = fmaf(M[0], M[0], fmaf(M[1], M[1], M[2] * M[2]));
+      const float rn1 = fmaf(M[3], M[3], fmaf(M[4], M[4], M[5] * M[5]));
+      const float rn2 = fmaf(M[6], M[6], fmaf(M[7], M[7], M[8] * M[8]));
+      const float r012 = rn0 * rn1 * rn2, dM = r012 * rsqrtf(r012);
+      const f3 Mx = mv(M, x);
+      const f3 c0 = mk(Mx.x * (dM / rn0), Mx.y * (dM / rn1), Mx.z * (dM / rn2));
+      const f3 ogf = mv(M, tof(wv)), e0 = mv(M, Df), U = mv(M, T1f), V = mv(M, T2f);
+      const f3 P = cross(ogf, U), Q = cross(ogf, V);
+      const float k2 = p1.z;
+      const float l2s = c.kdeg == 2 ? fmaf(k2, 0.72134752044448170f, l2amin) : p4.w;
+      float4 *t = tbl + lane * BW_NF;
+      t[0] = make_float4(c0.x, c0.y, c0.z, k2);
+      t[1] = make_float4(P.x, P.y, P.z, Q.x);
+      t[2] = make_float4(Q.y, Q.z, e0.x, e0.y);
+      t[3] = make_float4(e0.z, U.x, U.y, U.z);
+      t[4] = make_float4(V.x, V.y, V.z, l2s);
+      t[5] = make_float4(dot(ogf, e0), dot(ogf, U), dot(ogf, V), __uint_as_float(gid));
+      t[6] = make_float4(p4.x, p4.y, p4.z, 0.f);
+      // M^-1 = R S: (M^-1)_jk = M_kj / |M_k|^2
+      t[7] = make_float4(M[0] / rn0, M[3] / rn1, M[6] / rn2, M[1] / rn0);
+      t[8] = make_float4(M[4] / rn1, M[7] / rn2, M[2] / rn0, M[5] / rn1);
+      t[9] = make_float4(M[8] / rn2, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();
+    const int cnt = (int)min(32u, end - b0);
+    for (int j = 0; j < cnt; ++j) {
+      const float4 *t = tbl + j * BW_NF;
+      const float4 f0 = t[0], f1 = t[1], f2 = t[2], f3v = t[3], f4 = t[4];
+      const float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
+      const float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
+      const float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
+      const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
+      const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
+      const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
+      const float N = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
+      const float Dd = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
+      bool ok = !done && N <= f0.w * Dd;
+      if (!__any_sync(FULL, ok)) continue;
+      const float4 f5 = t[5], cc = t[6];
+      const float rD = 1.f / Dd;
+      const float w2 = N * rD;
+      const float raw = ex2f_(fmaf(-0.72134752044448170f, w2, f4.w));
+      const float al = fminf(c.alpha_max, raw);
+      const float gdot = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
+      const float taup = -gdot * rD, tau = taup * snorm;
+      ok = ok && al >= c.alpha_min && tau > 0.f;
+      float v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = 0.f;
+      if (ok) {
+        const float Tn = T * (1.f - al);
+        if (Tn < c.t_min) {
+          done = true;
+          ok = false;
+        } else {
+          const float wgt = al * T;
+          const float gi = cc.x * gr + cc.y * gg + cc.z * gb + tau * gD;
+          Gpre = fmaf(wgt, gi, Gpre);
+          const float dal = T * gi - (Gtot - Gpre) / (1.f - al);
+          const bool clamped = raw > c.alpha_max;
+          const float dw2 = clamped ? 0.f : -0.5f * raw * dal;
+          const float dtp = wgt * gD * snorm;  // dL/dtau'
+          // x_g = (d_g x n) / |d_g|^2
+          const float xgx = (ey * nz - ez * ny) * rD, xgy = (ez * nx - ex * nz) * rD, xgz = (ex * ny - ey * nx) * rD;
+          const float cg = dtp * rD;
+          const float gox = 2.f * dw2 * xgx - cg * ex, goy = 2.f * dw2 * xgy - cg * ey, goz = 2.f * dw2 * xgz - cg * ez;
+          const float4 m0 = t[7], m1 = t[8], m2 = t[9];
+          // y = M^-1 x_g
+          const float yx = m0.x * xgx + m0.y * xgy + m0.z * xgz;
+          const float yy = m0.w * xgx + m1.x * xgy + m1.y * xgz;
+          const float yz = m1.z * xgx + m1.w * xgy + m2.x * xgz;
+          v[0] = gox; v[1] = goy; v[2] = goz;
+          const float gx3[3] = {gox, goy, goz}, xg3[3] = {xgx, xgy, xgz}, y3[3] = {yx, yy, yz};
+          const float d3v[3] = {dpw.x, dpw.y, dpw.z};
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int s = 0; s < 3; ++s) v[3 + 3 * r + s] = gx3[r] * y3[s] - cg * xg3[r] * d3v[s];
+          v[12] = clamped ? 0.f : raw * ex2f_(-f4.w) * dal;  // rho = raw / sigma
+          v[13] = wgt * gr; v[14] = wgt * gg; v[15] = wgt * gb;
+          T = Tn;
+        }
+      }
+      if (!__any_sync(FULL, ok)) continue;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = wsum(v[q]);
+      if (lane == 0) {
+        float *acc = B.acc + (size_t)16 * __float_as_uint(f5.w);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) atomicAdd(acc + q, v[q]);
+      }
+    }
+  }
+}
+
+// Per Gaussian: dL/dmu = -M^T sum dL/do_g; dL/ds, dL/dq from dL/dM; dL/dsigma;
+// SH from the colour gradient at the forward's direction (clamped channels: 0).
+__global__ __launch_bounds__(256) void backward_finish_kernel(DevCam c, SceneDev s, BwdBufs B) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= s.n) return;
+  const int nc = (s.sh_degree + 1) * (s.sh_degree + 1);
+  float *gm = B.d_means + 3 * i, *gq = B.d_rots + 4 * i, *gs = B.d_scales + 3 * i, *gsh = B.d_sh + 3 * nc * i;
+  const bool vis = B.tiles[i] != 0;
+  float acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = vis ? B.acc[16 * i + q] : 0.f;
+  const float4 po = s.pos_opa[i], ro = s.rot[i], sc = s.scale[i];
+  const float qn = sqrtf(ro.x * ro.x + ro.y * ro.y + ro.z * ro.z + ro.w * ro.w);
+  const float qw = ro.x / qn, qx = ro.y / qn, qy = ro.z / qn, qz = ro.w / qn;
+  const float R[9] = {1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qw * qz), 2 * (qx * qz + qw * qy),
+                      2 * (qx * qy + qw * qz), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qw * qx),
+                      2 * (qx * qz - qw * qy), 2 * (qy * qz + qw * qx), 1 - 2 * (qx * qx + qy * qy)};
+  const float sv[3] = {sc.x, sc.y, sc.z};
+  float gR[9];
+  for (int j = 0; j < 3; ++j) {  // dL/dmu_j = -sum_i M_ij go_i, M_ij = R_ji / s_i
+    float m = 0.f;
+    for (int r = 0; r < 3; ++r) m += (R[3 * j + r] / sv[r]) * acc[r];
+    gm[j] = vis ? -m : 0.f;
+  }
+  for (int r = 0; r < 3; ++r) {
+    float t = 0.f;
+    for (int j = 0; j < 3; ++j) {
+      const float G = acc[3 + 3 * r + j];
+      t += G * (R[3 * j + r] / sv[r]);
+      gR[3 * j + r] = G / sv[r];
+    }
+    gs[r] = vis ? -t / sv[r] : 0.f;
+  }
+  const float dRw[9] = {0, -2 * qz, 2 * qy, 2 * qz, 0, -2 * qx, -2 * qy, 2 * qx, 0};
+  const float dRx[9] = {0, 2 * qy, 2 * qz, 2 * qy, -4 * qx, -2 * qw, 2 * qz, 2 * qw, -4 * qx};
+  const float dRy[9] = {-4 * qy, 2 * qx, 2 * qw, 2 * qx, 0, 2 * qz, -2 * qw, 2 * qz, -4 * qy};
+  const float dRz[9] = {-4 * qz, -2 * qw, 2 * qx, 2 * qw, -4 * qz, 2 * qy, 2 * qx, 2 * qy, 0};
+  float g4[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k = 0; k < 9; ++k) {
+    g4[0] += gR[k] * dRw[k]; g4[1] += gR[k] * dRx[k]; g4[2] += gR[k] * dRy[k]; g4[3] += gR[k] * dRz[k];
+  }
+  const float qh[4] = {qw, qx, qy, qz};
+  const float pr = g4[0] * qw + g4[1] * qx + g4[2] * qy + g4[3] * qz;
+  for (int k = 0; k < 4; ++k) gq[k] = vis ? (g4[k] - qh[k] * pr) / qn : 0.f;
+  B.d_opac[i] = acc[12];
+  if (B.d_rgb) { B.d_rgb[3 * i] = acc[13]; B.d_rgb[3 * i + 1] = acc[14]; B.d_rgb[3 * i + 2] = acc[15]; }
+  // SH (the forward's direction normalize(mu - c(0)); global shutter only)
+  const float4 col = vis ? B.payload[(size_t)GUT_PAYLOAD_F4 * i + 4] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const d3 dw = mkd(po.x, po.y, po.z) - mkd(c.c0[0], c.c0[1], c.c0[2]);
+  const f3 d = tof((1.0 / sqrt(dot(dw, dw))) * dw);
+  const float x = d.x, y = d.y, z = d.z, xx = x * x, yy = y * y, zz = z * z;
+  float Y[16];
+  Y[0] = 0.28209479177387814f;
+  Y[1] = -0.4886025119029199f * y; Y[2] = 0.4886025119029199f * z; Y[3] = -0.4886025119029199f * x;
+  Y[4] = 1.0925484305920792f * x * y; Y[5] = -1.0925484305920792f * y * z;
+  Y[6] = 0.31539156525252005f * (2.f * zz - xx - yy); Y[7] = -1.0925484305920792f * x * z;
+  Y[8] = 0.5462742152960396f * (xx - yy);
+  Y[9] = -0.5900435899266435f * y * (3.f * xx - yy); Y[10] = 2.890611442640554f * x * y * z;
+  Y[11] = -0.4570457994644658f * y * (4.f * zz - xx - yy);
+  Y[12] = 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+  Y[13] = -0.4570457994644658f * x * (4.f * zz - xx - yy); Y[14] = 1.445305721320277f * z * (xx - yy);
+  Y[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
+  const float gc[3] = {col.x > 0.f ? acc[13] : 0.f, col.y > 0.f ? acc[14] : 0.f, col.z > 0.f ? acc[15] : 0.f};
+  for (int k = 0; k < nc; ++k)
+    for (int ch = 0; ch < 3; ++ch) gsh[3 * k + ch] = gc[ch] * Y[k];
+}
+
+void launch_backward(const DevCam &cam, const SceneDev &s, const BwdBufs &b, cudaStream_t st) {
+  cudaMemsetAsync(b.acc, 0, (size_t)16 * s.n * sizeof(float), st);
+  if (cam.n_tiles > 0) backward_kernel<<<cam.n_tiles, 256, 0, st>>>(cam, b);
+  if (s.n > 0) backward_finish_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, st>>>(cam, s, b);
+}
+
+}  // namespace gut

@@ -117,4 +117,19 @@ void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st);
 // planned with GUT_KBUF_UNITS units per tile and one segment per tile
 void launch_blend_kbuf(const DevCam &cam, const BlendBufs &b, cudaStream_t st);
 
+// K6: backward of the last render (k6_backward.cu)
+struct BwdBufs {
+  const uint2 *ranges;
+  const uint32_t *gids;         // the forward's sorted Gaussian ids
+  const float4 *payload;        // K1 payload of the forward
+  const float4 *pix;
+  const TileAnchor *anchors;
+  const uint32_t *tiles;        // K1 tile code (0 = culled)
+  const float *rgb, *alpha, *depth;          // forward outputs (device)
+  const float *g_rgb, *g_alpha, *g_depth;    // upstream gradients (device; alpha / depth nullable)
+  float *acc;                   // per Gaussian 16 fp32 accumulators
+  float *d_means, *d_rots, *d_scales, *d_opac, *d_sh, *d_rgb;  // outputs (d_rgb nullable)
+};
+void launch_backward(const DevCam &cam, const SceneDev &s, const BwdBufs &b, cudaStream_t st);
+
 }  // namespace gut

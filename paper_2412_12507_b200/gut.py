@@ -68,9 +68,14 @@ class gut_proj_record(C.Structure):
                 ("rect", C.c_uint16 * 4)]
 
 
+class gut_gradients(C.Structure):
+    _fields_ = [("means", C.c_void_p), ("rotations", C.c_void_p), ("scales", C.c_void_p), ("opacities", C.c_void_p),
+                ("sh", C.c_void_p), ("rgb", C.c_void_p)]
+
+
 EXPORTS = ["gut_abi_version", "gut_options_default", "gut_context_create", "gut_context_destroy",
            "gut_last_error", "gut_workspace_reserve", "gut_scene_create", "gut_scene_destroy", "gut_render",
-           "gut_render_batch", "gut_timing_read", "gut_debug_copy_stage"]
+           "gut_render_batch", "gut_render_backward", "gut_timing_read", "gut_debug_copy_stage"]
 STAGE_NAMES = ["K1_project", "K3_sort_depth", "K2_emit", "K3_sort_tile", "K4_ranges", "K5_blend", "total"]
 
 _lib = None
@@ -105,9 +110,11 @@ def lib():
         L.gut_render_batch.argtypes = [vp, vp, C.POINTER(gut_camera), i32, C.POINTER(gut_options),
                                        C.POINTER(gut_outputs), vp, C.POINTER(gut_stats)]
         L.gut_debug_copy_stage.argtypes = [vp, i32, vp, C.c_size_t, C.POINTER(C.c_size_t)]
+        L.gut_render_backward.argtypes = [vp, vp, C.POINTER(gut_camera), C.POINTER(gut_options), vp, vp, vp, vp, vp,
+                                          vp, C.POINTER(gut_gradients), vp]
         L.gut_timing_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int32), i32]
         for name in ("gut_context_create", "gut_workspace_reserve", "gut_scene_create", "gut_render",
-                     "gut_render_batch", "gut_timing_read", "gut_debug_copy_stage"):
+                     "gut_render_batch", "gut_render_backward", "gut_timing_read", "gut_debug_copy_stage"):
             getattr(L, name).restype = C.c_int
         L.gut_options_default.restype = None
         L.gut_context_destroy.restype = None
@@ -226,6 +233,13 @@ def gut_render(ctx, scene, cam: gut_camera, opt: gut_options, out: gut_outputs, 
     return st
 
 
+def gut_render_backward(ctx, scene, cam: gut_camera, opt: gut_options, rgb, alpha, depth, grad_rgb, grad_alpha,
+                        grad_depth, grads: gut_gradients, stream=None):
+    """Backward of the last gut_render (device pointers as ints or None)."""
+    _check(lib().gut_render_backward(ctx, scene, C.byref(cam), C.byref(opt), rgb, alpha, depth, grad_rgb, grad_alpha,
+                                     grad_depth, C.byref(grads), _stream_ptr(stream)), ctx)
+
+
 def gut_render_batch(ctx, scene, cams: Sequence[gut_camera], opt: gut_options, outs: Sequence[gut_outputs],
                      stream=None, stats=False):
     n = len(cams)
@@ -277,6 +291,7 @@ class Renderer:
             gut_workspace_reserve(self.ctx, reserve_keys, scene.count, max_wh[0], max_wh[1])
         self.scene = gut_scene_create(self.ctx, scene.means, scene.rotations, scene.scales, scene.opacities,
                                       scene.sh, scene.sh_degree)
+        self.n, self.nc = scene.count, (scene.sh_degree + 1) ** 2
         torch.cuda.synchronize(device)
 
     def render(self, cam, opt=None, timing=False, stats=True, out=None):
@@ -289,6 +304,23 @@ class Renderer:
         o = gut_outputs(out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr() if out[2] is not None else None, 1, 0)
         st = gut_render(self.ctx, self.scene, make_camera(cam), make_options(opt, timing), o, stats=stats)
         return out[0], out[1], out[2], st
+
+    def backward(self, cam, opt, out, grad_rgb, grad_alpha=None, grad_depth=None, sh_shape=None):
+        """Gradients (torch tensors on the device) of sum(grad_rgb rgb + grad_alpha
+        alpha + grad_depth depth) for the last render(cam, opt) whose outputs
+        are `out` = (rgb, alpha, depth)."""
+        torch = self.torch
+        n = self.n
+        dev = torch.device("cuda", self.device)
+        g = {k: torch.empty(sz, device=dev) for k, sz in (("means", (n, 3)), ("rotations", (n, 4)), ("scales", (n, 3)),
+                                                           ("opacities", (n,)), ("sh", (n, self.nc, 3)),
+                                                           ("rgb", (n, 3)))}
+        gg = gut_gradients(*(g[k].data_ptr() for k in ("means", "rotations", "scales", "opacities", "sh", "rgb")))
+        p = lambda t: None if t is None else t.contiguous().data_ptr()  # noqa: E731
+        gut_render_backward(self.ctx, self.scene, make_camera(cam), make_options(opt), p(out[0]), p(out[1]),
+                            p(out[2]) if grad_depth is not None else p(out[2]), p(grad_rgb), p(grad_alpha),
+                            p(grad_depth), gg)
+        return g
 
     def stage(self, stage):
         return gut_debug_copy_stage(self.ctx, stage)

@@ -1,0 +1,101 @@
+"""GPU parity of the backward pass (K6, PAPER Supp. B; reading R30) through
+the C ABI against the fp64 oracle O7 on the same seeded inputs.  Upstream
+gradients are random; at pixels the oracle marks ambiguous (alpha-skip /
+termination bands, order ties, binning / cull ambiguity) they are set to 0
+on both sides, so both differentiate the same function.  Per-Gaussian
+gradients are compared per field: |gpu - oracle| <= 2e-3 |oracle| + 2e-4
+max|oracle| (fp32 sums over many pixels, fp32 atomics)."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import scenegen as S
+from gpu_common import pixel_mask
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("means", "rotations", "scales", "opacities", "sh", "rgb")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2412_12507_b200 import build
+    build.build()
+
+
+def _run(scene, cam, opt=None, seed=0, label=""):
+    import torch
+    from oracle import oracle as O
+    from paper_2412_12507_b200 import gut
+    opt = opt or S.RenderOptions()
+    o = O.render(scene, cam, opt)
+    mask = pixel_mask(o["diag"])
+    rng = np.random.default_rng(seed)
+    H, W = cam.height, cam.width
+    g_rgb = rng.standard_normal((H, W, 3)).astype(np.float32) * mask[..., None]
+    g_a = rng.standard_normal((H, W)).astype(np.float32) * mask
+    g_d = (0.1 * rng.standard_normal((H, W))).astype(np.float32) * mask
+    ob = O.backward(scene, cam, opt, g_rgb, g_a, g_d)
+    r = gut.Renderer(scene, max_wh=(max(W, 16), max(H, 16)))
+    out = r.render(cam, opt)[:3]
+    dev = out[0].device
+    gb = r.backward(cam, opt, out, torch.from_numpy(g_rgb).to(dev), torch.from_numpy(g_a).to(dev),
+                    torch.from_numpy(g_d).to(dev))
+    torch.cuda.synchronize()
+    worst = 0.0
+    for f in FIELDS:
+        a = gb[f].cpu().numpy().astype(np.float64).reshape(scene.count, -1)
+        b = ob[f].reshape(scene.count, -1)
+        scale = np.abs(b).max() + 1e-12
+        err = np.abs(a - b) / (2e-3 * np.abs(b) + 2e-4 * scale)
+        worst = max(worst, float(err.max(initial=0)))
+        i = np.unravel_index(np.argmax(err), err.shape) if err.size else None
+        print(f"{label} {f}: max |d| {np.abs(a - b).max(initial=0):.3e} (max |g| {scale:.3e}) ratio {err.max(initial=0):.3f}"
+              + (f" at {i}: gpu {a[i]:.6e} oracle {b[i]:.6e}" if i is not None else ""))
+    r.close()
+    assert worst <= 1.0, label
+    return gb, ob
+
+
+@pytest.mark.parametrize("variant", ["pinhole", "fisheye", "opencv"])
+@pytest.mark.parametrize("deg", [0, 3])
+def test_tiny_backward(variant, deg):
+    scene, cam = S.tiny(2, variant, n=96, sh_degree=deg)
+    _run(scene, cam, seed=deg, label=f"{variant} deg {deg}")
+
+
+def test_tiny_backward_ragged_dense():
+    scene, cam = S.tiny(9, "pinhole", n=300, size=64, sh_degree=1)
+    scene.scales[:] *= 1.5
+    cam = dataclasses.replace(cam, width=70, height=50, cx=35.0, cy=25.0)
+    _run(scene, cam, seed=5, label="ragged dense")
+
+
+@pytest.mark.parametrize("config,n,factor,view", [("multiview", 60_000, 0.12, 5), ("scannetpp", 30_000, 0.12, 3)])
+def test_reduced_config_backward(config, n, factor, view):
+    scene = S.make_scene(config, n=n)
+    cam = S.scaled_camera(S.make_views(config)[view], factor)
+    _run(scene, cam, seed=7, label=f"{config} n={n}")
+
+
+def test_backward_errors():
+    import torch
+    from paper_2412_12507_b200 import gut
+    scene, cam = S.tiny(0, "pinhole", n=16)
+    r = gut.Renderer(scene)
+    out = r.render(cam)[:3]
+    g = torch.zeros_like(out[0])
+    with pytest.raises(gut.GutError) as e:   # camera differs from the last render
+        r.backward(dataclasses.replace(cam, fx=cam.fx * 1.01), None, out, g)
+    assert e.value.status == 1
+    for c2, o2 in ((S.tiny(0, "ortho", n=16)[1], None), (S.tiny(0, "rs", n=16)[1], None),
+                   (cam, S.RenderOptions(kbuffer=16)), (cam, S.RenderOptions(kernel_degree=4))):
+        out2 = r.render(c2, o2)[:3]
+        with pytest.raises(gut.GutError) as e:
+            r.backward(c2, o2, out2, torch.zeros_like(out2[0]))
+        assert e.value.status == 2
+    r.close()
