@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--n", type=int, default=None, help="override N (debug only; the default is the config)")
     p.add_argument("--kbuffer", type=int, default=0, help="time \"Ours (sorted)\" (per-ray k-buffer of this size) "
                    "instead of \"Ours\" (0)")
+    p.add_argument("--no-backward", action="store_true", help="skip the forward+backward (training step) timing")
     p.add_argument("--sorted-k", type=int, default=16, help="also report \"Ours (sorted)\" with this k one frame "
                    "at a time (0: skip)")
     return p.parse_args()
@@ -321,6 +322,39 @@ def run_ours(args):
                        "ms_stage": sms, "what": "\"Ours (sorted)\": per-ray MLAB k-buffer K5 variant, the timed "
                        "views one at a time on one stream (library stage events); paper: 200 FPS / Render 2.85 ms "
                        "on MipNeRF360 with an RTX 6000 Ada (context only)"}
+    # forward + backward (Supp. B, gut_render_backward) of the same views, one at a
+    # time on one stream: the training-step workload of the rasterizer
+    backward_line = None
+    if args.kbuffer == 0 and not args.no_backward:
+        g_rgb = torch.randn((H, W, 3), device=dev)
+        g_a = torch.randn((H, W), device=dev)
+        gbuf = {k: torch.empty(sz, device=dev) for k, sz in (("means", (N, 3)), ("rotations", (N, 4)),
+                                                              ("scales", (N, 3)), ("opacities", (N,)),
+                                                              ("sh", (N, nc, 3)))}
+        grads = gut.gut_gradients(gbuf["means"].data_ptr(), gbuf["rotations"].data_ptr(), gbuf["scales"].data_ptr(),
+                                  gbuf["opacities"].data_ptr(), gbuf["sh"].data_ptr(), None)
+
+        def fwd_bwd(v):
+            gut.gut_render(ctx, scene, cams[v], gopt, out_dev, stream=stream, stats=False)
+            gut.gut_render_backward(ctx, scene, cams[v], gopt, rgb.data_ptr(), alpha.data_ptr(), depth.data_ptr(),
+                                    g_rgb.data_ptr(), g_a.data_ptr(), None, grads, stream=stream)
+        for v in timed_views[:2]:
+            fwd_bwd(v)
+        torch.cuda.synchronize()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for v in timed_views:
+            fwd_bwd(v)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        fb_ms = b0.elapsed_time(b1) / len(timed_views)
+        backward_line = {"frames_per_s": world * 1e3 / fb_ms, "ms_per_frame": fb_ms,
+                         "backward_ms": fb_ms - stage_ms["total"],
+                         "what": "forward + gut_render_backward (grad wrt mu, q, s, sigma, SH from random upstream "
+                                 "RGB/alpha gradients) per view, one at a time on one stream; backward_ms = this "
+                                 "minus the forward's single-stream time"}
+        del gbuf
+
     # timed region: `inflight` frames in flight, contexts (own workspaces, shared
     # read-only scene) on their own streams taking the views in turn, so one
     # frame's kernel tails overlap the next frame's first kernels
@@ -435,6 +469,7 @@ def run_ours(args):
                           "what": "one frame at a time on one stream (per-frame latency; library stage events)"},
         "ms_stage": stage_ms,
         "ours_sorted": sorted_line,
+        "ours_forward_backward": backward_line,
         "clocks": clk,
         "e2e": {"value": world * e2e_steps / (e2e_ms * 1e-3), "unit": "frames/s", "h2d_bytes_per_step": 240,
                 "d2h_bytes_per_step": npix * 5 * 4,

@@ -655,6 +655,7 @@ gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const g
   b.anchors = ctx->anchors; b.tiles = ctx->tiles;
   b.rgb = rgb; b.alpha = alpha; b.depth = depth; b.g_rgb = grad_rgb; b.g_alpha = grad_alpha; b.g_depth = grad_depth;
   b.acc = ctx->gacc;
+  b.order = ctx->q1; b.seg_base = ctx->seg_base; b.counters = ctx->counters;  // (forward plan scratch, reused)
   b.d_means = grads->means; b.d_rots = grads->rotations; b.d_scales = grads->scales; b.d_opac = grads->opacities;
   b.d_sh = grads->sh; b.d_rgb = grads->rgb;
   launch_backward(dc, scene->d, b, (cudaStream_t)s);

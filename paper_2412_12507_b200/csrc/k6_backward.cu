@@ -47,7 +47,9 @@ __device__ __forceinline__ T wsum(T v) {
 // rays_kernel's layout); every warp walks the whole list in chunks of 32.
 __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
   __shared__ float4 s_tbl[8][32 * BW_NF];
-  const int tile = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // CTAs take the tiles in decreasing list length (the plan's queue 1 with one
+  // unit per tile): the longest lists start first, no long tail
+  const int tile = (int)(B.order[blockIdx.x] & 0xFFFFFFu), w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr unsigned FULL = 0xffffffffu;
   float4 *tbl = s_tbl[w];
   int px, py;
@@ -75,6 +77,19 @@ __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
   const d3 T2 = mv(c.R0, mkd(A.T2[0], A.T2[1], A.T2[2]));
   const f3 Df = tof(D), T1f = tof(T1), T2f = tof(T2);
   const f3 dpw = Df + a * T1f + b * T2f;  // d' (world, |d'| = snorm)
+  // the warp's pixel box in (a, b) for the conservative entry cull (as K5)
+  float amin = done ? 3e38f : a, amax = done ? -3e38f : a, bmin = done ? 3e38f : b, bmax = done ? -3e38f : b;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    amin = fminf(amin, __shfl_xor_sync(FULL, amin, o));
+    amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, o));
+    bmin = fminf(bmin, __shfl_xor_sync(FULL, bmin, o));
+    bmax = fmaxf(bmax, __shfl_xor_sync(FULL, bmax, o));
+  }
+  if (amin > amax) { amin = amax = bmin = bmax = 0.f; }
+  const float ac = 0.5f * (amin + amax), bc = 0.5f * (bmin + bmax);
+  const float ra = 0.5f * (amax - amin) + 1e-7f * (fabsf(amin) + fabsf(amax));
+  const float rb = 0.5f * (bmax - bmin) + 1e-7f * (fabsf(bmin) + fabsf(bmax));
   const uint2 rg = B.ranges[tile];
   const uint32_t start = rg.y > rg.x ? rg.x : 0u, end = rg.y > rg.x ? rg.y : 0u;
   const float l2amin = log2f(c.alpha_min);
@@ -83,6 +98,7 @@ __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
     if (__all_sync(FULL, done)) break;
     const uint32_t kk = b0 + lane;
     __syncwarp();
+    bool maybe = false;
     if (kk < end) {
       const uint32_t gid = B.gids[kk];
       const float4 *src = B.payload + (size_t)GUT_PAYLOAD_F4 * gid;
@@ -113,10 +129,18 @@ __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
       t[7] = make_float4(M[0] / rn0, M[3] / rn1, M[6] / rn2, M[1] / rn0);
       t[8] = make_float4(M[4] / rn1, M[7] / rn2, M[2] / rn0, M[5] / rn1);
       t[9] = make_float4(M[8] / rn2, 0.f, 0.f, 0.f);
+      // conservative cull against the warp's pixel box (triangle inequality,
+      // 1e-3 margin): omega^2 > k^2 on the whole box -> no pixel can hit
+      const f3 n0 = c0 + ac * P + bc * Q, e0c = e0 + ac * U + bc * V;
+      const float lo = sqrtf(dot(n0, n0)) - (ra * sqrtf(dot(P, P)) + rb * sqrtf(dot(Q, Q)));
+      const float hi = sqrtf(dot(e0c, e0c)) + (ra * sqrtf(dot(U, U)) + rb * sqrtf(dot(V, V)));
+      maybe = !(lo > 0.f && lo * lo > 1.001f * k2 * (hi * hi));
     }
+    uint32_t msk = __ballot_sync(FULL, maybe);
     __syncwarp();
-    const int cnt = (int)min(32u, end - b0);
-    for (int j = 0; j < cnt; ++j) {
+    while (msk) {
+      const int j = __ffs(msk) - 1;
+      msk &= msk - 1;
       const float4 *t = tbl + j * BW_NF;
       const float4 f0 = t[0], f1 = t[1], f2 = t[2], f3v = t[3], f4 = t[4];
       const float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
@@ -255,6 +279,9 @@ __global__ __launch_bounds__(256) void backward_finish_kernel(DevCam c, SceneDev
 
 void launch_backward(const DevCam &cam, const SceneDev &s, const BwdBufs &b, cudaStream_t st) {
   cudaMemsetAsync(b.acc, 0, (size_t)16 * s.n * sizeof(float), st);
+  // queue-1 order of the tiles, longest list first (plan kernels, one unit per tile)
+  cudaMemsetAsync(b.counters + CNT_PLAN_HIST, 0, 1024 * sizeof(uint32_t), st);
+  launch_plan(b.ranges, cam.n_tiles, 1 << 30, 1, b.seg_base, b.order, b.counters, st, 1);
   if (cam.n_tiles > 0) backward_kernel<<<cam.n_tiles, 256, 0, st>>>(cam, b);
   if (s.n > 0) backward_finish_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, st>>>(cam, s, b);
 }

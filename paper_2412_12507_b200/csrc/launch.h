@@ -128,6 +128,9 @@ struct BwdBufs {
   const float *rgb, *alpha, *depth;          // forward outputs (device)
   const float *g_rgb, *g_alpha, *g_depth;    // upstream gradients (device; alpha / depth nullable)
   float *acc;                   // per Gaussian 16 fp32 accumulators
+  uint32_t *order;              // tiles, longest list first (plan queue 1, n_tiles entries)
+  uint32_t *seg_base;           // plan scratch (n_tiles)
+  uint32_t *counters;           // the context's counters block (plan histogram)
   float *d_means, *d_rots, *d_scales, *d_opac, *d_sh, *d_rgb;  // outputs (d_rgb nullable)
 };
 void launch_backward(const DevCam &cam, const SceneDev &s, const BwdBufs &b, cudaStream_t st);
