@@ -41,6 +41,32 @@ __device__ __forceinline__ T wsum(T v) {
   return v;
 }
 
+// Butterfly reduce-scatter: value q of the result (q = lane >> 1) summed over
+// the warp.  Step with offset o keeps the half of the values selected by the
+// lane's bit o and adds the partner's copy of that half.
+__device__ __forceinline__ float reduce16(const float (&v)[16], int lane) {
+  float x8[8], x4[4], x2[2];
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float keep = b4 ? v[8 + k] : v[k], send = b4 ? v[k] : v[8 + k];
+    x8[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float keep = b3 ? x8[4 + k] : x8[k], send = b3 ? x8[k] : x8[4 + k];
+    x4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float keep = b2 ? x4[2 + k] : x4[k], send = b2 ? x4[k] : x4[2 + k];
+    x2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  const float keep = b1 ? x2[1] : x2[0], send = b1 ? x2[0] : x2[1];
+  const float x1 = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  return x1 + __shfl_xor_sync(0xffffffffu, x1, 1);
+}
+
 }  // namespace
 
 // One CTA per tile, 8 warps = the tile's 8x4 pixel blocks (one pixel per lane,
@@ -199,12 +225,12 @@ __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
         }
       }
       if (!__any_sync(FULL, ok)) continue;
-#pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = wsum(v[q]);
-      if (lane == 0) {
-        float *acc = B.acc + (size_t)16 * __float_as_uint(f5.w);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) atomicAdd(acc + q, v[q]);
+      // reduce-scatter of the 16 values over the 32 lanes (16 + 1 shuffles
+      // instead of 80): afterwards lanes 2q and 2q + 1 hold the sum of value q
+      // and the 16 even lanes issue one atomic each (one instruction)
+      {
+        const float s = reduce16(v, lane);
+        if ((lane & 1) == 0) atomicAdd(B.acc + (size_t)16 * __float_as_uint(f5.w) + (lane >> 1), s);
       }
     }
   }
