@@ -14,8 +14,9 @@ def main():
     scene = S.make_scene(config)
     cam = S.make_views(config)[view]
     r = gut.Renderer(scene)
+    opt = S.RenderOptions(kbuffer=int(os.environ.get("KBUF", "0")))
     for _ in range(reps):
-        _, _, _, st = r.render(cam, timing=True)
+        _, _, _, st = r.render(cam, opt, timing=True)
     print("ms_stage", [round(x, 3) for x in st.ms_stage])
     r.close()
 
