@@ -1049,3 +1049,125 @@ int64_t orc_backward(const float *means, const float *rots, const float *scales,
   if (loss) *loss = Lsum;
   return K;
 }
+
+/* ======================================================================
+ * O8 — projection quality (Supp. C): for one Gaussian, its 2D
+ * image as estimated by (a) the UT (Eq. 6-10, O3 without the binning
+ * dilation), (b) EWA, the first-order linearisation at mu (Eq. 3):
+ * mean g(mu), covariance J Sigma J^T with J the central-difference Jacobian of
+ * the camera projection at mu's camera-frame point under the pose frozen at
+ * mu's own shutter time (RS-unaware, as the paper's EWA baseline), and
+ * (c) Monte Carlo: n samples x = mu + R S z, z ~ N(0, I3) from the shared
+ * counter-based generator below, each projected exactly (O2, RS-aware); sample
+ * mean and covariance (1/n).  KL(N_mc || N_ut) and KL(N_mc || N_ewa) in closed
+ * form (reading R31).  valid = 0 if any point fails to project.
+ * ====================================================================== */
+/* counter-based N(0,1) triple (shared spec with the GPU, implemented twice):
+ * splitmix64 finaliser of (seed, gaussian, sample, k); 53-bit uniforms in
+ * (0,1); Box-Muller in fp64 (z0, z1 from (u0, u1); z2 from (u2, u3)). */
+static uint64_t orc_mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+void orc_normal3(uint64_t seed, int64_t gid, int32_t s, double z[3]) {
+  double u[4];
+  for (int k = 0; k < 4; ++k) {
+    uint64_t h = orc_mix64(seed ^ orc_mix64(((uint64_t)gid << 24) ^ ((uint64_t)s << 2) ^ (uint64_t)k));
+    u[k] = ((double)(h >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+  }
+  const double two_pi = 6.283185307179586476925286766559;
+  double r0 = sqrt(-2.0 * log(u[0])), r1 = sqrt(-2.0 * log(u[2]));
+  z[0] = r0 * cos(two_pi * u[1]);
+  z[1] = r0 * sin(two_pi * u[1]);
+  z[2] = r1 * cos(two_pi * u[3]);
+}
+
+/* KL(N0 || N1) for 2D Gaussians g = (mx, my, cxx, cxy, cyy) */
+double orc_kl2(const double g0[5], const double g1[5]) {
+  double d1 = g1[2] * g1[4] - g1[3] * g1[3], d0 = g0[2] * g0[4] - g0[3] * g0[3];
+  double i00 = g1[4] / d1, i01 = -g1[3] / d1, i11 = g1[2] / d1;
+  double tr = i00 * g0[2] + 2.0 * i01 * g0[3] + i11 * g0[4];
+  double dx = g1[0] - g0[0], dy = g1[1] - g0[1];
+  double q = i00 * dx * dx + 2.0 * i01 * dx * dy + i11 * dy * dy;
+  return 0.5 * (tr + q - 2.0 + log(d1 / d0));
+}
+
+void orc_projection_quality(const float *means, const float *rots, const float *scales, int64_t n,
+                            const orc_camera *cam, const orc_options *o, int32_t n_mc, uint64_t seed,
+                            orc_quality *out) {
+  double wmu[7], wsig[7], lam;
+  orc_ut_weights(o->ut_alpha, o->ut_beta, o->ut_kappa, wmu, wsig, &lam);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t i = 0; i < n; ++i) {
+    orc_quality *q = &out[i];
+    memset(q, 0, sizeof(*q));
+    double mu[3] = {means[3 * i], means[3 * i + 1], means[3 * i + 2]}, R[9];
+    double s[3] = {scales[3 * i], scales[3 * i + 1], scales[3 * i + 2]};
+    double qq[4] = {rots[4 * i], rots[4 * i + 1], rots[4 * i + 2], rots[4 * i + 3]};
+    if (orc_quat_to_rot(qq, R) != 0 || !(s[0] > 0 && s[1] > 0 && s[2] > 0)) continue;
+    int ok = 1;
+    /* (a) UT */
+    double X[7][3], uv[7][2], t0 = 0;
+    orc_sigma_points(mu, R, s, lam, X);
+    for (int k = 0; k < 7 && ok; ++k) ok = orc_project_point(cam, o, X[k], uv[k], k == 0 ? &t0 : NULL, NULL, NULL);
+    if (!ok) continue;
+    double mx = 0, my = 0, cxx = 0, cxy = 0, cyy = 0;
+    for (int k = 0; k < 7; ++k) { mx += wmu[k] * uv[k][0]; my += wmu[k] * uv[k][1]; }
+    for (int k = 0; k < 7; ++k) {
+      double dx = uv[k][0] - mx, dy = uv[k][1] - my;
+      cxx += wsig[k] * dx * dx; cxy += wsig[k] * dx * dy; cyy += wsig[k] * dy * dy;
+    }
+    q->ut[0] = mx; q->ut[1] = my; q->ut[2] = cxx; q->ut[3] = cxy; q->ut[4] = cyy;
+    /* (b) EWA at the pose frozen at t0 */
+    double Rc[9], cc[3], d[3], xc[3], g0[2], J[2][3];
+    orc_pose_at(cam, t0, Rc, cc);
+    for (int a = 0; a < 3; ++a) d[a] = mu[a] - cc[a];
+    mtv3(Rc, d, xc);
+    ok = orc_project_cam(cam, o, xc, g0, NULL);
+    const double h = 1e-6 * sqrt(dot3(xc, xc));
+    for (int a = 0; a < 3 && ok; ++a) {
+      double xp[3] = {xc[0], xc[1], xc[2]}, xm[3] = {xc[0], xc[1], xc[2]}, up[2], um[2];
+      xp[a] += h; xm[a] -= h;
+      ok = orc_project_cam(cam, o, xp, up, NULL) && orc_project_cam(cam, o, xm, um, NULL);
+      J[0][a] = (up[0] - um[0]) / (2 * h);
+      J[1][a] = (up[1] - um[1]) / (2 * h);
+    }
+    if (!ok) continue;
+    /* Sigma_cam = Rc^T R S^2 R^T Rc */
+    double RS[9], A[9], Sc[9];
+    for (int r = 0; r < 3; ++r) for (int c2 = 0; c2 < 3; ++c2) RS[3 * r + c2] = R[3 * r + c2] * s[c2];
+    for (int r = 0; r < 3; ++r) for (int c2 = 0; c2 < 3; ++c2) {
+      double acc = 0; for (int k = 0; k < 3; ++k) acc += Rc[3 * k + r] * RS[3 * k + c2]; A[3 * r + c2] = acc;  /* Rc^T R S */
+    }
+    for (int r = 0; r < 3; ++r) for (int c2 = 0; c2 < 3; ++c2) {
+      double acc = 0; for (int k = 0; k < 3; ++k) acc += A[3 * r + k] * A[3 * c2 + k]; Sc[3 * r + c2] = acc;
+    }
+    double JS[2][3];
+    for (int r = 0; r < 2; ++r) for (int c2 = 0; c2 < 3; ++c2) {
+      double acc = 0; for (int k = 0; k < 3; ++k) acc += J[r][k] * Sc[3 * k + c2]; JS[r][c2] = acc;
+    }
+    q->ewa[0] = g0[0]; q->ewa[1] = g0[1];
+    q->ewa[2] = JS[0][0] * J[0][0] + JS[0][1] * J[0][1] + JS[0][2] * J[0][2];
+    q->ewa[3] = JS[0][0] * J[1][0] + JS[0][1] * J[1][1] + JS[0][2] * J[1][2];
+    q->ewa[4] = JS[1][0] * J[1][0] + JS[1][1] * J[1][1] + JS[1][2] * J[1][2];
+    /* (c) Monte Carlo (sums relative to the UT mean) */
+    double s1x = 0, s1y = 0, sxx = 0, sxy = 0, syy = 0;
+    for (int32_t smp = 0; smp < n_mc && ok; ++smp) {
+      double z[3], x[3], u2[2];
+      orc_normal3(seed, i, smp, z);
+      for (int a = 0; a < 3; ++a) x[a] = mu[a] + RS[3 * a] * z[0] + RS[3 * a + 1] * z[1] + RS[3 * a + 2] * z[2];
+      ok = orc_project_point(cam, o, x, u2, NULL, NULL, NULL);
+      double dx = u2[0] - mx, dy = u2[1] - my;
+      s1x += dx; s1y += dy; sxx += dx * dx; sxy += dx * dy; syy += dy * dy;
+    }
+    if (!ok || n_mc < 2) continue;
+    double ax = s1x / n_mc, ay = s1y / n_mc;
+    q->mc[0] = mx + ax; q->mc[1] = my + ay;
+    q->mc[2] = sxx / n_mc - ax * ax; q->mc[3] = sxy / n_mc - ax * ay; q->mc[4] = syy / n_mc - ay * ay;
+    q->kl_ut = orc_kl2(q->mc, q->ut);
+    q->kl_ewa = orc_kl2(q->mc, q->ewa);
+    q->valid = 1;
+  }
+}

@@ -132,6 +132,13 @@ void orc_mark_ambiguity(const float *means, const float *rots, const float *scal
                         double alpha_eps, const int32_t *tile_subset, int32_t n_subset,
                         orc_pixdiag *diag);
 int  orc_threads(void);
+/* ---- O8 (projection quality, Supp. C; reading R31) ---- */
+void orc_normal3(uint64_t seed, int64_t gid, int32_t s, double z[3]);
+double orc_kl2(const double g0[5], const double g1[5]);   /* KL(N0 || N1), g = (mx, my, cxx, cxy, cyy) */
+typedef struct { double ut[5], ewa[5], mc[5], kl_ut, kl_ewa; int32_t valid, pad; } orc_quality;
+void orc_projection_quality(const float *means, const float *rots, const float *scales, int64_t n,
+                            const orc_camera *cam, const orc_options *o, int32_t n_mc, uint64_t seed,
+                            orc_quality *out);
 /* ---- O7 (backward, Supp. B; "Ours" order, degree 2, reading R30) ----
  * upstream g_rgb [H][W][3], g_alpha [H][W], g_depth [H][W] (fp32);
  * outputs (fp64): d_means [n][3], d_rots [n][4], d_scales [n][3], d_opac [n],

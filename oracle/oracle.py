@@ -116,6 +116,11 @@ def lib():
         L.orc_backward.argtypes = [fp, fp, fp, fp, fp, C.c_int32, C.c_int64, C.POINTER(OrcCamera),
                                    C.POINTER(OrcOptions), fp, fp, fp, dp, dp, dp, dp, dp, dp, dp]
         L.orc_backward.restype = C.c_int64
+        L.orc_normal3.argtypes = [C.c_uint64, C.c_int64, C.c_int32, dp]
+        L.orc_kl2.argtypes = [dp, dp]
+        L.orc_kl2.restype = C.c_double
+        L.orc_projection_quality.argtypes = [fp, fp, fp, C.c_int64, C.POINTER(OrcCamera), C.POINTER(OrcOptions),
+                                             C.c_int32, C.c_uint64, C.c_void_p]
         L.orc_kernel_lambda.argtypes = [C.c_int32]
         L.orc_kernel_lambda.restype = C.c_double
         L.orc_kernel_response.argtypes = [C.c_double, C.c_int32]
@@ -363,6 +368,30 @@ def backward(scene, cam, opt, g_rgb, g_alpha, g_depth):
                        _fp(gr), _fp(ga), _fp(gd), _dp(out["means"]), _dp(out["rotations"]), _dp(out["scales"]),
                        _dp(out["opacities"]), _dp(out["sh"]), _dp(out["rgb"]), _dp(loss))
     out["loss"] = float(loss[0])
+    return out
+
+
+QUALITY_DTYPE = np.dtype([("ut", "<f8", 5), ("ewa", "<f8", 5), ("mc", "<f8", 5), ("kl_ut", "<f8"),
+                          ("kl_ewa", "<f8"), ("valid", "<i4"), ("pad", "<i4")])
+
+
+def normal3(seed, gid, s):
+    z = np.zeros(3)
+    lib().orc_normal3(int(seed), int(gid), int(s), _dp(z))
+    return z
+
+
+def kl2(g0, g1):
+    return float(lib().orc_kl2(_dp(np.ascontiguousarray(g0, np.float64)), _dp(np.ascontiguousarray(g1, np.float64))))
+
+
+def projection_quality(scene, cam, opt, n_mc=500, seed=0):
+    """O8 (Supp. C): per Gaussian UT / EWA / Monte-Carlo 2D Gaussians and KL."""
+    m, r, s, _, _ = _scene_arrays(scene)
+    out = np.zeros(scene.count, QUALITY_DTYPE)
+    oc, oo = camera(cam), options(opt)
+    lib().orc_projection_quality(_fp(m), _fp(r), _fp(s), scene.count, C.byref(oc), C.byref(oo), int(n_mc), int(seed),
+                                 out.ctypes.data)
     return out
 
 
