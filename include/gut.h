@@ -241,6 +241,25 @@ gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const g
                                const float *depth, const float *grad_rgb, const float *grad_alpha,
                                const float *grad_depth, const gut_gradients *grads, gut_stream s);
 
+/* Projection quality (PAPER Supp. C, L522-588; reading R31), a measurement
+ * tool: per Gaussian its 2D image (mean x, y in pixels; covariance xx, xy, yy)
+ * as estimated by the UT (Eq. 6-10, no binning dilation), by EWA (Eq. 3:
+ * linearisation at mu with a central-difference Jacobian, pose frozen at mu's
+ * own shutter time -- RS-unaware) and by Monte Carlo with n_samples points
+ * mu + R S z (z: counter-based N(0, I) from seed, gaussian, sample -- the
+ * splitmix64 / Box-Muller spec of DESIGN.md R31), each projected with its own
+ * rolling-shutter pose; kl_ut = KL(N_mc || N_ut), kl_ewa = KL(N_mc || N_ewa).
+ * valid = 0 when a point fails to project.  out: device array [count];
+ * asynchronous on s.  fp64. */
+typedef struct {
+  double ut[5], ewa[5], mc[5];
+  double kl_ut, kl_ewa;
+  int32_t valid, pad;
+} gut_quality;
+gut_status gut_projection_quality(gut_context *ctx, const gut_scene *scene, const gut_camera *cam,
+                                  const gut_options *opt, int32_t n_samples, uint64_t seed, gut_quality *out,
+                                  gut_stream s);
+
 /* Renders n_views views in order (outs[i] for cams[i]); stats nullable [n_views]. */
 gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_camera *cams,
                             int32_t n_views, const gut_options *opt, const gut_outputs *outs,

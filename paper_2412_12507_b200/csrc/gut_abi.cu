@@ -664,6 +664,24 @@ gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const g
   return GUT_OK;
 }
 
+gut_status gut_projection_quality(gut_context *ctx, const gut_scene *scene, const gut_camera *cam,
+                                  const gut_options *opt, int32_t n_samples, uint64_t seed, gut_quality *out,
+                                  gut_stream s) {
+  static_assert(sizeof(gut_quality) == sizeof(QualityRec), "gut_quality layout");
+  if (!ctx) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "ctx: NULL");
+  if (!scene || !out) return fail(ctx, GUT_E_INVALID_ARGUMENT, "scene / out: NULL");
+  if (n_samples < 2) return fail(ctx, GUT_E_INVALID_ARGUMENT, "n_samples < 2");
+  DevCam dc;
+  gut_status st_ = build_cam(ctx, cam, opt, dc);
+  if (st_ != GUT_OK) return st_;
+  cudaSetDevice(ctx->device);
+  launch_quality(dc, scene->d, n_samples, (unsigned long long)seed, reinterpret_cast<QualityRec *>(out),
+                 (cudaStream_t)s);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, GUT_E_CUDA, std::string("quality launch: ") + cudaGetErrorString(e));
+  return GUT_OK;
+}
+
 gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_camera *cams, int32_t n_views,
                             const gut_options *opt, const gut_outputs *outs, gut_stream s, gut_stats *stats) {
   if (!ctx) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "ctx: NULL");

@@ -593,3 +593,159 @@ void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32
 }
 
 }  // namespace gut
+
+namespace gut {
+
+// ---------------------------------------------------------------- Supp. C
+// Projection quality (reading R31): per Gaussian the 2D image
+// estimated by the UT (Eq. 6-10 without the binning dilation), by EWA (first-
+// order linearisation at mu, Eq. 3: central-difference Jacobian of the camera
+// projection, pose frozen at mu's own shutter time -- RS-unaware) and by Monte
+// Carlo (n samples mu + R S z, z from the shared counter-based generator, each
+// projected with its own RS-aware pose), and KL(MC || UT), KL(MC || EWA).
+// One warp per Gaussian, fp64 (a measurement tool, not the render path).
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+// N(0,1) triple of (seed, gaussian, sample): splitmix64 -> 53-bit uniforms ->
+// Box-Muller (the spec the oracle implements independently, orc_normal3)
+__device__ __forceinline__ d3 normal3(unsigned long long seed, long long gid, int s) {
+  double u[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const unsigned long long h =
+        mix64(seed ^ mix64(((unsigned long long)gid << 24) ^ ((unsigned long long)s << 2) ^ (unsigned long long)k));
+    u[k] = ((double)(h >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+  }
+  const double tp = 6.283185307179586476925286766559;
+  const double r0 = sqrt(-2.0 * log(u[0])), r1 = sqrt(-2.0 * log(u[2]));
+  double s1, c1, s3, c3;
+  sincos(tp * u[1], &s1, &c1);
+  sincos(tp * u[3], &s3, &c3);
+  return mkd(r0 * c1, r0 * s1, r1 * c3);
+}
+
+__device__ __forceinline__ double kl2(const double *g0, const double *g1) {
+  const double d1 = g1[2] * g1[4] - g1[3] * g1[3], d0 = g0[2] * g0[4] - g0[3] * g0[3];
+  const double i00 = g1[4] / d1, i01 = -g1[3] / d1, i11 = g1[2] / d1;
+  const double tr = i00 * g0[2] + 2.0 * i01 * g0[3] + i11 * g0[4];
+  const double dx = g1[0] - g0[0], dy = g1[1] - g0[1];
+  return 0.5 * (tr + i00 * dx * dx + 2.0 * i01 * dx * dy + i11 * dy * dy - 2.0 + log(d1 / d0));
+}
+
+__global__ __launch_bounds__(256) void quality_kernel(DevCam c, SceneDev s, int n_mc, unsigned long long seed,
+                                                      QualityRec *__restrict__ out) {
+  const long long i = ((long long)blockIdx.x * 256 + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= s.n) return;
+  const float4 po = s.pos_opa[i], ro = s.rot[i], sc = s.scale[i];
+  const double qn = sqrt((double)ro.x * ro.x + (double)ro.y * ro.y + (double)ro.z * ro.z + (double)ro.w * ro.w);
+  const double w_ = ro.x / qn, x_ = ro.y / qn, y_ = ro.z / qn, z_ = ro.w / qn;
+  const double R[9] = {1 - 2 * (y_ * y_ + z_ * z_), 2 * (x_ * y_ - w_ * z_), 2 * (x_ * z_ + w_ * y_),
+                       2 * (x_ * y_ + w_ * z_), 1 - 2 * (x_ * x_ + z_ * z_), 2 * (y_ * z_ - w_ * x_),
+                       2 * (x_ * z_ - w_ * y_), 2 * (y_ * z_ + w_ * x_), 1 - 2 * (x_ * x_ + y_ * y_)};
+  const double sv[3] = {sc.x, sc.y, sc.z};
+  const d3 mu = mkd(po.x, po.y, po.z), c0 = mkd(c.c0[0], c.c0[1], c.c0[2]);
+  const d3 w = mtv(c.R0, mkd(c.dc[0], c.dc[1], c.dc[2]));
+  bool ok = qn > 0 && sv[0] > 0 && sv[1] > 0 && sv[2] > 0;
+  QualityRec q;
+  memset(&q, 0, sizeof(q));
+  double mx = 0, my = 0, t0 = 0;
+  if (lane == 0 && ok) {
+    // (a) UT: sigma points mu +- gamma s_j R[:, j]
+    const d3 y0 = mtv(c.R0, mu - c0);
+    double du[7], dv[7], tt;
+    ok = project_sigma_d(c, y0, w, du[0], dv[0], t0);
+    for (int j = 0; j < 3 && ok; ++j) {
+      const d3 L = mtv(c.R0, ((double)c.gamma * sv[j]) * mkd(R[j], R[3 + j], R[6 + j]));
+      ok = ok && project_sigma_d(c, y0 + L, w, du[1 + j], dv[1 + j], tt);
+      ok = ok && project_sigma_d(c, y0 - L, w, du[4 + j], dv[4 + j], tt);
+    }
+    if (ok) {
+      mx = (double)c.wmu0 * du[0]; my = (double)c.wmu0 * dv[0];
+      for (int k = 1; k < 7; ++k) { mx += (double)c.wmui * du[k]; my += (double)c.wmui * dv[k]; }
+      double sxx = 0, sxy = 0, syy = 0;
+      for (int k = 0; k < 7; ++k) {
+        const double wk = k == 0 ? (double)c.wsig0 : (double)c.wsigi;
+        const double ax = du[k] - mx, ay = dv[k] - my;
+        sxx += wk * ax * ax; sxy += wk * ax * ay; syy += wk * ay * ay;
+      }
+      q.ut[0] = mx + c.cx; q.ut[1] = my + c.cy; q.ut[2] = sxx; q.ut[3] = sxy; q.ut[4] = syy;
+      // (b) EWA at the pose frozen at t0: p = R_t^T (y - t0 w)
+      double Rt[9];
+      rodrigues_d(mkd(c.phi_axis[0], c.phi_axis[1], c.phi_axis[2]), t0 * c.phi_angle, Rt);
+      const d3 p0 = mtv(Rt, y0 - t0 * w);
+      double g0u, g0v, J[2][3];
+      ok = project_cam_d(c, p0, g0u, g0v);
+      const double h = 1e-6 * sqrt(dot(p0, p0));
+      for (int a = 0; a < 3 && ok; ++a) {
+        d3 e = mkd(a == 0, a == 1, a == 2);
+        double up, vp, um, vm;
+        ok = project_cam_d(c, p0 + h * e, up, vp) && project_cam_d(c, p0 - h * e, um, vm);
+        J[0][a] = (up - um) / (2 * h);
+        J[1][a] = (vp - vm) / (2 * h);
+      }
+      if (ok) {
+        // Sigma_cam = A A^T, A = R_t^T R0^T R S
+        double A[9];
+        for (int col = 0; col < 3; ++col) {
+          const d3 v = mtv(Rt, mtv(c.R0, sv[col] * mkd(R[col], R[3 + col], R[6 + col])));
+          A[col] = v.x; A[3 + col] = v.y; A[6 + col] = v.z;
+        }
+        double JA[2][3];
+        for (int r = 0; r < 2; ++r)
+          for (int col = 0; col < 3; ++col) JA[r][col] = J[r][0] * A[col] + J[r][1] * A[3 + col] + J[r][2] * A[6 + col];
+        q.ewa[0] = g0u + c.cx; q.ewa[1] = g0v + c.cy;
+        q.ewa[2] = JA[0][0] * JA[0][0] + JA[0][1] * JA[0][1] + JA[0][2] * JA[0][2];
+        q.ewa[3] = JA[0][0] * JA[1][0] + JA[0][1] * JA[1][1] + JA[0][2] * JA[1][2];
+        q.ewa[4] = JA[1][0] * JA[1][0] + JA[1][1] * JA[1][1] + JA[1][2] * JA[1][2];
+      }
+    }
+  }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  mx = __shfl_sync(0xffffffffu, mx, 0);
+  my = __shfl_sync(0xffffffffu, my, 0);
+  // (c) Monte Carlo: sums relative to the UT mean
+  double s1x = 0, s1y = 0, sxx = 0, sxy = 0, syy = 0;
+  bool mok = ok;
+  for (int smp = lane; smp < n_mc && ok; smp += 32) {
+    const d3 z = normal3(seed, i, smp);
+    const d3 x = mu + mkd(R[0] * sv[0] * z.x + R[1] * sv[1] * z.y + R[2] * sv[2] * z.z,
+                          R[3] * sv[0] * z.x + R[4] * sv[1] * z.y + R[5] * sv[2] * z.z,
+                          R[6] * sv[0] * z.x + R[7] * sv[1] * z.y + R[8] * sv[2] * z.z);
+    double du, dv, tt;
+    mok = mok && project_sigma_d(c, mtv(c.R0, x - c0), w, du, dv, tt);
+    const double dx = du - mx, dy = dv - my;
+    s1x += dx; s1y += dy; sxx += dx * dx; sxy += dx * dy; syy += dy * dy;
+  }
+  ok = __all_sync(0xffffffffu, mok) && ok;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1x += __shfl_xor_sync(0xffffffffu, s1x, o); s1y += __shfl_xor_sync(0xffffffffu, s1y, o);
+    sxx += __shfl_xor_sync(0xffffffffu, sxx, o); sxy += __shfl_xor_sync(0xffffffffu, sxy, o);
+    syy += __shfl_xor_sync(0xffffffffu, syy, o);
+  }
+  if (lane == 0) {
+    if (ok && n_mc >= 2) {
+      const double ax = s1x / n_mc, ay = s1y / n_mc;
+      q.mc[0] = mx + ax + c.cx; q.mc[1] = my + ay + c.cy;
+      q.mc[2] = sxx / n_mc - ax * ax; q.mc[3] = sxy / n_mc - ax * ay; q.mc[4] = syy / n_mc - ay * ay;
+      q.kl_ut = kl2(q.mc, q.ut);
+      q.kl_ewa = kl2(q.mc, q.ewa);
+      q.valid = 1;
+    } else {
+      memset(&q, 0, sizeof(q));
+    }
+    out[i] = q;
+  }
+}
+
+void launch_quality(const DevCam &cam, const SceneDev &s, int n_mc, unsigned long long seed, QualityRec *out,
+                    cudaStream_t st) {
+  if (s.n > 0) quality_kernel<<<(unsigned)((s.n * 32 + 255) / 256), 256, 0, st>>>(cam, s, n_mc, seed, out);
+}
+
+}  // namespace gut

@@ -135,4 +135,12 @@ struct BwdBufs {
 };
 void launch_backward(const DevCam &cam, const SceneDev &s, const BwdBufs &b, cudaStream_t st);
 
+// Supp. C projection quality (k1_project.cu); layout = gut_quality (include/gut.h)
+struct QualityRec {
+  double ut[5], ewa[5], mc[5], kl_ut, kl_ewa;
+  int32_t valid, pad;
+};
+void launch_quality(const DevCam &cam, const SceneDev &s, int n_mc, unsigned long long seed, QualityRec *out,
+                    cudaStream_t st);
+
 }  // namespace gut

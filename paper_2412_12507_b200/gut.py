@@ -75,7 +75,8 @@ class gut_gradients(C.Structure):
 
 EXPORTS = ["gut_abi_version", "gut_options_default", "gut_context_create", "gut_context_destroy",
            "gut_last_error", "gut_workspace_reserve", "gut_scene_create", "gut_scene_destroy", "gut_render",
-           "gut_render_batch", "gut_render_backward", "gut_timing_read", "gut_debug_copy_stage"]
+           "gut_render_batch", "gut_render_backward", "gut_projection_quality", "gut_timing_read",
+           "gut_debug_copy_stage"]
 STAGE_NAMES = ["K1_project", "K3_sort_depth", "K2_emit", "K3_sort_tile", "K4_ranges", "K5_blend", "total"]
 
 _lib = None
@@ -112,9 +113,12 @@ def lib():
         L.gut_debug_copy_stage.argtypes = [vp, i32, vp, C.c_size_t, C.POINTER(C.c_size_t)]
         L.gut_render_backward.argtypes = [vp, vp, C.POINTER(gut_camera), C.POINTER(gut_options), vp, vp, vp, vp, vp,
                                           vp, C.POINTER(gut_gradients), vp]
+        L.gut_projection_quality.argtypes = [vp, vp, C.POINTER(gut_camera), C.POINTER(gut_options), i32, C.c_uint64,
+                                             vp, vp]
         L.gut_timing_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int32), i32]
         for name in ("gut_context_create", "gut_workspace_reserve", "gut_scene_create", "gut_render",
-                     "gut_render_batch", "gut_render_backward", "gut_timing_read", "gut_debug_copy_stage"):
+                     "gut_render_batch", "gut_render_backward", "gut_projection_quality", "gut_timing_read",
+                     "gut_debug_copy_stage"):
             getattr(L, name).restype = C.c_int
         L.gut_options_default.restype = None
         L.gut_context_destroy.restype = None
@@ -240,6 +244,17 @@ def gut_render_backward(ctx, scene, cam: gut_camera, opt: gut_options, rgb, alph
                                      grad_depth, C.byref(grads), _stream_ptr(stream)), ctx)
 
 
+QUALITY_FIELDS = ("ut", "ewa", "mc", "kl_ut", "kl_ewa", "valid")
+
+
+def gut_projection_quality(ctx, scene, cam: gut_camera, opt: gut_options, n_samples: int, seed: int, out_ptr,
+                           stream=None):
+    """Supp. C: per-Gaussian UT / EWA / Monte-Carlo 2D Gaussians and KL into a
+    device buffer of count x 144 bytes (gut_quality records)."""
+    _check(lib().gut_projection_quality(ctx, scene, C.byref(cam), C.byref(opt), int(n_samples), int(seed), out_ptr,
+                                        _stream_ptr(stream)), ctx)
+
+
 def gut_render_batch(ctx, scene, cams: Sequence[gut_camera], opt: gut_options, outs: Sequence[gut_outputs],
                      stream=None, stats=False):
     n = len(cams)
@@ -321,6 +336,18 @@ class Renderer:
                             p(out[2]) if grad_depth is not None else p(out[2]), p(grad_rgb), p(grad_alpha),
                             p(grad_depth), gg)
         return g
+
+    def projection_quality(self, cam, opt=None, n_samples=500, seed=0):
+        """numpy structured array (ut, ewa, mc [5], kl_ut, kl_ewa, valid) per Gaussian."""
+        import numpy as np
+        torch = self.torch
+        buf = torch.empty((self.n, 18), dtype=torch.float64, device=torch.device("cuda", self.device))
+        gut_projection_quality(self.ctx, self.scene, make_camera(cam), make_options(opt), n_samples, seed,
+                               buf.data_ptr())
+        torch.cuda.synchronize(self.device)
+        dt = np.dtype([("ut", "<f8", 5), ("ewa", "<f8", 5), ("mc", "<f8", 5), ("kl_ut", "<f8"), ("kl_ewa", "<f8"),
+                       ("valid", "<i4"), ("pad", "<i4")])
+        return buf.cpu().numpy().view(dt).reshape(-1)
 
     def stage(self, stage):
         return gut_debug_copy_stage(self.ctx, stage)
