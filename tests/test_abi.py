@@ -40,15 +40,17 @@ def test_exports_every_declared_symbol(libgut):
 def test_struct_layouts_match_header(libgut, tmp_path):
     prog = tmp_path / "sz.c"
     prog.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "gut.h"\n'
-                    'int main(){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(gut_camera), sizeof(gut_options),'
+                    'int main(){printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(gut_camera), sizeof(gut_options),'
                     'sizeof(gut_stats), sizeof(gut_proj_record), sizeof(gut_gaussians), sizeof(gut_outputs),'
-                    'offsetof(gut_camera, q_c2w));}\n')
+                    'offsetof(gut_camera, q_c2w), sizeof(gut_gradients), sizeof(gut_quality),'
+                    'offsetof(gut_options, kbuffer), offsetof(gut_options, kernel_degree));}\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I" + os.path.join(ROOT, "include"), str(prog), "-o", str(exe)])
     got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
     g = libgut
     want = [C.sizeof(g.gut_camera), C.sizeof(g.gut_options), C.sizeof(g.gut_stats), C.sizeof(g.gut_proj_record),
-            C.sizeof(g.gut_gaussians), C.sizeof(g.gut_outputs), g.gut_camera.q_c2w.offset]
+            C.sizeof(g.gut_gaussians), C.sizeof(g.gut_outputs), g.gut_camera.q_c2w.offset, C.sizeof(g.gut_gradients),
+            144, g.gut_options.kbuffer.offset, g.gut_options.kernel_degree.offset]
     assert got == want
 
 
