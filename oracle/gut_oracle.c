@@ -903,7 +903,8 @@ void orc_mark_ambiguity(const float *means, const float *rots, const float *scal
  * P:L494-513; "avoids propagating gradients through the projection", P:L202:
  * the UT / binning is not differentiated, reading R30).  Scalar loss
  * L = sum_px g_rgb . rgb + g_alpha alpha + g_depth depth with the given
- * per-pixel upstream gradients; "Ours" order (kbuffer = 0), degree-2 kernel.
+ * per-pixel upstream gradients; "Ours" order (kbuffer = 0); any kernel degree
+ * (Supp. A) and camera incl. rolling shutter (the pixel rays of O5).
  * Plain fp64 chain rule, written out per hit:
  *   Eq. 5: w_i = alpha_i T_i, C = sum w_i c_i, D = sum w_i tau_i, T_f = prod(1 - alpha_i)
  *   dL/dc_i = w_i g_rgb;  dL/dtau_i = w_i g_depth
@@ -919,7 +920,7 @@ void orc_mark_ambiguity(const float *means, const float *rots, const float *scal
  *   colour c = max(0, sum_k sh_k Y_k(dir) + 1/2) at the forward's direction
  *   (reading R18, held constant): dL/dsh_k = dL/dc Y_k where c > 0.
  * ====================================================================== */
-typedef struct { int32_t gid; double al, rho, T, tau, g; int clamped; } orc_bhit;
+typedef struct { int32_t gid; double al, rho, T, tau, g, w2; int clamped; } orc_bhit;
 
 int64_t orc_backward(const float *means, const float *rots, const float *scales, const float *opac,
                      const float *sh, int32_t sh_degree, int64_t n, const orc_camera *cam,
@@ -958,13 +959,13 @@ int64_t orc_backward(const float *means, const float *rots, const float *scales,
         for (int32_t k = ranges[2 * t]; k < ranges[2 * t + 1]; ++k) {
           const orc_gauss *g = &G[gids[k]];
           double tau, w2 = orc_max_response(g->mu, g->R, g->s, ro, rd, &tau);
-          double rho = exp(-0.5 * w2), al = g->sig * rho;
+          double rho = orc_kernel_response(w2, o->kernel_degree), al = g->sig * rho;
           int clamped = al > o->alpha_max;
           if (clamped) al = o->alpha_max;
           if (al < o->alpha_min || !(tau > 0.0)) continue;
           double Tn = T * (1.0 - al);
           if (Tn < o->t_min) break;
-          orc_bhit h = {gids[k], al, rho, T, tau, 0.0, clamped};
+          orc_bhit h = {gids[k], al, rho, T, tau, 0.0, w2, clamped};
           h.g = g->rgb[0] * gc[0] + g->rgb[1] * gc[1] + g->rgb[2] * gc[2] + tau * gdp;
           hits[m++] = h;
           T = Tn;
@@ -984,7 +985,11 @@ int64_t orc_backward(const float *means, const float *rots, const float *scales,
           double dw2 = 0.0;
           if (!h->clamped) {
             d_opac[h->gid] += h->rho * dal;
-            dw2 = -0.5 * g->sig * h->rho * dal;
+            /* d rho / d omega^2 = -(1/2) lambda_n (n/2) (omega^2)^(n/2 - 1) rho (Supp. A; n = 2: -rho/2) */
+            const int32_t nd = o->kernel_degree;
+            const double drho = nd == 2 ? -0.5 * h->rho
+                                        : -0.5 * orc_kernel_lambda(nd) * 0.5 * nd * pow(h->w2, 0.5 * nd - 1.0) * h->rho;
+            dw2 = g->sig * drho * dal;
           }
           /* Eq. 11 chain */
           double om[3] = {ro[0] - g->mu[0], ro[1] - g->mu[1], ro[2] - g->mu[2]}, og[3], dg[3];

@@ -49,12 +49,14 @@ def _fd(orc, scene, cam, opt, g, field, i, comp, h):
     return (Lp - Lm) / (float(hi) - float(lo))
 
 
-@pytest.mark.parametrize("variant,seed,deg", [("pinhole", 0, 0), ("fisheye", 1, 0), ("opencv", 2, 0), ("pinhole", 4, 2)])
-def test_backward_finite_differences(orc, variant, seed, deg):
+@pytest.mark.parametrize("variant,seed,deg,kdeg", [("pinhole", 0, 0, 2), ("fisheye", 1, 0, 2), ("opencv", 2, 0, 2),
+                                                   ("pinhole", 4, 2, 2), ("rs", 5, 0, 2), ("pinhole", 6, 0, 4),
+                                                   ("fisheye", 7, 0, 3)])
+def test_backward_finite_differences(orc, variant, seed, deg, kdeg):
     """deg 0: every parameter.  deg > 0: the colour's view direction is held
     constant in the backward (reading R30), so mu is checked at deg 0 only."""
     scene, cam = S.tiny(seed, variant, n=48, sh_degree=deg)
-    opt = S.RenderOptions()
+    opt = S.RenderOptions(kernel_degree=kdeg)
     rng = np.random.default_rng(10 + seed)
     g = _grads(rng, cam)
     b = orc.backward(scene, cam, opt, *g)
