@@ -232,8 +232,8 @@ typedef struct {
  * grad_rgb [H][W][3] required, grad_alpha / grad_depth nullable (zero); depth
  * is required when grad_depth is given.  All pointers device memory on the
  * context's device; asynchronous on s.  Per-Gaussian sums use fp32 atomics
- * (reproducible to rounding, not bitwise).  Supported: global-shutter
- * PINHOLE / OPENCV / FISHEYE, kbuffer 0, kernel_degree 2; otherwise
+ * (reproducible to rounding, not bitwise).  Supported: PINHOLE / OPENCV /
+ * FISHEYE with any shutter and kernel_degree, kbuffer 0; otherwise
  * GUT_E_UNSUPPORTED.  A camera / options mismatch with the last render:
  * GUT_E_INVALID_ARGUMENT. */
 gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const gut_camera *cam,

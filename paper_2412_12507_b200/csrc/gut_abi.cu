@@ -66,7 +66,7 @@ struct gut_context {
   const uint32_t *last_order = nullptr, *last_keys = nullptr, *last_vals = nullptr;
   DevCam last_cam;                    // (gut_render_backward: must match)
   const gut_scene *last_scene = nullptr;
-  float *gacc = nullptr;              // K6 accumulators (16 per Gaussian)
+  float *gacc = nullptr;              // K6 accumulators (16 per Gaussian) + centre shutter times (1 per Gaussian)
   size_t cap_gacc = 0;
 };
 
@@ -638,8 +638,8 @@ gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const g
   DevCam dc;
   gut_status st_ = build_cam(ctx, cam, opt, dc);
   if (st_ != GUT_OK) return st_;
-  if (dc.shutter != GUT_SHUTTER_GLOBAL || dc.model == CAM_ORTHO || dc.kbuf != 0 || dc.kdeg != 2)
-    return fail(ctx, GUT_E_UNSUPPORTED, "backward: global-shutter PINHOLE/OPENCV/FISHEYE, kbuffer 0, degree 2 only");
+  if (dc.model == CAM_ORTHO || dc.kbuf != 0)
+    return fail(ctx, GUT_E_UNSUPPORTED, "backward: PINHOLE/OPENCV/FISHEYE (any shutter, any degree), kbuffer 0 only");
   if (ctx->last_scene != scene || memcmp(&ctx->last_cam, &dc, sizeof(DevCam)) != 0)
     return fail(ctx, GUT_E_INVALID_ARGUMENT, "backward: scene / camera / options differ from the last render");
   cudaSetDevice(ctx->device);
@@ -647,7 +647,7 @@ gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const g
   if (ctx->cap_gacc < (size_t)N) {
     if (ctx->gacc) cudaFree(ctx->gacc);
     ctx->gacc = nullptr;
-    CUDA_TRY(ctx, cudaMalloc(&ctx->gacc, (size_t)16 * (N > 0 ? N : 1) * sizeof(float)));
+    CUDA_TRY(ctx, cudaMalloc(&ctx->gacc, (size_t)17 * (N > 0 ? N : 1) * sizeof(float)));
     ctx->cap_gacc = (size_t)N;
   }
   BwdBufs b;
@@ -656,6 +656,7 @@ gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const g
   b.rgb = rgb; b.alpha = alpha; b.depth = depth; b.g_rgb = grad_rgb; b.g_alpha = grad_alpha; b.g_depth = grad_depth;
   b.acc = ctx->gacc;
   b.order = ctx->q1; b.seg_base = ctx->seg_base; b.counters = ctx->counters;  // (forward plan scratch, reused)
+  b.t0 = dc.shutter != GUT_SHUTTER_GLOBAL ? ctx->gacc + (size_t)16 * (N > 0 ? N : 1) : nullptr;
   b.d_means = grads->means; b.d_rots = grads->rotations; b.d_scales = grads->scales; b.d_opac = grads->opacities;
   b.d_sh = grads->sh; b.d_rgb = grads->rgb;
   launch_backward(dc, scene->d, b, (cudaStream_t)s);

@@ -749,3 +749,26 @@ void launch_quality(const DevCam &cam, const SceneDev &s, int n_mc, unsigned lon
 }
 
 }  // namespace gut
+
+namespace gut {
+
+// Shutter time t0 of each Gaussian's centre (the fixed point K1 solves for
+// sigma point 0, reading R14; fp64 secant as the wide kernel): the view
+// direction of its SH colour is normalize(mu - c(t0)) (reading R18).  Used by
+// the backward's SH gradients under rolling shutter.
+__global__ __launch_bounds__(256) void centre_time_kernel(DevCam c, SceneDev s, float *__restrict__ t0) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= s.n) return;
+  const float4 po = s.pos_opa[i];
+  const d3 y0 = mtv(c.R0, mkd(po.x, po.y, po.z) - mkd(c.c0[0], c.c0[1], c.c0[2]));
+  const d3 w = mtv(c.R0, mkd(c.dc[0], c.dc[1], c.dc[2]));
+  double du, dv, t = 0.0;
+  if (!project_sigma_d(c, y0, w, du, dv, t)) t = 0.0;
+  t0[i] = (float)t;
+}
+
+void launch_centre_times(const DevCam &cam, const SceneDev &s, float *t0, cudaStream_t st) {
+  if (s.n > 0) centre_time_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, st>>>(cam, s, t0);
+}
+
+}  // namespace gut

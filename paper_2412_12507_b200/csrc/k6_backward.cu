@@ -26,7 +26,8 @@ namespace gut {
 
 namespace {
 
-constexpr int BW_NF = 10;  // float4 per staged entry
+template <int MODE> struct BwNF { static constexpr int v = 10; };  // float4 per staged entry
+template <> struct BwNF<2> { static constexpr int v = 13; };              // + rolling-shutter terms
 
 __device__ __forceinline__ float ex2f_(float x) {
   float y;
@@ -71,19 +72,21 @@ __device__ __forceinline__ float reduce16(const float (&v)[16], int lane) {
 
 // One CTA per tile, 8 warps = the tile's 8x4 pixel blocks (one pixel per lane,
 // rays_kernel's layout); every warp walks the whole list in chunks of 32.
+template <int MODE>
 __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
-  __shared__ float4 s_tbl[8][32 * BW_NF];
+  constexpr int BW_NF = BwNF<MODE>::v;
+  extern __shared__ float4 s_dyn[];
   // CTAs take the tiles in decreasing list length (the plan's queue 1 with one
   // unit per tile): the longest lists start first, no long tail
   const int tile = (int)(B.order[blockIdx.x] & 0xFFFFFFu), w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr unsigned FULL = 0xffffffffu;
-  float4 *tbl = s_tbl[w];
+  float4 *tbl = s_dyn + w * 32 * BW_NF;
   int px, py;
   px = (tile % c.tiles_x) * GUT_TILE + (w & 1) * 8 + (lane & 7);
   py = (tile / c.tiles_x) * GUT_TILE + (w >> 1) * 4 + (lane >> 3);
   const bool inside = px < c.width && py < c.height;
   const float4 pl = B.pix[(size_t)tile * GUT_TILE_PX + w * 32 + lane];
-  const float a = pl.x, b = pl.y, snorm = pl.z;
+  const float a = pl.x, b = pl.y, snorm = pl.z, beta = pl.w;  // beta: rolling shutter t_pixel - t_anchor
   bool done = !(inside && snorm > 0.f);
   // per-pixel upstream gradients and the forward's outputs
   float gr = 0.f, gg = 0.f, gb = 0.f, gA = 0.f, gD = 0.f, Gtot = 0.f;
@@ -96,11 +99,21 @@ __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
     Gtot = B.rgb[3 * p] * gr + B.rgb[3 * p + 1] * gg + B.rgb[3 * p + 2] * gb + (B.depth ? B.depth[p] * gD : 0.f) -
            Tf * gA;
   }
-  // tile anchor (camera frame) -> world
+  // tile anchor -> world (MODE 2: the anchors are world-frame, origin O = c(t_anchor))
   const TileAnchor &A = B.anchors[tile];
-  const d3 D = mv(c.R0, mkd(A.D[0], A.D[1], A.D[2]));
-  const d3 T1 = mv(c.R0, mkd(A.T1[0], A.T1[1], A.T1[2]));
-  const d3 T2 = mv(c.R0, mkd(A.T2[0], A.T2[1], A.T2[2]));
+  d3 D, T1, T2, dO = mkd(0, 0, 0);
+  if (MODE == 2) {
+    D = mkd(A.D[0], A.D[1], A.D[2]); T1 = mkd(A.T1[0], A.T1[1], A.T1[2]); T2 = mkd(A.T2[0], A.T2[1], A.T2[2]);
+    dO = mkd(A.O[0] - c.c0[0], A.O[1] - c.c0[1], A.O[2] - c.c0[2]);
+  } else {
+    D = mv(c.R0, mkd(A.D[0], A.D[1], A.D[2]));
+    T1 = mv(c.R0, mkd(A.T1[0], A.T1[1], A.T1[2]));
+    T2 = mv(c.R0, mkd(A.T2[0], A.T2[1], A.T2[2]));
+  }
+  const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
+  // kernel degree n (Supp. A): log2 alpha = log2 sigma - lambda_n (omega^2)^(n/2) / (2 ln 2)
+  const bool gen = c.kdeg != 2;
+  const float kgl = -0.72134752044448170f * c.klam, khn = 0.5f * (float)c.kdeg;
   const f3 Df = tof(D), T1f = tof(T1), T2f = tof(T2);
   const f3 dpw = Df + a * T1f + b * T2f;  // d' (world, |d'| = snorm)
   // the warp's pixel box in (a, b) for the conservative entry cull (as K5)
@@ -130,7 +143,7 @@ __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
       const float4 *src = B.payload + (size_t)GUT_PAYLOAD_F4 * gid;
       const double2 wxy = *reinterpret_cast<const double2 *>(src);
       const float4 p1 = src[1], p2 = src[2], p3 = src[3], p4 = src[4];
-      const d3 wv = mkd(wxy.x, wxy.y, __hiloint2double(__float_as_int(p1.y), __float_as_int(p1.x)));
+      const d3 wv = mkd(wxy.x, wxy.y, __hiloint2double(__float_as_int(p1.y), __float_as_int(p1.x))) + dO;
       const f3 x = tof(cross(wv, D));
       const float M[9] = {p1.w, p2.x, p2.y, p2.z, p2.w, p3.x, p3.y, p3.z, p3.w};
       const float rn0 = fmaf(M[0], M[0], fmaf(M[1], M[1], M[2] * M[2]));
@@ -155,12 +168,19 @@ __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
       t[7] = make_float4(M[0] / rn0, M[3] / rn1, M[6] / rn2, M[1] / rn0);
       t[8] = make_float4(M[4] / rn1, M[7] / rn2, M[2] / rn0, M[5] / rn1);
       t[9] = make_float4(M[8] / rn2, 0.f, 0.f, 0.f);
+      if (MODE == 2) {  // o_g(beta) = o_g + beta m, m = M dc: n += beta (h + a PU + b QV), g += beta (m.d_g)
+        const f3 m = mv(M, dcw);
+        const f3 h = cross(m, e0), PU = cross(m, U), QV = cross(m, V);
+        t[10] = make_float4(h.x, h.y, h.z, dot(m, e0));
+        t[11] = make_float4(PU.x, PU.y, PU.z, dot(m, U));
+        t[12] = make_float4(QV.x, QV.y, QV.z, dot(m, V));
+      }
       // conservative cull against the warp's pixel box (triangle inequality,
       // 1e-3 margin): omega^2 > k^2 on the whole box -> no pixel can hit
       const f3 n0 = c0 + ac * P + bc * Q, e0c = e0 + ac * U + bc * V;
       const float lo = sqrtf(dot(n0, n0)) - (ra * sqrtf(dot(P, P)) + rb * sqrtf(dot(Q, Q)));
       const float hi = sqrtf(dot(e0c, e0c)) + (ra * sqrtf(dot(U, U)) + rb * sqrtf(dot(V, V)));
-      maybe = !(lo > 0.f && lo * lo > 1.001f * k2 * (hi * hi));
+      maybe = MODE == 2 || !(lo > 0.f && lo * lo > 1.001f * k2 * (hi * hi));  // (RS: every entry kept, as K5)
     }
     uint32_t msk = __ballot_sync(FULL, maybe);
     __syncwarp();
@@ -169,9 +189,17 @@ __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
       msk &= msk - 1;
       const float4 *t = tbl + j * BW_NF;
       const float4 f0 = t[0], f1 = t[1], f2 = t[2], f3v = t[3], f4 = t[4];
-      const float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
-      const float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
-      const float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
+      float nx = fmaf(a, f1.x, fmaf(b, f1.w, f0.x));
+      float ny = fmaf(a, f1.y, fmaf(b, f2.x, f0.y));
+      float nz = fmaf(a, f1.z, fmaf(b, f2.y, f0.z));
+      float gb2 = 0.f;
+      if (MODE == 2) {
+        const float4 h = t[10], pu = t[11], qv = t[12];
+        nx = fmaf(beta, fmaf(a, pu.x, fmaf(b, qv.x, h.x)), nx);
+        ny = fmaf(beta, fmaf(a, pu.y, fmaf(b, qv.y, h.y)), ny);
+        nz = fmaf(beta, fmaf(a, pu.z, fmaf(b, qv.z, h.z)), nz);
+        gb2 = beta * fmaf(a, pu.w, fmaf(b, qv.w, h.w));
+      }
       const float ex = fmaf(a, f3v.y, fmaf(b, f4.x, f2.z));
       const float ey = fmaf(a, f3v.z, fmaf(b, f4.y, f2.w));
       const float ez = fmaf(a, f3v.w, fmaf(b, f4.z, f3v.x));
@@ -182,9 +210,11 @@ __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
       const float4 f5 = t[5], cc = t[6];
       const float rD = 1.f / Dd;
       const float w2 = N * rD;
-      const float raw = ex2f_(fmaf(-0.72134752044448170f, w2, f4.w));
+      float pw = w2;  // (omega^2)^(n/2)
+      if (gen) pw = ex2f_(khn * __log2f(w2));
+      const float raw = ex2f_(gen ? fmaf(kgl, pw, f4.w) : fmaf(-0.72134752044448170f, w2, f4.w));
       const float al = fminf(c.alpha_max, raw);
-      const float gdot = fmaf(a, f5.y, fmaf(b, f5.z, f5.x));
+      const float gdot = fmaf(a, f5.y, fmaf(b, f5.z, f5.x)) + gb2;
       const float taup = -gdot * rD, tau = taup * snorm;
       ok = ok && al >= c.alpha_min && tau > 0.f;
       float v[16];
@@ -201,7 +231,9 @@ __global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
           Gpre = fmaf(wgt, gi, Gpre);
           const float dal = T * gi - (Gtot - Gpre) / (1.f - al);
           const bool clamped = raw > c.alpha_max;
-          const float dw2 = clamped ? 0.f : -0.5f * raw * dal;
+          // d alpha / d omega^2 = -(1/2) lambda_n (n/2) (omega^2)^(n/2 - 1) alpha (n = 2: -alpha/2)
+          const float dadw = gen ? (w2 > 0.f ? -0.5f * c.klam * khn * pw / w2 * raw : 0.f) : -0.5f * raw;
+          const float dw2 = clamped ? 0.f : dadw * dal;
           const float dtp = wgt * gD * snorm;  // dL/dtau'
           // x_g = (d_g x n) / |d_g|^2
           const float xgx = (ey * nz - ez * ny) * rD, xgy = (ez * nx - ex * nz) * rD, xgz = (ex * ny - ey * nx) * rD;
@@ -282,9 +314,10 @@ __global__ __launch_bounds__(256) void backward_finish_kernel(DevCam c, SceneDev
   for (int k = 0; k < 4; ++k) gq[k] = vis ? (g4[k] - qh[k] * pr) / qn : 0.f;
   B.d_opac[i] = acc[12];
   if (B.d_rgb) { B.d_rgb[3 * i] = acc[13]; B.d_rgb[3 * i + 1] = acc[14]; B.d_rgb[3 * i + 2] = acc[15]; }
-  // SH (the forward's direction normalize(mu - c(0)); global shutter only)
+  // SH (the forward's direction normalize(mu - c(t0)), t0 = mu's shutter time)
   const float4 col = vis ? B.payload[(size_t)GUT_PAYLOAD_F4 * i + 4] : make_float4(0.f, 0.f, 0.f, 0.f);
-  const d3 dw = mkd(po.x, po.y, po.z) - mkd(c.c0[0], c.c0[1], c.c0[2]);
+  const double tc = B.t0 ? (double)B.t0[i] : 0.0;
+  const d3 dw = mkd(po.x, po.y, po.z) - mkd(c.c0[0] + tc * c.dc[0], c.c0[1] + tc * c.dc[1], c.c0[2] + tc * c.dc[2]);
   const f3 d = tof((1.0 / sqrt(dot(dw, dw))) * dw);
   const float x = d.x, y = d.y, z = d.z, xx = x * x, yy = y * y, zz = z * z;
   float Y[16];
@@ -304,11 +337,21 @@ __global__ __launch_bounds__(256) void backward_finish_kernel(DevCam c, SceneDev
 }
 
 void launch_backward(const DevCam &cam, const SceneDev &s, const BwdBufs &b, cudaStream_t st) {
+  if (b.t0) launch_centre_times(cam, s, const_cast<float *>(b.t0), st);
   cudaMemsetAsync(b.acc, 0, (size_t)16 * s.n * sizeof(float), st);
   // queue-1 order of the tiles, longest list first (plan kernels, one unit per tile)
   cudaMemsetAsync(b.counters + CNT_PLAN_HIST, 0, 1024 * sizeof(uint32_t), st);
   launch_plan(b.ranges, cam.n_tiles, 1 << 30, 1, b.seg_base, b.order, b.counters, st, 1);
-  if (cam.n_tiles > 0) backward_kernel<<<cam.n_tiles, 256, 0, st>>>(cam, b);
+  if (cam.n_tiles > 0) {
+    if (cam.shutter != SH_GLOBAL) {
+      constexpr size_t smem = sizeof(float4) * 8 * 32 * BwNF<2>::v;
+      static bool attr = false;
+      if (!attr) { cudaFuncSetAttribute(backward_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+      backward_kernel<2><<<cam.n_tiles, 256, smem, st>>>(cam, b);
+    } else {
+      backward_kernel<0><<<cam.n_tiles, 256, sizeof(float4) * 8 * 32 * BwNF<0>::v, st>>>(cam, b);
+    }
+  }
   if (s.n > 0) backward_finish_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, st>>>(cam, s, b);
 }
 

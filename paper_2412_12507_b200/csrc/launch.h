@@ -131,9 +131,12 @@ struct BwdBufs {
   uint32_t *order;              // tiles, longest list first (plan queue 1, n_tiles entries)
   uint32_t *seg_base;           // plan scratch (n_tiles)
   uint32_t *counters;           // the context's counters block (plan histogram)
+  const float *t0;              // per Gaussian centre shutter time (nullptr: global shutter)
   float *d_means, *d_rots, *d_scales, *d_opac, *d_sh, *d_rgb;  // outputs (d_rgb nullable)
 };
 void launch_backward(const DevCam &cam, const SceneDev &s, const BwdBufs &b, cudaStream_t st);
+// per Gaussian the shutter time of its centre (k1_project.cu; SH direction under rolling shutter)
+void launch_centre_times(const DevCam &cam, const SceneDev &s, float *t0, cudaStream_t st);
 
 // Supp. C projection quality (k1_project.cu); layout = gut_quality (include/gut.h)
 struct QualityRec {

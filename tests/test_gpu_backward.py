@@ -61,11 +61,17 @@ def _run(scene, cam, opt=None, seed=0, label=""):
     return gb, ob
 
 
-@pytest.mark.parametrize("variant", ["pinhole", "fisheye", "opencv"])
+@pytest.mark.parametrize("variant", ["pinhole", "fisheye", "opencv", "rs"])
 @pytest.mark.parametrize("deg", [0, 3])
 def test_tiny_backward(variant, deg):
     scene, cam = S.tiny(2, variant, n=96, sh_degree=deg)
     _run(scene, cam, seed=deg, label=f"{variant} deg {deg}")
+
+
+@pytest.mark.parametrize("variant,kdeg", [("pinhole", 4), ("fisheye", 3), ("rs", 8)])
+def test_tiny_backward_kernel_degree(variant, kdeg):
+    scene, cam = S.tiny(3, variant, n=96, sh_degree=1)
+    _run(scene, cam, S.RenderOptions(kernel_degree=kdeg), seed=kdeg, label=f"{variant} kernel degree {kdeg}")
 
 
 def test_tiny_backward_ragged_dense():
@@ -75,7 +81,8 @@ def test_tiny_backward_ragged_dense():
     _run(scene, cam, seed=5, label="ragged dense")
 
 
-@pytest.mark.parametrize("config,n,factor,view", [("multiview", 60_000, 0.12, 5), ("scannetpp", 30_000, 0.12, 3)])
+@pytest.mark.parametrize("config,n,factor,view", [("multiview", 60_000, 0.12, 5), ("scannetpp", 30_000, 0.12, 3),
+                                                  ("waymo", 40_000, 0.1, 1)])
 def test_reduced_config_backward(config, n, factor, view):
     scene = S.make_scene(config, n=n)
     cam = S.scaled_camera(S.make_views(config)[view], factor)
@@ -92,8 +99,7 @@ def test_backward_errors():
     with pytest.raises(gut.GutError) as e:   # camera differs from the last render
         r.backward(dataclasses.replace(cam, fx=cam.fx * 1.01), None, out, g)
     assert e.value.status == 1
-    for c2, o2 in ((S.tiny(0, "ortho", n=16)[1], None), (S.tiny(0, "rs", n=16)[1], None),
-                   (cam, S.RenderOptions(kbuffer=16)), (cam, S.RenderOptions(kernel_degree=4))):
+    for c2, o2 in ((S.tiny(0, "ortho", n=16)[1], None), (cam, S.RenderOptions(kbuffer=16))):
         out2 = r.render(c2, o2)[:3]
         with pytest.raises(gut.GutError) as e:
             r.backward(c2, o2, out2, torch.zeros_like(out2[0]))
