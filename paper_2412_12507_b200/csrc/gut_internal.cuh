@@ -254,6 +254,44 @@ __device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long 
 __device__ __forceinline__ unsigned long long mk_status(uint32_t epoch, uint32_t flag, uint32_t cnt) {
   return ((unsigned long long)epoch << 32) | ((unsigned long long)flag << 30) | (cnt & 0x3FFFFFFFu);
 }
+// Split form (k3_sort.cu): publish the partition's aggregate as soon as it is
+// known, then walk back later with a wider window of predecessors in flight.
+// A wave of CTAs publishes aggregates at about the same time, so a partition
+// j places into a wave sums ~j aggregates before it meets an inclusive word:
+// the window width sets the number of L2 round trips of that walk.
+__device__ __forceinline__ void lookback_publish(unsigned long long *status, int stride, int part, int col,
+                                                 uint32_t mine, uint32_t epoch) {
+  st_relaxed(&status[(size_t)part * stride + col], mk_status(epoch, part == 0 ? 2 : 1, mine));
+}
+template <int WIN>
+__device__ __forceinline__ uint32_t lookback_walk(unsigned long long *status, int stride, int part, int col,
+                                                  uint32_t mine, uint32_t epoch) {
+  if (part == 0) return 0;
+  uint32_t sum = 0;
+  int j = part - 1;
+  while (true) {
+    unsigned long long w[WIN];
+#pragma unroll
+    for (int q = 0; q < WIN; ++q) w[q] = j - q >= 0 ? ld_relaxed(&status[(size_t)(j - q) * stride + col]) : 0ull;
+    int used = 0;
+    bool fin = false;
+#pragma unroll
+    for (int q = 0; q < WIN; ++q) {
+      if (used != q || j - q < 0) break;
+      const unsigned long long s = w[q];
+      const uint32_t flag = (uint32_t)(s >> 30) & 3u;
+      if ((uint32_t)(s >> 32) != epoch || flag == 0) break;  // not ready yet: reload from here
+      sum += (uint32_t)s & 0x3FFFFFFFu;
+      ++used;
+      if (flag == 2) { fin = true; break; }
+    }
+    if (fin) break;
+    j -= used;
+  }
+  st_relaxed(&status[(size_t)part * stride + col], mk_status(epoch, 2, sum + mine));
+  return sum;
+}
+
 // exclusive prefix of `mine` for partition `part`, lane of status row `col`
 __device__ __forceinline__ uint32_t lookback(unsigned long long *status, int stride, int part, int col,
                                              uint32_t mine, uint32_t epoch) {

@@ -51,6 +51,9 @@ __device__ __forceinline__ void digit_scan2(uint32_t a, uint32_t b, uint32_t *s_
   __syncthreads();
 }
 
+#ifndef GUT_SORT_WIN
+#define GUT_SORT_WIN 8  // look-back predecessors loaded per round trip (16, 32 measured slower)
+#endif
 #ifndef GUT_SORT_BALLOT
 #define GUT_SORT_BALLOT 1  // digit peers by 9 ballots (measured faster than match.any)
 #endif
@@ -117,8 +120,10 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     rank[j] = valid ? (prev + before) : 0xFFFFFFFFu;
   }
   __syncthreads();
-  // per digit (threads 0..255): exclusive over warps, partition total, look-back
-  uint32_t tot = 0, gpre = 0, hv = 0;
+  // per digit (threads 0..255): exclusive over warps, partition total; the
+  // aggregate is published at once (the look-back walk comes after the
+  // shared-memory scatter, with the keys out of registers)
+  uint32_t tot = 0, hv = 0;
   if (threadIdx.x < 256) {
     const uint32_t dgt = threadIdx.x;
 #pragma unroll
@@ -127,16 +132,13 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
       s_wcnt[ww][dgt] = (uint16_t)tot;
       tot += c;
     }
-    gpre = lookback(status, 256, (int)part, (int)dgt, tot, epoch);
+    lookback_publish(status, 256, (int)part, (int)dgt, tot, epoch);
     hv = __ldg(&hist[dgt]);
   }
   // global digit start (exclusive scan of the pass histogram) and local digit start
   uint32_t hex, lex, ltotal;
   digit_scan2(hv, tot, s_tmp, hex, lex, ltotal);
-  if (threadIdx.x < 256) {
-    s_goff[threadIdx.x] = hex + gpre;
-    s_loff[threadIdx.x] = lex;
-  }
+  if (threadIdx.x < 256) s_loff[threadIdx.x] = lex;
   __syncthreads();
   // scatter into shared memory in digit order
 #pragma unroll
@@ -148,6 +150,9 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
       s_vals[pos] = val[j];
     }
   }
+  // decoupled look-back (window of GUT_SORT_WIN predecessors per round trip)
+  if (threadIdx.x < 256)
+    s_goff[threadIdx.x] = hex + lookback_walk<GUT_SORT_WIN>(status, 256, (int)part, (int)threadIdx.x, tot, epoch);
   __syncthreads();
   // coalesced write-out of the digit runs
   for (uint32_t p = threadIdx.x; p < ltotal; p += GUT_SORT_THREADS) {
