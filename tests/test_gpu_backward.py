@@ -99,6 +99,13 @@ def test_backward_errors():
     with pytest.raises(gut.GutError) as e:   # camera differs from the last render
         r.backward(dataclasses.replace(cam, fx=cam.fx * 1.01), None, out, g)
     assert e.value.status == 1
+    # empty scene: zero gradients, no error
+    empty = scene.subset(np.zeros(0, np.int64))
+    re_ = gut.Renderer(empty)
+    oe = re_.render(cam)[:3]
+    ge = re_.backward(cam, None, oe, torch.ones_like(oe[0]))
+    assert all(v.numel() == 0 for v in ge.values())
+    re_.close()
     for c2, o2 in ((S.tiny(0, "ortho", n=16)[1], None), (cam, S.RenderOptions(kbuffer=16))):
         out2 = r.render(c2, o2)[:3]
         with pytest.raises(gut.GutError) as e:
