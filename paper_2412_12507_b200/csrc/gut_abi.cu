@@ -633,7 +633,7 @@ gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const g
   if (!scene || !grads) return fail(ctx, GUT_E_INVALID_ARGUMENT, "scene / grads: NULL");
   if (!rgb || !alpha || !grad_rgb) return fail(ctx, GUT_E_INVALID_ARGUMENT, "rgb / alpha / grad_rgb: NULL");
   if (grad_depth && !depth) return fail(ctx, GUT_E_INVALID_ARGUMENT, "grad_depth needs the forward depth");
-  if (!grads->means || !grads->rotations || !grads->scales || !grads->opacities || !grads->sh)
+  if (scene->d.n > 0 && (!grads->means || !grads->rotations || !grads->scales || !grads->opacities || !grads->sh))
     return fail(ctx, GUT_E_INVALID_ARGUMENT, "grads: NULL buffer");
   DevCam dc;
   gut_status st_ = build_cam(ctx, cam, opt, dc);
