@@ -95,16 +95,21 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     if (!FIRST && !in) key[j] = 0xFFFFFFFFu;
     rank[j] = (in && (!FIRST || key[j] != GUT_CULLED_KEY)) ? 1u : 0u;  // validity until ranked
   }
-  // stable per-warp ranking, rounds in sequence order
+  // stable per-warp ranking, rounds in sequence order.  First pass: culled
+  // keys are interspersed, so validity is a 9th digit bit (9 ballots).  Later
+  // passes: the only invalid items are the tail past n -- the highest lanes
+  // of the last rounds of the last warps, after every valid item in sequence
+  // order -- so they rank as digit 255 behind the valid ones (8 ballots), are
+  // not written, and are taken off digit 255's partition total below.
+  constexpr int NB = FIRST ? 9 : 8;
 #pragma unroll
   for (int j = 0; j < GUT_SORT_ITEMS; ++j) {
     const bool valid = rank[j] != 0;
-    const uint32_t d = valid ? (key[j] >> shift) & 255u : 256u;
+    const uint32_t d = valid ? (key[j] >> shift) & 255u : (FIRST ? 256u : 255u);
 #if GUT_SORT_BALLOT
-    // peers with the same digit from 9 ballots (bit 8 = invalid)
     uint32_t peers = 0xffffffffu;
 #pragma unroll
-    for (int b = 0; b < 9; ++b) {
+    for (int b = 0; b < NB; ++b) {
       const bool bit = (d >> b) & 1u;
       const uint32_t bal = __ballot_sync(0xffffffffu, bit);
       peers &= bit ? bal : ~bal;
@@ -113,9 +118,10 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
 #endif
     const uint32_t before = __popc(peers & lt);
-    uint32_t prev = valid ? s_wcnt[w][d] : 0u;
+    const bool counted = FIRST ? valid : true;
+    uint32_t prev = counted ? s_wcnt[w][d & 255u] : 0u;
     __syncwarp();
-    if (valid && before == 0) s_wcnt[w][d] = (uint16_t)(prev + __popc(peers));
+    if (counted && before == 0) s_wcnt[w][d & 255u] = (uint16_t)(prev + __popc(peers));
     __syncwarp();
     rank[j] = valid ? (prev + before) : 0xFFFFFFFFu;
   }
@@ -132,6 +138,7 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
       s_wcnt[ww][dgt] = (uint16_t)tot;
       tot += c;
     }
+    if (!FIRST && dgt == 255u && base + GUT_SORT_PART > n) tot -= base + GUT_SORT_PART - n;  // the tail items
     lookback_publish(status, 256, (int)part, (int)dgt, tot, epoch);
     hv = __ldg(&hist[dgt]);
   }
