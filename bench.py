@@ -332,7 +332,7 @@ def run_ours(args):
                                                               ("scales", (N, 3)), ("opacities", (N,)),
                                                               ("sh", (N, nc, 3)))}
         grads = gut.gut_gradients(gbuf["means"].data_ptr(), gbuf["rotations"].data_ptr(), gbuf["scales"].data_ptr(),
-                                  gbuf["opacities"].data_ptr(), gbuf["sh"].data_ptr(), None)
+                                  gbuf["opacities"].data_ptr(), gbuf["sh"].data_ptr(), None, None)
 
         def fwd_bwd(v):
             gut.gut_render(ctx, scene, cams[v], gopt, out_dev, stream=stream, stats=False)

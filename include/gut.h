@@ -219,6 +219,10 @@ typedef struct {
   float *opacities;  /* [count] */
   float *sh;         /* [count][(sh_degree+1)^2][3] */
   float *rgb;        /* nullable: [count][3] gradient of the view's SH colour */
+  float *densify;    /* nullable: [count] densification statistic of this view, |dL/dmu| / (d / 2),
+                        d = distance from mu to the camera centre at mu's shutter time (PAPER L218:
+                        "3D positional gradients divided by half of the distance to the camera",
+                        reading R32) */
 } gut_gradients;
 
 /* Backward pass (PAPER Supp. B, L494-513; reading R30) of the LAST gut_render

@@ -64,7 +64,7 @@ class RenderFunction(torch.autograd.Function):
                                                            ("scales", (n, 3)), ("opacities", (n,)),
                                                            ("sh", (n, nc, 3)))}
         grads = gut.gut_gradients(*(g[k].data_ptr() for k in ("means", "rotations", "scales", "opacities", "sh")),
-                                  None)
+                                  None, None)
         p = lambda t: None if t is None else t.contiguous().data_ptr()  # noqa: E731
         g_rgb = g_rgb if g_rgb is not None else torch.zeros_like(rgb)
         gut.gut_render_backward(ctx.gctx.ctx, ctx.gctx.scene, ctx.gcam, ctx.gopt, rgb.data_ptr(), alpha.data_ptr(),

@@ -658,7 +658,7 @@ gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const g
   b.order = ctx->q1; b.seg_base = ctx->seg_base; b.counters = ctx->counters;  // (forward plan scratch, reused)
   b.t0 = dc.shutter != GUT_SHUTTER_GLOBAL ? ctx->gacc + (size_t)16 * (N > 0 ? N : 1) : nullptr;
   b.d_means = grads->means; b.d_rots = grads->rotations; b.d_scales = grads->scales; b.d_opac = grads->opacities;
-  b.d_sh = grads->sh; b.d_rgb = grads->rgb;
+  b.d_sh = grads->sh; b.d_rgb = grads->rgb; b.densify = grads->densify;
   launch_backward(dc, scene->d, b, (cudaStream_t)s);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ctx, GUT_E_CUDA, std::string("backward launch: ") + cudaGetErrorString(e));

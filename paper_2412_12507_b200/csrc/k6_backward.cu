@@ -292,6 +292,12 @@ __global__ __launch_bounds__(256) void backward_finish_kernel(DevCam c, SceneDev
     for (int r = 0; r < 3; ++r) m += (R[3 * j + r] / sv[r]) * acc[r];
     gm[j] = vis ? -m : 0.f;
   }
+  const double tc = B.t0 ? (double)B.t0[i] : 0.0;
+  const d3 dw = mkd(po.x, po.y, po.z) - mkd(c.c0[0] + tc * c.dc[0], c.c0[1] + tc * c.dc[1], c.c0[2] + tc * c.dc[2]);
+  if (B.densify) {  // PAPER L218 (reading R32): |dL/dmu| / (distance / 2)
+    const float gn = sqrtf(gm[0] * gm[0] + gm[1] * gm[1] + gm[2] * gm[2]);
+    B.densify[i] = gn / (0.5f * (float)sqrt(dot(dw, dw)));
+  }
   for (int r = 0; r < 3; ++r) {
     float t = 0.f;
     for (int j = 0; j < 3; ++j) {
@@ -316,8 +322,6 @@ __global__ __launch_bounds__(256) void backward_finish_kernel(DevCam c, SceneDev
   if (B.d_rgb) { B.d_rgb[3 * i] = acc[13]; B.d_rgb[3 * i + 1] = acc[14]; B.d_rgb[3 * i + 2] = acc[15]; }
   // SH (the forward's direction normalize(mu - c(t0)), t0 = mu's shutter time)
   const float4 col = vis ? B.payload[(size_t)GUT_PAYLOAD_F4 * i + 4] : make_float4(0.f, 0.f, 0.f, 0.f);
-  const double tc = B.t0 ? (double)B.t0[i] : 0.0;
-  const d3 dw = mkd(po.x, po.y, po.z) - mkd(c.c0[0] + tc * c.dc[0], c.c0[1] + tc * c.dc[1], c.c0[2] + tc * c.dc[2]);
   const f3 d = tof((1.0 / sqrt(dot(dw, dw))) * dw);
   const float x = d.x, y = d.y, z = d.z, xx = x * x, yy = y * y, zz = z * z;
   float Y[16];

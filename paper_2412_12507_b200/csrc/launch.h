@@ -133,6 +133,7 @@ struct BwdBufs {
   uint32_t *counters;           // the context's counters block (plan histogram)
   const float *t0;              // per Gaussian centre shutter time (nullptr: global shutter)
   float *d_means, *d_rots, *d_scales, *d_opac, *d_sh, *d_rgb;  // outputs (d_rgb nullable)
+  float *densify;               // nullable: |dL/dmu| / (distance / 2)
 };
 void launch_backward(const DevCam &cam, const SceneDev &s, const BwdBufs &b, cudaStream_t st);
 // per Gaussian the shutter time of its centre (k1_project.cu; SH direction under rolling shutter)

@@ -70,7 +70,7 @@ class gut_proj_record(C.Structure):
 
 class gut_gradients(C.Structure):
     _fields_ = [("means", C.c_void_p), ("rotations", C.c_void_p), ("scales", C.c_void_p), ("opacities", C.c_void_p),
-                ("sh", C.c_void_p), ("rgb", C.c_void_p)]
+                ("sh", C.c_void_p), ("rgb", C.c_void_p), ("densify", C.c_void_p)]
 
 
 EXPORTS = ["gut_abi_version", "gut_options_default", "gut_context_create", "gut_context_destroy",
@@ -329,8 +329,9 @@ class Renderer:
         dev = torch.device("cuda", self.device)
         g = {k: torch.empty(sz, device=dev) for k, sz in (("means", (n, 3)), ("rotations", (n, 4)), ("scales", (n, 3)),
                                                            ("opacities", (n,)), ("sh", (n, self.nc, 3)),
-                                                           ("rgb", (n, 3)))}
-        gg = gut_gradients(*(g[k].data_ptr() for k in ("means", "rotations", "scales", "opacities", "sh", "rgb")))
+                                                           ("rgb", (n, 3)), ("densify", (n,)))}
+        gg = gut_gradients(*(g[k].data_ptr() for k in ("means", "rotations", "scales", "opacities", "sh", "rgb",
+                                                         "densify")))
         p = lambda t: None if t is None else t.contiguous().data_ptr()  # noqa: E731
         gut_render_backward(self.ctx, self.scene, make_camera(cam), make_options(opt), p(out[0]), p(out[1]),
                             p(out[2]) if grad_depth is not None else p(out[2]), p(grad_rgb), p(grad_alpha),

@@ -56,6 +56,14 @@ def _run(scene, cam, opt=None, seed=0, label=""):
         i = np.unravel_index(np.argmax(err), err.shape) if err.size else None
         print(f"{label} {f}: max |d| {np.abs(a - b).max(initial=0):.3e} (max |g| {scale:.3e}) ratio {err.max(initial=0):.3f}"
               + (f" at {i}: gpu {a[i]:.6e} oracle {b[i]:.6e}" if i is not None else ""))
+    # densification statistic (reading R32): |dL/dmu| / (distance / 2)
+    p = O.preprocess(scene, cam, opt)
+    cen = np.array([O.pose_at(cam, t)[1] for t in p["t0"]]) if cam.shutter != "global" else np.array(cam.c_w[0])
+    dist = np.linalg.norm(scene.means.astype(np.float64) - cen, axis=-1)
+    want = np.linalg.norm(ob["means"], axis=1) / (0.5 * dist)
+    got = gb["densify"].cpu().numpy().astype(np.float64)
+    ok = p["reason"] == 0
+    np.testing.assert_allclose(got[ok], want[ok], rtol=5e-3, atol=2e-4 * want.max() + 1e-12)
     r.close()
     assert worst <= 1.0, label
     return gb, ob
