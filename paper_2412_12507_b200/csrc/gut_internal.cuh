@@ -292,39 +292,5 @@ __device__ __forceinline__ uint32_t lookback_walk(unsigned long long *status, in
   return sum;
 }
 
-// exclusive prefix of `mine` for partition `part`, lane of status row `col`
-__device__ __forceinline__ uint32_t lookback(unsigned long long *status, int stride, int part, int col,
-                                             uint32_t mine, uint32_t epoch) {
-  if (part == 0) {
-    st_relaxed(&status[col], mk_status(epoch, 2, mine));
-    return 0;
-  }
-  st_relaxed(&status[(size_t)part * stride + col], mk_status(epoch, 1, mine));
-  // walk back over windows of 8 predecessors loaded together (independent
-  // loads: one round trip per window instead of one per partition)
-  uint32_t sum = 0;
-  int j = part - 1;
-  while (true) {
-    unsigned long long w[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) w[q] = j - q >= 0 ? ld_relaxed(&status[(size_t)(j - q) * stride + col]) : 0ull;
-    int used = 0;
-    bool fin = false;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (used != q || j - q < 0) break;
-      const unsigned long long s = w[q];
-      const uint32_t flag = (uint32_t)(s >> 30) & 3u;
-      if ((uint32_t)(s >> 32) != epoch || flag == 0) break;  // not ready yet: reload from here
-      sum += (uint32_t)s & 0x3FFFFFFFu;
-      ++used;
-      if (flag == 2) { fin = true; break; }
-    }
-    if (fin) break;
-    j -= used;
-  }
-  st_relaxed(&status[(size_t)part * stride + col], mk_status(epoch, 2, sum + mine));
-  return sum;
-}
 
 }  // namespace gut
