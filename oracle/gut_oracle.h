@@ -14,6 +14,10 @@
  *   O4 per-tile depth-ordered lists
  *   O5 pixel rays
  *   O6 front-to-back compositing, 3D max response PAPER L115-121 (Eq.5), L192-200 (Eq.11)
+ *   O6' per-ray k-buffer / exact tau order        PAPER L205-212 (Sec. 4.3, "Ours (sorted)")
+ *   generalized kernels of degree n              PAPER L454-462 (Supp. A)
+ *   O7 backward of O6 (gradients)                PAPER L202, L494-513 (Supp. B), L218
+ *   O8 projection quality (UT / EWA / MC, KL)     PAPER L98-102 (Eq. 3), L522-588 (Supp. C)
  * Readings of silent/ambiguous points are listed in DESIGN.md "Readings".
  */
 #ifndef GUT_ORACLE_H
