@@ -143,7 +143,7 @@ typedef struct { double ut[5], ewa[5], mc[5], kl_ut, kl_ewa; int32_t valid, pad;
 void orc_projection_quality(const float *means, const float *rots, const float *scales, int64_t n,
                             const orc_camera *cam, const orc_options *o, int32_t n_mc, uint64_t seed,
                             orc_quality *out);
-/* ---- O7 (backward, Supp. B; "Ours" order, degree 2, reading R30) ----
+/* ---- O7 (backward, Supp. B; "Ours" order, any degree and shutter, reading R30) ----
  * upstream g_rgb [H][W][3], g_alpha [H][W], g_depth [H][W] (fp32);
  * outputs (fp64): d_means [n][3], d_rots [n][4], d_scales [n][3], d_opac [n],
  * d_sh [n][(d+1)^2][3], d_rgb [n][3] (gradient of the view's colour). Returns K. */
