@@ -42,19 +42,19 @@ def _proj_parity(scene, cam, g, o_proj, opt=OPT):
     # covariance within 1e-3 relative (fp32 pixel coordinates)
     # (the debug record is fp32: add its own representation error, 2 ulp, for
     # the "wide" Gaussians whose fp64 ellipse sits far from the image)
-    # Relative term 1e-6 * extent: R(q) and s are formed from the fp32 inputs on
+    # Relative term 2e-6 * extent: R(q) and s are formed from the fp32 inputs on
     # the GPU, so sigma points differ from the fp64 oracle's by ~1e-7 relative,
     # which the projection of edge-on Gaussians grazing the near plane (extents
     # of 10^4 px) amplifies; their tile sets still match bit for bit (above).
     hx_o, hy_o = o_proj["hx"][both], o_proj["hy"][both]
     for v, h_o in (("vx", hx_o), ("vy", hy_o)):
-        tol = 5e-4 + 1e-6 * h_o + 2 * np.spacing(np.abs(gp[v][both]).astype(np.float32)).astype(np.float64)
+        tol = 5e-4 + 2e-6 * h_o + 2 * np.spacing(np.abs(gp[v][both]).astype(np.float32)).astype(np.float64)
         assert np.all(np.abs(gp[v][both] - o_proj[v][both]) < tol), v
     for f, h in (("cxx", "hx"), ("cyy", "hy")):
         rel = np.abs(gp[f][both] - o_proj[f][both]) / np.abs(o_proj[f][both])
         assert rel.max(initial=0) < 1e-3, f
         hg = np.sqrt(gp["k2"][both].astype(np.float64) * gp[f][both])
-        assert np.all(np.abs(hg - o_proj[h][both]) < 5e-4 + 1e-6 * o_proj[h][both]), h
+        assert np.all(np.abs(hg - o_proj[h][both]) < 5e-4 + 2e-6 * o_proj[h][both]), h
     sc = np.sqrt(o_proj["cxx"][both] * o_proj["cyy"][both])
     assert (np.abs(gp["cxy"][both] - o_proj["cxy"][both]) / sc).max(initial=0) < 1e-3
     rel = np.abs(gp["depth"][both] - o_proj["depth"][both]) / o_proj["depth"][both]
@@ -195,13 +195,15 @@ def test_segmented_blend(config, n, factor, view, seg, window, monkeypatch):
     assert int(g["counters"][CNT_NITEMS]) >= len(lens) + (lens > seg).sum(), "segments in effect"
 
 
-def test_full_size_sampled_tiles():
-    """BASELINE configs[4] (3M Gaussians, 1920x1080 fisheye) in the launch
-    configuration bench.py times: sampled tiles against the oracle -- 16
-    random tiles and the 8 longest lists (split into segments, re-runs)."""
+@pytest.mark.parametrize("config,view", [("multiview", 0), ("waymo", 1), ("mipnerf360", 3), ("scannetpp", 5)])
+def test_full_size_sampled_tiles(config, view):
+    """Every BASELINE config at full size (multiview: configs[4] in the launch
+    configuration bench.py times; waymo: 2M Gaussians, OpenCV + rolling
+    shutter 1920x1280): 16 random tiles and the 8 longest lists (split into
+    segments, re-runs) against the oracle."""
     from oracle import oracle as O
-    scene = S.make_scene("multiview")
-    cam = S.make_views("multiview")[0]
+    scene = S.make_scene(config)
+    cam = S.make_views(config)[view]
     g = gpu_render(scene, cam, reserve=int(scene.count * 12))
     tx, ty = cam.tiles
     rng = np.random.default_rng(0)
@@ -218,7 +220,7 @@ def test_full_size_sampled_tiles():
     assert mask.sum() > 0.9 * 24 * 256 * 0.9
     e_rgb = np.abs(g["rgb"] - o["rgb"]).max(-1)[mask].max()
     e_a = np.abs(g["alpha"] - o["alpha"])[mask].max()
-    print(f"full-size sampled: rgb {e_rgb:.2e} alpha {e_a:.2e}; K={g['stats']['n_keys']}")
+    print(f"full-size sampled {config}: rgb {e_rgb:.2e} alpha {e_a:.2e}; K={g['stats']['n_keys']}")
     assert e_rgb <= TOL_RGB and e_a <= TOL_RGB
     _proj_parity(scene, cam, g, o["proj"])
 
