@@ -361,6 +361,10 @@ gut_status gut_workspace_reserve(gut_context *ctx, int64_t max_keys, int64_t max
   size_t tiles = (size_t)((max_w + 15) / 16) * ((max_h + 15) / 16);
   if ((s = ensure_tiles(ctx, tiles)) != GUT_OK) return s;
   if ((s = ensure_pix(ctx, (size_t)max_w * max_h)) != GUT_OK) return s;
+  // blend work items of either compositing order (segments of "Ours", 8x4
+  // units of the k-buffer) so that a reserved render never allocates
+  const size_t items = std::max(tiles + (size_t)max_keys / (size_t)ctx->blend_seg + 2, 2 * tiles + 2);
+  if ((s = ensure_items(ctx, items)) != GUT_OK) return s;
   ctx->reserved = true;
   return GUT_OK;
 }
