@@ -752,7 +752,8 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
     for (size_t i = 0; i < N; ++i) {
       memset(&r[i], 0, sizeof(r[i]));
       // tile code (gut_internal.cuh ell_tile_code) -> tile count
-      r[i].tiles = (tl[i] >> 31) ? (tl[i] & 0x7FFFFFFFu) : (uint32_t)__builtin_popcount(tl[i] & 0x1FFu);
+      r[i].tiles = (tl[i] >> 31) ? (tl[i] & 0x7FFFFFFFu)
+                                 : (uint32_t)__builtin_popcount(tl[i] & ((tl[i] >> 30) ? 0xFFFFu : 0x1FFu));
       if (!tl[i]) continue;
       float4 a = el[2 * i], b = el[2 * i + 1], p4 = pl[GUT_PAYLOAD_F4 * i + 4];
       r[i].vx = a.x; r[i].vy = a.y; r[i].cxx = a.z; r[i].cxy = a.w; r[i].cyy = b.x; r[i].k2 = fabsf(b.y);

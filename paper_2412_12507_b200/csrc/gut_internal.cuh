@@ -206,15 +206,16 @@ __device__ __forceinline__ int ell_tile_count(const EllT<Real> &e, int tile_cull
   return n;
 }
 
-// K1 -> K2 tile code per Gaussian: 0 = culled; bit 31 clear: tile rectangle
-// of at most 3x3 tiles, bits 0-8 = hit mask (row-major over the rectangle),
-// bits 9-19 = x0, bits 20-30 = y0; bit 31 set: bits 0-30 = tile count (K2
-// walks the rows of the ellipse record).  Counts and masks come from the same
+// K1 -> K2 tile code per Gaussian: 0 = culled; bits 31, 30 clear: tile
+// rectangle of at most 3x3 tiles, bits 0-8 = hit mask (row-major over the
+// rectangle), bits 9-19 = x0, bits 20-29 = y0; bit 30 set: at most 4x4 tiles
+// (x0, y0 < 128), bits 0-15 = hit mask, bits 16-22 = x0, bits 23-29 = y0;
+// bit 31 set: bits 0-30 = tile count (K2 walks the rows of the ellipse record).  Counts and masks come from the same
 // row_span() calls, so K2 emits exactly the counted keys.
 template <class Real>
 __device__ __forceinline__ uint32_t ell_tile_code(const EllT<Real> &e, int tile_cull) {
   const int w = e.x1 - e.x0 + 1, h = e.y1 - e.y0 + 1;
-  if (w <= 3 && h <= 3 && e.x0 < 2048 && e.y0 < 2048) {
+  if (w <= 3 && h <= 3 && e.x0 < 2048 && e.y0 < 1024) {
     uint32_t mask = 0;
     for (int r = 0; r < h; ++r) {
       int lo, hi;
@@ -223,11 +224,21 @@ __device__ __forceinline__ uint32_t ell_tile_code(const EllT<Real> &e, int tile_
     }
     return mask ? (mask | ((uint32_t)e.x0 << 9) | ((uint32_t)e.y0 << 20)) : 0u;
   }
+  if (w <= 4 && h <= 4 && e.x0 < 128 && e.y0 < 128) {  // 4x4 hit mask (bit 30)
+    uint32_t mask = 0;
+    for (int r = 0; r < h; ++r) {
+      int lo, hi;
+      row_span(e, e.y0 + r, tile_cull, lo, hi);
+      for (int x = lo; x <= hi; ++x) mask |= 1u << (4 * r + (x - e.x0));
+    }
+    return mask ? (0x40000000u | mask | ((uint32_t)e.x0 << 16) | ((uint32_t)e.y0 << 23)) : 0u;
+  }
   const int n = ell_tile_count(e, tile_cull);
   return n > 0 ? (0x80000000u | (uint32_t)min(n, 0x7FFFFFFF)) : 0u;
 }
 __device__ __forceinline__ uint32_t code_count(uint32_t code) {
-  return (code >> 31) ? (code & 0x7FFFFFFFu) : (uint32_t)__popc(code & 0x1FFu);
+  return (code >> 31) ? (code & 0x7FFFFFFFu)
+                      : (uint32_t)__popc(code & ((code >> 30) ? 0xFFFFu : 0x1FFu));
 }
 
 __device__ __forceinline__ Ell load_ell(const float4 *ell, uint32_t g) {

@@ -100,10 +100,13 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
     big[j] = (code[j] >> 31) != 0u;
     bpos[j] = pos;
     if (!big[j] && code[j]) {
-      const uint32_t x0 = (code[j] >> 9) & 0x7FFu, y0 = (code[j] >> 20) & 0x7FFu;
-      for (uint32_t m = code[j] & 0x1FFu; m; m &= m - 1) {
+      const bool m4 = (code[j] >> 30) & 1u;  // 4x4 mask format
+      const uint32_t x0 = m4 ? (code[j] >> 16) & 0x7Fu : (code[j] >> 9) & 0x7FFu;
+      const uint32_t y0 = m4 ? (code[j] >> 23) & 0x7Fu : (code[j] >> 20) & 0x3FFu;
+      const uint32_t cw = m4 ? 4u : 3u;
+      for (uint32_t m = code[j] & (m4 ? 0xFFFFu : 0x1FFu); m; m &= m - 1) {
         const uint32_t b = (uint32_t)(__ffs(m) - 1);
-        const uint32_t tile = (y0 + b / 3u) * (uint32_t)tiles_x + x0 + b % 3u;
+        const uint32_t tile = (y0 + b / cw) * (uint32_t)tiles_x + x0 + b % cw;
         emit_key(pos++, tile, g[j], cap_k, out_tile, out_gid, s_hist, counters);
       }
     } else {
