@@ -193,8 +193,11 @@ const char *gut_last_error(const gut_context *ctx);
 /* Capacity mode: pre-size the workspace for up to max_keys (Gaussian,tile)
  * keys, max_gaussians Gaussians and max_w x max_h images.  After this call
  * gut_render never synchronises; a frame whose key count exceeds max_keys is
- * truncated and reported through gut_stats.overflow / GUT_E_CAPACITY on the
- * next call that synchronises.  Without it, gut_render reads the key count
+ * truncated (its image is wrong) and the overflow is latched in a sticky
+ * device word that the per-render reset does not clear.  It is reported --
+ * and cleared -- as GUT_E_CAPACITY (plus gut_stats.overflow = 1) by the next
+ * synchronising call on the context: gut_render with stats != NULL,
+ * gut_timing_read or gut_check.  Without it, gut_render reads the key count
  * back (one stream sync per view) and grows the workspace. */
 gut_status gut_workspace_reserve(gut_context *ctx, int64_t max_keys, int64_t max_gaussians,
                                  int32_t max_w, int32_t max_h);
@@ -275,6 +278,11 @@ gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_
  * (order of gut_stats.ms_stage), *n_renders the number of renders summed;
  * reset != 0 clears the accumulator. */
 gut_status gut_timing_read(gut_context *ctx, double ms_sum[7], int32_t *n_renders, int32_t reset);
+
+/* Synchronises `s` and reports whether any render issued on ctx since the
+ * last synchronising call overflowed its reserved key capacity
+ * (GUT_E_CAPACITY; the latch is cleared) -- GUT_OK otherwise. */
+gut_status gut_check(gut_context *ctx, gut_stream s);
 
 /* Tests only: copies an intermediate buffer of the LAST render on ctx to host
  * memory (synchronises).  *bytes_needed receives the size; if host_dst is

@@ -437,15 +437,35 @@ void orc_preprocess(const float *means, const float *rots, const float *scales, 
 
 /* ======================================================================
  * O4 — per-tile lists in global depth order ("3DGS sorts them
- * globally for each tile"); ties by Gaussian index (reading R13).
+ * globally for each tile").  The sort key is the 3DGS key: the depth as a
+ * 32-bit float, (float)depth, with ties by Gaussian index (readings R13,
+ * R13'; SURVEY §8(a)-2 keys = tile << 32 | float bits of the depth).
  * ====================================================================== */
-typedef struct { int32_t tile; int32_t gid; double depth; } orc_key;
+typedef struct { int32_t tile; int32_t gid; float depth; } orc_key;
 
 static int key_cmp(const void *a, const void *b) {
   const orc_key *x = (const orc_key *)a, *y = (const orc_key *)b;
   if (x->tile != y->tile) return x->tile < y->tile ? -1 : 1;
   if (x->depth != y->depth) return x->depth < y->depth ? -1 : 1;
   return x->gid < y->gid ? -1 : (x->gid > y->gid);
+}
+
+/* Parity diagnostic for the order of two consecutive contributing entries
+ * with fp64 depths di, dj: the smallest relative perturbation of the depths
+ * that could change their order under the (fp32 key, index) rule.  Keys two
+ * or more fp32 steps apart: the relative depth gap.  Equal or adjacent keys:
+ * the distance of either depth to the nearest fp32 rounding boundary (a key
+ * that stays the same keeps the index tie-break). */
+static double rounding_margin(double d) {
+  float f = (float)d;
+  double lo = 0.5 * ((double)f + (double)nextafterf(f, 0.f));
+  double hi = 0.5 * ((double)f + (double)nextafterf(f, INFINITY));
+  return fmin(fabs(d - lo), fabs(hi - d)) / fabs(d);
+}
+static double order_margin(double di, double dj) {
+  float ki = (float)di, kj = (float)dj, km = ki > kj ? ki : kj, kl = ki > kj ? kj : ki;
+  if (nextafterf(kl, INFINITY) < km) return fabs(dj - di) / fmax(di, dj);
+  return fmin(rounding_margin(di), rounding_margin(dj));
 }
 
 int64_t orc_tile_lists(const orc_proj *proj, int64_t n, const orc_camera *cam, const orc_options *o,
@@ -462,7 +482,7 @@ int64_t orc_tile_lists(const orc_proj *proj, int64_t n, const orc_camera *cam, c
   for (int64_t i = 0; i < n; ++i) {
     if (proj[i].reason != ORC_OK) continue;
     int m = kept_tiles(&proj[i], o->tile_cull, tx_n, buf);
-    for (int j = 0; j < m; ++j) { keys[w].tile = buf[j]; keys[w].gid = (int32_t)i; keys[w].depth = proj[i].depth; ++w; }
+    for (int j = 0; j < m; ++j) { keys[w].tile = buf[j]; keys[w].gid = (int32_t)i; keys[w].depth = (float)proj[i].depth; ++w; }
   }
   qsort(keys, (size_t)K, sizeof(orc_key), key_cmp);
   for (int t = 0; t < tx_n * ty_n; ++t) { ranges[2 * t] = 0; ranges[2 * t + 1] = 0; }
@@ -702,7 +722,7 @@ static void composite_pixel_sorted(const orc_gauss *G, const int32_t *gids, int3
     /* order ambiguity over the hits that reached the buffer: stream (depth key)
      * neighbours and tau_max neighbours */
     for (int32_t i = 1; i < used; ++i) {
-      double rg = fabs(dk[i] - dk[i - 1]) / fmax(dk[i], dk[i - 1]);
+      double rg = order_margin(dk[i - 1], dk[i]);
       if (rg < dg->min_order_gap) dg->min_order_gap = rg;
     }
     qsort(tau, (size_t)used, sizeof(double), dbl_cmp);
@@ -744,7 +764,7 @@ static void composite_pixel(const orc_gauss *G, const int32_t *gids, int32_t a, 
       if (tg < dg->min_term_gap) dg->min_term_gap = tg;
       double dep = depth_of ? depth_of[gids[k]] : 0;
       if (prev_depth >= 0 && depth_of) {
-        double rg = fabs(dep - prev_depth) / fmax(dep, prev_depth);
+        double rg = order_margin(prev_depth, dep);
         if (rg < dg->min_order_gap) dg->min_order_gap = rg;
       }
       prev_depth = dep;
@@ -800,8 +820,8 @@ void orc_composite(const float *means, const float *rots, const float *scales, c
   free(G); free(dep);
 }
 
-/* order of the brute-force list: (depth, index) */
-typedef struct { double depth; int32_t gid; } orc_dk;
+/* order of the brute-force list: ((float)depth, index) as O4 */
+typedef struct { float depth; int32_t gid; } orc_dk;
 static int dk_cmp(const void *a, const void *b) {
   const orc_dk *x = (const orc_dk *)a, *y = (const orc_dk *)b;
   if (x->depth != y->depth) return x->depth < y->depth ? -1 : 1;
@@ -826,12 +846,12 @@ int64_t orc_render(const float *means, const float *rots, const float *scales, c
     orc_tile_lists(proj, n, cam, o, means, scales, tiles, gids, K, ranges);
   } else {
     /* brute force (SURVEY §8(c).2 mode B): every Gaussian valid through O1-O3
-     * (ignoring rectangles and tiles), sorted by (depth, index), at every pixel */
+     * (ignoring rectangles and tiles), sorted by ((float)depth, index), at every pixel */
     orc_dk *l = (orc_dk *)malloc(sizeof(orc_dk) * (size_t)(n > 0 ? n : 1));
     int64_t m = 0;
     for (int64_t i = 0; i < n; ++i) {
       int r = proj[i].reason;
-      if (r == ORC_OK || r == ORC_CULL_OFFSCREEN || r == ORC_CULL_NOTILE) { l[m].depth = proj[i].depth; l[m].gid = (int32_t)i; ++m; }
+      if (r == ORC_OK || r == ORC_CULL_OFFSCREEN || r == ORC_CULL_NOTILE) { l[m].depth = (float)proj[i].depth; l[m].gid = (int32_t)i; ++m; }
     }
     qsort(l, (size_t)m, sizeof(orc_dk), dk_cmp);
     gids = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));

@@ -79,7 +79,9 @@ typedef struct {
   int32_t visited, contributed, terminated, invalid;
   double min_alpha_gap;    /* min |alpha - alpha_min| over visited entries */
   double min_term_gap;     /* min |T' - T_min| over blended/stopping entries */
-  double min_order_gap;    /* min relative depth gap between consecutive contributing entries */
+  double min_order_gap;    /* min order margin of consecutive contributing entries: the relative
+                              depth perturbation that could swap them under the (fp32 key, index)
+                              order (gut_oracle.c order_margin) */
   int32_t amb_bin;         /* a binning-ambiguous pair could change this pixel */
   int32_t amb_cull;        /* a cull-ambiguous Gaussian could change this pixel */
   double min_tau_gap;      /* kbuffer != 0: min relative tau_max gap between two hits adjacent

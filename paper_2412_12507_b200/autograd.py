@@ -16,12 +16,18 @@ from . import gut
 
 
 class _Ctx:
-    """A libgut context reused across steps (the scene is re-packed per call)."""
+    """A libgut context reused across steps (the scene is re-packed per call).
+
+    gut_render_backward differentiates the context's LAST render (its lists and
+    workspace), so each backward must belong to the most recent forward on
+    this context: `seq` counts forwards and backward() checks it (render
+    several views before one backward with one _Ctx per outstanding view)."""
 
     def __init__(self, device: int = 0):
         self.device = device
         self.ctx = gut.gut_context_create(device)
         self.scene = None
+        self.seq = 0
 
     def close(self):
         if self.ctx:
@@ -38,10 +44,17 @@ class RenderFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, gctx: _Ctx, cam, opt, sh_degree: int, means, rotations, scales, opacities, sh):
+        # progressive SH (the 3DGS schedule): sh may store more coefficients than
+        # the active degree uses; only the first (d+1)^2 are packed and get gradients
+        nc = (sh_degree + 1) ** 2
+        if sh.dim() != 3 or sh.shape[2] != 3 or sh.shape[1] < nc:
+            raise ValueError(f"sh must be [N, >= {nc}, 3] for sh_degree {sh_degree}, got {tuple(sh.shape)}")
         if gctx.scene:
             gut.gut_scene_destroy(gctx.ctx, gctx.scene)
         gctx.scene = gut.gut_scene_create(gctx.ctx, means.detach(), rotations.detach(), scales.detach(),
-                                          opacities.detach(), sh.detach(), sh_degree)
+                                          opacities.detach(), sh.detach()[:, :nc].contiguous(), sh_degree)
+        gctx.seq += 1
+        ctx.seq = gctx.seq
         dev = means.device
         H, W = cam.height, cam.width
         rgb = torch.empty((H, W, 3), device=dev)
@@ -51,12 +64,15 @@ class RenderFunction(torch.autograd.Function):
         out = gut.gut_outputs(rgb.data_ptr(), alpha.data_ptr(), depth.data_ptr(), 1, 0)
         gut.gut_render(gctx.ctx, gctx.scene, gcam, gopt, out, stats=False)
         ctx.gctx, ctx.gcam, ctx.gopt = gctx, gcam, gopt
-        ctx.n, ctx.nc = means.shape[0], sh.shape[1]
+        ctx.n, ctx.nc, ctx.nc_stored = means.shape[0], nc, sh.shape[1]
         ctx.save_for_backward(rgb, alpha, depth)
         return rgb, alpha, depth
 
     @staticmethod
     def backward(ctx, g_rgb, g_alpha, g_depth):
+        if ctx.seq != ctx.gctx.seq:
+            raise RuntimeError("gut backward: this render is no longer the context's last render "
+                               "(one backward per forward, in order; use one context per outstanding view)")
         rgb, alpha, depth = ctx.saved_tensors
         dev = rgb.device
         n, nc = ctx.n, ctx.nc
@@ -69,7 +85,10 @@ class RenderFunction(torch.autograd.Function):
         g_rgb = g_rgb if g_rgb is not None else torch.zeros_like(rgb)
         gut.gut_render_backward(ctx.gctx.ctx, ctx.gctx.scene, ctx.gcam, ctx.gopt, rgb.data_ptr(), alpha.data_ptr(),
                                 depth.data_ptr(), p(g_rgb), p(g_alpha), p(g_depth), grads)
-        return (None, None, None, None, g["means"], g["rotations"], g["scales"], g["opacities"], g["sh"])
+        g_sh = g["sh"]
+        if ctx.nc_stored > nc:  # coefficients above the active degree: zero gradient
+            g_sh = torch.cat([g_sh, torch.zeros((n, ctx.nc_stored - nc, 3), device=dev)], dim=1)
+        return (None, None, None, None, g["means"], g["rotations"], g["scales"], g["opacities"], g_sh)
 
 
 def render(gctx: _Ctx, means, rotations, scales, opacities, sh, sh_degree: int, cam, opt=None):

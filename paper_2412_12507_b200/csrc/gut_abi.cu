@@ -323,8 +323,9 @@ gut_status gut_context_create(int32_t dev, gut_context **out) {
     int v = atoi(e);
     if (v >= 1 && v <= 255) ctx->blend_window = v;  // (queue-1 entries carry the segment in 8 bits)
   }
-  if (cudaMalloc((void **)&ctx->counters, CNT_WORDS * sizeof(uint32_t)) != cudaSuccess ||
-      cudaMallocHost((void **)&ctx->h_counters, CNT_WORDS * sizeof(uint32_t)) != cudaSuccess) {
+  if (cudaMalloc((void **)&ctx->counters, CNT_ALLOC * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMallocHost((void **)&ctx->h_counters, CNT_ALLOC * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemset(ctx->counters, 0, CNT_ALLOC * sizeof(uint32_t)) != cudaSuccess) {
     delete ctx;
     return fail(nullptr, GUT_E_OUT_OF_MEMORY, "counters");
   }
@@ -437,6 +438,20 @@ void gut_scene_destroy(gut_context *ctx, gut_scene *sc) {
   if (sc->d.scale) cudaFree(sc->d.scale);
   if (sc->d.sh) cudaFree(sc->d.sh);
   delete sc;
+}
+
+
+// Reads and clears the sticky overflow word (CNT_STICKY_OVERFLOW, outside the
+// per-render memset) after the work queued on `st` -- i.e. every render issued
+// on this context before the call -- has finished.  Synchronises st.
+static gut_status take_sticky(gut_context *ctx, cudaStream_t st, bool &overflow) {
+  overflow = false;
+  uint32_t *w = ctx->counters + CNT_STICKY_OVERFLOW;
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_counters + CNT_STICKY_OVERFLOW, w, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemsetAsync(w, 0, sizeof(uint32_t), st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  overflow = ctx->h_counters[CNT_STICKY_OVERFLOW] != 0;
+  return GUT_OK;
 }
 
 static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut_camera *cam, const gut_options *opt,
@@ -614,7 +629,9 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
     stats->pairs_evaluated = (int64_t)pe;
     stats->pairs_contributing = (int64_t)pc;
     stats->pixels_terminated = (int64_t)pt;
-    stats->overflow = (h[CNT_OVERFLOW] != 0 || K > ctx->cap_k) ? 1 : 0;
+    bool sticky = false;  // a truncated earlier render (stats = NULL) is reported here too
+    if ((s = take_sticky(ctx, st, sticky)) != GUT_OK) return s;
+    stats->overflow = (h[CNT_OVERFLOW] != 0 || K > ctx->cap_k || sticky) ? 1 : 0;
     if (timing) {
       for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&stats->ms_stage[i], ev[i], ev[i + 1]);
       cudaEventElapsedTime(&stats->ms_stage[6], ev[0], ev[6]);
@@ -715,6 +732,21 @@ gut_status gut_timing_read(gut_context *ctx, double ms_sum[7], int32_t *n_render
   }
   if (n_renders) *n_renders = (int32_t)ctx->tnext;
   if (reset) ctx->tnext = 0;
+  CUDA_TRY(ctx, cudaDeviceSynchronize());  // (renders without timing events too)
+  bool sticky = false;
+  gut_status s = take_sticky(ctx, (cudaStream_t)0, sticky);
+  if (s != GUT_OK) return s;
+  if (sticky) return fail(ctx, GUT_E_CAPACITY, "key capacity exceeded by an earlier render (gut_workspace_reserve)");
+  return GUT_OK;
+}
+
+gut_status gut_check(gut_context *ctx, gut_stream stream) {
+  if (!ctx) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "ctx: NULL");
+  cudaSetDevice(ctx->device);
+  bool sticky = false;
+  gut_status s = take_sticky(ctx, (cudaStream_t)stream, sticky);
+  if (s != GUT_OK) return s;
+  if (sticky) return fail(ctx, GUT_E_CAPACITY, "key capacity exceeded by an earlier render (gut_workspace_reserve)");
   return GUT_OK;
 }
 

@@ -56,6 +56,7 @@ __device__ __forceinline__ void emit_key(uint32_t pos, uint32_t tile, uint32_t g
     atomicAdd(&s_hist[1][(tile >> 8) & 255u], 1u);
   } else {
     counters[CNT_OVERFLOW] = 1u;
+    counters[CNT_STICKY_OVERFLOW] = 1u;  // latched until the host reads it (gut_check)
   }
 }
 

@@ -1265,15 +1265,21 @@ template <int MODE>
 static void blend_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
   constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_CTA / 32) * 2 * 32 * GUT_PAYLOAD_F4 +
                                             (GUT_BLEND_CTA / 32) * 32 * WarpTbl<MODE>::NF);
-  static int grid = 0;  // per template instance: persistent CTAs = SMs x resident CTAs per SM
-  if (!grid) {
+  // per device, thread-safe (a process may drive several devices): the
+  // dynamic shared-memory attribute is a per-device setting
+  static std::once_flag once[GUT_MAX_DEVICES];
+  static int grids[GUT_MAX_DEVICES];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev = min(dev, GUT_MAX_DEVICES - 1);
+  std::call_once(once[dev], [&] {
     cudaFuncSetAttribute(blend_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, blend_kernel<MODE>, GUT_BLEND_CTA, smem);
-    grid = max(1, sms) * max(1, per);
-  }
+    grids[dev] = max(1, sms) * max(1, per);
+  });
+  const int grid = grids[dev];
   blend_kernel<MODE><<<grid, GUT_BLEND_CTA, smem, st>>>(cam, b);
 }
 
@@ -1409,15 +1415,21 @@ template <int MODE, int KB>
 static void blend_kbuf_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
   constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_CTA / 32) * 2 * 32 * GUT_PAYLOAD_F4 +
                                             (GUT_BLEND_CTA / 32) * 32 * WarpTbl<MODE>::NF);
-  static int grid = 0;
-  if (!grid) {
+  // per device, thread-safe (a process may drive several devices): the
+  // dynamic shared-memory attribute is a per-device setting
+  static std::once_flag once[GUT_MAX_DEVICES];
+  static int grids[GUT_MAX_DEVICES];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev = min(dev, GUT_MAX_DEVICES - 1);
+  std::call_once(once[dev], [&] {
     cudaFuncSetAttribute(blend_kbuf_kernel<MODE, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, blend_kbuf_kernel<MODE, KB>, GUT_BLEND_CTA, smem);
-    grid = max(1, sms) * max(1, per);
-  }
+    grids[dev] = max(1, sms) * max(1, per);
+  });
+  const int grid = grids[dev];
   blend_kbuf_kernel<MODE, KB><<<grid, GUT_BLEND_CTA, smem, st>>>(cam, b);
 }
 

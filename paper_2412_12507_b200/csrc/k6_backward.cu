@@ -349,8 +349,12 @@ void launch_backward(const DevCam &cam, const SceneDev &s, const BwdBufs &b, cud
   if (cam.n_tiles > 0) {
     if (cam.shutter != SH_GLOBAL) {
       constexpr size_t smem = sizeof(float4) * 8 * 32 * BwNF<2>::v;
-      static bool attr = false;
-      if (!attr) { cudaFuncSetAttribute(backward_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+      static std::once_flag once[GUT_MAX_DEVICES];  // (a per-device attribute)
+      int dev = 0;
+      cudaGetDevice(&dev);
+      std::call_once(once[min(dev, GUT_MAX_DEVICES - 1)], [] {
+        cudaFuncSetAttribute(backward_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      });
       backward_kernel<2><<<cam.n_tiles, 256, smem, st>>>(cam, b);
     } else {
       backward_kernel<0><<<cam.n_tiles, 256, sizeof(float4) * 8 * 32 * BwNF<0>::v, st>>>(cam, b);

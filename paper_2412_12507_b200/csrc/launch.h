@@ -3,9 +3,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "gut_internal.cuh"
 
 namespace gut {
+
+constexpr int GUT_MAX_DEVICES = 64;  // per-device launch setup slots
 
 // Packed scene (device SoA).  pos_opa = (mu, sigma), rot = (w,x,y,z) raw,
 // scale = (s, 0), sh = float4 chunk c of Gaussian i at sh[c * n + i].
@@ -37,7 +41,11 @@ enum : int {
   CNT_HIST_DEPTH = 64,     // 4 x 256
   CNT_HIST_TILE = 64 + 1024,  // 2 x 256
   CNT_PLAN_HIST = 64 + 1024 + 512,  // 1024 blend queue-1 buckets
-  CNT_WORDS = 64 + 1024 + 512 + 1024
+  CNT_WORDS = 64 + 1024 + 512 + 1024,
+  // sticky words after the per-render memset range: set by the kernels, read
+  // and cleared only by the host at a synchronising call (gut_check & co.)
+  CNT_STICKY_OVERFLOW = CNT_WORDS,
+  CNT_ALLOC = CNT_WORDS + 4
 };
 
 void launch_pack_scene(const float *means, const float *rots, const float *scales, const float *opac,

@@ -116,9 +116,10 @@ def lib():
         L.gut_projection_quality.argtypes = [vp, vp, C.POINTER(gut_camera), C.POINTER(gut_options), i32, C.c_uint64,
                                              vp, vp]
         L.gut_timing_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int32), i32]
+        L.gut_check.argtypes = [vp, vp]
         for name in ("gut_context_create", "gut_workspace_reserve", "gut_scene_create", "gut_render",
                      "gut_render_batch", "gut_render_backward", "gut_projection_quality", "gut_timing_read",
-                     "gut_debug_copy_stage"):
+                     "gut_debug_copy_stage", "gut_check"):
             getattr(L, name).restype = C.c_int
         L.gut_options_default.restype = None
         L.gut_context_destroy.restype = None
@@ -192,6 +193,11 @@ def gut_workspace_reserve(ctx, max_keys: int, max_gaussians: int, max_w: int, ma
 
 def gut_scene_create(ctx, means, rotations, scales, opacities, sh, sh_degree: int, stream=None):
     """Arrays are torch CUDA tensors (on_device) or numpy float32 arrays (host)."""
+    nc = (int(sh_degree) + 1) ** 2
+    if int(sh.shape[0]) != int(means.shape[0]) or (sh.ndim == 3 and (sh.shape[1] != nc or sh.shape[2] != 3)) \
+            or (sh.ndim == 2 and sh.shape[1] != 3 * nc) or sh.ndim not in (2, 3):
+        raise ValueError(f"sh must be [N, {nc}, 3] (or [N, {3 * nc}]) for sh_degree {sh_degree}, "
+                         f"got {tuple(sh.shape)}")
     g = gut_gaussians()
     g.struct_size = C.sizeof(gut_gaussians)
     g.sh_degree = int(sh_degree)
@@ -271,6 +277,12 @@ def gut_timing_read(ctx, reset: bool = True):
     n = C.c_int32(0)
     _check(lib().gut_timing_read(ctx, ms, C.byref(n), int(reset)), ctx)
     return dict(zip(STAGE_NAMES, list(ms))), int(n.value)
+
+
+def gut_check(ctx, stream=None):
+    """Synchronises `stream`; raises GutError(GUT_E_CAPACITY) if a render since
+    the last synchronising call overflowed its reserved key capacity."""
+    _check(lib().gut_check(ctx, _stream_ptr(stream)), ctx)
 
 
 def gut_debug_copy_stage(ctx, stage: int):

@@ -10,9 +10,23 @@ TOL_RGB = 2e-4           # absolute, per fp32 RGB channel
 TOL_ALPHA = 2e-4         # absolute
 TOL_DEPTH_REL = 1e-3     # relative on depth
 # ambiguity bands
-ALPHA_BAND = 1e-5        # |alpha - alpha_min| <= band: the alpha-skip may flip
-TERM_BAND = 2e-8         # |T' - T_min| <= band: the termination may flip
-ORDER_BAND = 8 * 2 ** -23  # contributing depths within 8 fp32 ulps: order may swap
+# |alpha - alpha_min| <= band: the alpha-skip may flip.  Near alpha_min the GPU
+# alpha error is alpha_min |d omega^2| / 2: with the largest |d omega^2| implied
+# by SURVEY App. B's worst |d alpha| (4.8e-6 at alpha ~ 0.5, i.e. |d omega^2|
+# ~ 2e-5) that is ~4e-8, so 1e-6 keeps a 25x margin.
+ALPHA_BAND = 1e-6
+# |T' - T_min| <= band: the termination may flip.  T carries the relative error
+# sum_i |d alpha_i| / (1 - alpha_i) of every earlier hit (~1e-4 relative with
+# App. B's |d alpha| over 15-30 hits), i.e. ~1.4e-8 at T = T_min.
+TERM_BAND = 2e-8
+# order margin (oracle min_order_gap: the relative depth perturbation that could
+# swap two contributing entries under the (fp32 depth key, index) order,
+# reading R13').  Global shutter: K1 forms the depth in fp64 like the oracle
+# (differences ~1e-16), so only keys within 1e-12 of a rounding boundary can
+# differ.  Rolling shutter: the depth is taken at the centre's shutter time,
+# solved to 1e-4 px on the GPU (R14) -> depth differences up to ~1e-8 relative.
+ORDER_BAND_GLOBAL = 1e-12
+ORDER_BAND_RS = 2e-8
 
 
 def gpu_render(scene, cam, opt=None, reserve=None, timing=False):
@@ -28,10 +42,14 @@ def gpu_render(scene, cam, opt=None, reserve=None, timing=False):
     return out
 
 
-def pixel_mask(diag):
-    """True where the strict comparison applies."""
+def order_band(cam):
+    return ORDER_BAND_GLOBAL if cam is None or cam.shutter == "global" else ORDER_BAND_RS
+
+
+def pixel_mask(diag, cam=None):
+    """True where the strict comparison applies (cam: selects the order band)."""
     m = (diag["min_alpha_gap"] > ALPHA_BAND) & (diag["min_term_gap"] > TERM_BAND)
-    m &= diag["min_order_gap"] > ORDER_BAND
+    m &= diag["min_order_gap"] > order_band(cam)
     m &= (diag["amb_bin"] == 0) & (diag["amb_cull"] == 0)
     return m
 

@@ -33,7 +33,7 @@ def _run(scene, cam, opt=None, seed=0, label=""):
     from paper_2412_12507_b200 import gut
     opt = opt or S.RenderOptions()
     o = O.render(scene, cam, opt)
-    mask = pixel_mask(o["diag"])
+    mask = pixel_mask(o["diag"], cam)
     rng = np.random.default_rng(seed)
     H, W = cam.height, cam.width
     g_rgb = rng.standard_normal((H, W, 3)).astype(np.float32) * mask[..., None]

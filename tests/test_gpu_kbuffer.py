@@ -18,7 +18,7 @@ import numpy as np
 import pytest
 
 import scenegen as S
-from gpu_common import TOL_RGB, assert_images_close, gpu_lists, gpu_render, pixel_mask
+from gpu_common import ALPHA_BAND, TERM_BAND, TOL_RGB, assert_images_close, gpu_lists, gpu_render, pixel_mask
 
 pytestmark = pytest.mark.gpu
 
@@ -39,15 +39,15 @@ def _isolated(scene, cam, g, opt, max_excluded=0.01, label=""):
     proj = O.preprocess(scene, cam, opt)
     gids, ranges = gpu_lists(g, cam.tiles[0] * cam.tiles[1])
     rgb, alpha, depth, diag = O.composite(scene, proj, gids, ranges, cam, opt)
-    m = (diag["min_alpha_gap"] > 1e-5) & (diag["min_term_gap"] > 2e-8) & (diag["min_tau_gap"] > TAU_BAND)
+    m = (diag["min_alpha_gap"] > ALPHA_BAND) & (diag["min_term_gap"] > TERM_BAND) & (diag["min_tau_gap"] > TAU_BAND)
     return assert_images_close(g, dict(rgb=rgb, alpha=alpha, depth=depth), m, f"kbuf blend {label}",
                                max_excluded=max_excluded)
 
 
-def _alpha_on_tau_band(g, o, sel=None):
+def _alpha_on_tau_band(g, o, cam, sel=None):
     """Pixels excluded only by the tau band, ray not terminated: alpha is order-free."""
     d = o["diag"]
-    m = pixel_mask(d) & (d["min_tau_gap"] <= TAU_BAND) & (d["terminated"] == 0)
+    m = pixel_mask(d, cam) & (d["min_tau_gap"] <= TAU_BAND) & (d["terminated"] == 0)
     if sel is not None:
         m &= sel
     if m.any():
@@ -61,9 +61,9 @@ def _full(scene, cam, opt, max_excluded=0.01, label=""):
     g = gpu_render(scene, cam, opt)
     _isolated(scene, cam, g, opt, max_excluded, label)
     o = O.render(scene, cam, opt)
-    m = pixel_mask(o["diag"]) & (o["diag"]["min_tau_gap"] > TAU_BAND)
+    m = pixel_mask(o["diag"], cam) & (o["diag"]["min_tau_gap"] > TAU_BAND)
     assert_images_close(g, o, m, f"kbuf e2e {label}", max_excluded=max_excluded)
-    _alpha_on_tau_band(g, o)
+    _alpha_on_tau_band(g, o, cam)
     T = 1 - g["alpha"]
     assert np.all(np.isfinite(g["rgb"])) and np.all(T >= 0) and np.all(T <= 1)
     return g, o
@@ -121,8 +121,8 @@ def test_full_size_sampled_tiles_kbuffer():
         x0, y0 = (t % tx) * 16, (t // tx) * 16
         mask[y0:y0 + 16, x0:x0 + 16] = True
     inband = mask.sum()
-    _alpha_on_tau_band(g, o, mask)
-    mask &= pixel_mask(o["diag"]) & (o["diag"]["min_tau_gap"] > TAU_BAND)
+    _alpha_on_tau_band(g, o, cam, mask)
+    mask &= pixel_mask(o["diag"], cam) & (o["diag"]["min_tau_gap"] > TAU_BAND)
     # the 8 longest lists are the dense object cluster (~10^5 entries, hundreds of
     # hits per ray): many pixels hold two hits within 2e-6 in tau
     print(f"full-size kbuf: strict pixels {mask.sum()} of {inband}")

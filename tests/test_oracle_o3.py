@@ -158,8 +158,8 @@ def test_tile_lists_order_and_permutation(orc):
             p = orc.preprocess(sc, cam, opt)
             tiles, gids, ranges = orc.tile_lists(p, cam, opt)
             assert tiles.size == int(p["tiles"][p["reason"] == 0].sum())
-            # sorted by (tile, depth, gid)
-            key = list(zip(tiles, p["depth"][gids], gids))
+            # sorted by (tile, fp32 depth key, gid) -- the 3DGS key (reading R13')
+            key = list(zip(tiles, p["depth"][gids].astype(np.float32), gids))
             assert key == sorted(key)
             # each visible Gaussian appears exactly 'tiles' times, each pair once
             pairs = set(zip(tiles.tolist(), gids.tolist()))
@@ -169,6 +169,31 @@ def test_tile_lists_order_and_permutation(orc):
             for t in range(ranges.shape[0]):
                 a, b = ranges[t]
                 assert np.all(tiles[a:b] == t)
+
+
+def test_tile_lists_fp32_key_ties_by_index(orc):
+    """Two Gaussians whose fp64 depths differ but round to the same fp32 key
+    are listed by index, not by the fp64 depth (reading R13': the sort key is
+    the 3DGS (tile, float depth bits) key, ties by Gaussian index)."""
+    sc, cam = S.tiny(0, "pinhole", n=2)
+    x1 = np.nextafter(np.float32(0.1), np.float32(0))       # gid 1 nearer by ~2e-10 in fp64
+    sc.means[:] = [[0.1, 0.1, 4.0], [x1, 0.1, 4.0]]
+    sc.scales[:] = 0.05
+    sc.rotations[:] = [1, 0, 0, 0]
+    opt = S.RenderOptions()
+    p = orc.preprocess(sc, cam, opt)
+    assert np.all(p["reason"] == 0)
+    assert p["depth"][1] < p["depth"][0] and np.float32(p["depth"][1]) == np.float32(p["depth"][0])
+    tiles, gids, ranges = orc.tile_lists(p, cam, opt)
+    for t in np.unique(tiles):
+        a, b = ranges[t]
+        assert list(gids[a:b]) == [0, 1]
+    # distinct fp32 keys: the nearer one first
+    sc.means[1, 2] = 3.9
+    p = orc.preprocess(sc, cam, opt)
+    tiles, gids, ranges = orc.tile_lists(p, cam, opt)
+    a, b = ranges[tiles[0]]
+    assert list(gids[a:b]) == [1, 0]
 
 
 def test_aabb_mode_counts_rectangle(orc):
