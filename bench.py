@@ -38,7 +38,8 @@ METRIC = "frames/sec & Mpix/s at 1080p, 3M Gaussians (fisheye) at 1/2/4/8 B200; 
 CONFIG = "multiview"
 WORKLOAD = ("multiview: 3,000,000 Gaussians SH3 (garden recipe, s_med 0.007), equidistant fisheye 1920x1080 "
             "f=620 theta_max=105deg, 256-view spiral (BASELINE.json configs[4])")
-PEAK_FP32_NOTE = "148 SMs x 128 FP32 lanes x 2 FLOP/FMA x 1.965 GHz (B200_PROFILING.md unit counts, max clock)"
+PEAK_ISSUE_NOTE = ("148 SMs x 4 schedulers x 1 warp-instruction/clk x 32 lanes x 1.965 GHz = thread-instruction "
+                   "issue slots (B200_PROFILING.md unit counts, max clock)")
 
 
 def parse():
@@ -50,7 +51,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--inflight", type=int, default=3, help="frames in flight (contexts x streams) in the timed region")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-tiles", type=int, default=512, help="tiles in the oracle's bounded sample")
+    p.add_argument("--cpu-tiles", type=int, default=0, help="oracle: composite only this many random tiles and "
+                   "extrapolate (debug; default 0 = the full frame)")
     p.add_argument("--n", type=int, default=None, help="override N (debug only; the default is the config)")
     p.add_argument("--kbuffer", type=int, default=0, help="time \"Ours (sorted)\" (per-ray k-buffer of this size) "
                    "instead of \"Ours\" (0)")
@@ -110,26 +112,37 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- roofline
 def algorithmic_work(n, nv, k, tiles, pixels, pe, pc, sh_chunks=12):
-    """Algorithmic bytes / FLOPs per launch of each kernel.
-    n: Gaussians, nv: visible, k: keys, pe/pc: evaluated / contributing pairs."""
+    """Algorithmic work per launch, SURVEY §8(d).3 formulas.
+    n: Gaussians, nv: visible, k: keys, pe/pc: evaluated / contributing pairs.
+    Bytes for the HBM-bound stages; thread-instructions for K5 (issue-bound):
+    ~30 per evaluated pair up to the reject test + ~15 more per contributing one."""
     return {
-        "K1_project": ("hbm", 48 * n + 8 * n + nv * (16 * sh_chunks + 32 + 80)),
-        "K3_sort_depth": ("hbm", 4 * n + 8 * nv + 3 * 16 * nv - 4 * nv),
-        "K2_emit": ("hbm", 4 * nv + 4 * nv + 8 * k),  # depth order + tile code per visible, (tile, gid) per key
-        # (K4, the tile ranges, is fused into the final tile pass: + 8 B per tile)
-        "K3_sort_tile": ("hbm", (32 if tiles > 256 else 16) * k + 8 * tiles),
-        # FP32 work of Eq. 11 in the anchored form: 36 FLOP to the reject test per
-        # evaluated pair (n: 12, e: 12, |n|^2: 5, |e|^2: 5, k^2|e|^2: 1, compare: 1)
-        # + 30 FLOP per contributing pair (rcp, omega^2, ex2 argument, clamp,
-        # tau: 5, blend: 4 x 2 + transmittance: 2, ...)
-        "K5_blend": ("alu", 36 * pe + 30 * pc),
+        "K1_project": ("hbm", 52 * n + (16 * sh_chunks + 100) * nv),
+        "K2_emit": ("hbm", 8 * n + 32 * nv + 6 * k),           # 2-level design: u16 tile + u32 gid per key
+        "K3_sort": ("hbm", 68 * nv + 12 * k),                  # both levels: depth passes + tile pass(es)
+        "K5_blend": ("issue", 30 * pe + 15 * pc),
     }
 
 
-def roofline(stage_ms, work, peaks, clocks):
+def builder_work(n, nv, k, tiles, pe, pc, sh_chunks=12):
+    """The bytes this build's kernels actually have to move (its own layout:
+    80-B payload, u32 tile ids, two 8-bit tile passes) -- reported next to the
+    survey numbers, never as the headline."""
+    return {
+        "K1_project": 56 * n + nv * (16 * sh_chunks + 32 + 80),
+        "K2_emit": 8 * nv + 8 * k,
+        "K3_sort": 4 * n + 52 * nv + (32 if tiles > 256 else 16) * k + 8 * tiles,
+    }
+
+
+STAGE_TIME = {"K1_project": ("K1_project",), "K2_emit": ("K2_emit",),
+              "K3_sort": ("K3_sort_depth", "K3_sort_tile", "K4_ranges"), "K5_blend": ("K5_blend",)}
+
+
+def roofline(stage_ms, work, peaks, builder=None):
     out = {}
     for name, (bound, amount) in work.items():
-        ms = stage_ms.get(name)
+        ms = sum(stage_ms.get(s, 0.0) for s in STAGE_TIME[name])
         if not ms:
             continue
         if bound == "hbm":
@@ -137,24 +150,34 @@ def roofline(stage_ms, work, peaks, clocks):
             peak = peaks["hbm_gbs"]
             out[name] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                          "ms": ms, "algorithmic": amount}
-        else:
-            ach = amount / (ms * 1e-3) / 1e12
-            peak = peaks["fp32_tflops"]
-            out[name] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            if builder and name in builder:
+                out[name]["builder_bytes"] = builder[name]
+                out[name]["builder_frac"] = builder[name] / (ms * 1e-3) / 1e9 / peak
+        else:  # issue slots: thread-instructions / (SMs x 4 schedulers x 32 lanes x clock)
+            ach = amount / (ms * 1e-3) / 1e9
+            peak = peaks["issue_ginst"]
+            out[name] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Ginst/s", "frac": ach / peak,
                          "ms": ms, "algorithmic": amount}
+        m = load_ncu_metrics(name)
+        if m:
+            out[name]["ncu"] = m
     return out
 
 
 # ncu kernel names of the stages (profiles/<tag>_traffic.json, tools/profile_round.sh)
-NCU_NAMES = {"K5_blend": "blend_kernel<0>", "K1_project": "project_kernel<3>"}
+NCU_NAMES = {"K5_blend": "blend_kernel<0>", "K1_project": "project_kernel<3>", "K2_emit": "emit_kernel",
+             "K3_sort": "onesweep_kernel<0>"}
+
+
+def _traffic_files():
+    import glob
+    return sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))  # by name: r1 < r1v2 < r2 ...
 
 
 def load_traffic(stage):
     """dram read + write bytes per launch of the stage's kernel from the newest
     committed `ncu --set full` capture (profiles/*_traffic.json), or None."""
-    import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))  # by name: r1 < r1v2 < r1v3 < r2 ...)
-    for f in reversed(files):
+    for f in reversed(_traffic_files()):
         try:
             d = json.load(open(f))
             v = d["bytes_per_launch"].get(NCU_NAMES.get(stage, ""))
@@ -165,6 +188,19 @@ def load_traffic(stage):
     return None, None
 
 
+def load_ncu_metrics(stage):
+    """issue / DRAM utilisation of the stage's kernel from the newest committed capture."""
+    for f in reversed(_traffic_files()):
+        try:
+            d = json.load(open(f))
+            v = d.get("metrics", {}).get(NCU_NAMES.get(stage, ""))
+            if v:
+                return dict(v, source=os.path.relpath(f, ROOT))
+        except Exception:
+            continue
+    return None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = {"hbm_gbs": 6650.0, "hbm_source": "fallback (B200_PROFILING.md)"}
@@ -172,15 +208,16 @@ def load_peaks():
         d = json.load(open(p))
         if d.get("hbm_gbs"):
             peaks = {"hbm_gbs": float(d["hbm_gbs"]), "hbm_source": "measured (MEASURED_PEAKS.json)"}
-    peaks["fp32_tflops"] = 148 * 128 * 2 * 1.965e9 / 1e12
-    peaks["fp32_source"] = PEAK_FP32_NOTE
+    peaks["issue_ginst"] = 148 * 4 * 32 * 1.965e9 / 1e9
+    peaks["issue_source"] = PEAK_ISSUE_NOTE
     return peaks
 
 
 # ---------------------------------------------------------------- CPU oracle
-def oracle_frame_seconds(scene, cam, opt, n_tiles_sample, seed=0):
-    """The fp64 oracle as it stands, on the box's host cores: full O1-O4 for
-    the view, O5-O6 on a random sample of tiles, extrapolated to the frame."""
+def oracle_frame_seconds(scene, cam, opt, n_tiles_sample=0, seed=0):
+    """The fp64 oracle as it stands, on the box's host cores: one full frame
+    (O1-O4 for the view, O5-O6 on every tile) timed end to end.  n_tiles_sample
+    > 0 composites only a random sample of tiles and extrapolates (debug only)."""
     import numpy as np
     from oracle import oracle as O
     t0 = time.perf_counter()
@@ -190,9 +227,12 @@ def oracle_frame_seconds(scene, cam, opt, n_tiles_sample, seed=0):
     t2 = time.perf_counter()
     tx, ty = cam.tiles
     T = tx * ty
-    rng = np.random.default_rng(seed)
-    sub = np.sort(rng.choice(T, min(n_tiles_sample, T), replace=False)).astype(np.int32)
-    O.composite(scene, proj, gids, ranges, cam, opt, tile_subset=sub)
+    if n_tiles_sample and n_tiles_sample < T:
+        rng = np.random.default_rng(seed)
+        sub = np.sort(rng.choice(T, n_tiles_sample, replace=False)).astype(np.int32)
+    else:
+        sub = np.arange(T, dtype=np.int32)
+    O.composite(scene, proj, gids, ranges, cam, opt, tile_subset=None if len(sub) == T else sub)
     t3 = time.perf_counter()
     frame = (t1 - t0) + (t2 - t1) + (t3 - t2) * T / len(sub)
     return frame, {"preprocess_s": t1 - t0, "lists_s": t2 - t1, "composite_sample_s": t3 - t2,
@@ -219,8 +259,10 @@ def run_reference(args):
         f, detail = oracle_frame_seconds(scene, views[(args.warmup + s) % len(views)], opt, args.cpu_tiles, seed=s)
         tot += f
     fps = args.steps / tot
-    sample = (f"per step: one view, O1-O4 over all {scene.count} Gaussians + O5-O6 on {detail['tiles_sampled']} "
-              f"of {detail['tiles_total']} tiles, extrapolated to the full frame")
+    sample = (f"per step: one full view (O1-O4 over all {scene.count} Gaussians, O5-O6 on all "
+              f"{detail['tiles_total']} tiles), timed; no extrapolation" if detail["tiles_sampled"] ==
+              detail["tiles_total"] else f"per step: one view, O5-O6 on {detail['tiles_sampled']} of "
+              f"{detail['tiles_total']} tiles, extrapolated")
     line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -447,7 +489,7 @@ def run_ours(args):
     n_tiles = views[0].tiles[0] * views[0].tiles[1]
     peaks = load_peaks()
     work = algorithmic_work(N, mean_nv, mean_k, n_tiles, npix, mean_pe, mean_pc)
-    rl = roofline(stage_ms, work, peaks, clk)
+    rl = roofline(stage_ms, work, peaks, builder_work(N, mean_nv, mean_k, n_tiles, mean_pe, mean_pc))
     dom = max(rl, key=lambda k: rl[k]["ms"])
     d = rl[dom]
     traffic, traffic_src = load_traffic(dom)
@@ -479,7 +521,9 @@ def run_ours(args):
         "gpu_launches": launches_per_render * args.steps,
         "roofline": {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                      "unit": d["unit"], "frac": d["frac"], "traffic": traffic, "traffic_source": traffic_src,
-                     "peak_source": peaks["hbm_source"] if d["bound"] == "hbm" else peaks["fp32_source"]},
+                     "peak_source": peaks["hbm_source"] if d["bound"] == "hbm" else peaks["issue_source"],
+                     "definition": "SURVEY 8(d).3: K5 = (30 x evaluated + 15 x contributing pairs) thread-"
+                                   "instructions / issue-slot peak; K1-K3 = algorithmic bytes / HBM peak"},
         "roofline_all": rl,
         "workload_stats": {"n": N, "n_visible_mean": mean_nv, "keys_mean": mean_k, "kappa": mean_k / max(mean_nv, 1),
                            "pairs_evaluated_per_px": mean_pe / npix, "pairs_contributing_per_px": mean_pc / npix,
@@ -491,9 +535,8 @@ def run_ours(args):
             from oracle import oracle as O
             f, det = oracle_frame_seconds(sc, views[0], opt, args.cpu_tiles)
             line["cpu_baseline"] = {"value": 1.0 / f, "unit": "frames/s", "cores": O.threads(), "kind": "oracle",
-                                    "sample": f"view 0: O1-O4 over all {N} Gaussians + O5-O6 on "
-                                              f"{det['tiles_sampled']}/{det['tiles_total']} tiles, extrapolated "
-                                              f"to the frame ({det})"}
+                                    "sample": f"view 0, one full frame: O1-O4 over all {N} Gaussians + O5-O6 on "
+                                              f"{det['tiles_sampled']}/{det['tiles_total']} tiles, timed ({det})"}
         except Exception as e:  # reported, never fatal for the GPU number
             line["cpu_baseline"] = {"value": None, "unit": "frames/s", "cores": None, "kind": "oracle",
                                     "sample": f"failed: {e}"}

@@ -16,8 +16,12 @@
 #define GUT_BLEND_CTAS 2  // K5 resident CTAs per SM (register budget 65536 / (256 x 2) = 128)
 #endif
 #define GUT_PAYLOAD_F4 5  // K1 -> K5 blend payload per Gaussian, in float4 (k1_project.cu finish_gaussian)
+#ifndef GUT_SORT_THREADS
 #define GUT_SORT_THREADS 512
+#endif
+#ifndef GUT_SORT_ITEMS
 #define GUT_SORT_ITEMS 8
+#endif
 #define GUT_SORT_PART (GUT_SORT_THREADS * GUT_SORT_ITEMS)  // 4096 keys per onesweep partition
 #define GUT_EMIT_THREADS 256
 #define GUT_EMIT_ITEMS 4

@@ -1046,6 +1046,8 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     const uint32_t ck_step = max(32u, ((uint32_t)B.seg / GUT_CK) & ~31u);
     warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, L, n_eval, n_contrib, processed,
                         s > 0 ? stat : nullptr, s, s > 0 ? &ck : nullptr, ck_step, nullptr);
+    unsigned long long t_spec = 0, t_lb = 0;  // (trace only: end of the speculative pass / of the look-back)
+    if (B.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_spec));
     float T_pre[NP], T_end[NP];
     bool alive_in[NP], redo[NP], any_redo = false;
 #pragma unroll
@@ -1088,6 +1090,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
         T_end[k] = T_pre[k] * L.T[k];
       }
     }
+    if (B.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_lb));
     const bool wredo = __any_sync(FULL, any_redo);
     if (wredo) {
       // each re-running pixel resumes at the latest checkpoint its exact
@@ -1136,9 +1139,10 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
       const uint32_t e1 = warp_sum(n_eval), e2 = warp_sum(n_contrib);
       if (lane == 0) {
         unsigned long long t_end;
-        uint32_t smid;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        // (16-ns units from t_begin: end of the speculative pass | end of the look-back << 16)
+        const uint32_t smid = (uint32_t)min((t_spec - t_begin) >> 4, 65535ull) |
+                              ((uint32_t)min((t_lb - t_begin) >> 4, 65535ull) << 16);
         const size_t ti = 2 * ((size_t)slot * GUT_BLEND_WARPS + w);
         B.trace[ti] = make_uint4((uint32_t)tile | ((uint32_t)s << 16) | ((uint32_t)w << 29), smid,
                                  (uint32_t)t_begin, (uint32_t)t_end);

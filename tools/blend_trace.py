@@ -37,6 +37,12 @@ def analyse(tr, ranges, tx, seg, label):
           f"sum dur {dur.sum() / 1e3:.0f} us -> packed span {dur.sum() / peak / 1e3:.1f} us")
     print("  mean concurrency per 10% slice:", " ".join(f"{p:.0f}" for p in prof))
     print("  item dur pct 50/90/99/max [us]:", (np.percentile(dur, [50, 90, 99]) / 1e3).round(1), dur.max() / 1e3)
+    tsp = (tr[:, 1] & 0xFFFF) * 16
+    tlb = (tr[:, 1] >> 16) * 16
+    for lab, sel in (("s=0", s == 0), ("s>0", s > 0)):
+        if sel.any():
+            print(f"  {lab}: spec pass {tsp[sel].sum() / 1e3:.0f} us, look-back wait {(tlb - tsp)[sel].sum() / 1e3:.0f} us, "
+                  f"redo+outputs {(dur - tlb)[sel].sum() / 1e3:.0f} us (warp-time)")
     print(f"  totals: warp-entries visited {proc.sum()} pairs eval {nev.sum()} contrib {ncon.sum()} "
           f"redo warps {nredo.sum()};  ns per warp-entry {dur.sum() / max(proc.sum(), 1):.1f} (warp-time)")
     s0 = s == 0
@@ -48,11 +54,11 @@ def analyse(tr, ranges, tx, seg, label):
     for i in last:
         t = tile[i]
         print(f"    tile ({t % tx},{t // tx}) s {s[i]} len {L[t]} start {b[i] / 1e3:.1f} end {e[i] / 1e3:.1f} "
-              f"dur {dur[i] / 1e3:.1f} sm {tr[i, 1]} visited {proc[i]} eval {nev[i]} contrib {ncon[i]} redo {nredo[i]}")
+              f"dur {dur[i] / 1e3:.1f} spec {tsp[i] / 1e3:.1f} lb {tlb[i] / 1e3:.1f} visited {proc[i]} eval {nev[i]} contrib {ncon[i]} redo {nredo[i]}")
     longest = np.argsort(-dur)[:5]
     for i in longest:
         t = tile[i]
-        print(f"    longest: tile ({t % tx},{t // tx}) s {s[i]} len {L[t]} start {b[i] / 1e3:.1f} dur {dur[i] / 1e3:.1f} "
+        print(f"    longest: tile ({t % tx},{t // tx}) s {s[i]} len {L[t]} start {b[i] / 1e3:.1f} dur {dur[i] / 1e3:.1f} spec {tsp[i] / 1e3:.1f} lb {tlb[i] / 1e3:.1f} "
               f"visited {proc[i]} eval {nev[i]} contrib {ncon[i]} redo {nredo[i]}")
     # late starters: items whose ticket started after 80% of the span
     late = b > 0.8 * span

@@ -101,11 +101,14 @@ def main():
                     vals.append(f"{v:.1f}")
             print(f"| {d['kernel']} | " + " | ".join(vals) + " |")
         if tj:
-            traffic = {}
+            traffic, extra = {}, {}
             for d in full(fr):
                 if d.get("dram_read") is not None and d.get("dram_write") is not None:
                     traffic.setdefault(d["kernel"], d["dram_read"] + d["dram_write"])
-            json.dump({"source": f"ncu --set full ({fr})", "bytes_per_launch": traffic}, open(tj, "w"), indent=1)
+                    extra.setdefault(d["kernel"], {k: d.get(k) for k in ("issue_pct", "dram_pct", "duration_us",
+                                                                         "inst", "fma_pipe_pct", "xu_pipe_pct")})
+            json.dump({"source": f"ncu --set full ({fr})", "bytes_per_launch": traffic, "metrics": extra},
+                      open(tj, "w"), indent=1)
 
 
 if __name__ == "__main__":
