@@ -165,29 +165,42 @@ __device__ __forceinline__ float rs_rcp(float x) {
 }
 __device__ __forceinline__ double rs_rcp(double x) { return 1.0 / x; }
 
+// Row-invariant part of the per-tile-row x-extent of the ellipse (computed
+// once per Gaussian; K1's counts / masks and K2's key emission both go
+// through row_span_setup + row_span_at, so they agree bit for bit).
+template <class Real> struct RowSpan {
+  Real hy, hx, ystar, slope, cond, icyy;
+};
 template <class Real>
-__device__ __forceinline__ void row_span(const EllT<Real> &e, int ty, int tile_cull, int &lo, int &hi) {
+__device__ __forceinline__ RowSpan<Real> row_span_setup(const EllT<Real> &e) {
+  RowSpan<Real> r;
+  r.hy = rs_sqrt(e.k2 * e.cyy);
+  const Real icxx = rs_rcp(e.cxx);
+  r.icyy = rs_rcp(e.cyy);
+  r.hx = rs_sqrt(e.k2 * e.cxx);
+  r.ystar = e.cxy * rs_sqrt(e.k2 * icxx);  // dy of the rightmost point (leftmost at -ystar)
+  r.slope = e.cxy * r.icyy;
+  r.cond = fmax(e.cxx - e.cxy * r.slope, (Real)0);  // det / cyy
+  return r;
+}
+template <class Real>
+__device__ __forceinline__ void row_span_at(const EllT<Real> &e, const RowSpan<Real> &r, int ty, int tile_cull,
+                                            int &lo, int &hi) {
   if (tile_cull == 0) { lo = e.x0; hi = e.x1; return; }
   const Real zero = 0, itile = (Real)(1.0 / GUT_TILE);
-  Real hy = rs_sqrt(e.k2 * e.cyy);
-  Real a = fmax((Real)(GUT_TILE * ty) - e.vy, -hy);
-  Real b = fmin((Real)(GUT_TILE * ty + GUT_TILE) - e.vy, hy);
+  Real a = fmax((Real)(GUT_TILE * ty) - e.vy, -r.hy);
+  Real b = fmin((Real)(GUT_TILE * ty + GUT_TILE) - e.vy, r.hy);
   if (a > b) { lo = 1; hi = 0; return; }
-  const Real icxx = rs_rcp(e.cxx), icyy = rs_rcp(e.cyy);
-  Real hx = rs_sqrt(e.k2 * e.cxx);
-  Real ystar = e.cxy * rs_sqrt(e.k2 * icxx);  // dy of the rightmost point (leftmost at -ystar)
-  Real slope = e.cxy * icyy;
-  Real cond = fmax(e.cxx - e.cxy * slope, zero);  // det / cyy
   Real xr, xl;
-  if (ystar >= a && ystar <= b) xr = hx;
+  if (r.ystar >= a && r.ystar <= b) xr = r.hx;
   else {
-    Real yy = ystar < a ? a : b;
-    xr = slope * yy + rs_sqrt(fmax(cond * (e.k2 - yy * yy * icyy), zero));
+    Real yy = r.ystar < a ? a : b;
+    xr = r.slope * yy + rs_sqrt(fmax(r.cond * (e.k2 - yy * yy * r.icyy), zero));
   }
-  if (-ystar >= a && -ystar <= b) xl = -hx;
+  if (-r.ystar >= a && -r.ystar <= b) xl = -r.hx;
   else {
-    Real yy = -ystar < a ? a : b;
-    xl = slope * yy - rs_sqrt(fmax(cond * (e.k2 - yy * yy * icyy), zero));
+    Real yy = -r.ystar < a ? a : b;
+    xl = r.slope * yy - rs_sqrt(fmax(r.cond * (e.k2 - yy * yy * r.icyy), zero));
   }
   Real XL = e.vx + xl, XR = e.vx + xr;
   XL = fmin(fmax(XL, (Real)-1e7), (Real)1e7);
@@ -197,14 +210,19 @@ __device__ __forceinline__ void row_span(const EllT<Real> &e, int ty, int tile_c
   lo = max(l, e.x0);
   hi = min(h, e.x1);
 }
+template <class Real>
+__device__ __forceinline__ void row_span(const EllT<Real> &e, int ty, int tile_cull, int &lo, int &hi) {
+  row_span_at(e, row_span_setup(e), ty, tile_cull, lo, hi);
+}
 
 template <class Real>
 __device__ __forceinline__ int ell_tile_count(const EllT<Real> &e, int tile_cull) {
   if (tile_cull == 0) return (e.x1 - e.x0 + 1) * (e.y1 - e.y0 + 1);
+  const RowSpan<Real> rs = row_span_setup(e);
   int n = 0;
   for (int ty = e.y0; ty <= e.y1; ++ty) {
     int lo, hi;
-    row_span(e, ty, tile_cull, lo, hi);
+    row_span_at(e, rs, ty, tile_cull, lo, hi);
     n += max(hi - lo + 1, 0);
   }
   return n;
@@ -220,19 +238,21 @@ template <class Real>
 __device__ __forceinline__ uint32_t ell_tile_code(const EllT<Real> &e, int tile_cull) {
   const int w = e.x1 - e.x0 + 1, h = e.y1 - e.y0 + 1;
   if (w <= 3 && h <= 3 && e.x0 < 2048 && e.y0 < 1024) {
+    const RowSpan<Real> rs = row_span_setup(e);
     uint32_t mask = 0;
     for (int r = 0; r < h; ++r) {
       int lo, hi;
-      row_span(e, e.y0 + r, tile_cull, lo, hi);
+      row_span_at(e, rs, e.y0 + r, tile_cull, lo, hi);
       for (int x = lo; x <= hi; ++x) mask |= 1u << (3 * r + (x - e.x0));
     }
     return mask ? (mask | ((uint32_t)e.x0 << 9) | ((uint32_t)e.y0 << 20)) : 0u;
   }
   if (w <= 4 && h <= 4 && e.x0 < 128 && e.y0 < 128) {  // 4x4 hit mask (bit 30)
+    const RowSpan<Real> rs = row_span_setup(e);
     uint32_t mask = 0;
     for (int r = 0; r < h; ++r) {
       int lo, hi;
-      row_span(e, e.y0 + r, tile_cull, lo, hi);
+      row_span_at(e, rs, e.y0 + r, tile_cull, lo, hi);
       for (int x = lo; x <= hi; ++x) mask |= 1u << (4 * r + (x - e.x0));
     }
     return mask ? (0x40000000u | mask | ((uint32_t)e.x0 << 16) | ((uint32_t)e.y0 << 23)) : 0u;

@@ -261,17 +261,19 @@ __device__ __forceinline__ f3 sh_colour(const float4 *sh, int64_t n, int64_t i, 
 // packed ellipse record.  Returns the depth key.
 template <int DEG>
 __device__ __forceinline__ uint32_t finish_gaussian(const DevCam &c, const SceneDev &s, int64_t i, float4 po,
-                                                    float4 sc, const float *R, d3 y0d, double t0, float4 e0,
+                                                    float4 sc, const float *R, double t0, float4 e0,
                                                     float4 e1, float4 *__restrict__ ell,
                                                     float4 *__restrict__ payload) {
-  // depth key (reading R13): camera-frame distance of mu at its own time t0
-  const d3 dcw = mkd(c.dc[0], c.dc[1], c.dc[2]);
-  const d3 yc = y0d - t0 * mtv(c.R0, dcw);
-  const float depth = (float)sqrt(dot(yc, yc));
-  // colour (reading R18): SH at d = normalize(mu - c(t0))
-  const d3 dw = mkd(po.x, po.y, po.z) - (mkd(c.c0[0], c.c0[1], c.c0[2]) + t0 * dcw);
-  const double nd = sqrt(dot(dw, dw));
-  const f3 rgb = sh_colour<DEG>(s.sh, s.n, i, tof((1.0 / nd) * dw));
+  // depth key (reading R13): camera-frame distance of mu at its own time t0,
+  // |R(t0)^T (mu - c(t0))| = |mu - c(t0)| (fp64, then the fp32 key)
+  const d3 dw = mkd(po.x, po.y, po.z) - mkd(c.c0[0], c.c0[1], c.c0[2]) -
+                (c.shutter == SH_GLOBAL ? mkd(0, 0, 0) : t0 * mkd(c.dc[0], c.dc[1], c.dc[2]));
+  const double nd2 = dot(dw, dw);
+  const float depth = (float)sqrt(nd2);
+  // colour (reading R18): SH at d = normalize(mu - c(t0)) (the difference in
+  // fp64, the normalisation in fp32: ~1e-7 relative in the direction)
+  const f3 dwf = tof(dw);
+  const f3 rgb = sh_colour<DEG>(s.sh, s.n, i, rsqrtf(dot(dwf, dwf)) * dwf);
   ell[2 * i] = e0;
   ell[2 * i + 1] = e1;
   // blend payload (80 B): w0 = c(0) - mu in fp64 (K5 forms the cancelling
@@ -442,7 +444,7 @@ __global__ __launch_bounds__(256, GUT_K1_CTAS) void project_kernel(DevCam c, Sce
       }
     }
     if (ok) {
-      key = finish_gaussian<DEG>(c, s, i, po, sc, R, y0d, (double)tt[0],
+      key = finish_gaussian<DEG>(c, s, i, po, sc, R, (double)tt[0],
                                  make_float4(e.vx, e.vy, e.cxx, e.cxy),
                                  make_float4(e.cyy, e.k2, __uint_as_float(pack_rect(e.x0, e.y0)),
                                              __uint_as_float(pack_rect(e.x1, e.y1))),
@@ -526,7 +528,7 @@ __global__ __launch_bounds__(256) void project_wide_kernel(DevCam c, SceneDev s,
         ell64[3 * i] = make_double2(e.vx, e.vy);
         ell64[3 * i + 1] = make_double2(e.cxx, e.cxy);
         ell64[3 * i + 2] = make_double2(e.cyy, e.k2);
-        key = finish_gaussian<DEG>(c, s, i, po, sc, R, y0d, t0,
+        key = finish_gaussian<DEG>(c, s, i, po, sc, R, t0,
                                    make_float4((float)e.vx, (float)e.vy, (float)e.cxx, (float)e.cxy),
                                    make_float4((float)e.cyy, -(float)e.k2, __uint_as_float(pack_rect(e.x0, e.y0)),
                                                __uint_as_float(pack_rect(e.x1, e.y1))),
