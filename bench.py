@@ -11,13 +11,14 @@ rank r renders view (s * N + r) mod 256 at step s (weak scaling in views).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Prints ONE JSON line (rank 0).  value = frames/s over all ranks with the
-scene resident in HBM (device-timed with CUDA events, max over ranks; 3
-frames in flight per GPU on separate contexts/streams, --inflight 1 for
-strictly sequential frames; single_stream = one frame at a time);
-e2e = the same metric through the C ABI with HOST output buffers (device->host
-copy of RGB/alpha/depth inside the timed region, camera struct in by value).
---impl reference times the fp64 CPU oracle (the paper's algorithm written out)
-on the box's host cores on a bounded sample of the same workload.
+scene resident in HBM (device-timed with CUDA events, max over ranks) through
+the library's batch call gut_render_batch: 3 frames in flight per GPU on the
+library's lane contexts/streams (--inflight 1: strictly sequential frames);
+single_stream = one frame at a time with stage events; e2e = the same batch
+call with HOST output buffers (device->host copy of RGB/alpha/depth inside the
+timed region, camera structs in by value).  --impl reference times the fp64
+CPU oracle (the paper's algorithm written out) on the box's host cores, one
+full frame per step.
 """
 from __future__ import annotations
 
@@ -330,6 +331,7 @@ def run_ours(args):
     for v in used:
         st = gut.gut_render(ctx, scene, cams[v], gopt, out_dev, stream=stream, stats=True)
         per_view[v] = st.as_dict()
+        per_view[v]["checksum"] = P.image_checksum(rgb)  # (8-byte image digest, gathered over ranks)
     kmax = max(d["n_keys"] for d in per_view.values())
     gut.gut_workspace_reserve(ctx, int(kmax * 1.02) + 65536, N, W, H)
     # warm-up (capacity mode: fully asynchronous)
@@ -397,21 +399,20 @@ def run_ours(args):
                                  "minus the forward's single-stream time"}
         del gbuf
 
-    # timed region: `inflight` frames in flight, contexts (own workspaces, shared
-    # read-only scene) on their own streams taking the views in turn, so one
-    # frame's kernel tails overlap the next frame's first kernels
-    lanes_d = [(ctx, stream, out_dev)]
-    extra = []
-    for _ in range(args.inflight - 1):
-        c2 = gut.gut_context_create(local)
-        gut.gut_workspace_reserve(c2, int(kmax * 1.02) + 65536, N, W, H)
-        st2 = torch.cuda.Stream(device=dev)
-        bufs = (torch.empty((H, W, 3), device=dev), torch.empty((H, W), device=dev), torch.empty((H, W), device=dev))
-        extra.append((c2, bufs))
-        lanes_d.append((c2, st2, gut.gut_outputs(bufs[0].data_ptr(), bufs[1].data_ptr(), bufs[2].data_ptr(), 1, 0)))
-    for i, (c_, st_, o_) in enumerate(lanes_d):  # warm every context
-        for s in range(2):
-            gut.gut_render(c_, scene, cams[P.view_of(s + i, rank, world, nv)], gopt, o_, stream=st_, stats=False)
+    # timed region: the library's pipelined batch call (gut_render_batch):
+    # `inflight` frames in flight on lane contexts (own workspaces, shared
+    # read-only scene) and lane streams forked from / joined to this stream, so
+    # one frame's kernel tails overlap the next frame's first kernels
+    gut.gut_context_set_frames_in_flight(ctx, args.inflight)
+    nb = max(1, args.inflight)
+    dbufs = [(torch.empty((H, W, 3), device=dev), torch.empty((H, W), device=dev), torch.empty((H, W), device=dev))
+             for _ in range(nb)]
+    douts = [gut.gut_outputs(b[0].data_ptr(), b[1].data_ptr(), b[2].data_ptr(), 1, 0) for b in dbufs]
+
+    def batch(views, outs):
+        gut.gut_render_batch(ctx, scene, [cams[v] for v in views], gopt, [outs[i % nb] for i in range(len(views))],
+                             stream=stream)
+    batch([P.view_of(s, rank, world, nv) for s in range(2 * nb)], douts)  # warm every lane
     torch.cuda.synchronize()
     P.barrier()
     torch.cuda.synchronize()
@@ -420,64 +421,34 @@ def run_ours(args):
     time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for c_, st_, o_ in lanes_d[1:]:
-        st_.wait_event(ev0)
-    for i, v in enumerate(timed_views):
-        c_, st_, o_ = lanes_d[i % len(lanes_d)]
-        gut.gut_render(c_, scene, cams[v], gopt, o_, stream=st_, stats=False)
-    for c_, st_, o_ in lanes_d[1:]:
-        j = torch.cuda.Event()
-        j.record(st_)
-        stream.wait_event(j)
+    batch(timed_views, douts)
     ev1.record(stream)
     torch.cuda.synchronize()
     P.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     ms_max = P.max_over_ranks(ms, device=dev)
-    for c2, _ in extra:
-        gut.gut_context_destroy(c2)
-    # e2e: host (pinned) outputs through the same C-ABI call; D2H inside the timed
-    # region.  Two contexts on two streams alternate frames so the copy of one
-    # frame overlaps the render of the next (the scene is shared read-only).
-    e2e_ctx = [(ctx, stream)]
-    for _ in range(max(2, args.inflight) - 1):
-        c2 = gut.gut_context_create(local)
-        gut.gut_workspace_reserve(c2, int(kmax * 1.02) + 65536, N, W, H)
-        e2e_ctx.append((c2, torch.cuda.Stream(device=dev)))
-    lanes = []
-    for c_, st_ in e2e_ctx:
-        hr = torch.empty((H, W, 3), pin_memory=True)
-        ha = torch.empty((H, W), pin_memory=True)
-        hd = torch.empty((H, W), pin_memory=True)
-        lanes.append((c_, st_, gut.gut_outputs(hr.data_ptr(), ha.data_ptr(), hd.data_ptr(), 0, 0), (hr, ha, hd)))
+    gut.gut_check(ctx, stream)  # no reserved-capacity overflow in the timed region
+    # e2e: the same batch call with host (pinned) outputs: every view's RGB,
+    # alpha and depth are copied device->host inside the timed region, on the
+    # view's lane stream (the copy of one frame overlaps the next renders)
+    hbufs = [(torch.empty((H, W, 3), pin_memory=True), torch.empty((H, W), pin_memory=True),
+              torch.empty((H, W), pin_memory=True)) for _ in range(nb)]
+    houts = [gut.gut_outputs(b[0].data_ptr(), b[1].data_ptr(), b[2].data_ptr(), 0, 0) for b in hbufs]
     e2e_first = args.warmup + args.steps
-    for s in range(2):
-        for c_, st_, o_, _ in lanes:
-            gut.gut_render(c_, scene, cams[P.view_of(e2e_first + s, rank, world, nv)], gopt, o_, stream=st_,
-                           stats=False)
+    batch([P.view_of(e2e_first + s, rank, world, nv) for s in range(nb)], houts)
     torch.cuda.synchronize()
     P.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _, st_, _, _ in lanes[1:]:
-        st_.wait_event(e0)
-    for s in range(e2e_steps):
-        v = P.view_of(e2e_first + 2 + s, rank, world, nv)
-        c_, st_, o_, _ = lanes[s % len(lanes)]
-        gut.gut_render(c_, scene, cams[v], gopt, o_, stream=st_, stats=False)
-    for _, st_, _, _ in lanes[1:]:
-        j0 = torch.cuda.Event()
-        j0.record(st_)
-        stream.wait_event(j0)
+    batch([P.view_of(e2e_first + nb + s, rank, world, nv) for s in range(e2e_steps)], houts)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = P.max_over_ranks(e0.elapsed_time(e1), device=dev)
-    for c2, _ in e2e_ctx[1:]:
-        gut.gut_context_destroy(c2)
     # per-view statistics of the timed views (deterministic renders) gathered to rank 0
     rows = [[v, per_view[v]["n_visible"], per_view[v]["n_keys"], per_view[v]["pairs_evaluated"],
-             per_view[v]["pairs_contributing"], per_view[v]["max_tile_len"]] for v in timed_views]
+             per_view[v]["pairs_contributing"], per_view[v]["max_tile_len"], per_view[v]["checksum"]]
+            for v in timed_views]
     all_rows = P.gather_stats(rows, device=dev)
     overflow = any(per_view[v]["n_keys"] > int(kmax * 1.02) + 65536 for v in timed_views)
     gut.gut_scene_destroy(ctx, scene)
@@ -493,7 +464,8 @@ def run_ours(args):
     dom = max(rl, key=lambda k: rl[k]["ms"])
     d = rl[dom]
     traffic, traffic_src = load_traffic(dom)
-    launches_per_render = 2 + 4 + 4 + (2 if n_tiles > 256 else 1) + 1 + 4  # K1+wide, 4 depth, emit (count, scan, emit, big), tile passes, ranges init, plan (3) + blend
+    # epoch advance, K1 + wide, 4 depth passes, K2 (count, scan, emit, big), tile passes, ranges init, plan (3) + blend
+    launches_per_render = 1 + 2 + 4 + 4 + (2 if n_tiles > 256 else 1) + 1 + 4
     total_views = world * args.steps
     fps = total_views / (ms_max * 1e-3)
     line = {
@@ -515,9 +487,10 @@ def run_ours(args):
         "clocks": clk,
         "e2e": {"value": world * e2e_steps / (e2e_ms * 1e-3), "unit": "frames/s", "h2d_bytes_per_step": 240,
                 "d2h_bytes_per_step": npix * 5 * 4,
-                "what": "gut_render with host (pinned) output buffers: RGB+alpha+depth copied device->host each "
-                        "step; camera struct (240 B) passed by value; scene resident (uploaded once); "
-                        "frames in flight on separate contexts/streams (copies overlap later renders)"},
+                "what": "gut_render_batch with host (pinned) output buffers: RGB+alpha+depth copied device->host "
+                        "for every view inside the timed region; camera structs (240 B each) passed by value; "
+                        "scene resident (uploaded once); frames in flight on the library's lane streams "
+                        "(copies overlap later renders)"},
         "gpu_launches": launches_per_render * args.steps,
         "roofline": {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                      "unit": d["unit"], "frac": d["frac"], "traffic": traffic, "traffic_source": traffic_src,
@@ -529,6 +502,9 @@ def run_ours(args):
                            "pairs_evaluated_per_px": mean_pe / npix, "pairs_contributing_per_px": mean_pc / npix,
                            "max_tile_len": float(a[:, 5].max()), "overflow": overflow},
         "scene_broadcast_s": t_b2 - t_b1, "scene_generate_s": t_b1 - t_b0,
+        # 48-bit image digest per (rank-sharded) timed view, gathered to rank 0:
+        # identical for a view whatever the world size (bitwise-deterministic renders)
+        "view_checksums": sorted({int(r[0]): int(r[6]) for r in all_rows}.items()),
     }
     if world == 1 and not args.no_cpu_baseline:
         try:

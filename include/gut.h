@@ -267,10 +267,21 @@ gut_status gut_projection_quality(gut_context *ctx, const gut_scene *scene, cons
                                   const gut_options *opt, int32_t n_samples, uint64_t seed, gut_quality *out,
                                   gut_stream s);
 
-/* Renders n_views views in order (outs[i] for cams[i]); stats nullable [n_views]. */
+/* Renders n_views views (outs[i] for cams[i]).  With stats == NULL the views
+ * are pipelined: up to gut_context_set_frames_in_flight() frames (default 3)
+ * are in flight at once, view i on lane i mod F -- lane 0 is ctx on stream s,
+ * lanes 1..F-1 are child contexts (own workspaces, reserved like ctx, created
+ * on first use and owned by ctx) on their own streams, forked from and joined
+ * back to s with events, so the call stays asynchronous on s and every output
+ * is complete when s reaches the point after the call.  Results are identical
+ * to rendering the views one by one.  With stats != NULL the views are
+ * rendered one at a time on s and stats[i] filled (synchronising). */
 gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_camera *cams,
                             int32_t n_views, const gut_options *opt, const gut_outputs *outs,
                             gut_stream s, gut_stats *stats);
+
+/* Frames in flight of gut_render_batch (1..8; 1 = one at a time on s). */
+gut_status gut_context_set_frames_in_flight(gut_context *ctx, int32_t n);
 
 /* Per-stage device times of every render issued with options.timing = 1 since
  * the last reset: CUDA events recorded on the render's stream between the

@@ -56,7 +56,6 @@ struct gut_context {
   bool lut_valid = false;
   double lut_key[20] = {};
   int blend_seg = 1536, blend_window = 2;  // K5 segment length and speculation window (tools/seg_sweep.sh)
-  uint32_t epoch = 0;
   bool reserved = false;
   std::vector<std::array<cudaEvent_t, 7>> tsets;  // per-render stage events (timing = 1)
   size_t tnext = 0;
@@ -68,6 +67,16 @@ struct gut_context {
   const gut_scene *last_scene = nullptr;
   float *gacc = nullptr;              // K6 accumulators (16 per Gaussian) + centre shutter times (1 per Gaussian)
   size_t cap_gacc = 0;
+  // gut_render_batch: frames in flight -- lane 0 is this context on the
+  // caller's stream, lanes 1.. are child contexts (own workspaces) on their
+  // own streams, joined back to the caller's stream with events
+  int frames_in_flight = 3;
+  int64_t res_keys = 0, res_n = 0;
+  int32_t res_w = 0, res_h = 0;
+  std::vector<gut_context *> lanes;
+  std::vector<cudaStream_t> lane_streams;
+  std::vector<cudaEvent_t> lane_events;
+  cudaEvent_t fork_event = nullptr;
 };
 
 static thread_local std::string g_err;
@@ -336,6 +345,11 @@ gut_status gut_context_create(int32_t dev, gut_context **out) {
 void gut_context_destroy(gut_context *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  for (gut_context *l : ctx->lanes) gut_context_destroy(l);
+  for (cudaStream_t st : ctx->lane_streams) cudaStreamDestroy(st);
+  for (cudaEvent_t e : ctx->lane_events) cudaEventDestroy(e);
+  if (ctx->fork_event) cudaEventDestroy(ctx->fork_event);
+  cudaSetDevice(ctx->device);
   void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->deferred, ctx->big_list, ctx->payload, ctx->sa_k, ctx->sa_v,
                 ctx->sb_k, ctx->sb_v,
                 ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->tile_work, ctx->img, ctx->st_depth,
@@ -367,6 +381,17 @@ gut_status gut_workspace_reserve(gut_context *ctx, int64_t max_keys, int64_t max
   const size_t items = std::max(tiles + (size_t)max_keys / (size_t)ctx->blend_seg + 2, 2 * tiles + 2);
   if ((s = ensure_items(ctx, items)) != GUT_OK) return s;
   ctx->reserved = true;
+  ctx->res_keys = max_keys; ctx->res_n = max_gaussians; ctx->res_w = max_w; ctx->res_h = max_h;
+  for (gut_context *l : ctx->lanes)  // batch lanes follow the reservation
+    if ((s = gut_workspace_reserve(l, max_keys, max_gaussians, max_w, max_h)) != GUT_OK)
+      return fail(ctx, s, std::string("batch lane: ") + l->err);
+  return GUT_OK;
+}
+
+gut_status gut_context_set_frames_in_flight(gut_context *ctx, int32_t n) {
+  if (!ctx) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "ctx: NULL");
+  if (n < 1 || n > 8) return fail(ctx, GUT_E_INVALID_ARGUMENT, "frames_in_flight must be in [1, 8]");
+  ctx->frames_in_flight = n;
   return GUT_OK;
 }
 
@@ -451,6 +476,12 @@ static gut_status take_sticky(gut_context *ctx, cudaStream_t st, bool &overflow)
   CUDA_TRY(ctx, cudaMemsetAsync(w, 0, sizeof(uint32_t), st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   overflow = ctx->h_counters[CNT_STICKY_OVERFLOW] != 0;
+  for (size_t i = 0; i < ctx->lanes.size(); ++i) {  // batch lanes (their renders were joined to st)
+    bool o = false;
+    gut_status r = take_sticky(ctx->lanes[i], ctx->lane_streams[i], o);
+    if (r != GUT_OK) return fail(ctx, r, ctx->lanes[i]->err);
+    overflow = overflow || o;
+  }
   return GUT_OK;
 }
 
@@ -484,6 +515,8 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
 
   uint32_t *cnt = ctx->counters;
   CUDA_TRY(ctx, cudaMemsetAsync(cnt, 0, CNT_WORDS * sizeof(uint32_t), st));
+  // look-back epochs of this render (device-side, so a captured render replays correctly)
+  launch_epoch_advance(cnt, ctx->bstatus, ctx->cap_items * GUT_TILE_PX, st);
   // K1: UT projection
   launch_project(dc, scene->d, ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->payload, cnt, ctx->deferred, st);
   if (timing) cudaEventRecord(ev[1], st);
@@ -491,13 +524,13 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   const uint32_t n32 = (uint32_t)N;
   const uint32_t *hd = cnt + CNT_HIST_DEPTH;
   launch_sort_pass(ctx->dkey, nullptr, ctx->sa_k, ctx->sa_v, nullptr, n32, 0, hd, ctx->st_depth,
-                   cnt + CNT_TICKETS + 0, ++ctx->epoch, true, st);
+                   cnt + CNT_TICKETS + 0, cnt + CNT_EPOCH, 0u, true, st);
   launch_sort_pass(ctx->sa_k, ctx->sa_v, ctx->sb_k, ctx->sb_v, cnt + CNT_NVIS, n32, 8, hd + 256, ctx->st_depth,
-                   cnt + CNT_TICKETS + 1, ++ctx->epoch, false, st);
+                   cnt + CNT_TICKETS + 1, cnt + CNT_EPOCH, 1u, false, st);
   launch_sort_pass(ctx->sb_k, ctx->sb_v, ctx->sa_k, ctx->sa_v, cnt + CNT_NVIS, n32, 16, hd + 512, ctx->st_depth,
-                   cnt + CNT_TICKETS + 2, ++ctx->epoch, false, st);
+                   cnt + CNT_TICKETS + 2, cnt + CNT_EPOCH, 2u, false, st);
   launch_sort_pass(ctx->sa_k, ctx->sa_v, nullptr, ctx->sb_v, cnt + CNT_NVIS, n32, 24, hd + 768, ctx->st_depth,
-                   cnt + CNT_TICKETS + 3, ++ctx->epoch, false, st);
+                   cnt + CNT_TICKETS + 3, cnt + CNT_EPOCH, 3u, false, st);
   const uint32_t *order = ctx->sb_v;
   if (timing) cudaEventRecord(ev[2], st);
   // key count: capacity mode keeps the stream asynchronous; otherwise read K back
@@ -525,11 +558,11 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   launch_ranges_init(ctx->ranges, dc.n_tiles, st);
   const bool two = dc.n_tiles > 256;
   launch_sort_pass(ctx->ka, ctx->va, ctx->kb, ctx->vb, kdev, nk, 0, ht, ctx->st_tile, cnt + CNT_TICKETS + 5,
-                   ++ctx->epoch, false, st, two ? nullptr : ctx->ranges);
+                   cnt + CNT_EPOCH, 4u, false, st, two ? nullptr : ctx->ranges);
   fk = ctx->kb; fv = ctx->vb;
   if (two) {
     launch_sort_pass(ctx->kb, ctx->vb, ctx->ka, ctx->va, kdev, nk, 8, ht + 256, ctx->st_tile,
-                     cnt + CNT_TICKETS + 6, ++ctx->epoch, false, st, ctx->ranges);
+                     cnt + CNT_TICKETS + 6, cnt + CNT_EPOCH, 6u, false, st, ctx->ranges);
     fk = ctx->ka; fv = ctx->va;
   }
   if (timing) cudaEventRecord(ev[4], st);
@@ -564,12 +597,6 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
     launch_plan(ctx->ranges, dc.n_tiles, 1 << 30, 1, ctx->seg_base, ctx->q1, cnt, st, GUT_KBUF_UNITS);
   else
     launch_plan(ctx->ranges, dc.n_tiles, ctx->blend_seg, ctx->blend_window, ctx->seg_base, ctx->q1, cnt, st);
-  // blend look-back epochs live in 22 bits: clear the status words on wrap
-  uint32_t bepoch = ++ctx->epoch;
-  if ((bepoch & 0x3FFFFFu) == 0) {
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->bstatus, 0, ctx->cap_items * GUT_TILE_PX * sizeof(unsigned long long), st));
-    bepoch = ++ctx->epoch;
-  }
   BlendBufs bb;
   bb.ranges = ctx->ranges; bb.gids = fv; bb.payload = ctx->payload; bb.pix = ctx->pix; bb.anchors = ctx->anchors;
   bb.seg_base = ctx->seg_base; bb.granted = ctx->unit_ctr; bb.next_s = ctx->unit_ctr + n_units; bb.unit_done = ctx->unit_ctr + 2 * n_units;
@@ -589,7 +616,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
     bb.trace = ctx->trace;
     ctx->last_items = max_items;
   }
-  bb.epoch = bepoch;
+  bb.epoch = cnt + CNT_EPOCH;
   bb.rgb = rgb; bb.alpha = alpha; bb.depth = depth; bb.counters = cnt;
   if (dc.kbuf > 0) launch_blend_kbuf(dc, bb, st);
   else launch_blend(dc, bb, st);
@@ -704,15 +731,63 @@ gut_status gut_projection_quality(gut_context *ctx, const gut_scene *scene, cons
   return GUT_OK;
 }
 
+// Child contexts and streams of the batch lanes (created once, reserved like ctx).
+static gut_status ensure_lanes(gut_context *ctx, int n) {
+  while ((int)ctx->lanes.size() < n - 1) {
+    gut_context *l = nullptr;
+    gut_status r = gut_context_create(ctx->device, &l);
+    if (r != GUT_OK) return fail(ctx, r, "batch lane context");
+    l->blend_seg = ctx->blend_seg;
+    l->blend_window = ctx->blend_window;
+    l->frames_in_flight = 1;
+    if (ctx->reserved && (r = gut_workspace_reserve(l, ctx->res_keys, ctx->res_n, ctx->res_w, ctx->res_h)) != GUT_OK) {
+      gut_context_destroy(l);
+      return fail(ctx, r, "batch lane workspace");
+    }
+    cudaStream_t st;
+    cudaEvent_t ev;
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    ctx->lanes.push_back(l);
+    ctx->lane_streams.push_back(st);
+    ctx->lane_events.push_back(ev);
+  }
+  if (!ctx->fork_event) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->fork_event, cudaEventDisableTiming));
+  return GUT_OK;
+}
+
 gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_camera *cams, int32_t n_views,
                             const gut_options *opt, const gut_outputs *outs, gut_stream s, gut_stats *stats) {
   if (!ctx) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "ctx: NULL");
   if (n_views < 0 || (n_views > 0 && (!cams || !outs))) return fail(ctx, GUT_E_INVALID_ARGUMENT, "batch arguments");
-  for (int32_t v = 0; v < n_views; ++v) {
-    gut_status r = render_one(ctx, scene, &cams[v], opt, &outs[v], (cudaStream_t)s, stats ? &stats[v] : nullptr);
-    if (r != GUT_OK) return r;
+  cudaStream_t st = (cudaStream_t)s;
+  const int L = std::min(ctx->frames_in_flight, (int)n_views);
+  if (stats || L <= 1) {  // one frame at a time (stats synchronise per view anyway)
+    for (int32_t v = 0; v < n_views; ++v) {
+      gut_status r = render_one(ctx, scene, &cams[v], opt, &outs[v], st, stats ? &stats[v] : nullptr);
+      if (r != GUT_OK) return r;
+    }
+    return GUT_OK;
   }
-  return GUT_OK;
+  cudaSetDevice(ctx->device);
+  gut_status r = ensure_lanes(ctx, L);
+  if (r != GUT_OK) return r;
+  // fork: the lanes start after the work already queued on the caller's stream
+  CUDA_TRY(ctx, cudaEventRecord(ctx->fork_event, st));
+  for (int i = 0; i < L - 1; ++i) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->lane_streams[i], ctx->fork_event, 0));
+  // views round-robin over the lanes: frame v + 1's first kernels overlap frame v's tail
+  for (int32_t v = 0; v < n_views && r == GUT_OK; ++v) {
+    const int l = v % L;
+    gut_context *c = l == 0 ? ctx : ctx->lanes[l - 1];
+    r = render_one(c, scene, &cams[v], opt, &outs[v], l == 0 ? st : ctx->lane_streams[l - 1], nullptr);
+    if (r != GUT_OK && c != ctx) fail(ctx, r, c->err);
+  }
+  // join: the caller's stream waits for every lane (also after an error)
+  for (int i = 0; i < L - 1; ++i) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->lane_events[i], ctx->lane_streams[i]));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->lane_events[i], 0));
+  }
+  return r;
 }
 
 gut_status gut_timing_read(gut_context *ctx, double ms_sum[7], int32_t *n_renders, int32_t reset) {

@@ -61,8 +61,8 @@ template <bool FIRST>
 __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, uint32_t *__restrict__ keys_out,
     uint32_t *__restrict__ vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
-    const uint32_t *__restrict__ hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch,
-    uint2 *__restrict__ ranges) {
+    const uint32_t *__restrict__ hist, unsigned long long *status, uint32_t *ticket,
+    const uint32_t *__restrict__ epoch_base, uint32_t epoch_off, uint2 *__restrict__ ranges) {
   constexpr int W = GUT_SORT_THREADS / 32;
   static_assert(GUT_SORT_THREADS >= 256, "one thread per digit");
   __shared__ uint32_t s_keys[GUT_SORT_PART];
@@ -74,6 +74,7 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
   __shared__ uint32_t s_part;
 
   const uint32_t n = n_dev ? min(*n_dev, n_host) : n_host;
+  const uint32_t epoch = __ldg(epoch_base) + epoch_off;  // (device epoch: graph-replayable)
   if (threadIdx.x == 0) s_part = atomicAdd(ticket, 1u);
   for (int j = threadIdx.x; j < W * 256; j += GUT_SORT_THREADS) (&s_wcnt[0][0])[j] = 0;
   __syncthreads();
@@ -190,16 +191,36 @@ void launch_ranges_init(uint2 *ranges, int n_tiles, cudaStream_t st) {
 
 void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                       uint32_t *vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
-                      const uint32_t *hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch,
-                      bool first, cudaStream_t st, uint2 *ranges) {
+                      const uint32_t *hist, unsigned long long *status, uint32_t *ticket,
+                      const uint32_t *epoch_base, uint32_t epoch_off, bool first, cudaStream_t st, uint2 *ranges) {
   if (n_host == 0) return;
   unsigned blocks = (n_host + GUT_SORT_PART - 1) / GUT_SORT_PART;
   if (first)
     onesweep_kernel<true><<<blocks, GUT_SORT_THREADS, 0, st>>>(keys_in, vals_in, keys_out, vals_out, n_dev,
-                                                               n_host, shift, hist, status, ticket, epoch, ranges);
+                                                               n_host, shift, hist, status, ticket, epoch_base,
+                                                               epoch_off, ranges);
   else
     onesweep_kernel<false><<<blocks, GUT_SORT_THREADS, 0, st>>>(keys_in, vals_in, keys_out, vals_out, n_dev,
-                                                                n_host, shift, hist, status, ticket, epoch, ranges);
+                                                                n_host, shift, hist, status, ticket, epoch_base,
+                                                                epoch_off, ranges);
+}
+
+// One block: base += GUT_EPOCHS_PER_RENDER; on a wrap of the blend's 22-bit
+// epoch field the blend status words are cleared (every 2^19 renders).
+__global__ void epoch_advance_kernel(uint32_t *counters, unsigned long long *bstatus, size_t n) {
+  __shared__ uint32_t s_wrap;
+  if (threadIdx.x == 0) {
+    const uint32_t old = counters[CNT_EPOCH], nb = old + GUT_EPOCHS_PER_RENDER;
+    s_wrap = ((old + GUT_EPOCH_BLEND) >> 22) != ((nb + GUT_EPOCH_BLEND) >> 22);
+    counters[CNT_EPOCH] = nb;
+  }
+  __syncthreads();
+  if (s_wrap)
+    for (size_t j = threadIdx.x; j < n; j += blockDim.x) bstatus[j] = 0ull;
+}
+
+void launch_epoch_advance(uint32_t *counters, unsigned long long *bstatus, size_t n_bstatus, cudaStream_t st) {
+  epoch_advance_kernel<<<1, 1024, 0, st>>>(counters, bstatus, n_bstatus);
 }
 
 }  // namespace gut

@@ -606,7 +606,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
 #pragma unroll
       for (int k = 0; k < NP; ++k)
         if (!L.done[k]) {
-          const unsigned long long Lb = pred_L(poll_stat + 64 * k, poll_s, B.epoch);
+          const unsigned long long Lb = pred_L(poll_stat + 64 * k, poll_s, __ldg(B.epoch) + GUT_EPOCH_BLEND);
           if (Lb >= GUT_L_DEAD || L.T[k] * exp2f(-(float)Lb * 2.3283064365386963e-10f) < t_min)
             L.done[k] = L.term[k] = true;
         }
@@ -963,6 +963,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
   const int lane = threadIdx.x & 31;
   uint32_t n_eval_acc = 0, n_contrib_acc = 0, n_term_acc = 0;
   const uint32_t n_init = B.counters[CNT_Q_NINIT];
+  const uint32_t epoch = __ldg(B.epoch) + GUT_EPOCH_BLEND;  // (device epoch: graph-replayable)
 
   for (;;) {
     int unit = -1, s = 0;
@@ -1035,7 +1036,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     bool run[NP];
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
-      run[k] = valid[k] && !(s > 0 && pred_dead(stat + 64 * k, s, B.epoch));
+      run[k] = valid[k] && !(s > 0 && pred_dead(stat + 64 * k, s, epoch));
       L.done[k] = !run[k];
       L.term[k] = false;
       L.T[k] = 1.f;
@@ -1059,14 +1060,14 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
         unsigned long long *st = stat + 64 * k;
         unsigned long long Lpre = 0;
         if (s == 0) {
-          st_relaxed(st, st_word(2, B.epoch, Ls));
+          st_relaxed(st, st_word(2, epoch, Ls));
         } else {
-          st_relaxed(st, st_word(1, B.epoch, Ls));
+          st_relaxed(st, st_word(1, epoch, Ls));
           // decoupled look-back over this pixel's earlier segments (integer sums)
           for (int j = s - 1;; --j) {
             const unsigned long long wv = ld_relaxed(st - (size_t)(s - j) * NT);
             const uint32_t flag = (uint32_t)(wv >> 62);
-            if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (B.epoch & 0x3FFFFFu)) {
+            if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (epoch & 0x3FFFFFu)) {
               __nanosleep(256);  // predecessor still running: yield issue slots to the SM's other warps
               ++j;
               continue;
@@ -1076,7 +1077,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
             if (flag == 2) break;
           }
           const unsigned long long Lin = Lpre + Ls >= GUT_L_DEAD ? GUT_L_DEAD : Lpre + Ls;
-          st_relaxed(st, st_word(2, B.epoch, Lin));
+          st_relaxed(st, st_word(2, epoch, Lin));
         }
         T_pre[k] = t_of(Lpre);
         alive_in[k] = T_pre[k] >= c.t_min;

@@ -73,7 +73,10 @@ __device__ __forceinline__ float reduce16(const float (&v)[16], int lane) {
 // One CTA per tile, 8 warps = the tile's 8x4 pixel blocks (one pixel per lane,
 // rays_kernel's layout); every warp walks the whole list in chunks of 32.
 template <int MODE>
-__global__ __launch_bounds__(256) void backward_kernel(DevCam c, BwdBufs B) {
+#ifndef GUT_K6_MINB
+#define GUT_K6_MINB 1  // min resident CTAs per SM for the register budget (tuning switch)
+#endif
+__global__ __launch_bounds__(256, GUT_K6_MINB) void backward_kernel(DevCam c, BwdBufs B) {
   constexpr int BW_NF = BwNF<MODE>::v;
   extern __shared__ float4 s_dyn[];
   // CTAs take the tiles in decreasing list length (the plan's queue 1 with one

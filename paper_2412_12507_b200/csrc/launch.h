@@ -45,6 +45,9 @@ enum : int {
   // sticky words after the per-render memset range: set by the kernels, read
   // and cleared only by the host at a synchronising call (gut_check & co.)
   CNT_STICKY_OVERFLOW = CNT_WORDS,
+  // look-back epoch base of the current render, advanced on the device at the
+  // start of every render (epoch_advance): a render is replayable as a CUDA graph
+  CNT_EPOCH = CNT_WORDS + 1,
   CNT_ALLOC = CNT_WORDS + 4
 };
 
@@ -60,8 +63,16 @@ void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32
 // items equal to GUT_CULLED_KEY dropped.  n_dev: device count (nullable, then n_host).
 void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                       uint32_t *vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
-                      const uint32_t *hist, unsigned long long *status, uint32_t *ticket, uint32_t epoch,
-                      bool first, cudaStream_t st, uint2 *ranges = nullptr);
+                      const uint32_t *hist, unsigned long long *status, uint32_t *ticket,
+                      const uint32_t *epoch_base, uint32_t epoch_off, bool first, cudaStream_t st,
+                      uint2 *ranges = nullptr);
+// Epochs per render: sort passes use base + 0..6 (depth 0-3, tile 4 and 6), the blend base + GUT_EPOCH_BLEND.
+#define GUT_EPOCHS_PER_RENDER 8u
+#define GUT_EPOCH_BLEND 7u
+// Advances the device epoch base by GUT_EPOCHS_PER_RENDER (one thread block);
+// when the blend's 22-bit epoch field wraps it clears the blend status words
+// (n_bstatus), so a stale word can never alias the current render.
+void launch_epoch_advance(uint32_t *counters, unsigned long long *bstatus, size_t n_bstatus, cudaStream_t st);
 // K4 fused into the final tile pass (ranges != nullptr there): ranges start empty
 void launch_ranges_init(uint2 *ranges, int n_tiles, cudaStream_t st);
 
@@ -110,7 +121,7 @@ struct BlendBufs {
   uint2 *tile_work;
   uint4 *trace;  // optional (GUT_BLEND_TRACE=1): per (slot, warp block) 2 x uint4 (see GUT_STAGE_BLEND_TRACE)
   int seg, window, n_tiles;
-  uint32_t epoch;
+  const uint32_t *epoch;  // device epoch base (CNT_EPOCH); the blend uses base + GUT_EPOCH_BLEND
   float *rgb, *alpha, *depth;
   uint32_t *counters;
 };

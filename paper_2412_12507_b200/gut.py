@@ -117,9 +117,10 @@ def lib():
                                              vp, vp]
         L.gut_timing_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int32), i32]
         L.gut_check.argtypes = [vp, vp]
+        L.gut_context_set_frames_in_flight.argtypes = [vp, i32]
         for name in ("gut_context_create", "gut_workspace_reserve", "gut_scene_create", "gut_render",
                      "gut_render_batch", "gut_render_backward", "gut_projection_quality", "gut_timing_read",
-                     "gut_debug_copy_stage", "gut_check"):
+                     "gut_debug_copy_stage", "gut_check", "gut_context_set_frames_in_flight"):
             getattr(L, name).restype = C.c_int
         L.gut_options_default.restype = None
         L.gut_context_destroy.restype = None
@@ -269,6 +270,10 @@ def gut_render_batch(ctx, scene, cams: Sequence[gut_camera], opt: gut_options, o
     st = (gut_stats * n)() if stats else None
     _check(lib().gut_render_batch(ctx, scene, carr, n, C.byref(opt), oarr, _stream_ptr(stream), st), ctx)
     return st
+
+
+def gut_context_set_frames_in_flight(ctx, n: int):
+    _check(lib().gut_context_set_frames_in_flight(ctx, int(n)), ctx)
 
 
 def gut_timing_read(ctx, reset: bool = True):
