@@ -33,7 +33,7 @@ struct gut_context {
   uint32_t *dkey = nullptr, *tiles = nullptr;
   float4 *ell = nullptr, *payload = nullptr;
   double2 *ell64 = nullptr;
-  uint32_t *deferred = nullptr;
+  uint32_t *deferred = nullptr, *k1_list = nullptr;
   uint2 *big_list = nullptr;  // K2: (Gaussian, first key slot) of the big Gaussians
   uint32_t *sa_k = nullptr, *sa_v = nullptr, *sb_k = nullptr, *sb_v = nullptr;
   uint32_t *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr;
@@ -111,6 +111,7 @@ static gut_status ensure_n(gut_context *ctx, size_t n) {
   CUDA_TRY(ctx, regrow(ctx->ell, dummy, 2 * c));
   CUDA_TRY(ctx, regrow(ctx->ell64, dummy, 3 * c));
   CUDA_TRY(ctx, regrow(ctx->deferred, dummy, c));
+  CUDA_TRY(ctx, regrow(ctx->k1_list, dummy, c));
   CUDA_TRY(ctx, regrow(ctx->big_list, dummy, c));
   CUDA_TRY(ctx, regrow(ctx->payload, dummy, (size_t)GUT_PAYLOAD_F4 * c));
   CUDA_TRY(ctx, regrow(ctx->sa_k, dummy, c));
@@ -350,7 +351,7 @@ void gut_context_destroy(gut_context *ctx) {
   for (cudaEvent_t e : ctx->lane_events) cudaEventDestroy(e);
   if (ctx->fork_event) cudaEventDestroy(ctx->fork_event);
   cudaSetDevice(ctx->device);
-  void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->deferred, ctx->big_list, ctx->payload, ctx->sa_k, ctx->sa_v,
+  void *ps[] = {ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->deferred, ctx->k1_list, ctx->big_list, ctx->payload, ctx->sa_k, ctx->sa_v,
                 ctx->sb_k, ctx->sb_v,
                 ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->tile_work, ctx->img, ctx->st_depth,
                 ctx->st_emit, ctx->st_tile, ctx->counters, ctx->pix, ctx->anchors, ctx->seg_base, ctx->unit_ctr, ctx->q1, ctx->q2,
@@ -518,7 +519,8 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   // look-back epochs of this render (device-side, so a captured render replays correctly)
   launch_epoch_advance(cnt, ctx->bstatus, ctx->cap_items * GUT_TILE_PX, st);
   // K1: UT projection
-  launch_project(dc, scene->d, ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->payload, cnt, ctx->deferred, st);
+  launch_project(dc, scene->d, ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->payload, cnt, ctx->deferred,
+                 ctx->k1_list, st);
   if (timing) cudaEventRecord(ev[1], st);
   // K3 level 1: depth sort of the visible Gaussians (4 LSD passes, first one compacts)
   const uint32_t n32 = (uint32_t)N;

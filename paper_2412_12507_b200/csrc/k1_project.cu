@@ -357,20 +357,25 @@ __device__ __forceinline__ void k1_block_totals(uint32_t my_tiles, uint32_t key,
 }
 
 // ---- K1 main (fp32): one thread per Gaussian
-template <int DEG>
+template <int DEG, bool LIST>
 #ifndef GUT_K1_CTAS
 #define GUT_K1_CTAS 4  // 64 registers: 32 warps per SM (measured best)
 #endif
 __global__ __launch_bounds__(256, GUT_K1_CTAS) void project_kernel(DevCam c, SceneDev s, uint32_t *__restrict__ dkey,
                                                          uint32_t *__restrict__ tiles, float4 *__restrict__ ell,
                                                          float4 *__restrict__ payload, uint32_t *counters,
-                                                         uint32_t *__restrict__ deferred) {
+                                                         uint32_t *__restrict__ deferred,
+                                                         const uint32_t *__restrict__ list) {
   __shared__ uint32_t s_hist[4][256];
   __shared__ unsigned long long s_k[8];
   __shared__ uint32_t s_nv[8];
+  // LIST: the Gaussians the pre-filter kept (counters[CNT_K1LIST] of them)
+  const int64_t n_items = LIST ? (int64_t)counters[CNT_K1LIST] : s.n;
+  if (LIST && (int64_t)blockIdx.x * 256 >= n_items) return;  // (whole block past the list: uniform)
   for (int j = threadIdx.x; j < 1024; j += 256) (&s_hist[0][0])[j] = 0;
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t idx = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t i = LIST ? (idx < n_items ? (int64_t)list[idx] : s.n) : idx;
   uint32_t my_code = 0, key = GUT_CULLED_KEY;  // my_code: tile code (gut_internal.cuh)
   if (i < s.n) {
     float4 po, sc;
@@ -569,26 +574,89 @@ void launch_pack_scene(const float *means, const float *rots, const float *scale
 }
 
 
+// Rolling shutter: a cheap, conservative pre-filter so that the expensive
+// per-sigma-point shutter-time solves run on dense warps (street scenes cull
+// ~3/4 of the Gaussians per camera; without it warps average ~7 active lanes).
+// A Gaussian is dropped only if its CENTRE sigma point is invalid at every
+// shutter time t in [0, 1] -- and then the full K1 culls it too (reading R9:
+// any invalid sigma point culls).  Over t the camera-frame centre stays in the
+// ball |x_c(t) - y| <= |dc| + |phi| |y| around y = R0^T (mu - c0); the tests
+// below hold for every point of that ball (plus an fp32 slack): behind the near
+// plane; OpenCV outside the validity radius r_lim; fisheye beyond theta_max or
+// inside the near sphere.  Culled Gaussians get K1's culled outputs; the rest
+// are appended to a list (warp-aggregated) for project_kernel.
+__global__ __launch_bounds__(256) void project_prefilter_kernel(DevCam c, SceneDev s, uint32_t *__restrict__ dkey,
+                                                                uint32_t *__restrict__ tiles, uint32_t *counters,
+                                                                uint32_t *__restrict__ list) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  bool keep = false;
+  if (i < s.n) {
+    const float4 po = __ldg(&s.pos_opa[i]);
+    keep = true;
+    if (isfinite(po.x) && isfinite(po.y) && isfinite(po.z)) {
+      const f3 y = mtv(c.R0f, mk((float)((double)po.x - c.c0[0]), (float)((double)po.y - c.c0[1]),
+                                 (float)((double)po.z - c.c0[2])));
+      const float ny = sqrtf(dot(y, y));
+      const float dcn = sqrtf(c.dcf[0] * c.dcf[0] + c.dcf[1] * c.dcf[1] + c.dcf[2] * c.dcf[2]);
+      const float dl = dcn + fabsf(c.phi_anglef) * ny + 1e-4f * ny + 1e-4f;  // ball radius + fp32 slack
+      const float rho = sqrtf(y.x * y.x + y.y * y.y);
+      if (c.model == CAM_PINHOLE || c.model == CAM_OPENCV) {
+        if (y.z + dl < c.near_plane) keep = false;
+        else if (c.model == CAM_OPENCV && c.fovf > 0.f && rho - dl > 0.f && rho - dl > c.fovf * (y.z + dl))
+          keep = false;
+      } else if (c.model == CAM_FISHEYE) {
+        if (ny + dl < c.near_plane) keep = false;
+        else if (ny > 2.f * dl) {
+          // angle of y to the axis minus the ball's angular radius (asin(dl/|y|) <= 2 dl/|y| here)
+          const float th = atan2f(rho, y.z) - 2.f * dl / ny;
+          if (th > c.fovf + 1e-5f) keep = false;
+        }
+      }
+    }
+    if (!keep) {
+      dkey[i] = GUT_CULLED_KEY;
+      tiles[i] = 0u;
+    }
+  }
+  const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == 0 && bal) base = atomicAdd(&counters[CNT_K1LIST], (uint32_t)__popc(bal));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (keep) list[base + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)i;
+}
+
 void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32_t *tiles, float4 *ell,
-                    double2 *ell64, float4 *payload, uint32_t *counters, uint32_t *deferred, cudaStream_t st) {
+                    double2 *ell64, float4 *payload, uint32_t *counters, uint32_t *deferred, uint32_t *list,
+                    cudaStream_t st) {
   if (s.n == 0) return;
   const unsigned blocks = (unsigned)((s.n + 255) / 256);
   const unsigned wblocks = 148 * 4;  // grid-stride over the deferred Gaussians (count known on the device only)
+  // (global shutter: measured slower on every config -- the per-Gaussian work is small)
+  if (cam.shutter != SH_GLOBAL && cam.model != CAM_ORTHO) {
+    project_prefilter_kernel<<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, counters, list);
+  } else {
+    list = nullptr;
+  }
   switch (s.sh_degree) {
     case 0:
-      project_kernel<0><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      if (list) project_kernel<0, true><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+      else project_kernel<0, false><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
       project_wide_kernel<0><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
       break;
     case 1:
-      project_kernel<1><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      if (list) project_kernel<1, true><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+      else project_kernel<1, false><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
       project_wide_kernel<1><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
       break;
     case 2:
-      project_kernel<2><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      if (list) project_kernel<2, true><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+      else project_kernel<2, false><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
       project_wide_kernel<2><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
       break;
     default:
-      project_kernel<3><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred);
+      if (list) project_kernel<3, true><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+      else project_kernel<3, false><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
       project_wide_kernel<3><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
       break;
   }

@@ -528,7 +528,7 @@ __device__ __forceinline__ void kb_insert(KBuf<KB> &kb, LanePx<NP> &L, int k, fl
 template <int MODE, int NP, int KB = 0>
 __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, uint32_t s0, uint32_t s1,
                                           const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f, float ac, float bc,
-                                          float ra, float rb, LanePx<NP> &L, uint32_t &n_eval, uint32_t &n_contrib,
+                                          float ra, float rb, float tc, float rt, LanePx<NP> &L, uint32_t &n_eval, uint32_t &n_contrib,
                                           uint32_t &processed, const unsigned long long *poll_stat, int poll_s,
                                           Checkpoints<NP> *ck, uint32_t ck_step, const uint32_t *act,
                                           KBuf<KB> *kb = nullptr) {
@@ -693,8 +693,23 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
       // Rolling shutter: every entry is kept.
       const f3 n0 = c0 + ac * P + bc * Q;
       const f3 e0c = e0 + ac * U + bc * V;
+      f3 mdc = mk(0, 0, 0), h = mk(0, 0, 0), PU = mk(0, 0, 0), QV = mk(0, 0, 0);
       if (MODE == 2) {
-        maybe = true;
+        // rolling shutter: n = c0 + aP + bQ + beta (h + a PU + b QV) with beta
+        // (pixel time - anchor time) in tc +- rt over the warp's rows.  Around
+        // the box centre n = n_c + da (P + tc PU) + db (Q + tc QV) + dt (h + ac PU
+        // + bc QV) + da dt PU + db dt QV, so |n| >= |n_c| - (ra |P + tc PU| + rb |Q
+        // + tc QV| + rt |h + ac PU + bc QV| + ra rt |PU| + rb rt |QV|) (triangle
+        // inequality); e does not depend on beta.  Same 1e-3 margin as below.
+        mdc = mv(M, dcw);
+        h = cross(mdc, e0); PU = cross(mdc, U); QV = cross(mdc, V);
+        const f3 Pt = P + tc * PU, Qt = Q + tc * QV, Ht = h + ac * PU + bc * QV;
+        const f3 nc = n0 + tc * Ht;
+        const float lo = sqrt_approx(dot(nc, nc)) -
+                         (ra * sqrt_approx(dot(Pt, Pt)) + rb * sqrt_approx(dot(Qt, Qt)) + rt * sqrt_approx(dot(Ht, Ht)) +
+                          rt * (ra * sqrt_approx(dot(PU, PU)) + rb * sqrt_approx(dot(QV, QV))));
+        const float hi = sqrt_approx(dot(e0c, e0c)) + (ra * sqrt_approx(dot(U, U)) + rb * sqrt_approx(dot(V, V)));
+        maybe = !(lo > 0.f && lo * lo > 1.001f * k2 * (hi * hi));
       } else {
         // (MUFU square roots: 2^-22 relative, inside the 1e-3 margin below)
         const float lo = sqrt_approx(dot(n0, n0)) - (ra * sqrt_approx(dot(P, P)) + rb * sqrt_approx(dot(Q, Q)));
@@ -704,8 +719,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
       if (maybe) {
         float4 *t = wt + lane * NF;
         if (MODE == 2) {
-          const f3 m = mv(M, dcw);
-          const f3 h = cross(m, e0), PU = cross(m, U), QV = cross(m, V);
+          const f3 m = mdc;
           t[0] = make_float4(c0.x, c0.y, c0.z, k2);
           t[1] = make_float4(P.x, P.y, P.z, Q.x);
           t[2] = make_float4(Q.y, Q.z, e0.x, e0.y);
@@ -985,7 +999,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     LanePx<NP> L;
     bool valid[NP], inside[NP];
     int px[NP], py[NP];
-    float amin = 3e38f, amax = -3e38f, bmin = 3e38f, bmax = -3e38f;
+    float amin = 3e38f, amax = -3e38f, bmin = 3e38f, bmax = -3e38f, tmin = 3e38f, tmax = -3e38f;
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
       tile_pixel(tile, c.tiles_x, ((w & 1) | (((w >> 1) * 2 + k) << 1)), lane, px[k], py[k]);
@@ -996,6 +1010,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
       if (valid[k]) {
         amin = fminf(amin, pl.x); amax = fmaxf(amax, pl.x);
         bmin = fminf(bmin, pl.y); bmax = fmaxf(bmax, pl.y);
+        tmin = fminf(tmin, pl.w); tmax = fmaxf(tmax, pl.w);
       }
     }
     // ---- the tile anchor in the world frame (fp64)
@@ -1013,7 +1028,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     }
     const f3 T1f = tof(T1), T2f = tof(T2);
     // warp pixel box in (a, b) for the conservative warp cull
-    float ac, bc, ra, rb;
+    float ac, bc, ra, rb, tc = 0.f, rt = 0.f;
     {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1021,8 +1036,16 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
         amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, o));
         bmin = fminf(bmin, __shfl_xor_sync(FULL, bmin, o));
         bmax = fmaxf(bmax, __shfl_xor_sync(FULL, bmax, o));
+        if (MODE == 2) {
+          tmin = fminf(tmin, __shfl_xor_sync(FULL, tmin, o));
+          tmax = fmaxf(tmax, __shfl_xor_sync(FULL, tmax, o));
+        }
       }
-      if (amin > amax) { amin = amax = 0.f; bmin = bmax = 0.f; }  // no valid pixel: the warp is idle
+      if (amin > amax) { amin = amax = 0.f; bmin = bmax = 0.f; tmin = tmax = 0.f; }  // no valid pixel: the warp is idle
+      if (MODE == 2) {  // pixel-time offsets of the warp's rows (rolling shutter)
+        tc = 0.5f * (tmin + tmax);
+        rt = 0.5f * (tmax - tmin) + 1e-7f * (fabsf(tmin) + fabsf(tmax));
+      }
       ac = 0.5f * (amin + amax);
       bc = 0.5f * (bmin + bmax);
       ra = 0.5f * (amax - amin) + 1e-7f * (fabsf(amin) + fabsf(amax));
@@ -1045,7 +1068,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     uint32_t n_eval = 0, n_contrib = 0, processed = 0;
     Checkpoints<NP> ck;
     const uint32_t ck_step = max(32u, ((uint32_t)B.seg / GUT_CK) & ~31u);
-    warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, L, n_eval, n_contrib, processed,
+    warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, tc, rt, L, n_eval, n_contrib, processed,
                         s > 0 ? stat : nullptr, s, s > 0 ? &ck : nullptr, ck_step, nullptr);
     unsigned long long t_spec = 0, t_lb = 0;  // (trace only: end of the speculative pass / of the look-back)
     if (B.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_spec));
@@ -1118,7 +1141,8 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
         }
       }
       uint32_t e2 = 0, c2 = 0, p2 = 0;
-      warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, R, e2, c2, p2, nullptr, 0, nullptr, 0, act);
+      warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, tc, rt, R, e2, c2, p2, nullptr, 0, nullptr, 0,
+                          act);
 #pragma unroll
       for (int k = 0; k < NP; ++k)
         if (redo[k]) {
@@ -1329,6 +1353,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kbuf_kern
     const bool valid = inside && pl.z > 0.f;
     float amin = valid ? pl.x : 3e38f, amax = valid ? pl.x : -3e38f;
     float bmin = valid ? pl.y : 3e38f, bmax = valid ? pl.y : -3e38f;
+    float tmin = valid ? pl.w : 3e38f, tmax = valid ? pl.w : -3e38f;
     const TileAnchor &A = B.anchors[tile];
     d3 D, T1, T2, O;
     if (MODE == 2) {
@@ -1342,7 +1367,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kbuf_kern
       if (MODE == 1) O = O + mv(c.R0, mkd(A.O[0], A.O[1], A.O[2]));
     }
     const f3 T1f = tof(T1), T2f = tof(T2);
-    float ac, bc, ra, rb;
+    float ac, bc, ra, rb, tc = 0.f, rt = 0.f;
     {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1350,8 +1375,16 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kbuf_kern
         amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, o));
         bmin = fminf(bmin, __shfl_xor_sync(FULL, bmin, o));
         bmax = fmaxf(bmax, __shfl_xor_sync(FULL, bmax, o));
+        if (MODE == 2) {
+          tmin = fminf(tmin, __shfl_xor_sync(FULL, tmin, o));
+          tmax = fmaxf(tmax, __shfl_xor_sync(FULL, tmax, o));
+        }
       }
-      if (amin > amax) { amin = amax = 0.f; bmin = bmax = 0.f; }
+      if (amin > amax) { amin = amax = 0.f; bmin = bmax = 0.f; tmin = tmax = 0.f; }
+      if (MODE == 2) {
+        tc = 0.5f * (tmin + tmax);
+        rt = 0.5f * (tmax - tmin) + 1e-7f * (fabsf(tmin) + fabsf(tmax));
+      }
       ac = 0.5f * (amin + amax);
       bc = 0.5f * (bmin + bmax);
       ra = 0.5f * (amax - amin) + 1e-7f * (fabsf(amin) + fabsf(amax));
@@ -1366,7 +1399,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kbuf_kern
 #pragma unroll
     for (int i = 0; i < KB; ++i) { kb.t[i] = -INFINITY; kb.a[i] = 0.f; kb.g[i] = 0u; }
     uint32_t n_eval = 0, n_contrib = 0, processed = 0;
-    warp_pass<MODE, 1, KB>(c, B, start, end, D, O, T1f, T2f, ac, bc, ra, rb, L, n_eval, n_contrib, processed,
+    warp_pass<MODE, 1, KB>(c, B, start, end, D, O, T1f, T2f, ac, bc, ra, rb, tc, rt, L, n_eval, n_contrib, processed,
                            nullptr, 0, nullptr, 0, nullptr, &kb);
     // end of the list: the pending hits near to far (colours gathered up front)
     if (!L.done[0]) {

@@ -38,6 +38,7 @@ enum : int {
   CNT_Q_ALLOC2 = 35,       //   queue-2 entries allocated
   CNT_Q_FINISHED = 36,     //   units (8 per tile) whose pixels are written
   CNT_NBIG = 37,           // K2: Gaussians in the big list (tile rectangle > 3x3)
+  CNT_K1LIST = 38,         // K1 (rolling shutter): Gaussians kept by the pre-filter
   CNT_HIST_DEPTH = 64,     // 4 x 256
   CNT_HIST_TILE = 64 + 1024,  // 2 x 256
   CNT_PLAN_HIST = 64 + 1024 + 512,  // 1024 blend queue-1 buckets
@@ -56,8 +57,10 @@ void launch_pack_scene(const float *means, const float *rots, const float *scale
 
 // K1 (fp32) followed by the fp64 kernel for the deferred "wide" Gaussians;
 // ell64 [3 x double2 per Gaussian] holds their fp64 ellipse (record k2 < 0)
+// list: N uint32 scratch (rolling shutter: the Gaussians kept by the pre-filter)
 void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32_t *tiles, float4 *ell,
-                    double2 *ell64, float4 *payload, uint32_t *counters, uint32_t *deferred, cudaStream_t st);
+                    double2 *ell64, float4 *payload, uint32_t *counters, uint32_t *deferred, uint32_t *list,
+                    cudaStream_t st);
 
 // one onesweep LSD pass over 8-bit digit `shift`; first = keys only, value = index,
 // items equal to GUT_CULLED_KEY dropped.  n_dev: device count (nullable, then n_host).
