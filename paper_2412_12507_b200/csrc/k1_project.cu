@@ -113,12 +113,21 @@ __device__ __forceinline__ f3 cam_point_at(const DevCam &c, f3 y, f3 w, float t)
 // g(x) with the sigma point's own extrinsic (reading R14): the shutter time is
 // the fixed point t* = clamp(rho(g(x; pose(t*)))), solved by secant steps from
 // (0.5, rho(g(x; pose(0.5)))) until the pixel moves < rs_tol_px.
+// (one out-of-line copy: the seven inlined secant loops of a Gaussian overflow
+// the instruction cache -- ncu: 40% "no instruction" stalls in rolling shutter)
+__device__ __noinline__ bool project_sigma_rs(const DevCam &c, f3 y, f3 w, float &du, float &dv, float &t_out);
+// RS: the rolling-shutter instantiation of K1 (project_kernel<DEG, true>); the
+// global-shutter one never contains the shutter solve
+template <bool RS>
 __device__ __forceinline__ bool project_sigma(const DevCam &c, f3 y, f3 w, float &du, float &dv,
                                               float &t_out) {
-  if (c.shutter == SH_GLOBAL) {
+  if (!RS || c.shutter == SH_GLOBAL) {
     t_out = 0.f;
     return project_cam_f(c, y, du, dv);
   }
+  return project_sigma_rs(c, y, w, du, dv, t_out);
+}
+__device__ __noinline__ bool project_sigma_rs(const DevCam &c, f3 y, f3 w, float &du, float &dv, float &t_out) {
   float t0 = 0.5f, u0, v0;
   if (!project_cam_f(c, cam_point_at(c, y, w, t0), u0, v0)) return false;
   float f0 = shutter_coord(c, u0, v0) - t0;
@@ -390,13 +399,13 @@ __global__ __launch_bounds__(256, GUT_K1_CTAS) void project_kernel(DevCam c, Sce
       const f3 y0 = tof(y0d);
       const f3 wv = mtv(c.R0f, mk(c.dcf[0], c.dcf[1], c.dcf[2]));
       const float sj[3] = {sc.x, sc.y, sc.z};
-      ok = project_sigma(c, y0, wv, du[0], dv[0], tt[0]);
+      ok = project_sigma<LIST>(c, y0, wv, du[0], dv[0], tt[0]);
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         const f3 L = (c.gamma * sj[j]) * mk(R[j], R[3 + j], R[6 + j]);
         const f3 Lc = mtv(c.R0f, L);
-        ok = ok && project_sigma(c, y0 + Lc, wv, du[1 + j], dv[1 + j], tt[1 + j]);
-        ok = ok && project_sigma(c, y0 - Lc, wv, du[4 + j], dv[4 + j], tt[4 + j]);
+        ok = ok && project_sigma<LIST>(c, y0 + Lc, wv, du[1 + j], dv[1 + j], tt[1 + j]);
+        ok = ok && project_sigma<LIST>(c, y0 - Lc, wv, du[4 + j], dv[4 + j], tt[4 + j]);
       }
     }
     float vx = 0, vy = 0, cxx = 0, cxy = 0, cyy = 0, k2 = 0;
