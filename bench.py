@@ -166,7 +166,7 @@ def roofline(stage_ms, work, peaks, builder=None):
 
 
 # ncu kernel names of the stages (profiles/<tag>_traffic.json, tools/profile_round.sh)
-NCU_NAMES = {"K5_blend": "blend_kernel<0>", "K1_project": "project_kernel<3>", "K2_emit": "emit_kernel",
+NCU_NAMES = {"K5_blend": "blend_kernel<0>", "K1_project": "project_kernel<3, 0>", "K2_emit": "emit_kernel",
              "K3_sort": "onesweep_kernel<0>"}
 
 

@@ -88,12 +88,12 @@ def gather_stats(rows: Sequence[Sequence[float]], device=None) -> List[List[floa
 
 
 def image_checksum(t: torch.Tensor) -> int:
-    """48-bit position-weighted sum of the tensor's 32-bit words (integer
-    arithmetic: bitwise reproducible, exact in the float64 stats rows that
-    gather_stats carries).  Equal images <=> equal checksums (up to collisions)."""
-    w = t.contiguous().view(torch.int32).reshape(-1).to(torch.int64) & 0xFFFFFFFF
-    idx = torch.arange(1, w.numel() + 1, device=w.device, dtype=torch.int64)
-    return int(((w * idx).sum() + w.numel()).item()) & ((1 << 48) - 1)
+    """48-bit digest (BLAKE2b) of the tensor's bytes, hashed on the host (no
+    device kernels): exact in the float64 stats rows that gather_stats carries.
+    Equal images <=> equal checksums (up to collisions)."""
+    import hashlib
+    b = t.detach().contiguous().cpu().numpy().tobytes()
+    return int.from_bytes(hashlib.blake2b(b, digest_size=6).digest(), "little")
 
 
 def barrier():
