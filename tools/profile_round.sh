@@ -11,8 +11,9 @@ cd "$(dirname "$0")/.."
 tag=${1:-r2}
 part=${2:-all}   # main | configs | next | all  (gpurun brings back <= 64 MiB per call)
 if [ "$part" = main ] || [ "$part" = all ]; then
-ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 72 --csv \
-    --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 3 --warmup 5 --no-cpu-baseline --sorted-k 0 --no-backward \
+# launch list of bench.py's timed region (NVTX range bench_timed)
+ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "bench_timed/" --csv \
+    --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 4 --warmup 5 --no-cpu-baseline --sorted-k 0 --no-backward \
     > gpurun_out/${tag}_launches.log 2>&1
 # second render of view 1: skip the scene pack + the first render (18 kernels + the ray table)
 ncu --set full --clock-control none -s 20 -c 18 -o gpurun_out/${tag}_full \
