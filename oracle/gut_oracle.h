@@ -86,7 +86,14 @@ typedef struct {
   int32_t amb_cull;        /* a cull-ambiguous Gaussian could change this pixel */
   double min_tau_gap;      /* kbuffer != 0: min relative tau_max gap between two hits adjacent
                               in tau order (an fp32 tau could swap them) */
+  int32_t alt_valid;       /* kbuffer != 0: exactly one such pair within the alt band -> alt_*
+                              hold the pixel with the two hits' tau_max swapped (the other order) */
+  int32_t alt_pad;
+  double alt_rgb[3], alt_alpha, alt_depth;  /* (without the background term: C, 1 - T, D) */
 } orc_pixdiag;
+
+/* relative tau_max band of the alternative-order render (default 2e-6) */
+void orc_set_alt_band(double band);
 
 /* ---- O1 ---- */
 int  orc_ut_weights(double a, double b, double k, double wmu[7], double wsig[7], double *lambda);

@@ -63,7 +63,8 @@ class OrcPixDiag(C.Structure):
     _fields_ = [("visited", C.c_int32), ("contributed", C.c_int32), ("terminated", C.c_int32),
                 ("invalid", C.c_int32), ("min_alpha_gap", C.c_double), ("min_term_gap", C.c_double),
                 ("min_order_gap", C.c_double), ("amb_bin", C.c_int32), ("amb_cull", C.c_int32),
-                ("min_tau_gap", C.c_double)]
+                ("min_tau_gap", C.c_double), ("alt_valid", C.c_int32), ("alt_pad", C.c_int32),
+                ("alt_rgb", C.c_double * 3), ("alt_alpha", C.c_double), ("alt_depth", C.c_double)]
 
 
 PROJ_DTYPE = np.dtype([("reason", "<i4"), ("tiles", "<i4"), ("rect", "<i4", 4), ("cull_ambig", "<i4"),
@@ -73,7 +74,8 @@ PROJ_DTYPE = np.dtype([("reason", "<i4"), ("tiles", "<i4"), ("rect", "<i4", 4), 
 DIAG_DTYPE = np.dtype([("visited", "<i4"), ("contributed", "<i4"), ("terminated", "<i4"),
                        ("invalid", "<i4"), ("min_alpha_gap", "<f8"), ("min_term_gap", "<f8"),
                        ("min_order_gap", "<f8"), ("amb_bin", "<i4"), ("amb_cull", "<i4"),
-                       ("min_tau_gap", "<f8")])
+                       ("min_tau_gap", "<f8"), ("alt_valid", "<i4"), ("alt_pad", "<i4"),
+                       ("alt_rgb", "<f8", 3), ("alt_alpha", "<f8"), ("alt_depth", "<f8")])
 assert PROJ_DTYPE.itemsize == C.sizeof(OrcProj)
 assert DIAG_DTYPE.itemsize == C.sizeof(OrcPixDiag)
 
@@ -113,6 +115,8 @@ def lib():
         L.orc_threads.restype = C.c_int
         L.orc_kbuffer_blend.argtypes = [dp, dp, dp, C.c_int32, C.c_int32, C.c_double, dp, dp, dp, ip, dp]
         L.orc_kbuffer_blend.restype = C.c_int32
+        L.orc_set_alt_band.argtypes = [C.c_double]
+        L.orc_set_alt_band.restype = None
         L.orc_backward.argtypes = [fp, fp, fp, fp, fp, C.c_int32, C.c_int64, C.POINTER(OrcCamera),
                                    C.POINTER(OrcOptions), fp, fp, fp, dp, dp, dp, dp, dp, dp, dp]
         L.orc_backward.restype = C.c_int64

@@ -120,3 +120,55 @@ def test_backward_errors():
             r.backward(c2, o2, out2, torch.zeros_like(out2[0]))
         assert e.value.status == 2
     r.close()
+
+
+def test_full_size_sampled_backward():
+    """The bench frame (3M Gaussians, 1920x1080 fisheye, the launch
+    configuration bench.py times for ours_forward_backward) with random upstream
+    gradients on 24 sampled tiles (the 8 longest lists + 16 random ones), zero
+    elsewhere and on ambiguous pixels: every per-Gaussian gradient against the
+    fp64 oracle O7 (which skips zero-gradient pixels exactly)."""
+    import torch
+    from oracle import oracle as O
+    from paper_2412_12507_b200 import gut
+    scene = S.make_scene("multiview")
+    cam = S.make_views("multiview")[0]
+    opt = S.RenderOptions()
+    r = gut.Renderer(scene, reserve_keys=int(scene.count * 12), max_wh=(cam.width, cam.height))
+    out = r.render(cam, opt)[:3]
+    ranges = r.stage(gut.STAGE_RANGES)
+    tx, ty = cam.tiles
+    lens = ranges[:, 1].astype(np.int64) - ranges[:, 0]
+    rng = np.random.default_rng(7)
+    longest = np.argsort(-lens)[:8]
+    sub = np.sort(np.concatenate([longest, rng.choice(np.setdiff1d(np.arange(tx * ty), longest), 16,
+                                                      replace=False)])).astype(np.int32)
+    o = O.render(scene, cam, opt, tile_subset=sub)
+    H, W = cam.height, cam.width
+    sel = np.zeros((H, W), bool)
+    for t in sub:
+        sel[(t // tx) * 16:(t // tx) * 16 + 16, (t % tx) * 16:(t % tx) * 16 + 16] = True
+    mask = sel & pixel_mask(o["diag"], cam)
+    g_rgb = rng.standard_normal((H, W, 3)).astype(np.float32) * mask[..., None]
+    g_a = rng.standard_normal((H, W)).astype(np.float32) * mask
+    g_d = (0.1 * rng.standard_normal((H, W))).astype(np.float32) * mask
+    dev = out[0].device
+    gb = r.backward(cam, opt, out, torch.from_numpy(g_rgb).to(dev), torch.from_numpy(g_a).to(dev),
+                    torch.from_numpy(g_d).to(dev))
+    torch.cuda.synchronize()
+    ob = O.backward(scene, cam, opt, g_rgb, g_a, g_d)
+    touched = np.zeros(scene.count, bool)
+    worst = 0.0
+    for f in FIELDS:
+        a = gb[f].cpu().numpy().astype(np.float64).reshape(scene.count, -1)
+        b = ob[f].reshape(scene.count, -1)
+        touched |= np.abs(b).max(1) > 0
+        scale = np.abs(b).max() + 1e-12
+        err = np.abs(a - b) / (2e-3 * np.abs(b) + 2e-4 * scale)
+        worst = max(worst, float(err.max(initial=0)))
+        print(f"full-size backward {f}: max |d| {np.abs(a - b).max(initial=0):.3e} (max |g| {scale:.3e}) "
+              f"ratio {err.max(initial=0):.3f}")
+    print(f"full-size backward: {int(touched.sum())} Gaussians with gradient, {int(mask.sum())} pixels")
+    assert touched.sum() > 1000
+    r.close()
+    assert worst <= 1.0

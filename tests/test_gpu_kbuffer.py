@@ -122,13 +122,26 @@ def test_full_size_sampled_tiles_kbuffer():
         mask[y0:y0 + 16, x0:x0 + 16] = True
     inband = mask.sum()
     _alpha_on_tau_band(g, o, cam, mask)
-    mask &= pixel_mask(o["diag"], cam) & (o["diag"]["min_tau_gap"] > TAU_BAND)
+    d = o["diag"]
+    base = mask & pixel_mask(d, cam)
+    strict = base & (d["min_tau_gap"] > TAU_BAND)
     # the 8 longest lists are the dense object cluster (~10^5 entries, hundreds of
-    # hits per ray): many pixels hold two hits within 2e-6 in tau
-    print(f"full-size kbuf: strict pixels {mask.sum()} of {inband}")
-    assert mask.sum() > 0.6 * inband
-    e_rgb = np.abs(g["rgb"] - o["rgb"]).max(-1)[mask].max()
-    e_a = np.abs(g["alpha"] - o["alpha"])[mask].max()
+    # hits per ray): many pixels hold two hits within 2e-6 in tau.  With exactly
+    # one such pair the oracle also renders the other order (alt_*, the pair's
+    # tau_max exchanged): those pixels must match one of the two renders
+    alt = base & (d["min_tau_gap"] <= TAU_BAND) & (d["alt_valid"] == 1)
+    bg = np.asarray(opt.background, np.float64)
+    alt_rgb = d["alt_rgb"] + (1.0 - d["alt_alpha"])[..., None] * bg
+    e_p = np.maximum(np.abs(g["rgb"] - o["rgb"]).max(-1), np.abs(g["alpha"] - o["alpha"]))
+    e_q = np.maximum(np.abs(g["rgb"] - alt_rgb).max(-1), np.abs(g["alpha"] - d["alt_alpha"]))
+    e_alt = np.minimum(e_p, e_q)[alt]
+    covered = strict.sum() + alt.sum()
+    print(f"full-size kbuf: strict {strict.sum()} + one-tie (either order) {alt.sum()} = {covered} of {inband}; "
+          f"either-order max err {e_alt.max() if e_alt.size else 0.0:.2e}")
+    assert covered >= 0.85 * inband
+    assert e_alt.size == 0 or e_alt.max() <= TOL_RGB
+    e_rgb = np.abs(g["rgb"] - o["rgb"]).max(-1)[strict].max()
+    e_a = np.abs(g["alpha"] - o["alpha"])[strict].max()
     print(f"full-size sampled (k=16): rgb {e_rgb:.2e} alpha {e_a:.2e}")
     assert e_rgb <= TOL_RGB and e_a <= TOL_RGB
 
