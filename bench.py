@@ -466,8 +466,9 @@ def run_ours(args):
     dom = max(rl, key=lambda k: rl[k]["ms"])
     d = rl[dom]
     traffic, traffic_src = load_traffic(dom)
-    # epoch advance, K1 + wide, 4 depth passes, K2 (count, scan, emit, big), tile passes, ranges init, plan (3) + blend
-    launches_per_render = 1 + 2 + 4 + 4 + (2 if n_tiles > 256 else 1) + 1 + 4
+    # frame init (epochs + empty ranges), K1 + wide, 4 depth passes, K2 (count, scan, emit, big), tile
+    # passes, plan (count, scan, fill), blend
+    launches_per_render = 1 + 2 + 4 + 4 + (2 if n_tiles > 256 else 1) + 3 + 1
     total_views = world * args.steps
     fps = total_views / (ms_max * 1e-3)
     line = {

@@ -517,7 +517,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   uint32_t *cnt = ctx->counters;
   CUDA_TRY(ctx, cudaMemsetAsync(cnt, 0, CNT_WORDS * sizeof(uint32_t), st));
   // look-back epochs of this render (device-side, so a captured render replays correctly)
-  launch_epoch_advance(cnt, ctx->bstatus, ctx->cap_items * GUT_TILE_PX, st);
+  launch_frame_init(cnt, ctx->bstatus, ctx->cap_items * GUT_TILE_PX, ctx->ranges, dc.n_tiles, st);
   // K1: UT projection
   launch_project(dc, scene->d, ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->payload, cnt, ctx->deferred,
                  ctx->k1_list, st);
@@ -557,7 +557,6 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   const uint32_t nk = (uint32_t)n_keys_host;
   const uint32_t *fk, *fv;
   // (K4 ranges fused into the final tile pass)
-  launch_ranges_init(ctx->ranges, dc.n_tiles, st);
   const bool two = dc.n_tiles > 256;
   launch_sort_pass(ctx->ka, ctx->va, ctx->kb, ctx->vb, kdev, nk, 0, ht, ctx->st_tile, cnt + CNT_TICKETS + 5,
                    cnt + CNT_EPOCH, 4u, false, st, two ? nullptr : ctx->ranges);

@@ -179,16 +179,6 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
   }
 }
 
-// empty ranges (start UINT_MAX, end 0) before the final tile pass fills them
-__global__ void ranges_init_kernel(uint2 *__restrict__ ranges, int n_tiles) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < n_tiles) ranges[t] = make_uint2(0xFFFFFFFFu, 0u);
-}
-
-void launch_ranges_init(uint2 *ranges, int n_tiles, cudaStream_t st) {
-  ranges_init_kernel<<<(n_tiles + 255) / 256, 256, 0, st>>>(ranges, n_tiles);
-}
-
 void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                       uint32_t *vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
                       const uint32_t *hist, unsigned long long *status, uint32_t *ticket,
@@ -205,9 +195,15 @@ void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t
                                                                 epoch_off, ranges);
 }
 
-// One block: base += GUT_EPOCHS_PER_RENDER; on a wrap of the blend's 22-bit
-// epoch field the blend status words are cleared (every 2^19 renders).
-__global__ void epoch_advance_kernel(uint32_t *counters, unsigned long long *bstatus, size_t n) {
+// Start of a render (one launch): block 0 advances the device epoch base by
+// GUT_EPOCHS_PER_RENDER (clearing the blend status words when the blend's
+// 22-bit epoch field wraps, every 2^19 renders), every thread empties one
+// tile range (start UINT_MAX, end 0) for the final tile pass to fill (K4).
+__global__ void frame_init_kernel(uint32_t *counters, unsigned long long *bstatus, size_t n, uint2 *ranges,
+                                  int n_tiles) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n_tiles) ranges[t] = make_uint2(0xFFFFFFFFu, 0u);
+  if (blockIdx.x != 0) return;
   __shared__ uint32_t s_wrap;
   if (threadIdx.x == 0) {
     const uint32_t old = counters[CNT_EPOCH], nb = old + GUT_EPOCHS_PER_RENDER;
@@ -219,8 +215,10 @@ __global__ void epoch_advance_kernel(uint32_t *counters, unsigned long long *bst
     for (size_t j = threadIdx.x; j < n; j += blockDim.x) bstatus[j] = 0ull;
 }
 
-void launch_epoch_advance(uint32_t *counters, unsigned long long *bstatus, size_t n_bstatus, cudaStream_t st) {
-  epoch_advance_kernel<<<1, 1024, 0, st>>>(counters, bstatus, n_bstatus);
+void launch_frame_init(uint32_t *counters, unsigned long long *bstatus, size_t n_bstatus, uint2 *ranges,
+                       int n_tiles, cudaStream_t st) {
+  const unsigned blocks = (unsigned)max(1, (n_tiles + 255) / 256);
+  frame_init_kernel<<<blocks, 256, 0, st>>>(counters, bstatus, n_bstatus, ranges, n_tiles);
 }
 
 }  // namespace gut

@@ -47,7 +47,7 @@ enum : int {
   // and cleared only by the host at a synchronising call (gut_check & co.)
   CNT_STICKY_OVERFLOW = CNT_WORDS,
   // look-back epoch base of the current render, advanced on the device at the
-  // start of every render (epoch_advance): a render is replayable as a CUDA graph
+  // start of every render (frame_init_kernel): a render is replayable as a CUDA graph
   CNT_EPOCH = CNT_WORDS + 1,
   CNT_ALLOC = CNT_WORDS + 4
 };
@@ -72,12 +72,13 @@ void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t
 // Epochs per render: sort passes use base + 0..6 (depth 0-3, tile 4 and 6), the blend base + GUT_EPOCH_BLEND.
 #define GUT_EPOCHS_PER_RENDER 8u
 #define GUT_EPOCH_BLEND 7u
-// Advances the device epoch base by GUT_EPOCHS_PER_RENDER (one thread block);
-// when the blend's 22-bit epoch field wraps it clears the blend status words
-// (n_bstatus), so a stale word can never alias the current render.
-void launch_epoch_advance(uint32_t *counters, unsigned long long *bstatus, size_t n_bstatus, cudaStream_t st);
-// K4 fused into the final tile pass (ranges != nullptr there): ranges start empty
-void launch_ranges_init(uint2 *ranges, int n_tiles, cudaStream_t st);
+// Start of a render: advances the device epoch base by GUT_EPOCHS_PER_RENDER
+// (when the blend's 22-bit epoch field wraps it clears the blend status words,
+// n_bstatus, so a stale word can never alias the current render) and empties
+// the tile ranges that the final tile pass fills (K4).
+void launch_frame_init(uint32_t *counters, unsigned long long *bstatus, size_t n_bstatus, uint2 *ranges,
+                       int n_tiles, cudaStream_t st);
+// (K4 is fused into the final tile pass: ranges != nullptr there; launch_frame_init empties them)
 
 // K2: per-partition key totals, their scan, then the emission (part_off:
 // one uint32 per GUT_EMIT_PART Gaussians of the upper bound n_upper)
