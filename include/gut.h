@@ -268,7 +268,7 @@ gut_status gut_projection_quality(gut_context *ctx, const gut_scene *scene, cons
                                   gut_stream s);
 
 /* Renders n_views views (outs[i] for cams[i]).  With stats == NULL the views
- * are pipelined: up to gut_context_set_frames_in_flight() frames (default 3)
+ * are pipelined: up to gut_context_set_frames_in_flight() frames (default 4)
  * are in flight at once, view i on lane i mod F -- lane 0 is ctx on stream s,
  * lanes 1..F-1 are child contexts (own workspaces, reserved like ctx, created
  * on first use and owned by ctx) on their own streams, forked from and joined

@@ -70,7 +70,7 @@ struct gut_context {
   // gut_render_batch: frames in flight -- lane 0 is this context on the
   // caller's stream, lanes 1.. are child contexts (own workspaces) on their
   // own streams, joined back to the caller's stream with events
-  int frames_in_flight = 3;
+  int frames_in_flight = 4;
   int64_t res_keys = 0, res_n = 0;
   int32_t res_w = 0, res_h = 0;
   std::vector<gut_context *> lanes;
