@@ -525,10 +525,42 @@ __device__ __forceinline__ void kb_insert(KBuf<KB> &kb, LanePx<NP> &L, int k, fl
 // terminated.  Termination rule (reading R21): stop before an entry would take
 // T below T_min.  The caller sets L.a/b/beta/snorm, L.T (start), L.done
 // (= inactive) and L.term = false; the colour sums start at 0 here.
+// Per-warp constants of the current unit (the tile anchor D, dO = O - c(0) in
+// fp64, D / T1 / T2 in fp32, the pixel box) live in shared memory rather than
+// registers: the staging reloads them once per 32-entry chunk (broadcast),
+// which frees ~25 registers in the evaluation loops.
+#define GUT_WC_F4 7  // float4 per warp
+#ifndef GUT_K5_HALF_SKIP
+#define GUT_K5_HALF_SKIP 1  // per-pixel-row-half warp-uniform skip of the evaluation (tuning switch)
+#endif
+__device__ __forceinline__ float4 *warp_consts(int nf) {
+  extern __shared__ float4 s_dyn[];
+  return s_dyn + (GUT_BLEND_CTA / 32) * 2 * 32 * GUT_PAYLOAD_F4 + (GUT_BLEND_CTA / 32) * 32 * nf +
+         (threadIdx.x >> 5) * GUT_WC_F4;
+}
+__device__ __forceinline__ void store_warp_consts(float4 *wc, const d3 &D, const d3 &dO, const f3 &T1f, const f3 &T2f,
+                                                  float ac, float bc, float ra, float rb, float tc, float rt) {
+  if ((threadIdx.x & 31) == 0) {
+    double2 *wd = reinterpret_cast<double2 *>(wc);
+    wd[0] = make_double2(D.x, D.y);
+    wd[1] = make_double2(D.z, dO.x);
+    wd[2] = make_double2(dO.y, dO.z);
+    wc[3] = make_float4((float)D.x, (float)D.y, (float)D.z, T1f.x);
+    wc[4] = make_float4(T1f.y, T1f.z, T2f.x, T2f.y);
+    wc[5] = make_float4(T2f.z, ac, bc, ra);
+    wc[6] = make_float4(rb, tc, rt, 0.f);
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ double2 lds_d2(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 template <int MODE, int NP, int KB = 0>
 __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, uint32_t s0, uint32_t s1,
-                                          const d3 &D, const d3 &O, const f3 &T1f, const f3 &T2f, float ac, float bc,
-                                          float ra, float rb, float tc, float rt, LanePx<NP> &L, uint32_t &n_eval, uint32_t &n_contrib,
+                                          LanePx<NP> &L, uint32_t &n_eval, uint32_t &n_contrib,
                                           uint32_t &processed, const unsigned long long *poll_stat, int poll_s,
                                           Checkpoints<NP> *ck, uint32_t ck_step, const uint32_t *act,
                                           KBuf<KB> *kb = nullptr) {
@@ -550,9 +582,8 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   const f3 dcw = mk((float)c.dc[0], (float)c.dc[1], (float)c.dc[2]);
   // raw payload of the warp's current / next chunk (cp.async double buffer)
   float4 *__restrict__ raw = s_dyn + (threadIdx.x >> 5) * 2 * 32 * PF;
-  // the item's anchor: dO = O - c(0) (payload w0 = c(0) - mu), D in fp32
-  const d3 dO = O - mkd(c.c0[0], c.c0[1], c.c0[2]);
-  const f3 Df = tof(D);
+  // the unit's anchor and box (store_warp_consts): dO = O - c(0) (payload w0 = c(0) - mu)
+  const uint32_t wc_s = (uint32_t)__cvta_generic_to_shared(warp_consts(NF));
   bool all_done = true;
 #pragma unroll
   for (int k = 0; k < NP; ++k) {
@@ -661,6 +692,11 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
       // only w x D is formed in fp64 (the small vector), the rest in fp32.
       const float4 *src = raw + (buf * 32 + lane) * PF;
       const double2 wxy = *reinterpret_cast<const double2 *>(src);
+      const double2 q0 = lds_d2(wc_s), q1 = lds_d2(wc_s + 16), q2 = lds_d2(wc_s + 32);
+      const float4 q3 = lds128(wc_s + 48), q4 = lds128(wc_s + 64), q5 = lds128(wc_s + 80), q6 = lds128(wc_s + 96);
+      const d3 D = mkd(q0.x, q0.y, q1.x), dO = mkd(q1.y, q2.x, q2.y);
+      const f3 Df = mk(q3.x, q3.y, q3.z), T1f = mk(q3.w, q4.x, q4.y), T2f = mk(q4.z, q4.w, q5.x);
+      const float ac = q5.y, bc = q5.z, ra = q5.w, rb = q6.x, tc = q6.y, rt = q6.z;
       const float4 p1 = src[1], p2 = src[2], p3 = src[3], p4 = src[4];
       const d3 w = mkd(wxy.x, wxy.y, __hiloint2double(__float_as_int(p1.y), __float_as_int(p1.x))) + dO;
       const f3 x = tof(cross(w, D));
@@ -868,6 +904,10 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
         const float4 f2 = lds128(ta + 32), f3v = lds128(ta + 48), f4 = lds128(ta + 64), cc = lds128(ta + 80);
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
+#if GUT_K5_HALF_SKIP
+          // the entry covers only one of the warp's two 8x4 halves: skip the other
+          if (NP > 1 && !__any_sync(FULL, hit[k])) continue;
+#endif
           const float Dd = fmaf(da[k], fmaf(f2.w, da[k], fmaf(f3v.x, db[k], f2.y)),
                                 fmaf(db[k], fmaf(f3v.y, db[k], f2.z), f2.x));
           const float rD = rcp_approx(Dd);
@@ -1068,7 +1108,9 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     uint32_t n_eval = 0, n_contrib = 0, processed = 0;
     Checkpoints<NP> ck;
     const uint32_t ck_step = max(32u, ((uint32_t)B.seg / GUT_CK) & ~31u);
-    warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, tc, rt, L, n_eval, n_contrib, processed,
+    store_warp_consts(warp_consts(WarpTbl<MODE>::NF), D, O - mkd(c.c0[0], c.c0[1], c.c0[2]), T1f, T2f, ac, bc, ra,
+                      rb, tc, rt);
+    warp_pass<MODE, NP>(c, B, s0, s1, L, n_eval, n_contrib, processed,
                         s > 0 ? stat : nullptr, s, s > 0 ? &ck : nullptr, ck_step, nullptr);
     unsigned long long t_spec = 0, t_lb = 0;  // (trace only: end of the speculative pass / of the look-back)
     if (B.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_spec));
@@ -1141,7 +1183,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
         }
       }
       uint32_t e2 = 0, c2 = 0, p2 = 0;
-      warp_pass<MODE, NP>(c, B, s0, s1, D, O, T1f, T2f, ac, bc, ra, rb, tc, rt, R, e2, c2, p2, nullptr, 0, nullptr, 0,
+      warp_pass<MODE, NP>(c, B, s0, s1, R, e2, c2, p2, nullptr, 0, nullptr, 0,
                           act);
 #pragma unroll
       for (int k = 0; k < NP; ++k)
@@ -1293,7 +1335,8 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
 template <int MODE>
 static void blend_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
   constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_CTA / 32) * 2 * 32 * GUT_PAYLOAD_F4 +
-                                            (GUT_BLEND_CTA / 32) * 32 * WarpTbl<MODE>::NF);
+                                            (GUT_BLEND_CTA / 32) * 32 * WarpTbl<MODE>::NF +
+                                            (GUT_BLEND_CTA / 32) * GUT_WC_F4);
   // per device, thread-safe (a process may drive several devices): the
   // dynamic shared-memory attribute is a per-device setting
   static std::once_flag once[GUT_MAX_DEVICES];
@@ -1402,7 +1445,9 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kbuf_kern
 #pragma unroll
     for (int i = 0; i < KB; ++i) { kb.t[i] = -INFINITY; kb.a[i] = 0.f; kb.g[i] = 0u; }
     uint32_t n_eval = 0, n_contrib = 0, processed = 0;
-    warp_pass<MODE, 1, KB>(c, B, start, end, D, O, T1f, T2f, ac, bc, ra, rb, tc, rt, L, n_eval, n_contrib, processed,
+    store_warp_consts(warp_consts(WarpTbl<MODE>::NF), D, O - mkd(c.c0[0], c.c0[1], c.c0[2]), T1f, T2f, ac, bc, ra,
+                      rb, tc, rt);
+    warp_pass<MODE, 1, KB>(c, B, start, end, L, n_eval, n_contrib, processed,
                            nullptr, 0, nullptr, 0, nullptr, &kb);
     // end of the list: the pending hits near to far (colours gathered up front)
     if (!L.done[0]) {
@@ -1455,7 +1500,8 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kbuf_kern
 template <int MODE, int KB>
 static void blend_kbuf_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
   constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_CTA / 32) * 2 * 32 * GUT_PAYLOAD_F4 +
-                                            (GUT_BLEND_CTA / 32) * 32 * WarpTbl<MODE>::NF);
+                                            (GUT_BLEND_CTA / 32) * 32 * WarpTbl<MODE>::NF +
+                                            (GUT_BLEND_CTA / 32) * GUT_WC_F4);
   // per device, thread-safe (a process may drive several devices): the
   // dynamic shared-memory attribute is a per-device setting
   static std::once_flag once[GUT_MAX_DEVICES];
