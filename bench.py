@@ -284,7 +284,13 @@ def run_ours(args):
     from paper_2412_12507_b200 import gut
     from paper_2412_12507_b200 import parallel as P
 
-    rank, local, world = P.init("nccl")
+    # one process per GPU over NCCL; if there are more ranks than GPUs (a
+    # functional check of the multi-rank path on one device, never a scaling
+    # number) ranks share devices and the collectives fall back to gloo
+    ndev = torch.cuda.device_count()
+    shared = int(os.environ.get("WORLD_SIZE", 1)) > ndev
+    rank, local, world = P.init("gloo" if shared else "nccl")
+    local = local % ndev
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     torch.cuda.set_device(local)
@@ -430,7 +436,7 @@ def run_ours(args):
     P.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
-    ms_max = P.max_over_ranks(ms, device=dev)
+    ms_max = P.max_over_ranks(ms, device=None if shared else dev)
     gut.gut_check(ctx, stream)  # no reserved-capacity overflow in the timed region
     # e2e: the same batch call with host (pinned) outputs: every view's RGB,
     # alpha and depth are copied device->host inside the timed region, on the
@@ -447,12 +453,12 @@ def run_ours(args):
     batch([P.view_of(e2e_first + nb + s, rank, world, nv) for s in range(e2e_steps)], houts)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = P.max_over_ranks(e0.elapsed_time(e1), device=dev)
+    e2e_ms = P.max_over_ranks(e0.elapsed_time(e1), device=None if shared else dev)
     # per-view statistics of the timed views (deterministic renders) gathered to rank 0
     rows = [[v, per_view[v]["n_visible"], per_view[v]["n_keys"], per_view[v]["pairs_evaluated"],
              per_view[v]["pairs_contributing"], per_view[v]["max_tile_len"], per_view[v]["checksum"]]
             for v in timed_views]
-    all_rows = P.gather_stats(rows, device=dev)
+    all_rows = P.gather_stats(rows, device=None if shared else dev)
     overflow = any(per_view[v]["n_keys"] > int(kmax * 1.02) + 65536 for v in timed_views)
     gut.gut_scene_destroy(ctx, scene)
     gut.gut_context_destroy(ctx)
@@ -477,7 +483,8 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "views_per_step": world, "parallelism": f"views sharded over {world} GPU(s), "
-                   "scene replicated", "l2": "inputs larger than L2 (720 MB resident scene; 41 MB output/view)",
+                   "scene replicated" + (f" -- {world} ranks SHARE {torch.cuda.device_count()} GPU(s) (gloo): "
+                                         "functional check only, not a scaling measurement" if shared else ""), "l2": "inputs larger than L2 (720 MB resident scene; 41 MB output/view)",
                    "capacity_mode": True, "reserved_keys": int(kmax * 1.02) + 65536,
                    "frames_in_flight": args.inflight,
                    "variant": "Ours" if args.kbuffer == 0 else f"Ours (sorted), k-buffer k={args.kbuffer}",

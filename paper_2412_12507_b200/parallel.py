@@ -49,8 +49,15 @@ def broadcast_scene(tensors: Dict[str, torch.Tensor], src: int = 0) -> Dict[str,
     NVLink on GPUs, gloo on CPU).  Non-source ranks pass empty tensors of the
     right shape/dtype."""
     if dist.is_initialized() and dist.get_world_size() > 1:
+        gloo = dist.get_backend() == "gloo"
         for k in sorted(tensors):
-            dist.broadcast(tensors[k], src=src)
+            t = tensors[k]
+            if gloo and t.is_cuda:  # (gloo: through host memory)
+                h = t.cpu()
+                dist.broadcast(h, src=src)
+                t.copy_(h)
+            else:
+                dist.broadcast(t, src=src)
     return tensors
 
 
