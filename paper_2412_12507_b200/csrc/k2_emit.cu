@@ -107,7 +107,9 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
       const uint32_t cw = m4 ? 4u : 3u;
       for (uint32_t m = code[j] & (m4 ? 0xFFFFu : 0x1FFu); m; m &= m - 1) {
         const uint32_t b = (uint32_t)(__ffs(m) - 1);
-        const uint32_t tile = (y0 + b / cw) * (uint32_t)tiles_x + x0 + b % cw;
+        // row = b / cw without an integer division (cw = 3: b < 9, (11 b) >> 5 = b / 3)
+        const uint32_t row = m4 ? b >> 2 : (b * 11u) >> 5;
+        const uint32_t tile = (y0 + row) * (uint32_t)tiles_x + x0 + (b - row * cw);
         emit_key(pos++, tile, g[j], cap_k, out_tile, out_gid, s_hist, counters);
       }
     } else {
