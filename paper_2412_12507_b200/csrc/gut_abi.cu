@@ -41,7 +41,11 @@ struct gut_context {
   uint4 *trace = nullptr;  // K5 per-work-item trace (env GUT_BLEND_TRACE=1, diagnostics only)
   size_t cap_trace = 0, last_items = 0;
   bool trace_on = false;
-  float *img = nullptr;
+  float *img = nullptr;     // host-output staging (RGB, alpha, depth); two slots for the batch's copy stream
+  float *img_slot[2] = {nullptr, nullptr};
+  int img_next = 0;
+  cudaStream_t copy_stream = nullptr;                  // gut_render_batch: device->host copies off the render stream
+  cudaEvent_t ev_rendered[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr}, ev_copy_tail = nullptr;
   unsigned long long *st_depth = nullptr, *st_emit = nullptr, *st_tile = nullptr;
   uint32_t *counters = nullptr, *h_counters = nullptr;
   // K5: ray LUT (cached per intrinsics for global shutter), blend work plan
@@ -178,7 +182,10 @@ static gut_status ensure_items(gut_context *ctx, size_t items) {
 static gut_status ensure_pix(gut_context *ctx, size_t p) {
   if (p <= ctx->cap_pix) return GUT_OK;
   size_t dummy = 0;
-  CUDA_TRY(ctx, regrow(ctx->img, dummy, 5 * p));
+  CUDA_TRY(ctx, cudaDeviceSynchronize());  // (a copy may still read the old slots)
+  CUDA_TRY(ctx, regrow(ctx->img, dummy, 10 * p));
+  ctx->img_slot[0] = ctx->img;
+  ctx->img_slot[1] = ctx->img + 5 * p;
   ctx->cap_pix = p;
   return GUT_OK;
 }
@@ -347,6 +354,12 @@ void gut_context_destroy(gut_context *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   for (gut_context *l : ctx->lanes) gut_context_destroy(l);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    for (int i = 0; i < 2; ++i) { cudaEventDestroy(ctx->ev_rendered[i]); cudaEventDestroy(ctx->ev_copied[i]); }
+    cudaEventDestroy(ctx->ev_copy_tail);
+  }
   for (cudaStream_t st : ctx->lane_streams) cudaStreamDestroy(st);
   for (cudaEvent_t e : ctx->lane_events) cudaEventDestroy(e);
   if (ctx->fork_event) cudaEventDestroy(ctx->fork_event);
@@ -486,8 +499,11 @@ static gut_status take_sticky(gut_context *ctx, cudaStream_t st, bool &overflow)
   return GUT_OK;
 }
 
+// copy_st (gut_render_batch, host outputs): the device->host copies run on the
+// context's copy stream from one of two staging slots, so the next render on
+// st does not wait for them (it only waits until the slot it reuses is copied)
 static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut_camera *cam, const gut_options *opt,
-                             const gut_outputs *out, cudaStream_t st, gut_stats *stats) {
+                             const gut_outputs *out, cudaStream_t st, gut_stats *stats, bool use_copy_stream = false) {
   if (!ctx) return fail(nullptr, GUT_E_INVALID_ARGUMENT, "ctx: NULL");
   if (!scene) return fail(ctx, GUT_E_INVALID_ARGUMENT, "scene: NULL");
   if (!out || !out->rgb || !out->alpha) return fail(ctx, GUT_E_INVALID_ARGUMENT, "outputs.rgb/alpha: NULL");
@@ -569,10 +585,29 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   if (timing) cudaEventRecord(ev[4], st);
   if (timing) cudaEventRecord(ev[5], st);  // K4: fused (stage time ~0)
   float *rgb = out->rgb, *alpha = out->alpha, *depth = out->depth;
+  int slot = 0;
   if (!out->on_device) {
-    rgb = ctx->img;
-    alpha = ctx->img + 3 * npix;
-    depth = out->depth ? ctx->img + 4 * npix : nullptr;
+    if (use_copy_stream) {
+      slot = ctx->img_next;
+      ctx->img_next ^= 1;
+      if (!ctx->copy_stream) {
+        CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+          CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_rendered[i], cudaEventDisableTiming));
+          CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_copied[i], cudaEventDisableTiming));
+          CUDA_TRY(ctx, cudaEventRecord(ctx->ev_copied[i], ctx->copy_stream));
+        }
+        CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_copy_tail, cudaEventDisableTiming));
+      }
+      // the blend below writes the slot: wait until its previous copy has read it
+      CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_copied[slot], 0));
+    } else if (ctx->copy_stream) {  // (slot 0 may still be read by an earlier batch's copy)
+      CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_copied[0], 0));
+    }
+    float *img = ctx->img_slot[slot];
+    rgb = img;
+    alpha = img + 3 * npix;
+    depth = out->depth ? img + 4 * npix : nullptr;
   }
   // a5: pixel rays relative to per-tile anchors — a function of the intrinsics
   // only for global shutter (built once per intrinsics), per view for RS
@@ -627,10 +662,17 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
     if (e != cudaSuccess) return fail(ctx, GUT_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   }
   if (!out->on_device) {
-    CUDA_TRY(ctx, cudaMemcpyAsync(out->rgb, rgb, 3 * npix * sizeof(float), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(ctx, cudaMemcpyAsync(out->alpha, alpha, npix * sizeof(float), cudaMemcpyDeviceToHost, st));
+    cudaStream_t cs = st;
+    if (use_copy_stream) {
+      CUDA_TRY(ctx, cudaEventRecord(ctx->ev_rendered[slot], st));
+      CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_rendered[slot], 0));
+      cs = ctx->copy_stream;
+    }
+    CUDA_TRY(ctx, cudaMemcpyAsync(out->rgb, rgb, 3 * npix * sizeof(float), cudaMemcpyDeviceToHost, cs));
+    CUDA_TRY(ctx, cudaMemcpyAsync(out->alpha, alpha, npix * sizeof(float), cudaMemcpyDeviceToHost, cs));
     if (out->depth)
-      CUDA_TRY(ctx, cudaMemcpyAsync(out->depth, depth, npix * sizeof(float), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(ctx, cudaMemcpyAsync(out->depth, depth, npix * sizeof(float), cudaMemcpyDeviceToHost, cs));
+    if (use_copy_stream) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_copied[slot], cs));
   }
   ctx->last_n = N;
   ctx->last_tiles = dc.n_tiles;
@@ -780,13 +822,21 @@ gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_
   for (int32_t v = 0; v < n_views && r == GUT_OK; ++v) {
     const int l = v % L;
     gut_context *c = l == 0 ? ctx : ctx->lanes[l - 1];
-    r = render_one(c, scene, &cams[v], opt, &outs[v], l == 0 ? st : ctx->lane_streams[l - 1], nullptr);
+    r = render_one(c, scene, &cams[v], opt, &outs[v], l == 0 ? st : ctx->lane_streams[l - 1], nullptr, true);
     if (r != GUT_OK && c != ctx) fail(ctx, r, c->err);
   }
-  // join: the caller's stream waits for every lane (also after an error)
+  // join: the caller's stream waits for every lane and every lane's host
+  // copies (also after an error)
   for (int i = 0; i < L - 1; ++i) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->lane_events[i], ctx->lane_streams[i]));
     CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->lane_events[i], 0));
+  }
+  for (int i = 0; i < L; ++i) {
+    gut_context *c = i == 0 ? ctx : ctx->lanes[i - 1];
+    if (c->copy_stream) {
+      CUDA_TRY(ctx, cudaEventRecord(c->ev_copy_tail, c->copy_stream));
+      CUDA_TRY(ctx, cudaStreamWaitEvent(st, c->ev_copy_tail, 0));
+    }
   }
   return r;
 }

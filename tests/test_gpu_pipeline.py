@@ -128,3 +128,37 @@ def test_view_sharding_is_bitwise_equal_across_world_sizes(setup):
     # per-view 8-byte checksums (what bench.py gathers across ranks) agree too
     ck = {v: P.image_checksum(img) for v, img in world2.items()}
     assert all(ck[v] == P.image_checksum(world1[v]) for v in ck)
+
+
+@pytest.mark.parametrize("fif", [1, 4])
+def test_render_batch_host_outputs(setup, fif):
+    """Host (pinned) outputs through the batch: the copies run on each lane's
+    copy stream from two alternating staging slots; every view's host image
+    equals the device render, also when more views than slots are in flight."""
+    import torch
+    from paper_2412_12507_b200 import gut
+    scene, cams = setup
+    ref = _one_by_one(scene, cams)
+    r = gut.Renderer(scene, reserve_keys=2_000_000, max_wh=(cams[0].width, cams[0].height))
+    gut.gut_context_set_frames_in_flight(r.ctx, fif)
+    hb, outs = [], []
+    for c in cams:
+        b = (torch.full((c.height, c.width, 3), -1.0, pin_memory=True), torch.full((c.height, c.width), -1.0, pin_memory=True),
+             torch.full((c.height, c.width), -1.0, pin_memory=True))
+        hb.append(b)
+        outs.append(gut.gut_outputs(b[0].data_ptr(), b[1].data_ptr(), b[2].data_ptr(), 0, 0))
+    s = torch.cuda.Stream()
+    for _ in range(2):
+        gut.gut_render_batch(r.ctx, r.scene, [gut.make_camera(c) for c in cams], gut.make_options(), outs, stream=s)
+    s.synchronize()  # the call's copies are complete once the stream reaches this point
+    for a, b in zip(ref, hb):
+        for x, y in zip(a, b):
+            assert torch.equal(x.cpu(), y)
+    # an ordinary host-output render after the batch on another stream
+    b0 = hb[0]
+    for t in b0:
+        t.fill_(-1.0)
+    gut.gut_render(r.ctx, r.scene, gut.make_camera(cams[0]), gut.make_options(), outs[0])
+    torch.cuda.synchronize()
+    assert torch.equal(ref[0][0].cpu(), b0[0])
+    r.close()
