@@ -408,6 +408,8 @@ template <int NP> struct Checkpoints {
   float4 C[GUT_CK][NP];
   float T[GUT_CK][NP];
   int n[NP];
+  float4 keepC[NP];  // (between the two passes: the non-re-running pixels' results)
+  bool keepTerm[NP];
 };
 
 // Per-warp table of staged list entries (32 per chunk).  MODE 0/1: the
@@ -1110,64 +1112,72 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     const uint32_t ck_step = max(32u, ((uint32_t)B.seg / GUT_CK) & ~31u);
     store_warp_consts(warp_consts(WarpTbl<MODE>::NF), D, O - mkd(c.c0[0], c.c0[1], c.c0[2]), T1f, T2f, ac, bc, ra,
                       rb, tc, rt);
-    warp_pass<MODE, NP>(c, B, s0, s1, L, n_eval, n_contrib, processed,
-                        s > 0 ? stat : nullptr, s, s > 0 ? &ck : nullptr, ck_step, nullptr);
     unsigned long long t_spec = 0, t_lb = 0;  // (trace only: end of the speculative pass / of the look-back)
-    if (B.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_spec));
     float T_pre[NP], T_end[NP];
-    bool alive_in[NP], redo[NP], any_redo = false;
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const unsigned long long Ls = (L.term[k] || (valid[k] && !run[k])) ? GUT_L_DEAD : l_of(L.T[k]);
-      T_pre[k] = 1.f;
-      alive_in[k] = valid[k];
-      if (S > 1 && valid[k]) {
-        unsigned long long *st = stat + 64 * k;
-        unsigned long long Lpre = 0;
-        if (s == 0) {
-          st_relaxed(st, st_word(2, epoch, Ls));
-        } else {
-          st_relaxed(st, st_word(1, epoch, Ls));
-          // decoupled look-back over this pixel's earlier segments (integer sums)
-          for (int j = s - 1;; --j) {
-            const unsigned long long wv = ld_relaxed(st - (size_t)(s - j) * NT);
-            const uint32_t flag = (uint32_t)(wv >> 62);
-            if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (epoch & 0x3FFFFFu)) {
-              __nanosleep(256);  // predecessor still running: yield issue slots to the SM's other warps
-              ++j;
-              continue;
-            }
-            Lpre += wv & ((1ull << 40) - 1);
-            if (Lpre >= GUT_L_DEAD) { Lpre = GUT_L_DEAD; break; }
-            if (flag == 2) break;
-          }
-          const unsigned long long Lin = Lpre + Ls >= GUT_L_DEAD ? GUT_L_DEAD : Lpre + Ls;
-          st_relaxed(st, st_word(2, epoch, Lin));
-        }
-        T_pre[k] = t_of(Lpre);
-        alive_in[k] = T_pre[k] >= c.t_min;
-      }
-      // ---- exact result: scale the speculative sums, or redo the segment from T_pre
-      redo[k] = alive_in[k] && s > 0 && (L.term[k] || T_pre[k] * L.T[k] < c.t_min);
-      any_redo = any_redo || redo[k];
-      T_end[k] = L.T[k];
-      if (s > 0 && alive_in[k] && !redo[k]) {
-        L.Cr[k] *= T_pre[k]; L.Cg[k] *= T_pre[k]; L.Cb[k] *= T_pre[k]; L.Dp[k] *= T_pre[k];
-        T_end[k] = T_pre[k] * L.T[k];
-      }
-    }
-    if (B.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_lb));
-    const bool wredo = __any_sync(FULL, any_redo);
-    if (wredo) {
-      // each re-running pixel resumes at the latest checkpoint its exact
-      // sequence certainly reached (T_pre T_c >= T_min), or at the segment start
-      LanePx<NP> R;
-      uint32_t act[NP];
+    bool alive_in[NP], redo[NP], any_redo = false, wredo = false;
+    uint32_t act[NP];
+    uint32_t e2 = 0, c2 = 0, p2 = 0;
+    // pass 0: the speculative pass; pass 1 (only if a pixel needs it): the exact
+    // re-run of the pixels that terminate inside this segment.  ONE inlined copy
+    // of warp_pass serves both passes (half the blend kernel's code).
+    for (int pass = 0; pass < 2; ++pass) {
+      warp_pass<MODE, NP>(c, B, s0, s1, L, pass ? e2 : n_eval, pass ? c2 : n_contrib, pass ? p2 : processed,
+                          pass == 0 && s > 0 ? stat : nullptr, s, pass == 0 && s > 0 ? &ck : nullptr, ck_step,
+                          pass ? act : nullptr);
+      if (pass == 1) break;
+      if (B.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_spec));
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
-        R.a[k] = L.a[k]; R.b[k] = L.b[k]; R.beta[k] = L.beta[k]; R.snorm[k] = L.snorm[k];
-        R.done[k] = !redo[k];
-        R.term[k] = false;
+        const unsigned long long Ls = (L.term[k] || (valid[k] && !run[k])) ? GUT_L_DEAD : l_of(L.T[k]);
+        T_pre[k] = 1.f;
+        alive_in[k] = valid[k];
+        if (S > 1 && valid[k]) {
+          unsigned long long *st = stat + 64 * k;
+          unsigned long long Lpre = 0;
+          if (s == 0) {
+            st_relaxed(st, st_word(2, epoch, Ls));
+          } else {
+            st_relaxed(st, st_word(1, epoch, Ls));
+            // decoupled look-back over this pixel's earlier segments (integer sums)
+            for (int j = s - 1;; --j) {
+              const unsigned long long wv = ld_relaxed(st - (size_t)(s - j) * NT);
+              const uint32_t flag = (uint32_t)(wv >> 62);
+              if (flag == 0 || (uint32_t)((wv >> 40) & 0x3FFFFFu) != (epoch & 0x3FFFFFu)) {
+                __nanosleep(256);  // predecessor still running: yield issue slots to the SM's other warps
+                ++j;
+                continue;
+              }
+              Lpre += wv & ((1ull << 40) - 1);
+              if (Lpre >= GUT_L_DEAD) { Lpre = GUT_L_DEAD; break; }
+              if (flag == 2) break;
+            }
+            const unsigned long long Lin = Lpre + Ls >= GUT_L_DEAD ? GUT_L_DEAD : Lpre + Ls;
+            st_relaxed(st, st_word(2, epoch, Lin));
+          }
+          T_pre[k] = t_of(Lpre);
+          alive_in[k] = T_pre[k] >= c.t_min;
+        }
+        // ---- exact result: scale the speculative sums, or redo the segment from T_pre
+        redo[k] = alive_in[k] && s > 0 && (L.term[k] || T_pre[k] * L.T[k] < c.t_min);
+        any_redo = any_redo || redo[k];
+        T_end[k] = L.T[k];
+        if (s > 0 && alive_in[k] && !redo[k]) {
+          L.Cr[k] *= T_pre[k]; L.Cg[k] *= T_pre[k]; L.Cb[k] *= T_pre[k]; L.Dp[k] *= T_pre[k];
+          T_end[k] = T_pre[k] * L.T[k];
+        }
+      }
+      if (B.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_lb));
+      wredo = __any_sync(FULL, any_redo);
+      if (!wredo) break;
+      // each re-running pixel resumes at the latest checkpoint its exact
+      // sequence certainly reached (T_pre T_c >= T_min), or at the segment start;
+      // the other pixels' results wait in the checkpoint record meanwhile
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        ck.keepC[k] = make_float4(L.Cr[k], L.Cg[k], L.Cb[k], L.Dp[k]);
+        ck.keepTerm[k] = L.term[k];
+        L.done[k] = !redo[k];
+        L.term[k] = false;
         int ck_k = -1;
         if (redo[k])
           for (int q = ck.n[k] - 1; q >= 0; --q)
@@ -1175,22 +1185,23 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
         act[k] = ck_k >= 0 ? s0 + (uint32_t)(ck_k + 1) * ck_step : s0;
         if (ck_k >= 0) {
           const float4 cc = ck.C[ck_k][k];
-          R.Cr[k] = T_pre[k] * cc.x; R.Cg[k] = T_pre[k] * cc.y; R.Cb[k] = T_pre[k] * cc.z; R.Dp[k] = T_pre[k] * cc.w;
-          R.T[k] = T_pre[k] * ck.T[ck_k][k];
+          L.Cr[k] = T_pre[k] * cc.x; L.Cg[k] = T_pre[k] * cc.y; L.Cb[k] = T_pre[k] * cc.z; L.Dp[k] = T_pre[k] * cc.w;
+          L.T[k] = T_pre[k] * ck.T[ck_k][k];
         } else {
-          R.Cr[k] = R.Cg[k] = R.Cb[k] = R.Dp[k] = 0.f;
-          R.T[k] = T_pre[k];
+          L.Cr[k] = L.Cg[k] = L.Cb[k] = L.Dp[k] = 0.f;
+          L.T[k] = T_pre[k];
         }
       }
-      uint32_t e2 = 0, c2 = 0, p2 = 0;
-      warp_pass<MODE, NP>(c, B, s0, s1, R, e2, c2, p2, nullptr, 0, nullptr, 0,
-                          act);
+    }
+    if (wredo) {
 #pragma unroll
       for (int k = 0; k < NP; ++k)
         if (redo[k]) {
-          L.Cr[k] = R.Cr[k]; L.Cg[k] = R.Cg[k]; L.Cb[k] = R.Cb[k]; L.Dp[k] = R.Dp[k];
-          T_end[k] = R.T[k];
-          L.term[k] = R.term[k];
+          T_end[k] = L.T[k];
+        } else {
+          const float4 kc = ck.keepC[k];
+          L.Cr[k] = kc.x; L.Cg[k] = kc.y; L.Cb[k] = kc.z; L.Dp[k] = kc.w;
+          L.term[k] = ck.keepTerm[k];
         }
       processed += p2;
     }
