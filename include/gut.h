@@ -241,8 +241,10 @@ typedef struct {
  * context's device; asynchronous on s.  Per-Gaussian sums use fp32 atomics
  * (reproducible to rounding, not bitwise).  Supported: PINHOLE / OPENCV /
  * FISHEYE with any shutter and kernel_degree, kbuffer 0; otherwise
- * GUT_E_UNSUPPORTED.  A camera / options mismatch with the last render:
- * GUT_E_INVALID_ARGUMENT. */
+ * GUT_E_UNSUPPORTED.  It differentiates ctx's LAST render (its sorted lists
+ * and workspace): a camera / options mismatch with that render gives
+ * GUT_E_INVALID_ARGUMENT (after gut_render_batch the last render on ctx itself
+ * is the last view of lane 0, not the batch's last view). */
 gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const gut_camera *cam,
                                const gut_options *opt, const float *rgb, const float *alpha,
                                const float *depth, const float *grad_rgb, const float *grad_alpha,
@@ -284,8 +286,10 @@ gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_
 gut_status gut_context_set_frames_in_flight(gut_context *ctx, int32_t n);
 
 /* Per-stage device times of every render issued with options.timing = 1 since
- * the last reset: CUDA events recorded on the render's stream between the
- * stages.  Synchronises.  ms_sum[7] receives the summed milliseconds per stage
+ * the last reset -- including those gut_render_batch ran on the context's
+ * lanes: CUDA events recorded on the render's stream between the stages (with
+ * frames in flight a lane's stage times include time shared with other
+ * frames).  Synchronises.  ms_sum[7] receives the summed milliseconds per stage
  * (order of gut_stats.ms_stage), *n_renders the number of renders summed;
  * reset != 0 clears the accumulator. */
 gut_status gut_timing_read(gut_context *ctx, double ms_sum[7], int32_t *n_renders, int32_t reset);

@@ -845,19 +845,25 @@ gut_status gut_timing_read(gut_context *ctx, double ms_sum[7], int32_t *n_render
   if (!ctx || !ms_sum) return fail(ctx, GUT_E_INVALID_ARGUMENT, "gut_timing_read: NULL argument");
   cudaSetDevice(ctx->device);
   for (int i = 0; i < 7; ++i) ms_sum[i] = 0;
-  for (size_t r = 0; r < ctx->tnext; ++r) {
-    auto &e = ctx->tsets[r];
-    CUDA_TRY(ctx, cudaEventSynchronize(e[6]));
-    float t;
-    for (int i = 0; i < 6; ++i) {
-      CUDA_TRY(ctx, cudaEventElapsedTime(&t, e[i], e[i + 1]));
-      ms_sum[i] += t;
+  int32_t n = 0;
+  // this context's renders and its batch lanes' (gut_render_batch)
+  for (size_t li = 0; li <= ctx->lanes.size(); ++li) {
+    gut_context *c = li == 0 ? ctx : ctx->lanes[li - 1];
+    for (size_t r = 0; r < c->tnext; ++r) {
+      auto &e = c->tsets[r];
+      CUDA_TRY(ctx, cudaEventSynchronize(e[6]));
+      float t;
+      for (int i = 0; i < 6; ++i) {
+        CUDA_TRY(ctx, cudaEventElapsedTime(&t, e[i], e[i + 1]));
+        ms_sum[i] += t;
+      }
+      CUDA_TRY(ctx, cudaEventElapsedTime(&t, e[0], e[6]));
+      ms_sum[6] += t;
     }
-    CUDA_TRY(ctx, cudaEventElapsedTime(&t, e[0], e[6]));
-    ms_sum[6] += t;
+    n += (int32_t)c->tnext;
+    if (reset) c->tnext = 0;
   }
-  if (n_renders) *n_renders = (int32_t)ctx->tnext;
-  if (reset) ctx->tnext = 0;
+  if (n_renders) *n_renders = n;
   CUDA_TRY(ctx, cudaDeviceSynchronize());  // (renders without timing events too)
   bool sticky = false;
   gut_status s = take_sticky(ctx, (cudaStream_t)0, sticky);
