@@ -162,3 +162,36 @@ def test_render_batch_host_outputs(setup, fif):
     torch.cuda.synchronize()
     assert torch.equal(ref[0][0].cpu(), b0[0])
     r.close()
+
+
+def test_render_batch_stats_timing_overflow_and_errors(setup):
+    """Batch edge cases: stats (one view at a time, filled per view), timing of
+    the lanes' renders, a reservation too small for the views (the overflow of
+    a lane context is latched and reported by gut_check on the parent), and
+    invalid frames-in-flight values."""
+    import torch
+    from paper_2412_12507_b200 import gut
+    scene, cams = setup
+    r = gut.Renderer(scene, max_wh=(cams[0].width, cams[0].height))
+    bufs, outs = _outs(torch, cams)
+    gc = [gut.make_camera(c) for c in cams]
+    st = gut.gut_render_batch(r.ctx, r.scene, gc, gut.make_options(), outs, stats=True)
+    keys = [s.n_keys for s in st]
+    assert len(keys) == len(cams) and all(k > 0 for k in keys)
+    gut.gut_render_batch(r.ctx, r.scene, gc, gut.make_options(timing=True), outs)
+    ms, n = gut.gut_timing_read(r.ctx, reset=True)
+    assert n == len(cams) and ms["total"] > 0
+    with pytest.raises(gut.GutError):
+        gut.gut_context_set_frames_in_flight(r.ctx, 0)
+    with pytest.raises(gut.GutError):
+        gut.gut_context_set_frames_in_flight(r.ctx, 9)
+    r.close()
+    small = gut.Renderer(scene, reserve_keys=max(keys) // 3, max_wh=(cams[0].width, cams[0].height))
+    gut.gut_context_set_frames_in_flight(small.ctx, 3)
+    gut.gut_render_batch(small.ctx, small.scene, gc, gut.make_options(), outs)
+    with pytest.raises(gut.GutError) as e:
+        gut.gut_check(small.ctx)
+    assert e.value.status == 4
+    gut.gut_check(small.ctx)  # (cleared on every lane)
+    torch.cuda.synchronize()
+    small.close()
