@@ -1214,6 +1214,10 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
       if (s == 0 && w == 0) B.tile_work[tile].x = len;
     }
     if (B.trace) {
+      uint32_t na = 0;  // pixels still alive when the segment starts (exact prefix)
+#pragma unroll
+      for (int k = 0; k < NP; ++k) na += alive_in[k] ? 1u : 0u;
+      const uint32_t n_alive = warp_sum(na);
       const uint32_t e1 = warp_sum(n_eval), e2 = warp_sum(n_contrib);
       if (lane == 0) {
         unsigned long long t_end;
@@ -1224,7 +1228,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
         const size_t ti = 2 * ((size_t)slot * GUT_BLEND_WARPS + w);
         B.trace[ti] = make_uint4((uint32_t)tile | ((uint32_t)s << 16) | ((uint32_t)w << 29), smid,
                                  (uint32_t)t_begin, (uint32_t)t_end);
-        B.trace[ti + 1] = make_uint4(processed, e1, e2, wredo ? 1u : 0u);
+        B.trace[ti + 1] = make_uint4(processed, e1, e2, (wredo ? 1u : 0u) | (n_alive << 1));
       }
     }
 
@@ -1246,6 +1250,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(FULL, tmax, o));
+
       __syncwarp();  // the lanes' partials are ordered before lane 0's release below
       uint32_t nseg = 0;
       const uint32_t g0 = (uint32_t)min(S, B.window);

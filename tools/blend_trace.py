@@ -17,7 +17,8 @@ from paper_2412_12507_b200 import gut  # noqa: E402
 def analyse(tr, ranges, tx, seg, label):
     used = tr[:, 3] != 0
     tr = tr[used].astype(np.int64)
-    proc, nev, ncon, nredo = tr[:, 4], tr[:, 5], tr[:, 6], tr[:, 7]
+    proc, nev, ncon, nredo = tr[:, 4], tr[:, 5], tr[:, 6], tr[:, 7] & 1
+    nalive = tr[:, 7] >> 1
     tile, s = tr[:, 0] & 0xFFFF, (tr[:, 0] >> 16) & 0x1FFF
     t0 = tr[:, 2].min()
     b, e = tr[:, 2] - t0, tr[:, 3] - t0
@@ -43,6 +44,17 @@ def analyse(tr, ranges, tx, seg, label):
         if sel.any():
             print(f"  {lab}: spec pass {tsp[sel].sum() / 1e3:.0f} us, look-back wait {(tlb - tsp)[sel].sum() / 1e3:.0f} us, "
                   f"redo+outputs {(dur - tlb)[sel].sum() / 1e3:.0f} us (warp-time)")
+    sp = s > 0
+    if sp.any():
+        dead = sp & (nalive == 0)
+        print(f"  s>0 items with no pixel alive at their start (pure speculation waste): {dead.sum()} of {sp.sum()}, "
+              f"warp-time {dur[dead].sum() / 1e3:.0f} of {dur[sp].sum() / 1e3:.0f} us, visited {proc[dead].sum()}")
+        L0 = (ranges[:, 1] - ranges[:, 0]).astype(np.int64)
+        for lab, sel in (("wasted", dead), ("useful", sp & ~dead)):
+            if sel.any():
+                ll = L0[tile[sel]]
+                print(f"    {lab} s>0: tile len pct 10/50/90 {np.percentile(ll, [10, 50, 90]).astype(int)}, "
+                      f"s values {np.bincount(s[sel])[:8]}")
     print(f"  totals: warp-entries visited {proc.sum()} pairs eval {nev.sum()} contrib {ncon.sum()} "
           f"redo warps {nredo.sum()};  ns per warp-entry {dur.sum() / max(proc.sum(), 1):.1f} (warp-time)")
     s0 = s == 0
