@@ -325,3 +325,42 @@ def test_capacity_overflow_is_sticky():
     big.render(cam, stats=False)
     gut.gut_check(big.ctx)                          # no overflow, no error
     big.close()
+
+
+def test_4k_fisheye_sampled_tiles():
+    """Scale beyond the configs: the bench scene's recipe (1M Gaussians) at
+    3840x2160 fisheye (240 x 135 = 32,400 tiles: 15-bit tile ids, the two
+    8-bit tile passes) -- 24 sampled tiles (the 8 longest lists + 16 random)
+    against the oracle, and the sorted lists of those tiles bit-exact."""
+    from oracle import oracle as O
+    scene = S.make_scene("multiview", n=1_000_000)
+    cam = S.scaled_camera(S.make_views("multiview")[3], 2.0)
+    assert cam.width == 3840 and cam.height == 2160
+    g = gpu_render(scene, cam, reserve=int(scene.count * 12))
+    tx, ty = cam.tiles
+    assert tx * ty > 1 << 14  # (15 significant tile-id bits)
+    rng = np.random.default_rng(4)
+    lens = g["ranges"][:, 1].astype(np.int64) - g["ranges"][:, 0]
+    longest = np.argsort(-lens)[:8]
+    sub = np.sort(np.concatenate([longest, rng.choice(np.setdiff1d(np.arange(tx * ty), longest), 16,
+                                                      replace=False)])).astype(np.int32)
+    o = O.render(scene, cam, OPT, tile_subset=sub)
+    sampled = np.zeros((cam.height, cam.width), bool)
+    for t in sub:
+        sampled[(t // tx) * 16:(t // tx) * 16 + 16, (t % tx) * 16:(t % tx) * 16 + 16] = True
+    mask = sampled & pixel_mask(o["diag"], cam)
+    excluded = 1.0 - mask.sum() / sampled.sum()
+    e_rgb = np.abs(g["rgb"] - o["rgb"]).max(-1)[mask].max()
+    e_a = np.abs(g["alpha"] - o["alpha"])[mask].max()
+    print(f"4k fisheye sampled: rgb {e_rgb:.2e} alpha {e_a:.2e} excluded {excluded:.4%}; K={g['stats']['n_keys']}")
+    assert excluded <= 0.01 and e_rgb <= TOL_RGB and e_a <= TOL_ALPHA
+    # the sampled tiles' lists equal the oracle's (tile, fp32 depth, index) order
+    tiles_o, gids_o, ranges_o = O.tile_lists(O.preprocess(scene, cam, OPT), cam, OPT)
+    amb = (o["proj"]["cull_ambig"] != 0) | (o["proj"]["bin_ambig"] != 0)
+    pairs = g["sorted"]
+    for t in sub:
+        a, b = g["ranges"][t]
+        lg = [int(x) for x in pairs[a:b, 1] if not amb[x]] if b > a else []
+        ao, bo = ranges_o[t]
+        lo = [int(x) for x in gids_o[ao:bo] if not amb[x]]
+        assert lg == lo, t
