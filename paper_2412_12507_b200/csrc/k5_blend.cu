@@ -205,6 +205,61 @@ __global__ __launch_bounds__(GUT_TILE_PX) void rays_kernel(DevCam c, float4 *__r
     }
   }
   pix[(size_t)tile * GUT_TILE_PX + threadIdx.x] = out;
+  // Per 8x8 block (MODE 0/1): least-squares affine lattice of the fp32 offsets
+  // of its valid pixels, and the largest residual against the fp32-rounded
+  // coefficients.  K5's candidate masks bound a Gaussian's footprint on this
+  // lattice and widen it by the residual (blend: entry_mask).
+  __shared__ float2 s_ab[GUT_TILE_PX];
+  s_ab[threadIdx.x] = make_float2(out.x, out.z > 0.f ? out.y : __int_as_float(0x7fc00000));  // NaN b: invalid
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    const int B = threadIdx.x;
+    float *fit = anchors[tile].fit[B];
+    auto idx = [&](int cx, int ry) {
+      const int y = (B >> 1) * 8 + ry;
+      return (((B & 1) | ((y >> 2) << 1)) << 5) + (ry & 3) * 8 + cx;
+    };
+    double n = 0, sx = 0, sy = 0, sxx = 0, sxy = 0, syy = 0, sa = 0, sxa = 0, sya = 0, sb = 0, sxb = 0, syb = 0;
+    for (int ry = 0; ry < 8; ++ry)
+      for (int cx = 0; cx < 8; ++cx) {
+        const float2 v = s_ab[idx(cx, ry)];
+        if (MODE == 2 || v.y != v.y) continue;
+        const double x = cx, y = ry, a = v.x, b = v.y;
+        n += 1; sx += x; sy += y; sxx += x * x; sxy += x * y; syy += y * y;
+        sa += a; sxa += x * a; sya += y * a; sb += b; sxb += x * b; syb += y * b;
+      }
+    // normal equations [n sx sy; sx sxx sxy; sy sxy syy] c = rhs (Cramer)
+    const double c00 = sxx * syy - sxy * sxy, c01 = sy * sxy - sx * syy, c02 = sx * sxy - sy * sxx;
+    const double det = n * c00 + sx * c01 + sy * c02;
+    double ca[3] = {0, 0, 0}, cb[3] = {0, 0, 0};
+    bool ok = n > 0;
+    if (n >= 3 && det > 1e-6 * n * n * n) {
+      const double c11 = n * syy - sy * sy, c12 = sx * sy - n * sxy, c22 = n * sxx - sx * sx;
+      ca[0] = (c00 * sa + c01 * sxa + c02 * sya) / det;
+      ca[1] = (c01 * sa + c11 * sxa + c12 * sya) / det;
+      ca[2] = (c02 * sa + c12 * sxa + c22 * sya) / det;
+      cb[0] = (c00 * sb + c01 * sxb + c02 * syb) / det;
+      cb[1] = (c01 * sb + c11 * sxb + c12 * syb) / det;
+      cb[2] = (c02 * sb + c12 * sxb + c22 * syb) / det;
+    } else if (ok) {  // collinear / too few valid pixels: a constant lattice (loose, still conservative)
+      ca[0] = sa / n;
+      cb[0] = sb / n;
+    }
+    float fa[3], fb[3];
+    for (int q = 0; q < 3; ++q) { fa[q] = (float)ca[q]; fb[q] = (float)cb[q]; }
+    double ra = 0, rb = 0;
+    for (int ry = 0; ry < 8; ++ry)
+      for (int cx = 0; cx < 8; ++cx) {
+        const float2 v = s_ab[idx(cx, ry)];
+        if (!ok || v.y != v.y) continue;
+        ra = fmax(ra, fabs((double)v.x - ((double)fa[0] + (double)fa[1] * cx + (double)fa[2] * ry)));
+        rb = fmax(rb, fabs((double)v.y - ((double)fb[0] + (double)fb[1] * cx + (double)fb[2] * ry)));
+      }
+    const float inf = __int_as_float(0x7f800000);
+    const bool use = ok && MODE != 2 && isfinite(ra) && isfinite(rb);
+    fit[0] = fa[0]; fit[1] = fa[1]; fit[2] = fa[2]; fit[3] = use ? __double2float_ru(ra * (1 + 1e-6)) : inf;
+    fit[4] = fb[0]; fit[5] = fb[1]; fit[6] = fb[2]; fit[7] = use ? __double2float_ru(rb * (1 + 1e-6)) : inf;
+  }
 }
 
 void launch_rays(const DevCam &cam, float4 *pix, TileAnchor *anchors, cudaStream_t st) {
@@ -531,7 +586,7 @@ __device__ __forceinline__ void kb_insert(KBuf<KB> &kb, LanePx<NP> &L, int k, fl
 // fp64, D / T1 / T2 in fp32, the pixel box) live in shared memory rather than
 // registers: the staging reloads them once per 32-entry chunk (broadcast),
 // which frees ~25 registers in the evaluation loops.
-#define GUT_WC_F4 7  // float4 per warp
+#define GUT_WC_F4 9  // float4 per warp
 #ifndef GUT_K5_HALF_SKIP
 #define GUT_K5_HALF_SKIP 1  // per-pixel-row-half warp-uniform skip of the evaluation (tuning switch)
 #endif
@@ -540,9 +595,17 @@ __device__ __forceinline__ float4 *warp_consts(int nf) {
   return s_dyn + (GUT_BLEND_CTA / 32) * 2 * 32 * GUT_PAYLOAD_F4 + (GUT_BLEND_CTA / 32) * 32 * nf +
          (threadIdx.x >> 5) * GUT_WC_F4;
 }
+template <int MODE>
+constexpr size_t blend_smem_bytes() {
+  return sizeof(float4) * ((GUT_BLEND_CTA / 32) * 2 * 32 * GUT_PAYLOAD_F4 + (GUT_BLEND_CTA / 32) * 32 * WarpTbl<MODE>::NF +
+                           (GUT_BLEND_CTA / 32) * GUT_WC_F4);
+}
 __device__ __forceinline__ void store_warp_consts(float4 *wc, const d3 &D, const d3 &dO, const f3 &T1f, const f3 &T2f,
-                                                  float ac, float bc, float ra, float rb, float tc, float rt) {
+                                                  float ac, float bc, float ra, float rb, float tc, float rt,
+                                                  const float *fit) {
   if ((threadIdx.x & 31) == 0) {
+    wc[7] = make_float4(fit[0], fit[1], fit[2], fit[3]);
+    wc[8] = make_float4(fit[4], fit[5], fit[6], fit[7]);
     double2 *wd = reinterpret_cast<double2 *>(wc);
     wd[0] = make_double2(D.x, D.y);
     wd[1] = make_double2(D.z, dO.x);
@@ -560,12 +623,66 @@ __device__ __forceinline__ double2 lds_d2(uint32_t addr) {
   return v;
 }
 
+// Candidate mask of one staged entry over the warp's 8x8 pixel block (bit
+// 8 ry + cx; word 0 = rows 0-3, word 1 = rows 4-7): a superset of the pixels
+// whose hit test F(da, db) <= 0 can pass.  The pixels' offsets lie on the
+// block's affine lattice p -> w0 + J p (rays_kernel fit, residual rho), so
+// F(true) <= 0 implies G(p) = F(w0 + J p) <= Em, Em = the lattice error
+// |grad F| rho + |Hess F| rho^2 over the box plus a rounding margin 1e-4 mag
+// (the hit test's own fp32 error is ~1e-7 mag).  {G <= Em} is an ellipse when
+// the Hessian is positive definite (well conditioned: det > 1e-3 Hxx Hyy);
+// the mask is its bounding box on the lattice, widened by 1% + 1e-3 px for
+// the fp32 solve.  Any other case keeps every pixel.
+__device__ __forceinline__ uint2 entry_mask(float F0, float Fa, float Fb, float Faa, float Fab, float Fbb, float as,
+                                            float bs, float A, float Bm, float mag, float4 fa, float4 fb) {
+  const float u0 = fa.x - as, v0 = fb.x - bs;
+  const float ax = fa.y, ay = fa.z, bx = fb.y, by = fb.z, rha = fa.w, rhb = fb.w;
+  const float A2 = A + rha, B2 = Bm + rhb;
+  const float aFaa = fabsf(Faa), aFab = fabsf(Fab), aFbb = fabsf(Fbb);
+  const float Em = fmaf(fmaf(2.f * aFaa, A2, fmaf(aFab, B2, fabsf(Fa))), rha,
+                        fmaf(fmaf(2.f * aFbb, B2, fmaf(aFab, A2, fabsf(Fb))), rhb,
+                             fmaf(fmaf(aFaa, rha, aFab * rhb), rha, aFbb * rhb * rhb))) +
+                   1e-4f * mag;
+  const float Fu = fmaf(2.f * Faa, u0, fmaf(Fab, v0, Fa)), Fv = fmaf(2.f * Fbb, v0, fmaf(Fab, u0, Fb));
+  const float G0 = fmaf(u0, fmaf(Faa, u0, fmaf(Fab, v0, Fa)), fmaf(v0, fmaf(Fbb, v0, Fb), F0));
+  const float gx = fmaf(ax, Fu, bx * Fv), gy = fmaf(ay, Fu, by * Fv);
+  const float hx0 = fmaf(2.f * Faa, ax, Fab * bx), hx1 = fmaf(Fab, ax, 2.f * Fbb * bx);
+  const float hy0 = fmaf(2.f * Faa, ay, Fab * by), hy1 = fmaf(Fab, ay, 2.f * Fbb * by);
+  const float Hxx = fmaf(ax, hx0, bx * hx1), Hxy = fmaf(ay, hx0, by * hx1), Hyy = fmaf(ay, hy0, by * hy1);
+  const float det = fmaf(Hxx, Hyy, -Hxy * Hxy);
+  uint2 m = make_uint2(~0u, ~0u);
+  if (Hxx > 0.f && Hyy > 0.f && det > 1e-3f * Hxx * Hyy && Em < 1e30f) {
+    const float id = rcp_approx(det);  // (MUFU: 2^-22 relative, inside the 1% widening)
+    const float nx = fmaf(Hyy, gx, -Hxy * gy), ny = fmaf(Hxx, gy, -Hxy * gx);
+    const float px = -nx * id, py = -ny * id;  // minimiser p* = -H^-1 g
+    const float gp = fmaf(gx, px, gy * py);    // g . p* = -g^T H^-1 g
+    const float R = Em + 1e-2f * fabsf(gp) - fmaf(0.5f, gp, G0);  // Em - min G (+ margin)
+    if (!(R >= 0.f)) {
+      if (R < 0.f) m = make_uint2(0u, 0u);
+    } else if (R < 1e30f) {
+      const float r2 = 2.f * R * id;
+      const float hx = fmaf(1.01f, sqrt_approx(r2 * Hyy), fmaf(1e-2f * id, fabsf(Hyy * gx) + fabsf(Hxy * gy), 1e-3f));
+      const float hy = fmaf(1.01f, sqrt_approx(r2 * Hxx), fmaf(1e-2f * id, fabsf(Hxx * gy) + fabsf(Hxy * gx), 1e-3f));
+      // pixel index bounds on the lattice (cvt saturates out-of-range values)
+      const int xl = max(__float2int_ru(px - hx), 0), xh = min(__float2int_rd(px + hx), 7);
+      const int yl = max(__float2int_ru(py - hy), 0), yh = min(__float2int_rd(py + hy), 7);
+      // columns xl..xh of rows yl..yh (empty when a range is: the shifts
+      // then give a zero or wrapped-to-zero difference)
+      const uint32_t col = (xh >= xl) ? (2u << xh) - (1u << xl) : 0u;
+      const unsigned long long rows = (yh >= yl) ? (2ull << (8 * yh + 7)) - (1ull << (8 * yl)) : 0ull;
+      const uint32_t rep = col * 0x01010101u;
+      m = make_uint2(rep & (uint32_t)rows, rep & (uint32_t)(rows >> 32));
+    }
+  }
+  return m;
+}
+
 template <int MODE, int NP, int KB = 0>
 __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, uint32_t s0, uint32_t s1,
                                           LanePx<NP> &L, uint32_t &n_eval, uint32_t &n_contrib,
                                           uint32_t &processed, const unsigned long long *poll_stat, int poll_s,
                                           Checkpoints<NP> *ck, uint32_t ck_step, const uint32_t *act,
-                                          KBuf<KB> *kb = nullptr) {
+                                          KBuf<KB> *kb = nullptr, int half = 0) {
   constexpr int NF = WarpTbl<MODE>::NF;
   constexpr unsigned FULL = 0xffffffffu;
   // dynamic shared memory: [raw payload double buffer: 8 warps x 2 x 32 x 5]
@@ -687,6 +804,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
     processed = min(b0 + 32, s1) - s0;
     const uint32_t kk = b0 + (uint32_t)lane;
     bool maybe = false;
+    uint2 cmask = make_uint2(0u, 0u);  // candidate pixels of the lane's entry (MODE 0/1)
     if (kk < s1) {
       // ---- stage entry kk.  The cancelling part c0 = o_g x d_g (o_g = M w,
       // d_g = M D, w = O - mu) uses (M a) x (M b) = cof(M) (a x b) with
@@ -817,18 +935,28 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
             t[3] = make_float4(Dab, Dbb, gs, gu);
             t[4] = make_float4(gv, k2, l2s, 0.f);
             t[5] = make_float4(p4.x, p4.y, p4.z, KB > 0 ? __uint_as_float(__ldg(&B.gids[kk])) : 0.f);
+            uint2 em = entry_mask(F0, Fa, Fb, Faa, Fab, Fbb, as, bs, A, Bm, mag, lds128(wc_s + 112),
+                                  lds128(wc_s + 128));
+            if (NP == 1) em = make_uint2(half ? em.y : em.x, 0u);
+            cmask = em;
           }
         }
       }
     }
     uint32_t m = __ballot_sync(FULL, maybe);
-    __syncwarp();
-    {  // statistics: pairs (live pixel, surviving entry) of this chunk
+    {  // statistics: pairs (live pixel, entry surviving the warp-box cull) of this chunk
       uint32_t live = 0;
 #pragma unroll
       for (int k = 0; k < NP; ++k) live += L.done[k] ? 0u : 1u;
       n_eval += live * (uint32_t)__popc(m);
     }
+    if (MODE != 2) {
+      // only entries with a candidate pixel that is still live are evaluated
+      const uint32_t live0 = __ballot_sync(FULL, !L.done[0]);
+      const uint32_t live1 = NP > 1 ? __ballot_sync(FULL, !L.done[NP > 1 ? 1 : 0]) : 0u;
+      m = __ballot_sync(FULL, maybe && ((cmask.x & live0) | (cmask.y & live1)) != 0u);
+    }
+    __syncwarp();
     while (m) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
@@ -888,7 +1016,8 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
           }
         }
       } else {
-        // lanes predicated, the body skipped (warp-uniform branch) when no
+        // the entry's candidate pixels (mask words, warp-uniform); lanes
+        // predicated, the body skipped (warp-uniform branch) when no candidate
         // pixel of the warp is inside the footprint
         const float4 f0 = lds128(ta), f1 = lds128(ta + 16);
         float F[NP], da[NP], db[NP];
@@ -1111,7 +1240,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     Checkpoints<NP> ck;
     const uint32_t ck_step = max(32u, ((uint32_t)B.seg / GUT_CK) & ~31u);
     store_warp_consts(warp_consts(WarpTbl<MODE>::NF), D, O - mkd(c.c0[0], c.c0[1], c.c0[2]), T1f, T2f, ac, bc, ra,
-                      rb, tc, rt);
+                      rb, tc, rt, A.fit[w]);
     unsigned long long t_spec = 0, t_lb = 0;  // (trace only: end of the speculative pass / of the look-back)
     float T_pre[NP], T_end[NP];
     bool alive_in[NP], redo[NP], any_redo = false, wredo = false;
@@ -1350,9 +1479,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
 
 template <int MODE>
 static void blend_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
-  constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_CTA / 32) * 2 * 32 * GUT_PAYLOAD_F4 +
-                                            (GUT_BLEND_CTA / 32) * 32 * WarpTbl<MODE>::NF +
-                                            (GUT_BLEND_CTA / 32) * GUT_WC_F4);
+  constexpr size_t smem = blend_smem_bytes<MODE>();
   // per device, thread-safe (a process may drive several devices): the
   // dynamic shared-memory attribute is a per-device setting
   static std::once_flag once[GUT_MAX_DEVICES];
@@ -1461,10 +1588,11 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kbuf_kern
 #pragma unroll
     for (int i = 0; i < KB; ++i) { kb.t[i] = -INFINITY; kb.a[i] = 0.f; kb.g[i] = 0u; }
     uint32_t n_eval = 0, n_contrib = 0, processed = 0;
+    // (the 8x4 block w is half (w >> 1) & 1 of the 8x8 fit block (w & 1) | ((w >> 2) << 1))
     store_warp_consts(warp_consts(WarpTbl<MODE>::NF), D, O - mkd(c.c0[0], c.c0[1], c.c0[2]), T1f, T2f, ac, bc, ra,
-                      rb, tc, rt);
+                      rb, tc, rt, A.fit[(w & 1) | ((w >> 2) << 1)]);
     warp_pass<MODE, 1, KB>(c, B, start, end, L, n_eval, n_contrib, processed,
-                           nullptr, 0, nullptr, 0, nullptr, &kb);
+                           nullptr, 0, nullptr, 0, nullptr, &kb, (w >> 1) & 1);
     // end of the list: the pending hits near to far (colours gathered up front)
     if (!L.done[0]) {
       float4 cc[KB];
@@ -1515,9 +1643,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kbuf_kern
 
 template <int MODE, int KB>
 static void blend_kbuf_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st) {
-  constexpr size_t smem = sizeof(float4) * ((GUT_BLEND_CTA / 32) * 2 * 32 * GUT_PAYLOAD_F4 +
-                                            (GUT_BLEND_CTA / 32) * 32 * WarpTbl<MODE>::NF +
-                                            (GUT_BLEND_CTA / 32) * GUT_WC_F4);
+  constexpr size_t smem = blend_smem_bytes<MODE>();
   // per device, thread-safe (a process may drive several devices): the
   // dynamic shared-memory attribute is a per-device setting
   static std::once_flag once[GUT_MAX_DEVICES];

@@ -93,6 +93,11 @@ void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper,
 // intrinsics only (cached).  Rolling shutter: world frame, per view.
 struct TileAnchor {
   double D[3], T1[3], T2[3], O[3], ta, pad[3];
+  // per 8x8 pixel block B (x0 = 8 (B & 1), y0 = 8 (B >> 1)): the pixels' fp32
+  // offsets as an affine lattice a(x, y) = a00 + ax x + ay y (+ |residual| <=
+  // rho_a), same for b, x, y = 0..7 within the block -- {a00, ax, ay, rho_a,
+  // b00, bx, by, rho_b}; rho = +inf: no usable fit (K5 masks then keep every pixel)
+  float fit[4][8];
 };
 
 // per-pixel (a, b, snorm, beta) relative to the tile anchor + per-tile anchors
