@@ -23,7 +23,7 @@ namespace gut {
 __device__ __forceinline__ float atan2_pos(float y, float x) {
   const float ax = fabsf(x);
   const float mx = fmaxf(y, ax), mn = fminf(y, ax);
-  const float a = mx > 0.f ? mn * __frcp_rn(mx) : 0.f;
+  const float a = mx > 0.f ? mn * rs_rcp(mx) : 0.f;
   const float u = a * a;
   float p = 0.0024561970494687557f;
   p = fmaf(p, u, -0.014399108476936817f);
@@ -40,12 +40,16 @@ __device__ __forceinline__ float atan2_pos(float y, float x) {
   return t;
 }
 
+// MODEL: the camera model as a compile-time constant (-1: read from c at run
+// time).  MUFU reciprocal / square root (relative error ~2^-22, like the
+// other fp32 roundings here far inside the 1e-3 px binning band).
+template <int MODEL = -1>
 __device__ __forceinline__ bool project_cam_f(const DevCam &c, f3 x, float &du, float &dv) {
   // returns pixel offsets from the principal point (du, dv); validity first
-  switch (c.model) {
+  switch (MODEL >= 0 ? MODEL : c.model) {
     case CAM_PINHOLE: {
       if (!(x.z > c.near_plane)) return false;
-      const float rz = __frcp_rn(x.z);
+      const float rz = rs_rcp(x.z);
       du = c.fxf * (x.x * rz);
       dv = c.fyf * (x.y * rz);
       return true;
@@ -58,12 +62,12 @@ __device__ __forceinline__ bool project_cam_f(const DevCam &c, f3 x, float &du, 
     }
     case CAM_OPENCV: {
       if (!(x.z > c.near_plane)) return false;
-      const float rz = __frcp_rn(x.z);
+      const float rz = rs_rcp(x.z);
       float xn = x.x * rz, yn = x.y * rz, r2 = xn * xn + yn * yn;
       if (c.fovf > 0.f && !(r2 <= c.fovf * c.fovf)) return false;
       float num = 1.f + r2 * (c.kf[0] + r2 * (c.kf[1] + r2 * c.kf[2]));
       float den = 1.f + r2 * (c.kf[3] + r2 * (c.kf[4] + r2 * c.kf[5]));
-      float a = num * __frcp_rn(den);
+      float a = num * rs_rcp(den);
       float xd = xn * a + 2.f * c.pf[0] * xn * yn + c.pf[1] * (r2 + 2.f * xn * xn);
       float yd = yn * a + c.pf[0] * (r2 + 2.f * yn * yn) + 2.f * c.pf[1] * xn * yn;
       du = c.fxf * xd;
@@ -74,13 +78,13 @@ __device__ __forceinline__ bool project_cam_f(const DevCam &c, f3 x, float &du, 
       const float rho2 = x.x * x.x + x.y * x.y;
       // |x| > near, squared (near * |near| keeps a negative near always true)
       if (!(rho2 + x.z * x.z > c.near_plane * fabsf(c.near_plane))) return false;
-      const float rho = sqrtf(rho2);
+      const float rho = rs_sqrt(rho2);
       const float th = atan2_pos(rho, x.z);
       if (!(th <= c.fovf)) return false;
       if (rho == 0.f) { du = 0.f; dv = 0.f; return true; }
       float t2 = th * th;
       float td = th * (1.f + t2 * (c.kf[0] + t2 * (c.kf[1] + t2 * (c.kf[2] + t2 * c.kf[3]))));
-      float s = td * __frcp_rn(rho);
+      float s = td * rs_rcp(rho);
       du = c.fxf * (s * x.x);
       dv = c.fyf * (s * x.y);
       return true;
@@ -118,12 +122,12 @@ __device__ __forceinline__ f3 cam_point_at(const DevCam &c, f3 y, f3 w, float t)
 __device__ __noinline__ bool project_sigma_rs(const DevCam &c, f3 y, f3 w, float &du, float &dv, float &t_out);
 // RS: the rolling-shutter instantiation of K1 (project_kernel<DEG, true>); the
 // global-shutter one never contains the shutter solve
-template <bool RS>
+template <bool RS, int MODEL>
 __device__ __forceinline__ bool project_sigma(const DevCam &c, f3 y, f3 w, float &du, float &dv,
                                               float &t_out) {
   if (!RS || c.shutter == SH_GLOBAL) {
     t_out = 0.f;
-    return project_cam_f(c, y, du, dv);
+    return project_cam_f<MODEL>(c, y, du, dv);
   }
   return project_sigma_rs(c, y, w, du, dv, t_out);
 }
@@ -289,7 +293,7 @@ __device__ __forceinline__ uint32_t finish_gaussian(const DevCam &c, const Scene
   // o_g x d_g = cof(M) (w x d) from it, see k5_blend.cu), k^2 = 2 ln(sigma /
   // alpha_min) (the ellipse record's value; K5 derives log2 sigma from it),
   // M = diag(1/s) R^T (Eq. 11 o_g = M (o - mu)), rgb
-  const float is0 = 1.f / sc.x, is1 = 1.f / sc.y, is2 = 1.f / sc.z;
+  const float is0 = rs_rcp(sc.x), is1 = rs_rcp(sc.y), is2 = rs_rcp(sc.z);  // (MUFU, ~2^-22 relative)
   const d3 w0 = mkd(c.c0[0], c.c0[1], c.c0[2]) - mkd(po.x, po.y, po.z);
   const unsigned long long wz = (unsigned long long)__double_as_longlong(w0.z);
   float4 *pl = payload + (size_t)GUT_PAYLOAD_F4 * i;
@@ -298,7 +302,7 @@ __device__ __forceinline__ uint32_t finish_gaussian(const DevCam &c, const Scene
                       R[0] * is0);
   pl[2] = make_float4(R[3] * is0, R[6] * is0, R[1] * is1, R[4] * is1);
   pl[3] = make_float4(R[7] * is1, R[2] * is2, R[5] * is2, R[8] * is2);
-  pl[4] = make_float4(rgb.x, rgb.y, rgb.z, log2f(po.w));  // log2 sigma: K5's alpha for kernel degree != 2
+  pl[4] = make_float4(rgb.x, rgb.y, rgb.z, c.kdeg != 2 ? log2f(po.w) : 0.f);  // log2 sigma: K5's alpha for degree != 2
   return __float_as_uint(depth);
 }
 
@@ -366,7 +370,7 @@ __device__ __forceinline__ void k1_block_totals(uint32_t my_tiles, uint32_t key,
 }
 
 // ---- K1 main (fp32): one thread per Gaussian
-template <int DEG, bool LIST>
+template <int DEG, bool LIST, int MODEL>
 #ifndef GUT_K1_CTAS
 #define GUT_K1_CTAS 4  // 64 registers: 32 warps per SM (measured best)
 #endif
@@ -399,13 +403,13 @@ __global__ __launch_bounds__(256, GUT_K1_CTAS) void project_kernel(DevCam c, Sce
       const f3 y0 = tof(y0d);
       const f3 wv = mtv(c.R0f, mk(c.dcf[0], c.dcf[1], c.dcf[2]));
       const float sj[3] = {sc.x, sc.y, sc.z};
-      ok = project_sigma<LIST>(c, y0, wv, du[0], dv[0], tt[0]);
+      ok = project_sigma<LIST, MODEL>(c, y0, wv, du[0], dv[0], tt[0]);
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         const f3 L = (c.gamma * sj[j]) * mk(R[j], R[3 + j], R[6 + j]);
         const f3 Lc = mtv(c.R0f, L);
-        ok = ok && project_sigma<LIST>(c, y0 + Lc, wv, du[1 + j], dv[1 + j], tt[1 + j]);
-        ok = ok && project_sigma<LIST>(c, y0 - Lc, wv, du[4 + j], dv[4 + j], tt[4 + j]);
+        ok = ok && project_sigma<LIST, MODEL>(c, y0 + Lc, wv, du[1 + j], dv[1 + j], tt[1 + j]);
+        ok = ok && project_sigma<LIST, MODEL>(c, y0 - Lc, wv, du[4 + j], dv[4 + j], tt[4 + j]);
       }
     }
     float vx = 0, vy = 0, cxx = 0, cxy = 0, cyy = 0, k2 = 0;
@@ -635,6 +639,33 @@ __global__ __launch_bounds__(256) void project_prefilter_kernel(DevCam c, SceneD
   if (keep) list[base + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)i;
 }
 
+// one SH degree: the rolling-shutter K1 (compacted list) reads the camera model
+// at run time; the global-shutter K1 is instantiated per camera model
+template <int DEG>
+static void launch_k1_deg(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32_t *tiles, float4 *ell,
+                          double2 *ell64, float4 *payload, uint32_t *counters, uint32_t *deferred, uint32_t *list,
+                          unsigned blocks, unsigned wblocks, cudaStream_t st) {
+  if (list) {
+    project_kernel<DEG, true, -1><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+  } else {
+    switch (cam.model) {
+      case CAM_PINHOLE:
+        project_kernel<DEG, false, CAM_PINHOLE><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+        break;
+      case CAM_OPENCV:
+        project_kernel<DEG, false, CAM_OPENCV><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+        break;
+      case CAM_FISHEYE:
+        project_kernel<DEG, false, CAM_FISHEYE><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+        break;
+      default:
+        project_kernel<DEG, false, CAM_ORTHO><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+        break;
+    }
+  }
+  project_wide_kernel<DEG><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
+}
+
 void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32_t *tiles, float4 *ell,
                     double2 *ell64, float4 *payload, uint32_t *counters, uint32_t *deferred, uint32_t *list,
                     cudaStream_t st) {
@@ -648,26 +679,10 @@ void launch_project(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32
     list = nullptr;
   }
   switch (s.sh_degree) {
-    case 0:
-      if (list) project_kernel<0, true><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
-      else project_kernel<0, false><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
-      project_wide_kernel<0><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
-      break;
-    case 1:
-      if (list) project_kernel<1, true><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
-      else project_kernel<1, false><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
-      project_wide_kernel<1><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
-      break;
-    case 2:
-      if (list) project_kernel<2, true><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
-      else project_kernel<2, false><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
-      project_wide_kernel<2><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
-      break;
-    default:
-      if (list) project_kernel<3, true><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
-      else project_kernel<3, false><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
-      project_wide_kernel<3><<<wblocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred);
-      break;
+    case 0: launch_k1_deg<0>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred, list, blocks, wblocks, st); break;
+    case 1: launch_k1_deg<1>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred, list, blocks, wblocks, st); break;
+    case 2: launch_k1_deg<2>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred, list, blocks, wblocks, st); break;
+    default: launch_k1_deg<3>(cam, s, dkey, tiles, ell, ell64, payload, counters, deferred, list, blocks, wblocks, st); break;
   }
 }
 
