@@ -40,6 +40,12 @@ __device__ __forceinline__ void block_scan2(uint32_t x, uint32_t y, uint32_t *s_
   __syncthreads();  // s_tmp reusable
 }
 
+// keys staged in shared memory per CTA (written out as one coalesced run);
+// a partition with more keys writes them straight to global memory
+#ifndef GUT_EMIT_STAGE
+#define GUT_EMIT_STAGE 4096
+#endif
+
 // A CTA owns GUT_EMIT_PART consecutive Gaussians (depth order); its first
 // key slot comes from emit_count_kernel + emit_scan_kernel (per-partition key
 // totals, scanned), so no CTA waits on another.  K2 reads only the 4-byte
@@ -68,6 +74,7 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ uint32_t s_hist[2][256];
   __shared__ uint32_t s_tmp[16];
+  __shared__ uint32_t s_kt[GUT_EMIT_STAGE], s_kg[GUT_EMIT_STAGE];  // staged (tile, gid) keys of the CTA
 
   const uint32_t n = *n_vis_p;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -92,8 +99,10 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
   uint32_t ex, ey, total, ty_;
   block_scan2(sc, 0u, s_tmp, ex, ey, total, ty_);  // (its barriers also order the s_hist reset)
 
-  // ---- small Gaussians: keys from the mask, row-major
-  uint32_t pos = prefix + ex;
+  // ---- small Gaussians: keys from the mask, row-major (staged in shared
+  // memory when the CTA's keys fit, then written out as one coalesced run)
+  const bool staged = total <= GUT_EMIT_STAGE;
+  uint32_t pos = prefix + ex, lpos = ex;
   bool big[GUT_EMIT_ITEMS];
   uint32_t bpos[GUT_EMIT_ITEMS];
 #pragma unroll
@@ -110,10 +119,20 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
         // row = b / cw without an integer division (cw = 3: b < 9, (11 b) >> 5 = b / 3)
         const uint32_t row = m4 ? b >> 2 : (b * 11u) >> 5;
         const uint32_t tile = (y0 + row) * (uint32_t)tiles_x + x0 + (b - row * cw);
-        emit_key(pos++, tile, g[j], cap_k, out_tile, out_gid, s_hist, counters);
+        if (staged) {
+          s_kt[lpos] = tile;
+          s_kg[lpos] = g[j];
+          atomicAdd(&s_hist[0][tile & 255u], 1u);
+          atomicAdd(&s_hist[1][(tile >> 8) & 255u], 1u);
+        } else {
+          emit_key(pos, tile, g[j], cap_k, out_tile, out_gid, s_hist, counters);
+        }
+        ++pos;
+        ++lpos;
       }
     } else {
       pos += code_count(code[j]);
+      lpos += code_count(code[j]);
     }
   }
   // ---- big Gaussians: appended to a global list (depth order clusters them in
@@ -128,6 +147,18 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
     if (big[j]) big_list[slot] = make_uint2(g[j], bpos[j]);
   }
   __syncthreads();
+  if (staged) {  // the CTA's run [prefix, prefix + total): a big Gaussian's slots hold
+                 // stale words here, overwritten by emit_big_kernel (launched after)
+    const uint32_t lim = prefix < cap_k ? min(total, cap_k - prefix) : 0u;
+    for (uint32_t q = tid; q < lim; q += GUT_EMIT_THREADS) {
+      out_tile[prefix + q] = s_kt[q];
+      out_gid[prefix + q] = s_kg[q];
+    }
+    if (lim < total && tid == 0) {
+      counters[CNT_OVERFLOW] = 1u;
+      counters[CNT_STICKY_OVERFLOW] = 1u;  // latched until the host reads it (gut_check)
+    }
+  }
   for (int jj = tid; jj < 512; jj += GUT_EMIT_THREADS) {
     const uint32_t v = (&s_hist[0][0])[jj];
     if (v) atomicAdd(&counters[CNT_HIST_TILE + jj], v);
