@@ -533,7 +533,9 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   uint32_t *cnt = ctx->counters;
   CUDA_TRY(ctx, cudaMemsetAsync(cnt, 0, CNT_WORDS * sizeof(uint32_t), st));
   // look-back epochs of this render (device-side, so a captured render replays correctly)
-  launch_frame_init(cnt, ctx->bstatus, ctx->cap_items * GUT_TILE_PX, ctx->ranges, dc.n_tiles, st);
+  uint32_t *part_tot = reinterpret_cast<uint32_t *>(ctx->st_emit);  // K2 partition key totals (final depth pass)
+  launch_frame_init(cnt, ctx->bstatus, ctx->cap_items * GUT_TILE_PX, ctx->ranges, dc.n_tiles, part_tot,
+                    (int)((N + GUT_EMIT_PART - 1) / GUT_EMIT_PART), st);
   // K1: UT projection
   launch_project(dc, scene->d, ctx->dkey, ctx->tiles, ctx->ell, ctx->ell64, ctx->payload, cnt, ctx->deferred,
                  ctx->k1_list, st);
@@ -548,7 +550,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   launch_sort_pass(ctx->sb_k, ctx->sb_v, ctx->sa_k, ctx->sa_v, cnt + CNT_NVIS, n32, 16, hd + 512, ctx->st_depth,
                    cnt + CNT_TICKETS + 2, cnt + CNT_EPOCH, 2u, false, st);
   launch_sort_pass(ctx->sa_k, ctx->sa_v, nullptr, ctx->sb_v, cnt + CNT_NVIS, n32, 24, hd + 768, ctx->st_depth,
-                   cnt + CNT_TICKETS + 3, cnt + CNT_EPOCH, 3u, false, st);
+                   cnt + CNT_TICKETS + 3, cnt + CNT_EPOCH, 3u, false, st, nullptr, ctx->tiles, ctx->sb_k, part_tot);
   const uint32_t *order = ctx->sb_v;
   if (timing) cudaEventRecord(ev[2], st);
   // key count: capacity mode keeps the stream asynchronous; otherwise read K back
@@ -565,7 +567,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   }
   // K2: depth-ordered scan + emission of (tile, gid) keys
   launch_emit(order, cnt + CNT_NVIS, n32, ctx->tiles, ctx->ell, ctx->ell64, dc.tiles_x, dc.tile_cull, ctx->ka, ctx->va,
-              (uint32_t)ctx->cap_k, cnt, reinterpret_cast<uint32_t *>(ctx->st_emit), ctx->big_list, st);
+              (uint32_t)ctx->cap_k, cnt, part_tot, ctx->big_list, st, ctx->sb_k);
   if (timing) cudaEventRecord(ev[3], st);
   // K3 level 2: stable tile passes
   const uint32_t *ht = cnt + CNT_HIST_TILE;

@@ -70,7 +70,7 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
     const uint32_t *__restrict__ order, const uint32_t *n_vis_p, const uint32_t *__restrict__ tiles,
     const float4 *__restrict__ ell, const double2 *__restrict__ ell64, int tiles_x, int tile_cull,
     uint32_t *__restrict__ out_tile, uint32_t *__restrict__ out_gid, uint32_t cap_k, uint32_t *counters,
-    const uint32_t *__restrict__ part_off, uint2 *__restrict__ big_list) {
+    const uint32_t *__restrict__ part_off, uint2 *__restrict__ big_list, const uint32_t *__restrict__ codes) {
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ uint32_t s_hist[2][256];
   __shared__ uint32_t s_tmp[16];
@@ -92,7 +92,7 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
     code[j] = 0;
     if (gi < n) {
       g[j] = __ldg(&order[gi]);
-      code[j] = __ldg(&tiles[g[j]]);
+      code[j] = codes ? __ldg(&codes[gi]) : __ldg(&tiles[g[j]]);
     }
     sc += code_count(code[j]);
   }
@@ -122,8 +122,6 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
         if (staged) {
           s_kt[lpos] = tile;
           s_kg[lpos] = g[j];
-          atomicAdd(&s_hist[0][tile & 255u], 1u);
-          atomicAdd(&s_hist[1][(tile >> 8) & 255u], 1u);
         } else {
           emit_key(pos, tile, g[j], cap_k, out_tile, out_gid, s_hist, counters);
         }
@@ -131,8 +129,11 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
         ++lpos;
       }
     } else {
-      pos += code_count(code[j]);
-      lpos += code_count(code[j]);
+      const uint32_t cnt = code_count(code[j]);
+      if (staged)  // a big Gaussian's slots (emit_big_kernel writes them): not counted here
+        for (uint32_t q = 0; q < cnt; ++q) s_kt[lpos + q] = 0xFFFFFFFFu;
+      pos += cnt;
+      lpos += cnt;
     }
   }
   // ---- big Gaussians: appended to a global list (depth order clusters them in
@@ -148,16 +149,24 @@ __global__ __launch_bounds__(GUT_EMIT_THREADS) void emit_kernel(
   }
   __syncthreads();
   if (staged) {  // the CTA's run [prefix, prefix + total): a big Gaussian's slots hold
-                 // stale words here, overwritten by emit_big_kernel (launched after)
+                 // a sentinel here, overwritten by emit_big_kernel (launched after)
     const uint32_t lim = prefix < cap_k ? min(total, cap_k - prefix) : 0u;
+    // (the tile-digit histograms count only the keys written: a truncated
+    // list must not see more keys than it holds)
     for (uint32_t q = tid; q < lim; q += GUT_EMIT_THREADS) {
-      out_tile[prefix + q] = s_kt[q];
+      const uint32_t t = s_kt[q];
+      out_tile[prefix + q] = t;
       out_gid[prefix + q] = s_kg[q];
+      if (t != 0xFFFFFFFFu) {
+        atomicAdd(&s_hist[0][t & 255u], 1u);
+        atomicAdd(&s_hist[1][(t >> 8) & 255u], 1u);
+      }
     }
     if (lim < total && tid == 0) {
       counters[CNT_OVERFLOW] = 1u;
       counters[CNT_STICKY_OVERFLOW] = 1u;  // latched until the host reads it (gut_check)
     }
+    __syncthreads();  // (the histogram atomics above before the flush)
   }
   for (int jj = tid; jj < 512; jj += GUT_EMIT_THREADS) {
     const uint32_t v = (&s_hist[0][0])[jj];
@@ -300,13 +309,13 @@ __global__ __launch_bounds__(1024) void emit_scan_kernel(const uint32_t *n_vis_p
 void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper, const uint32_t *tiles,
                  const float4 *ell, const double2 *ell64, int tiles_x, int tile_cull, uint32_t *out_tile,
                  uint32_t *out_gid, uint32_t cap_k, uint32_t *counters, uint32_t *part_off, uint2 *big_list,
-                 cudaStream_t st) {
+                 cudaStream_t st, const uint32_t *codes) {
   if (n_upper == 0) return;
   unsigned blocks = (n_upper + GUT_EMIT_PART - 1) / GUT_EMIT_PART;
-  emit_count_kernel<<<blocks, GUT_EMIT_THREADS, 0, st>>>(order, n_vis, tiles, part_off);
+  if (!codes) emit_count_kernel<<<blocks, GUT_EMIT_THREADS, 0, st>>>(order, n_vis, tiles, part_off);
   emit_scan_kernel<<<1, 1024, 0, st>>>(n_vis, part_off);
   emit_kernel<<<blocks, GUT_EMIT_THREADS, 0, st>>>(order, n_vis, tiles, ell, ell64, tiles_x, tile_cull, out_tile, out_gid,
-                                                   cap_k, counters, part_off, big_list);
+                                                   cap_k, counters, part_off, big_list, codes);
   emit_big_kernel<<<148 * 4, GUT_EMIT_THREADS, 0, st>>>(big_list, ell, ell64, tiles_x, tile_cull, out_tile, out_gid,
                                                         cap_k, counters);
 }

@@ -62,7 +62,8 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, uint32_t *__restrict__ keys_out,
     uint32_t *__restrict__ vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
     const uint32_t *__restrict__ hist, unsigned long long *status, uint32_t *ticket,
-    const uint32_t *__restrict__ epoch_base, uint32_t epoch_off, uint2 *__restrict__ ranges) {
+    const uint32_t *__restrict__ epoch_base, uint32_t epoch_off, uint2 *__restrict__ ranges,
+    const uint32_t *__restrict__ codes_src, uint32_t *__restrict__ codes_out, uint32_t *__restrict__ part_tot) {
   constexpr int W = GUT_SORT_THREADS / 32;
   static_assert(GUT_SORT_THREADS >= 256, "one thread per digit");
   __shared__ uint32_t s_keys[GUT_SORT_PART];
@@ -168,7 +169,19 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     const uint32_t d = (k >> shift) & 255u;
     const uint32_t o = s_goff[d] + (p - s_loff[d]);
     if (keys_out) keys_out[o] = k;
-    vals_out[o] = s_vals[p];
+    const uint32_t v = s_vals[p];
+    vals_out[o] = v;
+    if (codes_out) {
+      // final depth pass (K2's inputs): the tile code of the Gaussian at depth
+      // position o, and the key total of each GUT_EMIT_PART-position partition
+      // (one atomic per run of equal partitions in the warp)
+      const uint32_t cd = __ldg(&codes_src[v]);
+      codes_out[o] = cd;
+      const uint32_t pp = o / GUT_EMIT_PART, am = __activemask();
+      const uint32_t peers = __match_any_sync(am, pp);
+      const uint32_t sum = __reduce_add_sync(peers, code_count(cd));
+      if ((threadIdx.x & 31) == __ffs(peers) - 1 && sum) atomicAdd(&part_tot[pp], sum);
+    }
     if (ranges) {
       // K4 fused into the final tile pass: a tile's keys are contiguous in this
       // CTA's run (the input is ordered by the lower digits) and in the output,
@@ -182,17 +195,18 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
 void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                       uint32_t *vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
                       const uint32_t *hist, unsigned long long *status, uint32_t *ticket,
-                      const uint32_t *epoch_base, uint32_t epoch_off, bool first, cudaStream_t st, uint2 *ranges) {
+                      const uint32_t *epoch_base, uint32_t epoch_off, bool first, cudaStream_t st, uint2 *ranges,
+                      const uint32_t *codes_src, uint32_t *codes_out, uint32_t *part_tot) {
   if (n_host == 0) return;
   unsigned blocks = (n_host + GUT_SORT_PART - 1) / GUT_SORT_PART;
   if (first)
     onesweep_kernel<true><<<blocks, GUT_SORT_THREADS, 0, st>>>(keys_in, vals_in, keys_out, vals_out, n_dev,
                                                                n_host, shift, hist, status, ticket, epoch_base,
-                                                               epoch_off, ranges);
+                                                               epoch_off, ranges, codes_src, codes_out, part_tot);
   else
     onesweep_kernel<false><<<blocks, GUT_SORT_THREADS, 0, st>>>(keys_in, vals_in, keys_out, vals_out, n_dev,
                                                                 n_host, shift, hist, status, ticket, epoch_base,
-                                                                epoch_off, ranges);
+                                                                epoch_off, ranges, codes_src, codes_out, part_tot);
 }
 
 // Start of a render (one launch): block 0 advances the device epoch base by
@@ -200,9 +214,10 @@ void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t
 // 22-bit epoch field wraps, every 2^19 renders), every thread empties one
 // tile range (start UINT_MAX, end 0) for the final tile pass to fill (K4).
 __global__ void frame_init_kernel(uint32_t *counters, unsigned long long *bstatus, size_t n, uint2 *ranges,
-                                  int n_tiles) {
+                                  int n_tiles, uint32_t *zero, int n_zero) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n_tiles) ranges[t] = make_uint2(0xFFFFFFFFu, 0u);
+  if (t < n_zero) zero[t] = 0u;
   if (blockIdx.x != 0) return;
   __shared__ uint32_t s_wrap;
   if (threadIdx.x == 0) {
@@ -216,9 +231,9 @@ __global__ void frame_init_kernel(uint32_t *counters, unsigned long long *bstatu
 }
 
 void launch_frame_init(uint32_t *counters, unsigned long long *bstatus, size_t n_bstatus, uint2 *ranges,
-                       int n_tiles, cudaStream_t st) {
-  const unsigned blocks = (unsigned)max(1, (n_tiles + 255) / 256);
-  frame_init_kernel<<<blocks, 256, 0, st>>>(counters, bstatus, n_bstatus, ranges, n_tiles);
+                       int n_tiles, uint32_t *zero, int n_zero, cudaStream_t st) {
+  const unsigned blocks = (unsigned)max(1, (max(n_tiles, n_zero) + 255) / 256);
+  frame_init_kernel<<<blocks, 256, 0, st>>>(counters, bstatus, n_bstatus, ranges, n_tiles, zero, n_zero);
 }
 
 }  // namespace gut

@@ -68,7 +68,10 @@ void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t
                       uint32_t *vals_out, const uint32_t *n_dev, uint32_t n_host, int shift,
                       const uint32_t *hist, unsigned long long *status, uint32_t *ticket,
                       const uint32_t *epoch_base, uint32_t epoch_off, bool first, cudaStream_t st,
-                      uint2 *ranges = nullptr);
+                      uint2 *ranges = nullptr, const uint32_t *codes_src = nullptr, uint32_t *codes_out = nullptr,
+                      uint32_t *part_tot = nullptr);
+// (final depth pass: codes_out[o] = codes_src[value] -- the K1 tile code in depth order -- and
+// part_tot[o / GUT_EMIT_PART] += its key count; part_tot zeroed by launch_frame_init)
 // Epochs per render: sort passes use base + 0..6 (depth 0-3, tile 4 and 6), the blend base + GUT_EPOCH_BLEND.
 #define GUT_EPOCHS_PER_RENDER 8u
 #define GUT_EPOCH_BLEND 7u
@@ -77,15 +80,17 @@ void launch_sort_pass(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t
 // n_bstatus, so a stale word can never alias the current render) and empties
 // the tile ranges that the final tile pass fills (K4).
 void launch_frame_init(uint32_t *counters, unsigned long long *bstatus, size_t n_bstatus, uint2 *ranges,
-                       int n_tiles, cudaStream_t st);
+                       int n_tiles, uint32_t *zero, int n_zero, cudaStream_t st);
 // (K4 is fused into the final tile pass: ranges != nullptr there; launch_frame_init empties them)
 
 // K2: per-partition key totals, their scan, then the emission (part_off:
 // one uint32 per GUT_EMIT_PART Gaussians of the upper bound n_upper)
+// (codes != nullptr: the tile codes in depth order with part_off already holding the
+// partition totals -- the final depth pass wrote both -- so only the scan and the emission run)
 void launch_emit(const uint32_t *order, const uint32_t *n_vis, uint32_t n_upper, const uint32_t *tiles,
                  const float4 *ell, const double2 *ell64, int tiles_x, int tile_cull, uint32_t *out_tile,
                  uint32_t *out_gid, uint32_t cap_k, uint32_t *counters, uint32_t *part_off, uint2 *big_list,
-                 cudaStream_t st);
+                 cudaStream_t st, const uint32_t *codes = nullptr);
 
 
 
