@@ -724,6 +724,12 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) start = min(start, __shfl_xor_sync(FULL, start, o));
+  bool anyp = false;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) anyp = anyp || pend[k];
+  const bool wpend = __any_sync(FULL, anyp);  // (only a re-run has dormant pixels)
+  uint32_t ck_next = s0 + ck_step;           // next checkpoint position (speculative pass)
+  int ck_idx = 0;
   if (start >= s1) {
 #pragma unroll
     for (int k = 0; k < NP; ++k) if (pend[k]) L.done[k] = false;  // (nothing left to walk: unchanged state)
@@ -744,10 +750,12 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   prime(start);
   for (uint32_t b0 = start; b0 < s1; b0 += 32, buf ^= 1) {
     bool anypend = false;
+    if (wpend) {
 #pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      if (pend[k] && actp[k] <= b0) { pend[k] = false; L.done[k] = false; }
-      anypend = anypend || pend[k];
+      for (int k = 0; k < NP; ++k) {
+        if (pend[k] && actp[k] <= b0) { pend[k] = false; L.done[k] = false; }
+        anypend = anypend || pend[k];
+      }
     }
     // speculative pass of a later segment: every 2 chunks, stop pixels whose
     // exact sequence has certainly terminated by now: T_spec times the bound of
@@ -757,19 +765,22 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
       for (int k = 0; k < NP; ++k)
         if (!L.done[k]) {
           const unsigned long long Lb = pred_L(poll_stat + 64 * k, poll_s, __ldg(B.epoch) + GUT_EPOCH_BLEND);
-          if (Lb >= GUT_L_DEAD || L.T[k] * exp2f(-(float)Lb * 2.3283064365386963e-10f) < t_min)
+          // (MUFU ex2: a pixel stopped here by a rounding error is re-run exactly
+          // from T_pre like any pixel that terminates in the segment)
+          if (Lb >= GUT_L_DEAD || L.T[k] * ex2_approx(-(float)Lb * 2.3283064365386963e-10f) < t_min)
             L.done[k] = L.term[k] = true;
         }
     }
-    if (ck && b0 > s0 && (b0 - s0) % ck_step == 0u) {
+    if (ck && b0 == ck_next) {  // (the speculative pass walks from s0 in steps of 32: no jumps)
+      ck_next += ck_step;
 #pragma unroll
       for (int k = 0; k < NP; ++k)
         if (!L.done[k]) {
-          const int c = (int)((b0 - s0) / ck_step) - 1;
-          ck->C[c][k] = make_float4(L.Cr[k], L.Cg[k], L.Cb[k], L.Dp[k]);
-          ck->T[c][k] = L.T[k];
-          ck->n[k] = c + 1;
+          ck->C[ck_idx][k] = make_float4(L.Cr[k], L.Cg[k], L.Cb[k], L.Dp[k]);
+          ck->T[ck_idx][k] = L.T[k];
+          ck->n[k] = ck_idx + 1;
         }
+      ++ck_idx;
     }
     all_done = true;
 #pragma unroll
