@@ -169,8 +169,18 @@ typedef enum {
                                entries visited, pairs evaluated, pairs contributing, re-ran);
                                all zero for units that did not run; only with env
                                GUT_BLEND_TRACE=1 */,
-  GUT_STAGE_COUNTERS = 7    /* uint32[64]: the render's device counters (diagnostics; layout
+  GUT_STAGE_COUNTERS = 7,   /* uint32[64]: the render's device counters (diagnostics; layout
                                internal, see csrc/launch.h CNT_*) */
+  GUT_STAGE_RAYS = 8        /* per tile: float4 (a, b, snorm, beta) [256] of the pixel rays
+                               relative to the tile anchor (PAPER L116 r(tau) = o + tau d; rays
+                               kernel layout: pixel (x, y) of the tile at index
+                               32 ((x >> 3) | ((y >> 2) << 1)) + 8 (y & 3) + (x & 7); snorm = 0
+                               marks an invalid pixel), then float[4][8] per 8x8 block b
+                               (x0 = 8 (b & 1), y0 = 8 (b >> 1)): {a00, ax, ay, rho_a, b00, bx,
+                               by, rho_b}, the affine lattice a(x, y) = a00 + ax x + ay y of the
+                               block's valid pixels (x, y = 0..7) with |residual| <= rho (rho =
+                               +inf: none) that K5's candidate masks rely on.  [n_tiles] records
+                               of 256 x 16 + 128 bytes */
 } gut_stage;
 
 typedef struct { /* GUT_STAGE_PROJECT record (K1 output, fp32) */

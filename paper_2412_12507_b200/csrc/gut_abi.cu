@@ -903,6 +903,7 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
     case GUT_STAGE_TILE_WORK: need = (size_t)ctx->last_tiles * 2 * sizeof(uint32_t); break;
     case GUT_STAGE_BLEND_TRACE: need = ctx->trace ? 2 * GUT_BLEND_WARPS * ctx->last_items * sizeof(uint4) : 0; break;
     case GUT_STAGE_COUNTERS: need = 64 * sizeof(uint32_t); break;
+    case GUT_STAGE_RAYS: need = (size_t)ctx->last_tiles * (GUT_TILE_PX * sizeof(float4) + 4 * 8 * sizeof(float)); break;
     default: return fail(ctx, GUT_E_INVALID_ARGUMENT, "stage");
   }
   if (bytes_needed) *bytes_needed = need;
@@ -950,6 +951,19 @@ gut_status gut_debug_copy_stage(gut_context *ctx, int32_t stage, void *host_dst,
     CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->counters, need, cudaMemcpyDeviceToHost));
   } else if (stage == GUT_STAGE_BLEND_TRACE) {
     CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->trace, need, cudaMemcpyDeviceToHost));
+  } else if (stage == GUT_STAGE_RAYS) {
+    const size_t nt = (size_t)ctx->last_tiles;
+    float4 *px = new float4[nt * GUT_TILE_PX + 1];
+    TileAnchor *an = new TileAnchor[nt + 1];
+    cudaMemcpy(px, ctx->pix, nt * GUT_TILE_PX * sizeof(float4), cudaMemcpyDeviceToHost);
+    cudaMemcpy(an, ctx->anchors, nt * sizeof(TileAnchor), cudaMemcpyDeviceToHost);
+    char *o = (char *)host_dst;
+    for (size_t t = 0; t < nt; ++t) {
+      memcpy(o, px + t * GUT_TILE_PX, GUT_TILE_PX * sizeof(float4));
+      memcpy(o + GUT_TILE_PX * sizeof(float4), an[t].fit, sizeof(an[t].fit));
+      o += GUT_TILE_PX * sizeof(float4) + sizeof(an[t].fit);
+    }
+    delete[] px; delete[] an;
   } else {
     CUDA_TRY(ctx, cudaMemcpy(host_dst, ctx->tile_work, need, cudaMemcpyDeviceToHost));
   }

@@ -20,7 +20,7 @@ STATUS = {0: "GUT_OK", 1: "GUT_E_INVALID_ARGUMENT", 2: "GUT_E_UNSUPPORTED", 3: "
 MODELS = {"pinhole": 0, "opencv": 1, "fisheye": 2, "ortho": 3}
 SHUTTERS = {"global": 0, "top_to_bottom": 1, "left_to_right": 2, "bottom_to_top": 3, "right_to_left": 4}
 STAGE_PROJECT, STAGE_DEPTH_ORDER, STAGE_SORTED, STAGE_RANGES, STAGE_TILE_WORK = 1, 2, 3, 4, 5
-STAGE_BLEND_TRACE, STAGE_COUNTERS = 6, 7
+STAGE_BLEND_TRACE, STAGE_COUNTERS, STAGE_RAYS = 6, 7, 8
 
 
 class gut_camera(C.Structure):
@@ -302,6 +302,9 @@ def gut_debug_copy_stage(ctx, stage: int):
                        ("depth", "<f4"), ("rgb", "<f4", 3), ("tiles", "<u4"), ("rect", "<u2", 4)])
         assert dt.itemsize == C.sizeof(gut_proj_record)
         return np.frombuffer(raw, dt).copy()
+    if stage == STAGE_RAYS:  # per tile: float4 [256] ray offsets, then float [4][8] block lattices
+        rec = np.frombuffer(raw, np.float32).reshape(-1, 256 * 4 + 32)
+        return rec[:, :1024].reshape(-1, 256, 4).copy(), rec[:, 1024:].reshape(-1, 4, 8).copy()
     arr = np.frombuffer(raw, np.uint32).copy()
     if stage in (STAGE_SORTED, STAGE_RANGES, STAGE_TILE_WORK):
         arr = arr.reshape(-1, 2)
