@@ -167,8 +167,16 @@ def roofline(stage_ms, work, peaks, builder=None):
 
 
 # ncu kernel names of the stages (profiles/<tag>_traffic.json, tools/profile_round.sh)
-NCU_NAMES = {"K5_blend": "blend_kernel<0>", "K1_project": "project_kernel<3, 0>", "K2_emit": "emit_kernel",
-             "K3_sort": "onesweep_kernel<0>"}
+# (K1: the fisheye instantiation <DEG, RS, MODEL> since round 2; older captures: <DEG, RS>)
+NCU_NAMES = {"K5_blend": ("blend_kernel<0>",), "K1_project": ("project_kernel<3, 0, 2>", "project_kernel<3, 0>"),
+             "K2_emit": ("emit_kernel",), "K3_sort": ("onesweep_kernel<0>",)}
+
+
+def _first(d, names):
+    for n in names:
+        if d.get(n):
+            return d[n]
+    return None
 
 
 def _traffic_files():
@@ -182,7 +190,7 @@ def load_traffic(stage):
     for f in reversed(_traffic_files()):
         try:
             d = json.load(open(f))
-            v = d["bytes_per_launch"].get(NCU_NAMES.get(stage, ""))
+            v = _first(d["bytes_per_launch"], NCU_NAMES.get(stage, ()))
             if v:
                 return float(v), os.path.relpath(f, ROOT)
         except Exception:
@@ -195,7 +203,7 @@ def load_ncu_metrics(stage):
     for f in reversed(_traffic_files()):
         try:
             d = json.load(open(f))
-            v = d.get("metrics", {}).get(NCU_NAMES.get(stage, ""))
+            v = _first(d.get("metrics", {}), NCU_NAMES.get(stage, ()))
             if v:
                 return dict(v, source=os.path.relpath(f, ROOT))
         except Exception:

@@ -677,6 +677,15 @@ __device__ __forceinline__ uint2 entry_mask(float F0, float Fa, float Fb, float 
   return m;
 }
 
+#ifndef GUT_K5_MASKS
+#define GUT_K5_MASKS 1  // candidate masks on/off (tuning switch)
+#endif
+#ifndef GUT_K5_MASK_MIN
+#define GUT_K5_MASK_MIN 2   // entries a chunk's masks must drop to stay on (tuning switch)
+#endif
+#ifndef GUT_K5_MASK_SKIP
+#define GUT_K5_MASK_SKIP 3  // chunks without masks after a chunk below GUT_K5_MASK_MIN
+#endif
 template <int MODE, int NP, int KB = 0>
 __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, uint32_t s0, uint32_t s1,
                                           LanePx<NP> &L, uint32_t &n_eval, uint32_t &n_contrib,
@@ -748,6 +757,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
     gnext = p + 32 + lane < s1 ? __ldg(&B.gids[p + 32 + lane]) : 0u;
   };
   prime(start);
+  int mk_skip = 0;  // chunks left without candidate masks (warp-uniform)
   for (uint32_t b0 = start; b0 < s1; b0 += 32, buf ^= 1) {
     bool anypend = false;
     if (wpend) {
@@ -946,10 +956,14 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
             t[3] = make_float4(Dab, Dbb, gs, gu);
             t[4] = make_float4(gv, k2, l2s, 0.f);
             t[5] = make_float4(p4.x, p4.y, p4.z, KB > 0 ? __uint_as_float(__ldg(&B.gids[kk])) : 0.f);
-            uint2 em = entry_mask(F0, Fa, Fb, Faa, Fab, Fbb, as, bs, A, Bm, mag, lds128(wc_s + 112),
-                                  lds128(wc_s + 128));
-            if (NP == 1) em = make_uint2(half ? em.y : em.x, 0u);
-            cmask = em;
+            if (GUT_K5_MASKS && mk_skip == 0) {
+              uint2 em = entry_mask(F0, Fa, Fb, Faa, Fab, Fbb, as, bs, A, Bm, mag, lds128(wc_s + 112),
+                                    lds128(wc_s + 128));
+              if (NP == 1) em = make_uint2(half ? em.y : em.x, 0u);
+              cmask = em;
+            } else {
+              cmask = make_uint2(~0u, NP > 1 ? ~0u : 0u);
+            }
           }
         }
       }
@@ -965,7 +979,13 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
       // only entries with a candidate pixel that is still live are evaluated
       const uint32_t live0 = __ballot_sync(FULL, !L.done[0]);
       const uint32_t live1 = NP > 1 ? __ballot_sync(FULL, !L.done[NP > 1 ? 1 : 0]) : 0u;
+      const uint32_t mb = m;
       m = __ballot_sync(FULL, maybe && ((cmask.x & live0) | (cmask.y & live1)) != 0u);
+      // adaptive: the masks cost ~150 warp-instructions a chunk and save ~30 per
+      // entry they drop; where a chunk drops fewer than GUT_K5_MASK_MIN entries
+      // (large footprints), the next GUT_K5_MASK_SKIP chunks go without
+      if (mk_skip > 0) --mk_skip;
+      else if (__popc(mb) - __popc(m) < GUT_K5_MASK_MIN) mk_skip = GUT_K5_MASK_SKIP;
     }
     __syncwarp();
     while (m) {
