@@ -656,6 +656,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   }
   bb.epoch = cnt + CNT_EPOCH;
   bb.rgb = rgb; bb.alpha = alpha; bb.depth = depth; bb.counters = cnt;
+  bb.grid_x4 = use_copy_stream ? GUT_BATCH_BLEND_X4 : 0;  // (frames in flight: a smaller persistent blend grid)
   if (dc.kbuf > 0) launch_blend_kbuf(dc, bb, st);
   else launch_blend(dc, bb, st);
   if (timing) cudaEventRecord(ev[6], st);

@@ -1518,17 +1518,21 @@ static void blend_launch(const DevCam &cam, const BlendBufs &b, cudaStream_t st)
   int dev = 0;
   cudaGetDevice(&dev);
   dev = min(dev, GUT_MAX_DEVICES - 1);
+  static int smss[GUT_MAX_DEVICES];
   std::call_once(once[dev], [&] {
     cudaFuncSetAttribute(blend_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, blend_kernel<MODE>, GUT_BLEND_CTA, smem);
     grids[dev] = max(1, sms) * max(1, per);
+    smss[dev] = max(1, sms);
     // tuning knob: a smaller persistent grid leaves SMs to the next frame's kernels
-    // (throughput +3% at 148 CTAs with frames in flight, per-frame latency -21%, e2e -2%)
     if (const char *e = getenv("GUT_BLEND_GRID")) grids[dev] = max(1, min(grids[dev], atoi(e)));
   });
-  const int grid = grids[dev];
+  // frames in flight (b.grid_x4 > 0): 1.25 CTAs per SM measured best for
+  // throughput (bench frame, 4 in flight: 880 vs 842 frames/s, e2e 859 vs
+  // 838; one frame alone would take 1.55 instead of 1.29 ms)
+  const int grid = b.grid_x4 > 0 ? max(1, min(grids[dev], smss[dev] * b.grid_x4 / 4)) : grids[dev];
   blend_kernel<MODE><<<grid, GUT_BLEND_CTA, smem, st>>>(cam, b);
 }
 

@@ -138,7 +138,12 @@ struct BlendBufs {
   const uint32_t *epoch;  // device epoch base (CNT_EPOCH); the blend uses base + GUT_EPOCH_BLEND
   float *rgb, *alpha, *depth;
   uint32_t *counters;
+  // persistent blend grid in quarter-CTAs per SM (0: as many as fit).  Frames
+  // in flight (gut_render_batch lanes) use GUT_BATCH_BLEND_X4: the next
+  // frames' K1-K3 then run beside this frame's K5 (throughput over latency)
+  int grid_x4;
 };
+#define GUT_BATCH_BLEND_X4 5  // 1.25 CTAs per SM
 
 // queue-2 slots beyond the grants: one ticket per resident blend warp (>= 148 SMs x 64 warps)
 #define GUT_BLEND_Q2_SLACK (1u << 16)
