@@ -109,13 +109,19 @@ __global__ __launch_bounds__(GUT_SORT_THREADS) void onesweep_kernel(
     const bool valid = rank[j] != 0;
     const uint32_t d = valid ? (key[j] >> shift) & 255u : (FIRST ? 256u : 255u);
 #if GUT_SORT_BALLOT
+    // peers = lanes with the same digit: per bit one predicate (bit test),
+    // one ballot and one predicated AND (4 instructions; the compiler's own
+    // form of "bit ? bal : ~bal" takes 6)
     uint32_t peers = 0xffffffffu;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const bool bit = (d >> b) & 1u;
-      const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-      peers &= bit ? bal : ~bal;
-    }
+    for (int b = 0; b < NB; ++b)
+      asm("{\n\t.reg .pred p;\n\t.reg .b32 t, bal;\n\t"
+          "and.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
+          "vote.sync.ballot.b32 bal, p, 0xffffffff;\n\t"
+          "@p and.b32 %0, %0, bal;\n\t"
+          "@!p lop3.b32 %0, %0, bal, 0, 0x30;\n\t}"
+          : "+r"(peers)
+          : "r"(d), "r"(1u << b));
 #else
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
 #endif
