@@ -481,9 +481,10 @@ def run_ours(args):
     dom = max(rl, key=lambda k: rl[k]["ms"])
     d = rl[dom]
     traffic, traffic_src = load_traffic(dom)
-    # frame init (epochs + empty ranges), K1 + wide, 4 depth passes, K2 (count, scan, emit, big), tile
-    # passes, plan (count, scan, fill), blend
-    launches_per_render = 1 + 2 + 4 + 4 + (2 if n_tiles > 256 else 1) + 3 + 1
+    # frame init (epochs + empty ranges), K1 + wide, 4 depth passes, K2 (scan, emit, big; the partition
+    # totals come from the final depth pass), tile passes, plan (count, scan, fill), blend -- 16 per
+    # render (the ncu launch list of the timed region, profiles/r2g_launches.csv: 64 for 4 steps)
+    launches_per_render = 1 + 2 + 4 + 3 + (2 if n_tiles > 256 else 1) + 3 + 1
     total_views = world * args.steps
     fps = total_views / (ms_max * 1e-3)
     line = {
