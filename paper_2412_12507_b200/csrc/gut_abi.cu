@@ -59,7 +59,14 @@ struct gut_context {
   size_t cap_items = 0;
   bool lut_valid = false;
   double lut_key[20] = {};
-  int blend_seg = 1536, blend_window = 2;  // K5 segment length and speculation window (tools/seg_sweep.sh)
+  // K5 segment length and speculation window: one frame at a time (latency:
+  // speculation shortens the densest tiles' critical path) and frames in flight
+  // (throughput: the other frames fill the GPU, so no speculation beyond the
+  // grants and a smaller persistent grid; DESIGN.md §5 "Scheduling")
+  // (one segment length for both: the split-list composition's rounding
+  // depends on it, and a batch must return exactly what single renders do)
+  int blend_seg = 2560, blend_window = 2;
+  int blend_window_batch = 1, batch_x4 = GUT_BATCH_BLEND_X4;
   bool reserved = false;
   std::vector<std::array<cudaEvent_t, 7>> tsets;  // per-render stage events (timing = 1)
   size_t tnext = 0;
@@ -340,6 +347,16 @@ gut_status gut_context_create(int32_t dev, gut_context **out) {
     int v = atoi(e);
     if (v >= 1 && v <= 255) ctx->blend_window = v;  // (queue-1 entries carry the segment in 8 bits)
   }
+  // frames in flight (gut_render_batch lanes): the window and the lanes'
+  // persistent blend grid in quarter-CTAs per SM
+  if (const char *e = getenv("GUT_BLEND_WINDOW_BATCH")) {
+    int v = atoi(e);
+    if (v >= 1 && v <= 255) ctx->blend_window_batch = v;
+  }
+  if (const char *e = getenv("GUT_BATCH_BLEND_X4")) {
+    int v = atoi(e);
+    if (v >= 1 && v <= 64) ctx->batch_x4 = v;
+  }
   if (cudaMalloc((void **)&ctx->counters, CNT_ALLOC * sizeof(uint32_t)) != cudaSuccess ||
       cudaMallocHost((void **)&ctx->h_counters, CNT_ALLOC * sizeof(uint32_t)) != cudaSuccess ||
       cudaMemset(ctx->counters, 0, CNT_ALLOC * sizeof(uint32_t)) != cudaSuccess) {
@@ -392,7 +409,8 @@ gut_status gut_workspace_reserve(gut_context *ctx, int64_t max_keys, int64_t max
   if ((s = ensure_pix(ctx, (size_t)max_w * max_h)) != GUT_OK) return s;
   // blend work items of either compositing order (segments of "Ours", 8x4
   // units of the k-buffer) so that a reserved render never allocates
-  const size_t items = std::max(tiles + (size_t)max_keys / (size_t)ctx->blend_seg + 2, 2 * tiles + 2);
+  const size_t items = std::max(tiles + (size_t)max_keys / (size_t)ctx->blend_seg + 2,
+                                2 * tiles + 2);
   if ((s = ensure_items(ctx, items)) != GUT_OK) return s;
   ctx->reserved = true;
   ctx->res_keys = max_keys; ctx->res_n = max_gaussians; ctx->res_w = max_w; ctx->res_h = max_h;
@@ -624,9 +642,11 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
       ctx->lut_valid = cacheable;
     }
   }
+  const int bseg = ctx->blend_seg;
+  const int bwin = use_copy_stream ? ctx->blend_window_batch : ctx->blend_window;
   // (k-buffer: one item per tile but twice the units per tile -> q1 needs 2 x n_tiles x GUT_BLEND_WARPS)
   const size_t max_items = dc.kbuf > 0 ? 2 * (size_t)dc.n_tiles + 2
-                                       : (size_t)dc.n_tiles + ctx->cap_k / (size_t)ctx->blend_seg + 2;
+                                       : (size_t)dc.n_tiles + ctx->cap_k / (size_t)bseg + 2;
   if ((s = ensure_items(ctx, max_items)) != GUT_OK) return s;
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->tile_work, 0, (size_t)dc.n_tiles * sizeof(uint2), st));
   const size_t n_units = (size_t)dc.n_tiles * GUT_BLEND_WARPS;
@@ -634,7 +654,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   if (dc.kbuf > 0)  // one segment per tile (the buffer state runs along the whole list), 8x4 units
     launch_plan(ctx->ranges, dc.n_tiles, 1 << 30, 1, ctx->seg_base, ctx->q1, cnt, st, GUT_KBUF_UNITS);
   else
-    launch_plan(ctx->ranges, dc.n_tiles, ctx->blend_seg, ctx->blend_window, ctx->seg_base, ctx->q1, cnt, st);
+    launch_plan(ctx->ranges, dc.n_tiles, bseg, bwin, ctx->seg_base, ctx->q1, cnt, st);
   BlendBufs bb;
   bb.ranges = ctx->ranges; bb.gids = fv; bb.payload = ctx->payload; bb.pix = ctx->pix; bb.anchors = ctx->anchors;
   bb.seg_base = ctx->seg_base; bb.granted = ctx->unit_ctr; bb.next_s = ctx->unit_ctr + n_units; bb.unit_done = ctx->unit_ctr + 2 * n_units;
@@ -642,7 +662,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   bb.q1 = ctx->q1; bb.q2 = ctx->q2;
   bb.status = ctx->bstatus;
   bb.part_c = ctx->part_c; bb.part_t = ctx->part_t;
-  bb.tile_work = ctx->tile_work; bb.seg = ctx->blend_seg; bb.window = ctx->blend_window; bb.n_tiles = dc.n_tiles;
+  bb.tile_work = ctx->tile_work; bb.seg = bseg; bb.window = bwin; bb.n_tiles = dc.n_tiles;
   bb.trace = nullptr;
   if (ctx->trace_on) {
     if (ctx->cap_trace < max_items) {
@@ -656,7 +676,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   }
   bb.epoch = cnt + CNT_EPOCH;
   bb.rgb = rgb; bb.alpha = alpha; bb.depth = depth; bb.counters = cnt;
-  bb.grid_x4 = use_copy_stream ? GUT_BATCH_BLEND_X4 : 0;  // (frames in flight: a smaller persistent blend grid)
+  bb.grid_x4 = use_copy_stream ? ctx->batch_x4 : 0;  // (frames in flight: a smaller persistent blend grid)
   if (dc.kbuf > 0) launch_blend_kbuf(dc, bb, st);
   else launch_blend(dc, bb, st);
   if (timing) cudaEventRecord(ev[6], st);
@@ -785,6 +805,8 @@ static gut_status ensure_lanes(gut_context *ctx, int n) {
     if (r != GUT_OK) return fail(ctx, r, "batch lane context");
     l->blend_seg = ctx->blend_seg;
     l->blend_window = ctx->blend_window;
+    l->blend_window_batch = ctx->blend_window_batch;
+    l->batch_x4 = ctx->batch_x4;
     l->frames_in_flight = 1;
     if (ctx->reserved && (r = gut_workspace_reserve(l, ctx->res_keys, ctx->res_n, ctx->res_w, ctx->res_h)) != GUT_OK) {
       gut_context_destroy(l);
