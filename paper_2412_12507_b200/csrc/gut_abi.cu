@@ -66,7 +66,7 @@ struct gut_context {
   // (one segment length for both: the split-list composition's rounding
   // depends on it, and a batch must return exactly what single renders do)
   int blend_seg = 2560, blend_window = 2;
-  int blend_window_batch = 1, batch_x4 = GUT_BATCH_BLEND_X4;
+  int blend_window_batch = 1, batch_x4 = GUT_BATCH_BLEND_X4, batch_grant_cap = 4;
   bool reserved = false;
   std::vector<std::array<cudaEvent_t, 7>> tsets;  // per-render stage events (timing = 1)
   size_t tnext = 0;
@@ -353,6 +353,7 @@ gut_status gut_context_create(int32_t dev, gut_context **out) {
     int v = atoi(e);
     if (v >= 1 && v <= 255) ctx->blend_window_batch = v;
   }
+  if (const char *e = getenv("GUT_BATCH_GRANT_CAP")) ctx->batch_grant_cap = std::max(0, atoi(e));
   if (const char *e = getenv("GUT_BATCH_BLEND_X4")) {
     int v = atoi(e);
     if (v >= 1 && v <= 64) ctx->batch_x4 = v;
@@ -677,6 +678,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
   bb.epoch = cnt + CNT_EPOCH;
   bb.rgb = rgb; bb.alpha = alpha; bb.depth = depth; bb.counters = cnt;
   bb.grid_x4 = use_copy_stream ? ctx->batch_x4 : 0;  // (frames in flight: a smaller persistent blend grid)
+  bb.grant_cap = use_copy_stream ? ctx->batch_grant_cap : 0;
   if (dc.kbuf > 0) launch_blend_kbuf(dc, bb, st);
   else launch_blend(dc, bb, st);
   if (timing) cudaEventRecord(ev[6], st);
@@ -807,6 +809,7 @@ static gut_status ensure_lanes(gut_context *ctx, int n) {
     l->blend_window = ctx->blend_window;
     l->blend_window_batch = ctx->blend_window_batch;
     l->batch_x4 = ctx->batch_x4;
+    l->batch_grant_cap = ctx->batch_grant_cap;
     l->frames_in_flight = 1;
     if (ctx->reserved && (r = gut_workspace_reserve(l, ctx->res_keys, ctx->res_n, ctx->res_w, ctx->res_h)) != GUT_OK) {
       gut_context_destroy(l);

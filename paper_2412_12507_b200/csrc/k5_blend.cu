@@ -1434,6 +1434,7 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
             const float rem = n_done * __logf(tmax / c.t_min) / decay;
             ahead = max(ahead, (int)fminf(rem / (float)B.seg + 1.f, (float)S));
           }
+          if (B.grant_cap > 0) ahead = min(ahead, B.grant_cap);  // (frames in flight: less speculation)
           // granted = g0 + extra (g0 = the up-front grants, extra zeroed per render)
           const uint32_t target = (uint32_t)min(S, s + 1 + ahead) - g0;
           uint32_t g = ld_volatile_u32(&B.granted[unit]);

@@ -142,6 +142,7 @@ struct BlendBufs {
   // in flight (gut_render_batch lanes) use GUT_BATCH_BLEND_X4: the next
   // frames' K1-K3 then run beside this frame's K5 (throughput over latency)
   int grid_x4;
+  int grant_cap;  // successor grants at most this many segments ahead (0: as the decay predicts)
 };
 #define GUT_BATCH_BLEND_X4 5  // 1.25 CTAs per SM
 
