@@ -195,3 +195,28 @@ def test_render_batch_stats_timing_overflow_and_errors(setup):
     gut.gut_check(small.ctx)  # (cleared on every lane)
     torch.cuda.synchronize()
     small.close()
+
+
+@pytest.mark.parametrize("window,cap,x4", [(1, 1, 4), (2, 0, 8), (3, 2, 5), (1, 4, 5)])
+def test_batch_scheduling_is_result_neutral(setup, window, cap, x4, monkeypatch):
+    """The frames-in-flight blend schedule (speculation window, successor
+    grant cap, persistent grid) changes only who computes what when: with
+    short segments (most tiles split, so speculation, look-back, re-runs and
+    grants all happen) a batch returns exactly the single renders' images."""
+    import torch
+    from paper_2412_12507_b200 import gut
+    monkeypatch.setenv("GUT_BLEND_SEG", "256")
+    monkeypatch.setenv("GUT_BLEND_WINDOW_BATCH", str(window))
+    monkeypatch.setenv("GUT_BATCH_GRANT_CAP", str(cap))
+    monkeypatch.setenv("GUT_BATCH_BLEND_X4", str(x4))
+    scene, cams = setup
+    ref = _one_by_one(scene, cams)
+    r = gut.Renderer(scene, max_wh=(cams[0].width, cams[0].height))
+    gut.gut_context_set_frames_in_flight(r.ctx, 3)
+    bufs, outs = _outs(torch, cams)
+    gut.gut_render_batch(r.ctx, r.scene, [gut.make_camera(c) for c in cams], gut.make_options(), outs)
+    torch.cuda.synchronize()
+    for (a, b) in zip(ref, bufs):
+        for x, y in zip(a, b):
+            assert torch.equal(x, y)
+    r.close()
