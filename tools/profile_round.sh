@@ -16,7 +16,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include 
     --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 4 --warmup 5 --no-cpu-baseline --sorted-k 0 --no-backward \
     > gpurun_out/${tag}_launches.log 2>&1
 # second render of view 1: skip the scene pack + the first render (18 kernels + the ray table)
-ncu --set full --clock-control none -s 20 -c 18 -o gpurun_out/${tag}_full \
+ncu --set full --clock-control none -s 18 -c 16 -o gpurun_out/${tag}_full \
     python tools/render_view.py 1 2 > gpurun_out/${tag}_full.log 2>&1
 fi
 if [ "$part" = configs ] || [ "$part" = all ]; then
