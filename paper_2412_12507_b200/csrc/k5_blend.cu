@@ -1104,6 +1104,9 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
   __syncwarp();
 }
 
+#ifndef GUT_BLEND_WAIT_NS
+#define GUT_BLEND_WAIT_NS 2048  // longest back-off of a warp waiting for a granted segment (tuning switch)
+#endif
 // Work queue (lane 0 of a warp).  Queue 2 (granted successors of running
 // chains) is served before queue 1 (initial grants).  Both hand out tickets
 // with one atomicAdd (no CAS retry storms among thousands of warps); a warp
@@ -1143,7 +1146,7 @@ __device__ bool fetch_work(const BlendBufs &B, uint32_t n_init, int &unit, int &
       uint32_t u1;
       for (int k = 0; (u1 = ld_volatile_u32(&B.q2[t2])) == 0; ++k) {
         if ((k & 3) == 3 && ld_volatile_u32(&cnt[CNT_Q_FINISHED]) >= n_units) return false;
-        __nanosleep(k < 2 ? 128 : (k < 6 ? 512 : 2048));
+        __nanosleep(k < 2 ? 128 : (k < 6 ? 512 : GUT_BLEND_WAIT_NS));
       }
       B.q2[t2] = 0;  // slot reusable by the next render
       unit = (int)(u1 - 1);

@@ -149,7 +149,9 @@ struct BlendBufs {
 // queue-2 slots beyond the grants: one ticket per resident blend warp (>= 148 SMs x 64 warps)
 #define GUT_BLEND_Q2_SLACK (1u << 16)
 // blend warps allowed to wait for future grants once queue 1 is drained
+#ifndef GUT_BLEND_MAX_WAITERS
 #define GUT_BLEND_MAX_WAITERS 768u
+#endif
 
 void launch_blend(const DevCam &cam, const BlendBufs &b, cudaStream_t st);
 // "Ours (sorted)": per-ray MLAB k-buffer of cam.kbuf hits (1, 2, 4, 8, 16), queue 1
