@@ -66,6 +66,7 @@ struct gut_context {
   // (one segment length for both: the split-list composition's rounding
   // depends on it, and a batch must return exactly what single renders do)
   int blend_seg = 2560, blend_window = 2;
+  int blend_seg_rs = 2048;  // rolling-shutter frames (Waymo-shaped: 0.847 vs 0.889 ms at 2560)
   int blend_window_batch = 1, batch_x4 = GUT_BATCH_BLEND_X4, batch_grant_cap = 4;
   bool reserved = false;
   std::vector<std::array<cudaEvent_t, 7>> tsets;  // per-render stage events (timing = 1)
@@ -341,7 +342,7 @@ gut_status gut_context_create(int32_t dev, gut_context **out) {
   if (const char *e = getenv("GUT_BLEND_TRACE")) ctx->trace_on = atoi(e) != 0;
   if (const char *e = getenv("GUT_BLEND_SEG")) {  // tuning knob: list entries per blend work item
     int v = atoi(e);
-    if (v >= 256 && v % 256 == 0) ctx->blend_seg = v;
+    if (v >= 256 && v % 256 == 0) ctx->blend_seg = ctx->blend_seg_rs = v;
   }
   if (const char *e = getenv("GUT_BLEND_WINDOW")) {  // tuning knob: speculative segments in flight per tile
     int v = atoi(e);
@@ -410,7 +411,7 @@ gut_status gut_workspace_reserve(gut_context *ctx, int64_t max_keys, int64_t max
   if ((s = ensure_pix(ctx, (size_t)max_w * max_h)) != GUT_OK) return s;
   // blend work items of either compositing order (segments of "Ours", 8x4
   // units of the k-buffer) so that a reserved render never allocates
-  const size_t items = std::max(tiles + (size_t)max_keys / (size_t)ctx->blend_seg + 2,
+  const size_t items = std::max(tiles + (size_t)max_keys / (size_t)std::min(ctx->blend_seg, ctx->blend_seg_rs) + 2,
                                 2 * tiles + 2);
   if ((s = ensure_items(ctx, items)) != GUT_OK) return s;
   ctx->reserved = true;
@@ -643,7 +644,7 @@ static gut_status render_one(gut_context *ctx, const gut_scene *scene, const gut
       ctx->lut_valid = cacheable;
     }
   }
-  const int bseg = ctx->blend_seg;
+  const int bseg = dc.shutter != SH_GLOBAL ? ctx->blend_seg_rs : ctx->blend_seg;
   const int bwin = use_copy_stream ? ctx->blend_window_batch : ctx->blend_window;
   // (k-buffer: one item per tile but twice the units per tile -> q1 needs 2 x n_tiles x GUT_BLEND_WARPS)
   const size_t max_items = dc.kbuf > 0 ? 2 * (size_t)dc.n_tiles + 2
@@ -806,6 +807,7 @@ static gut_status ensure_lanes(gut_context *ctx, int n) {
     gut_status r = gut_context_create(ctx->device, &l);
     if (r != GUT_OK) return fail(ctx, r, "batch lane context");
     l->blend_seg = ctx->blend_seg;
+    l->blend_seg_rs = ctx->blend_seg_rs;
     l->blend_window = ctx->blend_window;
     l->blend_window_batch = ctx->blend_window_batch;
     l->batch_x4 = ctx->batch_x4;
