@@ -152,9 +152,13 @@ __global__ __launch_bounds__(256, GUT_K6_MINB) void backward_kernel(DevCam c, Bw
       const float rn0 = fmaf(M[0], M[0], fmaf(M[1], M[1], M[2] * M[2]));
       const float rn1 = fmaf(M[3], M[3], fmaf(M[4], M[4], M[5] * M[5]));
       const float rn2 = fmaf(M[6], M[6], fmaf(M[7], M[7], M[8] * M[8]));
-      const float r012 = rn0 * rn1 * rn2, dM = r012 * rsqrtf(r012);
+      // (MUFU rsqrt / rcp as K5's staging: the same c0 and hit decisions)
+      float r012 = rn0 * rn1 * rn2, rq;
+      asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rq) : "f"(r012));
+      const float dM = r012 * rq;
+      const float irn0 = rs_rcp(rn0), irn1 = rs_rcp(rn1), irn2 = rs_rcp(rn2);
       const f3 Mx = mv(M, x);
-      const f3 c0 = mk(Mx.x * (dM / rn0), Mx.y * (dM / rn1), Mx.z * (dM / rn2));
+      const f3 c0 = mk(Mx.x * (dM * irn0), Mx.y * (dM * irn1), Mx.z * (dM * irn2));
       const f3 ogf = mv(M, tof(wv)), e0 = mv(M, Df), U = mv(M, T1f), V = mv(M, T2f);
       const f3 P = cross(ogf, U), Q = cross(ogf, V);
       const float k2 = p1.z;
@@ -168,9 +172,9 @@ __global__ __launch_bounds__(256, GUT_K6_MINB) void backward_kernel(DevCam c, Bw
       t[5] = make_float4(dot(ogf, e0), dot(ogf, U), dot(ogf, V), __uint_as_float(gid));
       t[6] = make_float4(p4.x, p4.y, p4.z, 0.f);
       // M^-1 = R S: (M^-1)_jk = M_kj / |M_k|^2
-      t[7] = make_float4(M[0] / rn0, M[3] / rn1, M[6] / rn2, M[1] / rn0);
-      t[8] = make_float4(M[4] / rn1, M[7] / rn2, M[2] / rn0, M[5] / rn1);
-      t[9] = make_float4(M[8] / rn2, 0.f, 0.f, 0.f);
+      t[7] = make_float4(M[0] * irn0, M[3] * irn1, M[6] * irn2, M[1] * irn0);
+      t[8] = make_float4(M[4] * irn1, M[7] * irn2, M[2] * irn0, M[5] * irn1);
+      t[9] = make_float4(M[8] * irn2, 0.f, 0.f, 0.f);
       if (MODE == 2) {  // o_g(beta) = o_g + beta m, m = M dc: n += beta (h + a PU + b QV), g += beta (m.d_g)
         const f3 m = mv(M, dcw);
         const f3 h = cross(m, e0), PU = cross(m, U), QV = cross(m, V);
@@ -181,8 +185,9 @@ __global__ __launch_bounds__(256, GUT_K6_MINB) void backward_kernel(DevCam c, Bw
       // conservative cull against the warp's pixel box (triangle inequality,
       // 1e-3 margin): omega^2 > k^2 on the whole box -> no pixel can hit
       const f3 n0 = c0 + ac * P + bc * Q, e0c = e0 + ac * U + bc * V;
-      const float lo = sqrtf(dot(n0, n0)) - (ra * sqrtf(dot(P, P)) + rb * sqrtf(dot(Q, Q)));
-      const float hi = sqrtf(dot(e0c, e0c)) + (ra * sqrtf(dot(U, U)) + rb * sqrtf(dot(V, V)));
+      // (MUFU square roots: 2^-22 relative, inside the 1e-3 margin)
+      const float lo = rs_sqrt(dot(n0, n0)) - (ra * rs_sqrt(dot(P, P)) + rb * rs_sqrt(dot(Q, Q)));
+      const float hi = rs_sqrt(dot(e0c, e0c)) + (ra * rs_sqrt(dot(U, U)) + rb * rs_sqrt(dot(V, V)));
       maybe = MODE == 2 || !(lo > 0.f && lo * lo > 1.001f * k2 * (hi * hi));  // (RS: every entry kept, as K5)
     }
     uint32_t msk = __ballot_sync(FULL, maybe);
@@ -211,7 +216,7 @@ __global__ __launch_bounds__(256, GUT_K6_MINB) void backward_kernel(DevCam c, Bw
       bool ok = !done && N <= f0.w * Dd;
       if (!__any_sync(FULL, ok)) continue;
       const float4 f5 = t[5], cc = t[6];
-      const float rD = 1.f / Dd;
+      const float rD = rs_rcp(Dd);  // (MUFU, as K5)
       const float w2 = N * rD;
       float pw = w2;  // (omega^2)^(n/2)
       if (gen) pw = ex2f_(khn * __log2f(w2));
@@ -232,7 +237,7 @@ __global__ __launch_bounds__(256, GUT_K6_MINB) void backward_kernel(DevCam c, Bw
           const float wgt = al * T;
           const float gi = cc.x * gr + cc.y * gg + cc.z * gb + tau * gD;
           Gpre = fmaf(wgt, gi, Gpre);
-          const float dal = T * gi - (Gtot - Gpre) / (1.f - al);
+          const float dal = T * gi - (Gtot - Gpre) * rs_rcp(1.f - al);
           const bool clamped = raw > c.alpha_max;
           // d alpha / d omega^2 = -(1/2) lambda_n (n/2) (omega^2)^(n/2 - 1) alpha (n = 2: -alpha/2)
           const float dadw = gen ? (w2 > 0.f ? -0.5f * c.klam * khn * pw / w2 * raw : 0.f) : -0.5f * raw;
