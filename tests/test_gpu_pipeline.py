@@ -220,3 +220,31 @@ def test_batch_scheduling_is_result_neutral(setup, window, cap, x4, monkeypatch)
         for x, y in zip(a, b):
             assert torch.equal(x, y)
     r.close()
+
+
+def test_bench_launch_configuration_full_size():
+    """bench.py times gut_render_batch (4 frames in flight: window-1 blend on the
+    1.25-CTA/SM grid, capacity mode) on the full 3M-Gaussian fisheye frames;
+    the parity tests check single renders of those frames against the oracle.
+    This ties the two: at full size the batch returns exactly the single
+    renders' images (RGB, alpha, depth)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2412_12507_b200 import gut
+    scene = S.make_scene("multiview")
+    cams = S.make_views("multiview")[:4]
+    r = gut.Renderer(scene, reserve_keys=8_000_000, max_wh=(cams[0].width, cams[0].height))
+    ref = []
+    for c in cams:
+        rgb, a, d, _ = r.render(c)
+        ref.append((rgb.clone(), a.clone(), d.clone()))
+    gut.gut_context_set_frames_in_flight(r.ctx, 4)
+    bufs, outs = _outs(torch, cams)
+    gut.gut_render_batch(r.ctx, r.scene, [gut.make_camera(c) for c in cams], gut.make_options(), outs)
+    torch.cuda.synchronize()
+    for (a, b) in zip(ref, bufs):
+        for x, y in zip(a, b):
+            assert torch.equal(x, y)
+    gut.gut_check(r.ctx)
+    r.close()
