@@ -119,6 +119,7 @@ __device__ __forceinline__ f3 cam_point_at(const DevCam &c, f3 y, f3 w, float t)
 // (0.5, rho(g(x; pose(0.5)))) until the pixel moves < rs_tol_px.
 // (one out-of-line copy: the seven inlined secant loops of a Gaussian overflow
 // the instruction cache -- ncu: 40% "no instruction" stalls in rolling shutter)
+template <int MODEL>
 __device__ __noinline__ bool project_sigma_rs(const DevCam &c, f3 y, f3 w, float &du, float &dv, float &t_out);
 // RS: the rolling-shutter instantiation of K1 (project_kernel<DEG, true>); the
 // global-shutter one never contains the shutter solve
@@ -129,14 +130,15 @@ __device__ __forceinline__ bool project_sigma(const DevCam &c, f3 y, f3 w, float
     t_out = 0.f;
     return project_cam_f<MODEL>(c, y, du, dv);
   }
-  return project_sigma_rs(c, y, w, du, dv, t_out);
+  return project_sigma_rs<MODEL>(c, y, w, du, dv, t_out);
 }
+template <int MODEL>
 __device__ __noinline__ bool project_sigma_rs(const DevCam &c, f3 y, f3 w, float &du, float &dv, float &t_out) {
   float t0 = 0.5f, u0, v0;
-  if (!project_cam_f(c, cam_point_at(c, y, w, t0), u0, v0)) return false;
+  if (!project_cam_f<MODEL>(c, cam_point_at(c, y, w, t0), u0, v0)) return false;
   float f0 = shutter_coord(c, u0, v0) - t0;
   float t1 = t0 + f0, u1, v1;
-  if (!project_cam_f(c, cam_point_at(c, y, w, t1), u1, v1)) return false;
+  if (!project_cam_f<MODEL>(c, cam_point_at(c, y, w, t1), u1, v1)) return false;
   float f1 = shutter_coord(c, u1, v1) - t1;
   // stop when the pixel moved less than the tolerance -- or than fp32 can
   // resolve at this pixel position (4 ulps), beyond which steps are noise -- or
@@ -149,7 +151,7 @@ __device__ __noinline__ bool project_sigma_rs(const DevCam &c, f3 y, f3 w, float
     float t2 = fabsf(den) > 1e-12f ? t1 - f1 * (t1 - t0) * __frcp_rn(den) : t1 + f1;
     t2 = fminf(fmaxf(t2, 0.f), 1.f);
     t0 = t1; u0 = u1; v0 = v1; f0 = f1; t1 = t2;
-    if (!project_cam_f(c, cam_point_at(c, y, w, t1), u1, v1)) return false;
+    if (!project_cam_f<MODEL>(c, cam_point_at(c, y, w, t1), u1, v1)) return false;
     f1 = shutter_coord(c, u1, v1) - t1;
   }
   du = u1; dv = v1; t_out = t1;
@@ -639,14 +641,24 @@ __global__ __launch_bounds__(256) void project_prefilter_kernel(DevCam c, SceneD
   if (keep) list[base + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)i;
 }
 
-// one SH degree: the rolling-shutter K1 (compacted list) reads the camera model
-// at run time; the global-shutter K1 is instantiated per camera model
+// one SH degree: K1 instantiated per camera model and shutter (the rolling-
+// shutter one over the pre-filter's compacted list)
 template <int DEG>
 static void launch_k1_deg(const DevCam &cam, const SceneDev &s, uint32_t *dkey, uint32_t *tiles, float4 *ell,
                           double2 *ell64, float4 *payload, uint32_t *counters, uint32_t *deferred, uint32_t *list,
                           unsigned blocks, unsigned wblocks, cudaStream_t st) {
-  if (list) {
-    project_kernel<DEG, true, -1><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+  if (list) {  // rolling shutter (compacted list); ortho never takes the pre-filter path
+    switch (cam.model) {
+      case CAM_PINHOLE:
+        project_kernel<DEG, true, CAM_PINHOLE><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+        break;
+      case CAM_OPENCV:
+        project_kernel<DEG, true, CAM_OPENCV><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+        break;
+      default:
+        project_kernel<DEG, true, CAM_FISHEYE><<<blocks, 256, 0, st>>>(cam, s, dkey, tiles, ell, payload, counters, deferred, list);
+        break;
+    }
   } else {
     switch (cam.model) {
       case CAM_PINHOLE:
