@@ -36,6 +36,27 @@ def main():
                         rgb, a, d, _ = r.render(cam, o)
                         print(f"tiny {v} s{seed} d{deg} kb{kb} kd{kd}", dig(rgb, a, d), flush=True)
                 r.close()
+    # stress scenes: the tiny cameras with Gaussians rescaled to extremes --
+    # sub-pixel dust, needles (one long axis), large flat splats near the
+    # camera, opacities at alpha_min -- where conservative culls are tightest
+    for v in S.TINY_VARIANTS:
+        for seed in range(4):
+            scene, cam = S.tiny(100 + seed, v, n=512, size=96, sh_degree=1)
+            rng = np.random.default_rng(seed)
+            sc = scene.scales.copy()
+            kind = rng.integers(0, 4, size=len(sc))
+            sc[kind == 0] *= 0.05                                        # dust
+            sc[kind == 1] *= np.array([8.0, 0.05, 0.05], np.float32)     # needles
+            sc[kind == 2] *= np.array([6.0, 6.0, 0.02], np.float32)      # flat splats
+            op = scene.opacities.copy()
+            op[kind == 3] = np.float32(1.0 / 255.0) * np.float32(1.0001)  # at alpha_min
+            scene.scales = sc.astype(np.float32)
+            scene.opacities = op.astype(np.float32)
+            r = gut.Renderer(scene)
+            for kb in (0, 4):
+                rgb, a, d, _ = r.render(cam, S.RenderOptions(kbuffer=kb))
+                print(f"stress {v} s{seed} kb{kb}", dig(rgb, a, d), flush=True)
+            r.close()
     cfgs = [("multiview", 4 if full else 1), ("mipnerf360", 2), ("scannetpp", 2), ("waymo", 2)]
     for cfg, nv in cfgs:
         scene = S.make_scene(cfg, None if full else 200_000)
