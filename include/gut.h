@@ -248,8 +248,9 @@ typedef struct {
  * rgb/alpha/depth: the forward's device outputs ([H][W][3], [H][W], [H][W]);
  * grad_rgb [H][W][3] required, grad_alpha / grad_depth nullable (zero); depth
  * is required when grad_depth is given.  All pointers device memory on the
- * context's device; asynchronous on s.  Per-Gaussian sums use fp32 atomics
- * (reproducible to rounding, not bitwise).  Supported: PINHOLE / OPENCV /
+ * context's device; asynchronous on s.  Per-Gaussian sums accumulate in 32.32
+ * fixed point (int64 atomics; resolution 2^-32 per term, range +-2^31): the
+ * gradients are bitwise reproducible.  Supported: PINHOLE / OPENCV /
  * FISHEYE with any shutter and kernel_degree, kbuffer 0; otherwise
  * GUT_E_UNSUPPORTED.  It differentiates ctx's LAST render (its sorted lists
  * and workspace): a camera / options mismatch with that render gives

@@ -77,7 +77,8 @@ struct gut_context {
   const uint32_t *last_order = nullptr, *last_keys = nullptr, *last_vals = nullptr;
   DevCam last_cam;                    // (gut_render_backward: must match)
   const gut_scene *last_scene = nullptr;
-  float *gacc = nullptr;              // K6 accumulators (16 per Gaussian) + centre shutter times (1 per Gaussian)
+  long long *gacc = nullptr;          // K6 fixed-point accumulators (16 per Gaussian)
+  float *gt0 = nullptr;               // K6 centre shutter times (1 per Gaussian)
   size_t cap_gacc = 0;
   // gut_render_batch: frames in flight -- lane 0 is this context on the
   // caller's stream, lanes 1.. are child contexts (own workspaces) on their
@@ -387,7 +388,7 @@ void gut_context_destroy(gut_context *ctx) {
                 ctx->sb_k, ctx->sb_v,
                 ctx->ka, ctx->va, ctx->kb, ctx->vb, ctx->ranges, ctx->tile_work, ctx->img, ctx->st_depth,
                 ctx->st_emit, ctx->st_tile, ctx->counters, ctx->pix, ctx->anchors, ctx->seg_base, ctx->unit_ctr, ctx->q1, ctx->q2,
-                ctx->bstatus, ctx->part_c, ctx->part_t, ctx->trace, ctx->gacc};
+                ctx->bstatus, ctx->part_c, ctx->part_t, ctx->trace, ctx->gacc, ctx->gt0};
   for (void *p : ps) if (p) cudaFree(p);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
   for (auto &set : ctx->tsets)
@@ -763,8 +764,11 @@ gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const g
   const int64_t N = scene->d.n;
   if (ctx->cap_gacc < (size_t)N) {
     if (ctx->gacc) cudaFree(ctx->gacc);
+    if (ctx->gt0) cudaFree(ctx->gt0);
     ctx->gacc = nullptr;
-    CUDA_TRY(ctx, cudaMalloc(&ctx->gacc, (size_t)17 * (N > 0 ? N : 1) * sizeof(float)));
+    ctx->gt0 = nullptr;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->gacc, (size_t)16 * (N > 0 ? N : 1) * sizeof(long long)));
+    CUDA_TRY(ctx, cudaMalloc(&ctx->gt0, (size_t)(N > 0 ? N : 1) * sizeof(float)));
     ctx->cap_gacc = (size_t)N;
   }
   BwdBufs b;
@@ -773,7 +777,7 @@ gut_status gut_render_backward(gut_context *ctx, const gut_scene *scene, const g
   b.rgb = rgb; b.alpha = alpha; b.depth = depth; b.g_rgb = grad_rgb; b.g_alpha = grad_alpha; b.g_depth = grad_depth;
   b.acc = ctx->gacc;
   b.order = ctx->q1; b.seg_base = ctx->seg_base; b.counters = ctx->counters;  // (forward plan scratch, reused)
-  b.t0 = dc.shutter != GUT_SHUTTER_GLOBAL ? ctx->gacc + (size_t)16 * (N > 0 ? N : 1) : nullptr;
+  b.t0 = dc.shutter != GUT_SHUTTER_GLOBAL ? ctx->gt0 : nullptr;
   b.d_means = grads->means; b.d_rots = grads->rotations; b.d_scales = grads->scales; b.d_opac = grads->opacities;
   b.d_sh = grads->sh; b.d_rgb = grads->rgb; b.densify = grads->densify;
   launch_backward(dc, scene->d, b, (cudaStream_t)s);

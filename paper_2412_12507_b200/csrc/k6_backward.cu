@@ -270,7 +270,10 @@ __global__ __launch_bounds__(256, GUT_K6_MINB) void backward_kernel(DevCam c, Bw
       // and the 16 even lanes issue one atomic each (one instruction)
       {
         const float s = reduce16(v, lane);
-        if ((lane & 1) == 0) atomicAdd(B.acc + (size_t)16 * __float_as_uint(f5.w) + (lane >> 1), s);
+        // 32.32 fixed point (cvt saturates beyond +-2^31): deterministic sums
+        if ((lane & 1) == 0)
+          atomicAdd(reinterpret_cast<unsigned long long *>(B.acc + (size_t)16 * __float_as_uint(f5.w) + (lane >> 1)),
+                    (unsigned long long)__float2ll_rn(s * (float)GUT_BWD_FIX));
       }
     }
   }
@@ -286,7 +289,7 @@ __global__ __launch_bounds__(256) void backward_finish_kernel(DevCam c, SceneDev
   const bool vis = B.tiles[i] != 0;
   float acc[16];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) acc[q] = vis ? B.acc[16 * i + q] : 0.f;
+  for (int q = 0; q < 16; ++q) acc[q] = vis ? (float)((double)B.acc[16 * i + q] * (1.0 / GUT_BWD_FIX)) : 0.f;
   const float4 po = s.pos_opa[i], ro = s.rot[i], sc = s.scale[i];
   const float qn = sqrtf(ro.x * ro.x + ro.y * ro.y + ro.z * ro.z + ro.w * ro.w);
   const float qw = ro.x / qn, qx = ro.y / qn, qy = ro.z / qn, qz = ro.w / qn;
@@ -350,7 +353,7 @@ __global__ __launch_bounds__(256) void backward_finish_kernel(DevCam c, SceneDev
 
 void launch_backward(const DevCam &cam, const SceneDev &s, const BwdBufs &b, cudaStream_t st) {
   if (b.t0) launch_centre_times(cam, s, const_cast<float *>(b.t0), st);
-  cudaMemsetAsync(b.acc, 0, (size_t)16 * s.n * sizeof(float), st);
+  cudaMemsetAsync(b.acc, 0, (size_t)16 * s.n * sizeof(long long), st);
   // queue-1 order of the tiles, longest list first (plan kernels, one unit per tile)
   cudaMemsetAsync(b.counters + CNT_PLAN_HIST, 0, 1024 * sizeof(uint32_t), st);
   launch_plan(b.ranges, cam.n_tiles, 1 << 30, 1, b.seg_base, b.order, b.counters, st, 1);

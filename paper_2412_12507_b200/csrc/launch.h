@@ -168,7 +168,10 @@ struct BwdBufs {
   const uint32_t *tiles;        // K1 tile code (0 = culled)
   const float *rgb, *alpha, *depth;          // forward outputs (device)
   const float *g_rgb, *g_alpha, *g_depth;    // upstream gradients (device; alpha / depth nullable)
-  float *acc;                   // per Gaussian 16 fp32 accumulators
+  // per Gaussian 16 accumulators in 32.32 fixed point (int64, two's
+  // complement): integer additions commute, so the gradients are bitwise
+  // reproducible whatever order the atomics land in
+  long long *acc;
   uint32_t *order;              // tiles, longest list first (plan queue 1, n_tiles entries)
   uint32_t *seg_base;           // plan scratch (n_tiles)
   uint32_t *counters;           // the context's counters block (plan histogram)
@@ -176,6 +179,7 @@ struct BwdBufs {
   float *d_means, *d_rots, *d_scales, *d_opac, *d_sh, *d_rgb;  // outputs (d_rgb nullable)
   float *densify;               // nullable: |dL/dmu| / (distance / 2)
 };
+#define GUT_BWD_FIX 4294967296.0  // fixed-point scale of the K6 accumulators (2^32)
 void launch_backward(const DevCam &cam, const SceneDev &s, const BwdBufs &b, cudaStream_t st);
 // per Gaussian the shutter time of its centre (k1_project.cu; SH direction under rolling shutter)
 void launch_centre_times(const DevCam &cam, const SceneDev &s, float *t0, cudaStream_t st);
