@@ -286,9 +286,14 @@ gut_status gut_projection_quality(gut_context *ctx, const gut_scene *scene, cons
  * lanes 1..F-1 are child contexts (own workspaces, reserved like ctx, created
  * on first use and owned by ctx) on their own streams, forked from and joined
  * back to s with events, so the call stays asynchronous on s and every output
- * is complete when s reaches the point after the call.  Results are identical
- * to rendering the views one by one.  With stats != NULL the views are
- * rendered one at a time on s and stats[i] filled (synchronising). */
+ * is complete when s reaches the point after the call.  Pipelined frames run
+ * the blend (K5) in a throughput schedule -- no speculative segments beyond
+ * the successor grants, grants at most 4 segments ahead, a persistent grid of
+ * 1.25 CTAs per SM so the next frames' projection and sorts share the SMs --
+ * where gut_render runs it for latency (speculation window 2, every SM).  The
+ * schedule decides only who computes what when: results are identical to
+ * rendering the views one by one.  With stats != NULL the views are rendered
+ * one at a time on s and stats[i] filled (synchronising). */
 gut_status gut_render_batch(gut_context *ctx, const gut_scene *scene, const gut_camera *cams,
                             int32_t n_views, const gut_options *opt, const gut_outputs *outs,
                             gut_stream s, gut_stats *stats);
