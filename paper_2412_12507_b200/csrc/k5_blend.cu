@@ -458,7 +458,9 @@ __device__ __forceinline__ bool pred_dead(const unsigned long long *stat, int s,
 // `seg / GUT_CK` entries, recorded while the pixel is live, so a re-run from
 // the exact prefix T_pre resumes at the last checkpoint the exact sequence
 // certainly reached (T_pre T_c >= T_min) instead of at the segment start.
-#define GUT_CK 8
+#ifndef GUT_CK
+#define GUT_CK 16  // checkpoints per speculative segment (8: K5 +2.8%; tuning switch)
+#endif
 template <int NP> struct Checkpoints {
   float4 C[GUT_CK][NP];
   float T[GUT_CK][NP];
@@ -781,7 +783,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
             L.done[k] = L.term[k] = true;
         }
     }
-    if (ck && b0 == ck_next) {  // (the speculative pass walks from s0 in steps of 32: no jumps)
+    if (ck && b0 == ck_next && ck_idx < GUT_CK) {  // (the speculative pass walks from s0 in steps of 32: no jumps)
       ck_next += ck_step;
 #pragma unroll
       for (int k = 0; k < NP; ++k)
@@ -1272,7 +1274,8 @@ __global__ __launch_bounds__(GUT_BLEND_CTA, GUT_BLEND_CTAS) void blend_kernel(De
     }
     uint32_t n_eval = 0, n_contrib = 0, processed = 0;
     Checkpoints<NP> ck;
-    const uint32_t ck_step = max(32u, ((uint32_t)B.seg / GUT_CK) & ~31u);
+    // (rounded up to whole chunks: at most GUT_CK checkpoints per segment)
+    const uint32_t ck_step = max(32u, ((uint32_t)B.seg / GUT_CK + 31u) & ~31u);
     store_warp_consts(warp_consts(WarpTbl<MODE>::NF), D, O - mkd(c.c0[0], c.c0[1], c.c0[2]), T1f, T2f, ac, bc, ra,
                       rb, tc, rt, A.fit[w]);
     unsigned long long t_spec = 0, t_lb = 0;  // (trace only: end of the speculative pass / of the look-back)
