@@ -459,7 +459,7 @@ __device__ __forceinline__ bool pred_dead(const unsigned long long *stat, int s,
 // the exact prefix T_pre resumes at the last checkpoint the exact sequence
 // certainly reached (T_pre T_c >= T_min) instead of at the segment start.
 #ifndef GUT_CK
-#define GUT_CK 16  // checkpoints per speculative segment (8: K5 +2.8%; tuning switch)
+#define GUT_CK 80  // checkpoints per speculative segment: with 2560-entry segments one per 32-entry chunk (8 / 16 / 32: K5 +6% / +3% / +1%; tuning switch)
 #endif
 template <int NP> struct Checkpoints {
   float4 C[GUT_CK][NP];
