@@ -458,6 +458,9 @@ __device__ __forceinline__ bool pred_dead(const unsigned long long *stat, int s,
 // `seg / GUT_CK` entries, recorded while the pixel is live, so a re-run from
 // the exact prefix T_pre resumes at the last checkpoint the exact sequence
 // certainly reached (T_pre T_c >= T_min) instead of at the segment start.
+#ifndef GUT_POLL_CHUNKS
+#define GUT_POLL_CHUNKS 2u  // speculative pass: chunks between predecessor polls (power of 2; tuning switch)
+#endif
 #ifndef GUT_CK
 #define GUT_CK 80  // checkpoints per speculative segment: with 2560-entry segments one per 32-entry chunk (8 / 16 / 32: K5 +6% / +3% / +1%; tuning switch)
 #endif
@@ -772,7 +775,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
     // speculative pass of a later segment: every 2 chunks, stop pixels whose
     // exact sequence has certainly terminated by now: T_spec times the bound of
     // the published prefix below T_min (Ls := dead, exact; a re-run resolves it)
-    if (poll_stat && ((b0 - s0) & 63u) == 32u) {
+    if (poll_stat && ((b0 - s0) & (GUT_POLL_CHUNKS * 32u - 1u)) == (((GUT_POLL_CHUNKS * 32u) / 2u) & ~31u)) {
 #pragma unroll
       for (int k = 0; k < NP; ++k)
         if (!L.done[k]) {
