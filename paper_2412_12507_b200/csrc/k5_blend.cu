@@ -1692,7 +1692,7 @@ static void blend_kbuf_launch(const DevCam &cam, const BlendBufs &b, cudaStream_
   // per device, thread-safe (a process may drive several devices): the
   // dynamic shared-memory attribute is a per-device setting
   static std::once_flag once[GUT_MAX_DEVICES];
-  static int grids[GUT_MAX_DEVICES];
+  static int grids[GUT_MAX_DEVICES], smss[GUT_MAX_DEVICES];
   int dev = 0;
   cudaGetDevice(&dev);
   dev = min(dev, GUT_MAX_DEVICES - 1);
@@ -1702,8 +1702,10 @@ static void blend_kbuf_launch(const DevCam &cam, const BlendBufs &b, cudaStream_
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, blend_kbuf_kernel<MODE, KB>, GUT_BLEND_CTA, smem);
     grids[dev] = max(1, sms) * max(1, per);
+    smss[dev] = max(1, sms);
   });
-  const int grid = grids[dev];
+  // frames in flight: the smaller persistent grid, as blend_launch
+  const int grid = b.grid_x4 > 0 ? max(1, min(grids[dev], smss[dev] * b.grid_x4 / 4)) : grids[dev];
   blend_kbuf_kernel<MODE, KB><<<grid, GUT_BLEND_CTA, smem, st>>>(cam, b);
 }
 
