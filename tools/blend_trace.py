@@ -90,7 +90,7 @@ def main():
         tr = r.stage(gut.STAGE_BLEND_TRACE)
         ranges = r.stage(gut.STAGE_RANGES)
         ms = list(st.ms_stage)
-        analyse(tr, ranges, cam.tiles[0], int(os.environ.get("GUT_BLEND_SEG", "2560"))  # (the library default, csrc/gut_abi.cu),
+        analyse(tr, ranges, cam.tiles[0], int(os.environ.get("GUT_BLEND_SEG", "2560")),  # (library default)
                 f"view {v} (blend {ms[5]:.3f} ms, K={st.n_keys})")
     r.close()
 
