@@ -772,7 +772,7 @@ __device__ __forceinline__ void warp_pass(const DevCam &c, const BlendBufs &B, u
         anypend = anypend || pend[k];
       }
     }
-    // speculative pass of a later segment: every 2 chunks, stop pixels whose
+    // speculative pass of a later segment: every GUT_POLL_CHUNKS chunks, stop pixels whose
     // exact sequence has certainly terminated by now: T_spec times the bound of
     // the published prefix below T_min (Ls := dead, exact; a re-run resolves it)
     if (poll_stat && ((b0 - s0) & (GUT_POLL_CHUNKS * 32u - 1u)) == (((GUT_POLL_CHUNKS * 32u) / 2u) & ~31u)) {
